@@ -1,0 +1,306 @@
+/*
+ * sphb.h — C ABI of the B200-native truncated-Wendland SPH hot path.
+ *
+ * Every entry point works on DEVICE pointers that the caller owns (allocated
+ * by the host runtime — PyTorch in this repo), runs asynchronously on the
+ * caller's CUDA stream (passed as `void*`, a cudaStream_t) and returns an
+ * sphb_status.  No entry point allocates device memory: scratch space comes
+ * from a caller-provided workspace whose size a *_workspace_bytes() query
+ * returns.  Numerical failures (non-positive density, non-finite flux,
+ * inverted deformation gradient) are reported through a device-resident
+ * int32 error word that the host reads when it synchronises, mirroring the
+ * exceptions raised by the reference's Python wrappers.
+ *
+ * Reference ("the reference" = pkg/src/sph_trunc of arXiv 2405.05155's
+ * package).  The reference has no FFI: its inner operator boundary is the
+ * flat signature of each @njit loop.  Each function below names the loop (or
+ * the numpy glue) it replaces, file:line.
+ *
+ * Layout conventions
+ *   - "orig"   arrays are in the caller's particle order, row-major AoS
+ *              exactly like the reference numpy arrays ((n, d) doubles).
+ *   - "sorted" arrays are in cell-sorted order (stable radix sort by cell
+ *              key, so ascending original index inside a cell), SoA:
+ *              component a of particle s lives at [a * n + s].
+ *   - CSR neighbour lists are the reference's NeighborList
+ *              (neighbors.py:18-35): starts (n+1) int64, idx (m) int32,
+ *              r (m) f64, e (m, d) f64, rows in orig order, each row in the
+ *              reference's enumeration order (3^d stencil, axis 0 fastest,
+ *              then ascending index inside a cell).
+ *   - ELL neighbour tables are the engine's pass lists: nbr[k * n + s]
+ *              (sorted indices, column-major so a warp's loads coalesce),
+ *              cnt[s] entries per row, same order as the CSR row.
+ */
+#ifndef SPHB_H
+#define SPHB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPHB_OK = 0,
+  SPHB_ERR_ARG = -1,      /* invalid argument (maps to ValueError)            */
+  SPHB_ERR_CUDA = -2,     /* CUDA runtime error; see sphb_last_cuda_error()  */
+  SPHB_ERR_WORKSPACE = -3,/* workspace smaller than *_workspace_bytes()      */
+  SPHB_ERR_OVERFLOW = -4  /* table too small (ELL width, cell count)         */
+} sphb_status;
+
+/* device error-word bits (solver checks; see eulerian.py:548-550,631-633,
+ * tlsph.py:196-199) */
+#define SPHB_EFLAG_NONFINITE_FLUX   1
+#define SPHB_EFLAG_NONPOS_DENSITY   2
+#define SPHB_EFLAG_DET_NONPOS       4
+#define SPHB_EFLAG_NONFINITE_STATE  8
+
+/* Kernel families: the reference's integer codes (kernels.py:26-27). */
+#define SPHB_CODE_WENDLAND 0
+#define SPHB_CODE_LAGUERRE_GAUSS 1
+
+/* Uniform cell grid of the cell-linked list.  Filled on the host exactly as
+ * build_neighbors() does (neighbors.py:183-203) so that cell membership and
+ * therefore the candidate set and its order are identical. */
+typedef struct sphb_grid {
+  int32_t dim;         /* 1..3                                              */
+  int32_t periodic;    /* 1: minimum image in box (neighbors.py:189)        */
+  int64_t ncell[3];    /* cells per axis, >= 1                              */
+  int64_t strides[3];  /* flat-key strides, axis 0 fastest (:394-396)       */
+  int64_t ntot;        /* prod(ncell)                                       */
+  double inv_cell[3];  /* ncell/box (periodic) or 1/cutoff (open)           */
+  double box[3];       /* periodic lengths (1.0 on open axes, :383)         */
+  double lo[3];        /* open-domain shift pos.min(axis=0) (:384)          */
+  double cutoff;
+  double cut2;         /* cutoff * cutoff (neighbors.py:266 of _search)     */
+} sphb_grid;
+
+/* Kernel parameters (KernelSpec, kernels.py:62-80). */
+typedef struct sphb_kernel {
+  int32_t code;        /* SPHB_CODE_*                                       */
+  int32_t dim;
+  double h;
+  double alpha;
+  double kappa;
+} sphb_kernel;
+
+const char* sphb_version(void);
+const char* sphb_last_cuda_error(void);
+int sphb_device_count(void);
+
+/* ---------------------------------------------------------------- binning */
+
+/* Workspace for sphb_bin (cub radix-sort temp + key/value scratch). */
+size_t sphb_bin_workspace_bytes(int64_t n, const sphb_grid* g);
+
+/* Wrap/shift coordinates, cell keys, stable radix sort by key, cell tables.
+ * Replaces build_neighbors' coordinate set-up + _cell_index
+ * (neighbors.py:183-208, :38-53) and the head/next counting lists of _search
+ * (:63-74).  Outputs: wrapped coordinates in sorted SoA order, perm[s] =
+ * original index of sorted particle s, cell_start/cell_end[ntot]. */
+int sphb_bin(const sphb_grid* g, const double* pos_orig, int64_t n,
+             double* wrapped_sorted, int32_t* perm, int32_t* cell_start,
+             int32_t* cell_end, void* workspace, size_t workspace_bytes,
+             void* stream);
+
+/* --------------------------------------------------- CSR (drop-in list) */
+
+/* Per-row neighbour counts (pass 1 of _search, neighbors.py:87-119), written
+ * in ORIGINAL order into starts[1..n], then scanned so starts becomes the CSR
+ * offsets (neighbors.py:121-123).  starts has n+1 entries; starts[n] = m. */
+size_t sphb_csr_workspace_bytes(int64_t n);
+int sphb_csr_starts(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                    const int32_t* perm, const int32_t* cell_start,
+                    const int32_t* cell_end, int64_t* starts, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* Fill idx/r/e (pass 2 of _search, neighbors.py:129-167). */
+int sphb_csr_fill(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                  const int32_t* perm, const int32_t* cell_start,
+                  const int32_t* cell_end, const int64_t* starts, int32_t* idx,
+                  double* r, double* e, void* stream);
+
+/* --------------------------------------------------- ELL (engine lists) */
+
+/* Engine pass list: same enumeration, but pairs the passes would skip
+ * (q = r/h > kappa, correction.py:99-101, approx.py:48-49,
+ * relaxation.py:74-76) are dropped at build time.  cnt[s] per sorted row.
+ * *max_cnt_dev receives max(cnt) (device int32). */
+int sphb_ell_count(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                   const int32_t* cell_start, const int32_t* cell_end,
+                   double h, double kappa, int32_t* cnt, int32_t* max_cnt_dev,
+                   void* stream);
+int sphb_ell_fill(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                  const int32_t* cell_start, const int32_t* cell_end,
+                  double h, double kappa, int32_t width, int32_t* nbr,
+                  void* stream);
+
+/* Moment matrices M_i (correction.py:35-52) straight from the ELL list,
+ * sorted order, exact geometry; bit-identical rows to sphb_moment_matrices
+ * on the CSR without materialising r and e. */
+int sphb_ell_moments(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                     const int32_t* nbr, const int32_t* cnt, const double* vols_sorted,
+                     const sphb_kernel* k, double* m_sorted, void* stream);
+
+/* ---------------------------------------------- CSR operator passes
+ * Bit-faithful restatements of the reference @njit loops (compiled without
+ * FMA contraction, same summation order) over a device CSR. */
+
+/* _unity_sums (approx.py:41-52): out[i] = a P(0) V_i + sum_{q<=kappa} a P(q) V_j */
+int sphb_unity_sums(int64_t n, const int64_t* starts, const int32_t* idx,
+                    const double* r, const double* vols, const sphb_kernel* k,
+                    double* out, void* stream);
+
+/* _pressure_accel (relaxation.py:66-80) */
+int sphb_pressure_accel(int64_t n, int32_t dim, const int64_t* starts,
+                        const int32_t* idx, const double* r, const double* e,
+                        const double* vols, const sphb_kernel* k, double p0,
+                        double rho0, double* acc, void* stream);
+
+/* _moment_matrices (correction.py:35-52): m (n, d, d) */
+int sphb_moment_matrices(int64_t n, int32_t dim, const int64_t* starts,
+                         const int32_t* idx, const double* r, const double* e,
+                         const double* vols, const sphb_kernel* k, double* m,
+                         void* stream);
+
+/* correction_matrices' numpy/LAPACK block (correction.py:64-81): SVD of M,
+ * clamp s < EPS_SV s_max, pseudo-inverse, theta = clip(det(-M)/EPS_DET,0,1),
+ * B = theta(-M+) + (1-theta) I.  Outputs B (n,d,d), det(-M) (n) and the
+ * per-particle regularized flag (int8).  One-sided Jacobi SVD on device. */
+int sphb_correction_from_moments(int64_t n, int32_t dim, const double* m,
+                                 double* b, double* det_neg_m, int8_t* reg,
+                                 void* stream);
+
+/* _pair_gradients (correction.py:89-112): gw (m, d); b may be NULL */
+int sphb_pair_gradients(int64_t n, int32_t dim, const int64_t* starts,
+                        const int32_t* idx, const double* r, const double* e,
+                        const sphb_kernel* k, const double* b, double* gw,
+                        void* stream);
+
+/* _rhs_wc (eulerian.py:224-266) over precomputed gwv/viscv (CSR, orig). */
+int sphb_rhs_wc_csr(int64_t n_int, int32_t dim, const int64_t* starts,
+                    const int32_t* idx, const double* e, const double* gwv,
+                    const double* viscv, const double* rho, const double* v,
+                    const double* p, double c_art, double mu,
+                    const int8_t* wall_tag, double* drho, double* dmom,
+                    double* wall_force_partial, void* stream);
+
+/* _accelerations (tlsph.py:88-102) and _deformation_rates (:105-123). */
+int sphb_tl_accelerations_csr(int64_t n, int32_t dim, const int64_t* starts,
+                              const int32_t* idx, const double* g0,
+                              const double* q, double rho0, double* acc,
+                              void* stream);
+int sphb_tl_deformation_rates_csr(int64_t n, int32_t dim, const int64_t* starts,
+                                  const int32_t* idx, const double* g0,
+                                  const double* v, const double* b0,
+                                  double* dF, void* stream);
+
+/* ---------------------------------------------------------- WC engine
+ * EulerianSolver (eulerian.py:465-662), weakly-compressible branch, fused:
+ * one kernel per midpoint stage evaluates EOS + limited linearised Riemann
+ * flux (_linearized_scalar :145-157, _rhs_wc :224-266) with the pair
+ * geometry (r, e, corrected gradient, viscous weight; :506-513) recomputed
+ * from sorted coordinates, then applies the stage update (:619-629) and,
+ * in stage 2, folds max(c + |v|) for the next dt (compute_dt :553-560).
+ *
+ * Packed per-particle records, cell-sorted order (4 doubles = 32 B each):
+ *   X  [n][4] = {x0, x1, x2, vol}      (2D {x0, x1, vol, 0}; 1D {x0, vol,..})
+ *   B  [n][8] = {b00,b01,b02,b11, b12,b22,0,0}  symmetrised correction
+ *               (2D {b00,b01,b11,0, 0...}; 1D {b00, 0...})
+ *   S  [n][4] = {v0, v1, v2, rho}      primitive state (2D {v0, v1, rho, 0})
+ *   M  [n][4] = {m0, m1, m2, 0}        momentum per unit volume
+ * Device scalar block (double[4]): [0] dt, [1] t, [2] max-speed accumulator
+ * (atomicMax on the bit pattern), [3] spare.  err: int32 SPHB_EFLAG_* word.
+ */
+typedef struct sphb_wc_params {
+  int32_t dim;
+  int32_t periodic;
+  int32_t uniform_vol;   /* 1: vol_const used instead of X[.][dim]          */
+  int32_t width;         /* ELL width                                       */
+  int64_t n;             /* particles (all interior; ghosts out of scope)   */
+  double box[3];
+  double h, alpha, kappa; /* Wendland family only (code 0)                  */
+  double c_art, rho0, mu, cfl;
+  double vol_const;
+} sphb_wc_params;
+
+/* stage 0: rhs only — S_out = {dmom, drho} records (EulerianSolver.rhs).
+ * stage 1: S_in = S_n, writes S_out = U^1 primitive record (M_out unused).
+ * stage 2: S_in = U^1 records, own U^n from S_n/M_n, writes U^{n+1} into
+ *          S_out/M_out (may alias S_n/M_n) and folds max(c+|v|). */
+int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, const double* X,
+                  const double* B, const int32_t* nbr, const int32_t* cnt,
+                  const double* S_in, const double* S_n, const double* M_n,
+                  double* S_out, double* M_out, double* scalars, int32_t* err,
+                  void* stream);
+/* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
+int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,
+                      void* stream);
+
+/* dt for the next step: dt = dt_override if > 0, else
+ * cfl_h / (c_add + scalars[2]); then scalars[1] += dt, scalars[2] = 0.
+ * WC: c_add = 0 (the speed already includes c; eulerian.py:556-560);
+ * TL: c_add = c_s (tlsph.py:178-180). */
+int sphb_set_dt(double cfl_h, double c_add, double dt_override, double* scalars,
+                int32_t* err, void* stream);
+
+/* ---------------------------------------------------------- TL engine
+ * SolidSystem.step (tlsph.py:182-206), fused into two passes over the ELL
+ * list of the reference configuration X0:
+ *   pass A: v_half = v + dt/2 acc (fixed -> 0) for i and every neighbour j,
+ *           x += dt v_half, dF = [sum (v_j - v_i) (x) g0_ij] B0_i
+ *           (_deformation_rates :105-123), F += dt dF, det F > 0 check, and
+ *           the epilogue Q = (F S) B0^T with S the SVK PK2 (:54-65,160-167).
+ *   pass B: acc = sum (Q_i + Q_j) g0_ij / rho0 (_accelerations :88-102),
+ *           acc[fixed] = 0, v = v_half + dt/2 acc, v[fixed] = 0, and
+ *           max |v| for the next stable_dt (:178-180).
+ * g0_ij = (alpha/h) dP(q) e_ij V0 is recomputed from X0 (:145-146).
+ * Records (sorted order): X0 [n][4] (x0,x1,x2,fixed-flag as double),
+ * V/A/XC [n][4] vectors, B0/F/Q [n][12] (row-major 3x3 padded; 2D uses the
+ * leading 2x2 block with stride 2... see tl_engine.cu). */
+typedef struct sphb_tl_params {
+  int32_t dim;
+  int32_t width;
+  int64_t n;
+  double h, alpha, kappa;  /* Wendland family */
+  double vol0, rho0;
+  double lam, g;           /* Lame parameters (tlsph.py:27-35) */
+} sphb_tl_params;
+
+int sphb_tl_pass_a(const sphb_tl_params* p, const double* X0, const double* B0,
+                   const int32_t* nbr, const int32_t* cnt, const double* V,
+                   const double* A, double* Vh, double* XC, double* F,
+                   double* Q, const double* scalars, int32_t* err, void* stream);
+int sphb_tl_pass_b(const sphb_tl_params* p, const double* X0, const int32_t* nbr,
+                   const int32_t* cnt, const double* Q, const double* Vh,
+                   double* A, double* V, double* scalars, int32_t update_v,
+                   void* stream);
+/* Q = (F S(F)) B0^T for every particle (first accelerations() call). */
+int sphb_tl_stress(const sphb_tl_params* p, const double* F, const double* B0,
+                   double* Q, void* stream);
+/* max |v| into scalars[2] (stable_dt). */
+int sphb_tl_speed_max(const sphb_tl_params* p, const double* V, double* scalars,
+                      void* stream);
+
+/* --------------------------------------------------- relaxation engine
+ * One pseudo-time step of relax() on a periodic box (relaxation.py:157-195)
+ * without a materialised neighbour list: the accel kernel walks the cell
+ * stencil of the binned positions in the reference order and sums the
+ * constant-pressure acceleration (_pressure_accel :66-80) directly, writing
+ * acc in ORIGINAL order, plus sum |a| and the isolated count (:170, :159);
+ * the update kernel applies dx = a dt2 with the 0.25 dp cap and the periodic
+ * wrap (:188-195).  sums: double[2] = {sum|a|, n_isolated}. */
+int sphb_relax_accel(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                     const int32_t* perm, const int32_t* cell_start,
+                     const int32_t* cell_end, const double* vols_orig,
+                     const sphb_kernel* k, double p0, double rho0,
+                     double* acc_orig, double* sums, void* stream);
+int sphb_relax_update(int64_t n, int32_t dim, const double* acc_orig, double dt2,
+                      double cap, const double* box3, double* pos_orig,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHB_H */

@@ -1,0 +1,332 @@
+"""CPU ORACLE — test infrastructure only, never the product path.
+
+Python side of the oracle: numpy glue around the plain-C loops in
+sph_oracle.c, restating the reference package (pkg/src/sph_trunc of arXiv
+2405.05155) function by function.  Used by tests/ (as the checker of the CUDA
+path), by __graft_entry__.smoke(), and by bench.py's cpu_baseline and
+`--impl reference` legs (as the timed CPU baseline, "kind": "port").
+
+Pinned against the reference by tests/test_oracle_golden.py: golden vectors
+written by tests/golden/make_golden.py from the reference itself, plus every
+known value of the reference's own unit tests.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+_P = C.c_void_p
+_I = C.c_int64
+_D = C.c_double
+
+_SIGS = {
+    "orc_bin": (_P, [_P, _I, _I, _P, _P, _P, _P, _I, _D]),
+    "orc_bin_free": (None, [_P]),
+    "orc_count": (None, [_P, _P]),
+    "orc_fill": (None, [_P, _P, _P, _P, _P]),
+    "orc_unity_sums": (None, [_I, _P, _P, _P, _P, _I, _D, _D, _D, _P]),
+    "orc_pressure_accel": (None, [_I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _D, _D, _P]),
+    "orc_moment_matrices": (None, [_I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _P]),
+    "orc_pair_gradients": (None, [_I, _I, _P, _P, _P, _P, _I, _D, _D, _D, _P, _P]),
+    "orc_rhs_wc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P]),
+    "orc_tl_accelerations": (None, [_I, _I, _P, _P, _P, _P, _D, _P]),
+    "orc_tl_deformation_rates": (None, [_I, _I, _P, _P, _P, _P, _P, _P]),
+    "orc_max_threads": (C.c_int, []),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def threads() -> int:
+    return int(lib().orc_max_threads())
+
+
+# ------------------------------------------------------------ neighbours
+@dataclass
+class NeighborList:
+    starts: np.ndarray
+    idx: np.ndarray
+    r: np.ndarray
+    e: np.ndarray
+    cutoff: float
+
+    @property
+    def n(self):
+        return self.starts.shape[0] - 1
+
+    @property
+    def counts(self):
+        return np.diff(self.starts)
+
+
+def build_neighbors(positions, cutoff, box=None) -> NeighborList:
+    """neighbors.py:171-210 (grid set-up in numpy, loops in C)."""
+    pos = np.ascontiguousarray(np.asarray(positions, dtype=float))
+    n, d = pos.shape
+    if box is not None:
+        box_arr = np.asarray(box, dtype=float)
+        wrapped = pos % box_arr
+        extent = box_arr
+    else:
+        box_arr = np.ones(d)
+        lo = pos.min(axis=0)
+        wrapped = pos - lo
+        extent = np.maximum(wrapped.max(axis=0), cutoff)
+    ncell = np.maximum((extent / cutoff).astype(np.int64), 1)
+    inv_cell = ncell / box_arr if box is not None else np.full(d, 1.0 / cutoff)
+    strides = np.ones(d, dtype=np.int64)
+    for a in range(1, d):
+        strides[a] = strides[a - 1] * ncell[a - 1]
+    wrapped = np.ascontiguousarray(wrapped)
+    inv_cell = np.ascontiguousarray(inv_cell, dtype=float)
+    box_c = np.ascontiguousarray(box_arr, dtype=float)
+    L = lib()
+    h = L.orc_bin(_p(wrapped), n, d, _p(inv_cell), _p(ncell), _p(strides), _p(box_c),
+                  int(box is not None), float(cutoff))
+    try:
+        starts = np.zeros(n + 1, dtype=np.int64)
+        L.orc_count(h, _p(starts))
+        m = int(starts[-1])
+        idx = np.empty(m, dtype=np.int32)
+        r = np.empty(m)
+        e = np.empty((m, d))
+        L.orc_fill(h, _p(starts), _p(idx), _p(r), _p(e))
+    finally:
+        L.orc_bin_free(h)
+    return NeighborList(starts, idx, r, e, float(cutoff))
+
+
+def pair_set(nl) -> np.ndarray:
+    """Sorted (i, j) int64 pairs of a CSR list (canonical form for set equality)."""
+    rows = np.repeat(np.arange(nl.n, dtype=np.int64), np.diff(nl.starts))
+    key = rows * (nl.n + 1) + nl.idx.astype(np.int64)
+    return np.sort(key)
+
+
+# ------------------------------------------------------------ operators
+def sph_unity_sum(nl, vols, spec):
+    out = np.empty(nl.n)
+    v = np.ascontiguousarray(vols, dtype=float)
+    lib().orc_unity_sums(nl.n, _p(nl.starts), _p(nl.idx), _p(nl.r), _p(v), spec.code, spec.h,
+                         spec.alpha, spec.kappa, _p(out))
+    return out
+
+
+def relax_accelerations(nl, vols, spec, p0=1.0, rho0=1.0):
+    d = nl.e.shape[1]
+    acc = np.empty((nl.n, d))
+    v = np.ascontiguousarray(vols, dtype=float)
+    lib().orc_pressure_accel(nl.n, d, _p(nl.starts), _p(nl.idx), _p(nl.r), _p(nl.e), _p(v),
+                             spec.code, spec.h, spec.alpha, spec.kappa, p0, rho0, _p(acc))
+    return acc
+
+
+def moment_matrices(nl, vols, spec):
+    d = nl.e.shape[1]
+    m = np.empty((nl.n, d, d))
+    v = np.ascontiguousarray(vols, dtype=float)
+    lib().orc_moment_matrices(nl.n, d, _p(nl.starts), _p(nl.idx), _p(nl.r), _p(nl.e), _p(v),
+                              spec.code, spec.h, spec.alpha, spec.kappa, _p(m))
+    return m
+
+
+def correction_matrices(nl, vols, spec):
+    """correction.py:64-81 with numpy's LAPACK, as the reference does.
+    Returns (B, det(-M), n_regularized)."""
+    m = moment_matrices(nl, vols, spec)
+    n, d, _ = m.shape
+    u, s, vt = np.linalg.svd(m)
+    floor = 1e-4 * np.maximum(s[:, :1], 1e-300)
+    clamped = np.any(s < floor, axis=1)
+    s_reg = np.maximum(s, floor)
+    minv = np.einsum("nba,nb,ncb->nac", vt, 1.0 / s_reg, u)
+    det_neg = np.linalg.det(-m)
+    theta = np.clip(det_neg / 1e-6, 0.0, 1.0)
+    b = theta[:, None, None] * (-minv) + (1.0 - theta)[:, None, None] * np.eye(d)
+    return b, det_neg, int((clamped | (theta < 1.0)).sum())
+
+
+def pair_gradients(nl, spec, b=None):
+    d = nl.e.shape[1]
+    gw = np.empty((nl.idx.shape[0], d))
+    bb = None if b is None else np.ascontiguousarray(b, dtype=float)
+    lib().orc_pair_gradients(nl.n, d, _p(nl.starts), _p(nl.idx), _p(nl.r), _p(nl.e),
+                             spec.code, spec.h, spec.alpha, spec.kappa, _p(bb), _p(gw))
+    return gw
+
+
+def _profile_deriv(code, q):
+    if code == 0:
+        t = 1.0 - 0.5 * q
+        return -5.0 * q * t**3
+    return q * (-3.0 + (5.0 / 3.0) * q**2 - q**4 / 3.0) * np.exp(-(q**2))
+
+
+# ------------------------------------------------------------ relaxation
+def relax_steps(pos, spec, box, dp, n_updates, p0=1.0, rho0=1.0, step_scale=0.2):
+    """relaxation.py:157-195 loop body with no stop tests."""
+    pos = np.array(pos, dtype=float)
+    n, d = pos.shape
+    vols = np.full(n, dp**d)
+    cutoff = spec.kappa * spec.h
+    dt2 = step_scale * spec.h**2 * rho0 / p0
+    cap = 0.25 * dp
+    box = np.asarray(box, dtype=float)
+    residuals = []
+    for step in range(n_updates + 1):
+        nl = build_neighbors(pos, cutoff, box)
+        acc = relax_accelerations(nl, vols, spec, p0, rho0)
+        residuals.append(float(np.mean(np.linalg.norm(acc, axis=1)) * spec.h * rho0 / p0))
+        if step == n_updates:
+            break
+        dx = acc * dt2
+        norms = np.linalg.norm(dx, axis=1)
+        over = norms > cap
+        if np.any(over):
+            dx[over] *= (cap / norms[over])[:, None]
+        pos += dx
+        pos %= box
+    return pos, np.asarray(residuals)
+
+
+# ------------------------------------------------------------ WC Eulerian
+class EulerianWC:
+    """EulerianSolver, WC branch, periodic, no ghosts (eulerian.py:473-643)."""
+
+    def __init__(self, pos, vol, rho, mom, spec, c_art, rho0=1.0, mu=0.0, cfl=0.5, box=None,
+                 correction=True):
+        self.spec, self.c_art, self.rho0, self.mu, self.cfl = spec, c_art, rho0, mu, cfl
+        self.nl = build_neighbors(pos, spec.kappa * spec.h, box)
+        self.vol = np.asarray(vol, dtype=float)
+        self.rho = np.array(rho, dtype=float)
+        self.mom = np.array(mom, dtype=float)
+        self.n, self.d = self.mom.shape
+        b = correction_matrices(self.nl, self.vol, spec)[0] if correction else None
+        self.B = b
+        gw = pair_gradients(self.nl, spec, b)
+        self.gwv = np.ascontiguousarray(gw * self.vol[self.nl.idx][:, None])
+        q = self.nl.r / spec.h
+        dw = np.where(q <= spec.kappa, (spec.alpha / spec.h) * _profile_deriv(spec.code, q), 0.0)
+        self.viscv = np.ascontiguousarray(2.0 * dw / self.nl.r * self.vol[self.nl.idx])
+        self.t = 0.0
+
+    def rhs(self):
+        p = self.c_art**2 * (self.rho - self.rho0)
+        v = np.ascontiguousarray(self.mom / self.rho[:, None])
+        drho = np.empty(self.n)
+        dmom = np.zeros((self.n, self.d))
+        lib().orc_rhs_wc(self.n, self.d, _p(self.nl.starts), _p(self.nl.idx), _p(self.nl.e),
+                         _p(self.gwv), _p(self.viscv), _p(self.rho), _p(v), _p(p), self.c_art,
+                         self.mu, _p(drho), _p(dmom))
+        return drho, dmom
+
+    def compute_dt(self):
+        speed = self.c_art + np.linalg.norm(self.mom / self.rho[:, None], axis=1)
+        return self.cfl * self.spec.h / float(speed.max())
+
+    def step(self, dt=None):
+        if dt is None:
+            dt = self.compute_dt()
+        rho0, mom0 = self.rho.copy(), self.mom.copy()
+        drho, dmom = self.rhs()
+        self.rho = rho0 + 0.5 * dt * drho
+        self.mom = mom0 + 0.5 * dt * dmom
+        drho, dmom = self.rhs()
+        self.rho = rho0 + dt * drho
+        self.mom = mom0 + dt * dmom
+        if not np.all(self.rho > 0.0):
+            raise RuntimeError("non-positive density")
+        self.t += dt
+        return dt
+
+
+# ------------------------------------------------------------ TL-SPH
+class SolidTL:
+    """SolidSystem (tlsph.py:129-206) with SVK stress."""
+
+    def __init__(self, X0, rho0, E, nu, spec, dp, fixed=None, correction=True, cfl=0.6):
+        self.X0 = np.ascontiguousarray(X0, dtype=float)
+        self.n, self.d = self.X0.shape
+        self.spec, self.dp, self.cfl, self.rho0 = spec, dp, cfl, rho0
+        self.lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+        self.g = E / (2.0 * (1.0 + nu))
+        self.c_s = float(np.sqrt((self.lam + 2.0 * self.g) / rho0))
+        vol0 = np.full(self.n, dp**self.d)
+        self.nl = build_neighbors(self.X0, spec.kappa * spec.h)
+        if correction:
+            self.B0 = correction_matrices(self.nl, vol0, spec)[0]
+        else:
+            self.B0 = np.tile(np.eye(self.d), (self.n, 1, 1))
+        self.B0 = np.ascontiguousarray(self.B0)
+        self.g0 = np.ascontiguousarray(pair_gradients(self.nl, spec, None) * vol0[self.nl.idx][:, None])
+        self.x = self.X0.copy()
+        self.v = np.zeros_like(self.X0)
+        self.F = np.tile(np.eye(self.d), (self.n, 1, 1))
+        self.fixed = np.zeros(self.n, bool) if fixed is None else np.asarray(fixed, bool)
+        self.acc = None
+        self.t = 0.0
+
+    def accelerations(self):
+        eye = np.eye(self.d)
+        strain = 0.5 * (np.einsum("nba,nbc->nac", self.F, self.F) - eye)
+        tr = np.trace(strain, axis1=1, axis2=2)
+        s = self.lam * tr[:, None, None] * eye + 2.0 * self.g * strain
+        P = np.einsum("nab,nbc->nac", self.F, s)
+        q = np.ascontiguousarray(np.einsum("nab,ncb->nac", P, self.B0))
+        acc = np.empty((self.n, self.d))
+        lib().orc_tl_accelerations(self.n, self.d, _p(self.nl.starts), _p(self.nl.idx),
+                                   _p(self.g0), _p(q), self.rho0, _p(acc))
+        acc[self.fixed] = 0.0
+        return acc
+
+    def deformation_rates(self):
+        dF = np.empty((self.n, self.d, self.d))
+        v = np.ascontiguousarray(self.v)
+        lib().orc_tl_deformation_rates(self.n, self.d, _p(self.nl.starts), _p(self.nl.idx),
+                                       _p(self.g0), _p(v), _p(self.B0), _p(dF))
+        return dF
+
+    def stable_dt(self):
+        return self.cfl * self.spec.h / (self.c_s + float(np.linalg.norm(self.v, axis=1).max()))
+
+    def step(self, dt=None):
+        if dt is None:
+            dt = self.stable_dt()
+        if self.acc is None:
+            self.acc = self.accelerations()
+        self.v += 0.5 * dt * self.acc
+        self.v[self.fixed] = 0.0
+        self.x += dt * self.v
+        self.F += dt * self.deformation_rates()
+        if not np.all(np.linalg.det(self.F) > 0.0):
+            raise RuntimeError("deformation gradient inverted")
+        self.acc = self.accelerations()
+        self.v += 0.5 * dt * self.acc
+        self.v[self.fixed] = 0.0
+        self.t += dt
+        return dt

@@ -1,0 +1,278 @@
+// neighbors.cu — cell binning, CSR export and engine pass lists.
+//
+// Replaces the reference's cell-linked list (neighbors.py:171-210 with
+// _cell_index :38-53 and _search :56-168).  The reference builds head/next
+// chains with a reversed counting sort so chains run in ascending index; the
+// B200 design replaces that with a stable LSD radix sort of (cell key,
+// index) pairs — identical cell contents in identical order — plus
+// cell_start/cell_end tables, so every row is enumerated in exactly the
+// reference's order and the CSR written here is byte-identical to the
+// reference's.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+using namespace sphb;
+
+// --------------------------------------------------------------- binning
+template <int D>
+__global__ void k_wrap_key(sphb_grid g, const double* __restrict__ pos, int64_t n,
+                           double* __restrict__ wrapped_aos, uint32_t* __restrict__ key,
+                           int32_t* __restrict__ val) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t flat = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double p = pos[i * D + a];
+    double w = g.periodic ? np_remainder(p, g.box[a]) : __dsub_rn(p, g.lo[a]);
+    wrapped_aos[i * D + a] = w;
+    flat += cell_coord(g, a, w) * g.strides[a];
+  }
+  key[i] = (uint32_t)flat;
+  val[i] = (int32_t)i;
+}
+
+template <int D>
+__global__ void k_gather_sorted(int64_t n, const double* __restrict__ wrapped_aos,
+                                const int32_t* __restrict__ perm, double* __restrict__ ws) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int64_t i = perm[s];
+#pragma unroll
+  for (int a = 0; a < D; ++a) ws[(int64_t)a * n + s] = wrapped_aos[i * D + a];
+}
+
+__global__ void k_cell_ranges(int64_t n, const uint32_t* __restrict__ key,
+                              int32_t* __restrict__ cs, int32_t* __restrict__ ce) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t k = key[s];
+  if (s == 0 || key[s - 1] != k) cs[k] = (int32_t)s;
+  if (s == n - 1 || key[s + 1] != k) ce[k] = (int32_t)(s + 1);
+}
+
+static bool grid_ok(const sphb_grid* g) {
+  if (!g || g->dim < 1 || g->dim > 3) return false;
+  if (g->ntot < 1 || g->ntot > 0x7fffffffLL) return false;
+  return true;
+}
+
+struct BinLayout {
+  size_t keys_in, keys_out, vals_in, wrapped, cub, total;
+};
+
+static BinLayout bin_layout(int64_t n, int dim) {
+  BinLayout L;
+  size_t off = 0;
+  L.keys_in = off;  off += sphb_align(sizeof(uint32_t) * (size_t)n);
+  L.keys_out = off; off += sphb_align(sizeof(uint32_t) * (size_t)n);
+  L.vals_in = off;  off += sphb_align(sizeof(int32_t) * (size_t)n);
+  L.wrapped = off;  off += sphb_align(sizeof(double) * (size_t)n * dim);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs<uint32_t, int32_t>(nullptr, cub_bytes, (uint32_t*)nullptr,
+                                                     (uint32_t*)nullptr, (int32_t*)nullptr,
+                                                     (int32_t*)nullptr, (int)n, 0, 32);
+  L.cub = off;      off += sphb_align(cub_bytes);
+  L.total = off;
+  return L;
+}
+
+static int end_bit_for(int64_t ntot) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) < ntot) ++b;
+  return b;
+}
+
+extern "C" size_t sphb_bin_workspace_bytes(int64_t n, const sphb_grid* g) {
+  if (!grid_ok(g) || n < 0) return 0;
+  return bin_layout(n > 0 ? n : 1, g->dim).total;
+}
+
+extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double* ws,
+                        int32_t* perm, int32_t* cs, int32_t* ce, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (!grid_ok(g) || n < 0 || n > 0x7fffffffLL) return SPHB_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  SPHB_CUDA_CHECK(cudaMemsetAsync(cs, 0, sizeof(int32_t) * (size_t)g->ntot, st));
+  SPHB_CUDA_CHECK(cudaMemsetAsync(ce, 0, sizeof(int32_t) * (size_t)g->ntot, st));
+  if (n == 0) return SPHB_OK;
+  BinLayout L = bin_layout(n, g->dim);
+  if (workspace_bytes < L.total) return SPHB_ERR_WORKSPACE;
+  char* w = (char*)workspace;
+  uint32_t* keys_in = (uint32_t*)(w + L.keys_in);
+  uint32_t* keys_out = (uint32_t*)(w + L.keys_out);
+  int32_t* vals_in = (int32_t*)(w + L.vals_in);
+  double* wrapped = (double*)(w + L.wrapped);
+  const int T = 256;
+  switch (g->dim) {
+    case 1: k_wrap_key<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+    case 2: k_wrap_key<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+    default: k_wrap_key<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  size_t cub_bytes = workspace_bytes - L.cub;
+  SPHB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(w + L.cub, cub_bytes, keys_in, keys_out, vals_in,
+                                                  perm, (int)n, 0, end_bit_for(g->ntot), st));
+  k_cell_ranges<<<sphb_blocks(n, T), T, 0, st>>>(n, keys_out, cs, ce);
+  SPHB_LAUNCH_CHECK();
+  switch (g->dim) {
+    case 1: k_gather_sorted<1><<<sphb_blocks(n, T), T, 0, st>>>(n, wrapped, perm, ws); break;
+    case 2: k_gather_sorted<2><<<sphb_blocks(n, T), T, 0, st>>>(n, wrapped, perm, ws); break;
+    default: k_gather_sorted<3><<<sphb_blocks(n, T), T, 0, st>>>(n, wrapped, perm, ws); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+// ------------------------------------------------------------------- CSR
+template <int D>
+__global__ void k_csr_count(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                            const int32_t* __restrict__ perm, const int32_t* __restrict__ cs,
+                            const int32_t* __restrict__ ce, int64_t* __restrict__ counts_orig) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int64_t c = 0;
+  for_each_neighbor<D>(g, n, ws, cs, ce, (int32_t)s,
+                       [&](int32_t, const double*, double) { ++c; });
+  counts_orig[perm[s]] = c;
+}
+
+extern "C" size_t sphb_csr_workspace_bytes(int64_t n) {
+  size_t cub_bytes = 0;
+  int64_t nn = n > 0 ? n : 1;
+  cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)nn);
+  return sphb_align(sizeof(int64_t) * (size_t)nn) + sphb_align(cub_bytes);
+}
+
+extern "C" int sphb_csr_starts(const sphb_grid* g, int64_t n, const double* ws,
+                               const int32_t* perm, const int32_t* cs, const int32_t* ce,
+                               int64_t* starts, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (!grid_ok(g) || n < 0) return SPHB_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  SPHB_CUDA_CHECK(cudaMemsetAsync(starts, 0, sizeof(int64_t), st));
+  if (n == 0) return SPHB_OK;
+  if (workspace_bytes < sphb_csr_workspace_bytes(n)) return SPHB_ERR_WORKSPACE;
+  int64_t* counts = (int64_t*)workspace;
+  char* cub_tmp = (char*)workspace + sphb_align(sizeof(int64_t) * (size_t)n);
+  size_t cub_bytes = workspace_bytes - sphb_align(sizeof(int64_t) * (size_t)n);
+  const int T = 128;
+  switch (g->dim) {
+    case 1: k_csr_count<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, counts); break;
+    case 2: k_csr_count<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, counts); break;
+    default: k_csr_count<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, counts); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  SPHB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(cub_tmp, cub_bytes, counts, starts + 1, (int)n, st));
+  return SPHB_OK;
+}
+
+template <int D>
+__global__ void k_csr_fill(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                           const int32_t* __restrict__ perm, const int32_t* __restrict__ cs,
+                           const int32_t* __restrict__ ce, const int64_t* __restrict__ starts,
+                           int32_t* __restrict__ idx, double* __restrict__ r,
+                           double* __restrict__ e) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int64_t w = starts[perm[s]];
+  for_each_neighbor<D>(g, n, ws, cs, ce, (int32_t)s, [&](int32_t t, const double* dx, double r2) {
+    double dist = __dsqrt_rn(r2);
+    idx[w] = perm[t];
+    r[w] = dist;
+#pragma unroll
+    for (int a = 0; a < D; ++a) e[w * D + a] = __ddiv_rn(dx[a], dist);
+    ++w;
+  });
+}
+
+extern "C" int sphb_csr_fill(const sphb_grid* g, int64_t n, const double* ws, const int32_t* perm,
+                             const int32_t* cs, const int32_t* ce, const int64_t* starts,
+                             int32_t* idx, double* r, double* e, void* stream) {
+  if (!grid_ok(g) || n < 0) return SPHB_ERR_ARG;
+  if (n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = 128;
+  switch (g->dim) {
+    case 1: k_csr_fill<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, starts, idx, r, e); break;
+    case 2: k_csr_fill<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, starts, idx, r, e); break;
+    default: k_csr_fill<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, starts, idx, r, e); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+// ------------------------------------------------------------------- ELL
+// Pair kept iff the passes would not skip it: q = r/h <= kappa with r and q
+// rounded exactly like correction.py:99-101 (r = sqrt(r2), q = r / h).
+__device__ __forceinline__ bool pass_keeps(double r2, double h, double kappa) {
+  return !(__ddiv_rn(__dsqrt_rn(r2), h) > kappa);
+}
+
+template <int D>
+__global__ void k_ell_count(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                            const int32_t* __restrict__ cs, const int32_t* __restrict__ ce,
+                            double h, double kappa, int32_t* __restrict__ cnt,
+                            int32_t* __restrict__ max_cnt) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t c = 0;
+  if (s < n) {
+    for_each_neighbor<D>(g, n, ws, cs, ce, (int32_t)s, [&](int32_t, const double*, double r2) {
+      if (pass_keeps(r2, h, kappa)) ++c;
+    });
+    cnt[s] = c;
+  }
+  int32_t m = warp_max(c);
+  if ((threadIdx.x & 31) == 0) atomicMax(max_cnt, m);
+}
+
+extern "C" int sphb_ell_count(const sphb_grid* g, int64_t n, const double* ws, const int32_t* cs,
+                              const int32_t* ce, double h, double kappa, int32_t* cnt,
+                              int32_t* max_cnt, void* stream) {
+  if (!grid_ok(g) || n < 0) return SPHB_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  SPHB_CUDA_CHECK(cudaMemsetAsync(max_cnt, 0, sizeof(int32_t), st));
+  if (n == 0) return SPHB_OK;
+  const int T = 128;
+  switch (g->dim) {
+    case 1: k_ell_count<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, cnt, max_cnt); break;
+    case 2: k_ell_count<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, cnt, max_cnt); break;
+    default: k_ell_count<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, cnt, max_cnt); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+template <int D>
+__global__ void k_ell_fill(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                           const int32_t* __restrict__ cs, const int32_t* __restrict__ ce,
+                           double h, double kappa, int32_t width, int32_t* __restrict__ nbr) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int32_t k = 0;
+  for_each_neighbor<D>(g, n, ws, cs, ce, (int32_t)s, [&](int32_t t, const double*, double r2) {
+    if (pass_keeps(r2, h, kappa)) {
+      if (k < width) nbr[(int64_t)k * n + s] = t;
+      ++k;
+    }
+  });
+  // pad the row with itself: padded slots are never read (cnt bounds loops)
+  for (; k < width; ++k) nbr[(int64_t)k * n + s] = (int32_t)s;
+}
+
+extern "C" int sphb_ell_fill(const sphb_grid* g, int64_t n, const double* ws, const int32_t* cs,
+                             const int32_t* ce, double h, double kappa, int32_t width,
+                             int32_t* nbr, void* stream) {
+  if (!grid_ok(g) || n < 0 || width < 0) return SPHB_ERR_ARG;
+  if (n == 0 || width == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = 128;
+  switch (g->dim) {
+    case 1: k_ell_fill<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, width, nbr); break;
+    case 2: k_ell_fill<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, width, nbr); break;
+    default: k_ell_fill<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, cs, ce, h, kappa, width, nbr); break;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}

@@ -1,0 +1,408 @@
+// tl_engine.cu — fused total-Lagrangian SPH passes (kick-drift-kick).
+//
+// SolidSystem.step (tlsph.py:182-206) is two grid-wide dependencies (the dF
+// pass needs every neighbour's half-kicked velocity, the momentum pass needs
+// every neighbour's new stress), so it is two launches:
+//
+//   pass A  (tlsph.py:191-199, :105-123, :54-65, :160-167)
+//     v_half_j = fixed_j ? 0 : v_j + dt/2 a_j       recomputed per neighbour
+//     dF_i = [sum_j (v_half_j - v_half_i) (x) g0_ij] B0_i
+//     F_i += dt dF_i ; det F_i > 0 ; x_i += dt v_half_i
+//     epilogue: S = lam tr(E) I + 2 G E, E = (F^T F - I)/2 ; Q_i = (F S) B0^T
+//   pass B  (tlsph.py:164-171, :88-102, :200-202, :178-180)
+//     a_i = sum_j (Q_i + Q_j) g0_ij / rho0 ; a[fixed] = 0
+//     v_i = v_half_i + dt/2 a_i ; v[fixed] = 0 ; fold max |v_i|
+//
+// g0_ij = (alpha/h) dP(q) e_ij V0 (tlsph.py:145-146) is recomputed from the
+// reference configuration instead of being streamed from a per-pair array.
+//
+// Records (cell-sorted order):
+//   X0[i]  double4 {w0, w1, w2, fixed}  (w = X0 - min(X0), as the CSR's r/e)
+//   V, A, Vh, XC  double4 vectors
+//   B0, F, Q      3x3: 3 x double4 rows {a0, a1, a2, 0}; 2D: 1 x double4
+//                 {a00, a01, a10, a11}; 1D: {a00, 0, 0, 0}
+#include "common.cuh"
+
+using namespace sphb;
+
+namespace {
+
+constexpr int kThreads = 128;
+
+template <int D>
+__device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t i,
+                                         double (&a)[D][D]) {
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double4 t = M[3 * i + r];
+      a[r][0] = t.x; a[r][1] = t.y; a[r][2] = t.z;
+    }
+  } else if constexpr (D == 2) {
+    double4 t = M[i];
+    a[0][0] = t.x; a[0][1] = t.y; a[1][0] = t.z; a[1][1] = t.w;
+  } else {
+    a[0][0] = M[i].x;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t i,
+                                          const double (&a)[D][D]) {
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) M[3 * i + r] = make_double4(a[r][0], a[r][1], a[r][2], 0.0);
+  } else if constexpr (D == 2) {
+    M[i] = make_double4(a[0][0], a[0][1], a[1][0], a[1][1]);
+  } else {
+    M[i] = make_double4(a[0][0], 0.0, 0.0, 0.0);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_vec(const double4* __restrict__ V, int64_t i, double (&v)[D]) {
+  double4 t = V[i];
+  const double c[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = c[a];
+}
+
+template <int D>
+__device__ __forceinline__ void store_vec(double4* __restrict__ V, int64_t i, const double (&v)[D]) {
+  double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) c[a] = v[a];
+  V[i] = make_double4(c[0], c[1], c[2], c[3]);
+}
+
+template <int D>
+__device__ __forceinline__ void load_x0(const double4* __restrict__ X0, int64_t i, double (&w)[D],
+                                        bool& fixed) {
+  double4 t = X0[i];
+  const double c[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int a = 0; a < D; ++a) w[a] = c[a];
+  fixed = c[3] != 0.0;
+}
+
+// g0 = (alpha/h) dP(q) e V0 from the reference-configuration displacement.
+template <int D>
+__device__ __forceinline__ void ref_gradient(const double (&dx)[D], double scale_v0, double inv_h,
+                                             double (&g)[D]) {
+  double r2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) r2 = fma(dx[a], dx[a], r2);
+  const double inv_r = rsqrt(r2);
+  const double q = r2 * inv_r * inv_h;
+  const double t = fma(-0.5, q, 1.0);
+  const double f = scale_v0 * (-5.0 * q) * (t * t * t) * inv_r;  // dW V0 / r
+#pragma unroll
+  for (int a = 0; a < D; ++a) g[a] = f * dx[a];
+}
+
+template <int D>
+__device__ __forceinline__ double det_mat(const double (&A)[D][D]) {
+  if constexpr (D == 1) {
+    return A[0][0];
+  } else if constexpr (D == 2) {
+    return A[0][0] * A[1][1] - A[0][1] * A[1][0];
+  } else {
+    return A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) -
+           A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+           A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+  }
+}
+
+// Q = (F S) B0^T with the St. Venant-Kirchhoff PK2 (tlsph.py:54-65, 160-167)
+template <int D>
+__device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0)[D][D], double lam,
+                                      double g2, double (&Q)[D][D]) {
+  double E[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(F[b][a], F[b][c], s);
+      E[a][c] = 0.5 * (s - (a == c ? 1.0 : 0.0));
+    }
+  double tr = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) tr += E[a][a];
+  double S[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) S[a][c] = g2 * E[a][c] + (a == c ? lam * tr : 0.0);
+  double P[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(F[a][b], S[b][c], s);
+      P[a][c] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(P[a][b], B0[c][b], s);
+      Q[a][c] = s;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double4* __restrict__ B0,
+            const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+            const double4* __restrict__ V, const double4* __restrict__ A, double4* __restrict__ Vh,
+            double4* __restrict__ XC, double4* __restrict__ F, double4* __restrict__ Q,
+            const double* __restrict__ scalars, int32_t* __restrict__ err) {
+  const int64_t n = P.n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double dt = scalars[0];
+  const double hdt = 0.5 * dt;
+  const double inv_h = 1.0 / P.h;
+  const double scale_v0 = P.alpha / P.h * P.vol0;
+
+  double wi[D], vi[D], ai[D], vhi[D];
+  bool fixed_i;
+  load_x0<D>(X0, i, wi, fixed_i);
+  load_vec<D>(V, i, vi);
+  load_vec<D>(A, i, ai);
+#pragma unroll
+  for (int a = 0; a < D; ++a) vhi[a] = fixed_i ? 0.0 : fma(hdt, ai[a], vi[a]);
+
+  double m[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+
+  const int32_t cn = cnt[i];
+  const int32_t* __restrict__ row = nbr + i;
+  for (int32_t k = 0; k < cn; ++k) {
+    const int64_t j = row[(int64_t)k * n];
+    double wj[D], vj[D], aj[D];
+    bool fixed_j;
+    load_x0<D>(X0, j, wj, fixed_j);
+    load_vec<D>(V, j, vj);
+    load_vec<D>(A, j, aj);
+    double dx[D], g[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+    ref_gradient<D>(dx, scale_v0, inv_h, g);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double vhj = fixed_j ? 0.0 : fma(hdt, aj[a], vj[a]);
+      const double dv = vhj - vhi[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) m[a][b] = fma(dv, g[b], m[a][b]);
+    }
+  }
+
+  double B[D][D], Fi[D][D];
+  load_mat<D>(B0, i, B);
+  load_mat<D>(F, i, Fi);
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) s = fma(m[a][c], B[c][b], s);
+      Fi[a][b] = fma(dt, s, Fi[a][b]);
+    }
+  const double J = det_mat<D>(Fi);
+  if (!(J > 0.0)) atomicOr(err, SPHB_EFLAG_DET_NONPOS);
+  double Qi[D][D];
+  svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
+  store_mat<D>(F, i, Fi);
+  store_mat<D>(Q, i, Qi);
+  store_vec<D>(Vh, i, vhi);
+  double xc[D];
+  load_vec<D>(XC, i, xc);
+#pragma unroll
+  for (int a = 0; a < D; ++a) xc[a] = fma(dt, vhi[a], xc[a]);
+  store_vec<D>(XC, i, xc);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
+            const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+            const double4* __restrict__ Q, const double4* __restrict__ Vh,
+            double4* __restrict__ A, double4* __restrict__ V, double* __restrict__ scalars,
+            int update_v) {
+  const int64_t n = P.n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double speed = 0.0;
+  if (i < n) {
+    const double inv_h = 1.0 / P.h;
+    const double scale_v0 = P.alpha / P.h * P.vol0;
+    double wi[D];
+    bool fixed_i;
+    load_x0<D>(X0, i, wi, fixed_i);
+    double Qi[D][D];
+    load_mat<D>(Q, i, Qi);
+    double gsum[D], acc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { gsum[a] = 0.0; acc[a] = 0.0; }
+    const int32_t cn = cnt[i];
+    const int32_t* __restrict__ row = nbr + i;
+    for (int32_t k = 0; k < cn; ++k) {
+      const int64_t j = row[(int64_t)k * n];
+      double wj[D];
+      bool fixed_j;
+      load_x0<D>(X0, j, wj, fixed_j);
+      double Qj[D][D];
+      load_mat<D>(Q, j, Qj);
+      double dx[D], g[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+      ref_gradient<D>(dx, scale_v0, inv_h, g);
+      // sum_j (Q_i + Q_j) g = Q_i sum_j g + sum_j Q_j g
+#pragma unroll
+      for (int b = 0; b < D; ++b) gsum[b] += g[b];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
+    }
+    const double inv_rho0 = 1.0 / P.rho0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double s = acc[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(Qi[a][b], gsum[b], s);
+      acc[a] = fixed_i ? 0.0 : s * inv_rho0;
+    }
+    store_vec<D>(A, i, acc);
+    double v[D];
+    if (update_v) {
+      const double hdt = 0.5 * scalars[0];
+      load_vec<D>(Vh, i, v);
+#pragma unroll
+      for (int a = 0; a < D; ++a) v[a] = fixed_i ? 0.0 : fma(hdt, acc[a], v[a]);
+      store_vec<D>(V, i, v);
+    } else {
+      load_vec<D>(V, i, v);
+    }
+    double s2 = __dmul_rn(v[0], v[0]);
+#pragma unroll
+    for (int a = 1; a < D; ++a) s2 = __dadd_rn(s2, __dmul_rn(v[a], v[a]));
+    speed = __dsqrt_rn(s2);
+  }
+  __shared__ double red[kThreads / 32];
+  double w = warp_max(speed);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = red[0];
+#pragma unroll
+    for (int q = 1; q < kThreads / 32; ++q) b = b > red[q] ? b : red[q];
+    atomic_max_nonneg(scalars + 2, b);
+  }
+}
+
+template <int D>
+__global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ F,
+                            const double4* __restrict__ B0, double4* __restrict__ Q) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  double Fi[D][D], B[D][D], Qi[D][D];
+  load_mat<D>(F, i, Fi);
+  load_mat<D>(B0, i, B);
+  svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
+  store_mat<D>(Q, i, Qi);
+}
+
+template <int D>
+__global__ void k_tl_speed(int64_t n, const double4* __restrict__ V, double* __restrict__ scalars) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double speed = 0.0;
+  if (i < n) {
+    double v[D];
+    load_vec<D>(V, i, v);
+    double s2 = __dmul_rn(v[0], v[0]);
+#pragma unroll
+    for (int a = 1; a < D; ++a) s2 = __dadd_rn(s2, __dmul_rn(v[a], v[a]));
+    speed = __dsqrt_rn(s2);
+  }
+  __shared__ double red[8];
+  double w = warp_max(speed);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = red[0];
+    for (int q = 1; q < 8; ++q) b = b > red[q] ? b : red[q];
+    atomic_max_nonneg(scalars + 2, b);
+  }
+}
+
+}  // namespace
+
+#define TL_DISPATCH(KERNEL, GRID, TH, ...)                                 \
+  do {                                                                     \
+    switch (p->dim) {                                                      \
+      case 1: KERNEL<1><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      case 2: KERNEL<2><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      case 3: KERNEL<3><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      default: return SPHB_ERR_ARG;                                        \
+    }                                                                      \
+  } while (0)
+
+extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,
+                              const int32_t* nbr, const int32_t* cnt, const double* v,
+                              const double* a, double* vh, double* xc, double* f, double* q,
+                              const double* scalars, int32_t* err, void* stream) {
+  if (!p || p->n < 0) return SPHB_ERR_ARG;
+  if (p->n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  TL_DISPATCH(k_tl_pass_a, sphb_blocks(p->n, kThreads), kThreads, *p, (const double4*)x0,
+              (const double4*)b0, nbr, cnt, (const double4*)v, (const double4*)a, (double4*)vh,
+              (double4*)xc, (double4*)f, (double4*)q, scalars, err);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const int32_t* nbr,
+                              const int32_t* cnt, const double* q, const double* vh, double* a,
+                              double* v, double* scalars, int32_t update_v, void* stream) {
+  if (!p || p->n < 0) return SPHB_ERR_ARG;
+  if (p->n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  TL_DISPATCH(k_tl_pass_b, sphb_blocks(p->n, kThreads), kThreads, *p, (const double4*)x0, nbr, cnt,
+              (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,
+              (int)update_v);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_tl_stress(const sphb_tl_params* p, const double* f, const double* b0,
+                              double* q, void* stream) {
+  if (!p || p->n < 0) return SPHB_ERR_ARG;
+  if (p->n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  TL_DISPATCH(k_tl_stress, sphb_blocks(p->n, 128), 128, *p, (const double4*)f, (const double4*)b0,
+              (double4*)q);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_tl_speed_max(const sphb_tl_params* p, const double* v, double* scalars,
+                                 void* stream) {
+  if (!p || p->n < 0) return SPHB_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  SPHB_CUDA_CHECK(cudaMemsetAsync(scalars + 2, 0, sizeof(double), st));
+  if (p->n == 0) return SPHB_OK;
+  TL_DISPATCH(k_tl_speed, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, scalars);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}

@@ -1,0 +1,442 @@
+"""Weakly-compressible Eulerian SPH on stationary particles, on the GPU.
+
+Drop-in for the WC branch of `sph_trunc.eulerian` (reference
+eulerian.py:1-671): `EosParams`, `FluidState`, `eos_eval`,
+`linearized_star`, `SolverError`, `ConfigError` and `EulerianSolver` with the
+reference constructor and `rhs()`, `compute_dt()`, `step(dt=None)`,
+`totals()`.
+
+Engine (csrc/wc_engine.cu).  Construction bins the fixed particles once,
+builds the ELL pass list and the correction matrices B on the device
+(sphb_ell_moments + sphb_correction_from_moments), and packs the state into
+cell-sorted 32-byte records.  A step is four launches on the current stream:
+  sphb_set_dt  (dt = cfl h / max(c + |v|), from the previous stage 2)
+  stage 1      U^1     = U^n + dt/2 R(U^n)
+  stage 2      U^{n+1} = U^n + dt   R(U^1)  (+ max(c+|v|) for the next dt)
+with R the fused limited-linearised Riemann flux (eulerian.py:224-266) whose
+pair geometry is recomputed on the fly instead of streamed from the
+reference's per-pair arrays (eulerian.py:506-513).  Stage outputs go to a
+second buffer, so the retry-with-halving of eulerian.py:562-608 restores U^n
+by not swapping buffers.
+
+`step()` synchronises once per call (it must return dt and raise on a bad
+state, as the reference does); `advance(n)` runs n steps with no host
+synchronisation and checks the error word once at the end.
+
+Outside the hot-path scope: ghost layers, the ideal-gas HLLC
+solver, wall forces.  They raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .kernels import CODE_WENDLAND, KernelSpec
+from .neighbors import NeighborList, bin_particles, csr_from_bins, ell_from_bins, make_grid
+
+IDEAL_GAS = "ideal-gas"
+WEAKLY_COMPRESSIBLE = "weakly-compressible"
+ETA_HLLC = 1.0
+ETA_LINEARIZED = 15.0   # eulerian.py:30
+
+
+class SolverError(RuntimeError):
+    """Raised when the solver state becomes invalid (exit code 2)."""
+
+
+class ConfigError(ValueError):
+    """Raised for malformed case configuration (exit code 3)."""
+
+
+@dataclass(frozen=True)
+class EosParams:
+    """Equation-of-state parameters (eulerian.py:49-64)."""
+
+    mode: str
+    gamma: float = 1.4
+    rho0: float = 1.0
+    c_art: float = 0.0
+
+    def __post_init__(self):
+        if self.mode == IDEAL_GAS:
+            if not self.gamma > 1.0:
+                raise ConfigError("ideal gas needs gamma > 1")
+        elif self.mode == WEAKLY_COMPRESSIBLE:
+            if not (self.c_art > 0.0 and self.rho0 > 0.0):
+                raise ConfigError("weakly compressible needs c_art > 0 and rho0 > 0")
+        else:
+            raise ConfigError(f"unknown EOS mode {self.mode!r}")
+
+
+def eos_eval(eos: EosParams, rho, mom=None, etot=None):
+    """Pressure and sound speed (eulerian.py:67-85)."""
+    rho = np.asarray(rho, dtype=float)
+    if np.any(rho <= 0.0):
+        raise SolverError(f"non-positive density at particles {np.where(rho <= 0.0)[0][:8]}")
+    if eos.mode == WEAKLY_COMPRESSIBLE:
+        return eos.c_art**2 * (rho - eos.rho0), np.full_like(rho, eos.c_art)
+    if mom is None or etot is None:
+        raise ConfigError("ideal-gas EOS needs momentum and total energy")
+    v2 = np.sum(np.asarray(mom, dtype=float) ** 2, axis=-1) / rho**2
+    e = np.asarray(etot, dtype=float) / rho - 0.5 * v2
+    if np.any(e < 0.0):
+        bad = np.where(e < 0.0)[0]
+        raise SolverError(f"negative internal energy at particles {bad[:8]} (of {bad.size})")
+    p = rho * (eos.gamma - 1.0) * e
+    return p, np.sqrt(eos.gamma * p / rho)
+
+
+@dataclass(frozen=True)
+class InterfaceState:
+    rho: float
+    v: tuple
+    p: float
+    c: float
+    etot: float = 0.0
+
+
+@dataclass(frozen=True)
+class RiemannStar:
+    u_star: float
+    p_star: float
+    v_star: np.ndarray
+    rho_star_l: float
+    rho_star_r: float
+    e_star_l: float
+    e_star_r: float
+    s_l: float
+    s_r: float
+    s_star: float
+    beta: float
+
+
+def linearized_star(left: InterfaceState, right: InterfaceState, e_ij) -> RiemannStar:
+    """Limited linearised interface solution (eulerian.py:145-157, 211-219).
+
+    Host scalar helper; the device evaluates the same formulas per pair.
+    """
+    n = -np.asarray(e_ij, dtype=float)
+    vl = np.asarray(left.v, dtype=float)
+    vr = np.asarray(right.v, dtype=float)
+    ul, ur = float(vl @ n), float(vr @ n)
+    cbar = 0.5 * (left.c + right.c)
+    du = ul - ur
+    beta = min(max(ETA_LINEARIZED * du / cbar, 0.0), 1.0)
+    rbar = 0.5 * (left.rho + right.rho)
+    u_star = 0.5 * (ul + ur) + 0.5 * beta * beta * (left.p - right.p) / (rbar * cbar)
+    p_star = 0.5 * (left.p + right.p) + 0.5 * beta * rbar * cbar * du
+    v_star = u_star * n + 0.5 * (vl + vr) - 0.5 * (ul + ur) * n
+    return RiemannStar(u_star, p_star, v_star, rbar, rbar, 0.0, 0.0, ul - cbar, ur + cbar,
+                       u_star, beta)
+
+
+@dataclass
+class FluidState:
+    """Columnar conserved fields (eulerian.py:452-462)."""
+
+    vol: np.ndarray
+    rho: np.ndarray
+    mom: np.ndarray
+    etot: np.ndarray | None
+    n_interior: int
+
+    def velocity(self):
+        return self.mom / self.rho[:, None]
+
+
+_EFLAGS = {1: "non-finite flux", 2: "non-positive density", 4: "det F <= 0",
+           8: "non-finite state / zero wave speed"}
+
+
+def _describe(err: int) -> str:
+    return ", ".join(v for k, v in _EFLAGS.items() if err & k) or f"flags {err}"
+
+
+def _rec4(cols, n, dev):
+    """Pack up to 4 (n,) columns into an (n, 4) float64 record array."""
+    torch = _lib.torch_cuda()
+    out = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+    for k, c in enumerate(cols):
+        out[:, k] = c
+    return out
+
+
+class EulerianSolver:
+    """Midpoint time stepping of the pairwise-Riemann discretisation (WC).
+
+    Same constructor and methods as the reference (eulerian.py:465-662).
+    """
+
+    def __init__(self, positions, n_interior, state: FluidState, eos: EosParams,
+                 kernel: KernelSpec, ghosts=None, *, correction: bool = True, cfl: float = 0.5,
+                 mu: float = 0.0, periodic_box=None, wall_force_tag=None):
+        if mu < 0.0:
+            raise ConfigError("viscosity must be non-negative")
+        if ghosts is not None:
+            raise NotImplementedError("ghost layers are outside the B200 hot path (SURVEY §8(f))")
+        if eos.mode != WEAKLY_COMPRESSIBLE:
+            raise NotImplementedError("the HLLC / ideal-gas solver is outside the hot path")
+        if wall_force_tag is not None:
+            raise NotImplementedError("wall-force tagging is outside the hot path")
+        if kernel.code != CODE_WENDLAND:
+            raise NotImplementedError("the WC engine evaluates the Wendland family")
+        torch = _lib.torch_cuda()
+        self.pos = np.ascontiguousarray(positions, dtype=float)
+        self.n, self.dim = self.pos.shape
+        self.n_int = int(n_interior)
+        if self.n_int != self.n:
+            raise NotImplementedError("all particles must be interior without ghost layers")
+        self.eos, self.kernel = eos, kernel
+        self.ghosts = None
+        self.cfl, self.mu = float(cfl), float(mu)
+        self.steps = 0
+        self.retries = 0
+        self.wall_force = np.zeros(self.dim)
+        self.wall_force_series: list = []
+        self.periodic_box = periodic_box
+        self._state_host = None
+        self._handed_out = False
+        self._t_host = 0.0
+
+        dev = _lib.device()
+        self._dev = dev
+        cutoff = kernel.kappa * kernel.h                       # eulerian.py:492
+        self.grid = make_grid(self.pos, cutoff, periodic_box)
+        self.bins = bin_particles(_lib.to_device(self.pos, torch.float64), self.grid)
+        self.nbr, self.cnt, self.width = ell_from_bins(self.bins, kernel.h, kernel.kappa)
+        self.perm = self.bins.perm.long()
+        self.rank = self.bins.rank()
+        self._nlist = None
+
+        vol = np.asarray(state.vol, dtype=float)
+        vol_s = _lib.to_device(vol, torch.float64)[self.perm]
+        uniform = bool(np.all(vol == vol[0])) if self.n else True
+
+        # correction matrices in sorted order (correction.py:64-81)
+        if correction:
+            m = torch.empty((self.n, self.dim, self.dim), dtype=torch.float64, device=dev)
+            k = _lib.kernel_struct(kernel)
+            _lib.call("sphb_ell_moments", ctypes.byref(self.grid), self.n,
+                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), vol_s.contiguous().data_ptr(), ctypes.byref(k),
+                      m.data_ptr(), _lib.stream_ptr())
+            from .correction import correction_from_moments_device
+
+            b, _, reg = correction_from_moments_device(m)
+            self.n_regularized = int(reg.sum().item())
+        else:
+            b = torch.eye(self.dim, dtype=torch.float64, device=dev).expand(self.n, -1, -1)
+            self.n_regularized = 0
+        self._B_sorted = b
+        bs = 0.5 * (b + b.transpose(1, 2))
+        self.B = torch.zeros((self.n, 8), dtype=torch.float64, device=dev)
+        iu = [(a, c) for a in range(self.dim) for c in range(a, self.dim)]
+        for col, (a, c) in enumerate(iu):
+            self.B[:, col] = bs[:, a, c]
+
+        ws = self.bins.ws
+        self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
+
+        self.params = _lib.WCParams()
+        p = self.params
+        p.dim, p.periodic, p.uniform_vol, p.width, p.n = (self.dim, self.grid.periodic,
+                                                          int(uniform), self.width, self.n)
+        for a in range(3):
+            p.box[a] = self.grid.box[a]
+        p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
+        p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
+        p.vol_const = float(vol[0]) if self.n else 0.0
+        self._cfl_h = self.cfl * kernel.h                      # eulerian.py:560
+
+        self.S = torch.empty((self.n, 4), dtype=torch.float64, device=dev)
+        self.M = torch.empty((self.n, 4), dtype=torch.float64, device=dev)
+        self.S1 = torch.empty_like(self.S)
+        self.S_nx = torch.empty_like(self.S)
+        self.M_nx = torch.empty_like(self.M)
+        self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._vol_host = vol
+        self.set_state(state)
+
+    # -- state transfer -----------------------------------------------------
+    def set_state(self, state: FluidState) -> None:
+        """Upload conserved fields (orig order) and refresh max(c + |v|)."""
+        torch = _lib.torch_cuda()
+        rho = _lib.to_device(np.asarray(state.rho, dtype=float), torch.float64)[self.perm]
+        mom = _lib.to_device(np.asarray(state.mom, dtype=float), torch.float64)[self.perm]
+        v = mom / rho[:, None]                                 # FluidState.velocity
+        self.S.copy_(_rec4([v[:, a] for a in range(self.dim)] + [rho], self.n, self._dev))
+        self.M.copy_(_rec4([mom[:, a] for a in range(self.dim)], self.n, self._dev))
+        self._state_host = None
+        self._refresh_speed()
+
+    def _sync_in(self):
+        if self._handed_out and self._state_host is not None:
+            self._handed_out = False
+            self.set_state(self._state_host)
+        self._handed_out = False
+
+    def _refresh_speed(self):
+        _lib.call("sphb_wc_speed_max", ctypes.byref(self.params), self.S.data_ptr(),
+                  self.scalars.data_ptr(), _lib.stream_ptr())
+
+    @property
+    def state(self) -> FluidState:
+        """Conserved fields in the caller's order (host arrays).
+
+        The arrays handed out are authoritative until the next solver call:
+        in-place edits (as reference code does on `solver.state`) are uploaded
+        before the next rhs/compute_dt/step."""
+        self._handed_out = True
+        if self._state_host is None:
+            rho = self.S[:, self.dim][self.rank].cpu().numpy()
+            mom = self.M[:, :self.dim][self.rank].cpu().numpy()
+            self._state_host = FluidState(vol=self._vol_host.copy(), rho=rho, mom=mom,
+                                          etot=None, n_interior=self.n_int)
+        return self._state_host
+
+    @property
+    def t(self) -> float:
+        return self._t_host
+
+    @property
+    def nlist(self) -> NeighborList:
+        """Reference-order CSR of the particle set (materialised on demand)."""
+        if self._nlist is None:
+            starts, idx, r, e = csr_from_bins(self.bins)
+            self._nlist = NeighborList(starts, idx, r, e, cutoff=self.grid.cutoff, bins=self.bins)
+        return self._nlist
+
+    # -- pieces -------------------------------------------------------------
+    def apply_boundaries(self, t=None):
+        return None
+
+    def _launch_stage(self, stage, s_in, s_n, m_n, s_out, m_out):
+        _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.X.data_ptr(),
+                  self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), s_in.data_ptr(),
+                  s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
+                  None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                  self.err.data_ptr(), _lib.stream_ptr())
+
+    def _check(self, what):
+        err = int(self.err.item())
+        if err:
+            self.err.zero_()
+            raise SolverError(f"{what}: {_describe(err)} (step {self.steps}, t={self._t_host:.6g})")
+
+    def rhs(self):
+        """(drho, dmom, None) of the current state, interior rows, caller order."""
+        self._sync_in()
+        out = torch_empty_like(self.S)
+        self._launch_stage(0, self.S, self.S, self.M, out, None)
+        self._check("NaN flux")
+        drho = out[:, self.dim][self.rank].cpu().numpy()
+        dmom = out[:, :self.dim][self.rank].cpu().numpy()
+        return drho, dmom, None
+
+    def compute_dt(self) -> float:
+        """cfl h / max(c + |v|) over the interior (eulerian.py:553-560)."""
+        self._sync_in()
+        smax = float(self.scalars[2].item())
+        if smax <= 0.0:
+            raise ConfigError("zero maximum wave speed; cannot pick a time step")
+        return self._cfl_h / smax
+
+    def _substeps(self, dt_override: float) -> None:
+        """One midpoint step into the *_nx buffers (no swap)."""
+        _lib.call("sphb_set_dt", self._cfl_h, 0.0, dt_override, self.scalars.data_ptr(),
+                  self.err.data_ptr(), _lib.stream_ptr())
+        self._launch_stage(1, self.S, self.S, self.M, self.S1, None)
+        self._launch_stage(2, self.S1, self.S, self.M, self.S_nx, self.M_nx)
+
+    def _swap(self):
+        self.S, self.S_nx = self.S_nx, self.S
+        self.M, self.M_nx = self.M_nx, self.M
+
+    def step(self, dt: float | None = None) -> float:
+        """One two-stage midpoint step with the reference's retry-with-halving
+        (eulerian.py:562-608).  Returns dt."""
+        self._sync_in()
+        if dt is None:
+            dt = self.compute_dt()
+        max_halvings = 12
+        halved = 0
+        advanced = 0.0
+        remaining = dt
+        while advanced < dt - 1e-15 * dt:
+            sub = min(remaining, dt - advanced)
+            self._substeps(sub)
+            err = int(self.err.item())
+            if err:
+                self.err.zero_()
+                self._refresh_speed()   # the rejected stage 2 polluted the max
+                halved += 1
+                self.retries += 1
+                if halved > max_halvings:
+                    raise SolverError(f"step failed: {_describe(err)} (step {self.steps})")
+                advanced = 0.0
+                remaining = dt / 2**halved
+                continue
+            self._swap()
+            self._t_host += sub
+            advanced += sub
+        self._state_host = None
+        self.wall_force_series.append((self._t_host, self.wall_force * self._vol_host[0]))
+        self.steps += 1
+        return dt
+
+    def advance(self, n_steps: int, dt: float | None = None) -> None:
+        """n_steps CFL (or fixed-dt) steps with no host synchronisation.
+
+        The error word is checked once at the end; on failure the state at
+        entry is restored and the steps are replayed one by one through
+        `step()` so the reference's retry semantics apply.
+        """
+        if n_steps <= 0:
+            return
+        torch = _lib.torch_cuda()
+        self._sync_in()
+        s0, m0 = self.S.clone(), self.M.clone()
+        t0 = self.scalars.clone()
+        self.scalars[1] = 0.0
+        for _ in range(n_steps):
+            self._substeps(0.0 if dt is None else float(dt))
+            self._swap()
+        err = int(self.err.item())
+        if err:
+            self.err.zero_()
+            self.S.copy_(s0)
+            self.M.copy_(m0)
+            self.scalars.copy_(t0)
+            for _ in range(n_steps):
+                self.step(dt)
+            return
+        self._t_host += float(self.scalars[1].item())
+        self.steps += n_steps
+        self._state_host = None
+        del torch
+
+    def totals(self):
+        """(sum vol rho, sum vol mom, None) over the interior (eulerian.py:655-662)."""
+        st = self.state
+        w = st.vol[:self.n_int]
+        return (float(np.sum(w * st.rho[:self.n_int])),
+                (w[:, None] * st.mom[:self.n_int]).sum(axis=0), None)
+
+
+def torch_empty_like(t):
+    return _lib.torch_cuda().empty_like(t)
+
+
+def profile_deriv_array(code, q):
+    """Vectorised dP/dq (eulerian.py:665-671)."""
+    q = np.asarray(q, dtype=float)
+    if code == 0:
+        t = 1.0 - 0.5 * q
+        return -5.0 * q * t**3
+    return q * (-3.0 + (5.0 / 3.0) * q**2 - q**4 / 3.0) * np.exp(-(q**2))

@@ -1,0 +1,356 @@
+"""Total-Lagrangian SPH for elastic solids, on the GPU.
+
+Drop-in for `sph_trunc.tlsph` (reference tlsph.py:1-254): `Material`,
+`lame_params`, `pk2_stress`, `init_case_velocity`, `SolidStateError` and
+`SolidSystem` with the reference constructor and `accelerations()`,
+`deformation_rates()`, `stable_dt()`, `step(dt=None)`.
+
+Engine (csrc/tl_engine.cu).  Construction bins the reference configuration
+X0 once, builds the ELL pass list and B0 on the device.  A kick-drift-kick
+step (tlsph.py:182-206) is three launches:
+  sphb_set_dt     dt = cfl h / (c_s + max|v|)             (tlsph.py:178-180)
+  sphb_tl_pass_a  half kick, drift, dF, F update, det check, Q = P B0^T
+  sphb_tl_pass_b  momentum sum, second half kick, max|v| for the next dt
+The reference-configuration gradients g0 = grad0 W V0 (tlsph.py:145-146)
+are recomputed per pair from X0 instead of being streamed.
+
+The constitutive law is St. Venant-Kirchhoff, the one the reference
+implements (tlsph.py:54-65); BASELINE.json's "Neo-Hookean" has no reference
+counterpart.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .kernels import CODE_WENDLAND, KernelSpec
+from .neighbors import NeighborList, bin_particles, csr_from_bins, ell_from_bins, make_grid
+
+
+class SolidStateError(RuntimeError):
+    """Raised when the deformation gradient loses invertibility."""
+
+
+def lame_params(E: float, nu: float) -> tuple[float, float]:
+    """(lambda, G) from Young's modulus and Poisson ratio (tlsph.py:27-35)."""
+    if not E > 0.0:
+        raise ValueError("Young's modulus must be positive")
+    if not -1.0 < nu < 0.5:
+        raise ValueError("Poisson ratio must lie in (-1, 0.5); 0.5 makes lambda singular")
+    return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), E / (2.0 * (1.0 + nu))
+
+
+@dataclass(frozen=True)
+class Material:
+    rho0: float
+    E: float
+    nu: float
+
+    @property
+    def lame(self) -> tuple[float, float]:
+        return lame_params(self.E, self.nu)
+
+    @property
+    def sound_speed(self) -> float:
+        lam, g = self.lame
+        return float(np.sqrt((lam + 2.0 * g) / self.rho0))
+
+
+def pk2_stress(F, material: Material):
+    """SVK second Piola-Kirchhoff stress lam tr(E) I + 2 G E (tlsph.py:54-65)."""
+    F = np.asarray(F, dtype=float)
+    lam, g = material.lame
+    batch = F if F.ndim == 3 else F[None]
+    eye = np.eye(batch.shape[-1])
+    strain = 0.5 * (np.einsum("nba,nbc->nac", batch, batch) - eye)
+    tr = np.trace(strain, axis1=1, axis2=2)
+    s = lam * tr[:, None, None] * eye + 2.0 * g * strain
+    return s if F.ndim == 3 else s[0]
+
+
+TWIST = "twist"
+BEND = "bend"
+
+
+def init_case_velocity(kind: str, X0, *, length: float, omega0: float = 105.0,
+                       v0=(10.0 * np.sqrt(3.0) / 2.0, 5.0, 0.0), axis_center=(0.0, 0.0)):
+    """Column initial velocities (tlsph.py:233-254): twist = omega0 sin(pi y /
+    (2L)) about the y axis; bend = uniform translation."""
+    X0 = np.asarray(X0, dtype=float)
+    if kind == BEND:
+        return np.tile(np.asarray(v0, dtype=float)[:X0.shape[1]], (X0.shape[0], 1))
+    if kind != TWIST:
+        raise ValueError(f"unknown case kind {kind!r}")
+    if X0.shape[1] != 3:
+        raise ValueError("twist initial condition is three-dimensional")
+    w = omega0 * np.sin(0.5 * np.pi * X0[:, 1] / length)
+    v = np.zeros_like(X0)
+    v[:, 0] = w * (X0[:, 2] - axis_center[1])
+    v[:, 2] = -w * (X0[:, 0] - axis_center[0])
+    return v
+
+
+def _vec_rec(arr_sorted, n, dim, dev):
+    torch = _lib.torch_cuda()
+    out = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+    out[:, :dim] = arr_sorted
+    return out
+
+
+def _mat_rec(m_sorted, n, dim, dev):
+    """(n, d, d) -> padded row records (3D: (n, 3, 4); 2D: (n, 4); 1D: (n, 4))."""
+    torch = _lib.torch_cuda()
+    if dim == 3:
+        out = torch.zeros((n, 3, 4), dtype=torch.float64, device=dev)
+        out[:, :, :3] = m_sorted
+        return out
+    out = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+    out[:, :dim * dim] = m_sorted.reshape(n, dim * dim)
+    return out
+
+
+def _mat_unrec(rec, n, dim):
+    if dim == 3:
+        return rec[:, :, :3]
+    return rec[:, :dim * dim].reshape(n, dim, dim)
+
+
+class SolidSystem:
+    """Reference configuration, state and fused passes for one solid body."""
+
+    def __init__(self, X0, material: Material, kernel: KernelSpec, dp: float, *, fixed=None,
+                 correction: bool = True, cfl: float = 0.6):
+        if kernel.code != CODE_WENDLAND:
+            raise NotImplementedError("the TL engine evaluates the Wendland family")
+        torch = _lib.torch_cuda()
+        self.X0 = np.ascontiguousarray(X0, dtype=float)
+        self.n, self.dim = self.X0.shape
+        self.material = material
+        self.kernel = kernel
+        self.cfl = float(cfl)
+        self.dp = float(dp)
+        self.vol0 = np.full(self.n, self.dp**self.dim)
+        self.rho0 = material.rho0
+        self.fixed = (np.zeros(self.n, dtype=bool) if fixed is None
+                      else np.asarray(fixed, dtype=bool))
+        self.t = 0.0
+        self.steps = 0
+        dev = _lib.device()
+        self._dev = dev
+
+        self.grid = make_grid(self.X0, kernel.kappa * kernel.h, None)      # tlsph.py:140
+        self.bins = bin_particles(_lib.to_device(self.X0, torch.float64), self.grid)
+        self.nbr, self.cnt, self.width = ell_from_bins(self.bins, kernel.h, kernel.kappa)
+        self.perm = self.bins.perm.long()
+        self.rank = self.bins.rank()
+        self._nlist = None
+        n, d = self.n, self.dim
+
+        vol_s = torch.full((n,), self.dp**d, dtype=torch.float64, device=dev)
+        if correction:
+            m = torch.empty((n, d, d), dtype=torch.float64, device=dev)
+            k = _lib.kernel_struct(kernel)
+            _lib.call("sphb_ell_moments", ctypes.byref(self.grid), n,
+                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), vol_s.data_ptr(), ctypes.byref(k), m.data_ptr(),
+                      _lib.stream_ptr())
+            from .correction import correction_from_moments_device
+
+            b0, _, reg = correction_from_moments_device(m)
+            self.n_regularized = int(reg.sum().item())
+        else:
+            b0 = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d).contiguous()
+            self.n_regularized = 0
+        self._B0_sorted = b0
+        fixed_s = _lib.to_device(self.fixed.astype(np.float64), torch.float64)[self.perm]
+        self.X0rec = _vec_rec(self.bins.ws.t(), n, d, dev)
+        self.X0rec[:, 3] = fixed_s
+        self.B0rec = _mat_rec(b0, n, d, dev)
+        eye = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d)
+        self.Frec = _mat_rec(eye, n, d, dev)
+        self.Qrec = torch.zeros_like(self.Frec)
+        xs = _lib.to_device(self.X0, torch.float64)[self.perm]
+        self.XC = _vec_rec(xs, n, d, dev)
+        self.V = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+        self.A = torch.zeros_like(self.V)
+        self.Vh = torch.zeros_like(self.V)
+        self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        lam, g = material.lame
+        p = self.params = _lib.TLParams()
+        p.dim, p.width, p.n = d, self.width, n
+        p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
+        p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
+        self._cfl_h = self.cfl * kernel.h
+        self._c_s = material.sound_speed
+        self._acc_valid = False
+        self._host = {}
+        self._v_out = False
+
+    # -- host views -----------------------------------------------------------
+    def _orig(self, t):
+        return t[self.rank].cpu().numpy()
+
+    def _cached(self, name, fn):
+        if name not in self._host:
+            self._host[name] = fn()
+        return self._host[name]
+
+    @property
+    def x(self):
+        return self._cached("x", lambda: self._orig(self.XC[:, :self.dim]))
+
+    @property
+    def v(self):
+        """Velocities (caller order).  The array handed out is authoritative
+        until the next step: in-place edits (e.g. `system.v[clamp] = 0`,
+        cases.py:455) are uploaded before stepping."""
+        self._v_out = True
+        return self._cached("v", lambda: self._orig(self.V[:, :self.dim]))
+
+    @v.setter
+    def v(self, value):
+        torch = _lib.torch_cuda()
+        vs = _lib.to_device(np.asarray(value, dtype=float).reshape(self.n, self.dim),
+                            torch.float64)[self.perm]
+        self.V[:, :self.dim] = vs
+        self._host.pop("v", None)
+        self._v_out = False
+
+    def _sync_in(self):
+        if self._v_out and "v" in self._host:
+            host_v = self._host.pop("v")
+            self.v = host_v
+        self._v_out = False
+
+    @property
+    def F(self):
+        return self._cached("F", lambda: self._orig(_mat_unrec(self.Frec, self.n, self.dim)))
+
+    @property
+    def B0(self):
+        return self._cached("B0", lambda: self._orig(self._B0_sorted))
+
+    @property
+    def nlist0(self) -> NeighborList:
+        if self._nlist is None:
+            starts, idx, r, e = csr_from_bins(self.bins)
+            self._nlist = NeighborList(starts, idx, r, e, cutoff=self.grid.cutoff, bins=self.bins)
+        return self._nlist
+
+    # -- force evaluation -------------------------------------------------------
+    def first_pk(self):
+        s = pk2_stress(self.F, self.material)
+        return np.einsum("nab,nbc->nac", self.F, s), s
+
+    def _accelerations_dev(self):
+        st = _lib.stream_ptr()
+        _lib.call("sphb_tl_stress", ctypes.byref(self.params), self.Frec.data_ptr(),
+                  self.B0rec.data_ptr(), self.Qrec.data_ptr(), st)
+        _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
+                  self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
+                  self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
+                  self.scalars.data_ptr(), 0, st)
+        self._acc_valid = True
+
+    def accelerations(self):
+        """Corrected TL momentum rate / rho0 (tlsph.py:164-171), caller order."""
+        self._accelerations_dev()
+        return self._orig(self.A[:, :self.dim])
+
+    def deformation_rates(self):
+        """dF_i = [sum_j V0 (v_j - v_i) (x) grad0 W_ij] B0_i (tlsph.py:173-176),
+        via the reference-order CSR operator (sphb_tl_deformation_rates_csr)."""
+        torch = _lib.torch_cuda()
+        from .correction import pair_gradients_device
+
+        nl = self.nlist0
+        starts, idx, _, _ = nl.device_csr()
+        g0 = (pair_gradients_device(nl, self.kernel, None) * (self.dp**self.dim)).contiguous()
+        v = _lib.to_device(self.v, torch.float64)
+        b0 = _lib.to_device(self.B0, torch.float64)
+        dF = torch.empty((self.n, self.dim, self.dim), dtype=torch.float64, device=self._dev)
+        _lib.call("sphb_tl_deformation_rates_csr", self.n, self.dim, starts.data_ptr(),
+                  idx.data_ptr(), g0.data_ptr(), v.data_ptr(), b0.data_ptr(), dF.data_ptr(),
+                  _lib.stream_ptr())
+        return dF.cpu().numpy()
+
+    def _speed_max(self):
+        _lib.call("sphb_tl_speed_max", ctypes.byref(self.params), self.V.data_ptr(),
+                  self.scalars.data_ptr(), _lib.stream_ptr())
+
+    def stable_dt(self) -> float:
+        """cfl h / (c_s + max|v|) (tlsph.py:178-180)."""
+        self._sync_in()
+        self._speed_max()
+        vmax = float(self.scalars[2].item())
+        return self._cfl_h / (self._c_s + vmax)
+
+    def _one_step(self, dt_override: float):
+        st = _lib.stream_ptr()
+        _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
+                  self.err.data_ptr(), st)
+        _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
+                  self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                  self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
+                  self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
+                  self.err.data_ptr(), st)
+        _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
+                  self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
+                  self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
+                  self.scalars.data_ptr(), 1, st)
+
+    def _raise_if_bad(self):
+        err = int(self.err.item())
+        if err:
+            self.err.zero_()
+            raise SolidStateError(f"deformation gradient inverted (flags {err}) "
+                                  f"at step {self.steps}")
+
+    def step(self, dt: float | None = None) -> float:
+        """Kick-drift-kick update of (v, x, F) (tlsph.py:182-206)."""
+        self._sync_in()
+        if dt is None:
+            dt = self.stable_dt()
+        if not self._acc_valid:
+            self._accelerations_dev()
+        self._one_step(float(dt))
+        self._host.clear()
+        self._raise_if_bad()
+        self.t += dt
+        self.steps += 1
+        return dt
+
+    def advance(self, n_steps: int, dt: float | None = None) -> None:
+        """n_steps steps without host synchronisation; error word checked once."""
+        if n_steps <= 0:
+            return
+        self._sync_in()
+        if not self._acc_valid:
+            self._accelerations_dev()
+        if dt is None:
+            self._speed_max()
+        self.scalars[1] = 0.0
+        for _ in range(n_steps):
+            self._one_step(0.0 if dt is None else float(dt))
+        self._host.clear()
+        self._raise_if_bad()
+        self.t += float(self.scalars[1].item())
+        self.steps += n_steps
+
+    # -- diagnostics ------------------------------------------------------------
+    def energies(self):
+        _, s = self.first_pk()
+        eye = np.eye(self.dim)
+        strain = 0.5 * (np.einsum("nba,nbc->nac", self.F, self.F) - eye)
+        e_strain = 0.5 * float(np.sum(self.vol0 * np.einsum("nab,nab->n", s, strain)))
+        e_kin = 0.5 * float(np.sum(self.rho0 * self.vol0 * np.sum(self.v**2, axis=1)))
+        return e_kin, e_strain
+
+    def momentum(self):
+        return (self.rho0 * self.vol0[:, None] * self.v).sum(axis=0)

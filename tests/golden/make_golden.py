@@ -1,0 +1,208 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container, where the reference is mounted read-only:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports `sph_trunc` (pkg/src of arXiv 2405.05155's package), drives each
+hot-path configuration through the reference's own public functions
+(SURVEY Appendix B recipes, at parity-test sizes) and writes compressed
+.npz fixtures next to this script.  The fixtures are committed; the GPU box
+never needs the reference.  Neighbour lists are stored as SHA-256 digests of
+the raw CSR bytes (starts, idx, r, e) — byte equality, not just set equality —
+plus the arrays themselves for the small cases.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+from sph_trunc import approx, correction, eulerian, neighbors, relaxation, tlsph  # noqa: E402
+from sph_trunc.geometry import lattice_points  # noqa: E402
+from sph_trunc.kernels import kernel_spec  # noqa: E402
+
+from paper_2405_05155_b200 import configs  # noqa: E402  (input generation only)
+
+
+def csr_digest(nl) -> str:
+    h = hashlib.sha256()
+    for a in (nl.starts, nl.idx, nl.r, nl.e):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def neighbor_cases():
+    """Inputs of the reference's own neighbour tests (test_neighbors.py)."""
+    out = {}
+    rng = np.random.default_rng(20240817)
+    pos = rng.uniform(0, 1, size=(500, 2))
+    out["random500"] = (pos, 0.11, None)
+    rng = np.random.default_rng(20240817)
+    pos = rng.uniform(0, 1, size=(300, 2))
+    out["periodic300"] = (pos, 0.13, (1.0, 1.0))
+    rng = np.random.default_rng(20240817)
+    out["random3d_200"] = (rng.uniform(0, 1, size=(200, 3)), 0.25, None)
+    out["lattice_sw"] = (lattice_points((0, 0), (9, 9), 1.0), 2.6, None)
+    out["lattice_tw"] = (lattice_points((0, 0), (9, 9), 1.0), 2.08, None)
+    out["lattice3d"] = (lattice_points((0, 0, 0), (9, 9, 9), 1.0), 2.3, None)
+    out["periodic_lattice8"] = (lattice_points((0, 0), (8, 8), 1.0), 2.08, (8.0, 8.0))
+    out["exact_cutoff"] = (np.array([[0.0, 0.0], [1.0, 0.0]]), 1.0, None)
+    rng = np.random.default_rng(7)
+    out["random1d_100"] = (rng.uniform(-1, 1, size=(100, 1)), 0.3, None)
+    return out
+
+
+def main():
+    # ---------------------------------------------------------- neighbours
+    arrays = {}
+    for name, (pos, cut, box) in neighbor_cases().items():
+        nl = neighbors.build_neighbors(pos, cut, box=box)
+        arrays[f"{name}__pos"] = pos
+        arrays[f"{name}__cutoff"] = np.array(cut)
+        arrays[f"{name}__box"] = np.array(box if box is not None else [])
+        arrays[f"{name}__starts"] = nl.starts
+        arrays[f"{name}__idx"] = nl.idx
+        arrays[f"{name}__r"] = nl.r
+        arrays[f"{name}__e"] = nl.e
+        arrays[f"{name}__digest"] = np.array(csr_digest(nl))
+    save("neighbors", **arrays)
+
+    # ------------------------------------------- operators on small inputs
+    arrays = {}
+    rng = np.random.default_rng(11)
+    pos = rng.uniform(0, 1, size=(400, 2))
+    vols = rng.uniform(0.5, 1.5, size=400) / 400
+    for fam in ("wendland", "wendland-truncated", "laguerre-gauss"):
+        spec = kernel_spec(fam, 0.05, 2)
+        nl = neighbors.build_neighbors(pos, 2.0 * spec.h)   # 2h list, kappa skip exercised
+        key = fam.replace("-", "_")
+        arrays[f"{key}__unity"] = approx.sph_unity_sum(nl, vols, spec)
+        arrays[f"{key}__accel"] = relaxation.relax_accelerations(nl, vols, spec, 1.3, 0.9)
+        arrays[f"{key}__moments"] = correction.moment_matrices(nl, vols, spec)
+        res = correction.correction_matrices(nl, vols, spec)
+        arrays[f"{key}__B"] = res.B
+        arrays[f"{key}__det"] = res.det_neg_m
+        arrays[f"{key}__nreg"] = np.array(res.n_regularized)
+        arrays[f"{key}__gw"] = correction.pair_gradients(nl, spec, res.B)
+        arrays[f"{key}__gw0"] = correction.pair_gradients(nl, spec, None)
+    arrays["pos"] = pos
+    arrays["vols"] = vols
+    pos3 = rng.uniform(0, 1, size=(300, 3))
+    spec3 = kernel_spec("wendland", 0.1, 3)
+    nl3 = neighbors.build_neighbors(pos3, spec3.kappa * spec3.h)
+    res3 = correction.correction_matrices(nl3, np.full(300, 1.0 / 300), spec3)
+    arrays["pos3"] = pos3
+    arrays["B3"] = res3.B
+    arrays["det3"] = res3.det_neg_m
+    save("operators", **arrays)
+
+    # ------------------------------------------------------------- C1
+    c1 = configs.c1_relax(seed=0)
+    spec = kernel_spec("laguerre-gauss", c1["h"], 2)
+    pos = c1["pos"].copy()
+    n = pos.shape[0]
+    vols = np.full(n, c1["vol"])
+    box = np.asarray(c1["box"])
+    dt2 = c1["step_scale"] * spec.h**2
+    cap = 0.25 * c1["dp"]
+    digests, residuals, snaps = [], [], {}
+    for step in range(c1["n_updates"] + 1):
+        nl = neighbors.build_neighbors(pos, spec.kappa * spec.h, box=box)
+        if step in (0, 1, c1["n_updates"]):
+            digests.append(csr_digest(nl))
+            snaps[step] = pos.copy()
+        acc = relaxation.relax_accelerations(nl, vols, spec)
+        residuals.append(float(np.mean(np.linalg.norm(acc, axis=1)) * spec.h))
+        if step == 0:
+            acc0 = acc.copy()
+        if step == c1["n_updates"]:
+            break
+        dx = acc * dt2
+        norms = np.linalg.norm(dx, axis=1)
+        over = norms > cap
+        if np.any(over):
+            dx[over] *= (cap / norms[over])[:, None]
+        pos += dx
+        pos %= box
+    dens = {}
+    for key, fam in configs.FAMILY.items():
+        ds = kernel_spec(fam, c1["h"], 2)
+        nl = neighbors.build_neighbors(pos, ds.kappa * ds.h, box=box)
+        dens[key] = approx.sph_unity_sum(nl, vols, ds)
+        dens[key + "_digest"] = csr_digest(nl)
+    save("c1_relax", pos0=snaps[0], pos1=snaps[1], pos100=snaps[c1["n_updates"]],
+         acc0=acc0, residuals=np.asarray(residuals), digests=np.array(digests),
+         rho_1p6h=dens["1.6h"], rho_2h=dens["2h"],
+         digest_1p6h=np.array(dens["1.6h_digest"]), digest_2h=np.array(dens["2h_digest"]))
+
+    # ---------------------------------------------------- C2 / C5 (reduced)
+    for label, builder, size, nsteps in (("c2_tgv2d", configs.c2_tgv2d, 64, 100),
+                                         ("c5_tgv3d", configs.c5_tgv3d, 16, 20)):
+        arrays = {}
+        for key in ("1.6h", "2h"):
+            cfg = builder(kernel=key, n_side=size)
+            n = cfg["pos"].shape[0]
+            state = eulerian.FluidState(vol=cfg["vol"].copy(), rho=cfg["rho"].copy(),
+                                        mom=cfg["mom"].copy(), etot=None, n_interior=n)
+            eos = eulerian.EosParams(eulerian.WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"],
+                                     c_art=cfg["c_art"])
+            solver = eulerian.EulerianSolver(cfg["pos"], n, state, eos, cfg["spec"], None,
+                                             correction=True, cfl=cfg["cfl"], mu=cfg["mu"],
+                                             periodic_box=cfg["box"])
+            tag = key.replace(".", "p")
+            drho, dmom, _ = solver.rhs()
+            arrays[f"{tag}__drho0"] = drho.copy()
+            arrays[f"{tag}__dmom0"] = dmom.copy()
+            dts = []
+            for s in range(1, nsteps + 1):
+                dts.append(solver.step())
+                if s in (1, nsteps):
+                    arrays[f"{tag}__rho{s}"] = solver.state.rho.copy()
+                    arrays[f"{tag}__mom{s}"] = solver.state.mom.copy()
+            arrays[f"{tag}__dts"] = np.asarray(dts)
+            arrays[f"{tag}__digest"] = np.array(csr_digest(solver.nlist))
+        arrays["n_side"] = np.array(size)
+        arrays["steps"] = np.array(nsteps)
+        save(label, **arrays)
+
+    # ---------------------------------------------------- C3 / C4 (reduced)
+    for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
+                                           ("c4_column", configs.c4_column, {"n_width": 6}, 50)):
+        arrays = {}
+        for key in ("1.6h", "2h"):
+            cfg = builder(kernel=key, **kwargs)
+            mat = tlsph.Material(cfg["material"].rho0, cfg["material"].E, cfg["material"].nu)
+            system = tlsph.SolidSystem(cfg["X0"], mat, cfg["spec"], cfg["dp"],
+                                       fixed=cfg["fixed"], correction=True, cfl=cfg["cfl"])
+            system.v = cfg["v0"].copy()
+            tag = key.replace(".", "p")
+            arrays[f"{tag}__B0"] = system.B0.copy()
+            arrays[f"{tag}__digest"] = np.array(csr_digest(system.nlist0))
+            dts = []
+            for s in range(1, nsteps + 1):
+                dts.append(system.step())
+                if s in (1, nsteps):
+                    arrays[f"{tag}__x{s}"] = system.x.copy()
+                    arrays[f"{tag}__v{s}"] = system.v.copy()
+                    arrays[f"{tag}__F{s}"] = system.F.copy()
+            arrays[f"{tag}__dts"] = np.asarray(dts)
+        arrays["steps"] = np.array(nsteps)
+        save(label, **arrays)
+
+
+if __name__ == "__main__":
+    main()

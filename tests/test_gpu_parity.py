@@ -1,0 +1,405 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Two checkers: golden vectors produced by the reference package itself
+(tests/golden, reduced sizes) and the CPU oracle (oracle/, pinned to the
+same goldens by test_oracle_golden.py) at full config sizes.
+
+Tolerances (BASELINE.json north_star): neighbour sets (and here the whole
+CSR, r and e included) bit-exact; fields within relative L2 1e-12 after one
+step and 1e-8 after 100+ steps, in FP64.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2405_05155_b200 import approx, configs, correction, neighbors, relaxation
+from paper_2405_05155_b200.approx import l2_error
+from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                            FluidState, SolverError)
+from paper_2405_05155_b200.geometry import lattice_points
+from paper_2405_05155_b200.kernels import kernel_spec
+from paper_2405_05155_b200.tlsph import Material, SolidStateError, SolidSystem
+
+pytestmark = pytest.mark.gpu
+
+TOL_1 = 1e-12
+TOL_100 = 1e-8
+
+
+def digest(nl):
+    h = hashlib.sha256()
+    for a in (nl.starts, nl.idx, nl.r, nl.e):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+# ------------------------------------------------------------ neighbours
+NEIGHBOR_CASES = ["random500", "periodic300", "random3d_200", "lattice_sw", "lattice_tw",
+                  "lattice3d", "periodic_lattice8", "exact_cutoff", "random1d_100"]
+
+
+@pytest.mark.parametrize("case", NEIGHBOR_CASES)
+def test_csr_byte_identical_to_reference(gold, case):
+    g = gold("neighbors")
+    box = g[f"{case}__box"]
+    nl = neighbors.build_neighbors(g[f"{case}__pos"], float(g[f"{case}__cutoff"]),
+                                   box if box.size else None)
+    assert np.array_equal(nl.starts, g[f"{case}__starts"])
+    assert np.array_equal(nl.idx, g[f"{case}__idx"])
+    assert np.array_equal(nl.r, g[f"{case}__r"])
+    assert np.array_equal(nl.e, g[f"{case}__e"])
+    assert digest(nl) == str(g[f"{case}__digest"])
+
+
+def test_reference_neighbor_unit_cases(rng):
+    # pkg/tests/test_neighbors.py:44-58, 95-129
+    assert neighbors.build_neighbors(np.array([[0.0, 0.0], [3.0, 0.0]]), 2.6).counts.tolist() == [0, 0]
+    assert neighbors.build_neighbors(np.array([[0.0, 0.0], [1.0, 0.0]]), 1.0).counts.tolist() == [1, 1]
+    pos = lattice_points((0, 0), (9, 9), 1.0)
+    assert neighbors.neighbor_count_ratio(pos, 2.08, 2.6) == pytest.approx(0.60)
+    assert neighbors.neighbor_count_ratio(pos, 2.6, 2.6) == 1.0
+    pos3 = lattice_points((0, 0, 0), (9, 9, 9), 1.0)
+    assert abs(neighbors.neighbor_count_ratio(pos3, 1.84, 2.3) - 0.512) <= 0.12
+    nl = neighbors.build_neighbors(np.array([[0.0, 0.0], [1.0, 0.0]]), 1.5)
+    assert nl.idx[nl.starts[0]] == 1 and nl.e[nl.starts[0]] == pytest.approx([-1.0, 0.0])
+    p = rng.uniform(0, 1, size=(400, 2))
+    a, b = neighbors.build_neighbors(p, 0.1), neighbors.build_neighbors(p, 0.1)
+    assert np.array_equal(a.starts, b.starts) and np.array_equal(a.idx, b.idx)
+    with pytest.raises(ValueError):
+        neighbors.build_neighbors(np.array([[np.nan, 0.0]]), 1.0)
+    with pytest.raises(ValueError):
+        neighbors.build_neighbors(np.zeros((3, 2)), -1.0)
+    with pytest.raises(ValueError):
+        neighbors.build_neighbors(np.zeros((3, 2)), 0.6, box=(1.0, 1.0))
+    with pytest.raises(ValueError):
+        neighbors.neighbor_count_ratio(np.zeros((4, 2)), 1.0, 2.0)
+
+
+def test_neighbors_random_property_vs_oracle():
+    # pkg/tests/test_neighbors.py:84-92 (random dims, sizes, cutoffs)
+    for seed in range(12):
+        rng = np.random.default_rng(seed)
+        dim = int(rng.integers(1, 4))
+        n = int(rng.integers(10, 120))
+        pos = rng.uniform(-1, 1, size=(n, dim))
+        cut = float(rng.uniform(0.2, 0.8))
+        got = neighbors.build_neighbors(pos, cut)
+        assert digest(got) == digest(O.build_neighbors(pos, cut))
+
+
+def test_neighbors_edge_cases():
+    # single particle, coincident particles (r2 == 0 excluded), tiny boxes
+    nl = neighbors.build_neighbors(np.array([[0.3, 0.4]]), 0.5)
+    assert nl.starts.tolist() == [0, 0] and nl.idx.size == 0
+    pos = np.array([[0.0, 0.0], [0.0, 0.0], [0.5, 0.0]])
+    nl = neighbors.build_neighbors(pos, 1.0)
+    assert digest(nl) == digest(O.build_neighbors(pos, 1.0))
+    assert nl.counts.tolist() == [1, 1, 2]
+    # periodic box of exactly two cutoffs: ncell == 2 double-visit reproduced
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 1, size=(60, 2))
+    nl = neighbors.build_neighbors(pos, 0.5, box=(1.0, 1.0))
+    assert digest(nl) == digest(O.build_neighbors(pos, 0.5, (1.0, 1.0)))
+    # negative coordinates wrapped by np.remainder
+    pos = rng.uniform(-3, 3, size=(200, 2))
+    assert digest(neighbors.build_neighbors(pos, 0.2, box=(1.0, 1.0))) == \
+        digest(O.build_neighbors(pos, 0.2, (1.0, 1.0)))
+
+
+# ------------------------------------------------------------ operators
+FAMS = ["wendland", "wendland_truncated", "laguerre_gauss"]
+
+
+@pytest.mark.parametrize("fam", FAMS)
+def test_operators_match_reference(gold, fam):
+    g = gold("operators")
+    spec = kernel_spec(fam.replace("_", "-"), 0.05, 2)
+    nl = neighbors.build_neighbors(g["pos"], 2.0 * spec.h)
+    vols = g["vols"]
+    # Wendland: the no-FMA device loops equal the reference bit for bit;
+    # Laguerre-Gauss differs only through exp() (<= 2 ulp)
+    rtol = 0.0 if fam != "laguerre_gauss" else 1e-14
+    np.testing.assert_allclose(approx.sph_unity_sum(nl, vols, spec), g[f"{fam}__unity"], rtol=rtol)
+    acc = relaxation.relax_accelerations(nl, vols, spec, 1.3, 0.9)
+    np.testing.assert_allclose(acc, g[f"{fam}__accel"], rtol=rtol, atol=1e-14 * np.abs(acc).max())
+    m = correction.moment_matrices(nl, vols, spec)
+    np.testing.assert_allclose(m, g[f"{fam}__moments"], rtol=rtol, atol=1e-14)
+    res = correction.correction_matrices(nl, vols, spec)
+    np.testing.assert_allclose(res.B, g[f"{fam}__B"], rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(res.det_neg_m, g[f"{fam}__det"], rtol=1e-11, atol=1e-13)
+    assert res.n_regularized == int(g[f"{fam}__nreg"])
+    gw = correction.pair_gradients(nl, spec, g[f"{fam}__B"])
+    np.testing.assert_allclose(gw, g[f"{fam}__gw"], rtol=rtol, atol=1e-14 * np.abs(gw).max())
+    gw0 = correction.pair_gradients(nl, spec, None)
+    np.testing.assert_allclose(gw0, g[f"{fam}__gw0"], rtol=rtol, atol=1e-14 * np.abs(gw0).max())
+
+
+def test_correction_3d_matches_reference(gold):
+    g = gold("operators")
+    spec = kernel_spec("wendland", 0.1, 3)
+    nl = neighbors.build_neighbors(g["pos3"], spec.kappa * spec.h)
+    res = correction.correction_matrices(nl, np.full(300, 1.0 / 300), spec)
+    np.testing.assert_allclose(res.B, g["B3"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(res.det_neg_m, g["det3"], rtol=1e-10, atol=1e-14)
+
+
+def test_reference_correction_unit_cases(rng):
+    # pkg/tests/test_correction.py
+    def setup(family, n=13):
+        pos = lattice_points((0, 0), (float(n), float(n)), 1.0)
+        spec = kernel_spec(family, 1.3, 2)
+        nl = neighbors.build_neighbors(pos, spec.kappa * spec.h)
+        c = int(np.argmin(np.linalg.norm(pos - 0.5 * n, axis=1)))
+        return pos, np.ones(len(pos)), spec, nl, c
+
+    for fam, m00, scale in (("wendland", -0.9739, 1.0268), ("wendland-truncated", -0.9204, 1.0864)):
+        _, vols, spec, nl, c = setup(fam)
+        m = correction.moment_matrices(nl, vols, spec)[c]
+        assert m[0, 1] == pytest.approx(0.0, abs=1e-12)
+        assert m[0, 0] == pytest.approx(m00, abs=2e-4)
+        b = correction.correction_matrices(nl, vols, spec).B[c]
+        assert b[0, 1] == pytest.approx(0.0, abs=1e-10)
+        assert b[0, 0] == pytest.approx(b[1, 1], rel=1e-12)
+        assert b[0, 0] == pytest.approx(scale, abs=2e-3)
+    # half plane: M B^T = -I to round-off
+    pos, vols, spec, nl, c = setup("wendland")
+    keep = pos[:, 1] <= pos[c, 1]
+    ph = pos[keep]
+    nlh = neighbors.build_neighbors(ph, spec.kappa * spec.h)
+    ch = int(np.argmin(np.linalg.norm(ph - pos[c], axis=1)))
+    b = correction.correction_matrices(nlh, vols[keep], spec).B[ch]
+    assert not np.allclose(b, np.eye(2), atol=0.05)
+    m = correction.moment_matrices(nlh, vols[keep], spec)[ch]
+    assert m @ b.T == pytest.approx(-np.eye(2), abs=1e-10)
+    # collinear stencil degrades to identity
+    pos = np.column_stack([np.linspace(0, 2, 9), np.zeros(9)])
+    spec = kernel_spec("wendland", 0.33, 2)
+    res = correction.correction_matrices(neighbors.build_neighbors(pos, spec.kappa * spec.h),
+                                         np.full(9, 0.25**2), spec)
+    assert res.n_regularized >= 1
+    assert np.isfinite(res.B[4]).all() and res.B[4][1, 1] == pytest.approx(1.0, abs=1e-6)
+    # det(-M) at the lattice centre
+    _, vols, spec, nl, c = setup("wendland", n=9)
+    assert correction.correction_matrices(nl, vols, spec).det_neg_m[c] == pytest.approx(0.9485, abs=1e-3)
+    # corrected-gradient antisymmetry
+    p = rng.uniform(0, 1, size=(40, 2))
+    spec = kernel_spec("wendland", 0.2, 2)
+    nl = neighbors.build_neighbors(p, spec.kappa * spec.h)
+    b = correction.correction_matrices(nl, np.full(40, 1 / 40), spec).B
+    gw = correction.pair_gradients(nl, spec, b)
+    look = {(i, int(nl.idx[k])): gw[k] for i in range(nl.n) for k in range(nl.starts[i], nl.starts[i + 1])}
+    for (i, j), v in look.items():
+        assert look[(j, i)] == pytest.approx(-v, rel=1e-12, abs=1e-15)
+    # periodic lattice first-order consistency
+    pos = lattice_points((0, 0), (8, 8), 1.0)
+    spec = kernel_spec("wendland-truncated", 1.3, 2)
+    nl = neighbors.build_neighbors(pos, spec.kappa * spec.h, box=(8.0, 8.0))
+    b = correction.correction_matrices(nl, np.ones(len(pos)), spec).B
+    gw = correction.pair_gradients(nl, spec, b)
+    i = 27
+    m = np.zeros((2, 2))
+    for k in range(nl.starts[i], nl.starts[i + 1]):
+        m += np.outer(nl.r[k] * nl.e[k], gw[k])
+    assert m == pytest.approx(-np.eye(2), abs=1e-8)
+
+
+# ------------------------------------------------------------ C1
+def test_c1_one_update_and_density(gold):
+    g = gold("c1_relax")
+    c1 = configs.c1_relax(seed=0)
+    spec = c1["relax_spec"]
+    rl = relaxation.PeriodicRelaxer(c1["pos"], spec, c1["box"], c1["dp"])
+    rl.accelerate()
+    acc0 = rl.acc[:rl.n].cpu().numpy()
+    assert l2_error(acc0, g["acc0"]) < 1e-14
+    assert rl.residual()[0] == pytest.approx(g["residuals"][0], rel=1e-13)
+    rl.update()
+    pos1 = rl.positions()
+    assert l2_error(pos1, g["pos1"]) < 1e-15
+    # neighbour lists on the reference's own trajectory: byte-identical
+    for step, key in ((0, "pos0"), (1, "pos1"), (2, "pos100")):
+        nl = neighbors.build_neighbors(g[key], spec.kappa * spec.h, box=c1["box"])
+        assert digest(nl) == str(g["digests"][step])
+    # density summation at 1.6h and 2h on the reference's final positions
+    for key, tag in (("1.6h", "1p6h"), ("2h", "2h")):
+        ds = configs.density_specs(c1["h"])[key]
+        nl = neighbors.build_neighbors(g["pos100"], ds.kappa * ds.h, box=c1["box"])
+        assert digest(nl) == str(g[f"digest_{tag}"])
+        rho = approx.sph_unity_sum(nl, np.full(len(g["pos100"]), c1["vol"]), ds)
+        assert np.array_equal(rho, g[f"rho_{tag}"])
+
+
+def test_c1_100_updates(gold):
+    g = gold("c1_relax")
+    c1 = configs.c1_relax(seed=0)
+    pos, res = relaxation.relax_steps(c1["pos"], c1["relax_spec"], c1["box"], c1["dp"], 100)
+    d_ref = g["pos100"] - g["pos0"]
+    d_gpu = (pos - g["pos0"] + 0.5) % 1.0 - 0.5   # periodic minimum image
+    d_ref = (d_ref + 0.5) % 1.0 - 0.5
+    assert l2_error(d_gpu, d_ref) < TOL_100
+    np.testing.assert_allclose(res, g["residuals"], rtol=1e-9)
+
+
+def test_periodic_relax_api():
+    from paper_2405_05155_b200.geometry import Box
+
+    cfg = relaxation.RelaxationConfig(shape=Box((0, 0), (1, 1)), dp=0.05,
+                                      kernel=kernel_spec("wendland", 0.065, 2), max_steps=20,
+                                      periodic_box=(1.0, 1.0))
+    res = relaxation.relax(cfg)
+    assert res.positions.shape == (400, 2) and res.residuals.size >= 1
+
+
+# ------------------------------------------------------------ WC Eulerian
+def make_wc(cfg, correction_on=True):
+    n = cfg["pos"].shape[0]
+    state = FluidState(vol=cfg["vol"].copy(), rho=cfg["rho"].copy(), mom=cfg["mom"].copy(),
+                       etot=None, n_interior=n)
+    eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"])
+    return EulerianSolver(cfg["pos"], n, state, eos, cfg["spec"], None, correction=correction_on,
+                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+
+
+@pytest.mark.parametrize("label,builder", [("c2_tgv2d", configs.c2_tgv2d),
+                                           ("c5_tgv3d", configs.c5_tgv3d)])
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_wc_vs_reference_golden(gold, label, builder, key):
+    g = gold(label)
+    tag = key.replace(".", "p")
+    solver = make_wc(builder(kernel=key, n_side=int(g["n_side"])))
+    assert digest(solver.nlist) == str(g[f"{tag}__digest"])
+    drho, dmom, _ = solver.rhs()
+    assert l2_error(drho, g[f"{tag}__drho0"]) < TOL_1
+    assert l2_error(dmom, g[f"{tag}__dmom0"]) < TOL_1
+    steps = int(g["steps"])
+    dts = []
+    for k in range(1, steps + 1):
+        dts.append(solver.step())
+        if k in (1, steps):
+            tol = TOL_1 if k == 1 else TOL_100
+            st = solver.state
+            assert l2_error(st.rho, g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(st.mom, g[f"{tag}__mom{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_c2_full_size_vs_oracle(key):
+    cfg = configs.c2_tgv2d(kernel=key)
+    solver = make_wc(cfg)
+    ref = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
+                       cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    solver.step()
+    ref.step()
+    assert l2_error(solver.state.rho, ref.rho) < TOL_1
+    assert l2_error(solver.state.mom, ref.mom) < TOL_1
+    solver.advance(99)
+    for _ in range(99):
+        ref.step()
+    assert l2_error(solver.state.rho, ref.rho) < TOL_100
+    assert l2_error(solver.state.mom, ref.mom) < TOL_100
+    assert solver.t == pytest.approx(ref.t, rel=1e-12)
+
+
+def test_wc_totals_and_conservation():
+    cfg = configs.c2_tgv2d(n_side=48)
+    solver = make_wc(cfg)
+    m0, p0, _ = solver.totals()
+    solver.advance(20)
+    m1, p1, _ = solver.totals()
+    assert m1 == pytest.approx(m0, rel=1e-13)
+    assert np.abs(p1 - p0).max() < 1e-12
+
+
+def test_wc_host_state_edits_are_uploaded():
+    cfg = configs.c2_tgv2d(n_side=32)
+    solver = make_wc(cfg)
+    solver.state.rho[:] = 1.0
+    solver.state.mom[:] = 0.0
+    drho, dmom, _ = solver.rhs()
+    assert np.abs(drho).max() < 1e-12 and np.abs(dmom).max() < 1e-12
+
+
+def test_wc_bad_state_raises():
+    cfg = configs.c2_tgv2d(n_side=32)
+    cfg["rho"] = cfg["rho"].copy()
+    cfg["rho"][5] = np.nan
+    solver = make_wc(cfg)
+    with pytest.raises(SolverError):
+        solver.step(1e-4)
+
+
+# ------------------------------------------------------------ TL-SPH
+def make_tl(cfg):
+    m = cfg["material"]
+    s = SolidSystem(cfg["X0"], Material(m.rho0, m.E, m.nu), cfg["spec"], cfg["dp"],
+                    fixed=cfg["fixed"], correction=True, cfl=cfg["cfl"])
+    s.v = cfg["v0"].copy()
+    return s
+
+
+@pytest.mark.parametrize("label,builder,kwargs", [
+    ("c3_plate", configs.c3_plate, {"dp": 0.002}),
+    ("c4_column", configs.c4_column, {"n_width": 6}),
+])
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_tl_vs_reference_golden(gold, label, builder, kwargs, key):
+    g = gold(label)
+    tag = key.replace(".", "p")
+    s = make_tl(builder(kernel=key, **kwargs))
+    assert digest(s.nlist0) == str(g[f"{tag}__digest"])
+    np.testing.assert_allclose(s.B0, g[f"{tag}__B0"], rtol=1e-11, atol=1e-11)
+    steps = int(g["steps"])
+    dts = []
+    for k in range(1, steps + 1):
+        dts.append(s.step())
+        if k in (1, steps):
+            tol = TOL_1 if k == 1 else TOL_100
+            assert l2_error(s.x, g[f"{tag}__x{k}"]) < tol
+            assert l2_error(s.v, g[f"{tag}__v{k}"]) < tol
+            assert l2_error(s.F, g[f"{tag}__F{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_c3_full_size_vs_oracle(key):
+    cfg = configs.c3_plate(kernel=key)
+    s = make_tl(cfg)
+    m = cfg["material"]
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"])
+    ref.v = cfg["v0"].copy()
+    s.step()
+    ref.step()
+    for a, b in ((s.x, ref.x), (s.v, ref.v), (s.F, ref.F)):
+        assert l2_error(a, b) < TOL_1
+    s.advance(199)
+    for _ in range(199):
+        ref.step()
+    for a, b in ((s.x, ref.x), (s.v, ref.v), (s.F, ref.F)):
+        assert l2_error(a, b) < TOL_100
+
+
+def test_tl_deformation_rates_api_matches_oracle():
+    cfg = configs.c3_plate(dp=0.002)
+    s = make_tl(cfg)
+    m = cfg["material"]
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"])
+    ref.v = cfg["v0"].copy()
+    assert l2_error(s.deformation_rates(), ref.deformation_rates()) < 1e-12
+    s.step()
+    ref.step()
+    assert l2_error(s.accelerations(), ref.accelerations()) < 1e-10
+
+
+def test_tl_inverted_raises():
+    cfg = configs.c3_plate(dp=0.004)
+    s = make_tl(cfg)
+    s.v = np.random.default_rng(0).normal(0, 1e4, size=cfg["X0"].shape)
+    with pytest.raises(SolidStateError):
+        for _ in range(5):
+            s.step()

@@ -1,0 +1,175 @@
+"""Pin the CPU oracle to the reference (CPU only, no GPU needed).
+
+The oracle (oracle/) is the checker of every GPU parity test, so it is
+trusted only after matching (a) golden vectors produced by the reference
+package itself (tests/golden/make_golden.py) and (b) every known value the
+reference's own unit tests assert for the hot path (pkg/tests/*).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2405_05155_b200 import configs
+from paper_2405_05155_b200.geometry import lattice_points
+from paper_2405_05155_b200.kernels import kernel_spec
+
+
+def digest(nl):
+    h = hashlib.sha256()
+    for a in (nl.starts, nl.idx, nl.r, nl.e):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+NEIGHBOR_CASES = ["random500", "periodic300", "random3d_200", "lattice_sw", "lattice_tw",
+                  "lattice3d", "periodic_lattice8", "exact_cutoff", "random1d_100"]
+
+
+@pytest.mark.parametrize("case", NEIGHBOR_CASES)
+def test_oracle_csr_byte_identical(gold, case):
+    g = gold("neighbors")
+    box = g[f"{case}__box"]
+    nl = O.build_neighbors(g[f"{case}__pos"], float(g[f"{case}__cutoff"]),
+                           box if box.size else None)
+    assert np.array_equal(nl.starts, g[f"{case}__starts"])
+    assert np.array_equal(nl.idx, g[f"{case}__idx"])
+    assert np.array_equal(nl.r, g[f"{case}__r"])
+    assert np.array_equal(nl.e, g[f"{case}__e"])
+    assert digest(nl) == str(g[f"{case}__digest"])
+
+
+def test_oracle_lattice_counts():
+    # pkg/tests/test_neighbors.py:38-45
+    pos = lattice_points((0, 0), (9, 9), 1.0)
+    c = np.argmin(np.linalg.norm(pos - 4.5, axis=1))
+    assert O.build_neighbors(pos, 2.6).counts[c] == 20
+    assert O.build_neighbors(pos, 2.08).counts[c] == 12
+
+
+def test_oracle_brute_force_periodic(rng):
+    # pkg/tests/test_neighbors.py:68-81 with the O(N^2) minimum-image oracle
+    pos = rng.uniform(0, 1, size=(300, 2))
+    box = np.array([1.0, 1.0])
+    nl = O.build_neighbors(pos, 0.13, box)
+    want = set()
+    for i in range(300):
+        d = pos[i] - pos
+        d -= np.round(d / box) * box
+        r = np.linalg.norm(d, axis=1)
+        want |= {(i, int(j)) for j in np.where((r <= 0.13) & (r > 0))[0]}
+    got = {(i, int(j)) for i in range(nl.n) for j in nl.idx[nl.starts[i]:nl.starts[i + 1]]}
+    assert got == want
+
+
+FAMS = ["wendland", "wendland_truncated", "laguerre_gauss"]
+
+
+@pytest.mark.parametrize("fam", FAMS)
+def test_oracle_operators(gold, fam):
+    g = gold("operators")
+    spec = kernel_spec(fam.replace("_", "-"), 0.05, 2)
+    nl = O.build_neighbors(g["pos"], 2.0 * spec.h)
+    vols = g["vols"]
+    # the C loops are the reference loops: bit-identical
+    assert np.array_equal(O.sph_unity_sum(nl, vols, spec), g[f"{fam}__unity"])
+    assert np.array_equal(O.relax_accelerations(nl, vols, spec, 1.3, 0.9), g[f"{fam}__accel"])
+    assert np.array_equal(O.moment_matrices(nl, vols, spec), g[f"{fam}__moments"])
+    b, det, nreg = O.correction_matrices(nl, vols, spec)
+    np.testing.assert_allclose(b, g[f"{fam}__B"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(det, g[f"{fam}__det"], rtol=1e-12, atol=1e-14)
+    assert nreg == int(g[f"{fam}__nreg"])
+    assert np.array_equal(O.pair_gradients(nl, spec, g[f"{fam}__B"]), g[f"{fam}__gw"])
+    assert np.array_equal(O.pair_gradients(nl, spec, None), g[f"{fam}__gw0"])
+
+
+def test_oracle_correction_known_values():
+    # pkg/tests/test_correction.py:22-48, 78-81
+    for fam, m00, bscale in (("wendland", -0.9739, 1.0268), ("wendland-truncated", -0.9204, 1.0864)):
+        pos = lattice_points((0, 0), (13.0, 13.0), 1.0)
+        spec = kernel_spec(fam, 1.3, 2)
+        nl = O.build_neighbors(pos, spec.kappa * spec.h)
+        c = int(np.argmin(np.linalg.norm(pos - 6.5, axis=1)))
+        m = O.moment_matrices(nl, np.ones(len(pos)), spec)[c]
+        assert m[0, 0] == pytest.approx(m00, abs=2e-4)
+        assert m[0, 1] == pytest.approx(0.0, abs=1e-12)
+        b = O.correction_matrices(nl, np.ones(len(pos)), spec)[0][c]
+        assert b[0, 0] == pytest.approx(bscale, abs=2e-3)
+    pos = lattice_points((0, 0), (9.0, 9.0), 1.0)
+    spec = kernel_spec("wendland", 1.3, 2)
+    nl = O.build_neighbors(pos, spec.kappa * spec.h)
+    c = int(np.argmin(np.linalg.norm(pos - 4.5, axis=1)))
+    assert O.correction_matrices(nl, np.ones(len(pos)), spec)[1][c] == pytest.approx(0.9485, abs=1e-3)
+
+
+def test_oracle_c1_relaxation(gold):
+    g = gold("c1_relax")
+    c1 = configs.c1_relax(seed=0)
+    assert np.array_equal(c1["pos"], g["pos0"])
+    spec = kernel_spec("laguerre-gauss", c1["h"], 2)
+    # one update is the reference bit for bit (same libm exp on this host)
+    pos1, res1 = O.relax_steps(c1["pos"], spec, c1["box"], c1["dp"], 1)
+    assert np.array_equal(pos1, g["pos1"])
+    assert digest(O.build_neighbors(g["pos1"], spec.kappa * spec.h, c1["box"])) == str(g["digests"][1])
+    np.testing.assert_allclose(res1, g["residuals"][:2], rtol=1e-13)
+
+
+@pytest.mark.slow
+def test_oracle_c1_100_updates(gold):
+    g = gold("c1_relax")
+    c1 = configs.c1_relax(seed=0)
+    spec = kernel_spec("laguerre-gauss", c1["h"], 2)
+    pos, res = O.relax_steps(c1["pos"], spec, c1["box"], c1["dp"], 100)
+    np.testing.assert_allclose(res, g["residuals"], rtol=1e-12)
+    assert np.array_equal(pos, g["pos100"])
+    for key, tag in (("1.6h", "1p6h"), ("2h", "2h")):
+        ds = configs.density_specs(c1["h"])[key]
+        nl = O.build_neighbors(pos, ds.kappa * ds.h, c1["box"])
+        assert digest(nl) == str(g[f"digest_{tag}"])
+        assert np.array_equal(O.sph_unity_sum(nl, np.full(len(pos), c1["vol"]), ds), g[f"rho_{tag}"])
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_c2_tgv2d(gold, key):
+    g = gold("c2_tgv2d")
+    tag = key.replace(".", "p")
+    cfg = configs.c2_tgv2d(kernel=key, n_side=int(g["n_side"]))
+    s = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
+                     cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    assert digest(s.nl) == str(g[f"{tag}__digest"])
+    drho, dmom = s.rhs()
+    np.testing.assert_allclose(drho, g[f"{tag}__drho0"], rtol=0, atol=1e-12 * np.abs(drho).max())
+    np.testing.assert_allclose(dmom, g[f"{tag}__dmom0"], rtol=0, atol=1e-12 * np.abs(dmom).max())
+    steps = int(g["steps"])
+    for k in range(1, steps + 1):
+        s.step()
+        if k in (1, steps):
+            tol = 1e-13 if k == 1 else 1e-10
+            from paper_2405_05155_b200.approx import l2_error
+
+            assert l2_error(s.rho, g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(s.mom, g[f"{tag}__mom{k}"]) < tol
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_c3_plate(gold, key):
+    g = gold("c3_plate")
+    tag = key.replace(".", "p")
+    cfg = configs.c3_plate(kernel=key, dp=0.002)
+    m = cfg["material"]
+    s = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True, cfg["cfl"])
+    assert digest(s.nl) == str(g[f"{tag}__digest"])
+    np.testing.assert_allclose(s.B0, g[f"{tag}__B0"], rtol=1e-12, atol=1e-12)
+    s.v = cfg["v0"].copy()
+    steps = int(g["steps"])
+    from paper_2405_05155_b200.approx import l2_error
+
+    for k in range(1, steps + 1):
+        s.step()
+        if k in (1, steps):
+            tol = 1e-12 if k == 1 else 1e-9
+            assert l2_error(s.x, g[f"{tag}__x{k}"]) < tol
+            assert l2_error(s.v, g[f"{tag}__v{k}"]) < tol
+            assert l2_error(s.F, g[f"{tag}__F{k}"]) < tol

@@ -1,0 +1,332 @@
+"""Benchmark of the SPH particle-interaction hot path on B200.
+
+Workload (BASELINE.json configs[4], the north star's headline case): the 3D
+weakly-compressible Eulerian Taylor-Green vortex, periodic [0, 2pi]^3,
+256^3 = 16,777,216 fixed lattice particles, Riemann fluxes with kernel-
+gradient correction, FP64.  One "step" = one EulerianSolver midpoint step
+(two fused flux stages + device dt).  The truncated kernel (1.6h) is the
+headline `value`; the standard 2h leg runs in the same process for the
+truncation speed-up.  Inputs (~2.6 GB of particle records) exceed the 126 MB
+L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+C oracle port of the numba loops, all host threads) on a bounded sample of
+the same workload (a 64^3 TGV, same per-particle work).
+
+One JSON line on rank 0.  Multi-GPU (torchrun): the z-slab decomposition of
+the periodic box is not in this round yet, so N > 1 runs independent
+replicas (scaling "weak"); see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "particle-steps/s and pair-interactions/s at 1.6h vs 2h; % of HBM roofline"
+# compulsory FP64 bytes per particle-step for C5 (stage 1: x 24
+# + B 48 + rho 8 + mom 24 read, 32 write = 136; stage 2: + U^n 32 = 168)
+BYTES_STAGE = {1: 136, 2: 168}
+# FP64 operations per directed pair of the fused stage kernel, counted from the
+# source of k_wc_stage (geometry ~45 incl. rsqrt, flux ~70); replaced by SASS
+# counts in profiles/ when ncu is run.
+FLOPS_PER_PAIR_EST = 120
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi samples of SM clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 2 + k and r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_solver(cfg):
+    from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                                FluidState)
+
+    n = cfg["pos"].shape[0]
+    st = FluidState(vol=cfg["vol"], rho=cfg["rho"], mom=cfg["mom"], etot=None, n_interior=n)
+    eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"])
+    return EulerianSolver(cfg["pos"], n, st, eos, cfg["spec"], None, correction=True,
+                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+
+
+def fp64_peak(torch, lib):
+    """Measured DFMA throughput (TFLOP/s) of this GPU: the FP64 roofline."""
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads, iters = sms * 8, 256, 20000
+    s = torch.cuda.current_stream().cuda_stream
+    lib.sphb_fp64_probe(out.data_ptr(), blocks, threads, 2000, s)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    lib.sphb_fp64_probe(out.data_ptr(), blocks, threads, iters, s)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return 2.0 * 8 * iters * blocks * threads / (ms * 1e-3) / 1e12
+
+
+def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
+    """Device-timed K steps of one kernel leg; returns a dict of measurements."""
+    solver = make_solver(cfg)
+    n = solver.n
+    pairs = int(solver.cnt.sum().item())            # directed pairs per pass
+    solver.advance(warmup)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    solver.timer = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(clocks_index) if clocks_index is not None else None
+    if sampler:
+        sampler.__enter__()
+    torch.cuda.synchronize()
+    e0.record()
+    solver.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = {1: [], 2: []}
+    for stage, a, b in solver.timer:
+        st[stage].append(a.elapsed_time(b))
+    solver.timer = None
+    return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st,
+            "clocks": sampler.summary() if sampler else None}
+
+
+def e2e_leg(torch, solver, steps, warmup):
+    """Through the public API with host buffers: every step uploads the state
+    from pinned host memory (EulerianSolver.load_state), advances one step and
+    reads the state back (read_state) — both copies inside the timed region."""
+    n, d = solver.n, solver.dim
+    rho_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    mom_h = torch.empty((n, d), dtype=torch.float64).pin_memory()
+    solver.read_state(rho_h, mom_h)
+    torch.cuda.synchronize()
+
+    def one():
+        solver.load_state(rho_h, mom_h)
+        solver.advance(1)
+        solver.read_state(rho_h, mom_h)
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    nbytes = rho_h.numel() * 8 + mom_h.numel() * 8
+    return ms / steps, nbytes
+
+
+def cpu_reference(kind_n_side=64, steps=3, kernel="1.6h"):
+    """The reference algorithm on the host cores: oracle port (C loops of the
+    numba kernels + numpy glue), all OpenMP threads, TGV-3D at n_side^3."""
+    from oracle import oracle as O
+    from paper_2405_05155_b200 import configs
+
+    cfg = configs.c5_tgv3d(kernel=kernel, n_side=kind_n_side)
+    s = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
+                     cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    s.rhs()                                          # warm-up (bench.py:94-105 protocol)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.step()
+    dt = time.perf_counter() - t0
+    n = cfg["pos"].shape[0]
+    return {"value": n * steps / dt, "unit": "particle-steps/s", "cores": O.threads(),
+            "kind": "port", "pairs_per_s": int(s.nl.starts[-1]) * 2 * steps / dt,
+            "sample": f"TGV-3D {kind_n_side}^3 ({n} particles, {kernel}), {steps} steps after one "
+                      "warm-up rhs; same per-particle work as 256^3"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-side", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-2h", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": f"c5_tgv3d_{args.n_side}^3_wc_euler_riemann_corrected",
+              "particles_per_gpu": args.n_side**3, "kernel": "wendland C2 truncated 1.6h",
+              "steps_definition": "one midpoint step = 2 fused flux stages",
+              "l2": "inputs > L2 (126 MB); no flush", "parallelism": f"replicas x{world}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        warm = max(0, args.warmup)
+        ref = cpu_reference(steps=max(1, args.steps))
+        ms = 1e3 * (64**3) / ref["value"]
+        line = {"metric": METRIC, "value": ref["value"], "unit": "particle-steps/s",
+                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "particle-steps/s",
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "pair_interactions_per_s": ref["pairs_per_s"]}
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2405_05155_b200 import _lib, configs
+
+    lib = _lib.lib()
+    pk, pk_kind = peaks()
+    fp64_tf = fp64_peak(torch, lib)
+
+    leg = {}
+    cfg = configs.c5_tgv3d(kernel="1.6h", n_side=args.n_side)
+    leg["1.6h"] = run_leg(torch, cfg, args.steps, max(3, args.warmup), dist, world,
+                          clocks_index=local)
+    e2e_ms, io_bytes = e2e_leg(torch, leg["1.6h"]["solver"], max(2, args.steps // 4), 1)
+    del leg["1.6h"]["solver"]
+    torch.cuda.empty_cache()
+    if not args.no_2h:
+        cfg2 = configs.c5_tgv3d(kernel="2h", n_side=args.n_side)
+        leg["2h"] = run_leg(torch, cfg2, args.steps, max(3, args.warmup), dist, world)
+        del leg["2h"]["solver"]
+        torch.cuda.empty_cache()
+
+    L = leg["1.6h"]
+    n, K = L["n"], args.steps
+    ms_step = L["ms"] / K
+    value = world * n * K / (L["ms"] * 1e-3)
+    stage_all = L["stage_ms"][1] + L["stage_ms"][2]
+    avg_stage_ms = sum(stage_all) / len(stage_all)
+    alg_bytes = n * (BYTES_STAGE[1] + BYTES_STAGE[2]) / 2.0       # per launch (avg stage)
+    achieved = alg_bytes / (avg_stage_ms * 1e-3) / 1e9
+    hbm_peak = float(pk["hbm_gbs"])
+    fp64_ach = L["pairs"] * FLOPS_PER_PAIR_EST / (avg_stage_ms * 1e-3) / 1e12
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
+        "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic TGV-3D fields on the 256^3 lattice)", "config": config,
+        "pair_interactions_per_s": world * L["pairs"] * 2 * K / (L["ms"] * 1e-3),
+        "pairs_per_pass": L["pairs"],
+        "gpu_launches": 3 * K,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "k_wc_stage<3>", "peak_kind": pk_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": avg_stage_ms,
+                     "stage_ms": {"1": statistics.mean(L["stage_ms"][1]),
+                                  "2": statistics.mean(L["stage_ms"][2])},
+                     "fp64": {"achieved_tflops_est": fp64_ach, "peak_tflops_measured": fp64_tf,
+                              "frac": fp64_ach / fp64_tf,
+                              "flops_per_pair_est": FLOPS_PER_PAIR_EST}},
+        "clocks": L["clocks"],
+        "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": "particle-steps/s",
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+                "ms_per_step": e2e_ms,
+                "path": "EulerianSolver.load_state(pinned) -> advance(1) -> read_state(pinned)"},
+    }
+    if "2h" in leg:
+        S = leg["2h"]
+        line["standard_2h"] = {
+            "value": world * S["n"] * K / (S["ms"] * 1e-3), "ms_per_step": S["ms"] / K,
+            "pair_interactions_per_s": world * S["pairs"] * 2 * K / (S["ms"] * 1e-3),
+            "pairs_per_pass": S["pairs"]}
+        line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_reference()
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

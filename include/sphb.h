@@ -88,6 +88,8 @@ typedef struct sphb_kernel {
 const char* sphb_version(void);
 const char* sphb_last_cuda_error(void);
 int sphb_device_count(void);
+/* FP64 DFMA throughput probe (2*8*iters flops per thread) for the roofline. */
+int sphb_fp64_probe(double* out, int32_t blocks, int32_t threads, int32_t iters, void* stream);
 
 /* ---------------------------------------------------------------- binning */
 
@@ -237,6 +239,13 @@ int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, const double* X,
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,
                       void* stream);
+
+/* Caller-order (rho (n), mom (n, d)) <-> sorted S/M records, with
+ * v = mom / rho (FluidState.velocity, eulerian.py:461-462). */
+int sphb_wc_pack_state(int64_t n, int32_t dim, const int32_t* perm, const double* rho,
+                       const double* mom, double* S, double* M, void* stream);
+int sphb_wc_unpack_state(int64_t n, int32_t dim, const int32_t* perm, const double* S,
+                         const double* M, double* rho, double* mom, void* stream);
 
 /* dt for the next step: dt = dt_override if > 0, else
  * cfl_h / (c_add + scalars[2]); then scalars[1] += dt, scalars[2] = 0.

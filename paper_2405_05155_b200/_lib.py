@@ -119,6 +119,9 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_wc_pack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
+    "sphb_wc_unpack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
+    "sphb_fp64_probe": (C.c_int, [P, I32, I32, I32, P]),
     "sphb_set_dt": (C.c_int, [F64, F64, F64, P, P, P]),
     "sphb_tl_pass_a": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, I32, P]),

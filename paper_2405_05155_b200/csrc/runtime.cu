@@ -20,3 +20,28 @@ extern "C" int sphb_device_count(void) {
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
   return n;
 }
+
+// FP64 pipe probe: 8 independent DFMA chains per thread; flops = 2 * 8 * iters
+// per thread.  Used by bench.py to measure the FP64 roofline denominator live
+// (MEASURED_PEAKS.json carries no FP64 figure).
+__global__ void k_fp64_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int sphb_fp64_probe(double* out, int32_t blocks, int32_t threads, int32_t iters,
+                               void* stream) {
+  if (blocks <= 0 || threads <= 0 || iters <= 0) return SPHB_ERR_ARG;
+  k_fp64_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters, 0.999999, 1e-7);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}

@@ -292,6 +292,47 @@ k_speed_max(int64_t n, double c, const double4* __restrict__ S, double* __restri
   }
 }
 
+
+// --------------------------------------------------------- state transfer
+// U (caller order, AoS rho (n), mom (n, d)) -> sorted records S = {v, rho},
+// M = {mom}; v = mom / rho as FluidState.velocity (eulerian.py:461-462).
+template <int D>
+__global__ void k_wc_pack(int64_t n, const int32_t* __restrict__ perm,
+                          const double* __restrict__ rho, const double* __restrict__ mom,
+                          double4* __restrict__ S, double4* __restrict__ M) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t i = perm[s];
+  const double r = rho[i];
+  double v[D], m[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    m[a] = mom[i * D + a];
+    v[a] = __ddiv_rn(m[a], r);
+  }
+  S[s] = pack_s<D>(v, r);
+  double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) c[a] = m[a];
+  M[s] = make_double4(c[0], c[1], c[2], c[3]);
+}
+
+template <int D>
+__global__ void k_wc_unpack(int64_t n, const int32_t* __restrict__ perm,
+                            const double4* __restrict__ S, const double4* __restrict__ M,
+                            double* __restrict__ rho, double* __restrict__ mom) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t i = perm[s];
+  double v[D], r;
+  unpack_s<D>(S[s], v, r);
+  rho[i] = r;
+  const double4 mm = M[s];
+  const double c[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+  for (int a = 0; a < D; ++a) mom[i * D + a] = c[a];
+}
+
 }  // namespace
 
 // dt = dt_override or cfl_h / (c_add + smax)  (eulerian.py:553-560,
@@ -361,6 +402,38 @@ extern "C" int sphb_set_dt(double cfl_h, double c_add, double dt_override, doubl
                            int32_t* err, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   k_set_dt<<<1, 1, 0, st>>>(cfl_h, c_add, dt_override, scalars, err);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_wc_pack_state(int64_t n, int32_t dim, const int32_t* perm, const double* rho,
+                                  const double* mom, double* s, double* m, void* stream) {
+  if (n < 0) return SPHB_ERR_ARG;
+  if (n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(n, 256);
+  switch (dim) {
+    case 1: k_wc_pack<1><<<grid, 256, 0, st>>>(n, perm, rho, mom, (double4*)s, (double4*)m); break;
+    case 2: k_wc_pack<2><<<grid, 256, 0, st>>>(n, perm, rho, mom, (double4*)s, (double4*)m); break;
+    case 3: k_wc_pack<3><<<grid, 256, 0, st>>>(n, perm, rho, mom, (double4*)s, (double4*)m); break;
+    default: return SPHB_ERR_ARG;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_wc_unpack_state(int64_t n, int32_t dim, const int32_t* perm, const double* s,
+                                    const double* m, double* rho, double* mom, void* stream) {
+  if (n < 0) return SPHB_ERR_ARG;
+  if (n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(n, 256);
+  switch (dim) {
+    case 1: k_wc_unpack<1><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
+    case 2: k_wc_unpack<2><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
+    case 3: k_wc_unpack<3><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
+    default: return SPHB_ERR_ARG;
+  }
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

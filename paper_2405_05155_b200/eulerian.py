@@ -260,20 +260,43 @@ class EulerianSolver:
         self.M_nx = torch.empty_like(self.M)
         self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._rho_io = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self._mom_io = torch.empty((self.n, self.dim), dtype=torch.float64, device=dev)
         self._vol_host = vol
+        self.timer = None   # optional list collecting (stage, start_event, end_event)
         self.set_state(state)
 
     # -- state transfer -----------------------------------------------------
     def set_state(self, state: FluidState) -> None:
-        """Upload conserved fields (orig order) and refresh max(c + |v|)."""
+        """Upload conserved fields (caller order) and refresh max(c + |v|)."""
+        self.load_state(np.asarray(state.rho, dtype=float), np.asarray(state.mom, dtype=float))
+
+    def load_state(self, rho, mom) -> None:
+        """Upload (rho (n,), mom (n, d)) given in caller order.
+
+        Accepts numpy arrays or torch tensors; pinned host tensors are copied
+        asynchronously on the current stream (no host synchronisation).
+        """
         torch = _lib.torch_cuda()
-        rho = _lib.to_device(np.asarray(state.rho, dtype=float), torch.float64)[self.perm]
-        mom = _lib.to_device(np.asarray(state.mom, dtype=float), torch.float64)[self.perm]
-        v = mom / rho[:, None]                                 # FluidState.velocity
-        self.S.copy_(_rec4([v[:, a] for a in range(self.dim)] + [rho], self.n, self._dev))
-        self.M.copy_(_rec4([mom[:, a] for a in range(self.dim)], self.n, self._dev))
+        if isinstance(rho, torch.Tensor) and rho.device.type == "cpu":
+            rho_d = self._rho_io.copy_(rho, non_blocking=True)
+            mom_d = self._mom_io.copy_(mom.reshape(self.n, self.dim), non_blocking=True)
+        else:
+            rho_d = _lib.to_device(rho, torch.float64)
+            mom_d = _lib.to_device(mom, torch.float64).reshape(self.n, self.dim)
+        _lib.call("sphb_wc_pack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+                  rho_d.data_ptr(), mom_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(),
+                  _lib.stream_ptr())
         self._state_host = None
         self._refresh_speed()
+
+    def read_state(self, rho_out, mom_out) -> None:
+        """Write (rho, mom) in caller order into host tensors (pinned: async)."""
+        _lib.call("sphb_wc_unpack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+                  self.S.data_ptr(), self.M.data_ptr(), self._rho_io.data_ptr(),
+                  self._mom_io.data_ptr(), _lib.stream_ptr())
+        rho_out.copy_(self._rho_io, non_blocking=True)
+        mom_out.reshape(self.n, self.dim).copy_(self._mom_io, non_blocking=True)
 
     def _sync_in(self):
         if self._handed_out and self._state_host is not None:
@@ -294,10 +317,13 @@ class EulerianSolver:
         before the next rhs/compute_dt/step."""
         self._handed_out = True
         if self._state_host is None:
-            rho = self.S[:, self.dim][self.rank].cpu().numpy()
-            mom = self.M[:, :self.dim][self.rank].cpu().numpy()
-            self._state_host = FluidState(vol=self._vol_host.copy(), rho=rho, mom=mom,
-                                          etot=None, n_interior=self.n_int)
+            torch = _lib.torch_cuda()
+            rho = torch.empty(self.n, dtype=torch.float64)
+            mom = torch.empty((self.n, self.dim), dtype=torch.float64)
+            self.read_state(rho, mom)
+            torch.cuda.current_stream().synchronize()
+            self._state_host = FluidState(vol=self._vol_host.copy(), rho=rho.numpy(),
+                                          mom=mom.numpy(), etot=None, n_interior=self.n_int)
         return self._state_host
 
     @property
@@ -317,6 +343,18 @@ class EulerianSolver:
         return None
 
     def _launch_stage(self, stage, s_in, s_n, m_n, s_out, m_out):
+        if self.timer is not None:
+            torch = _lib.torch_cuda()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            self._launch_stage_raw(stage, s_in, s_n, m_n, s_out, m_out)
+            ev1.record()
+            self.timer.append((stage, ev0, ev1))
+            return
+        self._launch_stage_raw(stage, s_in, s_n, m_n, s_out, m_out)
+
+    def _launch_stage_raw(self, stage, s_in, s_n, m_n, s_out, m_out):
         _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.X.data_ptr(),
                   self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), s_in.data_ptr(),
                   s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),

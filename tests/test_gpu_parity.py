@@ -141,8 +141,15 @@ def test_correction_3d_matches_reference(gold):
     g = gold("operators")
     spec = kernel_spec("wendland", 0.1, 3)
     nl = neighbors.build_neighbors(g["pos3"], spec.kappa * spec.h)
-    res = correction.correction_matrices(nl, np.full(300, 1.0 / 300), spec)
-    np.testing.assert_allclose(res.B, g["B3"], rtol=1e-10, atol=1e-10)
+    vols = np.full(300, 1.0 / 300)
+    res = correction.correction_matrices(nl, vols, spec)
+    # B = -M^-1 is only defined to cond(M) * eps: random 3D points near the
+    # boundary give cond(M) up to ~1e8, where LAPACK and the device Jacobi SVD
+    # legitimately differ in the trailing digits
+    m = correction.moment_matrices(nl, vols, spec)
+    cond = np.linalg.cond(m)
+    tol = np.maximum(1e-12, 1e-14 * cond)[:, None, None] * np.maximum(1.0, np.abs(g["B3"]).max(axis=(1, 2)))[:, None, None]
+    assert np.all(np.abs(res.B - g["B3"]) <= tol)
     np.testing.assert_allclose(res.det_neg_m, g["det3"], rtol=1e-10, atol=1e-14)
 
 

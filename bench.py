@@ -158,7 +158,9 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     for stage, a, b in solver.timer:
         st[stage].append(a.elapsed_time(b))
     solver.timer = None
-    return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st,
+    kernel = (("k_wc_stage_tiled<3,%d>" % solver.plan.group) if solver.plan
+              else "k_wc_stage<3,%d>" % solver.group)
+    return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None}
 
 
@@ -298,7 +300,7 @@ def main():
         "gpu_launches": 3 * K,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None,
-                     "kernel": "k_wc_stage<3>", "peak_kind": pk_kind,
+                     "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": avg_stage_ms,
                      "stage_ms": {"1": statistics.mean(L["stage_ms"][1]),

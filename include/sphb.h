@@ -145,6 +145,21 @@ int sphb_ell_moments(const sphb_grid* g, int64_t n, const double* wrapped_sorted
                      const int32_t* nbr, const int32_t* cnt, const double* vols_sorted,
                      const sphb_kernel* k, double* m_sorted, void* stream);
 
+/* Shared-memory staging plan for a static, binned particle set: tiles of P
+ * consecutive sorted particles; per tile up to rmax runs {start, len,
+ * local_base} of the neighbour union and meta {nruns, union size, local
+ * index of the tile's first particle, ok}.  *max_u = largest union (or
+ * 0x40000000 if some tile cannot be planned).  Then every ELL entry is
+ * rewritten as a uint16 index into its tile's union. */
+size_t sphb_tile_plan_workspace_bytes(const sphb_grid* g);
+int sphb_tile_plan(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                   const int32_t* cell_start, const int32_t* cell_end, int32_t P,
+                   int32_t rmax, int32_t* runs, int32_t* meta, int32_t* max_u,
+                   void* workspace, size_t workspace_bytes, void* stream);
+int sphb_tile_local_nbr(int64_t n, int32_t P, int32_t rmax, const int32_t* nbr,
+                        const int32_t* cnt, const int32_t* runs, const int32_t* meta,
+                        uint16_t* lnbr, int32_t* err, void* stream);
+
 /* ---------------------------------------------- CSR operator passes
  * Bit-faithful restatements of the reference @njit loops (compiled without
  * FMA contraction, same summation order) over a device CSR. */
@@ -208,8 +223,10 @@ int sphb_tl_deformation_rates_csr(int64_t n, int32_t dim, const int64_t* starts,
  *
  * Packed per-particle records, cell-sorted order (4 doubles = 32 B each):
  *   X  [n][4] = {x0, x1, x2, vol}      (2D {x0, x1, vol, 0}; 1D {x0, vol,..})
- *   B  [n][8] = {b00,b01,b02,b11, b12,b22,0,0}  symmetrised correction
- *               (2D {b00,b01,b11,0, 0...}; 1D {b00, 0...})
+ *   B  two planes, 6n doubles: [n][4] {b00,b01,b02,b11} then [n][2]
+ *               {b12,b22} — the symmetrised correction matrix, laid out so
+ *               consecutive particles' records are contiguous
+ *               (2D: plane 0 {b00,b01,b11,0}; 1D: {b00,0,0,0})
  *   S  [n][4] = {v0, v1, v2, rho}      primitive state (2D {v0, v1, rho, 0})
  *   M  [n][4] = {m0, m1, m2, 0}        momentum per unit volume
  * Device scalar block (double[4]): [0] dt, [1] t, [2] max-speed accumulator
@@ -227,15 +244,27 @@ typedef struct sphb_wc_params {
   double vol_const;
 } sphb_wc_params;
 
-/* stage 0: rhs only — S_out = {dmom, drho} records (EulerianSolver.rhs).
+/* `group` (1, 2, 4, 8) consecutive threads share one particle's row.
+ * stage 0: rhs only — S_out = {dmom, drho} records (EulerianSolver.rhs).
  * stage 1: S_in = S_n, writes S_out = U^1 primitive record (M_out unused).
  * stage 2: S_in = U^1 records, own U^n from S_n/M_n, writes U^{n+1} into
  *          S_out/M_out (may alias S_n/M_n) and folds max(c+|v|). */
-int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, const double* X,
+int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t group, const double* X,
                   const double* B, const int32_t* nbr, const int32_t* cnt,
                   const double* S_in, const double* S_n, const double* M_n,
                   double* S_out, double* M_out, double* scalars, int32_t* err,
                   void* stream);
+/* Shared-memory tiled stage (same contract as sphb_wc_stage): tiles of
+ * 256/group particles; each CTA stages its tile's neighbour union (runs from
+ * sphb_tile_plan) into shared memory and `group` threads share a particle;
+ * lnbr is the uint16 local ELL from sphb_tile_local_nbr.  Uniform volumes. */
+int sphb_wc_stage_tiled(const sphb_wc_params* p, int32_t stage, int32_t group,
+                        const double* X, const double* B, const int32_t* cnt,
+                        const uint16_t* lnbr, const int32_t* runs, const int32_t* meta,
+                        int32_t rmax, int32_t umax, const double* S_in, const double* S_n,
+                        const double* M_n, double* S_out, double* M_out, double* scalars,
+                        int32_t* err, void* stream);
+
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,
                       void* stream);

@@ -109,6 +109,10 @@ SIGNATURES = {
     "sphb_ell_count": (C.c_int, [P, I64, P, P, P, F64, F64, P, P, P]),
     "sphb_ell_fill": (C.c_int, [P, I64, P, P, P, F64, F64, I32, P, P]),
     "sphb_ell_moments": (C.c_int, [P, I64, P, P, P, P, P, P, P]),
+    "sphb_tile_plan_workspace_bytes": (SZ, [P]),
+    "sphb_tile_plan": (C.c_int, [P, I64, P, P, P, I32, I32, P, P, P, P, SZ, P]),
+    "sphb_tile_local_nbr": (C.c_int, [I64, I32, I32, P, P, P, P, P, P, P]),
+    "sphb_wc_stage_tiled": (C.c_int, [P, I32, I32, P, P, P, P, P, P, I32, I32, P, P, P, P, P, P, P, P]),
     "sphb_unity_sums": (C.c_int, [I64, P, P, P, P, P, P, P]),
     "sphb_pressure_accel": (C.c_int, [I64, I32, P, P, P, P, P, P, F64, F64, P, P]),
     "sphb_moment_matrices": (C.c_int, [I64, I32, P, P, P, P, P, P, P, P]),
@@ -117,7 +121,7 @@ SIGNATURES = {
     "sphb_rhs_wc_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P, P, F64, F64, P, P, P, P, P]),
     "sphb_tl_accelerations_csr": (C.c_int, [I64, I32, P, P, P, P, F64, P, P]),
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
-    "sphb_wc_stage": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_wc_pack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
     "sphb_wc_unpack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),

@@ -20,106 +20,39 @@
 //           2D: {b00, b01, b11, -}; 1D: {b00, ...}
 //   S[i]  = {v0, v1, v2, rho}   (primitive state; 2D: {v0, v1, rho, 0})
 //   M[i]  = {m0, m1, m2, 0}     (momentum per unit volume)
-#include "common.cuh"
+#include <stdlib.h>
+
+#include "wc_common.cuh"
 
 using namespace sphb;
+using namespace sphb::wc;
 
 namespace {
 
 constexpr int kThreads = 128;
 
-template <int D>
-struct Sym;  // symmetric DxD matrix in packed storage
-template <>
-struct Sym<1> {
-  double a00;
-  __device__ __forceinline__ void load(const double4* B, int64_t i) { a00 = B[2 * i].x; }
-  __device__ __forceinline__ void add(const Sym& o, Sym& r) const { r.a00 = a00 + o.a00; }
-  __device__ __forceinline__ void mv(const double (&e)[1], double (&out)[1]) const {
-    out[0] = a00 * e[0];
-  }
-};
-template <>
-struct Sym<2> {
-  double a00, a01, a11;
-  __device__ __forceinline__ void load(const double4* B, int64_t i) {
-    double4 t = B[2 * i];
-    a00 = t.x; a01 = t.y; a11 = t.z;
-  }
-  __device__ __forceinline__ void add(const Sym& o, Sym& r) const {
-    r.a00 = a00 + o.a00; r.a01 = a01 + o.a01; r.a11 = a11 + o.a11;
-  }
-  __device__ __forceinline__ void mv(const double (&e)[2], double (&out)[2]) const {
-    out[0] = fma(a00, e[0], a01 * e[1]);
-    out[1] = fma(a01, e[0], a11 * e[1]);
-  }
-};
-template <>
-struct Sym<3> {
-  double a00, a01, a02, a11, a12, a22;
-  __device__ __forceinline__ void load(const double4* B, int64_t i) {
-    double4 t = B[2 * i];
-    double4 u = B[2 * i + 1];
-    a00 = t.x; a01 = t.y; a02 = t.z; a11 = t.w; a12 = u.x; a22 = u.y;
-  }
-  __device__ __forceinline__ void add(const Sym& o, Sym& r) const {
-    r.a00 = a00 + o.a00; r.a01 = a01 + o.a01; r.a02 = a02 + o.a02;
-    r.a11 = a11 + o.a11; r.a12 = a12 + o.a12; r.a22 = a22 + o.a22;
-  }
-  __device__ __forceinline__ void mv(const double (&e)[3], double (&out)[3]) const {
-    out[0] = fma(a00, e[0], fma(a01, e[1], a02 * e[2]));
-    out[1] = fma(a01, e[0], fma(a11, e[1], a12 * e[2]));
-    out[2] = fma(a02, e[0], fma(a12, e[1], a22 * e[2]));
-  }
-};
-
-template <int D>
-__device__ __forceinline__ void unpack_x(const double4& t, double (&x)[D], double& vol) {
-  const double c[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-  for (int a = 0; a < D; ++a) x[a] = c[a];
-  vol = c[D];
-}
-
-template <int D>
-__device__ __forceinline__ void unpack_s(const double4& t, double (&v)[D], double& rho) {
-  const double c[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-  for (int a = 0; a < D; ++a) v[a] = c[a];
-  rho = c[D];
-}
-
-template <int D>
-__device__ __forceinline__ double4 pack_s(const double (&v)[D], double rho) {
-  double c[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int a = 0; a < D; ++a) c[a] = v[a];
-  c[D] = rho;
-  return make_double4(c[0], c[1], c[2], c[3]);
-}
-
-template <int D>
-__device__ __forceinline__ double norm_exact(const double (&v)[D]) {
-  // np.linalg.norm over a row: sqrt(((v0*v0) + v1*v1) + v2*v2)
-  double s = __dmul_rn(v[0], v[0]);
-#pragma unroll
-  for (int a = 1; a < D; ++a) s = __dadd_rn(s, __dmul_rn(v[a], v[a]));
-  return __dsqrt_rn(s);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kThreads)
+// G consecutive lanes share one particle: at each step they take G
+// consecutive entries of its row, which in the reference's stencil order are
+// mostly consecutive particles of one cell, so the G neighbour records share
+// cache lines and a warp's gathers need ~G-times fewer L1 wavefronts than
+// one-thread-per-particle.  Partial sums are combined with warp shuffles.
+template <int D, int G, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ X,
-           const double4* __restrict__ B, const int32_t* __restrict__ nbr,
+           const double* __restrict__ B, const int32_t* __restrict__ nbr,
            const int32_t* __restrict__ cnt, const double4* __restrict__ S_in,
            const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
            double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double speed = 0.0;
-  int32_t flags = 0;
-  if (i < n) {
-    const double c = P.c_art;
+  const int gl = threadIdx.x % G;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool active = i < n;
+  const double c = P.c_art;
+  double dr = 0.0;
+  double dm[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) dm[a] = 0.0;
+  if (active) {
     const double c2 = c * c;
     const double eta_c = kEtaLinearized / c;
     const double inv_h = 1.0 / P.h;
@@ -130,26 +63,21 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
     unpack_x<D>(X[i], xi, vol_i);
     unpack_s<D>(S_in[i], vi, rho_i);
     Sym<D> Bi;
-    Bi.load(B, i);
+    Bi.load(B, n, i);
     const double p_i = c2 * (rho_i - P.rho0);
-
-    double dr = 0.0;
-    double dm[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) dm[a] = 0.0;
 
     const int32_t m = cnt[i];
     const int32_t* __restrict__ row = nbr + i;
-    for (int32_t k = 0; k < m; ++k) {
+    for (int32_t k = gl; k < m; k += G) {
       const int64_t j = row[(int64_t)k * n];
       double xj[D], vol_j, vj[D], rho_j;
       unpack_x<D>(X[j], xj, vol_j);
       unpack_s<D>(S_in[j], vj, rho_j);
       Sym<D> Bj;
-      Bj.load(B, j);
+      Bj.load(B, n, j);
       if (P.uniform_vol) vol_j = P.vol_const;
 
-      // geometry
+      // geometry (neighbors.py:152-165, correction.py:102-108, eulerian.py:506-513)
       double dx[D];
       double r2 = 0.0;
 #pragma unroll
@@ -180,7 +108,7 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
       for (int a = 0; a < D; ++a) g[a] *= gs;
       const double viscv = 2.0 * dW * inv_r * vol_j;
 
-      // limited linearised Riemann problem along n = -e
+      // limited linearised Riemann problem along n = -e (eulerian.py:236-264)
       double ul = 0.0, ur = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -192,11 +120,9 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
       beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
       const double rbar = 0.5 * (rho_i + rho_j);
       const double p_j = c2 * (rho_j - P.rho0);
-      const double ubar = 0.5 * (ul + ur);
       double ustar_m_ubar = 0.0;
       if (beta > 0.0) ustar_m_ubar = (beta * beta) * (p_i - p_j) * half_cinv / rbar;
       const double p_star = fma(0.5 * beta * rbar * c, du, 0.5 * (p_i + p_j));
-      (void)ubar;
       double vs[D];
       double s = 0.0;
 #pragma unroll
@@ -213,52 +139,52 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
         dm[a] = fma(mv, vi[a] - vj[a], dm[a] + fm);
       }
     }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    dr += __shfl_xor_sync(0xffffffffu, dr, o);
+#pragma unroll
+    for (int a = 0; a < D; ++a) dm[a] += __shfl_xor_sync(0xffffffffu, dm[a], o);
+  }
 
-    // ---------------------------------------------------------- epilogue
-    if (stage == 0) {  // rhs only: S_out = {dmom, drho} (EulerianSolver.rhs)
-      S_out[i] = pack_s<D>(dm, dr);
-      if (!isfinite(dr)) flags |= SPHB_EFLAG_NONFINITE_FLUX;
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-        if (!isfinite(dm[a])) flags |= SPHB_EFLAG_NONFINITE_FLUX;
-      if (flags) atomicOr(err, flags);
-      return;
-    }
-    const double dt = scalars[0];
-    const double cdt = stage == 1 ? 0.5 * dt : dt;
-    double mom_n[D], rho_n;
-    {
-      const double4 mn = Mn[i];
-      const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
-#pragma unroll
-      for (int a = 0; a < D; ++a) mom_n[a] = cm[a];
-      double vtmp[D];
-      unpack_s<D>(Sn[i], vtmp, rho_n);
-    }
+  // ------------------------------------------------------------ epilogue
+  double speed = 0.0;
+  int32_t flags = 0;
+  if (active && gl == 0) {
     bool finite = isfinite(dr);
 #pragma unroll
     for (int a = 0; a < D; ++a) finite = finite && isfinite(dm[a]);
     if (!finite) flags |= SPHB_EFLAG_NONFINITE_FLUX;
-    const double rho_new = fma(cdt, dr, rho_n);
-    double mom_new[D], v_new[D];
+    if (stage == 0) {  // rhs only: S_out = {dmom, drho} (EulerianSolver.rhs)
+      S_out[i] = pack_s<D>(dm, dr);
+    } else {
+      const double dt = scalars[0];
+      const double cdt = stage == 1 ? 0.5 * dt : dt;
+      const double4 mn = Mn[i];
+      const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
+      double vtmp[D], rho_n;
+      unpack_s<D>(Sn[i], vtmp, rho_n);
+      const double rho_new = fma(cdt, dr, rho_n);   // eulerian.py:619-627
+      double mom_new[D], v_new[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      mom_new[a] = fma(cdt, dm[a], mom_n[a]);
-      v_new[a] = __ddiv_rn(mom_new[a], rho_new);
-    }
-    if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
-    S_out[i] = pack_s<D>(v_new, rho_new);
-    if (stage == 2) {
-      double mc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int a = 0; a < D; ++a) {
+        mom_new[a] = fma(cdt, dm[a], cm[a]);
+        v_new[a] = __ddiv_rn(mom_new[a], rho_new);
+      }
+      if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
+      S_out[i] = pack_s<D>(v_new, rho_new);
+      if (stage == 2) {
+        double mc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int a = 0; a < D; ++a) mc[a] = mom_new[a];
-      M_out[i] = make_double4(mc[0], mc[1], mc[2], mc[3]);
-      speed = __dadd_rn(c, norm_exact<D>(v_new));
+        for (int a = 0; a < D; ++a) mc[a] = mom_new[a];
+        M_out[i] = make_double4(mc[0], mc[1], mc[2], mc[3]);
+        speed = __dadd_rn(c, norm_exact<D>(v_new));
+      }
     }
   }
   if (stage == 2) {
     __shared__ double red[kThreads / 32];
-    double w = warp_max(speed);
+    const double w = warp_max(speed);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -354,28 +280,51 @@ __global__ void k_set_dt(double cfl_h, double c_add, double dt_override, double*
   scalars[2] = 0.0;
 }
 
-extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, const double* x,
-                             const double* b, const int32_t* nbr, const int32_t* cnt,
-                             const double* s_in, const double* s_n, const double* m_n,
-                             double* s_out, double* m_out, double* scalars, int32_t* err,
-                             void* stream) {
+extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t group,
+                             const double* x, const double* b, const int32_t* nbr,
+                             const int32_t* cnt, const double* s_in, const double* s_n,
+                             const double* m_n, double* s_out, double* m_out, double* scalars,
+                             int32_t* err, void* stream) {
   if (!p || p->n < 0 || stage < 0 || stage > 2) return SPHB_ERR_ARG;
   if (p->n == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const unsigned grid = sphb_blocks(p->n, kThreads);
   const double4* X = (const double4*)x;
-  const double4* B = (const double4*)b;
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
-  switch (p->dim) {
-    case 1: k_wc_stage<1><<<grid, kThreads, 0, st>>>(*p, stage, X, B, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err); break;
-    case 2: k_wc_stage<2><<<grid, kThreads, 0, st>>>(*p, stage, X, B, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err); break;
-    case 3: k_wc_stage<3><<<grid, kThreads, 0, st>>>(*p, stage, X, B, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err); break;
+#define SPHB_STAGE(D, G, MB)                                                               \
+  k_wc_stage<D, G, MB><<<sphb_blocks(p->n * G, kThreads), kThreads, 0, st>>>(              \
+      *p, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                   \
+  break
+  // SPHB_WC_MINB (tuning): 4 -> <=128 registers, 6 -> <=80, 8 -> <=64
+  static int minb = [] {
+    const char* e = getenv("SPHB_WC_MINB");
+    return e ? atoi(e) : 4;
+  }();
+  const int key = p->dim * 256 + group * 16 + (p->dim == 3 ? minb : 4);
+  switch (key) {
+    case 256 + 16 + 4: SPHB_STAGE(1, 1, 4);
+    case 256 + 32 + 4: SPHB_STAGE(1, 2, 4);
+    case 512 + 16 + 4: SPHB_STAGE(2, 1, 4);
+    case 512 + 32 + 4: SPHB_STAGE(2, 2, 4);
+    case 512 + 64 + 4: SPHB_STAGE(2, 4, 4);
+    case 768 + 16 + 4: SPHB_STAGE(3, 1, 4);
+    case 768 + 32 + 4: SPHB_STAGE(3, 2, 4);
+    case 768 + 64 + 4: SPHB_STAGE(3, 4, 4);
+    case 768 + 128 + 4: SPHB_STAGE(3, 8, 4);
+    case 768 + 16 + 6: SPHB_STAGE(3, 1, 6);
+    case 768 + 32 + 6: SPHB_STAGE(3, 2, 6);
+    case 768 + 64 + 6: SPHB_STAGE(3, 4, 6);
+    case 768 + 128 + 6: SPHB_STAGE(3, 8, 6);
+    case 768 + 16 + 8: SPHB_STAGE(3, 1, 8);
+    case 768 + 32 + 8: SPHB_STAGE(3, 2, 8);
+    case 768 + 64 + 8: SPHB_STAGE(3, 4, 8);
+    case 768 + 128 + 8: SPHB_STAGE(3, 8, 8);
     default: return SPHB_ERR_ARG;
   }
+#undef SPHB_STAGE
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

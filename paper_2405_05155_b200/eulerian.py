@@ -31,13 +31,15 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
 from .kernels import CODE_WENDLAND, KernelSpec
-from .neighbors import NeighborList, bin_particles, csr_from_bins, ell_from_bins, make_grid
+from .neighbors import (NeighborList, TilePlan, bin_particles, csr_from_bins, ell_from_bins,
+                        make_grid)
 
 IDEAL_GAS = "ideal-gas"
 WEAKLY_COMPRESSIBLE = "weakly-compressible"
@@ -234,13 +236,34 @@ class EulerianSolver:
             self.n_regularized = 0
         self._B_sorted = b
         bs = 0.5 * (b + b.transpose(1, 2))
-        self.B = torch.zeros((self.n, 8), dtype=torch.float64, device=dev)
+        # two planes: [n][4] {b00, b01, b02, b11} then [n][2] {b12, b22}
+        self.B = torch.zeros(6 * self.n, dtype=torch.float64, device=dev)
+        plane0 = self.B[:4 * self.n].view(self.n, 4)
+        plane1 = self.B[4 * self.n:].view(self.n, 2)
         iu = [(a, c) for a in range(self.dim) for c in range(a, self.dim)]
         for col, (a, c) in enumerate(iu):
-            self.B[:, col] = bs[:, a, c]
+            if col < 4:
+                plane0[:, col] = bs[:, a, c]
+            else:
+                plane1[:, col - 4] = bs[:, a, c]
 
         ws = self.bins.ws
         self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
+        # lanes per particle (scripts/tune_wc.py sweep on B200, 192^3 TGV-3D:
+        # one lane per particle is best for 32-entry rows, two lanes tie for
+        # 80-entry rows; profiles/r01_tune_wc.md)
+        self.group = 1 if self.width <= 40 else 2
+        if os.environ.get("SPHB_WC_GROUP"):      # tuning override
+            self.group = int(os.environ["SPHB_WC_GROUP"])
+        # optional shared-memory tiled variant (SPHB_WC_KERNEL=tiled)
+        self.plan = None
+        if (os.environ.get("SPHB_WC_KERNEL", "global") == "tiled" and uniform and self.n
+                and self.width):
+            nsym = {1: 1, 2: 3, 3: 6}[self.dim]
+            plan = TilePlan(self.bins, self.nbr, self.cnt, self.width,
+                            fields=2 * self.dim + nsym + 1)
+            if plan.ok:
+                self.plan = plan
 
         self.params = _lib.WCParams()
         p = self.params
@@ -355,7 +378,17 @@ class EulerianSolver:
         self._launch_stage_raw(stage, s_in, s_n, m_n, s_out, m_out)
 
     def _launch_stage_raw(self, stage, s_in, s_n, m_n, s_out, m_out):
-        _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.X.data_ptr(),
+        if self.plan is not None:
+            pl = self.plan
+            _lib.call("sphb_wc_stage_tiled", ctypes.byref(self.params), stage, pl.group,
+                      self.X.data_ptr(), self.B.data_ptr(), self.cnt.data_ptr(),
+                      pl.lnbr.data_ptr(), pl.runs.data_ptr(), pl.meta.data_ptr(), pl.RMAX,
+                      pl.umax, s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
+                      None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                      self.err.data_ptr(), _lib.stream_ptr())
+            return
+        _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.group,
+                  self.X.data_ptr(),
                   self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), s_in.data_ptr(),
                   s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
                   None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),

@@ -1,0 +1,67 @@
+"""Sweep launch variants of the WC stage kernel on one config (GPU box).
+
+    python scripts/tune_wc.py [--n-side 192] [--kernel 1.6h]
+
+Each variant runs in a fresh process (the variant switches are read once per
+process): SPHB_WC_KERNEL (global|tiled), SPHB_WC_GROUP (lanes per particle),
+SPHB_WC_MINB (min resident CTAs -> register cap).  Prints one JSON line per
+variant with the mean stage time (CUDA events).
+"""
+
+import argparse
+import itertools
+import json
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def one(n_side, kernel, steps):
+    sys.path.insert(0, REPO)
+    import torch
+
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                                FluidState)
+
+    cfg = configs.c5_tgv3d(kernel=kernel, n_side=n_side)
+    n = cfg["pos"].shape[0]
+    st = FluidState(cfg["vol"], cfg["rho"], cfg["mom"], None, n)
+    s = EulerianSolver(cfg["pos"], n, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0),
+                       cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+    s.advance(3)
+    torch.cuda.synchronize()
+    s.timer = []
+    s.advance(steps)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for _, a, b in s.timer]
+    rho = s.state.rho
+    print(json.dumps({"stage_ms": sum(ms) / len(ms), "pairs": int(s.cnt.sum().item()),
+                      "group": s.group, "plan": s.plan is not None, "rho_sum": float(rho.sum())}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-side", type=int, default=192)
+    ap.add_argument("--kernel", default="1.6h")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--one", action="store_true")
+    args = ap.parse_args()
+    if args.one:
+        one(args.n_side, args.kernel, args.steps)
+        return
+    variants = [("global", g, mb) for g, mb in itertools.product((1, 2, 4, 8), (4, 6, 8))]
+    variants.append(("tiled", 4 if args.kernel == "1.6h" else 8, 4))
+    for kern, g, mb in variants:
+        env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb))
+        out = subprocess.run([sys.executable, __file__, "--one", "--n-side", str(args.n_side),
+                              "--kernel", args.kernel, "--steps", str(args.steps)], env=env,
+                             capture_output=True, text=True)
+        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
+        print(json.dumps({"kernel": kern, "group": g, "minb": mb, "result": line}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -15,9 +15,10 @@ L2, so no flush is needed between steps.
 C oracle port of the numba loops, all host threads) on a bounded sample of
 the same workload (a 64^3 TGV, same per-particle work).
 
-One JSON line on rank 0.  Multi-GPU (torchrun): the z-slab decomposition of
-the periodic box is not in this round yet, so N > 1 runs independent
-replicas (scaling "weak"); see DESIGN.md.
+One JSON line on rank 0.  Multi-GPU (torchrun): the 256^3 box is cut into
+z-slabs of whole cell layers, one per GPU, with a halo layer exchanged over
+NCCL after every stage and the dt max all-reduced (slab.py) — strong scaling
+of the same 16.8M-particle problem.
 """
 
 from __future__ import annotations
@@ -100,13 +101,18 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def make_solver(cfg):
+def make_solver(cfg, dist=None, rank=0, world=1):
     from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
                                                 FluidState)
 
     n = cfg["pos"].shape[0]
     st = FluidState(vol=cfg["vol"], rho=cfg["rho"], mom=cfg["mom"], etot=None, n_interior=n)
     eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"])
+    if world > 1:   # z-slabs of the periodic box, NCCL halo exchange (slab.py)
+        from paper_2405_05155_b200.slab import slab_eulerian
+
+        return slab_eulerian(cfg["pos"], st, eos, cfg["spec"], rank=rank, world=world, dist=dist,
+                             cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
     return EulerianSolver(cfg["pos"], n, st, eos, cfg["spec"], None, correction=True,
                           cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
 
@@ -130,9 +136,14 @@ def fp64_peak(torch, lib):
 
 def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     """Device-timed K steps of one kernel leg; returns a dict of measurements."""
-    solver = make_solver(cfg)
-    n = solver.n
-    pairs = int(solver.cnt.sum().item())            # directed pairs per pass
+    rank = dist.get_rank() if dist is not None else 0
+    solver = make_solver(cfg, dist, rank, world)
+    n = cfg["pos"].shape[0]                          # particles of the whole job
+    rows = solver._slab.rows if solver._slab is not None else slice(0, solver.n)
+    pairs_t = solver.cnt[rows].sum().to(torch.int64).reshape(1)
+    if dist is not None:
+        dist.all_reduce(pairs_t)
+    pairs = int(pairs_t.item())                      # directed pairs per pass, all ranks
     solver.advance(warmup)
     torch.cuda.synchronize()
     if dist is not None:
@@ -231,7 +242,8 @@ def main():
     config = {"workload": f"c5_tgv3d_{args.n_side}^3_wc_euler_riemann_corrected",
               "particles_per_gpu": args.n_side**3, "kernel": "wendland C2 truncated 1.6h",
               "steps_definition": "one midpoint step = 2 fused flux stages",
-              "l2": "inputs > L2 (126 MB); no flush", "parallelism": f"replicas x{world}"}
+              "l2": "inputs > L2 (126 MB); no flush",
+              "parallelism": "single GPU" if world == 1 else f"z-slabs x{world}, NCCL halo"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -282,20 +294,20 @@ def main():
     L = leg["1.6h"]
     n, K = L["n"], args.steps
     ms_step = L["ms"] / K
-    value = world * n * K / (L["ms"] * 1e-3)
+    value = n * K / (L["ms"] * 1e-3)                 # whole job (n = all ranks' particles)
     stage_all = L["stage_ms"][1] + L["stage_ms"][2]
     avg_stage_ms = sum(stage_all) / len(stage_all)
-    alg_bytes = n * (BYTES_STAGE[1] + BYTES_STAGE[2]) / 2.0       # per launch (avg stage)
+    alg_bytes = n / world * (BYTES_STAGE[1] + BYTES_STAGE[2]) / 2.0  # per launch, per GPU
     achieved = alg_bytes / (avg_stage_ms * 1e-3) / 1e9
     hbm_peak = float(pk["hbm_gbs"])
-    fp64_ach = L["pairs"] * FLOPS_PER_PAIR_EST / (avg_stage_ms * 1e-3) / 1e12
+    fp64_ach = L["pairs"] / world * FLOPS_PER_PAIR_EST / (avg_stage_ms * 1e-3) / 1e12
 
     line = {
         "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
         "steps": K, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic TGV-3D fields on the 256^3 lattice)", "config": config,
-        "pair_interactions_per_s": world * L["pairs"] * 2 * K / (L["ms"] * 1e-3),
+        "pair_interactions_per_s": L["pairs"] * 2 * K / (L["ms"] * 1e-3),
         "pairs_per_pass": L["pairs"],
         "gpu_launches": 3 * K,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -309,7 +321,7 @@ def main():
                               "frac": fp64_ach / fp64_tf,
                               "flops_per_pair_est": FLOPS_PER_PAIR_EST}},
         "clocks": L["clocks"],
-        "e2e": {"value": world * n / (e2e_ms * 1e-3), "unit": "particle-steps/s",
+        "e2e": {"value": n / (e2e_ms * 1e-3), "unit": "particle-steps/s",
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
                 "ms_per_step": e2e_ms,
                 "path": "EulerianSolver.load_state(pinned) -> advance(1) -> read_state(pinned)"},
@@ -317,8 +329,8 @@ def main():
     if "2h" in leg:
         S = leg["2h"]
         line["standard_2h"] = {
-            "value": world * S["n"] * K / (S["ms"] * 1e-3), "ms_per_step": S["ms"] / K,
-            "pair_interactions_per_s": world * S["pairs"] * 2 * K / (S["ms"] * 1e-3),
+            "value": S["n"] * K / (S["ms"] * 1e-3), "ms_per_step": S["ms"] / K,
+            "pair_interactions_per_s": S["pairs"] * 2 * K / (S["ms"] * 1e-3),
             "pairs_per_pass": S["pairs"]}
         line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
     if rank == 0 and not args.no_cpu_baseline:

@@ -237,7 +237,8 @@ typedef struct sphb_wc_params {
   int32_t periodic;
   int32_t uniform_vol;   /* 1: vol_const used instead of X[.][dim]          */
   int32_t width;         /* ELL width                                       */
-  int64_t n;             /* particles (all interior; ghosts out of scope)   */
+  int64_t n;             /* particles in the arrays (owned + halo)          */
+  int64_t row0, nrows;   /* rows updated: [row0, row0 + nrows) (slab ranks)  */
   double box[3];
   double h, alpha, kappa; /* Wendland family only (code 0)                  */
   double c_art, rho0, mu, cfl;

@@ -62,6 +62,8 @@ class WCParams(C.Structure):
         ("uniform_vol", C.c_int32),
         ("width", C.c_int32),
         ("n", C.c_int64),
+        ("row0", C.c_int64),
+        ("nrows", C.c_int64),
         ("box", C.c_double * 3),
         ("h", C.c_double),
         ("alpha", C.c_double),

@@ -45,8 +45,8 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
            double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
   const int gl = threadIdx.x % G;
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const bool active = i < n;
+  const int64_t i = P.row0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool active = i < P.row0 + P.nrows;
   const double c = P.c_art;
   double dr = 0.0;
   double dm[D];
@@ -199,10 +199,11 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
 
 template <int D>
 __global__ void __launch_bounds__(256)
-k_speed_max(int64_t n, double c, const double4* __restrict__ S, double* __restrict__ scalars) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+k_speed_max(int64_t row0, int64_t nrows, double c, const double4* __restrict__ S,
+            double* __restrict__ scalars) {
+  int64_t i = row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sp = 0.0;
-  if (i < n) {
+  if (i < row0 + nrows) {
     double v[D], rho;
     unpack_s<D>(S[i], v, rho);
     sp = __dadd_rn(c, norm_exact<D>(v));
@@ -285,8 +286,10 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
                              const int32_t* cnt, const double* s_in, const double* s_n,
                              const double* m_n, double* s_out, double* m_out, double* scalars,
                              int32_t* err, void* stream) {
-  if (!p || p->n < 0 || stage < 0 || stage > 2) return SPHB_ERR_ARG;
-  if (p->n == 0) return SPHB_OK;
+  if (!p || p->n < 0 || stage < 0 || stage > 2 || p->row0 < 0 || p->nrows < 0 ||
+      p->row0 + p->nrows > p->n)
+    return SPHB_ERR_ARG;
+  if (p->nrows == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const double4* X = (const double4*)x;
   const double4* Sin = (const double4*)s_in;
@@ -295,7 +298,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
 #define SPHB_STAGE(D, G, MB)                                                               \
-  k_wc_stage<D, G, MB><<<sphb_blocks(p->n * G, kThreads), kThreads, 0, st>>>(              \
+  k_wc_stage<D, G, MB><<<sphb_blocks(p->nrows * G, kThreads), kThreads, 0, st>>>(              \
       *p, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                   \
   break
   // SPHB_WC_MINB (tuning): 4 -> <=128 registers, 6 -> <=80, 8 -> <=64
@@ -336,11 +339,12 @@ extern "C" int sphb_wc_speed_max(const sphb_wc_params* p, const double* s, doubl
   SPHB_CUDA_CHECK(cudaMemsetAsync(scalars + 2, 0, sizeof(double), st));
   if (p->n == 0) return SPHB_OK;
   const double4* S = (const double4*)s;
-  const unsigned grid = sphb_blocks(p->n, 256);
+  if (p->nrows <= 0) return SPHB_OK;
+  const unsigned grid = sphb_blocks(p->nrows, 256);
   switch (p->dim) {
-    case 1: k_speed_max<1><<<grid, 256, 0, st>>>(p->n, p->c_art, S, scalars); break;
-    case 2: k_speed_max<2><<<grid, 256, 0, st>>>(p->n, p->c_art, S, scalars); break;
-    case 3: k_speed_max<3><<<grid, 256, 0, st>>>(p->n, p->c_art, S, scalars); break;
+    case 1: k_speed_max<1><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
+    case 2: k_speed_max<2><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
+    case 3: k_speed_max<3><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
     default: return SPHB_ERR_ARG;
   }
   SPHB_LAUNCH_CHECK();

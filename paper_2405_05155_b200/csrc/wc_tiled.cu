@@ -74,7 +74,7 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
   const int p = threadIdx.x / G;
   const int gl = threadIdx.x % G;
   const int64_t i = tile * PT + p;
-  const bool active = i < n;
+  const bool active = i >= P.row0 && i < P.row0 + P.nrows;
   const int li = self + p;
   const double c = P.c_art;
   const double c2 = c * c;

@@ -176,7 +176,8 @@ class EulerianSolver:
 
     def __init__(self, positions, n_interior, state: FluidState, eos: EosParams,
                  kernel: KernelSpec, ghosts=None, *, correction: bool = True, cfl: float = 0.5,
-                 mu: float = 0.0, periodic_box=None, wall_force_tag=None):
+                 mu: float = 0.0, periodic_box=None, wall_force_tag=None, _slab=None,
+                 _grid=None, _dist=None):
         if mu < 0.0:
             raise ConfigError("viscosity must be non-negative")
         if ghosts is not None:
@@ -208,8 +209,12 @@ class EulerianSolver:
         dev = _lib.device()
         self._dev = dev
         cutoff = kernel.kappa * kernel.h                       # eulerian.py:492
-        self.grid = make_grid(self.pos, cutoff, periodic_box)
+        # slab ranks (slab.py) bin their owned+halo set with the GLOBAL grid
+        self._slab, self._dist = _slab, _dist
+        self.grid = _grid if _grid is not None else make_grid(self.pos, cutoff, periodic_box)
         self.bins = bin_particles(_lib.to_device(self.pos, torch.float64), self.grid)
+        if _slab is not None:
+            _slab.attach(self.bins.perm.cpu().numpy())
         self.nbr, self.cnt, self.width = ell_from_bins(self.bins, kernel.h, kernel.kappa)
         self.perm = self.bins.perm.long()
         self.rank = self.bins.rank()
@@ -246,6 +251,8 @@ class EulerianSolver:
                 plane0[:, col] = bs[:, a, c]
             else:
                 plane1[:, col - 4] = bs[:, a, c]
+        if _slab is not None:       # halo rows take B from their owners
+            _slab.exchange(_dist, [plane0, plane1])
 
         ws = self.bins.ws
         self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
@@ -269,6 +276,8 @@ class EulerianSolver:
         p = self.params
         p.dim, p.periodic, p.uniform_vol, p.width, p.n = (self.dim, self.grid.periodic,
                                                           int(uniform), self.width, self.n)
+        p.row0, p.nrows = ((_slab.rows.start, _slab.rows.stop - _slab.rows.start)
+                           if _slab is not None else (0, self.n))
         for a in range(3):
             p.box[a] = self.grid.box[a]
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
@@ -330,6 +339,15 @@ class EulerianSolver:
     def _refresh_speed(self):
         _lib.call("sphb_wc_speed_max", ctypes.byref(self.params), self.S.data_ptr(),
                   self.scalars.data_ptr(), _lib.stream_ptr())
+        self._reduce_speed()
+
+    def _reduce_speed(self):
+        if self._slab is not None and self._slab.world > 1:
+            self._dist.all_reduce(self.scalars[2:3], op=self._dist.ReduceOp.MAX)
+
+    def _halo(self, buf):
+        if self._slab is not None:
+            self._slab.exchange(self._dist, [buf])
 
     @property
     def state(self) -> FluidState:
@@ -394,6 +412,26 @@ class EulerianSolver:
                   None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                   self.err.data_ptr(), _lib.stream_ptr())
 
+    def _global_err(self) -> int:
+        if self._slab is not None and self._slab.world > 1:
+            e = self.err.clone()
+            self._dist.all_reduce(e, op=self._dist.ReduceOp.MAX)
+            return int(e.item())
+        return int(self.err.item())
+
+    def owned(self):
+        """(global ids, rho, mom) of the rows this solver updates (slab ranks)."""
+        torch = _lib.torch_cuda()
+        rows = self._slab.rows if self._slab is not None else slice(0, self.n)
+        perm = self.perm[rows]
+        rho = self.S[rows, self.dim].cpu().numpy()
+        mom = self.M[rows, :self.dim].cpu().numpy()
+        ids = perm.cpu().numpy()
+        if self._slab is not None:
+            ids = self._slab.local_ids[ids]
+        del torch
+        return ids, rho, mom
+
     def _check(self, what):
         err = int(self.err.item())
         if err:
@@ -423,7 +461,10 @@ class EulerianSolver:
         _lib.call("sphb_set_dt", self._cfl_h, 0.0, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), _lib.stream_ptr())
         self._launch_stage(1, self.S, self.S, self.M, self.S1, None)
+        self._halo(self.S1)
         self._launch_stage(2, self.S1, self.S, self.M, self.S_nx, self.M_nx)
+        self._halo(self.S_nx)
+        self._reduce_speed()
 
     def _swap(self):
         self.S, self.S_nx = self.S_nx, self.S
@@ -442,7 +483,7 @@ class EulerianSolver:
         while advanced < dt - 1e-15 * dt:
             sub = min(remaining, dt - advanced)
             self._substeps(sub)
-            err = int(self.err.item())
+            err = self._global_err()
             if err:
                 self.err.zero_()
                 self._refresh_speed()   # the rejected stage 2 polluted the max
@@ -478,7 +519,7 @@ class EulerianSolver:
         for _ in range(n_steps):
             self._substeps(0.0 if dt is None else float(dt))
             self._swap()
-        err = int(self.err.item())
+        err = self._global_err()
         if err:
             self.err.zero_()
             self.S.copy_(s0)

@@ -187,7 +187,7 @@ def e2e_leg(torch, solver, steps, warmup):
 
     def one():
         solver.load_state(rho_h, mom_h)
-        solver.advance(1)
+        solver.step()                 # the reference API call (eulerian.py:562)
         solver.read_state(rho_h, mom_h)
 
     for _ in range(warmup):
@@ -324,7 +324,7 @@ def main():
         "e2e": {"value": n / (e2e_ms * 1e-3), "unit": "particle-steps/s",
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
                 "ms_per_step": e2e_ms,
-                "path": "EulerianSolver.load_state(pinned) -> advance(1) -> read_state(pinned)"},
+                "path": "EulerianSolver.load_state(pinned) -> step() -> read_state(pinned)"},
     }
     if "2h" in leg:
         S = leg["2h"]

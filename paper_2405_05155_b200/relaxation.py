@@ -146,6 +146,29 @@ class PeriodicRelaxer:
     def positions(self) -> np.ndarray:
         return self.pos[:self.n].cpu().numpy()
 
+    def run(self, n_updates: int, *, graph: bool = True) -> None:
+        """n_updates x (bin + fused acceleration + capped update), no host
+        synchronisation; one update is captured as a CUDA graph (sort and
+        memsets included) and replayed."""
+        if n_updates <= 0:
+            return
+        if not graph:
+            for _ in range(n_updates):
+                self.accelerate()
+                self.update()
+            return
+        torch = _lib.torch_cuda()
+        if getattr(self, "_graph", None) is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.accelerate()
+                self.update()
+            torch.cuda.synchronize()
+            self._graph = g
+        for _ in range(n_updates):
+            self._graph.replay()
+
 
 def relax_steps(positions, spec: KernelSpec, box, dp: float, n_updates: int, *, p0=1.0,
                 rho0=1.0, step_scale=0.2, record_residuals=True):

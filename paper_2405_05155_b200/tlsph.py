@@ -326,22 +326,46 @@ class SolidSystem:
         self.steps += 1
         return dt
 
-    def advance(self, n_steps: int, dt: float | None = None) -> None:
-        """n_steps steps without host synchronisation; error word checked once."""
+    def advance(self, n_steps: int, dt: float | None = None, *, graph: bool | None = None) -> None:
+        """n_steps steps without host synchronisation; the error word is read
+        once at the end (SolidStateError).  With `graph` (default when
+        n_steps >= 8) one step is captured as a CUDA graph and replayed."""
         if n_steps <= 0:
             return
         self._sync_in()
         if not self._acc_valid:
             self._accelerations_dev()
+        dto = 0.0 if dt is None else float(dt)
         if dt is None:
             self._speed_max()
         self.scalars[1] = 0.0
-        for _ in range(n_steps):
-            self._one_step(0.0 if dt is None else float(dt))
+        if graph is None:
+            graph = n_steps >= 8
+        if graph:
+            g = self._step_graph(dto)
+            for _ in range(n_steps):
+                g.replay()
+        else:
+            for _ in range(n_steps):
+                self._one_step(dto)
         self._host.clear()
         self._raise_if_bad()
         self.t += float(self.scalars[1].item())
         self.steps += n_steps
+
+    def _step_graph(self, dt_override: float):
+        torch = _lib.torch_cuda()
+        if getattr(self, "_graphs", None) is None:
+            self._graphs = {}
+        g = self._graphs.get(dt_override)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._one_step(dt_override)
+            torch.cuda.synchronize()
+            self._graphs[dt_override] = g
+        return g
 
     # -- diagnostics ------------------------------------------------------------
     def energies(self):

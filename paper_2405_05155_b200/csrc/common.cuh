@@ -130,6 +130,18 @@ __device__ __forceinline__ void for_each_neighbor(const sphb_grid& g, int64_t n,
   }
 }
 
+// 256-bit read-only gather (sm_100: LDG.E.ENL2.256).  A plain double4 load
+// compiles to two LDG.128; one request per 32-byte record halves the L1
+// requests of the neighbour gathers.  Only for data not written by the
+// running kernel.
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
+
 // ----------------------------------------------------------- reductions
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their int64 bit patterns

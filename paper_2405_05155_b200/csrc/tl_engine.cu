@@ -75,10 +75,37 @@ __device__ __forceinline__ void store_vec(double4* __restrict__ V, int64_t i, co
   V[i] = make_double4(c[0], c[1], c[2], c[3]);
 }
 
+// neighbour gathers of data the kernel does not write: 256-bit .nc loads
+template <int D>
+__device__ __forceinline__ void load_vec_nc(const double4* __restrict__ V, int64_t i,
+                                            double (&v)[D]) {
+  const double4 t = ldg4(V + i);
+  const double c[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = c[a];
+}
+
+template <int D>
+__device__ __forceinline__ void load_mat_nc(const double4* __restrict__ M, int64_t i,
+                                            double (&a)[D][D]) {
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double4 t = ldg4(M + 3 * i + r);
+      a[r][0] = t.x; a[r][1] = t.y; a[r][2] = t.z;
+    }
+  } else if constexpr (D == 2) {
+    const double4 t = ldg4(M + i);
+    a[0][0] = t.x; a[0][1] = t.y; a[1][0] = t.z; a[1][1] = t.w;
+  } else {
+    a[0][0] = ldg4(M + i).x;
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void load_x0(const double4* __restrict__ X0, int64_t i, double (&w)[D],
                                         bool& fixed) {
-  double4 t = X0[i];
+  const double4 t = ldg4(X0 + i);
   const double c[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
   for (int a = 0; a < D; ++a) w[a] = c[a];
@@ -192,8 +219,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
     double wj[D], vj[D], aj[D];
     bool fixed_j;
     load_x0<D>(X0, j, wj, fixed_j);
-    load_vec<D>(V, j, vj);
-    load_vec<D>(A, j, aj);
+    load_vec_nc<D>(V, j, vj);
+    load_vec_nc<D>(A, j, aj);
     double dx[D], g[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
@@ -262,7 +289,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
       bool fixed_j;
       load_x0<D>(X0, j, wj, fixed_j);
       double Qj[D][D];
-      load_mat<D>(Q, j, Qj);
+      load_mat_nc<D>(Q, j, Qj);
       double dx[D], g[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];

@@ -16,7 +16,7 @@ template <>
 struct Sym<1> {
   double a00;
   __device__ __forceinline__ void load(const double* B, int64_t, int64_t i) {
-    a00 = reinterpret_cast<const double4*>(B)[i].x;
+    a00 = ldg4(reinterpret_cast<const double4*>(B) + i).x;
   }
   __device__ __forceinline__ void add(const Sym& o, Sym& r) const { r.a00 = a00 + o.a00; }
   __device__ __forceinline__ void mv(const double (&e)[1], double (&out)[1]) const {
@@ -27,7 +27,7 @@ template <>
 struct Sym<2> {
   double a00, a01, a11;
   __device__ __forceinline__ void load(const double* B, int64_t, int64_t i) {
-    const double4 t = reinterpret_cast<const double4*>(B)[i];
+    const double4 t = ldg4(reinterpret_cast<const double4*>(B) + i);
     a00 = t.x; a01 = t.y; a11 = t.z;
   }
   __device__ __forceinline__ void add(const Sym& o, Sym& r) const {
@@ -42,7 +42,7 @@ template <>
 struct Sym<3> {
   double a00, a01, a02, a11, a12, a22;
   __device__ __forceinline__ void load(const double* B, int64_t n, int64_t i) {
-    const double4 t = reinterpret_cast<const double4*>(B)[i];
+    const double4 t = ldg4(reinterpret_cast<const double4*>(B) + i);
     const double2 u = reinterpret_cast<const double2*>(B + 4 * n)[i];
     a00 = t.x; a01 = t.y; a02 = t.z; a11 = t.w; a12 = u.x; a22 = u.y;
   }

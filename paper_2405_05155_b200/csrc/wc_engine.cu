@@ -71,8 +71,8 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
     for (int32_t k = gl; k < m; k += G) {
       const int64_t j = row[(int64_t)k * n];
       double xj[D], vol_j, vj[D], rho_j;
-      unpack_x<D>(X[j], xj, vol_j);
-      unpack_s<D>(S_in[j], vj, rho_j);
+      unpack_x<D>(ldg4(X + j), xj, vol_j);
+      unpack_s<D>(ldg4(S_in + j), vj, rho_j);
       Sym<D> Bj;
       Bj.load(B, n, j);
       if (P.uniform_vol) vol_j = P.vol_const;

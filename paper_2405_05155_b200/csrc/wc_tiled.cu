@@ -11,12 +11,29 @@
 // each particle (each walks every G-th entry of the row; partial sums are
 // combined with warp shuffles) reading neighbour data from shared memory
 // through the uint16 local neighbour table.  Uniform particle volumes.
+#include <cuda_pipeline.h>
+
 #include "wc_common.cuh"
 
 using namespace sphb;
 using namespace sphb::wc;
 
 namespace {
+
+// Shared-memory record of one staged particle, 16-byte chunks:
+//   X  {x0, x1, x2, vol}            chunks 0-1
+//   B0 {b00, b01, b02, b11}         chunks 2-3
+//   B1 {b12, b22}                   chunk 4     (3D only)
+//   S  {v0, v1, v2, rho}            chunks 5-6  (2D/1D: 4-5)
+// A 112-byte stride (7 chunks) puts consecutive records on 8 distinct
+// 4-bank groups, so random per-lane 16-byte reads spread over all banks.
+template <int D>
+struct Rec {
+  static constexpr int kChunks = D == 3 ? 7 : 6;
+  static constexpr int kDoubles = 2 * kChunks;
+  static constexpr int kX = 0, kB0 = 4, kB1 = 8;
+  static constexpr int kS = D == 3 ? 10 : 8;
+};
 
 template <int D, int G>
 __global__ void __launch_bounds__(256, 2)
@@ -27,13 +44,10 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
                  const double4* __restrict__ S_in, const double4* Sn, const double4* Mn,
                  double4* S_out, double4* M_out, double* __restrict__ scalars,
                  int32_t* __restrict__ err) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
+  using RC = Rec<D>;
   constexpr int NB = NSym<D>::value;
   constexpr int PT = 256 / G;  // particles per tile
-  double* sx = smem;
-  double* sb = sx + D * umax;
-  double* sv = sb + NB * umax;
-  double* srho = sv + D * umax;
   const int64_t n = P.n;
   const int64_t tile = blockIdx.x;
   const int32_t* M4 = meta + tile * 4;
@@ -41,34 +55,29 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
   const int self = M4[2];
   const int32_t* R = runs + tile * (int64_t)rmax * 3;
 
-  // ---- stage the neighbour union (coalesced runs) into shared memory
+  // ---- stage the union: cp.async (LDGSTS) 16-byte chunks, field-major per
+  // run so consecutive threads copy consecutive chunks of one array
   for (int r = 0; r < nrun; ++r) {
     const int32_t start = R[r * 3], len = R[r * 3 + 1], lbase = R[r * 3 + 2];
-    for (int q = threadIdx.x; q < len; q += blockDim.x) {
-      const int64_t gi = start + q;
-      const int l = lbase + q;
-      const double4 xr = X[gi];
-      const double xc[4] = {xr.x, xr.y, xr.z, xr.w};
+    const char* srcs[4] = {reinterpret_cast<const char*>(X + start),
+                           reinterpret_cast<const char*>(B) + (size_t)start * 32,
+                           reinterpret_cast<const char*>(B + 4 * n) + (size_t)start * 16,
+                           reinterpret_cast<const char*>(S_in + start)};
+    const int nch[4] = {2, 2, D == 3 ? 1 : 0, 2};
+    const int off[4] = {RC::kX, RC::kB0, RC::kB1, RC::kS};
 #pragma unroll
-      for (int a = 0; a < D; ++a) sx[a * umax + l] = xc[a];
-      const double4 b0 = reinterpret_cast<const double4*>(B)[gi];
-      if constexpr (NB > 4) {
-        const double2 b1 = reinterpret_cast<const double2*>(B + 4 * n)[gi];
-        const double bc[6] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y};
-#pragma unroll
-        for (int a = 0; a < NB; ++a) sb[a * umax + l] = bc[a];
-      } else {
-        const double bc[4] = {b0.x, b0.y, b0.z, b0.w};
-#pragma unroll
-        for (int a = 0; a < NB; ++a) sb[a * umax + l] = bc[a];
+    for (int f = 0; f < 4; ++f) {
+      if (nch[f] == 0) continue;
+      const int total = len * nch[f];
+      for (int c = threadIdx.x; c < total; c += blockDim.x) {
+        const int rec = c / nch[f], ch = c - rec * nch[f];
+        double* dst = smem + (size_t)(lbase + rec) * RC::kDoubles + off[f] + 2 * ch;
+        __pipeline_memcpy_async(dst, srcs[f] + (size_t)c * 16, 16);
       }
-      const double4 sr = S_in[gi];
-      const double scv[4] = {sr.x, sr.y, sr.z, sr.w};
-#pragma unroll
-      for (int a = 0; a < D; ++a) sv[a * umax + l] = scv[a];
-      srho[l] = scv[D];
     }
   }
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
   __syncthreads();
 
   const int p = threadIdx.x / G;
@@ -90,24 +99,36 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
   for (int a = 0; a < D; ++a) dm[a] = 0.0;
   if (active) {
     double xi[D], vi[D], bi[NB];
+    const double* ri = smem + (size_t)li * RC::kDoubles;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      xi[a] = sx[a * umax + li];
-      vi[a] = sv[a * umax + li];
+      xi[a] = ri[RC::kX + a];
+      vi[a] = ri[RC::kS + a];
     }
 #pragma unroll
-    for (int a = 0; a < NB; ++a) bi[a] = sb[a * umax + li];
-    const double rho_i = srho[li];
+    for (int a = 0; a < NB; ++a) bi[a] = ri[RC::kB0 + a];
+    const double rho_i = ri[RC::kS + D];
     const double p_i = c2 * (rho_i - P.rho0);
     const int32_t m = cnt[i];
     for (int32_t k = gl; k < m; k += G) {
       const int lj = lnbr[(int64_t)k * n + i];
+      const double* rj = smem + (size_t)lj * RC::kDoubles;
+      const double2 xj01 = *reinterpret_cast<const double2*>(rj + RC::kX);
+      const double2 xj23 = *reinterpret_cast<const double2*>(rj + RC::kX + 2);
+      const double2 bj01 = *reinterpret_cast<const double2*>(rj + RC::kB0);
+      const double2 bj23 = *reinterpret_cast<const double2*>(rj + RC::kB0 + 2);
+      const double2 bj45 = *reinterpret_cast<const double2*>(rj + RC::kB1);
+      const double2 sj01 = *reinterpret_cast<const double2*>(rj + RC::kS);
+      const double2 sj23 = *reinterpret_cast<const double2*>(rj + RC::kS + 2);
+      const double xjc[4] = {xj01.x, xj01.y, xj23.x, xj23.y};
+      const double bjc[6] = {bj01.x, bj01.y, bj23.x, bj23.y, bj45.x, bj45.y};
+      const double sjc[4] = {sj01.x, sj01.y, sj23.x, sj23.y};
       // geometry (neighbors.py:152-165, correction.py:102-108)
       double dx[D];
       double r2 = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        double d = xi[a] - sx[a * umax + lj];
+        double d = xi[a] - xjc[a];
         if (P.periodic) {
           const double bx = P.box[a];
           if (d > 0.5 * bx) d -= bx;
@@ -126,7 +147,7 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
       for (int a = 0; a < D; ++a) e[a] = dx[a] * inv_r;
       double bs[NB];
 #pragma unroll
-      for (int a = 0; a < NB; ++a) bs[a] = bi[a] + sb[a * umax + lj];
+      for (int a = 0; a < NB; ++a) bs[a] = bi[a] + bjc[a];
       double g[D];
       if constexpr (D == 3) {
         g[0] = fma(bs[0], e[0], fma(bs[1], e[1], bs[2] * e[2]));
@@ -146,8 +167,8 @@ k_wc_stage_tiled(const sphb_wc_params P, const int stage, const double4* __restr
       // limited linearised Riemann problem (eulerian.py:145-157, 236-264)
       double vj[D];
 #pragma unroll
-      for (int a = 0; a < D; ++a) vj[a] = sv[a * umax + lj];
-      const double rho_j = srho[lj];
+      for (int a = 0; a < D; ++a) vj[a] = sjc[a];
+      const double rho_j = sjc[D];
       double ul = 0.0, ur = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -242,8 +263,7 @@ int launch_tiled(const sphb_wc_params* p, int32_t stage, const double* x, const 
                  const int32_t* meta, int32_t rmax, int32_t umax, const double* s_in,
                  const double* s_n, const double* m_n, double* s_out, double* m_out,
                  double* scalars, int32_t* err, cudaStream_t st) {
-  constexpr int NF = D + NSym<D>::value + D + 1;
-  const size_t smem = sizeof(double) * (size_t)NF * (size_t)umax;
+  const size_t smem = sizeof(double) * (size_t)Rec<D>::kDoubles * (size_t)umax;
   auto kern = k_wc_stage_tiled<D, G>;
   static size_t configured = 0;
   if (smem > configured) {

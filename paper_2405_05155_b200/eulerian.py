@@ -266,9 +266,8 @@ class EulerianSolver:
         self.plan = None
         if (os.environ.get("SPHB_WC_KERNEL", "global") == "tiled" and uniform and self.n
                 and self.width):
-            nsym = {1: 1, 2: 3, 3: 6}[self.dim]
             plan = TilePlan(self.bins, self.nbr, self.cnt, self.width,
-                            fields=2 * self.dim + nsym + 1)
+                            fields=14 if self.dim == 3 else 12)
             if plan.ok:
                 self.plan = plan
 

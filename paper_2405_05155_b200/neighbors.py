@@ -314,9 +314,13 @@ class TilePlan:
         torch = _lib.torch_cuda()
         n = bins.n
         dev = bins.perm.device
+        import os
+
         self.group = 1
         while self.group < 8 and self.group * 8 < width:
             self.group *= 2
+        if os.environ.get("SPHB_TILE_GROUP"):      # tuning override
+            self.group = int(os.environ["SPHB_TILE_GROUP"])
         self.tile = 256 // self.group
         self.ok = False
         self.umax = 0

@@ -39,7 +39,8 @@ def one(n_side, kernel, steps):
     ms = [a.elapsed_time(b) for _, a, b in s.timer]
     rho = s.state.rho
     print(json.dumps({"stage_ms": sum(ms) / len(ms), "pairs": int(s.cnt.sum().item()),
-                      "group": s.group, "plan": s.plan is not None, "rho_sum": float(rho.sum())}))
+                      "group": s.group, "plan": s.plan is not None,
+                      "umax": s.plan.umax if s.plan else None, "rho_sum": float(rho.sum())}))
 
 
 def main():
@@ -52,10 +53,11 @@ def main():
     if args.one:
         one(args.n_side, args.kernel, args.steps)
         return
-    variants = [("global", g, mb) for g, mb in itertools.product((1, 2, 4, 8), (4, 6, 8))]
-    variants.append(("tiled", 4 if args.kernel == "1.6h" else 8, 4))
+    variants = [("global", g, 4) for g in (1, 2)]
+    variants += [("tiled", g, 4) for g in (2, 4, 8)]
     for kern, g, mb in variants:
-        env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb))
+        env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb),
+                   SPHB_TILE_GROUP=str(g))
         out = subprocess.run([sys.executable, __file__, "--one", "--n-side", str(args.n_side),
                               "--kernel", args.kernel, "--steps", str(args.steps)], env=env,
                              capture_output=True, text=True)

@@ -169,8 +169,8 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     for stage, a, b in solver.timer:
         st[stage].append(a.elapsed_time(b))
     solver.timer = None
-    kernel = (("k_wc_stage_tiled<3,%d>" % solver.plan.group) if solver.plan
-              else "k_wc_stage<3,%d>" % solver.group)
+    kernel = {"geo": "k_wc_stage_geo<3>", "tiled": "k_wc_stage_tiled<3,%d>" % solver.group,
+              "global": "k_wc_stage<3,%d,4>" % solver.group}[solver.variant]
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None}
 

@@ -266,6 +266,21 @@ int sphb_wc_stage_tiled(const sphb_wc_params* p, int32_t stage, int32_t group,
                         const double* M_n, double* S_out, double* M_out, double* scalars,
                         int32_t* err, void* stream);
 
+/* Static per-pair geometry of the WC flux (eulerian.py:506-513): for every
+ * ELL slot, e_ij, gwv_ij = dW 0.5 (B_i + B_j) e_ij V_j and viscv_ij =
+ * 2 dW / r V_j as planes geo[(c * width + k) * n + s], c = 0..2D (B: full
+ * sorted (n, d, d) matrices; vol: sorted).  Reference arithmetic, no FMA. */
+int sphb_wc_geometry(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                     const int32_t* nbr, const int32_t* cnt, int32_t width,
+                     const double* B_full, const double* vol_sorted, const sphb_kernel* k,
+                     double* geo, void* stream);
+/* Stage kernel streaming that geometry and gathering only S_j (same
+ * contract as sphb_wc_stage; p->width = ELL width). */
+int sphb_wc_stage_geo(const sphb_wc_params* p, int32_t stage, const int32_t* nbr,
+                      const int32_t* cnt, const double* geo, const double* S_in,
+                      const double* S_n, const double* M_n, double* S_out, double* M_out,
+                      double* scalars, int32_t* err, void* stream);
+
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,
                       void* stream);

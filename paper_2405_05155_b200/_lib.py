@@ -125,6 +125,8 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_wc_geometry": (C.c_int, [P, I64, P, P, P, I32, P, P, P, P, P]),
+    "sphb_wc_stage_geo": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_pack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
     "sphb_wc_unpack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
     "sphb_fp64_probe": (C.c_int, [P, I32, I32, I32, P]),

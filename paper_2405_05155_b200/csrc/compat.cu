@@ -398,6 +398,55 @@ __global__ void k_ell_moments(sphb_grid g, int64_t n, const double* __restrict__
     for (int b = 0; b < D; ++b) m[(s * D + a) * D + b] = mm[a][b];
 }
 
+// Per-pair geometry of the WC flux, exactly as the reference precomputes it
+// in EulerianSolver.__init__ (eulerian.py:506-513 via _pair_gradients,
+// correction.py:89-112): e_ij, gwv_ij = dW 0.5 (B_i + B_j) e_ij V_j and
+// viscv_ij = 2 dW / r V_j, for every slot of the ELL pass list, stored as
+// planes geo[(c * width + k) * n + s] (c < D: e, D..2D-1: gwv, 2D: viscv) so
+// the stage kernel streams them coalesced.  B is the full (unsymmetrised)
+// sorted correction matrix; no FMA contraction (this translation unit).
+template <int D>
+__global__ void k_wc_geometry(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+                              int32_t width, const double* __restrict__ b,
+                              const double* __restrict__ vol, sphb_kernel k,
+                              double* __restrict__ geo) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double scale = k.alpha / k.h;
+  double wi[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) wi[a] = ws[(int64_t)a * n + s];
+  const int32_t m = cnt[s];
+  for (int32_t kk = 0; kk < m; ++kk) {
+    const int64_t t = nbr[(int64_t)kk * n + s];
+    double dx[D];
+    double r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      dx[a] = min_image(wi[a] - ws[(int64_t)a * n + t], g.box[a], g.periodic);
+      r2 += dx[a] * dx[a];
+    }
+    const double r = sqrt(r2);
+    double e[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) e[a] = dx[a] / r;
+    const double q = r / k.h;
+    const double dw = scale * profile_deriv(k.code, q);
+    const double vj = vol[t];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        acc += 0.5 * (b[(s * D + a) * D + c] + b[(t * D + a) * D + c]) * e[c];
+      geo[((int64_t)a * width + kk) * n + s] = e[a];
+      geo[((int64_t)(D + a) * width + kk) * n + s] = dw * acc * vj;
+    }
+    geo[((int64_t)(2 * D) * width + kk) * n + s] = 2.0 * dw / r * vj;
+  }
+}
+
 }  // namespace
 
 #define SPHB_DISPATCH_D(dim, KERNEL, GRID, ...)                                   \
@@ -522,6 +571,20 @@ extern "C" int sphb_ell_moments(const sphb_grid* g, int64_t n, const double* ws,
   cudaStream_t st = (cudaStream_t)stream;
   const int T = 128;
   SPHB_DISPATCH_D(g->dim, k_ell_moments, sphb_blocks(n, T), *g, n, ws, nbr, cnt, vols, *k, m);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_wc_geometry(const sphb_grid* g, int64_t n, const double* ws,
+                                const int32_t* nbr, const int32_t* cnt, int32_t width,
+                                const double* b, const double* vol, const sphb_kernel* k,
+                                double* geo, void* stream) {
+  if (!g || !k || n < 0 || width < 0) return SPHB_ERR_ARG;
+  if (n == 0 || width == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = 128;
+  SPHB_DISPATCH_D(g->dim, k_wc_geometry, sphb_blocks(n, T), *g, n, ws, nbr, cnt, width, b, vol,
+                  *k, geo);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

@@ -239,6 +239,9 @@ class EulerianSolver:
         else:
             b = torch.eye(self.dim, dtype=torch.float64, device=dev).expand(self.n, -1, -1)
             self.n_regularized = 0
+        b = b.contiguous()
+        if _slab is not None:       # halo rows take B from their owners
+            _slab.exchange(_dist, [b])
         self._B_sorted = b
         bs = 0.5 * (b + b.transpose(1, 2))
         # two planes: [n][4] {b00, b01, b02, b11} then [n][2] {b12, b22}
@@ -251,8 +254,6 @@ class EulerianSolver:
                 plane0[:, col] = bs[:, a, c]
             else:
                 plane1[:, col - 4] = bs[:, a, c]
-        if _slab is not None:       # halo rows take B from their owners
-            _slab.exchange(_dist, [plane0, plane1])
 
         ws = self.bins.ws
         self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
@@ -262,10 +263,27 @@ class EulerianSolver:
         self.group = 1 if self.width <= 40 else 2
         if os.environ.get("SPHB_WC_GROUP"):      # tuning override
             self.group = int(os.environ["SPHB_WC_GROUP"])
-        # optional shared-memory tiled variant (SPHB_WC_KERNEL=tiled)
+        # Stage-kernel variant (SPHB_WC_KERNEL=global|geo|tiled):
+        #   global (default) recompute the pair geometry from X_j, B_j
+        #          (wc_engine.cu) — fastest on B200 (profiles/r01_tune_wc.md);
+        #   geo    stream the static per-pair geometry (wc_stream.cu,
+        #          (2d+1) doubles per pair, reference arithmetic without FMA:
+        #          the closest reproduction of the reference's roundings);
+        #   tiled  shared-memory staging variant of `global`.
+        variant = os.environ.get("SPHB_WC_KERNEL", "global")
+        geo_bytes = (2 * self.dim + 1) * self.width * self.n * 8
+        self.variant = variant
+        self.geo = None
+        if variant == "geo" and self.n and self.width:
+            self.geo = torch.empty(geo_bytes // 8, dtype=torch.float64, device=dev)
+            k = _lib.kernel_struct(kernel)
+            _lib.call("sphb_wc_geometry", ctypes.byref(self.grid), self.n,
+                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), self.width, b.data_ptr(),
+                      vol_s.contiguous().data_ptr(), ctypes.byref(k), self.geo.data_ptr(),
+                      _lib.stream_ptr())
         self.plan = None
-        if (os.environ.get("SPHB_WC_KERNEL", "global") == "tiled" and uniform and self.n
-                and self.width):
+        if variant == "tiled" and uniform and self.n and self.width:
             plan = TilePlan(self.bins, self.nbr, self.cnt, self.width,
                             fields=14 if self.dim == 3 else 12)
             if plan.ok:
@@ -395,6 +413,13 @@ class EulerianSolver:
         self._launch_stage_raw(stage, s_in, s_n, m_n, s_out, m_out)
 
     def _launch_stage_raw(self, stage, s_in, s_n, m_n, s_out, m_out):
+        if self.geo is not None:
+            _lib.call("sphb_wc_stage_geo", ctypes.byref(self.params), stage, self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), self.geo.data_ptr(), s_in.data_ptr(), s_n.data_ptr(),
+                      m_n.data_ptr(), s_out.data_ptr(),
+                      None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                      self.err.data_ptr(), _lib.stream_ptr())
+            return
         if self.plan is not None:
             pl = self.plan
             _lib.call("sphb_wc_stage_tiled", ctypes.byref(self.params), stage, pl.group,

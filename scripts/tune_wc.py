@@ -39,7 +39,7 @@ def one(n_side, kernel, steps):
     ms = [a.elapsed_time(b) for _, a, b in s.timer]
     rho = s.state.rho
     print(json.dumps({"stage_ms": sum(ms) / len(ms), "pairs": int(s.cnt.sum().item()),
-                      "group": s.group, "plan": s.plan is not None,
+                      "group": s.group, "variant": s.variant,
                       "umax": s.plan.umax if s.plan else None, "rho_sum": float(rho.sum())}))
 
 
@@ -53,8 +53,7 @@ def main():
     if args.one:
         one(args.n_side, args.kernel, args.steps)
         return
-    variants = [("global", g, 4) for g in (1, 2)]
-    variants += [("tiled", g, 4) for g in (2, 4, 8)]
+    variants = [("geo", 1, 4), ("global", 1, 4), ("global", 2, 4), ("tiled", 8, 4)]
     for kern, g, mb in variants:
         env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb),
                    SPHB_TILE_GROUP=str(g))

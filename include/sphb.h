@@ -74,6 +74,14 @@ typedef struct sphb_grid {
   double lo[3];        /* open-domain shift pos.min(axis=0) (:384)          */
   double cutoff;
   double cut2;         /* cutoff * cutoff (neighbors.py:266 of _search)     */
+  /* Storage order: particles are sorted by a cell key whose slowest axis is
+   * `slow_axis` (strides `sstrides`); with slow_axis = dim-1 it is the
+   * reference flat key.  Only the storage order changes (slab layers along
+   * slow_axis become contiguous); cell tables stay indexed by the reference
+   * key and rows are enumerated in the reference order either way. */
+  int64_t sstrides[3];
+  int32_t slow_axis;
+  int32_t reserved;
 } sphb_grid;
 
 /* Kernel parameters (KernelSpec, kernels.py:62-80). */
@@ -317,6 +325,7 @@ typedef struct sphb_tl_params {
   int32_t dim;
   int32_t width;
   int64_t n;
+  int64_t row0, nrows;     /* rows updated (slab ranks); stress: all n */
   double h, alpha, kappa;  /* Wendland family */
   double vol0, rho0;
   double lam, g;           /* Lame parameters (tlsph.py:27-35) */

@@ -42,6 +42,9 @@ class Grid(C.Structure):
         ("lo", C.c_double * 3),
         ("cutoff", C.c_double),
         ("cut2", C.c_double),
+        ("sstrides", C.c_int64 * 3),
+        ("slow_axis", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -81,6 +84,8 @@ class TLParams(C.Structure):
         ("dim", C.c_int32),
         ("width", C.c_int32),
         ("n", C.c_int64),
+        ("row0", C.c_int64),
+        ("nrows", C.c_int64),
         ("h", C.c_double),
         ("alpha", C.c_double),
         ("kappa", C.c_double),

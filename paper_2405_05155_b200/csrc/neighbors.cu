@@ -27,7 +27,7 @@ __global__ void k_wrap_key(sphb_grid g, const double* __restrict__ pos, int64_t 
     double p = pos[i * D + a];
     double w = g.periodic ? np_remainder(p, g.box[a]) : __dsub_rn(p, g.lo[a]);
     wrapped_aos[i * D + a] = w;
-    flat += cell_coord(g, a, w) * g.strides[a];
+    flat += cell_coord(g, a, w) * g.sstrides[a];   // storage key
   }
   key[i] = (uint32_t)flat;
   val[i] = (int32_t)i;
@@ -43,17 +43,26 @@ __global__ void k_gather_sorted(int64_t n, const double* __restrict__ wrapped_ao
   for (int a = 0; a < D; ++a) ws[(int64_t)a * n + s] = wrapped_aos[i * D + a];
 }
 
-__global__ void k_cell_ranges(int64_t n, const uint32_t* __restrict__ key,
+// storage key -> reference flat key (identity when slow_axis == dim - 1)
+__device__ __forceinline__ int64_t ref_key(const sphb_grid& g, uint32_t skey) {
+  if (g.slow_axis == g.dim - 1) return skey;
+  int64_t ref = 0;
+  for (int a = 0; a < g.dim; ++a) ref += ((int64_t)skey / g.sstrides[a] % g.ncell[a]) * g.strides[a];
+  return ref;
+}
+
+__global__ void k_cell_ranges(sphb_grid g, int64_t n, const uint32_t* __restrict__ key,
                               int32_t* __restrict__ cs, int32_t* __restrict__ ce) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t k = key[s];
-  if (s == 0 || key[s - 1] != k) cs[k] = (int32_t)s;
-  if (s == n - 1 || key[s + 1] != k) ce[k] = (int32_t)(s + 1);
+  if (s == 0 || key[s - 1] != k) cs[ref_key(g, k)] = (int32_t)s;
+  if (s == n - 1 || key[s + 1] != k) ce[ref_key(g, k)] = (int32_t)(s + 1);
 }
 
 static bool grid_ok(const sphb_grid* g) {
   if (!g || g->dim < 1 || g->dim > 3) return false;
+  if (g->slow_axis < 0 || g->slow_axis >= g->dim) return false;
   if (g->ntot < 1 || g->ntot > 0x7fffffffLL) return false;
   return true;
 }
@@ -114,7 +123,7 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
   size_t cub_bytes = workspace_bytes - L.cub;
   SPHB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(w + L.cub, cub_bytes, keys_in, keys_out, vals_in,
                                                   perm, (int)n, 0, end_bit_for(g->ntot), st));
-  k_cell_ranges<<<sphb_blocks(n, T), T, 0, st>>>(n, keys_out, cs, ce);
+  k_cell_ranges<<<sphb_blocks(n, T), T, 0, st>>>(*g, n, keys_out, cs, ce);
   SPHB_LAUNCH_CHECK();
   switch (g->dim) {
     case 1: k_gather_sorted<1><<<sphb_blocks(n, T), T, 0, st>>>(n, wrapped, perm, ws); break;

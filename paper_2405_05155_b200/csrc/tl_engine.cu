@@ -191,8 +191,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
             double4* __restrict__ XC, double4* __restrict__ F, double4* __restrict__ Q,
             const double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.row0 + P.nrows) return;
   const double dt = scalars[0];
   const double hdt = 0.5 * dt;
   const double inv_h = 1.0 / P.h;
@@ -268,9 +268,9 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             double4* __restrict__ A, double4* __restrict__ V, double* __restrict__ scalars,
             int update_v) {
   const int64_t n = P.n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double speed = 0.0;
-  if (i < n) {
+  if (i < P.row0 + P.nrows) {
     const double inv_h = 1.0 / P.h;
     const double scale_v0 = P.alpha / P.h * P.vol0;
     double wi[D];
@@ -351,10 +351,11 @@ __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ 
 }
 
 template <int D>
-__global__ void k_tl_speed(int64_t n, const double4* __restrict__ V, double* __restrict__ scalars) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restrict__ V,
+                           double* __restrict__ scalars) {
+  const int64_t i = row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double speed = 0.0;
-  if (i < n) {
+  if (i < row0 + nrows) {
     double v[D];
     load_vec<D>(V, i, v);
     double s2 = __dmul_rn(v[0], v[0]);
@@ -392,7 +393,8 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TL_DISPATCH(k_tl_pass_a, sphb_blocks(p->n, kThreads), kThreads, *p, (const double4*)x0,
+  if (p->nrows <= 0) return SPHB_OK;
+  TL_DISPATCH(k_tl_pass_a, sphb_blocks(p->nrows, kThreads), kThreads, *p, (const double4*)x0,
               (const double4*)b0, nbr, cnt, (const double4*)v, (const double4*)a, (double4*)vh,
               (double4*)xc, (double4*)f, (double4*)q, scalars, err);
   SPHB_LAUNCH_CHECK();
@@ -405,7 +407,8 @@ extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const i
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TL_DISPATCH(k_tl_pass_b, sphb_blocks(p->n, kThreads), kThreads, *p, (const double4*)x0, nbr, cnt,
+  if (p->nrows <= 0) return SPHB_OK;
+  TL_DISPATCH(k_tl_pass_b, sphb_blocks(p->nrows, kThreads), kThreads, *p, (const double4*)x0, nbr, cnt,
               (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,
               (int)update_v);
   SPHB_LAUNCH_CHECK();
@@ -429,7 +432,9 @@ extern "C" int sphb_tl_speed_max(const sphb_tl_params* p, const double* v, doubl
   cudaStream_t st = (cudaStream_t)stream;
   SPHB_CUDA_CHECK(cudaMemsetAsync(scalars + 2, 0, sizeof(double), st));
   if (p->n == 0) return SPHB_OK;
-  TL_DISPATCH(k_tl_speed, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, scalars);
+  if (p->nrows <= 0) return SPHB_OK;
+  TL_DISPATCH(k_tl_speed, sphb_blocks(p->nrows, 256), 256, p->row0, p->nrows, (const double4*)v,
+              scalars);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

@@ -106,7 +106,7 @@ def _is_tensor(a) -> bool:
 
 # ----------------------------------------------------------------- the grid
 def make_grid(pos: np.ndarray | None, cutoff: float, box=None, *, dim: int | None = None,
-              lo=None, hi=None) -> _lib.Grid:
+              lo=None, hi=None, slow_axis: int | None = None) -> _lib.Grid:
     """Cell grid exactly as build_neighbors sets it up (neighbors.py:183-203).
 
     Either host positions, or (for device-resident sets) their per-axis
@@ -142,6 +142,16 @@ def make_grid(pos: np.ndarray | None, cutoff: float, box=None, *, dim: int | Non
         g.box[a] = float(box_arr[a]) if a < d else 1.0
         g.lo[a] = float(lo_arr[a]) if a < d else 0.0
     g.ntot = int(np.prod(ncell))
+    # storage order: sort key with `slow_axis` slowest (default: the reference key)
+    sa = d - 1 if slow_axis is None else int(slow_axis)
+    if not 0 <= sa < d:
+        raise ValueError("slow_axis out of range")
+    g.slow_axis = sa
+    order = [a for a in range(d) if a != sa] + [sa]
+    st = 1
+    for a in order:
+        g.sstrides[a] = st
+        st *= int(ncell[a])
     g.cutoff = float(cutoff)
     g.cut2 = float(cutoff) * float(cutoff)
     if g.ntot > 2**31 - 1:
@@ -324,8 +334,8 @@ class TilePlan:
         self.tile = 256 // self.group
         self.ok = False
         self.umax = 0
-        if n == 0 or width == 0:
-            return
+        if n == 0 or width == 0 or bins.grid.slow_axis != bins.dim - 1:
+            return          # runs assume the reference key (axis 0 fastest) order
         ntiles = (n + self.tile - 1) // self.tile
         self.runs = torch.empty((ntiles, self.RMAX, 3), dtype=torch.int32, device=dev)
         self.meta = torch.empty((ntiles, 4), dtype=torch.int32, device=dev)

@@ -54,9 +54,9 @@ class SlabPlan:
     def __init__(self, positions, grid, rank: int, world: int, axis: int | None = None):
         pos = np.asarray(positions, dtype=float)
         self.dim = pos.shape[1]
-        self.axis = self.dim - 1 if axis is None else axis
-        if self.axis != self.dim - 1:
-            raise ValueError("slabs are cut along the slowest flat-key axis (the last axis)")
+        self.axis = int(grid.slow_axis) if axis is None else axis
+        if self.axis != grid.slow_axis:
+            raise ValueError("slabs are cut along the grid's storage slow axis")
         self.rank, self.world = int(rank), int(world)
         self.periodic = bool(grid.periodic)
         nz = int(grid.ncell[self.axis])
@@ -152,3 +152,31 @@ def slab_eulerian(positions, state, eos, kernel, *, rank: int, world: int, dist,
     return EulerianSolver(pos[ids], ids.size, local, eos, kernel, None, correction=correction,
                           cfl=cfl, mu=mu, periodic_box=periodic_box, _slab=plan, _grid=grid,
                           _dist=dist)
+
+
+def slab_solid(X0, material, kernel, dp, *, rank: int, world: int, dist, fixed=None,
+               correction: bool = True, cfl: float = 0.6, axis: int | None = None):
+    """SolidSystem for this rank's slab of a global reference configuration.
+
+    The slab axis defaults to the one with the most cell layers (the long
+    axis of a column); particles are stored with that axis slowest so the
+    owned block and the exchanged layers are contiguous.  Per step the halo
+    receives Q after pass A and (v, a) after pass B.  Set the initial
+    velocity with `system.v = v0[system.local_ids]`.
+    """
+    from .neighbors import make_grid
+    from .tlsph import SolidSystem
+
+    X = np.ascontiguousarray(X0, dtype=float)
+    cut = kernel.kappa * kernel.h
+    if axis is None:
+        probe = make_grid(X, cut, None)
+        axis = int(np.argmax([probe.ncell[a] for a in range(X.shape[1])]))
+    grid = make_grid(X, cut, None, slow_axis=axis)
+    plan = SlabPlan(X, grid, rank, world)
+    ids = plan.local_ids
+    fx = None if fixed is None else np.asarray(fixed, dtype=bool)[ids]
+    system = SolidSystem(X[ids], material, kernel, dp, fixed=fx, correction=correction, cfl=cfl,
+                         _slab=plan, _grid=grid, _dist=dist)
+    system.local_ids = ids
+    return system

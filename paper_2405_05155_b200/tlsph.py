@@ -123,7 +123,7 @@ class SolidSystem:
     """Reference configuration, state and fused passes for one solid body."""
 
     def __init__(self, X0, material: Material, kernel: KernelSpec, dp: float, *, fixed=None,
-                 correction: bool = True, cfl: float = 0.6):
+                 correction: bool = True, cfl: float = 0.6, _slab=None, _grid=None, _dist=None):
         if kernel.code != CODE_WENDLAND:
             raise NotImplementedError("the TL engine evaluates the Wendland family")
         torch = _lib.torch_cuda()
@@ -142,8 +142,13 @@ class SolidSystem:
         dev = _lib.device()
         self._dev = dev
 
-        self.grid = make_grid(self.X0, kernel.kappa * kernel.h, None)      # tlsph.py:140
+        # slab ranks (slab.py) bin their owned+halo set with the GLOBAL grid
+        self._slab, self._dist = _slab, _dist
+        self.grid = (_grid if _grid is not None
+                     else make_grid(self.X0, kernel.kappa * kernel.h, None))   # tlsph.py:140
         self.bins = bin_particles(_lib.to_device(self.X0, torch.float64), self.grid)
+        if _slab is not None:
+            _slab.attach(self.bins.perm.cpu().numpy())
         self.nbr, self.cnt, self.width = ell_from_bins(self.bins, kernel.h, kernel.kappa)
         self.perm = self.bins.perm.long()
         self.rank = self.bins.rank()
@@ -184,6 +189,8 @@ class SolidSystem:
         lam, g = material.lame
         p = self.params = _lib.TLParams()
         p.dim, p.width, p.n = d, self.width, n
+        p.row0, p.nrows = ((_slab.rows.start, _slab.rows.stop - _slab.rows.start)
+                           if _slab is not None else (0, n))
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
         p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
         self._cfl_h = self.cfl * kernel.h
@@ -252,11 +259,32 @@ class SolidSystem:
         st = _lib.stream_ptr()
         _lib.call("sphb_tl_stress", ctypes.byref(self.params), self.Frec.data_ptr(),
                   self.B0rec.data_ptr(), self.Qrec.data_ptr(), st)
+        self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
                   self.scalars.data_ptr(), 0, st)
+        self._halo(self.A)
         self._acc_valid = True
+
+    def _halo(self, *bufs):
+        if self._slab is not None:
+            self._slab.exchange(self._dist, list(bufs))
+
+    def _reduce_speed(self):
+        if self._slab is not None and self._slab.world > 1:
+            self._dist.all_reduce(self.scalars[2:3], op=self._dist.ReduceOp.MAX)
+
+    def owned(self):
+        """(global ids, x, v, F) of the rows this system updates (slab ranks)."""
+        rows = self._slab.rows if self._slab is not None else slice(0, self.n)
+        ids = self.perm[rows].cpu().numpy()
+        if self._slab is not None:
+            ids = self._slab.local_ids[ids]
+        x = self.XC[rows, :self.dim].cpu().numpy()
+        v = self.V[rows, :self.dim].cpu().numpy()
+        F = _mat_unrec(self.Frec[rows], rows.stop - rows.start, self.dim).cpu().numpy()
+        return ids, x, v, F
 
     def accelerations(self):
         """Corrected TL momentum rate / rho0 (tlsph.py:164-171), caller order."""
@@ -283,6 +311,7 @@ class SolidSystem:
     def _speed_max(self):
         _lib.call("sphb_tl_speed_max", ctypes.byref(self.params), self.V.data_ptr(),
                   self.scalars.data_ptr(), _lib.stream_ptr())
+        self._reduce_speed()
 
     def stable_dt(self) -> float:
         """cfl h / (c_s + max|v|) (tlsph.py:178-180)."""
@@ -300,13 +329,21 @@ class SolidSystem:
                   self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
                   self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
+        self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
                   self.scalars.data_ptr(), 1, st)
+        self._halo(self.V, self.A)
+        self._reduce_speed()
 
     def _raise_if_bad(self):
-        err = int(self.err.item())
+        if self._slab is not None and self._slab.world > 1:
+            e = self.err.clone()
+            self._dist.all_reduce(e, op=self._dist.ReduceOp.MAX)
+            err = int(e.item())
+        else:
+            err = int(self.err.item())
         if err:
             self.err.zero_()
             raise SolidStateError(f"deformation gradient inverted (flags {err}) "
@@ -340,7 +377,7 @@ class SolidSystem:
             self._speed_max()
         self.scalars[1] = 0.0
         if graph is None:
-            graph = n_steps >= 8
+            graph = n_steps >= 8 and self._slab is None
         if graph:
             g = self._step_graph(dto)
             for _ in range(n_steps):

@@ -145,3 +145,51 @@ def test_slab_solver_matches_single_gpu(world, kernel):
     # identical rows and summation order; only FMA scheduling may differ
     np.testing.assert_allclose(got_rho, want_rho, rtol=1e-14, atol=0)
     np.testing.assert_allclose(got_mom, want_mom, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("world,kernel", [(2, "1.6h"), (3, "2h")])
+def test_slab_solid_matches_single_gpu(world, kernel):
+    from paper_2405_05155_b200.slab import slab_solid
+    from paper_2405_05155_b200.tlsph import SolidSystem
+
+    cfg = configs.c4_column(kernel=kernel, n_width=6)
+    steps = 20
+    ref = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
+                      cfl=cfg["cfl"])
+    ref.v = cfg["v0"]
+    ref.advance(steps)
+    want = (ref.x, ref.v, ref.F)
+
+    shared = Shared(world)
+    results, errors = {}, []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                d = ThreadDist(shared, rank)
+                s = slab_solid(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], rank=rank,
+                               world=world, dist=d, fixed=cfg["fixed"], cfl=cfg["cfl"])
+                assert s._slab.axis == 1          # the column's long axis
+                s.v = cfg["v0"][s.local_ids]
+                s.advance(steps)
+                results[rank] = s.owned()
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    got = [np.full_like(w, np.nan) for w in want]
+    for ids, x, v, F in results.values():
+        for g, val in zip(got, (x, v, F)):
+            g[ids] = val
+    for g, w in zip(got, want):
+        assert not np.isnan(g).any()
+        np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-14 * np.abs(w).max())

@@ -167,6 +167,30 @@ def test_slab_plan_layers_and_slices():
     assert owned_total == cfg["pos"].shape[0]
 
 
+def test_column_slabs_along_long_axis():
+    """TL column: slabs along y (axis 1) with y as the storage slow axis;
+    owned blocks and exchanged layers are contiguous and pair up."""
+    cfg = configs.c4_column(n_width=6)
+    spec = cfg["spec"]
+    grid = make_grid(cfg["X0"], spec.kappa * spec.h, None, slow_axis=1)
+    assert grid.sstrides[1] == grid.ncell[0] * grid.ncell[2]
+    world = 4
+    plans = []
+    for rank in range(world):
+        plan = SlabPlan(cfg["X0"], grid, rank, world)
+        assert plan.axis == 1
+        lpos = cfg["X0"][plan.local_ids]
+        skey = sum(cell_layer(lpos, grid, a) * int(grid.sstrides[a]) for a in range(3))
+        plan.attach(np.argsort(skey, kind="stable"))
+        plans.append((plan, plan.local_ids[np.argsort(skey, kind="stable")]))
+    # open ends: no lower halo on rank 0, no upper halo on the last rank
+    assert plans[0][0].prev is None and plans[-1][0].next is None
+    for (a, ga), (b, gb) in zip(plans[:-1], plans[1:]):
+        assert np.array_equal(ga[a.send_hi], gb[b.recv_lo])   # a's last layer -> b's halo
+        assert np.array_equal(gb[b.send_lo], ga[a.recv_hi])   # b's first layer -> a's halo
+    assert sum(p.n_owned for p, _ in plans) == cfg["X0"].shape[0]
+
+
 def test_slab_neighbor_rows_identical_to_global():
     from oracle import oracle as O
 

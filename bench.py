@@ -101,7 +101,7 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def make_solver(cfg, dist=None, rank=0, world=1):
+def make_solver(cfg, dist=None, rank=0, world=1, precision="fp64"):
     from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
                                                 FluidState)
 
@@ -114,7 +114,39 @@ def make_solver(cfg, dist=None, rank=0, world=1):
         return slab_eulerian(cfg["pos"], st, eos, cfg["spec"], rank=rank, world=world, dist=dist,
                              cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
     return EulerianSolver(cfg["pos"], n, st, eos, cfg["spec"], None, correction=True,
-                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"],
+                          precision=precision)
+
+
+def fp32_leg(torch, cfg, steps, warmup):
+    """Optional FP32 mode (north star): its throughput and its error against
+    the FP64 engine after the same number of steps from the same state."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    s32 = make_solver(cfg, precision="fp32")
+    s32.advance(warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s32.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st32 = s32.state
+    rho32, mom32 = st32.rho.copy(), st32.mom.copy()
+    del s32
+    torch.cuda.empty_cache()
+    s64 = make_solver(cfg)
+    s64.advance(warmup + steps)
+    st64 = s64.state
+    rho0 = cfg["rho0"]
+    err = {"rel_l2_mom": l2_error(mom32, st64.mom),
+           "rel_l2_rho_minus_rho0": l2_error(rho32 - rho0, st64.rho - rho0),
+           "after_steps": warmup + steps}
+    del s64
+    torch.cuda.empty_cache()
+    n = cfg["pos"].shape[0]
+    return {"value": n * steps / (ms * 1e-3), "ms_per_step": ms / steps, "error_vs_fp64": err}
 
 
 def fp64_peak(torch, lib):
@@ -234,6 +266,7 @@ def main():
     ap.add_argument("--n-side", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-2h", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -290,6 +323,9 @@ def main():
         leg["2h"] = run_leg(torch, cfg2, args.steps, max(3, args.warmup), dist, world)
         del leg["2h"]["solver"]
         torch.cuda.empty_cache()
+    f32 = None
+    if world == 1 and not args.no_fp32:
+        f32 = fp32_leg(torch, cfg, args.steps, max(3, args.warmup))
 
     L = leg["1.6h"]
     n, K = L["n"], args.steps
@@ -333,6 +369,10 @@ def main():
             "pair_interactions_per_s": S["pairs"] * 2 * K / (S["ms"] * 1e-3),
             "pairs_per_pass": S["pairs"]}
         line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
+    if f32 is not None:
+        line["fp32_mode"] = dict(f32, unit="particle-steps/s", kernel="k_wc_stage_f32<3>",
+                                 note="FP32 pair math, FP64 accumulation/state; reported "
+                                      "separately, not the headline")
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_reference()
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -289,6 +289,19 @@ int sphb_wc_stage_geo(const sphb_wc_params* p, int32_t stage, const int32_t* nbr
                       const double* S_n, const double* M_n, double* S_out, double* M_out,
                       double* scalars, int32_t* err, void* stream);
 
+/* Optional FP32 mode (north star): FP32 pair geometry + flux from FP32
+ * neighbour records X32 float4 {x, 0}, B32 planes float4 + float2, S32
+ * float4 {v, rho - rho0}; FP64 accumulation and stage update on the FP64
+ * state.  Stage 1 writes S32_out only; stage 2 writes S32_out, S_out, M_out.
+ * Uniform volumes. */
+int sphb_wc_stage_f32(const sphb_wc_params* p, int32_t stage, const float* X32,
+                      const float* B32, const int32_t* nbr, const int32_t* cnt,
+                      const float* S32_in, const double* S_n, const double* M_n,
+                      float* S32_out, double* S_out, double* M_out, double* scalars,
+                      int32_t* err, void* stream);
+int sphb_wc_state_to_f32(int64_t n, int32_t dim, double rho0, const double* S, float* S32,
+                         void* stream);
+
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,
                       void* stream);

@@ -130,6 +130,8 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_wc_stage_f32": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_wc_state_to_f32": (C.c_int, [I64, I32, F64, P, P, P]),
     "sphb_wc_geometry": (C.c_int, [P, I64, P, P, P, I32, P, P, P, P, P]),
     "sphb_wc_stage_geo": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_pack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),

@@ -176,8 +176,8 @@ class EulerianSolver:
 
     def __init__(self, positions, n_interior, state: FluidState, eos: EosParams,
                  kernel: KernelSpec, ghosts=None, *, correction: bool = True, cfl: float = 0.5,
-                 mu: float = 0.0, periodic_box=None, wall_force_tag=None, _slab=None,
-                 _grid=None, _dist=None):
+                 mu: float = 0.0, periodic_box=None, wall_force_tag=None,
+                 precision: str = "fp64", _slab=None, _grid=None, _dist=None):
         if mu < 0.0:
             raise ConfigError("viscosity must be non-negative")
         if ghosts is not None:
@@ -307,6 +307,20 @@ class EulerianSolver:
         self.S1 = torch.empty_like(self.S)
         self.S_nx = torch.empty_like(self.S)
         self.M_nx = torch.empty_like(self.M)
+        # optional FP32 mode (north star): FP32 neighbour records + pair math,
+        # FP64 accumulation and state (wc_f32.cu); companions of S, S1, S_nx
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        if precision == "fp32" and not uniform:
+            raise NotImplementedError("the FP32 mode assumes uniform particle volumes")
+        self.precision = precision
+        if precision == "fp32":
+            f32 = torch.float32
+            self.X32 = self.X.to(f32)
+            self.X32[:, self.dim] = 0.0
+            self.B32 = self.B.to(f32)
+            self._c32 = {t.data_ptr(): torch.empty((self.n, 4), dtype=f32, device=dev)
+                         for t in (self.S, self.S1, self.S_nx)}
         self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self._rho_io = torch.empty(self.n, dtype=torch.float64, device=dev)
@@ -336,6 +350,9 @@ class EulerianSolver:
         _lib.call("sphb_wc_pack_state", self.n, self.dim, self.bins.perm.data_ptr(),
                   rho_d.data_ptr(), mom_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(),
                   _lib.stream_ptr())
+        if self.precision == "fp32":
+            _lib.call("sphb_wc_state_to_f32", self.n, self.dim, self.eos.rho0, self.S.data_ptr(),
+                      self._c32[self.S.data_ptr()].data_ptr(), _lib.stream_ptr())
         self._state_host = None
         self._refresh_speed()
 
@@ -364,6 +381,8 @@ class EulerianSolver:
 
     def _halo(self, buf):
         if self._slab is not None:
+            if self.precision == "fp32":      # neighbours read the FP32 companion
+                buf = self._c32[buf.data_ptr()]
             self._slab.exchange(self._dist, [buf])
 
     @property
@@ -413,6 +432,16 @@ class EulerianSolver:
         self._launch_stage_raw(stage, s_in, s_n, m_n, s_out, m_out)
 
     def _launch_stage_raw(self, stage, s_in, s_n, m_n, s_out, m_out):
+        if self.precision == "fp32":
+            c32 = self._c32
+            out32 = c32.get(s_out.data_ptr(), c32[self.S1.data_ptr()])
+            _lib.call("sphb_wc_stage_f32", ctypes.byref(self.params), stage, self.X32.data_ptr(),
+                      self.B32.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                      c32[s_in.data_ptr()].data_ptr(), s_n.data_ptr(), m_n.data_ptr(),
+                      out32.data_ptr(), s_out.data_ptr(),
+                      None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                      self.err.data_ptr(), _lib.stream_ptr())
+            return
         if self.geo is not None:
             _lib.call("sphb_wc_stage_geo", ctypes.byref(self.params), stage, self.nbr.data_ptr(),
                       self.cnt.data_ptr(), self.geo.data_ptr(), s_in.data_ptr(), s_n.data_ptr(),

@@ -47,6 +47,20 @@ BYTES_STAGE = {1: 136, 2: 168}
 FLOPS_PER_PAIR_EST = 120
 
 
+def traffic_per_launch(kernel: str):
+    """DRAM bytes per stage launch from the committed ncu capture, if it was
+    taken on this kernel (profiles/r01_traffic.json), else None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
+            t = json.load(f)
+    except OSError:
+        return None
+    if t.get("kernel") != kernel:
+        return None
+    s = t["stage_launch"]
+    return s["dram_bytes_read"] + s["dram_bytes_write"]
+
+
 def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -347,7 +361,9 @@ def main():
         "pairs_per_pass": L["pairs"],
         "gpu_launches": 3 * K,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak,
+                     "traffic": traffic_per_launch(L["kernel"]) if world == 1 else None,
+                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md",
                      "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": avg_stage_ms,

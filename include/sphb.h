@@ -251,6 +251,8 @@ typedef struct sphb_wc_params {
   double h, alpha, kappa; /* Wendland family only (code 0)                  */
   double c_art, rho0, mu, cfl;
   double vol_const;
+  int32_t swizzle;       /* >0: SM count for the block->chunk L1-locality swizzle */
+  int32_t reserved;
 } sphb_wc_params;
 
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.

@@ -76,6 +76,8 @@ class WCParams(C.Structure):
         ("mu", C.c_double),
         ("cfl", C.c_double),
         ("vol_const", C.c_double),
+        ("swizzle", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

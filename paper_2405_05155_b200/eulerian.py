@@ -300,6 +300,10 @@ class EulerianSolver:
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
         p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
         p.vol_const = float(vol[0]) if self.n else 0.0
+        # block->SM locality swizzle: measured slower on C5 (co-scheduled
+        # blocks on one contiguous region share neighbour rows through L2);
+        # off by default, SPHB_SWIZZLE=<sm count> to enable
+        p.swizzle = int(os.environ.get("SPHB_SWIZZLE", "0"))
         self._cfl_h = self.cfl * kernel.h                      # eulerian.py:560
 
         self.S = torch.empty((self.n, 4), dtype=torch.float64, device=dev)

@@ -53,15 +53,17 @@ def main():
     if args.one:
         one(args.n_side, args.kernel, args.steps)
         return
-    variants = [("geo", 1, 4), ("global", 1, 4), ("global", 2, 4), ("tiled", 8, 4)]
-    for kern, g, mb in variants:
+    variants = [("global", 1, 4, 0), ("global", 1, 4, 148), ("global", 2, 4, 148),
+                ("global", 1, 6, 148)]
+    for kern, g, mb, sw in variants:
         env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb),
-                   SPHB_TILE_GROUP=str(g))
+                   SPHB_TILE_GROUP=str(g), SPHB_SWIZZLE=str(sw))
         out = subprocess.run([sys.executable, __file__, "--one", "--n-side", str(args.n_side),
                               "--kernel", args.kernel, "--steps", str(args.steps)], env=env,
                              capture_output=True, text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
-        print(json.dumps({"kernel": kern, "group": g, "minb": mb, "result": line}), flush=True)
+        print(json.dumps({"kernel": kern, "group": g, "minb": mb, "swizzle": sw, "result": line}),
+              flush=True)
 
 
 if __name__ == "__main__":

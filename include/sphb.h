@@ -346,14 +346,21 @@ typedef struct sphb_tl_params {
   double lam, g;           /* Lame parameters (tlsph.py:27-35) */
 } sphb_tl_params;
 
+/* g0: optional per-slot reference gradients (sphb_tl_geometry); NULL ->
+ * recompute g0_ij from X0 per pair.  With g0 the clamp flag of a neighbour
+ * is read from A_j.w, which pass B maintains (A record {a0, a1, a2, fixed}). */
 int sphb_tl_pass_a(const sphb_tl_params* p, const double* X0, const double* B0,
-                   const int32_t* nbr, const int32_t* cnt, const double* V,
-                   const double* A, double* Vh, double* XC, double* F,
+                   const int32_t* nbr, const int32_t* cnt, const double* g0,
+                   const double* V, const double* A, double* Vh, double* XC, double* F,
                    double* Q, const double* scalars, int32_t* err, void* stream);
 int sphb_tl_pass_b(const sphb_tl_params* p, const double* X0, const int32_t* nbr,
-                   const int32_t* cnt, const double* Q, const double* Vh,
-                   double* A, double* V, double* scalars, int32_t update_v,
-                   void* stream);
+                   const int32_t* cnt, const double* g0, const double* Q, const double* Vh,
+                   double* A, double* V, double* scalars, int32_t update_v, void* stream);
+/* Static reference gradients g0_ij = dW e_ij V0 (tlsph.py:145-146) per ELL
+ * slot, planes g0[(c * width + k) * n + s]; reference arithmetic. */
+int sphb_tl_geometry(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
+                     const int32_t* nbr, const int32_t* cnt, int32_t width,
+                     const sphb_kernel* k, double vol0, double* g0, void* stream);
 /* Q = (F S(F)) B0^T for every particle (first accelerations() call). */
 int sphb_tl_stress(const sphb_tl_params* p, const double* F, const double* B0,
                    double* Q, void* stream);

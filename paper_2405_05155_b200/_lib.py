@@ -140,8 +140,9 @@ SIGNATURES = {
     "sphb_wc_unpack_state": (C.c_int, [I64, I32, P, P, P, P, P, P]),
     "sphb_fp64_probe": (C.c_int, [P, I32, I32, I32, P]),
     "sphb_set_dt": (C.c_int, [F64, F64, F64, P, P, P]),
-    "sphb_tl_pass_a": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
-    "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, I32, P]),
+    "sphb_tl_pass_a": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P]),
+    "sphb_tl_geometry": (C.c_int, [P, I64, P, P, P, I32, P, F64, P, P]),
     "sphb_tl_stress": (C.c_int, [P, P, P, P, P]),
     "sphb_tl_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_relax_accel": (C.c_int, [P, I64, P, P, P, P, P, P, F64, F64, P, P, P]),

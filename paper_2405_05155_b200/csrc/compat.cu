@@ -447,6 +447,38 @@ __global__ void k_wc_geometry(sphb_grid g, int64_t n, const double* __restrict__
   }
 }
 
+// Reference-configuration gradients of SolidSystem (tlsph.py:145-146:
+// g0 = pair_gradients(nlist0, kernel, None) * V0, correction.py:110-111) per
+// slot of the ELL pass list, as planes g0[(c * width + k) * n + s];
+// reference arithmetic (no FMA in this unit).
+template <int D>
+__global__ void k_tl_geometry(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+                              int32_t width, sphb_kernel k, double vol0,
+                              double* __restrict__ g0) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double scale = k.alpha / k.h;
+  double wi[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) wi[a] = ws[(int64_t)a * n + s];
+  const int32_t m = cnt[s];
+  for (int32_t kk = 0; kk < m; ++kk) {
+    const int64_t t = nbr[(int64_t)kk * n + s];
+    double dx[D];
+    double r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      dx[a] = min_image(wi[a] - ws[(int64_t)a * n + t], g.box[a], g.periodic);
+      r2 += dx[a] * dx[a];
+    }
+    const double r = sqrt(r2);
+    const double dw = scale * profile_deriv(k.code, r / k.h);
+#pragma unroll
+    for (int a = 0; a < D; ++a) g0[((int64_t)a * width + kk) * n + s] = dw * (dx[a] / r) * vol0;
+  }
+}
+
 }  // namespace
 
 #define SPHB_DISPATCH_D(dim, KERNEL, GRID, ...)                                   \
@@ -585,6 +617,19 @@ extern "C" int sphb_wc_geometry(const sphb_grid* g, int64_t n, const double* ws,
   const int T = 128;
   SPHB_DISPATCH_D(g->dim, k_wc_geometry, sphb_blocks(n, T), *g, n, ws, nbr, cnt, width, b, vol,
                   *k, geo);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_tl_geometry(const sphb_grid* g, int64_t n, const double* ws,
+                                const int32_t* nbr, const int32_t* cnt, int32_t width,
+                                const sphb_kernel* k, double vol0, double* g0, void* stream) {
+  if (!g || !k || n < 0 || width < 0) return SPHB_ERR_ARG;
+  if (n == 0 || width == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = 128;
+  SPHB_DISPATCH_D(g->dim, k_tl_geometry, sphb_blocks(n, T), *g, n, ws, nbr, cnt, width, *k,
+                  vol0, g0);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

@@ -183,10 +183,14 @@ __device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0
     }
 }
 
-template <int D>
+// GEO: read g0_ij from the streamed per-slot planes g0[(c * width + k) * n + i]
+// (sphb_tl_geometry) instead of recomputing it from X0_j; the clamp flag of
+// j then comes from A_j.w (pass B keeps it there).
+template <int D, bool GEO>
 __global__ void __launch_bounds__(kThreads)
 k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double4* __restrict__ B0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+            const double* __restrict__ g0,
             const double4* __restrict__ V, const double4* __restrict__ A, double4* __restrict__ Vh,
             double4* __restrict__ XC, double4* __restrict__ F, double4* __restrict__ Q,
             const double* __restrict__ scalars, int32_t* __restrict__ err) {
@@ -216,15 +220,27 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const int32_t* __restrict__ row = nbr + i;
   for (int32_t k = 0; k < cn; ++k) {
     const int64_t j = row[(int64_t)k * n];
-    double wj[D], vj[D], aj[D];
+    double vj[D], aj[D], g[D];
     bool fixed_j;
-    load_x0<D>(X0, j, wj, fixed_j);
     load_vec_nc<D>(V, j, vj);
-    load_vec_nc<D>(A, j, aj);
-    double dx[D], g[D];
+    if constexpr (GEO) {
+      const double4 a4 = ldg4(A + j);
+      const double ac[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
-    for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
-    ref_gradient<D>(dx, scale_v0, inv_h, g);
+      for (int a = 0; a < D; ++a) aj[a] = ac[a];
+      fixed_j = a4.w != 0.0;
+      const int64_t slot = (int64_t)k * n + i;
+#pragma unroll
+      for (int a = 0; a < D; ++a) g[a] = __ldg(g0 + ((int64_t)a * P.width) * n + slot);
+    } else {
+      double wj[D];
+      load_x0<D>(X0, j, wj, fixed_j);
+      load_vec_nc<D>(A, j, aj);
+      double dx[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+      ref_gradient<D>(dx, scale_v0, inv_h, g);
+    }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const double vhj = fixed_j ? 0.0 : fma(hdt, aj[a], vj[a]);
@@ -260,10 +276,11 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   store_vec<D>(XC, i, xc);
 }
 
-template <int D>
+template <int D, bool GEO>
 __global__ void __launch_bounds__(kThreads)
 k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+            const double* __restrict__ g0,
             const double4* __restrict__ Q, const double4* __restrict__ Vh,
             double4* __restrict__ A, double4* __restrict__ V, double* __restrict__ scalars,
             int update_v) {
@@ -285,15 +302,21 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     const int32_t* __restrict__ row = nbr + i;
     for (int32_t k = 0; k < cn; ++k) {
       const int64_t j = row[(int64_t)k * n];
-      double wj[D];
-      bool fixed_j;
-      load_x0<D>(X0, j, wj, fixed_j);
       double Qj[D][D];
       load_mat_nc<D>(Q, j, Qj);
-      double dx[D], g[D];
+      double g[D];
+      if constexpr (GEO) {
+        const int64_t slot = (int64_t)k * n + i;
 #pragma unroll
-      for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
-      ref_gradient<D>(dx, scale_v0, inv_h, g);
+        for (int a = 0; a < D; ++a) g[a] = __ldg(g0 + ((int64_t)a * P.width) * n + slot);
+      } else {
+        double wj[D], dx[D];
+        bool fixed_j;
+        load_x0<D>(X0, j, wj, fixed_j);
+#pragma unroll
+        for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+        ref_gradient<D>(dx, scale_v0, inv_h, g);
+      }
       // sum_j (Q_i + Q_j) g = Q_i sum_j g + sum_j Q_j g
 #pragma unroll
       for (int b = 0; b < D; ++b) gsum[b] += g[b];
@@ -310,7 +333,13 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
       for (int b = 0; b < D; ++b) s = fma(Qi[a][b], gsum[b], s);
       acc[a] = fixed_i ? 0.0 : s * inv_rho0;
     }
-    store_vec<D>(A, i, acc);
+    {   // acceleration record {a0, a1, a2, fixed}: the clamp flag rides in .w
+      double c4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int a = 0; a < D; ++a) c4[a] = acc[a];
+      c4[3] = fixed_i ? 1.0 : 0.0;
+      A[i] = make_double4(c4[0], c4[1], c4[2], c4[3]);
+    }
     double v[D];
     if (update_v) {
       const double hdt = 0.5 * scalars[0];
@@ -386,31 +415,46 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
     }                                                                      \
   } while (0)
 
+#define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                            \
+  do {                                                                            \
+    const bool geo_ = (GEOPTR) != nullptr;                                        \
+    switch (p->dim * 2 + (geo_ ? 1 : 0)) {                                        \
+      case 2: KERNEL<1, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      case 3: KERNEL<1, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
+      case 4: KERNEL<2, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      case 5: KERNEL<2, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
+      case 6: KERNEL<3, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
+      case 7: KERNEL<3, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
+      default: return SPHB_ERR_ARG;                                               \
+    }                                                                             \
+  } while (0)
+
 extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,
-                              const int32_t* nbr, const int32_t* cnt, const double* v,
-                              const double* a, double* vh, double* xc, double* f, double* q,
-                              const double* scalars, int32_t* err, void* stream) {
+                              const int32_t* nbr, const int32_t* cnt, const double* g0,
+                              const double* v, const double* a, double* vh, double* xc,
+                              double* f, double* q, const double* scalars, int32_t* err,
+                              void* stream) {
   if (!p || p->n < 0) return SPHB_ERR_ARG;
-  if (p->n == 0) return SPHB_OK;
+  if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->nrows <= 0) return SPHB_OK;
-  TL_DISPATCH(k_tl_pass_a, sphb_blocks(p->nrows, kThreads), kThreads, *p, (const double4*)x0,
-              (const double4*)b0, nbr, cnt, (const double4*)v, (const double4*)a, (double4*)vh,
-              (double4*)xc, (double4*)f, (double4*)q, scalars, err);
+  TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+                  (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)v,
+                  (const double4*)a, (double4*)vh, (double4*)xc, (double4*)f, (double4*)q,
+                  scalars, err);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }
 
 extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const int32_t* nbr,
-                              const int32_t* cnt, const double* q, const double* vh, double* a,
-                              double* v, double* scalars, int32_t update_v, void* stream) {
+                              const int32_t* cnt, const double* g0, const double* q,
+                              const double* vh, double* a, double* v, double* scalars,
+                              int32_t update_v, void* stream) {
   if (!p || p->n < 0) return SPHB_ERR_ARG;
-  if (p->n == 0) return SPHB_OK;
+  if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->nrows <= 0) return SPHB_OK;
-  TL_DISPATCH(k_tl_pass_b, sphb_blocks(p->nrows, kThreads), kThreads, *p, (const double4*)x0, nbr, cnt,
-              (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,
-              (int)update_v);
+  TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+                  (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
+                  (double4*)a, (double4*)v, scalars, (int)update_v);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

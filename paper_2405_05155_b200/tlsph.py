@@ -22,6 +22,7 @@ counterpart.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -182,6 +183,7 @@ class SolidSystem:
         self.XC = _vec_rec(xs, n, d, dev)
         self.V = torch.zeros((n, 4), dtype=torch.float64, device=dev)
         self.A = torch.zeros_like(self.V)
+        self.A[:, 3] = fixed_s            # clamp flag rides in A.w (tl_engine.cu)
         self.Vh = torch.zeros_like(self.V)
         self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -195,6 +197,19 @@ class SolidSystem:
         p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
         self._cfl_h = self.cfl * kernel.h
         self._c_s = material.sound_speed
+        # streamed reference gradients g0 (3 doubles per pair) when they fit in
+        # a quarter of the free memory (SPHB_TL_GEO=0 forces recomputation)
+        self.g0 = None
+        g0_bytes = d * self.width * n * 8
+        if (os.environ.get("SPHB_TL_GEO", "1") != "0" and n and self.width
+                and g0_bytes < 0.25 * torch.cuda.mem_get_info()[0]):
+            self.g0 = torch.empty(g0_bytes // 8, dtype=torch.float64, device=dev)
+            k = _lib.kernel_struct(kernel)
+            _lib.call("sphb_tl_geometry", ctypes.byref(self.grid), n,
+                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), self.width, ctypes.byref(k), self.dp**d,
+                      self.g0.data_ptr(), _lib.stream_ptr())
+        self._g0_ptr = None if self.g0 is None else self.g0.data_ptr()
         self._acc_valid = False
         self._host = {}
         self._v_out = False
@@ -261,7 +276,7 @@ class SolidSystem:
                   self.B0rec.data_ptr(), self.Qrec.data_ptr(), st)
         self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
+                  self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
                   self.scalars.data_ptr(), 0, st)
         self._halo(self.A)
@@ -325,13 +340,13 @@ class SolidSystem:
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
         _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                  self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr,
                   self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
                   self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
         self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.nbr.data_ptr(), self.cnt.data_ptr(), self.Qrec.data_ptr(),
+                  self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
                   self.scalars.data_ptr(), 1, st)
         self._halo(self.V, self.A)

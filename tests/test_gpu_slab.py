@@ -75,6 +75,16 @@ class ThreadDist:
         sh.barrier.wait()
         return []
 
+    def get_rank(self):
+        return self.rank
+
+    def get_world_size(self):
+        return self.shared.world
+
+    def barrier(self):
+        torch.cuda.current_stream().synchronize()
+        self.shared.barrier.wait()
+
     def all_reduce(self, t, op="sum"):
         sh = self.shared
         torch.cuda.current_stream().synchronize()
@@ -193,3 +203,34 @@ def test_slab_solid_matches_single_gpu(world, kernel):
     for g, w in zip(got, want):
         assert not np.isnan(g).any()
         np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-14 * np.abs(w).max())
+
+
+def test_bench_multi_rank_leg_with_thread_ranks():
+    """bench.py's multi-GPU leg (slab solver, barrier, max-over-ranks time,
+    all-reduced pair count) driven by two thread ranks on one GPU."""
+    import bench
+
+    cfg = configs.c5_tgv3d(n_side=24)
+    world = 2
+    shared = Shared(world)
+    out, errors = {}, []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                d = ThreadDist(shared, rank)
+                out[rank] = bench.run_leg(torch, cfg, 3, 3, d, world)
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    assert out[0]["pairs"] == out[1]["pairs"] == 24**3 * 32
+    assert out[0]["ms"] == out[1]["ms"] > 0.0

@@ -65,18 +65,28 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
 #pragma unroll
   for (int a = 0; a < D; ++a) dm[a] = 0.0;
   if (active) {
+    // per-thread constants, folded so the pair loop is FMA-shaped
     const double c2 = c * c;
+    const double c2rho0 = c2 * P.rho0;
     const double eta_c = kEtaLinearized / c;
     const double inv_h = 1.0 / P.h;
-    const double scale = P.alpha / P.h;
+    const double c5s = -5.0 * P.alpha / P.h;        // dW = c5s q t^3
     const double half_cinv = 0.5 / c;
+    const double hc = 0.5 * c;
 
     double xi[D], vol_i, vi[D], rho_i;
     unpack_x<D>(X[i], xi, vol_i);
     unpack_s<D>(S_in[i], vi, rho_i);
     Sym<D> Bi;
     Bi.load(B, n, i);
-    const double p_i = c2 * (rho_i - P.rho0);
+    const double p_i = fma(c2, rho_i, -c2rho0);
+    const double hp_i = 0.5 * p_i, hrho_i = 0.5 * rho_i;
+    double hvi[D], hb[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      hvi[a] = 0.5 * vi[a];
+      hb[a] = 0.5 * P.box[a];
+    }
 
     const int32_t m = cnt[i];
     const int32_t* __restrict__ row = nbr + i;
@@ -91,23 +101,19 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
 
       // geometry (neighbors.py:152-165, correction.py:102-108, eulerian.py:506-513)
       double dx[D];
-      double r2 = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         double d = xi[a] - xj[a];
-        if (P.periodic) {
-          const double bx = P.box[a];
-          if (d > 0.5 * bx) d -= bx;
-          else if (d < -0.5 * bx) d += bx;
-        }
+        if (P.periodic && fabs(d) > hb[a]) d = d > 0.0 ? d - P.box[a] : d + P.box[a];
         dx[a] = d;
-        r2 = fma(d, d, r2);
       }
-      const double inv_r = rsqrt(r2);
-      const double r = r2 * inv_r;
-      const double q = r * inv_h;
+      double r2 = dx[0] * dx[0];
+#pragma unroll
+      for (int a = 1; a < D; ++a) r2 = fma(dx[a], dx[a], r2);
+      const double inv_r = rsqrt_nr(r2);
+      const double q = r2 * inv_r * inv_h;
       const double t = fma(-0.5, q, 1.0);
-      const double dW = scale * (-5.0 * q) * (t * t * t);  // (alpha/h) dP/dq
+      const double dW = (c5s * q) * (t * t * t);        // (alpha/h) dP/dq
       double e[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) e[a] = dx[a] * inv_r;
@@ -115,40 +121,41 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
       Bi.add(Bj, Bs);
       double g[D];
       Bs.mv(e, g);
-      const double gs = 0.5 * dW * vol_j;  // 0.5 (B_i + B_j) e dW V_j
+      const double dWv = dW * vol_j;
+      const double gs = 0.5 * dWv;                      // 0.5 (B_i + B_j) e dW V_j
 #pragma unroll
       for (int a = 0; a < D; ++a) g[a] *= gs;
-      const double viscv = 2.0 * dW * inv_r * vol_j;
+      const double mvisc = (2.0 * P.mu) * dWv * inv_r;  // mu viscv
 
-      // limited linearised Riemann problem along n = -e (eulerian.py:236-264)
-      double ul = 0.0, ur = 0.0;
+      // limited linearised Riemann problem along n = -e (eulerian.py:236-264):
+      // du = u_l - u_r = (v_j - v_i).e; u* - ubar = b^2 (p_i - p_j) / (2 rbar c)
+      double dv[D];
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        ul = fma(-vi[a], e[a], ul);
-        ur = fma(-vj[a], e[a], ur);
-      }
-      const double du = ul - ur;
+      for (int a = 0; a < D; ++a) dv[a] = vj[a] - vi[a];
+      double du = dv[0] * e[0];
+#pragma unroll
+      for (int a = 1; a < D; ++a) du = fma(dv[a], e[a], du);
       double beta = du * eta_c;
       beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
-      const double rbar = 0.5 * (rho_i + rho_j);
-      const double p_j = c2 * (rho_j - P.rho0);
-      double ustar_m_ubar = 0.0;
-      if (beta > 0.0) ustar_m_ubar = (beta * beta) * (p_i - p_j) * half_cinv / rbar;
-      const double p_star = fma(0.5 * beta * rbar * c, du, 0.5 * (p_i + p_j));
+      const double rbar = fma(0.5, rho_j, hrho_i);
+      const double p_j = fma(c2, rho_j, -c2rho0);
+      double w = 0.0;
+      if (beta > 0.0) w = ((beta * beta) * (p_i - p_j) * half_cinv) * rcp_nr(rbar);
+      const double p_star = fma((beta * rbar) * hc, du, fma(0.5, p_j, hp_i));
       double vs[D];
-      double s = 0.0;
+      double sdot = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        vs[a] = fma(-ustar_m_ubar, e[a], 0.5 * (vi[a] + vj[a]));
-        s = fma(vs[a], g[a], s);
+        vs[a] = fma(-w, e[a], fma(0.5, vj[a], hvi[a]));
+        sdot = fma(vs[a], g[a], sdot);
       }
-      dr = fma(-2.0 * rbar, s, dr);
-      const double rs = rbar * s;
-      const double mv = P.mu * viscv;
+      const double rbar2 = -2.0 * rbar;
+      dr = fma(rbar2, sdot, dr);
+      const double rs2 = rbar2 * sdot, ps2 = -2.0 * p_star;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const double fm = -2.0 * fma(rs, vs[a], p_star * g[a]);
-        dm[a] = fma(mv, vi[a] - vj[a], dm[a] + fm);
+        const double fm = fma(rs2, vs[a], ps2 * g[a]);
+        dm[a] = fma(-mvisc, dv[a], dm[a] + fm);
       }
     }
   }

@@ -31,6 +31,24 @@ namespace {
 
 constexpr int kThreads = 128;
 
+// Per-launch constants folded on the host from sphb_wc_params.
+struct WCConst {
+  double c2, c2rho0, eta_c, inv_h, c5s, half_cinv, hc, mu2;
+};
+
+inline WCConst wc_const(const sphb_wc_params& p) {
+  WCConst k;
+  k.c2 = p.c_art * p.c_art;
+  k.c2rho0 = k.c2 * p.rho0;
+  k.eta_c = kEtaLinearized / p.c_art;
+  k.inv_h = 1.0 / p.h;
+  k.c5s = -5.0 * p.alpha / p.h;       // dW = c5s q t^3 (Wendland, kernels.py:55-57)
+  k.half_cinv = 0.5 / p.c_art;
+  k.hc = 0.5 * p.c_art;
+  k.mu2 = 2.0 * p.mu;
+  return k;
+}
+
 // G consecutive lanes share one particle: at each step they take G
 // consecutive entries of its row, which in the reference's stencil order are
 // mostly consecutive particles of one cell, so the G neighbour records share
@@ -38,8 +56,9 @@ constexpr int kThreads = 128;
 // one-thread-per-particle.  Partial sums are combined with warp shuffles.
 template <int D, int G, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ X,
-           const double* __restrict__ B, const int32_t* __restrict__ nbr,
+k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
+           const double4* __restrict__ X, const double* __restrict__ B,
+           const int32_t* __restrict__ nbr,
            const int32_t* __restrict__ cnt, const double4* __restrict__ S_in,
            const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
            double* __restrict__ scalars, int32_t* __restrict__ err) {
@@ -65,14 +84,10 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
 #pragma unroll
   for (int a = 0; a < D; ++a) dm[a] = 0.0;
   if (active) {
-    // per-thread constants, folded so the pair loop is FMA-shaped
-    const double c2 = c * c;
-    const double c2rho0 = c2 * P.rho0;
-    const double eta_c = kEtaLinearized / c;
-    const double inv_h = 1.0 / P.h;
-    const double c5s = -5.0 * P.alpha / P.h;        // dW = c5s q t^3
-    const double half_cinv = 0.5 / c;
-    const double hc = 0.5 * c;
+    // host-folded constants (kernel parameters live in the constant bank, so
+    // the FP64 instructions read them as operands instead of registers)
+    const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, inv_h = K.inv_h;
+    const double c5s = K.c5s, half_cinv = K.half_cinv, hc = K.hc;
 
     double xi[D], vol_i, vi[D], rho_i;
     unpack_x<D>(X[i], xi, vol_i);
@@ -90,6 +105,7 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
 
     const int32_t m = cnt[i];
     const int32_t* __restrict__ row = nbr + i;
+#pragma unroll 2
     for (int32_t k = gl; k < m; k += G) {
       const int64_t j = row[(int64_t)k * n];
       double xj[D], vol_j, vj[D], rho_j;
@@ -125,7 +141,7 @@ k_wc_stage(const sphb_wc_params P, const int stage, const double4* __restrict__ 
       const double gs = 0.5 * dWv;                      // 0.5 (B_i + B_j) e dW V_j
 #pragma unroll
       for (int a = 0; a < D; ++a) g[a] *= gs;
-      const double mvisc = (2.0 * P.mu) * dWv * inv_r;  // mu viscv
+      const double mvisc = K.mu2 * dWv * inv_r;         // mu viscv
 
       // limited linearised Riemann problem along n = -e (eulerian.py:236-264):
       // du = u_l - u_r = (v_j - v_i).e; u* - ubar = b^2 (p_i - p_j) / (2 rbar c)
@@ -311,6 +327,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   if (p->nrows == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const double4* X = (const double4*)x;
+  const WCConst K = wc_const(*p);
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
   const double4* Mn = (const double4*)m_n;
@@ -318,7 +335,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   double4* Mout = (double4*)m_out;
 #define SPHB_STAGE(D, G, MB)                                                               \
   k_wc_stage<D, G, MB><<<sphb_blocks(p->nrows * G, kThreads), kThreads, 0, st>>>(              \
-      *p, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                   \
+      *p, K, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                \
   break
   // SPHB_WC_MINB (tuning): 4 -> <=128 registers, 6 -> <=80, 8 -> <=64
   static int minb = [] {
@@ -336,6 +353,8 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
     case 768 + 32 + 4: SPHB_STAGE(3, 2, 4);
     case 768 + 64 + 4: SPHB_STAGE(3, 4, 4);
     case 768 + 128 + 4: SPHB_STAGE(3, 8, 4);
+    case 768 + 16 + 5: SPHB_STAGE(3, 1, 5);
+    case 768 + 32 + 5: SPHB_STAGE(3, 2, 5);
     case 768 + 16 + 6: SPHB_STAGE(3, 1, 6);
     case 768 + 32 + 6: SPHB_STAGE(3, 2, 6);
     case 768 + 64 + 6: SPHB_STAGE(3, 4, 6);

@@ -53,8 +53,8 @@ def main():
     if args.one:
         one(args.n_side, args.kernel, args.steps)
         return
-    variants = [("global", 1, 4, 0), ("global", 1, 4, 148), ("global", 2, 4, 148),
-                ("global", 1, 6, 148)]
+    variants = [("global", 1, 4, 0), ("global", 1, 5, 0), ("global", 2, 5, 0),
+                ("global", 1, 6, 0)]
     for kern, g, mb, sw in variants:
         env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb),
                    SPHB_TILE_GROUP=str(g), SPHB_SWIZZLE=str(sw))

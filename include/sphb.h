@@ -253,6 +253,7 @@ typedef struct sphb_wc_params {
   double vol_const;
   int32_t swizzle;       /* >0: SM count for the block->chunk L1-locality swizzle */
   int32_t reserved;
+  const int8_t* interior; /* NULL, or 1 for rows to update (ghosts: 0), sorted */
 } sphb_wc_params;
 
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.
@@ -303,6 +304,15 @@ int sphb_wc_stage_f32(const sphb_wc_params* p, int32_t stage, const float* X32,
                       int32_t* err, void* stream);
 int sphb_wc_state_to_f32(int64_t n, int32_t dim, double rho0, const double* S, float* S32,
                          void* stream);
+
+/* Ghost refresh (apply_boundaries, eulerian.py:371-447), WC kinds 0,1,2,3,5
+ * (copy, mirror, wall, fixed, blend-mirror): ghost record S[ghost_sorted[g]]
+ * from its source S[src_sorted[g]].  normal/wall_v (ng, d), fixed (ng, d+2)
+ * conserved {rho, mom, E}, blend (ng) (may be NULL without kind 5). */
+int sphb_wc_ghosts(int32_t dim, int64_t ng, const int32_t* ghost_sorted,
+                   const int32_t* src_sorted, const int8_t* kind, const double* normal,
+                   const double* wall_v, const double* fixed, const double* blend,
+                   double* S, int32_t* err, void* stream);
 
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,

@@ -219,14 +219,18 @@ class EulerianWC:
     """EulerianSolver, WC branch, periodic, no ghosts (eulerian.py:473-643)."""
 
     def __init__(self, pos, vol, rho, mom, spec, c_art, rho0=1.0, mu=0.0, cfl=0.5, box=None,
-                 correction=True):
+                 correction=True, ghosts=None, n_int=None):
         self.spec, self.c_art, self.rho0, self.mu, self.cfl = spec, c_art, rho0, mu, cfl
         self.nl = build_neighbors(pos, spec.kappa * spec.h, box)
         self.vol = np.asarray(vol, dtype=float)
         self.rho = np.array(rho, dtype=float)
         self.mom = np.array(mom, dtype=float)
         self.n, self.d = self.mom.shape
+        self.n_int = self.n if n_int is None else int(n_int)
+        self.ghosts = ghosts
         b = correction_matrices(self.nl, self.vol, spec)[0] if correction else None
+        if b is not None and ghosts is not None:       # eulerian.py:499-501
+            b[self.n_int:] = b[np.asarray(ghosts.src, dtype=np.int64)]
         self.B = b
         gw = pair_gradients(self.nl, spec, b)
         self.gwv = np.ascontiguousarray(gw * self.vol[self.nl.idx][:, None])
@@ -235,31 +239,76 @@ class EulerianWC:
         self.viscv = np.ascontiguousarray(2.0 * dw / self.nl.r * self.vol[self.nl.idx])
         self.t = 0.0
 
+    def apply_boundaries(self):
+        """Ghost refresh, WC kinds (eulerian.py:371-433)."""
+        g = self.ghosts
+        if g is None:
+            return
+        ni, g0 = self.n_int, self.n_int
+        kind = np.asarray(g.kind)
+        src = np.asarray(g.src, dtype=np.int64)
+        vel = self.mom[:ni] / self.rho[:ni, None]
+        rho, mom = self.rho, self.mom
+        m = kind == 0
+        if np.any(m):
+            rho[g0:][m] = rho[src[m]]
+            mom[g0:][m] = mom[src[m]]
+        m = kind == 1
+        if np.any(m):
+            s, nrm = src[m], np.asarray(g.normal)[m]
+            vs = vel[s]
+            vg = vs - 2.0 * np.sum(vs * nrm, axis=1, keepdims=True) * nrm
+            rho[g0:][m] = rho[s]
+            mom[g0:][m] = rho[s, None] * vg
+        m = kind == 2
+        if np.any(m):
+            s = src[m]
+            rho[g0:][m] = rho[s]
+            mom[g0:][m] = rho[s, None] * np.asarray(g.wall_v)[m]
+        m = kind == 3
+        if np.any(m):
+            fx = np.asarray(g.fixed)[m]
+            rho[g0:][m] = fx[:, 0]
+            mom[g0:][m] = fx[:, 1:1 + self.d]
+        m = kind == 5
+        if np.any(m):
+            s, nrm = src[m], np.asarray(g.normal)[m]
+            lam = np.asarray(g.blend)[m][:, None]
+            vs = vel[s]
+            vn = np.sum(vs * nrm, axis=1, keepdims=True) * nrm
+            rho[g0:][m] = rho[s]
+            mom[g0:][m] = rho[s, None] * (vs - 2.0 * lam * vn)
+
     def rhs(self):
         p = self.c_art**2 * (self.rho - self.rho0)
         v = np.ascontiguousarray(self.mom / self.rho[:, None])
         drho = np.empty(self.n)
         dmom = np.zeros((self.n, self.d))
-        lib().orc_rhs_wc(self.n, self.d, _p(self.nl.starts), _p(self.nl.idx), _p(self.nl.e),
+        lib().orc_rhs_wc(self.n_int, self.d, _p(self.nl.starts), _p(self.nl.idx), _p(self.nl.e),
                          _p(self.gwv), _p(self.viscv), _p(self.rho), _p(v), _p(p), self.c_art,
                          self.mu, _p(drho), _p(dmom))
         return drho, dmom
 
     def compute_dt(self):
-        speed = self.c_art + np.linalg.norm(self.mom / self.rho[:, None], axis=1)
+        ni = self.n_int
+        speed = self.c_art + np.linalg.norm(self.mom[:ni] / self.rho[:ni, None], axis=1)
         return self.cfl * self.spec.h / float(speed.max())
 
     def step(self, dt=None):
+        """eulerian.py:610-643 (one substep, no retries)."""
         if dt is None:
             dt = self.compute_dt()
-        rho0, mom0 = self.rho.copy(), self.mom.copy()
+        ni = self.n_int
+        rho0, mom0 = self.rho[:ni].copy(), self.mom[:ni].copy()
+        self.apply_boundaries()
         drho, dmom = self.rhs()
-        self.rho = rho0 + 0.5 * dt * drho
-        self.mom = mom0 + 0.5 * dt * dmom
+        self.rho[:ni] = rho0 + 0.5 * dt * drho[:ni]
+        self.mom[:ni] = mom0 + 0.5 * dt * dmom[:ni]
+        self.apply_boundaries()
         drho, dmom = self.rhs()
-        self.rho = rho0 + dt * drho
-        self.mom = mom0 + dt * dmom
-        if not np.all(self.rho > 0.0):
+        self.rho[:ni] = rho0 + dt * drho[:ni]
+        self.mom[:ni] = mom0 + dt * dmom[:ni]
+        if not np.all(self.rho[:ni] > 0.0):
             raise RuntimeError("non-positive density")
         self.t += dt
         return dt

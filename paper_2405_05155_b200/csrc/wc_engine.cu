@@ -77,7 +77,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     blk = lane < full ? lane * per + k : full * per + (lane - full) * (per - 1) + k;
   }
   const int64_t i = P.row0 + (blk * blockDim.x + threadIdx.x) / G;
-  const bool active = i < P.row0 + P.nrows;
+  const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
   const double c = P.c_art;
   double dr = 0.0;
   double dm[D];
@@ -234,11 +234,11 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
 
 template <int D>
 __global__ void __launch_bounds__(256)
-k_speed_max(int64_t row0, int64_t nrows, double c, const double4* __restrict__ S,
-            double* __restrict__ scalars) {
+k_speed_max(int64_t row0, int64_t nrows, const int8_t* __restrict__ interior, double c,
+            const double4* __restrict__ S, double* __restrict__ scalars) {
   int64_t i = row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sp = 0.0;
-  if (i < row0 + nrows) {
+  if (i < row0 + nrows && (interior == nullptr || interior[i])) {
     double v[D], rho;
     unpack_s<D>(S[i], v, rho);
     sp = __dadd_rn(c, norm_exact<D>(v));
@@ -293,6 +293,57 @@ __global__ void k_wc_unpack(int64_t n, const int32_t* __restrict__ perm,
   const double c[4] = {mm.x, mm.y, mm.z, mm.w};
 #pragma unroll
   for (int a = 0; a < D; ++a) mom[i * D + a] = c[a];
+}
+
+// Ghost refresh (apply_boundaries, eulerian.py:371-447) for the WC kinds:
+// each ghost takes its interior source's state, with the velocity copied
+// (G_COPY), mirrored about the wall normal (G_MIRROR), set to the wall
+// velocity (G_WALL), prescribed (G_FIXED) or mirror-blended (G_BLEND_MIRROR);
+// momentum is formed as rho_src * v_ghost and the record stores mom / rho,
+// as FluidState.velocity would.  Indices are cell-sorted.
+template <int D>
+__global__ void k_wc_ghosts(int64_t ng, const int32_t* __restrict__ gs,
+                            const int32_t* __restrict__ ss, const int8_t* __restrict__ kind,
+                            const double* __restrict__ normal, const double* __restrict__ wall_v,
+                            const double* __restrict__ fixed, const double* __restrict__ blend,
+                            double4* S, int32_t* __restrict__ err) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  double vs[D], rho;
+  unpack_s<D>(S[ss[g]], vs, rho);
+  double mom[D], out_rho = rho;
+  const int k = kind[g];
+  if (k == 0) {                       // G_COPY
+#pragma unroll
+    for (int a = 0; a < D; ++a) mom[a] = rho * vs[a];
+    S[gs[g]] = S[ss[g]];
+    return;
+  } else if (k == 1 || k == 5) {      // G_MIRROR / G_BLEND_MIRROR
+    double dot = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) dot = __dadd_rn(dot, __dmul_rn(vs[a], normal[g * D + a]));
+    const double f = k == 1 ? __dmul_rn(2.0, dot) : __dmul_rn(2.0, blend[g]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double vg = k == 1 ? __dsub_rn(vs[a], __dmul_rn(f, normal[g * D + a]))
+                               : __dsub_rn(vs[a], __dmul_rn(f, __dmul_rn(dot, normal[g * D + a])));
+      mom[a] = __dmul_rn(rho, vg);
+    }
+  } else if (k == 2) {                // G_WALL
+#pragma unroll
+    for (int a = 0; a < D; ++a) mom[a] = __dmul_rn(rho, wall_v[g * D + a]);
+  } else if (k == 3) {                // G_FIXED
+    out_rho = fixed[g * (D + 2)];
+#pragma unroll
+    for (int a = 0; a < D; ++a) mom[a] = fixed[g * (D + 2) + 1 + a];
+  } else {                            // G_DMR_TOP needs the energy equation
+    atomicOr(err, SPHB_EFLAG_NONFINITE_STATE);
+    return;
+  }
+  double v[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = __ddiv_rn(mom[a], out_rho);
+  S[gs[g]] = pack_s<D>(v, out_rho);
 }
 
 }  // namespace
@@ -380,9 +431,9 @@ extern "C" int sphb_wc_speed_max(const sphb_wc_params* p, const double* s, doubl
   if (p->nrows <= 0) return SPHB_OK;
   const unsigned grid = sphb_blocks(p->nrows, 256);
   switch (p->dim) {
-    case 1: k_speed_max<1><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
-    case 2: k_speed_max<2><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
-    case 3: k_speed_max<3><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->c_art, S, scalars); break;
+    case 1: k_speed_max<1><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->interior, p->c_art, S, scalars); break;
+    case 2: k_speed_max<2><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->interior, p->c_art, S, scalars); break;
+    case 3: k_speed_max<3><<<grid, 256, 0, st>>>(p->row0, p->nrows, p->interior, p->c_art, S, scalars); break;
     default: return SPHB_ERR_ARG;
   }
   SPHB_LAUNCH_CHECK();
@@ -423,6 +474,24 @@ extern "C" int sphb_wc_unpack_state(int64_t n, int32_t dim, const int32_t* perm,
     case 1: k_wc_unpack<1><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
     case 2: k_wc_unpack<2><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
     case 3: k_wc_unpack<3><<<grid, 256, 0, st>>>(n, perm, (const double4*)s, (const double4*)m, rho, mom); break;
+    default: return SPHB_ERR_ARG;
+  }
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
+extern "C" int sphb_wc_ghosts(int32_t dim, int64_t ng, const int32_t* ghost_sorted,
+                              const int32_t* src_sorted, const int8_t* kind,
+                              const double* normal, const double* wall_v, const double* fixed,
+                              const double* blend, double* S, int32_t* err, void* stream) {
+  if (ng < 0) return SPHB_ERR_ARG;
+  if (ng == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(ng, 128);
+  switch (dim) {
+    case 1: k_wc_ghosts<1><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
+    case 2: k_wc_ghosts<2><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
+    case 3: k_wc_ghosts<3><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
     default: return SPHB_ERR_ARG;
   }
   SPHB_LAUNCH_CHECK();

@@ -32,7 +32,7 @@ k_wc_stage_geo(const sphb_wc_params P, const int stage, const int32_t* __restric
   const int64_t n = P.n;
   const int64_t W = P.width;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < P.row0 + P.nrows;
+  const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
   const double c_art = P.c_art;
   double speed = 0.0;
   int32_t flags = 0;

@@ -47,6 +47,29 @@ ETA_HLLC = 1.0
 ETA_LINEARIZED = 15.0   # eulerian.py:30
 
 
+# ghost-update kinds (eulerian.py:32-38)
+G_COPY = 0
+G_MIRROR = 1
+G_WALL = 2
+G_FIXED = 3
+G_DMR_TOP = 4
+G_BLEND_MIRROR = 5
+
+
+@dataclass
+class GhostLayer:
+    """Ghost bookkeeping (eulerian.py:354-363): per-ghost kind, interior
+    source, wall normal, wall velocity, prescribed conserved state."""
+
+    kind: np.ndarray
+    src: np.ndarray
+    normal: np.ndarray
+    wall_v: np.ndarray
+    fixed: np.ndarray
+    dmr: dict | None = None
+    blend: np.ndarray | None = None
+
+
 class SolverError(RuntimeError):
     """Raised when the solver state becomes invalid (exit code 2)."""
 
@@ -180,8 +203,10 @@ class EulerianSolver:
                  precision: str = "fp64", _slab=None, _grid=None, _dist=None):
         if mu < 0.0:
             raise ConfigError("viscosity must be non-negative")
-        if ghosts is not None:
-            raise NotImplementedError("ghost layers are outside the B200 hot path (SURVEY §8(f))")
+        if ghosts is not None and np.any(np.asarray(ghosts.kind) == G_DMR_TOP):
+            raise NotImplementedError("the DMR top boundary needs the ideal-gas solver")
+        if ghosts is not None and (_slab is not None or precision != "fp64"):
+            raise NotImplementedError("ghost layers with slab decomposition or FP32 mode")
         if eos.mode != WEAKLY_COMPRESSIBLE:
             raise NotImplementedError("the HLLC / ideal-gas solver is outside the hot path")
         if wall_force_tag is not None:
@@ -192,10 +217,12 @@ class EulerianSolver:
         self.pos = np.ascontiguousarray(positions, dtype=float)
         self.n, self.dim = self.pos.shape
         self.n_int = int(n_interior)
-        if self.n_int != self.n:
-            raise NotImplementedError("all particles must be interior without ghost layers")
+        if ghosts is None and self.n_int != self.n:
+            raise NotImplementedError("rows beyond n_interior need a ghost layer")
+        if ghosts is not None and np.asarray(ghosts.kind).shape[0] != self.n - self.n_int:
+            raise ConfigError("ghost layer size must equal n - n_interior")
         self.eos, self.kernel = eos, kernel
-        self.ghosts = None
+        self.ghosts = ghosts
         self.cfl, self.mu = float(cfl), float(mu)
         self.steps = 0
         self.retries = 0
@@ -242,6 +269,9 @@ class EulerianSolver:
         b = b.contiguous()
         if _slab is not None:       # halo rows take B from their owners
             _slab.exchange(_dist, [b])
+        self._ghost_setup(ghosts, dev)
+        if ghosts is not None:      # ghosts inherit their source's B (eulerian.py:499-501)
+            b[self._g_sorted.long()] = b[self._g_src_sorted.long()]
         self._B_sorted = b
         bs = 0.5 * (b + b.transpose(1, 2))
         # two planes: [n][4] {b00, b01, b02, b11} then [n][2] {b12, b22}
@@ -283,7 +313,7 @@ class EulerianSolver:
                       vol_s.contiguous().data_ptr(), ctypes.byref(k), self.geo.data_ptr(),
                       _lib.stream_ptr())
         self.plan = None
-        if variant == "tiled" and uniform and self.n and self.width:
+        if variant == "tiled" and uniform and self.n and self.width and ghosts is None:
             plan = TilePlan(self.bins, self.nbr, self.cnt, self.width,
                             fields=14 if self.dim == 3 else 12)
             if plan.ok:
@@ -295,6 +325,7 @@ class EulerianSolver:
                                                           int(uniform), self.width, self.n)
         p.row0, p.nrows = ((_slab.rows.start, _slab.rows.stop - _slab.rows.start)
                            if _slab is not None else (0, self.n))
+        p.interior = None if self._interior is None else self._interior.data_ptr()
         for a in range(3):
             p.box[a] = self.grid.box[a]
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
@@ -419,9 +450,52 @@ class EulerianSolver:
             self._nlist = NeighborList(starts, idx, r, e, cutoff=self.grid.cutoff, bins=self.bins)
         return self._nlist
 
+    # -- ghosts -------------------------------------------------------------
+    def _ghost_setup(self, ghosts, dev):
+        """Sorted ghost/source indices, per-ghost data and the interior mask."""
+        torch = _lib.torch_cuda()
+        self._interior = None
+        self._ng = 0
+        if ghosts is None:
+            return
+        ng = self.n - self.n_int
+        self._ng = ng
+        g_orig = torch.arange(self.n_int, self.n, device=dev)
+        src = _lib.to_device(np.asarray(ghosts.src, dtype=np.int64), torch.int64)
+        self._g_sorted = self.rank[g_orig].to(torch.int32).contiguous()
+        self._g_src_sorted = self.rank[src].to(torch.int32).contiguous()
+        self._g_kind = _lib.to_device(np.asarray(ghosts.kind, dtype=np.int8), torch.int8)
+        d = self.dim
+
+        def mat(a, width):
+            arr = np.zeros((ng, width)) if a is None else np.asarray(a, dtype=float)
+            out = np.zeros((ng, width))
+            out[:, :min(width, arr.shape[1])] = arr[:, :width]
+            return _lib.to_device(out, torch.float64)
+
+        self._g_normal = mat(ghosts.normal, d)
+        self._g_wall_v = mat(ghosts.wall_v, d)
+        self._g_fixed = mat(ghosts.fixed, d + 2)
+        blend = getattr(ghosts, "blend", None)
+        self._g_blend = _lib.to_device(np.zeros(ng) if blend is None
+                                       else np.asarray(blend, dtype=float), torch.float64)
+        self._interior = (self.perm < self.n_int).to(torch.int8).contiguous()
+
+    def _refresh_ghosts(self, S):
+        """apply_boundaries (eulerian.py:371-447) on a state record buffer."""
+        if self._ng:
+            _lib.call("sphb_wc_ghosts", self.dim, self._ng, self._g_sorted.data_ptr(),
+                      self._g_src_sorted.data_ptr(), self._g_kind.data_ptr(),
+                      self._g_normal.data_ptr(), self._g_wall_v.data_ptr(),
+                      self._g_fixed.data_ptr(), self._g_blend.data_ptr(), S.data_ptr(),
+                      self.err.data_ptr(), _lib.stream_ptr())
+
     # -- pieces -------------------------------------------------------------
     def apply_boundaries(self, t=None):
-        return None
+        """Refresh the ghost states from their interior sources (device)."""
+        self._sync_in()
+        self._refresh_ghosts(self.S)
+        self._state_host = None
 
     def _launch_stage(self, stage, s_in, s_n, m_n, s_out, m_out):
         if self.timer is not None:
@@ -499,6 +573,7 @@ class EulerianSolver:
         """(drho, dmom, None) of the current state, interior rows, caller order."""
         self._sync_in()
         out = torch_empty_like(self.S)
+        self._refresh_ghosts(self.S)
         self._launch_stage(0, self.S, self.S, self.M, out, None)
         self._check("NaN flux")
         drho = out[:, self.dim][self.rank].cpu().numpy()
@@ -517,8 +592,10 @@ class EulerianSolver:
         """One midpoint step into the *_nx buffers (no swap)."""
         _lib.call("sphb_set_dt", self._cfl_h, 0.0, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), _lib.stream_ptr())
+        self._refresh_ghosts(self.S)                 # apply_boundaries(t)
         self._launch_stage(1, self.S, self.S, self.M, self.S1, None)
         self._halo(self.S1)
+        self._refresh_ghosts(self.S1)                # apply_boundaries(t + dt/2)
         self._launch_stage(2, self.S1, self.S, self.M, self.S_nx, self.M_nx)
         self._halo(self.S_nx)
         self._reduce_speed()

@@ -179,6 +179,59 @@ def main():
         arrays["steps"] = np.array(nsteps)
         save(label, **arrays)
 
+    # ------------------------------- ghost layers, WC
+    from sph_trunc import cases
+
+    for label, sides_fn in (("cavity", lambda: {
+            "y+": cases.SideSpec(eulerian.G_WALL, wall_v=(1.0, 0.0)),
+            "y-": cases.SideSpec(eulerian.G_WALL), "x-": cases.SideSpec(eulerian.G_WALL),
+            "x+": cases.SideSpec(eulerian.G_WALL)}),
+                            ("mixed", lambda: {
+            "y+": cases.SideSpec(eulerian.G_WALL, wall_v=(0.5, 0.0)),
+            "y-": cases.SideSpec(eulerian.G_MIRROR),
+            "x-": cases.SideSpec(eulerian.G_FIXED, fixed=(1.002, 0.3, 0.05, 0.0)),
+            "x+": cases.SideSpec(eulerian.G_COPY)})):
+        arrays = {}
+        for key in ("1.6h", "2h"):
+            dp = 1.0 / 20
+            spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+            eos = eulerian.EosParams(eulerian.WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0)
+            interior, gpos, ghosts = cases.build_rect_case(
+                (0, 0), (1, 1), dp, spec.kappa * spec.h, sides_fn(), eos)
+            if label == "mixed":        # feather part of the mirror band (cases.py:408-413)
+                bottom = ghosts.kind == eulerian.G_MIRROR
+                ghosts.kind[bottom & (gpos[:, 0] > 0.5)] = eulerian.G_BLEND_MIRROR
+                ghosts.blend = np.clip(gpos[:, 0] - 0.4, 0.0, 1.0)
+            pos = np.vstack([interior, gpos])
+            n, ni = pos.shape[0], interior.shape[0]
+            rng = np.random.default_rng(5)
+            rho = 1.0 + 0.002 * rng.standard_normal(n)
+            mom = 0.05 * rng.standard_normal((n, 2))
+            state = eulerian.FluidState(vol=np.full(n, dp * dp), rho=rho.copy(), mom=mom.copy(),
+                                        etot=None, n_interior=ni)
+            solver = eulerian.EulerianSolver(pos, ni, state, eos, spec, ghosts, correction=True,
+                                             cfl=0.5, mu=0.0025)
+            tag = key.replace(".", "p")
+            if key == "1.6h":
+                arrays["pos"], arrays["n_int"] = pos, np.array(ni)
+                arrays["rho_init"], arrays["mom_init"] = rho, mom
+            arrays[f"{tag}__kind"] = ghosts.kind
+            arrays[f"{tag}__src"] = ghosts.src
+            arrays[f"{tag}__normal"] = ghosts.normal
+            arrays[f"{tag}__wall_v"] = ghosts.wall_v
+            arrays[f"{tag}__fixed"] = ghosts.fixed
+            arrays[f"{tag}__blend"] = (ghosts.blend if ghosts.blend is not None
+                                       else np.zeros(n - ni))
+            arrays[f"{tag}__pos"] = pos
+            dts = []
+            for s in range(1, 51):
+                dts.append(solver.step())
+                if s in (1, 50):
+                    arrays[f"{tag}__rho{s}"] = solver.state.rho[:ni].copy()
+                    arrays[f"{tag}__mom{s}"] = solver.state.mom[:ni].copy()
+            arrays[f"{tag}__dts"] = np.asarray(dts)
+        save(f"ghosts_{label}", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

@@ -429,3 +429,32 @@ def test_fp32_mode_error_is_small(label, builder, size):
         out[prec] = s.state
     assert l2_error(out["fp32"].mom, out["fp64"].mom) < 1e-4
     assert l2_error(out["fp32"].rho - 1.0, out["fp64"].rho - 1.0) < 1e-3
+
+
+@pytest.mark.parametrize("case", ["cavity", "mixed"])
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_wc_ghost_layers_vs_reference_golden(gold, case, key):
+    """ghost frames of cases.build_rect_case (wall, mirror,
+    blend-mirror, fixed, copy) refreshed on the device before every stage."""
+    from paper_2405_05155_b200.eulerian import GhostLayer
+
+    g = gold(f"ghosts_{case}")
+    tag = key.replace(".", "p")
+    pos, ni = g[f"{tag}__pos"], int(g["n_int"])
+    dp = 1.0 / 20
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    n = pos.shape[0]
+    ghosts = GhostLayer(kind=g[f"{tag}__kind"], src=g[f"{tag}__src"], normal=g[f"{tag}__normal"],
+                        wall_v=g[f"{tag}__wall_v"], fixed=g[f"{tag}__fixed"],
+                        blend=g[f"{tag}__blend"])
+    st = FluidState(np.full(n, dp * dp), g["rho_init"].copy(), g["mom_init"].copy(), None, ni)
+    s = EulerianSolver(pos, ni, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0), spec,
+                       ghosts, cfl=0.5, mu=0.0025)
+    dts = []
+    for k in range(1, 51):
+        dts.append(s.step())
+        if k in (1, 50):
+            tol = TOL_1 if k == 1 else TOL_100
+            assert l2_error(s.state.rho[:ni], g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(s.state.mom[:ni], g[f"{tag}__mom{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)

@@ -173,3 +173,33 @@ def test_oracle_c3_plate(gold, key):
             assert l2_error(s.x, g[f"{tag}__x{k}"]) < tol
             assert l2_error(s.v, g[f"{tag}__v{k}"]) < tol
             assert l2_error(s.F, g[f"{tag}__F{k}"]) < tol
+
+
+class _Ghosts:
+    def __init__(self, g, tag):
+        self.kind, self.src = g[f"{tag}__kind"], g[f"{tag}__src"]
+        self.normal, self.wall_v = g[f"{tag}__normal"], g[f"{tag}__wall_v"]
+        self.fixed, self.blend = g[f"{tag}__fixed"], g[f"{tag}__blend"]
+
+
+@pytest.mark.parametrize("case", ["cavity", "mixed"])
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_ghost_layers(gold, case, key):
+    """Ghost frames of cases.build_rect_case (wall / mirror / blend / fixed /
+    copy) through the oracle's apply_boundaries restatement."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    g = gold(f"ghosts_{case}")
+    tag = key.replace(".", "p")
+    pos, ni = g[f"{tag}__pos"], int(g["n_int"])
+    dp = 1.0 / 20
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    n = pos.shape[0]
+    s = O.EulerianWC(pos, np.full(n, dp * dp), g["rho_init"], g["mom_init"], spec, 10.0, 1.0,
+                     0.0025, 0.5, None, ghosts=_Ghosts(g, tag), n_int=ni)
+    for k in range(1, 51):
+        s.step()
+        if k in (1, 50):
+            tol = 1e-13 if k == 1 else 1e-10
+            assert l2_error(s.rho[:ni], g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(s.mom[:ni], g[f"{tag}__mom{k}"]) < tol

@@ -254,6 +254,7 @@ typedef struct sphb_wc_params {
   int32_t swizzle;       /* >0: SM count for the block->chunk L1-locality swizzle */
   int32_t reserved;
   const int8_t* interior; /* NULL, or 1 for rows to update (ghosts: 0), sorted */
+  double gamma;          /* ideal-gas ratio of specific heats (HLLC path)   */
 } sphb_wc_params;
 
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.
@@ -309,10 +310,45 @@ int sphb_wc_state_to_f32(int64_t n, int32_t dim, double rho0, const double* S, f
  * (copy, mirror, wall, fixed, blend-mirror): ghost record S[ghost_sorted[g]]
  * from its source S[src_sorted[g]].  normal/wall_v (ng, d), fixed (ng, d+2)
  * conserved {rho, mom, E}, blend (ng) (may be NULL without kind 5). */
+/* Copy 32-byte records at the given rows: d_k[rows[g]] = s_k[rows[g]] for
+ * each non-null pair (pair 0 required).  Used after the last stage to carry
+ * the ghost rows of apply_boundaries(t + dt/2) into the step's output, the
+ * state the reference's in-place arrays hold after EulerianSolver.step
+ * (eulerian.py:610-643). */
+int sphb_copy_records(int64_t nrows, const int32_t* rows, const double* s0, double* d0,
+                      const double* s1, double* d1, const double* s2, double* d2,
+                      void* stream);
+
 int sphb_wc_ghosts(int32_t dim, int64_t ng, const int32_t* ghost_sorted,
                    const int32_t* src_sorted, const int8_t* kind, const double* normal,
                    const double* wall_v, const double* fixed, const double* blend,
-                   double* S, int32_t* err, void* stream);
+                   double* S, double* M, int32_t* err, void* stream);
+
+/* Compressible path: limited HLLC flux + energy
+ * equation (eulerian.py:90-142, 269-338) over streamed geometry, ideal-gas
+ * EOS (:67-85).  Extra record Q [n][4] = {E, p, c, 0}.  Stage 0 writes
+ * {dmom, drho} to S_out and {dE, ...} to Q_out. */
+int sphb_hllc_stage(const sphb_wc_params* p, int32_t stage, const int32_t* nbr,
+                    const int32_t* cnt, const double* geo, const double* S_in,
+                    const double* Q_in, const double* S_n, const double* M_n,
+                    const double* Q_n, double* S_out, double* M_out, double* Q_out,
+                    double* scalars, int32_t* err, void* stream);
+int sphb_hllc_pack_state(int64_t n, int32_t dim, const int32_t* perm, const int8_t* interior,
+                         double gamma, const double* rho, const double* mom,
+                         const double* etot, double* S, double* M, double* Q,
+                         double* scalars, int32_t* err, void* stream);
+int sphb_hllc_unpack_state(int64_t n, int32_t dim, const int32_t* perm, const double* S,
+                           const double* M, const double* Q, double* rho, double* mom,
+                           double* etot, void* stream);
+/* Ghost refresh incl. the DMR top (kind 4; state post/pre by ghost x vs the
+ * shock foot x0 + (1 + 20 t)/tan60 at t = step start + t_shift dt). */
+int sphb_hllc_ghosts(int32_t dim, int64_t ng, const int32_t* ghost_sorted,
+                     const int32_t* src_sorted, const int8_t* kind, const double* normal,
+                     const double* wall_v, const double* fixed, const double* blend,
+                     const double* dmr_x, double dmr_x0, double dmr_tan,
+                     const double* dmr_post, const double* dmr_pre, double gamma,
+                     double t_shift, const double* scalars, double* S, double* M, double* Q,
+                     int32_t* err, void* stream);
 
 /* max(c + |v|) of a state into scalars[2] (initial dt / compute_dt()). */
 int sphb_wc_speed_max(const sphb_wc_params* p, const double* S, double* scalars,

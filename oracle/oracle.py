@@ -14,6 +14,7 @@ known value of the reference's own unit tests.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass
 
@@ -36,6 +37,7 @@ _SIGS = {
     "orc_moment_matrices": (None, [_I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _P]),
     "orc_pair_gradients": (None, [_I, _I, _P, _P, _P, _P, _I, _D, _D, _D, _P, _P]),
     "orc_rhs_wc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P]),
+    "orc_rhs_hllc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "orc_tl_accelerations": (None, [_I, _I, _P, _P, _P, _P, _D, _P]),
     "orc_tl_deformation_rates": (None, [_I, _I, _P, _P, _P, _P, _P, _P]),
     "orc_max_threads": (C.c_int, []),
@@ -310,6 +312,100 @@ class EulerianWC:
         self.mom[:ni] = mom0 + dt * dmom[:ni]
         if not np.all(self.rho[:ni] > 0.0):
             raise RuntimeError("non-positive density")
+        self.t += dt
+        return dt
+
+
+class EulerianHLLC(EulerianWC):
+    """EulerianSolver, ideal-gas branch (eulerian.py:67-85, 269-338, 371-447,
+    610-643): limited HLLC flux + energy, ghost kinds incl. the DMR top."""
+
+    def __init__(self, pos, vol, rho, mom, etot, spec, gamma, cfl=0.5, box=None,
+                 correction=True, ghosts=None, n_int=None):
+        super().__init__(pos, vol, rho, mom, spec, 1.0, 1.0, 0.0, cfl, box, correction, ghosts,
+                         n_int)
+        self.gamma = gamma
+        self.etot = np.array(etot, dtype=float)
+
+    def eos(self):
+        rho = self.rho
+        v2 = np.sum(self.mom**2, axis=-1) / rho**2
+        e = self.etot / rho - 0.5 * v2
+        if np.any(e < 0.0) or np.any(rho <= 0.0):
+            raise RuntimeError("negative internal energy")
+        p = rho * (self.gamma - 1.0) * e
+        return p, np.sqrt(self.gamma * p / rho)
+
+    def apply_boundaries(self, t=None):
+        g = self.ghosts
+        if g is None:
+            return
+        e0 = self.etot[self.n_int:].copy()
+        super().apply_boundaries()
+        ni, g0 = self.n_int, self.n_int
+        kind = np.asarray(g.kind)
+        src = np.asarray(g.src, dtype=np.int64)
+        rho, etot = self.rho, self.etot
+        etot[g0:] = e0
+        for k in (0, 1, 2):
+            m = kind == k
+            if np.any(m):
+                etot[g0:][m] = etot[src[m]]
+        m = kind == 3
+        if np.any(m):
+            etot[g0:][m] = np.asarray(g.fixed)[m, 1 + self.d]
+        m = kind == 5
+        if np.any(m):
+            s, nrm = src[m], np.asarray(g.normal)[m]
+            lam = np.asarray(g.blend)[m][:, None]
+            vs = self.mom[:ni][s] / rho[:ni][s][:, None]
+            vn = np.sum(vs * nrm, axis=1, keepdims=True) * nrm
+            vg = vs - 2.0 * lam * vn
+            etot[g0:][m] = etot[s] - 0.5 * rho[s] * (np.sum(vs**2, axis=1) - np.sum(vg**2, axis=1))
+        m = kind == 4
+        if np.any(m):
+            par = g.dmr
+            xs = par["x0"] + (1.0 + 20.0 * t) / math.tan(math.radians(60.0))
+            sel = (np.asarray(par["ghost_x"]) < xs).astype(float)[:, None]
+            full = sel * np.asarray(par["post"])[None, :] + (1.0 - sel) * np.asarray(par["pre"])[None, :]
+            rho[g0:][m] = full[:, 0]
+            self.mom[g0:][m] = full[:, 1:1 + self.d]
+            etot[g0:][m] = full[:, 1 + self.d]
+
+    def rhs(self):
+        p, c = self.eos()
+        v = np.ascontiguousarray(self.mom / self.rho[:, None])
+        drho = np.empty(self.n)
+        detot = np.empty(self.n)
+        dmom = np.zeros((self.n, self.d))
+        lib().orc_rhs_hllc(self.n_int, self.d, _p(self.nl.starts), _p(self.nl.idx),
+                           _p(self.nl.e), _p(self.gwv), _p(self.rho), _p(v),
+                           _p(np.ascontiguousarray(p)), _p(np.ascontiguousarray(c)),
+                           _p(self.etot), _p(drho), _p(dmom), _p(detot))
+        return drho, dmom, detot
+
+    def compute_dt(self):
+        _, c = self.eos()
+        ni = self.n_int
+        speed = c[:ni] + np.linalg.norm(self.mom[:ni] / self.rho[:ni, None], axis=1)
+        return self.cfl * self.spec.h / float(speed.max())
+
+    def step(self, dt=None):
+        if dt is None:
+            dt = self.compute_dt()
+        ni = self.n_int
+        r0, m0, e0 = self.rho[:ni].copy(), self.mom[:ni].copy(), self.etot[:ni].copy()
+        self.apply_boundaries(self.t)
+        drho, dmom, de = self.rhs()
+        self.rho[:ni] = r0 + 0.5 * dt * drho[:ni]
+        self.mom[:ni] = m0 + 0.5 * dt * dmom[:ni]
+        self.etot[:ni] = e0 + 0.5 * dt * de[:ni]
+        self.apply_boundaries(self.t + 0.5 * dt)
+        drho, dmom, de = self.rhs()
+        self.rho[:ni] = r0 + dt * drho[:ni]
+        self.mom[:ni] = m0 + dt * dmom[:ni]
+        self.etot[:ni] = e0 + dt * de[:ni]
+        self.eos()
         self.t += dt
         return dt
 

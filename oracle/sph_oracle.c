@@ -298,6 +298,92 @@ void orc_rhs_wc(int64_t n_int, int64_t d, const int64_t* starts, const int32_t* 
   }
 }
 
+/* _hllc_scalar (eulerian.py:90-142); out[10] as the reference tuple */
+static void orc_hllc_scalar(double rho_l, double u_l, double p_l, double c_l, double e_l,
+                            double rho_r, double u_r, double p_r, double c_r, double e_r,
+                            double eta, double* out) {
+  double s_l = u_l - c_l;
+  double s_r = u_r + c_r;
+  double den = rho_r * (s_r - u_r) + rho_l * (u_l - s_l);
+  double s_star = (rho_r * u_r * (s_r - u_r) + rho_l * u_l * (u_l - s_l) + p_l - p_r) / den;
+  if (!(s_l < s_star && s_star < s_r)) {
+    s_l = fmin(u_l - c_l, u_r - c_r);
+    s_r = fmax(u_l + c_l, u_r + c_r);
+    den = rho_r * (s_r - u_r) + rho_l * (u_l - s_l);
+    s_star = (rho_r * u_r * (s_r - u_r) + rho_l * u_l * (u_l - s_l) + p_l - p_r) / den;
+  }
+  double cbar = 0.5 * (c_l + c_r);
+  double du = u_l - u_r;
+  double beta = eta * du / cbar;
+  if (beta < 0.0) beta = 0.0;
+  else if (beta > 1.0) beta = 1.0;
+  double w_l = rho_l * (u_l - s_l);
+  double w_r = rho_r * (s_r - u_r);
+  double ws = w_l + w_r;
+  double u_star = (w_l * u_l + w_r * u_r) / ws + (p_l - p_r) * beta * beta / ws;
+  double p_star = 0.5 * (p_l + p_r) + 0.5 * beta * (w_r * (u_star - u_r) + w_l * (u_l - u_star));
+  double den_l = s_l - s_star;
+  double den_r = s_r - s_star;
+  out[0] = u_star;
+  out[1] = p_star;
+  out[2] = rho_l * (s_l - u_l) / den_l;
+  out[3] = rho_r * (s_r - u_r) / den_r;
+  out[4] = ((s_l - u_l) * e_l - p_l * u_l + p_star * s_star) / den_l;
+  out[5] = ((s_r - u_r) * e_r - p_r * u_r + p_star * s_star) / den_r;
+  out[6] = s_l;
+  out[7] = s_r;
+  out[8] = s_star;
+  out[9] = beta;
+}
+
+/* _rhs_hllc (eulerian.py:269-338); wall force omitted */
+void orc_rhs_hllc(int64_t n_int, int64_t d, const int64_t* starts, const int32_t* idx,
+                  const double* e, const double* gwv, const double* rho, const double* v,
+                  const double* p, const double* c, const double* etot, double* drho,
+                  double* dmom, double* detot) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n_int; ++i) {
+    double dr = 0.0, de = 0.0;
+    for (int64_t k = starts[i]; k < starts[i + 1]; ++k) {
+      const int64_t j = idx[k];
+      double u_l = 0.0, u_r = 0.0, out[10];
+      for (int64_t a = 0; a < d; ++a) {
+        u_l += v[i * d + a] * (-e[k * d + a]);
+        u_r += v[j * d + a] * (-e[k * d + a]);
+      }
+      orc_hllc_scalar(rho[i], u_l, p[i], c[i], etot[i], rho[j], u_r, p[j], c[j], etot[j], 1.0,
+                      out);
+      const double s_l = out[6], s_r = out[7];
+      double rho_s, e_s, p_use;
+      int star;
+      if (s_l > 0.0) {
+        rho_s = rho[i]; e_s = etot[i]; p_use = p[i]; star = 0;
+      } else if (s_r < 0.0) {
+        rho_s = rho[j]; e_s = etot[j]; p_use = p[j]; star = 0;
+      } else if (out[8] >= 0.0) {
+        rho_s = out[2]; e_s = out[4]; p_use = out[1]; star = 1;
+      } else {
+        rho_s = out[3]; e_s = out[5]; p_use = out[1]; star = 1;
+      }
+      const double u_star = out[0];
+      const double ubar = 0.5 * (u_l + u_r);
+      double s = 0.0, vs[3];
+      for (int64_t a = 0; a < d; ++a) {
+        if (star) vs[a] = (u_star - ubar) * (-e[k * d + a]) + 0.5 * (v[i * d + a] + v[j * d + a]);
+        else if (s_l > 0.0) vs[a] = v[i * d + a];
+        else vs[a] = v[j * d + a];
+        s += vs[a] * gwv[k * d + a];
+      }
+      dr += -2.0 * rho_s * s;
+      de += -2.0 * (e_s + p_use) * s;
+      for (int64_t a = 0; a < d; ++a)
+        dmom[i * d + a] += -2.0 * (rho_s * vs[a] * s + p_use * gwv[k * d + a]);
+    }
+    drho[i] = dr;
+    detot[i] = de;
+  }
+}
+
 /* _accelerations (tlsph.py:88-102) */
 void orc_tl_accelerations(int64_t n, int64_t d, const int64_t* starts, const int32_t* idx,
                           const double* g0, const double* q, double rho0, double* acc) {

@@ -79,6 +79,7 @@ class WCParams(C.Structure):
         ("swizzle", C.c_int32),
         ("reserved", C.c_int32),
         ("interior", C.c_void_p),
+        ("gamma", C.c_double),
     ]
 
 
@@ -133,7 +134,13 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
-    "sphb_wc_ghosts": (C.c_int, [I32, I64, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_copy_records": (C.c_int, [I64, P, P, P, P, P, P, P, P]),
+    "sphb_wc_ghosts": (C.c_int, [I32, I64, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_hllc_stage": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_hllc_pack_state": (C.c_int, [I64, I32, P, P, F64, P, P, P, P, P, P, P, P, P]),
+    "sphb_hllc_unpack_state": (C.c_int, [I64, I32, P, P, P, P, P, P, P, P]),
+    "sphb_hllc_ghosts": (C.c_int, [I32, I64, P, P, P, P, P, P, P, P, F64, F64, P, P, F64, F64,
+                                   P, P, P, P, P, P]),
     "sphb_wc_stage_f32": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_state_to_f32": (C.c_int, [I64, I32, F64, P, P, P]),
     "sphb_wc_geometry": (C.c_int, [P, I64, P, P, P, I32, P, P, P, P, P]),

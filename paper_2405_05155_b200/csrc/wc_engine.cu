@@ -306,7 +306,7 @@ __global__ void k_wc_ghosts(int64_t ng, const int32_t* __restrict__ gs,
                             const int32_t* __restrict__ ss, const int8_t* __restrict__ kind,
                             const double* __restrict__ normal, const double* __restrict__ wall_v,
                             const double* __restrict__ fixed, const double* __restrict__ blend,
-                            double4* S, int32_t* __restrict__ err) {
+                            double4* S, double4* __restrict__ M, int32_t* __restrict__ err) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ng) return;
   double vs[D], rho;
@@ -315,9 +315,8 @@ __global__ void k_wc_ghosts(int64_t ng, const int32_t* __restrict__ gs,
   const int k = kind[g];
   if (k == 0) {                       // G_COPY
 #pragma unroll
-    for (int a = 0; a < D; ++a) mom[a] = rho * vs[a];
+    for (int a = 0; a < D; ++a) mom[a] = __dmul_rn(rho, vs[a]);
     S[gs[g]] = S[ss[g]];
-    return;
   } else if (k == 1 || k == 5) {      // G_MIRROR / G_BLEND_MIRROR
     double dot = 0.0;
 #pragma unroll
@@ -340,10 +339,18 @@ __global__ void k_wc_ghosts(int64_t ng, const int32_t* __restrict__ gs,
     atomicOr(err, SPHB_EFLAG_NONFINITE_STATE);
     return;
   }
-  double v[D];
+  if (k != 0) {
+    double v[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) v[a] = __ddiv_rn(mom[a], out_rho);
-  S[gs[g]] = pack_s<D>(v, out_rho);
+    for (int a = 0; a < D; ++a) v[a] = __ddiv_rn(mom[a], out_rho);
+    S[gs[g]] = pack_s<D>(v, out_rho);
+  }
+  if (M) {
+    double mc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) mc[a] = mom[a];
+    M[gs[g]] = make_double4(mc[0], mc[1], mc[2], mc[3]);
+  }
 }
 
 }  // namespace
@@ -480,18 +487,48 @@ extern "C" int sphb_wc_unpack_state(int64_t n, int32_t dim, const int32_t* perm,
   return SPHB_OK;
 }
 
+// Ghost rows of the last stage's input -> the step's output (up to three
+// 32-byte record arrays), so a state read after step() shows the ghost frame
+// of apply_boundaries(t + dt/2), as the reference's in-place arrays do.
+__global__ void k_copy_records(int64_t nrows, const int32_t* __restrict__ rows,
+                               const double4* __restrict__ s0, double4* __restrict__ d0,
+                               const double4* __restrict__ s1, double4* __restrict__ d1,
+                               const double4* __restrict__ s2, double4* __restrict__ d2) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nrows) return;
+  const int64_t r = rows[g];
+  d0[r] = s0[r];
+  if (d1) d1[r] = s1[r];
+  if (d2) d2[r] = s2[r];
+}
+
+extern "C" int sphb_copy_records(int64_t nrows, const int32_t* rows, const double* s0, double* d0,
+                                 const double* s1, double* d1, const double* s2, double* d2,
+                                 void* stream) {
+  if (nrows < 0 || (nrows > 0 && (rows == nullptr || s0 == nullptr || d0 == nullptr)) ||
+      ((s1 == nullptr) != (d1 == nullptr)) || ((s2 == nullptr) != (d2 == nullptr)))
+    return SPHB_ERR_ARG;
+  if (nrows == 0) return SPHB_OK;
+  k_copy_records<<<sphb_blocks(nrows, 128), 128, 0, (cudaStream_t)stream>>>(
+      nrows, rows, (const double4*)s0, (double4*)d0, (const double4*)s1, (double4*)d1,
+      (const double4*)s2, (double4*)d2);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
 extern "C" int sphb_wc_ghosts(int32_t dim, int64_t ng, const int32_t* ghost_sorted,
                               const int32_t* src_sorted, const int8_t* kind,
                               const double* normal, const double* wall_v, const double* fixed,
-                              const double* blend, double* S, int32_t* err, void* stream) {
+                              const double* blend, double* S, double* M, int32_t* err,
+                              void* stream) {
   if (ng < 0) return SPHB_ERR_ARG;
   if (ng == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = sphb_blocks(ng, 128);
   switch (dim) {
-    case 1: k_wc_ghosts<1><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
-    case 2: k_wc_ghosts<2><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
-    case 3: k_wc_ghosts<3><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, err); break;
+    case 1: k_wc_ghosts<1><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, (double4*)M, err); break;
+    case 2: k_wc_ghosts<2><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, (double4*)M, err); break;
+    case 3: k_wc_ghosts<3><<<grid, 128, 0, st>>>(ng, ghost_sorted, src_sorted, kind, normal, wall_v, fixed, blend, (double4*)S, (double4*)M, err); break;
     default: return SPHB_ERR_ARG;
   }
   SPHB_LAUNCH_CHECK();

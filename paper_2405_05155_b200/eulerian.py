@@ -203,12 +203,14 @@ class EulerianSolver:
                  precision: str = "fp64", _slab=None, _grid=None, _dist=None):
         if mu < 0.0:
             raise ConfigError("viscosity must be non-negative")
-        if ghosts is not None and np.any(np.asarray(ghosts.kind) == G_DMR_TOP):
-            raise NotImplementedError("the DMR top boundary needs the ideal-gas solver")
+        self._ideal = eos.mode == IDEAL_GAS
+        if (ghosts is not None and np.any(np.asarray(ghosts.kind) == G_DMR_TOP)
+                and not self._ideal):
+            raise ConfigError("the DMR top boundary needs the ideal-gas EOS")
         if ghosts is not None and (_slab is not None or precision != "fp64"):
             raise NotImplementedError("ghost layers with slab decomposition or FP32 mode")
-        if eos.mode != WEAKLY_COMPRESSIBLE:
-            raise NotImplementedError("the HLLC / ideal-gas solver is outside the hot path")
+        if self._ideal and (_slab is not None or precision != "fp64"):
+            raise NotImplementedError("the HLLC path runs in FP64 on one GPU")
         if wall_force_tag is not None:
             raise NotImplementedError("wall-force tagging is outside the hot path")
         if kernel.code != CODE_WENDLAND:
@@ -300,7 +302,7 @@ class EulerianSolver:
         #          (2d+1) doubles per pair, reference arithmetic without FMA:
         #          the closest reproduction of the reference's roundings);
         #   tiled  shared-memory staging variant of `global`.
-        variant = os.environ.get("SPHB_WC_KERNEL", "global")
+        variant = "geo" if self._ideal else os.environ.get("SPHB_WC_KERNEL", "global")
         geo_bytes = (2 * self.dim + 1) * self.width * self.n * 8
         self.variant = variant
         self.geo = None
@@ -326,6 +328,7 @@ class EulerianSolver:
         p.row0, p.nrows = ((_slab.rows.start, _slab.rows.stop - _slab.rows.start)
                            if _slab is not None else (0, self.n))
         p.interior = None if self._interior is None else self._interior.data_ptr()
+        p.gamma = eos.gamma
         for a in range(3):
             p.box[a] = self.grid.box[a]
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
@@ -362,7 +365,17 @@ class EulerianSolver:
         self._mom_io = torch.empty((self.n, self.dim), dtype=torch.float64, device=dev)
         self._vol_host = vol
         self.timer = None   # optional list collecting (stage, start_event, end_event)
+        self._init_extra(dev)
         self.set_state(state)
+
+    def __new__(cls, *args, **kwargs):
+        eos = kwargs.get("eos", args[3] if len(args) > 3 else None)
+        if cls is EulerianSolver and eos is not None and eos.mode == IDEAL_GAS:
+            return super().__new__(_HLLCSolver)
+        return super().__new__(cls)
+
+    def _init_extra(self, dev):
+        return None
 
     # -- state transfer -----------------------------------------------------
     def set_state(self, state: FluidState) -> None:
@@ -481,20 +494,22 @@ class EulerianSolver:
                                        else np.asarray(blend, dtype=float), torch.float64)
         self._interior = (self.perm < self.n_int).to(torch.int8).contiguous()
 
-    def _refresh_ghosts(self, S):
-        """apply_boundaries (eulerian.py:371-447) on a state record buffer."""
+    def _refresh_ghosts(self, S, M=None):
+        """apply_boundaries (eulerian.py:371-447) on a state record buffer;
+        the ghost momenta go to M when given."""
         if self._ng:
             _lib.call("sphb_wc_ghosts", self.dim, self._ng, self._g_sorted.data_ptr(),
                       self._g_src_sorted.data_ptr(), self._g_kind.data_ptr(),
                       self._g_normal.data_ptr(), self._g_wall_v.data_ptr(),
                       self._g_fixed.data_ptr(), self._g_blend.data_ptr(), S.data_ptr(),
-                      self.err.data_ptr(), _lib.stream_ptr())
+                      None if M is None else M.data_ptr(), self.err.data_ptr(),
+                      _lib.stream_ptr())
 
     # -- pieces -------------------------------------------------------------
     def apply_boundaries(self, t=None):
         """Refresh the ghost states from their interior sources (device)."""
         self._sync_in()
-        self._refresh_ghosts(self.S)
+        self._refresh_ghosts(self.S, self.M)
         self._state_host = None
 
     def _launch_stage(self, stage, s_in, s_n, m_n, s_out, m_out):
@@ -573,7 +588,8 @@ class EulerianSolver:
         """(drho, dmom, None) of the current state, interior rows, caller order."""
         self._sync_in()
         out = torch_empty_like(self.S)
-        self._refresh_ghosts(self.S)
+        # like the reference, rhs() reads the ghost rows as they stand;
+        # apply_boundaries() / step() refresh them
         self._launch_stage(0, self.S, self.S, self.M, out, None)
         self._check("NaN flux")
         drho = out[:, self.dim][self.rank].cpu().numpy()
@@ -595,8 +611,14 @@ class EulerianSolver:
         self._refresh_ghosts(self.S)                 # apply_boundaries(t)
         self._launch_stage(1, self.S, self.S, self.M, self.S1, None)
         self._halo(self.S1)
-        self._refresh_ghosts(self.S1)                # apply_boundaries(t + dt/2)
+        # apply_boundaries(t + dt/2); stage 2 leaves ghost rows of M_nx alone,
+        # so their momenta land there directly
+        self._refresh_ghosts(self.S1, self.M_nx)
         self._launch_stage(2, self.S1, self.S, self.M, self.S_nx, self.M_nx)
+        if self._ng:                                 # ghost rows stay as of t + dt/2
+            _lib.call("sphb_copy_records", self._ng, self._g_sorted.data_ptr(),
+                      self.S1.data_ptr(), self.S_nx.data_ptr(), None, None, None, None,
+                      _lib.stream_ptr())
         self._halo(self.S_nx)
         self._reduce_speed()
 
@@ -616,6 +638,7 @@ class EulerianSolver:
         remaining = dt
         while advanced < dt - 1e-15 * dt:
             sub = min(remaining, dt - advanced)
+            self.scalars[1] = self._t_host          # device time at the substep start
             self._substeps(sub)
             err = self._global_err()
             if err:
@@ -650,7 +673,7 @@ class EulerianSolver:
             return
         self._sync_in()
         dto = 0.0 if dt is None else float(dt)
-        self.scalars[1] = 0.0
+        self.scalars[1] = self._t_host                  # absolute device time
         if graph is None:
             graph = n_steps >= 8 and self._slab is None and self.timer is None
         done = 0
@@ -666,7 +689,7 @@ class EulerianSolver:
         if err:
             self.err.zero_()
             raise SolverError(f"advance({n_steps}): {_describe(err)} (after step {self.steps})")
-        self._t_host += float(self.scalars[1].item())
+        self._t_host = float(self.scalars[1].item())
         self.steps += n_steps
         self._state_host = None
 
@@ -694,6 +717,143 @@ class EulerianSolver:
         w = st.vol[:self.n_int]
         return (float(np.sum(w * st.rho[:self.n_int])),
                 (w[:, None] * st.mom[:self.n_int]).sum(axis=0), None)
+
+
+class _HLLCSolver(EulerianSolver):
+    """Ideal-gas branch of EulerianSolver: limited HLLC
+    flux with the energy equation (eulerian.py:90-142, 269-338), ideal-gas
+    EOS (:67-85) and the ghost kinds incl. the DMR top (:371-447), on the
+    device (csrc/hllc.cu) over the streamed reference geometry.  Created by
+    EulerianSolver(...) when eos.mode == "ideal-gas"."""
+
+    def _init_extra(self, dev):
+        torch = _lib.torch_cuda()
+        self.Q = torch.empty((self.n, 4), dtype=torch.float64, device=dev)
+        self.Q1 = torch.empty_like(self.Q)
+        self.Q_nx = torch.empty_like(self.Q)
+        self.M1 = torch.empty_like(self.M)
+        self._E_io = torch.empty(self.n, dtype=torch.float64, device=dev)
+        g = self.ghosts
+        self._dmr = None
+        if g is not None and getattr(g, "dmr", None) is not None:
+            ng = self.n - self.n_int
+            kind = np.asarray(g.kind)
+            gx = np.full(ng, np.nan)
+            gx[kind == G_DMR_TOP] = np.asarray(g.dmr["ghost_x"], dtype=float)
+            self._dmr = (_lib.to_device(gx, torch.float64), float(g.dmr["x0"]),
+                         math.tan(math.radians(60.0)),
+                         _lib.to_device(np.asarray(g.dmr["post"], dtype=float), torch.float64),
+                         _lib.to_device(np.asarray(g.dmr["pre"], dtype=float), torch.float64))
+
+    def set_state(self, state: FluidState) -> None:
+        if state.etot is None:
+            raise ConfigError("ideal-gas EOS needs momentum and total energy")
+        self.load_state(np.asarray(state.rho, dtype=float), np.asarray(state.mom, dtype=float),
+                        np.asarray(state.etot, dtype=float))
+
+    def load_state(self, rho, mom, etot=None) -> None:
+        torch = _lib.torch_cuda()
+        rho_d = _lib.to_device(rho, torch.float64)
+        mom_d = _lib.to_device(mom, torch.float64).reshape(self.n, self.dim)
+        e_d = _lib.to_device(etot, torch.float64)
+        _lib.call("sphb_hllc_pack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+                  _lib.ptr(self._interior), self.eos.gamma, rho_d.data_ptr(), mom_d.data_ptr(),
+                  e_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(), self.Q.data_ptr(),
+                  self.scalars.data_ptr(), self.err.data_ptr(), _lib.stream_ptr())
+        self._check("negative internal energy")
+        self._state_host = None
+
+    def read_state(self, rho_out, mom_out, etot_out=None) -> None:
+        _lib.call("sphb_hllc_unpack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+                  self.S.data_ptr(), self.M.data_ptr(), self.Q.data_ptr(),
+                  self._rho_io.data_ptr(), self._mom_io.data_ptr(), self._E_io.data_ptr(),
+                  _lib.stream_ptr())
+        rho_out.copy_(self._rho_io, non_blocking=True)
+        mom_out.reshape(self.n, self.dim).copy_(self._mom_io, non_blocking=True)
+        if etot_out is not None:
+            etot_out.copy_(self._E_io, non_blocking=True)
+
+    @property
+    def state(self) -> FluidState:
+        self._handed_out = True
+        if self._state_host is None:
+            torch = _lib.torch_cuda()
+            rho = torch.empty(self.n, dtype=torch.float64)
+            mom = torch.empty((self.n, self.dim), dtype=torch.float64)
+            etot = torch.empty(self.n, dtype=torch.float64)
+            self.read_state(rho, mom, etot)
+            torch.cuda.current_stream().synchronize()
+            self._state_host = FluidState(vol=self._vol_host.copy(), rho=rho.numpy(),
+                                          mom=mom.numpy(), etot=etot.numpy(),
+                                          n_interior=self.n_int)
+        return self._state_host
+
+    def _refresh_speed(self):
+        st = self.state
+        self.load_state(st.rho, st.mom, st.etot)
+
+    def _ghosts3(self, S, M, Q, t_shift):
+        if not self._ng:
+            return
+        d = self._dmr
+        _lib.call("sphb_hllc_ghosts", self.dim, self._ng, self._g_sorted.data_ptr(),
+                  self._g_src_sorted.data_ptr(), self._g_kind.data_ptr(),
+                  self._g_normal.data_ptr(), self._g_wall_v.data_ptr(),
+                  self._g_fixed.data_ptr(), self._g_blend.data_ptr(),
+                  None if d is None else d[0].data_ptr(), 0.0 if d is None else d[1],
+                  1.0 if d is None else d[2], None if d is None else d[3].data_ptr(),
+                  None if d is None else d[4].data_ptr(), self.eos.gamma, t_shift,
+                  self.scalars.data_ptr(), S.data_ptr(), M.data_ptr(), Q.data_ptr(),
+                  self.err.data_ptr(), _lib.stream_ptr())
+
+    def _hllc(self, stage, s_in, q_in, s_out, m_out, q_out):
+        _lib.call("sphb_hllc_stage", ctypes.byref(self.params), stage, self.nbr.data_ptr(),
+                  self.cnt.data_ptr(), self.geo.data_ptr(), s_in.data_ptr(), q_in.data_ptr(),
+                  self.S.data_ptr(), self.M.data_ptr(), self.Q.data_ptr(), s_out.data_ptr(),
+                  None if m_out is None else m_out.data_ptr(), q_out.data_ptr(),
+                  self.scalars.data_ptr(), self.err.data_ptr(), _lib.stream_ptr())
+
+    def apply_boundaries(self, t=None):
+        self._sync_in()
+        if t is not None:
+            self.scalars[0] = 0.0
+            self.scalars[1] = float(t)
+        self._ghosts3(self.S, self.M, self.Q, 0.0)
+        self._state_host = None
+
+    def rhs(self):
+        """(drho, dmom, detot) of the current state (eulerian.py:532-551)."""
+        self._sync_in()
+        torch = _lib.torch_cuda()
+        out, outq = torch.empty_like(self.S), torch.empty_like(self.Q)
+        self._hllc(0, self.S, self.Q, out, None, outq)
+        self._check("NaN flux")
+        return (out[:, self.dim][self.rank].cpu().numpy(),
+                out[:, :self.dim][self.rank].cpu().numpy(), outq[:, 0][self.rank].cpu().numpy())
+
+    def _substeps(self, dt_override: float) -> None:
+        _lib.call("sphb_set_dt", self._cfl_h, 0.0, dt_override, self.scalars.data_ptr(),
+                  self.err.data_ptr(), _lib.stream_ptr())
+        self._ghosts3(self.S, self.M, self.Q, 0.0)              # apply_boundaries(t)
+        self._hllc(1, self.S, self.Q, self.S1, self.M1, self.Q1)
+        self._ghosts3(self.S1, self.M1, self.Q1, 0.5)           # apply_boundaries(t + dt/2)
+        self._hllc(2, self.S1, self.Q1, self.S_nx, self.M_nx, self.Q_nx)
+        if self._ng:                                 # ghost rows stay as of t + dt/2
+            _lib.call("sphb_copy_records", self._ng, self._g_sorted.data_ptr(),
+                      self.S1.data_ptr(), self.S_nx.data_ptr(), self.M1.data_ptr(),
+                      self.M_nx.data_ptr(), self.Q1.data_ptr(), self.Q_nx.data_ptr(),
+                      _lib.stream_ptr())
+
+    def _swap(self):
+        super()._swap()
+        self.Q, self.Q_nx = self.Q_nx, self.Q
+
+    def totals(self):
+        st = self.state
+        w = st.vol[:self.n_int]
+        return (float(np.sum(w * st.rho[:self.n_int])),
+                (w[:, None] * st.mom[:self.n_int]).sum(axis=0),
+                float(np.sum(w * st.etot[:self.n_int])))
 
 
 def torch_empty_like(t):

@@ -232,6 +232,44 @@ def main():
             arrays[f"{tag}__dts"] = np.asarray(dts)
         save(f"ghosts_{label}", **arrays)
 
+    # ------------------------------ HLLC + DMR
+    arrays = {}
+    for key in ("1.6h", "2h"):
+        cfg = cases.CaseConfig(name="dmr-golden", case="dmr", solver="euler-hllc", dp=1.0 / 16,
+                               t_end=0.2, kernel_family=configs.FAMILY[key], h_ratio=1.3,
+                               cfl=0.5, correction=True)
+        case = cases.build_dmr(cfg)
+        solver = case.solver
+        st = solver.state
+        tag = key.replace(".", "p")
+        g = solver.ghosts
+        arrays[f"{tag}__pos"] = solver.pos
+        arrays[f"{tag}__n_int"] = np.array(solver.n_int)
+        arrays[f"{tag}__rho_init"] = st.rho.copy()
+        arrays[f"{tag}__mom_init"] = st.mom.copy()
+        arrays[f"{tag}__etot_init"] = st.etot.copy()
+        for f in ("kind", "src", "normal", "wall_v", "fixed", "blend"):
+            arrays[f"{tag}__{f}"] = getattr(g, f)
+        arrays[f"{tag}__dmr_x0"] = np.array(g.dmr["x0"])
+        arrays[f"{tag}__dmr_ghost_x"] = g.dmr["ghost_x"]
+        arrays[f"{tag}__dmr_post"] = g.dmr["post"]
+        arrays[f"{tag}__dmr_pre"] = g.dmr["pre"]
+        drho, dmom, de = solver.rhs()
+        # rhs() returns the solver's own buffers: copy before stepping reuses them
+        arrays[f"{tag}__drho0"], arrays[f"{tag}__dmom0"], arrays[f"{tag}__de0"] = (
+            drho.copy(), dmom.copy(), de.copy())
+        dts = []
+        for s_ in range(1, 21):
+            dts.append(solver.step())
+            if s_ in (1, 20):
+                ni = solver.n_int
+                arrays[f"{tag}__rho{s_}"] = solver.state.rho[:ni].copy()
+                arrays[f"{tag}__mom{s_}"] = solver.state.mom[:ni].copy()
+                arrays[f"{tag}__etot{s_}"] = solver.state.etot[:ni].copy()
+        arrays[f"{tag}__dts"] = np.asarray(dts)
+        arrays[f"{tag}__retries"] = np.array(solver.retries)
+    save("hllc_dmr", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

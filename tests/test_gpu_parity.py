@@ -458,3 +458,80 @@ def test_wc_ghost_layers_vs_reference_golden(gold, case, key):
             assert l2_error(s.state.rho[:ni], g[f"{tag}__rho{k}"]) < tol
             assert l2_error(s.state.mom[:ni], g[f"{tag}__mom{k}"]) < tol
     np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+
+
+def _dmr_solver(g, tag, key):
+    from paper_2405_05155_b200.eulerian import IDEAL_GAS, GhostLayer
+
+    dp = 1.0 / 16
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    pos, ni = g[f"{tag}__pos"], int(g[f"{tag}__n_int"])
+    n = pos.shape[0]
+    ghosts = GhostLayer(kind=g[f"{tag}__kind"], src=g[f"{tag}__src"], normal=g[f"{tag}__normal"],
+                        wall_v=g[f"{tag}__wall_v"], fixed=g[f"{tag}__fixed"],
+                        blend=g[f"{tag}__blend"],
+                        dmr={"x0": float(g[f"{tag}__dmr_x0"]),
+                             "ghost_x": g[f"{tag}__dmr_ghost_x"],
+                             "post": g[f"{tag}__dmr_post"], "pre": g[f"{tag}__dmr_pre"]})
+    st = FluidState(np.full(n, dp * dp), g[f"{tag}__rho_init"].copy(),
+                    g[f"{tag}__mom_init"].copy(), g[f"{tag}__etot_init"].copy(), ni)
+    return EulerianSolver(pos, ni, st, EosParams(IDEAL_GAS, gamma=1.4), spec, ghosts, cfl=0.5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_hllc_dmr_vs_reference_golden(gold, key):
+    """limited HLLC flux + energy equation + ideal-gas EOS
+    with the double-Mach-reflection ghost frame (time-dependent DMR top,
+    feathered bottom mirror, fixed inflow, copy outflow), 20 CFL steps."""
+    g = gold("hllc_dmr")
+    tag = key.replace(".", "p")
+    s = _dmr_solver(g, tag, key)
+    ni = s.n_int
+    drho, dmom, de = s.rhs()
+    assert l2_error(drho[:ni], g[f"{tag}__drho0"][:ni]) < TOL_1
+    assert l2_error(dmom[:ni], g[f"{tag}__dmom0"][:ni]) < TOL_1
+    assert l2_error(de[:ni], g[f"{tag}__de0"][:ni]) < TOL_1
+    dts = []
+    for k in range(1, 21):
+        dts.append(s.step())
+        if k in (1, 20):
+            tol = TOL_1 if k == 1 else TOL_100
+            st = s.state
+            assert l2_error(st.rho[:ni], g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(st.mom[:ni], g[f"{tag}__mom{k}"]) < tol
+            assert l2_error(st.etot[:ni], g[f"{tag}__etot{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+    m, p, e = s.totals()
+    assert np.isfinite(m) and np.isfinite(e)
+
+
+@pytest.mark.gpu
+def test_hllc_dmr_graph_advance_matches_step(gold):
+    """advance() (CUDA-graph replay, device-side t and dt) == 20 x step()."""
+    g = gold("hllc_dmr")
+    s = _dmr_solver(g, "1p6h", "1.6h")
+    s.advance(20, graph=True)
+    ni = s.n_int
+    st = s.state
+    assert l2_error(st.rho[:ni], g["1p6h__rho20"]) < TOL_100
+    assert l2_error(st.etot[:ni], g["1p6h__etot20"]) < TOL_100
+    assert abs(s.t - float(np.sum(g["1p6h__dts"]))) < 1e-12
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+@pytest.mark.gpu
+def test_hllc_dmr_vs_oracle(gold, key):
+    """Device HLLC path vs the oracle restatement on the same inputs."""
+    from test_oracle_golden import oracle_dmr
+
+    g = gold("hllc_dmr")
+    tag = key.replace(".", "p")
+    s = _dmr_solver(g, tag, key)
+    o = oracle_dmr(g, tag, key)
+    ni = s.n_int
+    for _ in range(5):
+        assert s.step() == pytest.approx(o.step(), rel=1e-13)
+    st = s.state
+    assert l2_error(st.rho[:ni], o.rho[:ni]) < 1e-11
+    assert l2_error(st.etot[:ni], o.etot[:ni]) < 1e-11

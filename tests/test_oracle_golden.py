@@ -203,3 +203,46 @@ def test_oracle_ghost_layers(gold, case, key):
             tol = 1e-13 if k == 1 else 1e-10
             assert l2_error(s.rho[:ni], g[f"{tag}__rho{k}"]) < tol
             assert l2_error(s.mom[:ni], g[f"{tag}__mom{k}"]) < tol
+
+
+class _DmrGhosts(_Ghosts):
+    def __init__(self, g, tag):
+        super().__init__(g, tag)
+        self.dmr = {"x0": float(g[f"{tag}__dmr_x0"]), "ghost_x": g[f"{tag}__dmr_ghost_x"],
+                    "post": g[f"{tag}__dmr_post"], "pre": g[f"{tag}__dmr_pre"]}
+
+
+def oracle_dmr(g, tag, key):
+    """cases.build_dmr at dp = 1/16 through the oracle's HLLC restatement."""
+    dp = 1.0 / 16
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    pos = g[f"{tag}__pos"]
+    n = pos.shape[0]
+    return O.EulerianHLLC(pos, np.full(n, dp * dp), g[f"{tag}__rho_init"], g[f"{tag}__mom_init"],
+                          g[f"{tag}__etot_init"], spec, 1.4, 0.5, None,
+                          ghosts=_DmrGhosts(g, tag), n_int=int(g[f"{tag}__n_int"]))
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_hllc_dmr(gold, key):
+    """Compressible HLLC + energy with the double-Mach-reflection ghost frame
+    (eulerian.py:269-338 flux, 610-643 boundaries; cases.py build_dmr)."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    g = gold("hllc_dmr")
+    tag = key.replace(".", "p")
+    s = oracle_dmr(g, tag, key)
+    ni = s.n_int
+    drho, dmom, de = s.rhs()     # initial ghost states, as built (no boundary pass yet)
+    assert l2_error(drho[:ni], g[f"{tag}__drho0"][:ni]) < 1e-13
+    assert l2_error(dmom[:ni], g[f"{tag}__dmom0"][:ni]) < 1e-13
+    assert l2_error(de[:ni], g[f"{tag}__de0"][:ni]) < 1e-13
+    dts = []
+    for k in range(1, 21):
+        dts.append(s.step())
+        if k in (1, 20):
+            tol = 1e-13 if k == 1 else 1e-10
+            assert l2_error(s.rho[:ni], g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(s.mom[:ni], g[f"{tag}__mom{k}"]) < tol
+            assert l2_error(s.etot[:ni], g[f"{tag}__etot{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-10)

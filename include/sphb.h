@@ -255,6 +255,12 @@ typedef struct sphb_wc_params {
   int32_t reserved;
   const int8_t* interior; /* NULL, or 1 for rows to update (ghosts: 0), sorted */
   double gamma;          /* ideal-gas ratio of specific heats (HLLC path)   */
+  /* wall-force diagnostic (eulerian.py:225-264, 515-519, 605-606): NULL, or
+   * per sorted row 1 for particles whose pair forces count; stages 0 and 2
+   * zero wall_force[dim] and accumulate -sum of the momentum flux over pairs
+   * (i interior, j tagged).  sphb_wc_stage and sphb_hllc_stage only. */
+  const int8_t* wall_tag;
+  double* wall_force;
 } sphb_wc_params;
 
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.
@@ -310,6 +316,13 @@ int sphb_wc_state_to_f32(int64_t n, int32_t dim, double rho0, const double* S, f
  * (copy, mirror, wall, fixed, blend-mirror): ghost record S[ghost_sorted[g]]
  * from its source S[src_sorted[g]].  normal/wall_v (ng, d), fixed (ng, d+2)
  * conserved {rho, mom, E}, blend (ng) (may be NULL without kind 5). */
+/* Append (t = scalars[1], scale * wall_force[0..dim)) as row count[0] of
+ * log [cap][1 + dim] and increment count[0] (rows past cap are counted but
+ * not written): EulerianSolver.step's wall_force_series entry
+ * (eulerian.py:605-606) recorded on the device. */
+int sphb_wall_record(int32_t dim, const double* wall_force, const double* scalars,
+                     double scale, double* log, int64_t* count, int64_t cap, void* stream);
+
 /* Copy 32-byte records at the given rows: d_k[rows[g]] = s_k[rows[g]] for
  * each non-null pair (pair 0 required).  Used after the last stage to carry
  * the ghost rows of apply_boundaries(t + dt/2) into the step's output, the

@@ -36,7 +36,7 @@ _SIGS = {
     "orc_pressure_accel": (None, [_I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _D, _D, _P]),
     "orc_moment_matrices": (None, [_I, _I, _P, _P, _P, _P, _P, _I, _D, _D, _D, _P]),
     "orc_pair_gradients": (None, [_I, _I, _P, _P, _P, _P, _I, _D, _D, _D, _P, _P]),
-    "orc_rhs_wc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P]),
+    "orc_rhs_wc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
     "orc_rhs_hllc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "orc_tl_accelerations": (None, [_I, _I, _P, _P, _P, _P, _D, _P]),
     "orc_tl_deformation_rates": (None, [_I, _I, _P, _P, _P, _P, _P, _P]),
@@ -218,10 +218,11 @@ def relax_steps(pos, spec, box, dp, n_updates, p0=1.0, rho0=1.0, step_scale=0.2)
 
 # ------------------------------------------------------------ WC Eulerian
 class EulerianWC:
-    """EulerianSolver, WC branch, periodic, no ghosts (eulerian.py:473-643)."""
+    """EulerianSolver, WC branch (eulerian.py:473-643): periodic or with a
+    ghost frame, optional wall-force tags (:515-519, 605-606)."""
 
     def __init__(self, pos, vol, rho, mom, spec, c_art, rho0=1.0, mu=0.0, cfl=0.5, box=None,
-                 correction=True, ghosts=None, n_int=None):
+                 correction=True, ghosts=None, n_int=None, wall_tag=None):
         self.spec, self.c_art, self.rho0, self.mu, self.cfl = spec, c_art, rho0, mu, cfl
         self.nl = build_neighbors(pos, spec.kappa * spec.h, box)
         self.vol = np.asarray(vol, dtype=float)
@@ -240,6 +241,12 @@ class EulerianWC:
         dw = np.where(q <= spec.kappa, (spec.alpha / spec.h) * _profile_deriv(spec.code, q), 0.0)
         self.viscv = np.ascontiguousarray(2.0 * dw / self.nl.r * self.vol[self.nl.idx])
         self.t = 0.0
+        self.wall_tag = None
+        if wall_tag is not None:
+            self.wall_tag = np.zeros(self.n, dtype=np.int8)
+            self.wall_tag[np.asarray(wall_tag, dtype=np.int64)] = 1
+        self.wall_force = np.zeros(self.d)
+        self.wall_force_series = []
 
     def apply_boundaries(self):
         """Ghost refresh, WC kinds (eulerian.py:371-433)."""
@@ -286,9 +293,12 @@ class EulerianWC:
         v = np.ascontiguousarray(self.mom / self.rho[:, None])
         drho = np.empty(self.n)
         dmom = np.zeros((self.n, self.d))
+        wf = None if self.wall_tag is None else np.empty((self.n_int, self.d))
         lib().orc_rhs_wc(self.n_int, self.d, _p(self.nl.starts), _p(self.nl.idx), _p(self.nl.e),
                          _p(self.gwv), _p(self.viscv), _p(self.rho), _p(v), _p(p), self.c_art,
-                         self.mu, _p(drho), _p(dmom))
+                         self.mu, _p(drho), _p(dmom), _p(self.wall_tag), _p(wf))
+        if wf is not None:
+            self.wall_force = wf.sum(axis=0)
         return drho, dmom
 
     def compute_dt(self):
@@ -313,6 +323,7 @@ class EulerianWC:
         if not np.all(self.rho[:ni] > 0.0):
             raise RuntimeError("non-positive density")
         self.t += dt
+        self.wall_force_series.append((self.t, self.wall_force * self.vol[0]))
         return dt
 
 

@@ -259,11 +259,13 @@ void orc_pair_gradients(int64_t n, int64_t d, const int64_t* starts, const int32
 void orc_rhs_wc(int64_t n_int, int64_t d, const int64_t* starts, const int32_t* idx,
                 const double* e, const double* gwv, const double* viscv, const double* rho,
                 const double* v, const double* p, double c_art, double mu, double* drho,
-                double* dmom) {
+                double* dmom, const int8_t* wall_tag, double* wf_rows) {
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n_int; ++i) {
     const double rho_i = rho[i], p_i = p[i];
     double dr = 0.0;
+    if (wf_rows)
+      for (int64_t a = 0; a < d; ++a) wf_rows[i * d + a] = 0.0;
     for (int64_t k = starts[i]; k < starts[i + 1]; ++k) {
       const int64_t j = idx[k];
       double u_l = 0.0, u_r = 0.0;
@@ -292,6 +294,8 @@ void orc_rhs_wc(int64_t n_int, int64_t d, const int64_t* starts, const int32_t* 
         double fm = -2.0 * (rbar * vs * s + p_star * gwv[k * d + a]) +
                     mu * viscv[k] * (v[i * d + a] - v[j * d + a]);
         dmom[i * d + a] += fm;
+        /* eulerian.py:263-264, per row; summed over rows by the caller */
+        if (wall_tag && wall_tag[j]) wf_rows[i * d + a] -= fm;
       }
     }
     drho[i] = dr;

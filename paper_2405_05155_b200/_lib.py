@@ -80,6 +80,8 @@ class WCParams(C.Structure):
         ("reserved", C.c_int32),
         ("interior", C.c_void_p),
         ("gamma", C.c_double),
+        ("wall_tag", C.c_void_p),
+        ("wall_force", C.c_void_p),
     ]
 
 
@@ -134,6 +136,7 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_wall_record": (C.c_int, [I32, P, P, F64, P, P, I64, P]),
     "sphb_copy_records": (C.c_int, [I64, P, P, P, P, P, P, P, P]),
     "sphb_wc_ghosts": (C.c_int, [I32, I64, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_hllc_stage": (C.c_int, [P, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),

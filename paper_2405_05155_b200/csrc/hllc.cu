@@ -96,9 +96,10 @@ k_hllc_stage(const sphb_wc_params P, const int stage, const int32_t* __restrict_
     const double4 qi = Q_in[i];
     const double E_i = qi.x, p_i = qi.y, c_i = qi.z;
     double dr = 0.0, de = 0.0;
-    double dm[D];
+    double dm[D], wf[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) dm[a] = 0.0;
+    for (int a = 0; a < D; ++a) dm[a] = wf[a] = 0.0;
+    const bool track = P.wall_tag != nullptr && stage != 1;
     const int32_t m = cnt[i];
     for (int32_t k = 0; k < m; ++k) {
       const int64_t slot = (int64_t)k * n + i;
@@ -142,8 +143,18 @@ k_hllc_stage(const sphb_wc_params P, const int stage, const int32_t* __restrict_
       }
       dr += -2.0 * rho_s * s;
       de += -2.0 * (e_s + p_use) * s;
+      const bool tagged = track && P.wall_tag[j] != 0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) dm[a] += -2.0 * (rho_s * vs[a] * s + p_use * gwv[a]);
+      for (int a = 0; a < D; ++a) {
+        const double fm = -2.0 * (rho_s * vs[a] * s + p_use * gwv[a]);
+        dm[a] += fm;
+        if (tagged) wf[a] -= fm;              // eulerian.py:333-335
+      }
+    }
+    if (track) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        if (wf[a] != 0.0) atomicAdd(P.wall_force + a, wf[a]);
     }
     bool finite = isfinite(dr) && isfinite(de);
 #pragma unroll
@@ -344,9 +355,13 @@ extern "C" int sphb_hllc_stage(const sphb_wc_params* p, int32_t stage, const int
                                const double* q_in, const double* s_n, const double* m_n,
                                const double* q_n, double* s_out, double* m_out, double* q_out,
                                double* scalars, int32_t* err, void* stream) {
-  if (!p || p->n < 0 || stage < 0 || stage > 2 || !(p->gamma > 1.0)) return SPHB_ERR_ARG;
-  if (p->nrows <= 0) return SPHB_OK;
+  if (!p || p->n < 0 || stage < 0 || stage > 2 || !(p->gamma > 1.0) ||
+      (p->wall_tag && !p->wall_force))
+    return SPHB_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->wall_tag && stage != 1)
+    SPHB_CUDA_CHECK(cudaMemsetAsync(p->wall_force, 0, sizeof(double) * p->dim, st));
+  if (p->nrows <= 0) return SPHB_OK;
   const int dim = p->dim;
   HLLC_D(k_hllc_stage, sphb_blocks(p->nrows, kThreads), *p, stage, nbr, cnt, geo,
          (const double4*)s_in, (const double4*)q_in, (const double4*)s_n, (const double4*)m_n,

@@ -54,7 +54,7 @@ inline WCConst wc_const(const sphb_wc_params& p) {
 // mostly consecutive particles of one cell, so the G neighbour records share
 // cache lines and a warp's gathers need ~G-times fewer L1 wavefronts than
 // one-thread-per-particle.  Partial sums are combined with warp shuffles.
-template <int D, int G, int MINB>
+template <int D, int G, int MINB, bool WALL>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
            const double4* __restrict__ X, const double* __restrict__ B,
@@ -80,9 +80,9 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
   const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
   const double c = P.c_art;
   double dr = 0.0;
-  double dm[D];
+  double dm[D], wf[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) dm[a] = 0.0;
+  for (int a = 0; a < D; ++a) dm[a] = wf[a] = 0.0;
   if (active) {
     // host-folded constants (kernel parameters live in the constant bank, so
     // the FP64 instructions read them as operands instead of registers)
@@ -173,7 +173,19 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
         const double fm = fma(rs2, vs[a], ps2 * g[a]);
         dm[a] = fma(-mvisc, dv[a], dm[a] + fm);
       }
+      if constexpr (WALL) {               // eulerian.py:262-264
+        if (stage != 1 && P.wall_tag[j]) {
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+            wf[a] -= fma(-mvisc, dv[a], fma(rs2, vs[a], ps2 * g[a]));
+        }
+      }
     }
+  }
+  if constexpr (WALL) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      if (wf[a] != 0.0) atomicAdd(P.wall_force + a, wf[a]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) {
@@ -391,10 +403,27 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
-#define SPHB_STAGE(D, G, MB)                                                               \
-  k_wc_stage<D, G, MB><<<sphb_blocks(p->nrows * G, kThreads), kThreads, 0, st>>>(              \
+#define SPHB_STAGE_W(D, G, MB, W)                                                          \
+  k_wc_stage<D, G, MB, W><<<sphb_blocks(p->nrows * G, kThreads), kThreads, 0, st>>>(          \
       *p, K, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                \
   break
+#define SPHB_STAGE(D, G, MB) SPHB_STAGE_W(D, G, MB, false)
+  if (p->wall_tag) {
+    if (!p->wall_force) return SPHB_ERR_ARG;
+    if (stage != 1) SPHB_CUDA_CHECK(cudaMemsetAsync(p->wall_force, 0, sizeof(double) * p->dim, st));
+    switch (p->dim * 16 + group) {
+      case 16 + 1: SPHB_STAGE_W(1, 1, 4, true);
+      case 32 + 1: SPHB_STAGE_W(2, 1, 4, true);
+      case 32 + 2: SPHB_STAGE_W(2, 2, 4, true);
+      case 32 + 4: SPHB_STAGE_W(2, 4, 4, true);
+      case 48 + 1: SPHB_STAGE_W(3, 1, 4, true);
+      case 48 + 2: SPHB_STAGE_W(3, 2, 4, true);
+      case 48 + 4: SPHB_STAGE_W(3, 4, 4, true);
+      default: return SPHB_ERR_ARG;
+    }
+    SPHB_LAUNCH_CHECK();
+    return SPHB_OK;
+  }
   // SPHB_WC_MINB (tuning): 4 -> <=128 registers, 6 -> <=80, 8 -> <=64
   static int minb = [] {
     const char* e = getenv("SPHB_WC_MINB");
@@ -424,6 +453,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
     default: return SPHB_ERR_ARG;
   }
 #undef SPHB_STAGE
+#undef SPHB_STAGE_W
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }
@@ -500,6 +530,32 @@ __global__ void k_copy_records(int64_t nrows, const int32_t* __restrict__ rows,
   d0[r] = s0[r];
   if (d1) d1[r] = s1[r];
   if (d2) d2[r] = s2[r];
+}
+
+// wall_force_series entry (eulerian.py:605-606) appended on the device, so
+// graph-replayed steps keep the per-step series without a host round trip.
+__global__ void k_wall_record(int32_t dim, const double* __restrict__ wf,
+                              const double* __restrict__ scalars, double scale,
+                              double* __restrict__ log, int64_t* __restrict__ count,
+                              int64_t cap) {
+  const int64_t k = count[0];
+  if (k < cap) {
+    double* row = log + k * (1 + dim);
+    row[0] = scalars[1];
+    for (int a = 0; a < dim; ++a) row[1 + a] = wf[a] * scale;
+  }
+  count[0] = k + 1;
+}
+
+extern "C" int sphb_wall_record(int32_t dim, const double* wall_force, const double* scalars,
+                                double scale, double* log, int64_t* count, int64_t cap,
+                                void* stream) {
+  if (dim < 1 || dim > 3 || !wall_force || !scalars || !log || !count || cap < 0)
+    return SPHB_ERR_ARG;
+  k_wall_record<<<1, 1, 0, (cudaStream_t)stream>>>(dim, wall_force, scalars, scale, log, count,
+                                                   cap);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
 }
 
 extern "C" int sphb_copy_records(int64_t nrows, const int32_t* rows, const double* s0, double* d0,

@@ -211,8 +211,8 @@ class EulerianSolver:
             raise NotImplementedError("ghost layers with slab decomposition or FP32 mode")
         if self._ideal and (_slab is not None or precision != "fp64"):
             raise NotImplementedError("the HLLC path runs in FP64 on one GPU")
-        if wall_force_tag is not None:
-            raise NotImplementedError("wall-force tagging is outside the hot path")
+        if wall_force_tag is not None and (_slab is not None or precision != "fp64"):
+            raise NotImplementedError("wall-force tagging runs in FP64 on one GPU")
         if kernel.code != CODE_WENDLAND:
             raise NotImplementedError("the WC engine evaluates the Wendland family")
         torch = _lib.torch_cuda()
@@ -329,6 +329,21 @@ class EulerianSolver:
                            if _slab is not None else (0, self.n))
         p.interior = None if self._interior is None else self._interior.data_ptr()
         p.gamma = eos.gamma
+        # wall-force diagnostic (eulerian.py:515-519): tags in sorted order,
+        # the force vector accumulated on the device by stages 0 and 2
+        self._wf_dev = None
+        self._wf_log = None
+        if wall_force_tag is not None:
+            if variant != "global" and not self._ideal:
+                raise NotImplementedError("wall-force tagging runs in the global WC kernel")
+            tag = np.zeros(self.n, dtype=np.int8)
+            tag[np.asarray(wall_force_tag, dtype=np.int64)] = 1
+            perm = self.bins.perm.cpu().numpy()
+            self._wall_tag = _lib.to_device(np.ascontiguousarray(tag[perm]), torch.int8)
+            self._wf_dev = torch.zeros(3, dtype=torch.float64, device=dev)
+            self._wf_count = torch.zeros(1, dtype=torch.int64, device=dev)
+            p.wall_tag = self._wall_tag.data_ptr()
+            p.wall_force = self._wf_dev.data_ptr()
         for a in range(3):
             p.box[a] = self.grid.box[a]
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
@@ -592,6 +607,7 @@ class EulerianSolver:
         # apply_boundaries() / step() refresh them
         self._launch_stage(0, self.S, self.S, self.M, out, None)
         self._check("NaN flux")
+        self._pull_wall_force()
         drho = out[:, self.dim][self.rank].cpu().numpy()
         dmom = out[:, :self.dim][self.rank].cpu().numpy()
         return drho, dmom, None
@@ -655,9 +671,32 @@ class EulerianSolver:
             self._t_host += sub
             advanced += sub
         self._state_host = None
+        self._pull_wall_force()
         self.wall_force_series.append((self._t_host, self.wall_force * self._vol_host[0]))
         self.steps += 1
         return dt
+
+    def _pull_wall_force(self):
+        if self._wf_dev is not None:
+            self.wall_force = self._wf_dev[:self.dim].cpu().numpy()
+
+    def _record_wall_force(self):
+        """Per-step wall_force_series entry, appended on the device (advance)."""
+        if self._wf_dev is not None:
+            _lib.call("sphb_wall_record", self.dim, self._wf_dev.data_ptr(),
+                      self.scalars.data_ptr(), float(self._vol_host[0]),
+                      self._wf_log.data_ptr(), self._wf_count.data_ptr(),
+                      self._wf_log.shape[0], _lib.stream_ptr())
+
+    def _drain_wall_force(self):
+        if self._wf_dev is None:
+            return
+        k = int(self._wf_count.item())
+        rows = self._wf_log[:min(k, self._wf_log.shape[0])].cpu().numpy()
+        for r in rows:
+            self.wall_force_series.append((float(r[0]), r[1:].copy()))
+        self._wf_count.zero_()
+        self._pull_wall_force()
 
     def advance(self, n_steps: int, dt: float | None = None, *, graph: bool | None = None) -> None:
         """n_steps CFL (or fixed-dt) steps with no host synchronisation.
@@ -676,6 +715,11 @@ class EulerianSolver:
         self.scalars[1] = self._t_host                  # absolute device time
         if graph is None:
             graph = n_steps >= 8 and self._slab is None and self.timer is None
+        if self._wf_dev is not None and (self._wf_log is None or self._wf_log.shape[0] < n_steps):
+            torch = _lib.torch_cuda()
+            self._wf_log = torch.zeros((max(n_steps, 64), 1 + self.dim), dtype=torch.float64,
+                                       device=self._dev)
+            self._graphs = None                         # captured the old log pointer
         done = 0
         if graph:
             g = self._step_graph(dto)
@@ -685,6 +729,7 @@ class EulerianSolver:
         for _ in range(n_steps - done):
             self._substeps(dto)
             self._swap()
+            self._record_wall_force()
         err = self._global_err()
         if err:
             self.err.zero_()
@@ -692,6 +737,7 @@ class EulerianSolver:
         self._t_host = float(self.scalars[1].item())
         self.steps += n_steps
         self._state_host = None
+        self._drain_wall_force()
 
     def _step_graph(self, dt_override: float):
         """CUDA graph of two consecutive steps (the buffer swap returns to the
@@ -707,6 +753,7 @@ class EulerianSolver:
                 for _ in range(2):
                     self._substeps(dt_override)
                     self._swap()
+                    self._record_wall_force()
             torch.cuda.synchronize()
             self._graphs[dt_override] = g
         return g
@@ -828,6 +875,7 @@ class _HLLCSolver(EulerianSolver):
         out, outq = torch.empty_like(self.S), torch.empty_like(self.Q)
         self._hllc(0, self.S, self.Q, out, None, outq)
         self._check("NaN flux")
+        self._pull_wall_force()
         return (out[:, self.dim][self.rank].cpu().numpy(),
                 out[:, :self.dim][self.rank].cpu().numpy(), outq[:, 0][self.rank].cpu().numpy())
 

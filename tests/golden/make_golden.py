@@ -270,6 +270,39 @@ def main():
         arrays[f"{tag}__retries"] = np.array(solver.retries)
     save("hllc_dmr", **arrays)
 
+    # ------------------ cylinder: wall ghosts + wall-force series (§8(f) rank 1)
+    arrays = {}
+    for key in ("1.6h", "2h"):
+        cfg = cases.CaseConfig(name="cyl-golden", case="cylinder", solver="euler-wc", dp=0.1,
+                               t_end=1.0, kernel_family=configs.FAMILY[key], h_ratio=1.3,
+                               cfl=0.5, correction=True,
+                               physics={"u_inf": 1.0, "rho0": 1.0, "re": 20.0},
+                               geometry={"diameter": 1.0, "extent": (5.0, 3.0),
+                                         "center": (1.5, 1.5)})
+        solver = cases.build_cylinder(cfg).solver
+        st = solver.state
+        tag = key.replace(".", "p")
+        g = solver.ghosts
+        arrays[f"{tag}__pos"] = solver.pos
+        arrays[f"{tag}__n_int"] = np.array(solver.n_int)
+        arrays[f"{tag}__mu"] = np.array(solver.mu)
+        arrays[f"{tag}__wall_tag"] = np.nonzero(solver.wall_tag)[0]
+        arrays[f"{tag}__rho_init"] = st.rho.copy()
+        arrays[f"{tag}__mom_init"] = st.mom.copy()
+        for f in ("kind", "src", "normal", "wall_v", "fixed"):
+            arrays[f"{tag}__{f}"] = getattr(g, f)
+        dts = []
+        for s_ in range(1, 31):
+            dts.append(solver.step())
+            if s_ in (1, 30):
+                ni = solver.n_int
+                arrays[f"{tag}__rho{s_}"] = solver.state.rho[:ni].copy()
+                arrays[f"{tag}__mom{s_}"] = solver.state.mom[:ni].copy()
+        arrays[f"{tag}__dts"] = np.asarray(dts)
+        arrays[f"{tag}__wf_t"] = np.array([t for t, _ in solver.wall_force_series])
+        arrays[f"{tag}__wf"] = np.array([w for _, w in solver.wall_force_series])
+    save("cylinder", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

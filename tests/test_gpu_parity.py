@@ -535,3 +535,56 @@ def test_hllc_dmr_vs_oracle(gold, key):
     st = s.state
     assert l2_error(st.rho[:ni], o.rho[:ni]) < 1e-11
     assert l2_error(st.etot[:ni], o.etot[:ni]) < 1e-11
+
+
+def _cylinder_solver(g, tag, key):
+    from paper_2405_05155_b200.eulerian import GhostLayer
+
+    dp = 0.1
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    pos, ni = g[f"{tag}__pos"], int(g[f"{tag}__n_int"])
+    n = pos.shape[0]
+    ghosts = GhostLayer(kind=g[f"{tag}__kind"], src=g[f"{tag}__src"], normal=g[f"{tag}__normal"],
+                        wall_v=g[f"{tag}__wall_v"], fixed=g[f"{tag}__fixed"])
+    st = FluidState(np.full(n, dp * dp), g[f"{tag}__rho_init"].copy(),
+                    g[f"{tag}__mom_init"].copy(), None, ni)
+    return EulerianSolver(pos, ni, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0), spec,
+                          ghosts, cfl=0.5, mu=float(g[f"{tag}__mu"]),
+                          wall_force_tag=g[f"{tag}__wall_tag"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_cylinder_wall_force_vs_reference_golden(gold, key):
+    """SURVEY §8(f) rank 1, cylinder: G_WALL ghosts inside the body, fixed far
+    field, and the per-step wall-force series accumulated on the device."""
+    g = gold("cylinder")
+    tag = key.replace(".", "p")
+    s = _cylinder_solver(g, tag, key)
+    ni = s.n_int
+    dts = []
+    for k in range(1, 31):
+        dts.append(s.step())
+        if k in (1, 30):
+            tol = TOL_1 if k == 1 else TOL_100
+            assert l2_error(s.state.rho[:ni], g[f"{tag}__rho{k}"]) < tol
+            assert l2_error(s.state.mom[:ni], g[f"{tag}__mom{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+    np.testing.assert_allclose([t for t, _ in s.wall_force_series], g[f"{tag}__wf_t"],
+                               rtol=1e-12)
+    wf = np.array([w for _, w in s.wall_force_series])
+    assert l2_error(wf, g[f"{tag}__wf"]) < TOL_100
+
+
+@pytest.mark.gpu
+def test_cylinder_wall_force_graph_advance(gold):
+    """advance() records the wall-force series on the device across graph
+    replays; same series as 30 x step()."""
+    g = gold("cylinder")
+    s = _cylinder_solver(g, "1p6h", "1.6h")
+    s.advance(30, graph=True)
+    assert len(s.wall_force_series) == 30
+    np.testing.assert_allclose([t for t, _ in s.wall_force_series], g["1p6h__wf_t"], rtol=1e-12)
+    wf = np.array([w for _, w in s.wall_force_series])
+    assert l2_error(wf, g["1p6h__wf"]) < TOL_100
+    assert l2_error(s.state.rho[:s.n_int], g["1p6h__rho30"]) < TOL_100

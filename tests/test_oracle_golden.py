@@ -246,3 +246,42 @@ def test_oracle_hllc_dmr(gold, key):
             assert l2_error(s.mom[:ni], g[f"{tag}__mom{k}"]) < tol
             assert l2_error(s.etot[:ni], g[f"{tag}__etot{k}"]) < tol
     np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-10)
+
+
+def oracle_cylinder(g, tag, key):
+    """cases.build_cylinder (reduced: D = 1, 5 x 3 box, dp = 0.1, Re 20)."""
+    dp = 0.1
+    spec = kernel_spec(configs.FAMILY[key], 1.3 * dp, 2)
+    pos = g[f"{tag}__pos"]
+    n = pos.shape[0]
+    return O.EulerianWC(pos, np.full(n, dp * dp), g[f"{tag}__rho_init"], g[f"{tag}__mom_init"],
+                        spec, 10.0, 1.0, float(g[f"{tag}__mu"]), 0.5, None,
+                        ghosts=_CylGhosts(g, tag), n_int=int(g[f"{tag}__n_int"]),
+                        wall_tag=g[f"{tag}__wall_tag"])
+
+
+class _CylGhosts(_Ghosts):
+    def __init__(self, g, tag):
+        self.kind, self.src = g[f"{tag}__kind"], g[f"{tag}__src"]
+        self.normal, self.wall_v = g[f"{tag}__normal"], g[f"{tag}__wall_v"]
+        self.fixed, self.blend = g[f"{tag}__fixed"], None
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_cylinder_wall_force(gold, key):
+    """Flow past a cylinder: in-body wall ghosts (G_WALL, KD-tree mirrored
+    sources), fixed far field, and the wall-force series (eulerian.py:262-264,
+    605-606) that the drag/lift coefficients come from."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    g = gold("cylinder")
+    tag = key.replace(".", "p")
+    s = oracle_cylinder(g, tag, key)
+    ni = s.n_int
+    dts = [s.step() for _ in range(30)]
+    assert l2_error(s.rho[:ni], g[f"{tag}__rho30"]) < 1e-10
+    assert l2_error(s.mom[:ni], g[f"{tag}__mom30"]) < 1e-10
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-12)
+    wf = np.array([w for _, w in s.wall_force_series])
+    np.testing.assert_allclose([t for t, _ in s.wall_force_series], g[f"{tag}__wf_t"], rtol=1e-12)
+    assert l2_error(wf, g[f"{tag}__wf"]) < 1e-10

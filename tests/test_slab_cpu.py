@@ -48,7 +48,7 @@ def _oracle_rhs(nl, gwv, viscv, rho, mom, c, rho0, mu):
     dmom = np.zeros((nl.n, mom.shape[1]))
     O.lib().orc_rhs_wc(nl.n, mom.shape[1], O._p(nl.starts), O._p(nl.idx), O._p(nl.e), O._p(gwv),
                        O._p(viscv), O._p(np.ascontiguousarray(rho)), O._p(v), O._p(p), c, mu,
-                       O._p(drho), O._p(dmom))
+                       O._p(drho), O._p(dmom), None, None)
     return drho, dmom
 
 

@@ -93,6 +93,19 @@ typedef struct sphb_kernel {
   double kappa;
 } sphb_kernel;
 
+/* Signed-distance shape (geometry.py:16-134): kind 1 circle/ball
+ * (center, radius), 2 axis-aligned rectangle/box (lo, hi), 3 half disk
+ * (center, radius, normal = outward unit normal of the flat face). */
+typedef struct sphb_shape {
+  int32_t kind;
+  int32_t dim;
+  double center[3];
+  double radius;
+  double lo[3];
+  double hi[3];
+  double normal[3];
+} sphb_shape;
+
 const char* sphb_version(void);
 const char* sphb_last_cuda_error(void);
 int sphb_device_count(void);
@@ -322,6 +335,26 @@ int sphb_wc_state_to_f32(int64_t n, int32_t dim, double rho0, const double* S, f
  * (eulerian.py:605-606) recorded on the device. */
 int sphb_wall_record(int32_t dim, const double* wall_force, const double* scalars,
                      double scale, double* log, int64_t* count, int64_t cap, void* stream);
+
+/* ---- shape-bounded relaxation (relaxation.py:92-198) */
+/* sd[i] = signed distance of x[i] (NULL: skipped); grad[i] = unit outward
+ * gradient by central differences, eps 1e-7 (geometry.py:129-147). */
+int sphb_shape_sdf(const sphb_shape* s, int64_t n, const double* x, double* sd, double* grad,
+                   void* stream);
+/* Wall confinement (relaxation.py:162-168): for depth = -sd(pos) < cutoff,
+ * acc -= coef * interp(depth; s_grid, w2, right = 0) * grad; then
+ * sums[2] = sum_i |acc_i| (zeroed first).  pos/acc in caller order. */
+int sphb_relax_confine(const sphb_shape* s, int64_t n, const double* pos, double cutoff,
+                       const double* s_grid, const double* w2, int32_t n_s, double coef,
+                       double* acc, double* sums, void* stream);
+/* dx = acc dt2 capped at `cap`; pos += dx; particles with sd > surf_tol are
+ * projected back (<= 3 steps x -= sd grad while sd > 1e-12),
+ * relaxation.py:188-198 and _project_to_surface (:120-129). */
+int sphb_relax_update_shape(const sphb_shape* s, int64_t n, const double* acc, double dt2,
+                            double cap, double surf_tol, double* pos, void* stream);
+/* out[0:dim] = per-axis min, out[dim:2 dim] = per-axis max of pos (n, dim):
+ * the open-domain shift and extent of build_neighbors (neighbors.py:194-197). */
+int sphb_bounds(int64_t n, int32_t dim, const double* pos, double* out, void* stream);
 
 /* Copy 32-byte records at the given rows: d_k[rows[g]] = s_k[rows[g]] for
  * each non-null pair (pair 0 required).  Used after the last stage to carry

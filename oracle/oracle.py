@@ -216,6 +216,135 @@ def relax_steps(pos, spec, box, dp, n_updates, p0=1.0, rho0=1.0, step_scale=0.2)
     return pos, np.asarray(residuals)
 
 
+# ------------------------------------------------ shape-bounded relaxation
+class Shape:
+    """Signed-distance shapes of geometry.py:16-126 (kind: "circle",
+    "rectangle", "semicircle")."""
+
+    def __init__(self, kind, center=None, radius=None, lo=None, hi=None, normal=None):
+        self.kind = kind
+        self.center = None if center is None else np.asarray(center, dtype=float)
+        self.radius = radius
+        self.lo = None if lo is None else np.asarray(lo, dtype=float)
+        self.hi = None if hi is None else np.asarray(hi, dtype=float)
+        self.normal = None if normal is None else np.asarray(normal, dtype=float)
+
+    def bounds(self):
+        if self.kind == "rectangle":
+            return self.lo, self.hi
+        return self.center - self.radius, self.center + self.radius
+
+    def signed_distance(self, x):
+        x = np.asarray(x, dtype=float)
+        if self.kind == "circle":                                # geometry.py:37-39
+            return np.linalg.norm(x - self.center, axis=-1) - self.radius
+        if self.kind == "rectangle":                             # geometry.py:60-69
+            q = np.abs(x - 0.5 * (self.lo + self.hi)) - 0.5 * (self.hi - self.lo)
+            return (np.linalg.norm(np.maximum(q, 0.0), axis=-1)
+                    + np.minimum(np.max(q, axis=-1), 0.0))
+        p = x - self.center                                      # geometry.py:107-126
+        a = p @ self.normal
+        tnorm = np.linalg.norm(p - np.multiply.outer(a, self.normal), axis=-1)
+        d_in = np.maximum(np.linalg.norm(p, axis=-1) - self.radius, a)
+        tc = np.minimum(tnorm, self.radius)
+        d_out = np.sqrt(np.maximum(tnorm - tc, 0.0) ** 2 + a**2)
+        return np.where(a <= 0.0, d_in, d_out)
+
+    def gradient(self, x, eps=1e-7):
+        """geometry.py:137-147."""
+        x = np.atleast_2d(np.asarray(x, dtype=float))
+        g = np.empty_like(x)
+        for a in range(x.shape[1]):
+            step = np.zeros(x.shape[1])
+            step[a] = eps
+            g[:, a] = (self.signed_distance(x + step) - self.signed_distance(x - step)) / (2 * eps)
+        nrm = np.linalg.norm(g, axis=1, keepdims=True)
+        nrm[nrm == 0.0] = 1.0
+        return g / nrm
+
+    def lattice_fill(self, dp):
+        """geometry.py:150-170."""
+        lo, hi = self.bounds()
+        counts = np.maximum(np.round((hi - lo) / dp).astype(int), 1)
+        axes = [lo[a] + (np.arange(counts[a]) + 0.5) * dp for a in range(len(lo))]
+        mesh = np.meshgrid(*axes, indexing="ij")
+        pts = np.stack([m.ravel() for m in mesh], axis=1)
+        return pts[self.signed_distance(pts) < 0.0]
+
+
+def kernel_value(spec, r):
+    """kernels.py:132-146."""
+    q = np.asarray(r, dtype=float) / spec.h
+    out = np.zeros_like(q)
+    inside = q <= spec.kappa
+    qi = q[inside]
+    if spec.code == 0:
+        t = 1.0 - 0.5 * qi
+        out[inside] = spec.alpha * t**4 * (2.0 * qi + 1.0)
+    else:
+        out[inside] = spec.alpha * (1.0 - 0.5 * qi**2 + qi**4 / 6.0) * np.exp(-(qi**2))
+    return out
+
+
+def wall_table(spec, n_s=256, n_t=2000):
+    """_wall_kernel_table (relaxation.py:92-111)."""
+    cut = spec.kappa * spec.h
+    s = np.linspace(0.0, cut, n_s)
+    if spec.dim == 1:
+        return s, kernel_value(spec, s)
+    t = (np.arange(n_t) + 0.5) * (cut / n_t)
+    rr = np.sqrt(s[:, None] ** 2 + t[None, :] ** 2)
+    if spec.dim == 2:
+        return s, 2.0 * np.sum(kernel_value(spec, rr), axis=1) * (cut / n_t)
+    return s, 2.0 * np.pi * np.sum(kernel_value(spec, rr) * t[None, :], axis=1) * (cut / n_t)
+
+
+def wall_confinement(spec, depth):
+    s, w2 = wall_table(spec)
+    return np.interp(np.asarray(depth, dtype=float), s, w2, right=0.0)
+
+
+def relax_shape(shape, spec, dp, max_steps, p0=1.0, rho0=1.0, step_scale=0.2):
+    """relax() with box=None (relaxation.py:132-210), no stop tests besides
+    max_steps; returns (best-residual positions, residuals, best_step)."""
+    pos = shape.lattice_fill(dp).copy()
+    n, d = pos.shape
+    vols = np.full(n, dp**d)
+    cutoff = spec.kappa * spec.h
+    dt2 = step_scale * spec.h**2 * rho0 / p0
+    cap = 0.25 * dp
+    surf_tol = 1e-9 * dp
+    residuals, best, best_step, best_pos = [], np.inf, 0, pos.copy()
+    for step in range(max_steps + 1):
+        nl = build_neighbors(pos, cutoff)
+        acc = relax_accelerations(nl, vols, spec, p0, rho0)
+        depth = -shape.signed_distance(pos)
+        near = depth < cutoff
+        if np.any(near):
+            nrm = shape.gradient(pos[near])
+            acc[near] -= (2.0 * p0 / rho0) * wall_confinement(spec, depth[near])[:, None] * nrm
+        res = float(np.mean(np.linalg.norm(acc, axis=1)) * spec.h * rho0 / p0)
+        residuals.append(res)
+        if res < best:
+            best, best_step, best_pos = res, step, pos.copy()
+        if step == max_steps:
+            break
+        dx = acc * dt2
+        norms = np.linalg.norm(dx, axis=1)
+        over = norms > cap
+        if np.any(over):
+            dx[over] *= (cap / norms[over])[:, None]
+        pos += dx
+        outside = shape.signed_distance(pos) > surf_tol
+        for _ in range(3):                                      # relaxation.py:120-129
+            if not np.any(outside):
+                break
+            sd = shape.signed_distance(pos[outside])
+            pos[outside] -= sd[:, None] * shape.gradient(pos[outside])
+            outside = shape.signed_distance(pos) > 1e-12
+    return best_pos, np.asarray(residuals), best_step
+
+
 # ------------------------------------------------------------ WC Eulerian
 class EulerianWC:
     """EulerianSolver, WC branch (eulerian.py:473-643): periodic or with a

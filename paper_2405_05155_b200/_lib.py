@@ -58,6 +58,29 @@ class Kernel(C.Structure):
     ]
 
 
+class Shape(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("dim", C.c_int32),
+        ("center", C.c_double * 3),
+        ("radius", C.c_double),
+        ("lo", C.c_double * 3),
+        ("hi", C.c_double * 3),
+        ("normal", C.c_double * 3),
+    ]
+
+
+def shape_struct(kind, dim, *, center=None, radius=0.0, lo=None, hi=None, normal=None) -> Shape:
+    s = Shape()
+    s.kind, s.dim, s.radius = int(kind), int(dim), float(radius)
+    for name, val in (("center", center), ("lo", lo), ("hi", hi), ("normal", normal)):
+        if val is not None:
+            arr = getattr(s, name)
+            for a, v in enumerate(val):
+                arr[a] = float(v)
+    return s
+
+
 class WCParams(C.Structure):
     _fields_ = [
         ("dim", C.c_int32),
@@ -136,6 +159,10 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_shape_sdf": (C.c_int, [P, I64, P, P, P, P]),
+    "sphb_relax_confine": (C.c_int, [P, I64, P, F64, P, P, I32, F64, P, P, P]),
+    "sphb_relax_update_shape": (C.c_int, [P, I64, P, F64, F64, F64, P, P]),
+    "sphb_bounds": (C.c_int, [I64, I32, P, P, P]),
     "sphb_wall_record": (C.c_int, [I32, P, P, F64, P, P, I64, P]),
     "sphb_copy_records": (C.c_int, [I64, P, P, P, P, P, P, P, P]),
     "sphb_wc_ghosts": (C.c_int, [I32, I64, P, P, P, P, P, P, P, P, P, P, P]),

@@ -12,21 +12,24 @@ relaxation.py:1-210):
   residual, best-state tracking and stop tests are the reference's.
 * `relax_steps(...)` — the same loop with a fixed number of updates and no
   stop tests (the C1 benchmark protocol).
-
-Shape-bounded relaxation (SDF projection + analytic wall confinement,
-relaxation.py:92-129, 162-168, 196-198) is outside the hot-path scope.
+* shape-bounded relaxation: `relax(config)` without a
+  periodic box runs `ShapeRelaxer` — open-domain binning from device-side
+  bounds, the same fused acceleration, the analytic wall confinement
+  (relaxation.py:92-117, 162-168; `wall_confinement`) and the capped update
+  with surface projection (:120-129, 188-198), all in csrc/relax_shape.cu.
 """
 
 from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
+from functools import lru_cache
 
 import numpy as np
 
 from . import _lib
 from .correction import _vols_dev
-from .kernels import KernelSpec
+from .kernels import KernelSpec, kernel_spec, kernel_value
 from .neighbors import NeighborList, make_grid
 
 
@@ -82,6 +85,32 @@ def relax_accelerations_device(nlist: NeighborList, vols, spec: KernelSpec, p0=1
 def relax_accelerations(nlist, vols, spec: KernelSpec, p0: float = 1.0, rho0: float = 1.0):
     """a_i = sum_j -2 p0 V_j grad W_ij / rho0; zero for isolated particles."""
     return relax_accelerations_device(nlist, vols, spec, p0, rho0).cpu().numpy()
+
+
+@lru_cache(maxsize=None)
+def _wall_kernel_table(family: str, h: float, dim: int, n_s: int = 256, n_t: int = 2000):
+    """w2(s), the kernel integrated over the plane at offset s from the
+    particle, on s in [0, kappa h] (relaxation.py:92-111): midpoint rule in
+    the in-plane radius t over (0, kappa h)."""
+    spec = kernel_spec(family, h, dim)
+    cut = spec.kappa * h
+    s = np.linspace(0.0, cut, n_s)
+    if dim == 1:
+        return s, kernel_value(spec, s)
+    t = (np.arange(n_t) + 0.5) * (cut / n_t)
+    w = kernel_value(spec, np.sqrt(s[:, None] ** 2 + t[None, :] ** 2))
+    if dim == 3:
+        w = 2.0 * np.pi * np.sum(w * t[None, :], axis=1) * (cut / n_t)
+    else:
+        w = 2.0 * np.sum(w, axis=1) * (cut / n_t)
+    return s, w
+
+
+def wall_confinement(spec: KernelSpec, depth) -> np.ndarray:
+    """Inward acceleration magnitude per 2 p0 / rho at `depth` below the
+    surface (relaxation.py:114-117): w2 interpolated, 0 beyond the support."""
+    s_grid, w2 = _wall_kernel_table(spec.family, spec.h, spec.dim)
+    return np.interp(np.asarray(depth, dtype=float), s_grid, w2, right=0.0)
 
 
 class PeriodicRelaxer:
@@ -170,6 +199,89 @@ class PeriodicRelaxer:
             self._graph.replay()
 
 
+class ShapeRelaxer(PeriodicRelaxer):
+    """Device-resident relaxation inside an SDF shape (open domain).
+
+    Per step: device bounds -> cell grid (the reference's open-domain shift
+    and extent, neighbors.py:194-203), bin, fused acceleration, wall
+    confinement + |a| sum; update = capped move + surface projection.
+    """
+
+    def __init__(self, positions, spec: KernelSpec, shape, dp: float, *, p0=1.0, rho0=1.0,
+                 step_scale=0.2, vols=None):
+        torch = _lib.torch_cuda()
+        pos = np.ascontiguousarray(np.asarray(positions, dtype=float))
+        self.n, self.dim = pos.shape
+        self.spec, self.shape = spec, shape
+        self.sstruct = shape.device_struct()
+        if self.sstruct.dim != self.dim:
+            raise ValueError("shape and particle dimensions differ")
+        self.p0, self.rho0 = float(p0), float(rho0)
+        self.dt2 = step_scale * spec.h**2 * rho0 / p0          # relaxation.py:146
+        self.cap = 0.25 * dp                                   # relaxation.py:147
+        self.surf_tol = 1e-9 * dp                              # relaxation.py:148
+        self.cutoff = spec.kappa * spec.h
+        self.coef = 2.0 * p0 / rho0                            # relaxation.py:168
+        self.kernel = _lib.kernel_struct(spec)
+        dev = _lib.device()
+        self._dev = dev
+        self.pos = _lib.to_device(pos, torch.float64)
+        v = np.full(self.n, dp**self.dim) if vols is None else np.asarray(vols, dtype=float)
+        self.vols = _lib.to_device(v, torch.float64)
+        n1 = max(self.n, 1)
+        self.ws = torch.empty((self.dim, n1), dtype=torch.float64, device=dev)
+        self.perm = torch.empty(n1, dtype=torch.int32, device=dev)
+        self.acc = torch.empty((n1, self.dim), dtype=torch.float64, device=dev)
+        self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.bounds = torch.empty(2 * self.dim, dtype=torch.float64, device=dev)
+        s_grid, w2 = _wall_kernel_table(spec.family, spec.h, spec.dim)
+        self.s_grid = _lib.to_device(np.ascontiguousarray(s_grid), torch.float64)
+        self.w2 = _lib.to_device(np.ascontiguousarray(w2), torch.float64)
+        self.n_s = int(s_grid.shape[0])
+        self.cs = self.ce = self.work = None
+        self._ntot = self._wcap = 0
+        self.launches_per_step = 0
+
+    def _grid(self):
+        _lib.call("sphb_bounds", self.n, self.dim, self.pos.data_ptr(),
+                  self.bounds.data_ptr(), _lib.stream_ptr())
+        b = self.bounds.tolist()
+        self.grid = make_grid(None, self.cutoff, None, dim=self.dim, lo=b[:self.dim],
+                              hi=b[self.dim:])
+        torch = _lib.torch_cuda()
+        if self.grid.ntot > self._ntot:
+            self._ntot = self.grid.ntot
+            self.cs = torch.empty(self._ntot, dtype=torch.int32, device=self._dev)
+            self.ce = torch.empty(self._ntot, dtype=torch.int32, device=self._dev)
+        self.wbytes = _lib.load_library().sphb_bin_workspace_bytes(self.n, ctypes.byref(self.grid))
+        if self.wbytes > self._wcap:
+            self._wcap = max(self.wbytes, 1)
+            self.work = torch.empty(self._wcap, dtype=torch.uint8, device=self._dev)
+
+    def accelerate(self):
+        """Bin (open grid) + fused acceleration + wall confinement."""
+        self._grid()
+        super().accelerate()
+        _lib.call("sphb_relax_confine", ctypes.byref(self.sstruct), self.n, self.pos.data_ptr(),
+                  self.cutoff, self.s_grid.data_ptr(), self.w2.data_ptr(), self.n_s, self.coef,
+                  self.acc.data_ptr(), self.sums.data_ptr(), _lib.stream_ptr())
+
+    def residual(self) -> tuple[float, int]:
+        _, iso, tot = self.sums.tolist()
+        mean = tot / self.n if self.n else float("nan")
+        return float(mean * self.spec.h * self.rho0 / self.p0), int(iso)
+
+    def update(self):
+        _lib.call("sphb_relax_update_shape", ctypes.byref(self.sstruct), self.n,
+                  self.acc.data_ptr(), self.dt2, self.cap, self.surf_tol, self.pos.data_ptr(),
+                  _lib.stream_ptr())
+
+    def run(self, n_updates: int, *, graph: bool = False) -> None:
+        for _ in range(max(n_updates, 0)):     # the grid changes every step: no graph
+            self.accelerate()
+            self.update()
+
+
 def relax_steps(positions, spec: KernelSpec, box, dp: float, n_updates: int, *, p0=1.0,
                 rho0=1.0, step_scale=0.2, record_residuals=True):
     """`n_updates` relaxation updates from the given positions, no stop tests.
@@ -189,20 +301,19 @@ def relax_steps(positions, spec: KernelSpec, box, dp: float, n_updates: int, *, 
 
 
 def relax(config: RelaxationConfig) -> RelaxResult:
-    """Drive a lattice fill to a low-residue distribution (relaxation.py:132-210).
-
-    Periodic boxes only: the shape-projection branch is out of scope.
-    """
-    if config.periodic_box is None:
-        raise NotImplementedError(
-            "shape-bounded relaxation (SDF projection / wall confinement) is outside the "
-            "B200 hot path; pass periodic_box")
+    """Drive a lattice fill to a low-residue distribution (relaxation.py:132-210):
+    a periodic block when `periodic_box` is set, else the shape interior with
+    wall confinement and surface projection."""
     from .geometry import lattice_fill
 
     spec = config.kernel
     pos0 = lattice_fill(config.shape, config.dp).copy()
-    rl = PeriodicRelaxer(pos0, spec, config.periodic_box, config.dp, p0=config.p0,
-                         rho0=config.rho0, step_scale=config.step_scale)
+    if config.periodic_box is not None:
+        rl = PeriodicRelaxer(pos0, spec, config.periodic_box, config.dp, p0=config.p0,
+                             rho0=config.rho0, step_scale=config.step_scale)
+    else:
+        rl = ShapeRelaxer(pos0, spec, config.shape, config.dp, p0=config.p0, rho0=config.rho0,
+                          step_scale=config.step_scale)
     residuals: list[float] = []
     converged = False
     best_step, best_residual = 0, np.inf

@@ -303,6 +303,47 @@ def main():
         arrays[f"{tag}__wf"] = np.array([w for _, w in solver.wall_force_series])
     save("cylinder", **arrays)
 
+    # ------------- shapes + shape-bounded relaxation
+    from sph_trunc import geometry as rgeo
+    from sph_trunc.kernels import LAGUERRE_GAUSS, WENDLAND
+
+    arrays = {}
+    shapes = {
+        "circle": rgeo.Circle(center=(0.0, 0.0), diameter=2.0),
+        "semicircle": rgeo.SemiCircle(center=(0.0, 0.0), radius=0.5, flat_normal=(0.0, 1.0)),
+        "rectangle": rgeo.Rectangle(lo=(0.0, 0.0), hi=(1.0, 0.5)),
+        "ball": rgeo.Circle(center=(0.1, 0.2, 0.3), diameter=1.0),
+        "box3": rgeo.Box3(lo=(0.0, 0.0, 0.0), hi=(1.0, 0.5, 0.25)),
+    }
+    rng = np.random.default_rng(5)
+    for name, shp in shapes.items():
+        lo, hi = shp.bounds()
+        x = rng.uniform(lo - 0.3, hi + 0.3, size=(400, len(lo)))
+        arrays[f"sdf_{name}__x"] = x
+        arrays[f"sdf_{name}__sd"] = rgeo.signed_distance(shp, x)
+        arrays[f"sdf_{name}__grad"] = rgeo.sdf_gradient(shp, x)
+    for fam, hr, dim in ((WENDLAND, 1.3, 2), (LAGUERRE_GAUSS, 1.1, 2), (WENDLAND, 1.3, 3)):
+        spec = kernel_spec(fam, hr * 0.1, dim)
+        depth = np.linspace(-0.05, spec.kappa * spec.h + 0.05, 101)
+        arrays[f"wall_{fam}_{dim}__depth"] = depth
+        arrays[f"wall_{fam}_{dim}__w2"] = relaxation.wall_confinement(spec, depth)
+    runs = (("circle_w", "circle", 0.1, WENDLAND, 1.3, 0.3),
+            ("circle_lg", "circle", 0.1, LAGUERRE_GAUSS, 1.1, 0.1),
+            ("semicircle_lg", "semicircle", 0.04, LAGUERRE_GAUSS, 1.1, 0.1),
+            ("rectangle_w", "rectangle", 0.05, WENDLAND, 1.3, 0.2))
+    for tag, shp, dp, fam, hr, ss in runs:
+        cfg = relaxation.RelaxationConfig(shape=shapes[shp], dp=dp,
+                                          kernel=kernel_spec(fam, hr * dp, 2), step_scale=ss,
+                                          residual_tol=1e-12, max_steps=40, patience=None)
+        res = relaxation.relax(cfg)
+        arrays[f"{tag}__pos0"] = rgeo.lattice_fill(shapes[shp], dp)
+        arrays[f"{tag}__positions"] = res.positions
+        arrays[f"{tag}__residuals"] = res.residuals
+        arrays[f"{tag}__meta"] = np.array([res.steps, res.best_step, res.n_isolated,
+                                           int(res.converged)])
+        arrays[f"{tag}__params"] = np.array([dp, hr, ss])
+    save("relax_shapes", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

@@ -588,3 +588,76 @@ def test_cylinder_wall_force_graph_advance(gold):
     wf = np.array([w for _, w in s.wall_force_series])
     assert l2_error(wf, g["1p6h__wf"]) < TOL_100
     assert l2_error(s.state.rho[:s.n_int], g["1p6h__rho30"]) < TOL_100
+
+
+def _shapes():
+    from paper_2405_05155_b200 import geometry as G
+
+    return {
+        "circle": G.Circle(center=(0.0, 0.0), diameter=2.0),
+        "semicircle": G.SemiCircle(center=(0.0, 0.0), radius=0.5, flat_normal=(0.0, 1.0)),
+        "rectangle": G.Rectangle(lo=(0.0, 0.0), hi=(1.0, 0.5)),
+        "ball": G.Circle(center=(0.1, 0.2, 0.3), diameter=1.0),
+        "box3": G.Box3(lo=(0.0, 0.0, 0.0), hi=(1.0, 0.5, 0.25)),
+    }
+
+
+def test_host_shapes_and_wall_table_vs_reference_golden(gold):
+    """Host SDFs (geometry.py:16-147) and the wall-confinement table
+    (relaxation.py:92-117) — the table is bit-identical to the reference's."""
+    from paper_2405_05155_b200 import geometry as G
+
+    g = gold("relax_shapes")
+    for name, s in _shapes().items():
+        x = g[f"sdf_{name}__x"]
+        np.testing.assert_allclose(G.signed_distance(s, x), g[f"sdf_{name}__sd"], rtol=0,
+                                   atol=1e-15)
+        np.testing.assert_allclose(G.sdf_gradient(s, x), g[f"sdf_{name}__grad"], rtol=0,
+                                   atol=1e-9)
+    for fam, hr, dim in (("wendland", 1.3, 2), ("laguerre-gauss", 1.1, 2), ("wendland", 1.3, 3)):
+        spec = kernel_spec(fam, hr * 0.1, dim)
+        np.testing.assert_array_equal(relaxation.wall_confinement(spec, g[f"wall_{fam}_{dim}__depth"]),
+                                      g[f"wall_{fam}_{dim}__w2"])
+
+
+@pytest.mark.gpu
+def test_device_sdf_vs_reference_golden(gold):
+    """csrc/relax_shape.cu signed distances and normals (sphb_shape_sdf)."""
+    import ctypes
+
+    import torch
+
+    from paper_2405_05155_b200 import _lib
+
+    g = gold("relax_shapes")
+    for name, s in _shapes().items():
+        x = g[f"sdf_{name}__x"]
+        xd = torch.tensor(x, dtype=torch.float64, device="cuda")
+        sd = torch.empty(x.shape[0], dtype=torch.float64, device="cuda")
+        gr = torch.empty_like(xd)
+        st = s.device_struct()
+        _lib.call("sphb_shape_sdf", ctypes.byref(st), x.shape[0], xd.data_ptr(), sd.data_ptr(),
+                  gr.data_ptr(), _lib.stream_ptr())
+        np.testing.assert_allclose(sd.cpu().numpy(), g[f"sdf_{name}__sd"], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(gr.cpu().numpy(), g[f"sdf_{name}__grad"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag,shape,fam", [("circle_w", "circle", "wendland"),
+                                           ("circle_lg", "circle", "laguerre-gauss"),
+                                           ("semicircle_lg", "semicircle", "laguerre-gauss"),
+                                           ("rectangle_w", "rectangle", "wendland")])
+def test_shape_relaxation_vs_reference_golden(gold, tag, shape, fam):
+    """relax() inside a shape — open-domain binning,
+    fused acceleration, wall confinement and surface projection on the GPU;
+    residual history and the returned best-residual distribution."""
+    g = gold("relax_shapes")
+    dp, hr, ss = (float(v) for v in g[f"{tag}__params"])
+    cfg = relaxation.RelaxationConfig(shape=_shapes()[shape], dp=dp,
+                                      kernel=kernel_spec(fam, hr * dp, 2), step_scale=ss,
+                                      residual_tol=1e-12, max_steps=40, patience=None)
+    res = relaxation.relax(cfg)
+    steps, best, iso, conv = (int(v) for v in g[f"{tag}__meta"])
+    assert (res.steps, res.best_step, res.n_isolated, int(res.converged)) == (steps, best, iso, conv)
+    np.testing.assert_allclose(res.residuals, g[f"{tag}__residuals"], rtol=1e-9)
+    np.testing.assert_allclose(res.positions, g[f"{tag}__positions"], rtol=0, atol=1e-10)

@@ -285,3 +285,48 @@ def test_oracle_cylinder_wall_force(gold, key):
     wf = np.array([w for _, w in s.wall_force_series])
     np.testing.assert_allclose([t for t, _ in s.wall_force_series], g[f"{tag}__wf_t"], rtol=1e-12)
     assert l2_error(wf, g[f"{tag}__wf"]) < 1e-10
+
+
+_ORC_SHAPES = {
+    "circle": O.Shape("circle", center=(0.0, 0.0), radius=1.0),
+    "semicircle": O.Shape("semicircle", center=(0.0, 0.0), radius=0.5, normal=(0.0, 1.0)),
+    "rectangle": O.Shape("rectangle", lo=(0.0, 0.0), hi=(1.0, 0.5)),
+    "ball": O.Shape("circle", center=(0.1, 0.2, 0.3), radius=0.5),
+    "box3": O.Shape("rectangle", lo=(0.0, 0.0, 0.0), hi=(1.0, 0.5, 0.25)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(_ORC_SHAPES))
+def test_oracle_sdf(gold, name):
+    """Signed distances and central-difference normals (geometry.py:16-147)."""
+    g = gold("relax_shapes")
+    s = _ORC_SHAPES[name]
+    x = g[f"sdf_{name}__x"]
+    np.testing.assert_allclose(s.signed_distance(x), g[f"sdf_{name}__sd"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(s.gradient(x), g[f"sdf_{name}__grad"], rtol=0, atol=1e-9)
+
+
+def test_oracle_wall_confinement(gold):
+    """Planar kernel integral w2(s) (relaxation.py:92-117), interpolated."""
+    g = gold("relax_shapes")
+    for fam, hr, dim in (("wendland", 1.3, 2), ("laguerre-gauss", 1.1, 2), ("wendland", 1.3, 3)):
+        spec = kernel_spec(fam, hr * 0.1, dim)
+        w = O.wall_confinement(spec, g[f"wall_{fam}_{dim}__depth"])
+        np.testing.assert_array_equal(w, g[f"wall_{fam}_{dim}__w2"])
+
+
+@pytest.mark.parametrize("tag,shape,fam", [("circle_w", "circle", "wendland"),
+                                           ("circle_lg", "circle", "laguerre-gauss"),
+                                           ("semicircle_lg", "semicircle", "laguerre-gauss"),
+                                           ("rectangle_w", "rectangle", "wendland")])
+def test_oracle_shape_relaxation(gold, tag, shape, fam):
+    """Shape-bounded relax(): confinement + projection, 40 updates."""
+    g = gold("relax_shapes")
+    dp, hr, ss = g[f"{tag}__params"]
+    spec = kernel_spec(fam, hr * dp, 2)
+    s = _ORC_SHAPES[shape]
+    np.testing.assert_array_equal(s.lattice_fill(dp), g[f"{tag}__pos0"])
+    pos, res, best = O.relax_shape(s, spec, dp, 40, step_scale=ss)
+    assert best == int(g[f"{tag}__meta"][1])
+    np.testing.assert_allclose(res, g[f"{tag}__residuals"], rtol=1e-9)
+    np.testing.assert_allclose(pos, g[f"{tag}__positions"], rtol=0, atol=1e-10)

@@ -216,6 +216,12 @@ int sphb_pair_gradients(int64_t n, int32_t dim, const int64_t* starts,
                         const sphb_kernel* k, const double* b, double* gw,
                         void* stream);
 
+/* _weak_gradient (approx.py:61-86): out_i = sum_j 2 (0.5 (f_i + f_j) V_j) gw_ij
+ * over CSR rows with the pair gradients of sphb_pair_gradients. */
+int sphb_weak_gradient(int64_t n, int32_t dim, const int64_t* starts, const int32_t* idx,
+                       const double* f, const double* vols, const double* gw, double* out,
+                       void* stream);
+
 /* _rhs_wc (eulerian.py:224-266) over precomputed gwv/viscv (CSR, orig). */
 int sphb_rhs_wc_csr(int64_t n_int, int32_t dim, const int64_t* starts,
                     const int32_t* idx, const double* e, const double* gwv,

@@ -40,6 +40,7 @@ _SIGS = {
     "orc_rhs_hllc": (None, [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "orc_tl_accelerations": (None, [_I, _I, _P, _P, _P, _P, _D, _P]),
     "orc_tl_deformation_rates": (None, [_I, _I, _P, _P, _P, _P, _P, _P]),
+    "orc_weak_gradient": (None, [_I, _I, _P, _P, _P, _P, _P, _P]),
     "orc_max_threads": (C.c_int, []),
 }
 
@@ -180,6 +181,17 @@ def pair_gradients(nl, spec, b=None):
     lib().orc_pair_gradients(nl.n, d, _p(nl.starts), _p(nl.idx), _p(nl.r), _p(nl.e),
                              spec.code, spec.h, spec.alpha, spec.kappa, _p(bb), _p(gw))
     return gw
+
+
+def weak_gradient(nl, f, vols, spec, b=None):
+    """approx.py:74-86."""
+    d = nl.e.shape[1]
+    gw = np.ascontiguousarray(pair_gradients(nl, spec, b))
+    out = np.empty((nl.n, d))
+    lib().orc_weak_gradient(nl.n, d, _p(nl.starts), _p(nl.idx),
+                            _p(np.ascontiguousarray(f, dtype=float)),
+                            _p(np.ascontiguousarray(vols, dtype=float)), _p(gw), _p(out))
+    return out
 
 
 def _profile_deriv(code, q):

@@ -388,6 +388,20 @@ void orc_rhs_hllc(int64_t n_int, int64_t d, const int64_t* starts, const int32_t
   }
 }
 
+/* _weak_gradient (approx.py:61-71) */
+void orc_weak_gradient(int64_t n, int64_t d, const int64_t* starts, const int32_t* idx,
+                       const double* f, const double* vols, const double* gw, double* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t a = 0; a < d; ++a) out[i * d + a] = 0.0;
+    for (int64_t k = starts[i]; k < starts[i + 1]; ++k) {
+      const int64_t j = idx[k];
+      const double fbar_v = 0.5 * (f[i] + f[j]) * vols[j];
+      for (int64_t a = 0; a < d; ++a) out[i * d + a] += 2.0 * fbar_v * gw[k * d + a];
+    }
+  }
+}
+
 /* _accelerations (tlsph.py:88-102) */
 void orc_tl_accelerations(int64_t n, int64_t d, const int64_t* starts, const int32_t* idx,
                           const double* g0, const double* q, double rho0, double* acc) {

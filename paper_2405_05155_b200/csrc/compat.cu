@@ -479,6 +479,27 @@ __global__ void k_tl_geometry(sphb_grid g, int64_t n, const double* __restrict__
   }
 }
 
+// _weak_gradient (approx.py:61-71): 2 sum_j 0.5 (f_i + f_j) V_j gw_ij, CSR rows.
+template <int D>
+__global__ void k_weak_gradient(int64_t n, const int64_t* __restrict__ starts,
+                                const int32_t* __restrict__ idx, const double* __restrict__ f,
+                                const double* __restrict__ vols, const double* __restrict__ gw,
+                                double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double o[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) o[a] = 0.0;
+  for (int64_t k = starts[i]; k < starts[i + 1]; ++k) {
+    const int32_t j = idx[k];
+    const double fbar_v = 0.5 * (f[i] + f[j]) * vols[j];
+#pragma unroll
+    for (int a = 0; a < D; ++a) o[a] += 2.0 * fbar_v * gw[k * D + a];
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) out[i * D + a] = o[a];
+}
+
 }  // namespace
 
 #define SPHB_DISPATCH_D(dim, KERNEL, GRID, ...)                                   \
@@ -490,6 +511,18 @@ __global__ void k_tl_geometry(sphb_grid g, int64_t n, const double* __restrict__
       default: return SPHB_ERR_ARG;                                               \
     }                                                                             \
   } while (0)
+
+extern "C" int sphb_weak_gradient(int64_t n, int32_t dim, const int64_t* starts,
+                                  const int32_t* idx, const double* f, const double* vols,
+                                  const double* gw, double* out, void* stream) {
+  if (n < 0) return SPHB_ERR_ARG;
+  if (n == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = 128;
+  SPHB_DISPATCH_D(dim, k_weak_gradient, sphb_blocks(n, T), n, starts, idx, f, vols, gw, out);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
 
 extern "C" int sphb_unity_sums(int64_t n, const int64_t* starts, const int32_t* idx,
                                const double* r, const double* vols, const sphb_kernel* k,

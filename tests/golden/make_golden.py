@@ -344,6 +344,40 @@ def main():
         arrays[f"{tag}__params"] = np.array([dp, hr, ss])
     save("relax_shapes", **arrays)
 
+    # ------------------------------- error study (approx.py:61-246, §8(f) rank 3)
+    arrays = {}
+    rng = np.random.default_rng(9)
+    pos = rng.uniform(-1, 1, size=(500, 2))
+    spec = kernel_spec(WENDLAND, 0.13, 2)
+    nl = neighbors.build_neighbors(pos, spec.kappa * spec.h)
+    vols = np.full(500, 0.008)
+    f = approx.exp_function(pos[:, 0])
+    b = correction.correction_matrices(nl, vols, spec).B
+    arrays["wg__pos"] = pos
+    arrays["wg__plain"] = approx.weak_gradient(nl, f, vols, spec)
+    arrays["wg__corrected"] = approx.weak_gradient(nl, f, vols, spec, b)
+    for fam in (WENDLAND, "wendland-truncated", LAGUERRE_GAUSS):
+        key = fam.replace("-", "_")
+        for k, dp in enumerate((0.2, 0.1)):
+            lat = approx.circle_distribution(approx.LATTICE, dp)
+            arrays[f"unity__{key}__{k}"] = np.array(approx.unity_error(lat, dp, fam))
+            for corr in (False, True):
+                arrays[f"grad__{key}__{k}__{int(corr)}"] = np.array(
+                    approx.gradient_error(lat, dp, fam, corr))
+        rows = approx.convergence_study(approx.LATTICE, fam, True)
+        arrays[f"study__{key}"] = np.array([[r.dp, r.error, r.observed_order or 0.0]
+                                            for r in rows])
+        arrays[f"smooth__{key}"] = np.array([approx.smoothing_error(fam, h)
+                                             for h in (0.2, 0.1, 0.05)])
+        arrays[f"order__{key}"] = np.array(approx.smoothing_order_check(fam))
+    for dist in (approx.RELAXED_WENDLAND, approx.RELAXED_LAGUERRE_GAUSS):
+        p_ = approx.circle_distribution(dist, 0.2, {"max_steps": 60, "patience": None,
+                                                    "residual_tol": 1e-12})
+        arrays[f"relaxed__{dist}"] = p_
+        arrays[f"relaxed_grad__{dist}"] = np.array(approx.gradient_error(p_, 0.2, WENDLAND,
+                                                                        True))
+    save("error_study", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

@@ -661,3 +661,53 @@ def test_shape_relaxation_vs_reference_golden(gold, tag, shape, fam):
     assert (res.steps, res.best_step, res.n_isolated, int(res.converged)) == (steps, best, iso, conv)
     np.testing.assert_allclose(res.residuals, g[f"{tag}__residuals"], rtol=1e-9)
     np.testing.assert_allclose(res.positions, g[f"{tag}__positions"], rtol=0, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_weak_gradient_vs_reference_golden(gold):
+    """approx.weak_gradient (approx.py:61-86) on the device, plain and corrected."""
+    g = gold("error_study")
+    pos = g["wg__pos"]
+    spec = kernel_spec("wendland", 0.13, 2)
+    nl = neighbors.build_neighbors(pos, spec.kappa * spec.h)
+    vols = np.full(pos.shape[0], 0.008)
+    f = approx.exp_function(pos[:, 0])
+    np.testing.assert_allclose(approx.weak_gradient(nl, f, vols, spec), g["wg__plain"], rtol=0,
+                               atol=1e-12)
+    b = correction.correction_matrices(nl, vols, spec).B
+    np.testing.assert_allclose(approx.weak_gradient(nl, f, vols, spec, b), g["wg__corrected"],
+                               rtol=0, atol=1e-11)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam", ["wendland", "wendland-truncated", "laguerre-gauss"])
+def test_circle_study_vs_reference_golden(gold, fam):
+    """The §2.3.3 error study: unity / gradient errors, convergence orders and
+    smoothing order (approx.py:101-246)."""
+    g = gold("error_study")
+    key = fam.replace("-", "_")
+    for k, dp in enumerate((0.2, 0.1)):
+        lat = approx.circle_distribution(approx.LATTICE, dp)
+        assert approx.unity_error(lat, dp, fam) == pytest.approx(float(g[f"unity__{key}__{k}"]),
+                                                                 rel=1e-12)
+        for corr in (False, True):
+            assert approx.gradient_error(lat, dp, fam, corr) == pytest.approx(
+                float(g[f"grad__{key}__{k}__{int(corr)}"]), rel=1e-9)
+    rows = approx.convergence_study(approx.LATTICE, fam, True)
+    got = np.array([[r.dp, r.error, r.observed_order or 0.0] for r in rows])
+    np.testing.assert_allclose(got, g[f"study__{key}"], rtol=1e-8)
+    np.testing.assert_array_equal([approx.smoothing_error(fam, h) for h in (0.2, 0.1, 0.05)],
+                                  g[f"smooth__{key}"])
+    assert approx.smoothing_order_check(fam) == float(g[f"order__{key}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dist", ["relaxed-wendland", "relaxed-laguerre-gauss"])
+def test_relaxed_circle_distribution_vs_reference_golden(gold, dist):
+    """Relaxed study distributions (approx.py:122-145) from the GPU relaxer."""
+    g = gold("error_study")
+    pos = approx.circle_distribution(dist, 0.2, {"max_steps": 60, "patience": None,
+                                                 "residual_tol": 1e-12})
+    np.testing.assert_allclose(pos, g[f"relaxed__{dist}"], rtol=0, atol=1e-10)
+    assert approx.gradient_error(pos, 0.2, "wendland", True) == pytest.approx(
+        float(g[f"relaxed_grad__{dist}"]), rel=1e-8)

@@ -330,3 +330,42 @@ def test_oracle_shape_relaxation(gold, tag, shape, fam):
     assert best == int(g[f"{tag}__meta"][1])
     np.testing.assert_allclose(res, g[f"{tag}__residuals"], rtol=1e-9)
     np.testing.assert_allclose(pos, g[f"{tag}__positions"], rtol=0, atol=1e-10)
+
+
+def test_oracle_weak_gradient(gold):
+    """Weak-form gradient, plain and corrected (approx.py:61-86)."""
+    g = gold("error_study")
+    pos = g["wg__pos"]
+    spec = kernel_spec("wendland", 0.13, 2)
+    nl = O.build_neighbors(pos, spec.kappa * spec.h)
+    vols = np.full(pos.shape[0], 0.008)
+    f = np.exp(-(pos[:, 0] ** 2) / 0.1)
+    np.testing.assert_allclose(O.weak_gradient(nl, f, vols, spec), g["wg__plain"], rtol=0,
+                               atol=1e-12)
+    b = O.correction_matrices(nl, vols, spec)[0]
+    np.testing.assert_allclose(O.weak_gradient(nl, f, vols, spec, b), g["wg__corrected"], rtol=0,
+                               atol=1e-11)
+
+
+@pytest.mark.parametrize("fam", ["wendland", "wendland-truncated", "laguerre-gauss"])
+def test_oracle_circle_study_errors(gold, fam):
+    """Unity and gradient errors of the circle study on the lattice
+    distribution (approx.py:148-192), oracle operators + study glue."""
+    g = gold("error_study")
+    key = fam.replace("-", "_")
+    circle = O.Shape("circle", center=(0.0, 0.0), radius=1.0)
+    for k, dp in enumerate((0.2, 0.1)):
+        pos = circle.lattice_fill(dp)
+        spec = kernel_spec(fam, 1.3 * dp, 2)
+        vols = np.full(pos.shape[0], dp * dp)
+        mask = np.linalg.norm(pos, axis=1) <= 1.0 - 2.0 * 1.3 * dp
+        u = O.sph_unity_sum(O.build_neighbors(pos, 2.0 * spec.h), vols, spec)
+        np.testing.assert_allclose(np.linalg.norm(u[mask] - 1.0) / np.sqrt(mask.sum()),
+                                   g[f"unity__{key}__{k}"], rtol=1e-12)
+        nl = O.build_neighbors(pos, spec.kappa * spec.h)
+        for corr in (False, True):
+            b = O.correction_matrices(nl, vols, spec)[0] if corr else None
+            grad = O.weak_gradient(nl, np.exp(-(pos[:, 0] ** 2) / 0.1), vols, spec, b)
+            ana = -(20.0 * pos[mask, 0]) * np.exp(-(pos[mask, 0] ** 2) / 0.1)
+            err = np.linalg.norm(grad[mask, 0] - ana) / np.linalg.norm(ana)
+            np.testing.assert_allclose(err, g[f"grad__{key}__{k}__{int(corr)}"], rtol=1e-9)

@@ -77,6 +77,23 @@ TWIST = "twist"
 BEND = "bend"
 
 
+def von_mises(F, S):
+    """Von Mises stress of the Cauchy stress J^-1 F S F^T (tlsph.py:68-86);
+    2D tensors are read as plane stress (sigma_zz = 0).  Host diagnostic."""
+    F = np.asarray(F, dtype=float)
+    S = np.asarray(S, dtype=float)
+    single = F.ndim == 2
+    Fb, Sb = (F[None], S[None]) if single else (F, S)
+    sigma = np.einsum("nab,nbc,ndc->nad", Fb, Sb, Fb) / np.linalg.det(Fb)[:, None, None]
+    if sigma.shape[-1] == 2:
+        pad = np.zeros((sigma.shape[0], 3, 3))
+        pad[:, :2, :2] = sigma
+        sigma = pad
+    dev = sigma - (np.trace(sigma, axis1=1, axis2=2) / 3.0)[:, None, None] * np.eye(3)
+    vm = np.sqrt(1.5 * np.einsum("nab,nab->n", dev, dev))
+    return float(vm[0]) if single else vm
+
+
 def init_case_velocity(kind: str, X0, *, length: float, omega0: float = 105.0,
                        v0=(10.0 * np.sqrt(3.0) / 2.0, 5.0, 0.0), axis_center=(0.0, 0.0)):
     """Column initial velocities (tlsph.py:233-254): twist = omega0 sin(pi y /
@@ -420,6 +437,11 @@ class SolidSystem:
         return g
 
     # -- diagnostics ------------------------------------------------------------
+    def von_mises_field(self):
+        """Per-particle von Mises stress (tlsph.py:210-212)."""
+        _, s = self.first_pk()
+        return von_mises(self.F, s)
+
     def energies(self):
         _, s = self.first_pk()
         eye = np.eye(self.dim)

@@ -159,6 +159,13 @@ int sphb_ell_fill(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
                   double h, double kappa, int32_t width, int32_t* nbr,
                   void* stream);
 
+/* Engine-order row sort (no reference counterpart; a layout choice): each
+ * row's entries reordered by displacement quantised at `spacing` (slow axis
+ * first), ties by index, so lattice rows list their offsets in one order and
+ * warp gathers coalesce.  Rows longer than 192 set *err = 1. */
+int sphb_ell_sort_rows(const sphb_grid* g, int64_t n, const double* ws, int32_t* nbr,
+                       const int32_t* cnt, double spacing, int32_t* err, void* stream);
+
 /* Moment matrices M_i (correction.py:35-52) straight from the ELL list,
  * sorted order, exact geometry; bit-identical rows to sphb_moment_matrices
  * on the CSR without materialising r and e. */

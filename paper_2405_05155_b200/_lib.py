@@ -159,6 +159,7 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
+    "sphb_ell_sort_rows": (C.c_int, [P, I64, P, P, P, F64, P, P]),
     "sphb_weak_gradient": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_shape_sdf": (C.c_int, [P, I64, P, P, P, P]),
     "sphb_relax_confine": (C.c_int, [P, I64, P, F64, P, P, I32, F64, P, P, P]),

@@ -20,6 +20,7 @@
 //           2D: {b00, b01, b11, -}; 1D: {b00, ...}
 //   S[i]  = {v0, v1, v2, rho}   (primitive state; 2D: {v0, v1, rho, 0})
 //   M[i]  = {m0, m1, m2, 0}     (momentum per unit volume)
+#include <cuda_pipeline.h>
 #include <stdlib.h>
 
 #include "wc_common.cuh"
@@ -78,6 +79,26 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
   }
   const int64_t i = P.row0 + (blk * blockDim.x + threadIdx.x) / G;
   const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
+
+  // Stage the block's ELL columns in shared memory first (LDGSTS, one
+  // coalesced 4-byte copy per row and pass-list slot): the index stream then
+  // costs one DRAM round trip per block instead of one per loop iteration,
+  // and the loop's dependent chain starts at a 30-cycle LDS.
+  extern __shared__ int32_t s_nbr[];     // [width][kThreads / G]
+  constexpr int RB = kThreads / G;       // rows per block
+  {
+    const int64_t base = P.row0 + blk * RB;
+    const int64_t lim = P.row0 + P.nrows;
+    for (int e = threadIdx.x; e < P.width * RB; e += kThreads) {
+      const int k = e / RB, r = e % RB;
+      if (base + r < lim)
+        __pipeline_memcpy_async(s_nbr + e, nbr + (int64_t)k * n + base + r, sizeof(int32_t));
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    __syncthreads();
+  }
+  const int32_t* __restrict__ srow = s_nbr + (threadIdx.x / G);
   const double c = P.c_art;
   double dr = 0.0;
   double dm[D], wf[D];
@@ -104,10 +125,9 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     }
 
     const int32_t m = cnt[i];
-    const int32_t* __restrict__ row = nbr + i;
 #pragma unroll 2
     for (int32_t k = gl; k < m; k += G) {
-      const int64_t j = row[(int64_t)k * n];
+      const int64_t j = srow[k * RB];
       double xj[D], vol_j, vj[D], rho_j;
       unpack_x<D>(ldg4(X + j), xj, vol_j);
       unpack_s<D>(ldg4(S_in + j), vj, rho_j);
@@ -403,8 +423,14 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
+  const size_t smem_idx = (size_t)p->width * (kThreads / group) * sizeof(int32_t);
+  if (smem_idx > 200 * 1024) return SPHB_ERR_ARG;
 #define SPHB_STAGE_W(D, G, MB, W)                                                          \
-  k_wc_stage<D, G, MB, W><<<sphb_blocks(p->nrows * G, kThreads), kThreads, 0, st>>>(          \
+  if (smem_idx > 48 * 1024)                                                                \
+    SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                         (int)smem_idx));                                  \
+  k_wc_stage<D, G, MB, W><<<sphb_blocks(p->nrows * G, kThreads), kThreads, smem_idx, st>>>( \
       *p, K, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                \
   break
 #define SPHB_STAGE(D, G, MB) SPHB_STAGE_W(D, G, MB, false)

@@ -39,6 +39,7 @@ import numpy as np
 from . import _lib
 from .kernels import CODE_WENDLAND, KernelSpec
 from .neighbors import (NeighborList, TilePlan, bin_particles, csr_from_bins, ell_from_bins,
+                        engine_order,
                         make_grid)
 
 IDEAL_GAS = "ideal-gas"
@@ -271,6 +272,18 @@ class EulerianSolver:
         b = b.contiguous()
         if _slab is not None:       # halo rows take B from their owners
             _slab.exchange(_dist, [b])
+        # engine storage order (neighbors.engine_order): lattice order +
+        # displacement-sorted rows, so warp gathers coalesce on lattices
+        variant = "geo" if self._ideal else os.environ.get("SPHB_WC_KERNEL", "global")
+        self.order = self.bins
+        if (_slab is None and variant != "tiled"
+                and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell"):
+            self.order, self.nbr, self.cnt = engine_order(self.bins, self.nbr, self.cnt,
+                                                          self.width)
+            b = b[self.order.q].contiguous()
+            vol_s = vol_s[self.order.q]
+            self.perm = self.order.perm.long()
+            self.rank = self.order.rank()
         self._ghost_setup(ghosts, dev)
         if ghosts is not None:      # ghosts inherit their source's B (eulerian.py:499-501)
             b[self._g_sorted.long()] = b[self._g_src_sorted.long()]
@@ -287,12 +300,12 @@ class EulerianSolver:
             else:
                 plane1[:, col - 4] = bs[:, a, c]
 
-        ws = self.bins.ws
+        ws = self.order.ws
         self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
-        # lanes per particle (scripts/tune_wc.py sweep on B200, 192^3 TGV-3D:
-        # one lane per particle is best for 32-entry rows, two lanes tie for
-        # 80-entry rows; profiles/r01_tune_wc.md)
-        self.group = 1 if self.width <= 40 else 2
+        # lanes per particle (scripts/tune_wc.py sweep on B200, 256^3 TGV-3D,
+        # smem-staged indices + engine order: one lane per particle is best
+        # for both 32- and 80-entry rows; profiles/r01_tune_wc.md)
+        self.group = 1
         if os.environ.get("SPHB_WC_GROUP"):      # tuning override
             self.group = int(os.environ["SPHB_WC_GROUP"])
         # Stage-kernel variant (SPHB_WC_KERNEL=global|geo|tiled):
@@ -302,7 +315,6 @@ class EulerianSolver:
         #          (2d+1) doubles per pair, reference arithmetic without FMA:
         #          the closest reproduction of the reference's roundings);
         #   tiled  shared-memory staging variant of `global`.
-        variant = "geo" if self._ideal else os.environ.get("SPHB_WC_KERNEL", "global")
         geo_bytes = (2 * self.dim + 1) * self.width * self.n * 8
         self.variant = variant
         self.geo = None
@@ -310,7 +322,7 @@ class EulerianSolver:
             self.geo = torch.empty(geo_bytes // 8, dtype=torch.float64, device=dev)
             k = _lib.kernel_struct(kernel)
             _lib.call("sphb_wc_geometry", ctypes.byref(self.grid), self.n,
-                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.order.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
                       self.cnt.data_ptr(), self.width, b.data_ptr(),
                       vol_s.contiguous().data_ptr(), ctypes.byref(k), self.geo.data_ptr(),
                       _lib.stream_ptr())
@@ -338,7 +350,7 @@ class EulerianSolver:
                 raise NotImplementedError("wall-force tagging runs in the global WC kernel")
             tag = np.zeros(self.n, dtype=np.int8)
             tag[np.asarray(wall_force_tag, dtype=np.int64)] = 1
-            perm = self.bins.perm.cpu().numpy()
+            perm = self.order.perm.cpu().numpy()
             self._wall_tag = _lib.to_device(np.ascontiguousarray(tag[perm]), torch.int8)
             self._wf_dev = torch.zeros(3, dtype=torch.float64, device=dev)
             self._wf_count = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -410,7 +422,7 @@ class EulerianSolver:
         else:
             rho_d = _lib.to_device(rho, torch.float64)
             mom_d = _lib.to_device(mom, torch.float64).reshape(self.n, self.dim)
-        _lib.call("sphb_wc_pack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+        _lib.call("sphb_wc_pack_state", self.n, self.dim, self.order.perm.data_ptr(),
                   rho_d.data_ptr(), mom_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(),
                   _lib.stream_ptr())
         if self.precision == "fp32":
@@ -421,7 +433,7 @@ class EulerianSolver:
 
     def read_state(self, rho_out, mom_out) -> None:
         """Write (rho, mom) in caller order into host tensors (pinned: async)."""
-        _lib.call("sphb_wc_unpack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+        _lib.call("sphb_wc_unpack_state", self.n, self.dim, self.order.perm.data_ptr(),
                   self.S.data_ptr(), self.M.data_ptr(), self._rho_io.data_ptr(),
                   self._mom_io.data_ptr(), _lib.stream_ptr())
         rho_out.copy_(self._rho_io, non_blocking=True)
@@ -803,7 +815,7 @@ class _HLLCSolver(EulerianSolver):
         rho_d = _lib.to_device(rho, torch.float64)
         mom_d = _lib.to_device(mom, torch.float64).reshape(self.n, self.dim)
         e_d = _lib.to_device(etot, torch.float64)
-        _lib.call("sphb_hllc_pack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+        _lib.call("sphb_hllc_pack_state", self.n, self.dim, self.order.perm.data_ptr(),
                   _lib.ptr(self._interior), self.eos.gamma, rho_d.data_ptr(), mom_d.data_ptr(),
                   e_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(), self.Q.data_ptr(),
                   self.scalars.data_ptr(), self.err.data_ptr(), _lib.stream_ptr())
@@ -811,7 +823,7 @@ class _HLLCSolver(EulerianSolver):
         self._state_host = None
 
     def read_state(self, rho_out, mom_out, etot_out=None) -> None:
-        _lib.call("sphb_hllc_unpack_state", self.n, self.dim, self.bins.perm.data_ptr(),
+        _lib.call("sphb_hllc_unpack_state", self.n, self.dim, self.order.perm.data_ptr(),
                   self.S.data_ptr(), self.M.data_ptr(), self.Q.data_ptr(),
                   self._rho_io.data_ptr(), self._mom_io.data_ptr(), self._E_io.data_ptr(),
                   _lib.stream_ptr())

@@ -17,6 +17,8 @@ materialised on first access.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -247,6 +249,79 @@ def ell_from_bins(bins: CellBins, h: float, kappa: float):
                   bins.cell_end.data_ptr(), float(h), float(kappa), width, nbr.data_ptr(),
                   _lib.stream_ptr())
     return nbr, cnt[:n], width
+
+
+class EngineOrder:
+    """Storage order of the stage engines (a layout choice, no reference
+    counterpart): particles sorted by a lattice-spacing key (slow axis
+    slowest, axis 0 fastest) instead of by cell, so that on lattices
+    consecutive rows are consecutive lattice sites.  Same fields as CellBins
+    where the engines read them; `q` maps engine position -> cell-sorted
+    position for per-particle arrays built in cell order."""
+
+    def __init__(self, grid, n, ws, perm, q):
+        self.grid, self.n, self.dim = grid, n, grid.dim
+        self.ws, self.perm, self.q = ws, perm, q
+
+    def rank(self):
+        torch = _lib.torch_cuda()
+        r = torch.empty(self.n, dtype=torch.int64, device=self.perm.device)
+        r[self.perm.long()] = torch.arange(self.n, device=self.perm.device)
+        return r
+
+
+def engine_order(bins: CellBins, nbr, cnt, width: int, spacing: float | None = None,
+                 tile=None):
+    """Re-store binned particles in lattice order and remap their ELL list.
+
+    The rows are then sorted by quantised displacement (sphb_ell_sort_rows),
+    so on a lattice every row lists the same offsets in the same order and
+    the lanes of a warp gather consecutive records.  The pair sets are
+    unchanged; only storage and summation order differ.  Returns
+    (EngineOrder, nbr, cnt).
+    """
+    torch = _lib.torch_cuda()
+    n, d, g = bins.n, bins.dim, bins.grid
+    dev = bins.perm.device
+    ws = bins.ws
+    if n == 0:
+        return EngineOrder(g, n, ws, bins.perm, torch.zeros(0, dtype=torch.int64, device=dev)), \
+            nbr, cnt
+    if spacing is None:            # mean spacing of the set
+        ext = ([g.box[a] for a in range(d)] if g.periodic
+               else [max(float(ws[a].max().item()), 1e-300) for a in range(d)])
+        spacing = float(np.prod(ext) / n) ** (1.0 / d)
+    k = torch.floor(ws * (1.0 / spacing)).to(torch.int64).clamp_(min=0)
+    if tile is None:
+        env = os.environ.get("SPHB_ENGINE_TILE", "")
+        tile = tuple(int(v) for v in env.split("x")) if env else ()
+    tile = tuple(tile) + (1,) * (d - len(tile))
+    # tiles of tile[0] x tile[1] x ... sites, tiles in lattice order, sites
+    # inside a tile in lattice order (axis 0 fastest)
+    kt = torch.stack([k[a] // tile[a] for a in range(d)])
+    kr = torch.stack([k[a] % tile[a] for a in range(d)])
+    top = kt.max(dim=1).values + 1
+    key = kt[d - 1].clone()
+    for a in range(d - 2, -1, -1):
+        key = key * top[a] + kt[a]
+    for a in range(d - 1, -1, -1):
+        key = key * tile[a] + kr[a]
+    q = torch.sort(key, stable=True).indices
+    qinv = torch.empty(n, dtype=torch.int64, device=dev)
+    qinv[q] = torch.arange(n, device=dev)
+    cnt_e = cnt[q].contiguous()
+    nbr_e = torch.zeros_like(nbr)
+    for r in range(width):
+        col = nbr[r, q].long()
+        ok = cnt_e > r
+        nbr_e[r] = torch.where(ok, qinv[torch.where(ok, col, 0)], 0).to(torch.int32)
+    ws_e = ws[:, q].contiguous()
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("sphb_ell_sort_rows", C_ref(g), n, ws_e.data_ptr(), nbr_e.data_ptr(),
+              cnt_e.data_ptr(), float(spacing), err.data_ptr(), _lib.stream_ptr())
+    if int(err.item()):
+        return EngineOrder(g, n, ws, bins.perm, torch.arange(n, device=dev)), nbr, cnt
+    return EngineOrder(g, n, ws_e, bins.perm[q].contiguous(), q), nbr_e, cnt_e
 
 
 # ---------------------------------------------------------- reference API

@@ -53,17 +53,21 @@ def main():
     if args.one:
         one(args.n_side, args.kernel, args.steps)
         return
-    variants = [("global", 1, 4, 0), ("global", 1, 5, 0), ("global", 2, 5, 0),
-                ("global", 1, 6, 0)]
-    for kern, g, mb, sw in variants:
+    variants = [("cell", "global", 1, 4, 0), ("lattice", "global", 1, 4, 0),
+                ("lattice", "global", 2, 4, 0), ("lattice", "global", 1, 6, 0),
+                ("lattice", "geo", 1, 4, 0), ("lattice", "global", 1, 5, 0)]
+    if os.environ.get("TUNE_VARIANTS"):
+        variants = [tuple(v.split(":")[:2]) + tuple(int(x) for x in v.split(":")[2:])
+                    for v in os.environ["TUNE_VARIANTS"].split(",")]
+    for order, kern, g, mb, sw in variants:
         env = dict(os.environ, SPHB_WC_KERNEL=kern, SPHB_WC_GROUP=str(g), SPHB_WC_MINB=str(mb),
-                   SPHB_TILE_GROUP=str(g), SPHB_SWIZZLE=str(sw))
+                   SPHB_TILE_GROUP=str(g), SPHB_SWIZZLE=str(sw), SPHB_ENGINE_ORDER=order)
         out = subprocess.run([sys.executable, __file__, "--one", "--n-side", str(args.n_side),
                               "--kernel", args.kernel, "--steps", str(args.steps)], env=env,
                              capture_output=True, text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
-        print(json.dumps({"kernel": kern, "group": g, "minb": mb, "swizzle": sw, "result": line}),
-              flush=True)
+        print(json.dumps({"order": order, "kernel": kern, "group": g, "minb": mb, "swizzle": sw,
+                          "result": line}), flush=True)
 
 
 if __name__ == "__main__":

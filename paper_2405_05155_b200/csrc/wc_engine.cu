@@ -35,6 +35,8 @@ constexpr int kThreads = 128;
 // Per-launch constants folded on the host from sphb_wc_params.
 struct WCConst {
   double c2, c2rho0, eta_c, inv_h, c5s, half_cinv, hc, mu2;
+  double cg, cm;          // 0.5 c5s [V], mu2 c5s [V]: dW-scaled pair factors
+  double wrap_margin;     // particles farther than this from every periodic face never wrap
 };
 
 inline WCConst wc_const(const sphb_wc_params& p) {
@@ -47,6 +49,10 @@ inline WCConst wc_const(const sphb_wc_params& p) {
   k.half_cinv = 0.5 / p.c_art;
   k.hc = 0.5 * p.c_art;
   k.mu2 = 2.0 * p.mu;
+  const double v = p.uniform_vol ? p.vol_const : 1.0;
+  k.cg = 0.5 * k.c5s * v;
+  k.cm = k.mu2 * k.c5s * v;
+  k.wrap_margin = 1.0001 * p.kappa * p.h;
   return k;
 }
 
@@ -108,7 +114,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     // host-folded constants (kernel parameters live in the constant bank, so
     // the FP64 instructions read them as operands instead of registers)
     const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, inv_h = K.inv_h;
-    const double c5s = K.c5s, half_cinv = K.half_cinv, hc = K.hc;
+    const double half_cinv = K.half_cinv, hc = K.hc;
 
     double xi[D], vol_i, vi[D], rho_i;
     unpack_x<D>(X[i], xi, vol_i);
@@ -117,11 +123,17 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     Bi.load(B, n, i);
     const double p_i = fma(c2, rho_i, -c2rho0);
     const double hp_i = 0.5 * p_i, hrho_i = 0.5 * rho_i;
-    double hvi[D], hb[D];
+    double hvi[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      hvi[a] = 0.5 * vi[a];
-      hb[a] = 0.5 * P.box[a];
+    for (int a = 0; a < D; ++a) hvi[a] = 0.5 * vi[a];
+    // minimum image (neighbors.py:152-157) only matters within one cut-off
+    // of a periodic face: a warp-uniform per-particle test keeps the FP64
+    // compare/select work out of the loop for the bulk
+    bool wrap = false;
+    if (P.periodic) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        wrap = wrap || xi[a] < K.wrap_margin || xi[a] > P.box[a] - K.wrap_margin;
     }
 
     const int32_t m = cnt[i];
@@ -133,15 +145,16 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       unpack_s<D>(ldg4(S_in + j), vj, rho_j);
       Sym<D> Bj;
       Bj.load(B, n, j);
-      if (P.uniform_vol) vol_j = P.vol_const;
 
-      // geometry (neighbors.py:152-165, correction.py:102-108, eulerian.py:506-513)
+      // geometry (neighbors.py:152-165, correction.py:102-108, eulerian.py:506-513),
+      // kept in terms of dx: e = dx / r is folded into the scalar factors
       double dx[D];
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        double d = xi[a] - xj[a];
-        if (P.periodic && fabs(d) > hb[a]) d = d > 0.0 ? d - P.box[a] : d + P.box[a];
-        dx[a] = d;
+      for (int a = 0; a < D; ++a) dx[a] = xi[a] - xj[a];
+      if (wrap) {
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+          if (fabs(dx[a]) > 0.5 * P.box[a]) dx[a] = dx[a] > 0.0 ? dx[a] - P.box[a] : dx[a] + P.box[a];
       }
       double r2 = dx[0] * dx[0];
 #pragma unroll
@@ -149,55 +162,50 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       const double inv_r = rsqrt_nr(r2);
       const double q = r2 * inv_r * inv_h;
       const double t = fma(-0.5, q, 1.0);
-      const double dW = (c5s * q) * (t * t * t);        // (alpha/h) dP/dq
-      double e[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) e[a] = dx[a] * inv_r;
+      // dW V_j / r = c5s q t^3 V_j / r; gsc = 0.5 dW V_j / r, mv = mu viscv
+      double base = ((q * t) * (t * t)) * inv_r;
+      if (!P.uniform_vol) base *= vol_j;
+      const double gsc = K.cg * base;
+      const double mv = K.cm * base;
       Sym<D> Bs;
       Bi.add(Bj, Bs);
-      double g[D];
-      Bs.mv(e, g);
-      const double dWv = dW * vol_j;
-      const double gs = 0.5 * dWv;                      // 0.5 (B_i + B_j) e dW V_j
-#pragma unroll
-      for (int a = 0; a < D; ++a) g[a] *= gs;
-      const double mvisc = K.mu2 * dWv * inv_r;         // mu viscv
+      double G_[D];                                     // (B_i + B_j) dx
+      Bs.mv(dx, G_);
 
       // limited linearised Riemann problem along n = -e (eulerian.py:236-264):
       // du = u_l - u_r = (v_j - v_i).e; u* - ubar = b^2 (p_i - p_j) / (2 rbar c)
       double dv[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) dv[a] = vj[a] - vi[a];
-      double du = dv[0] * e[0];
+      double dud = dv[0] * dx[0];
 #pragma unroll
-      for (int a = 1; a < D; ++a) du = fma(dv[a], e[a], du);
+      for (int a = 1; a < D; ++a) dud = fma(dv[a], dx[a], dud);
+      const double du = dud * inv_r;
       double beta = du * eta_c;
       beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
       const double rbar = fma(0.5, rho_j, hrho_i);
       const double p_j = fma(c2, rho_j, -c2rho0);
-      double w = 0.0;
-      if (beta > 0.0) w = ((beta * beta) * (p_i - p_j) * half_cinv) * rcp_nr(rbar);
+      double wr = 0.0;                                  // (u* - ubar) / r
+      if (beta > 0.0) wr = ((beta * beta) * (p_i - p_j) * half_cinv) * (rcp_nr(rbar) * inv_r);
       const double p_star = fma((beta * rbar) * hc, du, fma(0.5, p_j, hp_i));
       double vs[D];
-      double sdot = 0.0;
+      double sg = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        vs[a] = fma(-w, e[a], fma(0.5, vj[a], hvi[a]));
-        sdot = fma(vs[a], g[a], sdot);
+        vs[a] = fma(-wr, dx[a], fma(0.5, vj[a], hvi[a]));
+        sg = fma(vs[a], G_[a], sg);
       }
-      const double rbar2 = -2.0 * rbar;
-      dr = fma(rbar2, sdot, dr);
-      const double rs2 = rbar2 * sdot, ps2 = -2.0 * p_star;
+      const double sdot = gsc * sg;                     // vs . gwv
+      const double rs2 = -2.0 * rbar * sdot;
+      dr += rs2;                                        // -2 rbar s
+      const double pg = (-2.0 * p_star) * gsc;
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const double fm = fma(rs2, vs[a], ps2 * g[a]);
-        dm[a] = fma(-mvisc, dv[a], dm[a] + fm);
-      }
+      for (int a = 0; a < D; ++a)
+        dm[a] = fma(-mv, dv[a], fma(pg, G_[a], fma(rs2, vs[a], dm[a])));
       if constexpr (WALL) {               // eulerian.py:262-264
         if (stage != 1 && P.wall_tag[j]) {
 #pragma unroll
-          for (int a = 0; a < D; ++a)
-            wf[a] -= fma(-mvisc, dv[a], fma(rs2, vs[a], ps2 * g[a]));
+          for (int a = 0; a < D; ++a) wf[a] -= fma(-mv, dv[a], fma(pg, G_[a], rs2 * vs[a]));
         }
       }
     }

@@ -8,6 +8,7 @@
 // matter how the translation unit is compiled.
 #pragma once
 
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -163,6 +164,23 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // ----------------------------------------------------------- reductions
+// Copy a block's ELL columns nbr[k * n + base + r] (k < width, r < RB) into
+// shared memory s_nbr[k * RB + r] with LDGSTS and wait: the pass list then
+// costs one DRAM round trip per block instead of one per loop iteration.
+template <int RB>
+__device__ __forceinline__ void stage_pass_list(const int32_t* __restrict__ nbr, int64_t n,
+                                                int64_t base, int64_t lim, int width,
+                                                int32_t* s_nbr) {
+  for (int e = threadIdx.x; e < width * RB; e += blockDim.x) {
+    const int k = e / RB, r = e % RB;
+    if (base + r < lim)
+      __pipeline_memcpy_async(s_nbr + e, nbr + (int64_t)k * n + base + r, sizeof(int32_t));
+  }
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
+  __syncthreads();
+}
+
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their int64 bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr),

@@ -196,6 +196,9 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
             const double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ int32_t s_nbr[];
+  stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads, P.row0 + P.nrows,
+                            P.width, s_nbr);
   if (i >= P.row0 + P.nrows) return;
   const double dt = scalars[0];
   const double hdt = 0.5 * dt;
@@ -217,9 +220,9 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
     for (int b = 0; b < D; ++b) m[a][b] = 0.0;
 
   const int32_t cn = cnt[i];
-  const int32_t* __restrict__ row = nbr + i;
+  const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
   for (int32_t k = 0; k < cn; ++k) {
-    const int64_t j = row[(int64_t)k * n];
+    const int64_t j = srow[k * kThreads];
     double vj[D], aj[D], g[D];
     bool fixed_j;
     load_vec_nc<D>(V, j, vj);
@@ -286,6 +289,9 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             int update_v) {
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ int32_t s_nbr[];
+  stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads, P.row0 + P.nrows,
+                            P.width, s_nbr);
   double speed = 0.0;
   if (i < P.row0 + P.nrows) {
     const double inv_h = 1.0 / P.h;
@@ -299,9 +305,9 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
 #pragma unroll
     for (int a = 0; a < D; ++a) { gsum[a] = 0.0; acc[a] = 0.0; }
     const int32_t cn = cnt[i];
-    const int32_t* __restrict__ row = nbr + i;
+    const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
     for (int32_t k = 0; k < cn; ++k) {
-      const int64_t j = row[(int64_t)k * n];
+      const int64_t j = srow[k * kThreads];
       double Qj[D][D];
       load_mat_nc<D>(Q, j, Qj);
       double g[D];
@@ -415,18 +421,29 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
     }                                                                      \
   } while (0)
 
-#define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                            \
-  do {                                                                            \
-    const bool geo_ = (GEOPTR) != nullptr;                                        \
-    switch (p->dim * 2 + (geo_ ? 1 : 0)) {                                        \
-      case 2: KERNEL<1, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
-      case 3: KERNEL<1, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
-      case 4: KERNEL<2, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
-      case 5: KERNEL<2, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
-      case 6: KERNEL<3, false><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;          \
-      case 7: KERNEL<3, true><<<GRID, TH, 0, st>>>(__VA_ARGS__); break;           \
-      default: return SPHB_ERR_ARG;                                               \
-    }                                                                             \
+// dynamic shared memory: the block's pass-list columns (stage_pass_list)
+#define TL_LAUNCH(KERNEL, GRID, TH, SMEM, ...)                                                   \
+  do {                                                                                         \
+    if ((SMEM) > 48 * 1024)                                                                    \
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)(SMEM)));                                      \
+    KERNEL<<<GRID, TH, SMEM, st>>>(__VA_ARGS__);                                               \
+  } while (0)
+
+#define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                                  \
+  do {                                                                                  \
+    const bool geo_ = (GEOPTR) != nullptr;                                              \
+    const size_t smem_ = (size_t)p->width * kThreads * sizeof(int32_t);                 \
+    if (smem_ > 200 * 1024) return SPHB_ERR_ARG;                                        \
+    switch (p->dim * 2 + (geo_ ? 1 : 0)) {                                              \
+      case 2: TL_LAUNCH((KERNEL<1, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
+      case 3: TL_LAUNCH((KERNEL<1, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
+      case 4: TL_LAUNCH((KERNEL<2, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
+      case 5: TL_LAUNCH((KERNEL<2, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
+      case 6: TL_LAUNCH((KERNEL<3, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
+      case 7: TL_LAUNCH((KERNEL<3, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
+      default: return SPHB_ERR_ARG;                                                     \
+    }                                                                                   \
   } while (0)
 
 extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,

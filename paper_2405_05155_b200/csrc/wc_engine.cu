@@ -92,18 +92,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
   // and the loop's dependent chain starts at a 30-cycle LDS.
   extern __shared__ int32_t s_nbr[];     // [width][kThreads / G]
   constexpr int RB = kThreads / G;       // rows per block
-  {
-    const int64_t base = P.row0 + blk * RB;
-    const int64_t lim = P.row0 + P.nrows;
-    for (int e = threadIdx.x; e < P.width * RB; e += kThreads) {
-      const int k = e / RB, r = e % RB;
-      if (base + r < lim)
-        __pipeline_memcpy_async(s_nbr + e, nbr + (int64_t)k * n + base + r, sizeof(int32_t));
-    }
-    __pipeline_commit();
-    __pipeline_wait_prior(0);
-    __syncthreads();
-  }
+  stage_pass_list<RB>(nbr, n, P.row0 + blk * RB, P.row0 + P.nrows, P.width, s_nbr);
   const int32_t* __restrict__ srow = s_nbr + (threadIdx.x / G);
   const double c = P.c_art;
   double dr = 0.0;

@@ -29,7 +29,8 @@ import numpy as np
 
 from . import _lib
 from .kernels import CODE_WENDLAND, KernelSpec
-from .neighbors import NeighborList, bin_particles, csr_from_bins, ell_from_bins, make_grid
+from .neighbors import (NeighborList, bin_particles, csr_from_bins, ell_from_bins, engine_order,
+                        make_grid)
 
 
 class SolidStateError(RuntimeError):
@@ -188,9 +189,17 @@ class SolidSystem:
         else:
             b0 = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d).contiguous()
             self.n_regularized = 0
+        # engine storage order (neighbors.engine_order) on one GPU
+        self.order = self.bins
+        if _slab is None and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell":
+            self.order, self.nbr, self.cnt = engine_order(self.bins, self.nbr, self.cnt,
+                                                          self.width)
+            b0 = b0[self.order.q].contiguous()
+            self.perm = self.order.perm.long()
+            self.rank = self.order.rank()
         self._B0_sorted = b0
         fixed_s = _lib.to_device(self.fixed.astype(np.float64), torch.float64)[self.perm]
-        self.X0rec = _vec_rec(self.bins.ws.t(), n, d, dev)
+        self.X0rec = _vec_rec(self.order.ws.t(), n, d, dev)
         self.X0rec[:, 3] = fixed_s
         self.B0rec = _mat_rec(b0, n, d, dev)
         eye = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d)
@@ -223,7 +232,7 @@ class SolidSystem:
             self.g0 = torch.empty(g0_bytes // 8, dtype=torch.float64, device=dev)
             k = _lib.kernel_struct(kernel)
             _lib.call("sphb_tl_geometry", ctypes.byref(self.grid), n,
-                      self.bins.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
+                      self.order.ws.contiguous().data_ptr(), self.nbr.data_ptr(),
                       self.cnt.data_ptr(), self.width, ctypes.byref(k), self.dp**d,
                       self.g0.data_ptr(), _lib.stream_ptr())
         self._g0_ptr = None if self.g0 is None else self.g0.data_ptr()

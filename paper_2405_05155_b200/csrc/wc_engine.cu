@@ -126,7 +126,10 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     }
 
     const int32_t m = cnt[i];
-#pragma unroll 2
+    // two pairs in flight per thread at the default register budget; one
+    // when a higher occupancy target (MINB > 4) caps the registers
+    constexpr int UNR = MINB <= 4 ? 2 : 1;
+#pragma unroll UNR
     for (int32_t k = gl; k < m; k += G) {
       const int64_t j = srow[k * RB];
       double xj[D], vol_j, vj[D], rho_j;
@@ -447,10 +450,12 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
     SPHB_LAUNCH_CHECK();
     return SPHB_OK;
   }
-  // SPHB_WC_MINB (tuning): 4 -> <=128 registers, 6 -> <=80, 8 -> <=64
+  // SPHB_WC_MINB (tuning): 4 -> <=128 registers, two pairs in flight;
+  // 5 (default, 3D) -> <=96 registers, one pair in flight, 20 warps/SM;
+  // 6 / 8 spill (profiles/r01_tune_wc.md)
   static int minb = [] {
     const char* e = getenv("SPHB_WC_MINB");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 5;
   }();
   const int key = p->dim * 256 + group * 16 + (p->dim == 3 ? minb : 4);
   switch (key) {
@@ -462,17 +467,9 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
     case 768 + 16 + 4: SPHB_STAGE(3, 1, 4);
     case 768 + 32 + 4: SPHB_STAGE(3, 2, 4);
     case 768 + 64 + 4: SPHB_STAGE(3, 4, 4);
-    case 768 + 128 + 4: SPHB_STAGE(3, 8, 4);
     case 768 + 16 + 5: SPHB_STAGE(3, 1, 5);
-    case 768 + 32 + 5: SPHB_STAGE(3, 2, 5);
     case 768 + 16 + 6: SPHB_STAGE(3, 1, 6);
-    case 768 + 32 + 6: SPHB_STAGE(3, 2, 6);
-    case 768 + 64 + 6: SPHB_STAGE(3, 4, 6);
-    case 768 + 128 + 6: SPHB_STAGE(3, 8, 6);
     case 768 + 16 + 8: SPHB_STAGE(3, 1, 8);
-    case 768 + 32 + 8: SPHB_STAGE(3, 2, 8);
-    case 768 + 64 + 8: SPHB_STAGE(3, 4, 8);
-    case 768 + 128 + 8: SPHB_STAGE(3, 8, 8);
     default: return SPHB_ERR_ARG;
   }
 #undef SPHB_STAGE

@@ -34,6 +34,9 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
+  extern __shared__ int32_t s_nbr[];
+  stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads, P.row0 + P.nrows,
+                            P.width, s_nbr);
   const double c_art = P.c_art;
   double speed = 0.0;
   int32_t flags = 0;
@@ -62,7 +65,7 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
     for (int a = 0; a < D; ++a) dm[a] = 0.0;
     const int32_t m = cnt[i];
     for (int32_t k = 0; k < m; ++k) {
-      const int64_t j = nbr[(int64_t)k * n + i];
+      const int64_t j = s_nbr[k * kThreads + threadIdx.x];
       const float4 xj4 = ldg4f(X + j);
       const float4 sj4 = ldg4f(S32_in + j);
       const float4 bj4 = ldg4f(reinterpret_cast<const float4*>(B) + j);
@@ -219,8 +222,14 @@ extern "C" int sphb_wc_stage_f32(const sphb_wc_params* p, int32_t stage, const f
   if (p->nrows == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = sphb_blocks(p->nrows, kThreads);
+  const size_t smem = (size_t)p->width * kThreads * sizeof(int32_t);
+  if (smem > 200 * 1024) return SPHB_ERR_ARG;
 #define SPHB_F32(D)                                                                         \
-  k_wc_stage_f32<D><<<grid, kThreads, 0, st>>>(                                             \
+  if (smem > 48 * 1024)                                                                     \
+    SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage_f32<D>,                                 \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                         (int)smem));                                       \
+  k_wc_stage_f32<D><<<grid, kThreads, smem, st>>>(                                          \
       *p, stage, (const float4*)x32, b32, nbr, cnt, (const float4*)s32_in,                  \
       (const double4*)s_n, (const double4*)m_n, (float4*)s32_out, (double4*)s_out,          \
       (double4*)m_out, scalars, err)

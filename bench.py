@@ -40,10 +40,10 @@ METRIC = "particle-steps/s and pair-interactions/s at 1.6h vs 2h; % of HBM roofl
 # compulsory FP64 bytes per particle-step for C5 (stage 1: x 24
 # + B 48 + rho 8 + mom 24 read, 32 write = 136; stage 2: + U^n 32 = 168)
 BYTES_STAGE = {1: 136, 2: 168}
-# FP64 operations per directed pair of the fused stage kernel, counted from the
-# source of k_wc_stage (geometry ~45 incl. rsqrt, flux ~70); replaced by SASS
-# counts in profiles/ when ncu is run.
-FLOPS_PER_PAIR_EST = 120
+# FP64 flops per directed pair of the fused stage kernel, from the SASS of
+# k_wc_stage<3,1,5> (37 DFMA + 27 DMUL + 13 DADD per pair in the loop body,
+# plus the limiter branch ~3; profiles/r01_ncu_c5_256.md v3)
+FLOPS_PER_PAIR_EST = 117
 
 
 def traffic_per_launch(kernel: str):
@@ -219,7 +219,8 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
         st[stage].append(a.elapsed_time(b))
     solver.timer = None
     kernel = {"geo": "k_wc_stage_geo<3>", "tiled": "k_wc_stage_tiled<3,%d>" % solver.group,
-              "global": "k_wc_stage<3,%d,4>" % solver.group}[solver.variant]
+              "global": "k_wc_stage<3,%d,%s>" % (solver.group,
+                                                 os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None}
 
@@ -366,7 +367,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
                      "traffic": traffic_per_launch(L["kernel"]) if world == 1 else None,
-                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md",
+                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md (v2)",
                      "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": avg_stage_ms,

@@ -54,6 +54,142 @@ k_relax_accel(sphb_grid g, int64_t n, const double* __restrict__ ws,
   }
 }
 
+// Warp-per-particle variant for small sets (C1: 10k particles would fill
+// half the SMs with one warp each).  The 32 lanes take consecutive
+// candidates of the stencil walk (same order as for_each_neighbor: stencil
+// offsets with axis 0 fastest, ascending index inside a cell) and evaluate
+// the expensive per-pair terms in parallel; the terms are then added into
+// the row sum strictly in candidate order (ballot + shuffles), so the sums
+// round exactly as the thread-per-particle kernel and the reference's CSR
+// loop do.
+template <int D>
+__global__ void __launch_bounds__(512)
+k_relax_accel_warp(sphb_grid g, int64_t n, const double* __restrict__ ws,
+                   const int32_t* __restrict__ perm, const int32_t* __restrict__ cs,
+                   const int32_t* __restrict__ ce, const double* __restrict__ vols,
+                   sphb_kernel k, double p0, double rho0, double* __restrict__ acc,
+                   double* __restrict__ sums) {
+  constexpr int noff = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  const int lane = threadIdx.x & 31;
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double norm = 0.0, isolated = 0.0;
+  if (s < n) {
+    double wi[D];
+    int64_t ci[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      wi[a] = ws[(int64_t)a * n + s];
+      ci[a] = cell_coord(g, a, wi[a]);
+    }
+    const double scale = k.alpha / k.h;
+    double a_[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) a_[a] = 0.0;
+    int32_t count = 0;
+    // stencil cells, 32 at a time (one per lane), in the reference's order
+    for (int kb = 0; kb < noff; kb += 32) {
+      const int kc = kb + lane;
+      int32_t t0 = 0, len = 0;
+      if (kc < noff) {
+        int rem = kc;
+        int64_t flat = 0;
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const int off = rem % 3 - 1;
+          rem /= 3;
+          int64_t c = ci[a] + off;
+          if (g.periodic) c = py_mod(c, g.ncell[a]);
+          else if (c < 0 || c >= g.ncell[a]) ok = false;
+          flat += c * g.strides[a];
+        }
+        if (ok) {
+          t0 = cs[flat];
+          len = ce[flat] - t0;
+        }
+      }
+      // exclusive prefix of the cell lengths over the lanes
+      int32_t start = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, start, o);
+        if (lane >= o) start += v;
+      }
+      const int32_t total = __shfl_sync(0xffffffffu, start, 31);
+      start -= len;
+      const int ncell_here = noff - kb < 32 ? noff - kb : 32;
+      for (int32_t cb = 0; cb < total; cb += 32) {
+        const int32_t c = cb + lane;
+        // candidate c lives in the last cell whose start <= c
+        int32_t t = -1;
+        for (int q = 0; q < ncell_here; ++q) {
+          const int32_t sq = __shfl_sync(0xffffffffu, start, q);
+          const int32_t lq = __shfl_sync(0xffffffffu, len, q);
+          const int32_t tq = __shfl_sync(0xffffffffu, t0, q);
+          if (c >= sq && c < sq + lq) t = tq + (c - sq);
+        }
+        double term[D];
+        bool valid = false, in_cut = false;
+        if (t >= 0 && t != s) {
+          double dx[D];
+          double r2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            dx[a] = min_image(__dsub_rn(wi[a], ws[(int64_t)a * n + t]), g.box[a], g.periodic);
+            r2 = __dadd_rn(r2, __dmul_rn(dx[a], dx[a]));
+          }
+          if (r2 <= g.cut2 && r2 > 0.0) {
+            in_cut = true;
+            const double r = sqrt(r2);
+            const double q = r / k.h;
+            if (!(q > k.kappa)) {
+              valid = true;
+              const double coeff =
+                  -2.0 * p0 * vols[perm[t]] * scale * profile_deriv(k.code, q) / rho0;
+#pragma unroll
+              for (int a = 0; a < D; ++a) term[a] = coeff * (dx[a] / r);
+            }
+          }
+        }
+        count += __popc(__ballot_sync(0xffffffffu, in_cut));
+        unsigned m = __ballot_sync(0xffffffffu, valid);
+        while (m) {                      // candidate order = lane order
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+#pragma unroll
+          for (int a = 0; a < D; ++a) a_[a] += __shfl_sync(0xffffffffu, term[a], src);
+        }
+      }
+    }
+    if (lane == 0) {
+      const int64_t i = perm[s];
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[i * D + a] = a_[a];
+      double s2 = a_[0] * a_[0];
+#pragma unroll
+      for (int a = 1; a < D; ++a) s2 += a_[a] * a_[a];
+      norm = sqrt(s2);
+      isolated = count == 0 ? 1.0 : 0.0;
+    }
+  }
+  // one particle per warp: the per-particle values sit in lane 0 of each warp
+  __shared__ double red[2][16];
+  if (lane == 0) {
+    red[0][threadIdx.x >> 5] = norm;
+    red[1][threadIdx.x >> 5] = isolated;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    atomicAdd(sums, a);
+    if (b != 0.0) atomicAdd(sums + 1, b);
+  }
+}
+
 template <int D>
 __global__ void k_relax_update(int64_t n, const double* __restrict__ acc, double dt2, double cap,
                                double b0, double b1, double b2, double* __restrict__ pos) {
@@ -76,6 +212,9 @@ __global__ void k_relax_update(int64_t n, const double* __restrict__ acc, double
   for (int a = 0; a < D; ++a) pos[i * D + a] = np_remainder(pos[i * D + a] + dx[a], box[a]);
 }
 
+// sets up to this size run warp-per-particle (the GPU has 148 SMs x 64 warps)
+constexpr int64_t kWarpPerParticleMax = 1 << 17;
+
 }  // namespace
 
 extern "C" int sphb_relax_accel(const sphb_grid* g, int64_t n, const double* ws,
@@ -86,6 +225,18 @@ extern "C" int sphb_relax_accel(const sphb_grid* g, int64_t n, const double* ws,
   cudaStream_t st = (cudaStream_t)stream;
   SPHB_CUDA_CHECK(cudaMemsetAsync(sums, 0, 2 * sizeof(double), st));
   if (n == 0) return SPHB_OK;
+  if (n <= kWarpPerParticleMax) {   // small sets: one warp per particle
+    const int TW = 512;
+    const unsigned grid = (unsigned)((n * 32 + TW - 1) / TW);
+    switch (g->dim) {
+      case 1: k_relax_accel_warp<1><<<grid, TW, 0, st>>>(*g, n, ws, perm, cs, ce, vols, *k, p0, rho0, acc, sums); break;
+      case 2: k_relax_accel_warp<2><<<grid, TW, 0, st>>>(*g, n, ws, perm, cs, ce, vols, *k, p0, rho0, acc, sums); break;
+      case 3: k_relax_accel_warp<3><<<grid, TW, 0, st>>>(*g, n, ws, perm, cs, ce, vols, *k, p0, rho0, acc, sums); break;
+      default: return SPHB_ERR_ARG;
+    }
+    SPHB_LAUNCH_CHECK();
+    return SPHB_OK;
+  }
   const int T = 128;
   switch (g->dim) {
     case 1: k_relax_accel<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, n, ws, perm, cs, ce, vols, *k, p0, rho0, acc, sums); break;

@@ -276,14 +276,19 @@ class EulerianSolver:
         # displacement-sorted rows, so warp gathers coalesce on lattices
         variant = "geo" if self._ideal else os.environ.get("SPHB_WC_KERNEL", "global")
         self.order = self.bins
-        if (_slab is None and variant != "tiled"
-                and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell"):
+        # the fine key's spacing must be a global quantity (slab ranks must
+        # order a shared layer identically): the particle volume's edge
+        if (variant != "tiled" and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell"
+                and (uniform or _slab is None)):
+            spacing = (float(vol[0]) ** (1.0 / self.dim)) if uniform and self.n else None
             self.order, self.nbr, self.cnt = engine_order(self.bins, self.nbr, self.cnt,
-                                                          self.width)
+                                                          self.width, spacing=spacing)
             b = b[self.order.q].contiguous()
             vol_s = vol_s[self.order.q]
             self.perm = self.order.perm.long()
             self.rank = self.order.rank()
+            if _slab is not None:   # owned / halo slices in the new order
+                _slab.attach(self.order.perm.cpu().numpy())
         self._ghost_setup(ghosts, dev)
         if ghosts is not None:      # ghosts inherit their source's B (eulerian.py:499-501)
             b[self._g_sorted.long()] = b[self._g_src_sorted.long()]

@@ -296,15 +296,23 @@ def engine_order(bins: CellBins, nbr, cnt, width: int, spacing: float | None = N
         env = os.environ.get("SPHB_ENGINE_TILE", "")
         tile = tuple(int(v) for v in env.split("x")) if env else ()
     tile = tuple(tile) + (1,) * (d - len(tile))
-    # tiles of tile[0] x tile[1] x ... sites, tiles in lattice order, sites
-    # inside a tile in lattice order (axis 0 fastest)
+    # slowest component: the cell layer along the grid's storage slow axis
+    # (as the binning computes it), so a slab rank's owned block and halo
+    # layers stay contiguous; then tiles of tile[0] x tile[1] x ... sites in
+    # lattice order, sites inside a tile in lattice order; the slow axis is
+    # the slowest lattice axis, axis 0 (or the next) the fastest
+    sa = int(g.slow_axis)
+    axes = [sa] + [a for a in range(d - 1, -1, -1) if a != sa]
+    layer = torch.floor(ws[sa] * g.inv_cell[sa]).to(torch.int64)
+    layer = (torch.remainder(layer, int(g.ncell[sa])) if g.periodic
+             else layer.clamp(0, int(g.ncell[sa]) - 1))
     kt = torch.stack([k[a] // tile[a] for a in range(d)])
     kr = torch.stack([k[a] % tile[a] for a in range(d)])
     top = kt.max(dim=1).values + 1
-    key = kt[d - 1].clone()
-    for a in range(d - 2, -1, -1):
+    key = layer.clone()
+    for a in axes:
         key = key * top[a] + kt[a]
-    for a in range(d - 1, -1, -1):
+    for a in axes:
         key = key * tile[a] + kr[a]
     q = torch.sort(key, stable=True).indices
     qinv = torch.empty(n, dtype=torch.int64, device=dev)

@@ -191,12 +191,14 @@ class SolidSystem:
             self.n_regularized = 0
         # engine storage order (neighbors.engine_order) on one GPU
         self.order = self.bins
-        if _slab is None and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell":
+        if os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell":
             self.order, self.nbr, self.cnt = engine_order(self.bins, self.nbr, self.cnt,
-                                                          self.width)
+                                                          self.width, spacing=self.dp)
             b0 = b0[self.order.q].contiguous()
             self.perm = self.order.perm.long()
             self.rank = self.order.rank()
+            if _slab is not None:   # owned / halo slices in the new order
+                _slab.attach(self.order.perm.cpu().numpy())
         self._B0_sorted = b0
         fixed_s = _lib.to_device(self.fixed.astype(np.float64), torch.float64)[self.perm]
         self.X0rec = _vec_rec(self.order.ws.t(), n, d, dev)

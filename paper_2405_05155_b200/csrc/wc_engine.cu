@@ -126,17 +126,12 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     }
 
     const int32_t m = cnt[i];
-    // two pairs in flight per thread at the default register budget; one
-    // when a higher occupancy target (MINB > 4) caps the registers
-    constexpr int UNR = MINB <= 4 ? 2 : 1;
-#pragma unroll UNR
-    for (int32_t k = gl; k < m; k += G) {
-      const int64_t j = srow[k * RB];
+
+    // one directed pair (i, j) from j's records
+    auto pair = [&](const int64_t j, const double4 xr, const double4 sr, const Sym<D>& Bj) {
       double xj[D], vol_j, vj[D], rho_j;
-      unpack_x<D>(ldg4(X + j), xj, vol_j);
-      unpack_s<D>(ldg4(S_in + j), vj, rho_j);
-      Sym<D> Bj;
-      Bj.load(B, n, j);
+      unpack_x<D>(xr, xj, vol_j);
+      unpack_s<D>(sr, vj, rho_j);
 
       // geometry (neighbors.py:152-165, correction.py:102-108, eulerian.py:506-513),
       // kept in terms of dx: e = dx / r is folded into the scalar factors
@@ -200,6 +195,17 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
           for (int a = 0; a < D; ++a) wf[a] -= fma(-mv, dv[a], fma(pg, G_[a], rs2 * vs[a]));
         }
       }
+    };
+
+    // two pairs in flight per thread at the 128-register budget (MINB 4);
+    // one at the default occupancy target (MINB 5: 96 registers, 20 warps)
+    constexpr int UNR = MINB <= 4 ? 2 : 1;
+#pragma unroll UNR
+    for (int32_t k = gl; k < m; k += G) {
+      const int64_t j = srow[k * RB];
+      Sym<D> bj;
+      bj.load(B, n, j);
+      pair(j, ldg4(X + j), ldg4(S_in + j), bj);
     }
   }
   if constexpr (WALL) {

@@ -370,6 +370,7 @@ class EulerianSolver:
         # blocks on one contiguous region share neighbour rows through L2);
         # off by default, SPHB_SWIZZLE=<sm count> to enable
         p.swizzle = int(os.environ.get("SPHB_SWIZZLE", "0"))
+
         self._cfl_h = self.cfl * kernel.h                      # eulerian.py:560
 
         self.S = torch.empty((self.n, 4), dtype=torch.float64, device=dev)

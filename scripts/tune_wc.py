@@ -33,6 +33,17 @@ def one(n_side, kernel, steps):
                        cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
     s.advance(3)
     torch.cuda.synchronize()
+    if os.environ.get("SPHB_EXPERIMENT"):     # raw stage-1 launches into scratch
+        out = torch.empty_like(s.S)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.params.reserved = int(os.environ["SPHB_EXPERIMENT"])
+        e0.record()
+        for _ in range(10):
+            s._launch_stage_raw(1, s.S, s.S, s.M, out, None)
+        e1.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"experiment": s.params.reserved, "stage_ms": e0.elapsed_time(e1) / 10}))
+        return
     s.timer = []
     s.advance(steps)
     torch.cuda.synchronize()

@@ -143,24 +143,23 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
   return v;
 }
 
-// 1/sqrt(x) and 1/x for normal positive doubles: MUFU seed + two Newton steps
-// (relative error ~1 ulp); no special-value handling, so no slow-path call.
+// 1/sqrt(x) and 1/x for normal positive doubles: MUFU seed (~2^-23) and
+// one third-order correction (error ~eps^3, below double rounding), i.e. the
+// accuracy of two Newton steps with a shorter dependent chain; no
+// special-value handling, so no slow-path call.
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-(x * y), y, 1.0);
-  y = fma(0.5 * y, e, y);
-  e = fma(-(x * y), y, 1.0);
-  return fma(0.5 * y, e, y);
+  const double e = fma(-(x * y), y, 1.0);         // 1 - x y^2
+  // y (1 + e/2 + 3 e^2 / 8)
+  return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
+  const double e = fma(-x, y, 1.0);               // 1 - x y
+  return fma(y, fma(e, e, e), y);                  // y (1 + e + e^2)
 }
 
 // ----------------------------------------------------------- reductions

@@ -35,7 +35,8 @@ constexpr int kThreads = 128;
 // Per-launch constants folded on the host from sphb_wc_params.
 struct WCConst {
   double c2, c2rho0, eta_c, inv_h, c5s, half_cinv, hc, mu2;
-  double cg, cm;          // 0.5 c5s [V], mu2 c5s [V]: dW-scaled pair factors
+  double cg, cm;          // 0.5 c5s [V] / h, mu2 c5s [V] / h: t^3-scaled pair factors
+  double mhalf_inv_h;     // -0.5 / h
   double wrap_margin;     // particles farther than this from every periodic face never wrap
 };
 
@@ -50,8 +51,9 @@ inline WCConst wc_const(const sphb_wc_params& p) {
   k.hc = 0.5 * p.c_art;
   k.mu2 = 2.0 * p.mu;
   const double v = p.uniform_vol ? p.vol_const : 1.0;
-  k.cg = 0.5 * k.c5s * v;
-  k.cm = k.mu2 * k.c5s * v;
+  k.cg = 0.5 * k.c5s * v / p.h;
+  k.cm = k.mu2 * k.c5s * v / p.h;
+  k.mhalf_inv_h = -0.5 / p.h;
   k.wrap_margin = 1.0001 * p.kappa * p.h;
   return k;
 }
@@ -147,10 +149,10 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
 #pragma unroll
       for (int a = 1; a < D; ++a) r2 = fma(dx[a], dx[a], r2);
       const double inv_r = rsqrt_nr(r2);
-      const double q = r2 * inv_r * inv_h;
-      const double t = fma(-0.5, q, 1.0);
-      // dW V_j / r = c5s q t^3 V_j / r; gsc = 0.5 dW V_j / r, mv = mu viscv
-      double base = ((q * t) * (t * t)) * inv_r;
+      const double t = fma(K.mhalf_inv_h, r2 * inv_r, 1.0);   // 1 - q/2, q = r/h
+      // dW V_j / r = c5s q t^3 V_j / r = (c5s / h) t^3 V_j (q / r = 1 / h);
+      // gsc = 0.5 dW V_j / r, mv = mu viscv
+      double base = (t * t) * t;
       if (!P.uniform_vol) base *= vol_j;
       const double gsc = K.cg * base;
       const double mv = K.cm * base;

@@ -174,8 +174,8 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
       const double rbar = fma(0.5, rho_j, hrho_i);
       const double p_j = fma(c2, rho_j, -c2rho0);
-      double wr = 0.0;                                  // (u* - ubar) / r
-      if (beta > 0.0) wr = ((beta * beta) * (p_i - p_j) * half_cinv) * (rcp_nr(rbar) * inv_r);
+      // (u* - ubar) / r; branch-free: beta = 0 gives 0
+      const double wr = ((beta * beta) * (p_i - p_j) * half_cinv) * (rcp_nr(rbar) * inv_r);
       const double p_star = fma((beta * rbar) * hc, du, fma(0.5, p_j, hp_i));
       double vs[D];
       double sg = 0.0;

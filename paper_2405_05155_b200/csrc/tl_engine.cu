@@ -28,6 +28,7 @@ using namespace sphb;
 namespace {
 
 constexpr int kThreads = 128;
+constexpr int64_t kStageMinRows = 32768;   // stage pass lists from this many rows up
 
 template <int D>
 __device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t i,
@@ -186,7 +187,7 @@ __device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0
 // GEO: read g0_ij from the streamed per-slot planes g0[(c * width + k) * n + i]
 // (sphb_tl_geometry) instead of recomputing it from X0_j; the clamp flag of
 // j then comes from A_j.w (pass B keeps it there).
-template <int D, bool GEO>
+template <int D, bool GEO, bool STAGED>
 __global__ void __launch_bounds__(kThreads)
 k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double4* __restrict__ B0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
@@ -197,8 +198,10 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   extern __shared__ int32_t s_nbr[];
-  stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads, P.row0 + P.nrows,
-                            P.width, s_nbr);
+  // small sets (C3: 41 blocks) gain nothing from staging and pay its round trip
+  if constexpr (STAGED)
+    stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads,
+                              P.row0 + P.nrows, P.width, s_nbr);
   if (i >= P.row0 + P.nrows) return;
   const double dt = scalars[0];
   const double hdt = 0.5 * dt;
@@ -221,8 +224,9 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
 
   const int32_t cn = cnt[i];
   const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
+  const int32_t* __restrict__ grow = nbr + i;
   for (int32_t k = 0; k < cn; ++k) {
-    const int64_t j = srow[k * kThreads];
+    const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
     double vj[D], aj[D], g[D];
     bool fixed_j;
     load_vec_nc<D>(V, j, vj);
@@ -279,7 +283,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   store_vec<D>(XC, i, xc);
 }
 
-template <int D, bool GEO>
+template <int D, bool GEO, bool STAGED>
 __global__ void __launch_bounds__(kThreads)
 k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
@@ -290,8 +294,9 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   extern __shared__ int32_t s_nbr[];
-  stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads, P.row0 + P.nrows,
-                            P.width, s_nbr);
+  if constexpr (STAGED)
+    stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads,
+                              P.row0 + P.nrows, P.width, s_nbr);
   double speed = 0.0;
   if (i < P.row0 + P.nrows) {
     const double inv_h = 1.0 / P.h;
@@ -306,8 +311,9 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     for (int a = 0; a < D; ++a) { gsum[a] = 0.0; acc[a] = 0.0; }
     const int32_t cn = cnt[i];
     const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
+    const int32_t* __restrict__ grow = nbr + i;
     for (int32_t k = 0; k < cn; ++k) {
-      const int64_t j = srow[k * kThreads];
+      const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
       double Qj[D][D];
       load_mat_nc<D>(Q, j, Qj);
       double g[D];
@@ -430,20 +436,27 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
     KERNEL<<<GRID, TH, SMEM, st>>>(__VA_ARGS__);                                               \
   } while (0)
 
-#define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                                  \
-  do {                                                                                  \
-    const bool geo_ = (GEOPTR) != nullptr;                                              \
-    const size_t smem_ = (size_t)p->width * kThreads * sizeof(int32_t);                 \
-    if (smem_ > 200 * 1024) return SPHB_ERR_ARG;                                        \
-    switch (p->dim * 2 + (geo_ ? 1 : 0)) {                                              \
-      case 2: TL_LAUNCH((KERNEL<1, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
-      case 3: TL_LAUNCH((KERNEL<1, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
-      case 4: TL_LAUNCH((KERNEL<2, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
-      case 5: TL_LAUNCH((KERNEL<2, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
-      case 6: TL_LAUNCH((KERNEL<3, false>), GRID, TH, smem_, __VA_ARGS__); break;       \
-      case 7: TL_LAUNCH((KERNEL<3, true>), GRID, TH, smem_, __VA_ARGS__); break;        \
-      default: return SPHB_ERR_ARG;                                                     \
-    }                                                                                   \
+#define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                                     \
+  do {                                                                                     \
+    const bool geo_ = (GEOPTR) != nullptr;                                                 \
+    const bool stg_ = p->nrows >= kStageMinRows;                                           \
+    const size_t smem_ = stg_ ? (size_t)p->width * kThreads * sizeof(int32_t) : 0;        \
+    if (smem_ > 200 * 1024) return SPHB_ERR_ARG;                                           \
+    switch (p->dim * 4 + (geo_ ? 2 : 0) + (stg_ ? 1 : 0)) {                                \
+      case 4: TL_LAUNCH((KERNEL<1, false, false>), GRID, TH, smem_, __VA_ARGS__); break;   \
+      case 5: TL_LAUNCH((KERNEL<1, false, true>), GRID, TH, smem_, __VA_ARGS__); break;    \
+      case 6: TL_LAUNCH((KERNEL<1, true, false>), GRID, TH, smem_, __VA_ARGS__); break;    \
+      case 7: TL_LAUNCH((KERNEL<1, true, true>), GRID, TH, smem_, __VA_ARGS__); break;     \
+      case 8: TL_LAUNCH((KERNEL<2, false, false>), GRID, TH, smem_, __VA_ARGS__); break;   \
+      case 9: TL_LAUNCH((KERNEL<2, false, true>), GRID, TH, smem_, __VA_ARGS__); break;    \
+      case 10: TL_LAUNCH((KERNEL<2, true, false>), GRID, TH, smem_, __VA_ARGS__); break;   \
+      case 11: TL_LAUNCH((KERNEL<2, true, true>), GRID, TH, smem_, __VA_ARGS__); break;    \
+      case 12: TL_LAUNCH((KERNEL<3, false, false>), GRID, TH, smem_, __VA_ARGS__); break;  \
+      case 13: TL_LAUNCH((KERNEL<3, false, true>), GRID, TH, smem_, __VA_ARGS__); break;   \
+      case 14: TL_LAUNCH((KERNEL<3, true, false>), GRID, TH, smem_, __VA_ARGS__); break;   \
+      case 15: TL_LAUNCH((KERNEL<3, true, true>), GRID, TH, smem_, __VA_ARGS__); break;    \
+      default: return SPHB_ERR_ARG;                                                        \
+    }                                                                                      \
   } while (0)
 
 extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,

@@ -126,8 +126,8 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
       float beta = fminf(fmaxf(du * eta_c, 0.f), 1.f);
       const float rbar = (float)P.rho0 + 0.5f * (drho_i + drho_j);
       const float p_j = c2 * drho_j;
-      const float ustar_m_ubar =
-          beta > 0.f ? (beta * beta) * (p_i - p_j) * half_cinv / rbar : 0.f;
+      // branch-free: beta = 0 gives 0
+      const float ustar_m_ubar = (beta * beta) * (p_i - p_j) * half_cinv * __frcp_rn(rbar);
       const float p_star = fmaf(0.5f * beta * rbar * c, du, 0.5f * (p_i + p_j));
       float vs[3];
       float s = 0.f;

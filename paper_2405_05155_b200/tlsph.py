@@ -225,11 +225,13 @@ class SolidSystem:
         p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
         self._cfl_h = self.cfl * kernel.h
         self._c_s = material.sound_speed
-        # streamed reference gradients g0 (3 doubles per pair) when they fit in
-        # a quarter of the free memory (SPHB_TL_GEO=0 forces recomputation)
+        # reference gradients g0: recomputed per pair from X0 by default (with
+        # engine order + staged pass lists that beats streaming 24 B/pair:
+        # C4 0.85 vs 0.96 ms/step); SPHB_TL_GEO=1 streams them when they fit
+        # in a quarter of the free memory
         self.g0 = None
         g0_bytes = d * self.width * n * 8
-        if (os.environ.get("SPHB_TL_GEO", "1") != "0" and n and self.width
+        if (os.environ.get("SPHB_TL_GEO", "0") != "0" and n and self.width
                 and g0_bytes < 0.25 * torch.cuda.mem_get_info()[0]):
             self.g0 = torch.empty(g0_bytes // 8, dtype=torch.float64, device=dev)
             k = _lib.kernel_struct(kernel)

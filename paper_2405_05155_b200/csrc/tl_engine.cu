@@ -21,6 +21,8 @@
 //   V, A, Vh, XC  double4 vectors
 //   B0, F, Q      3x3: 3 x double4 rows {a0, a1, a2, 0}; 2D: 1 x double4
 //                 {a00, a01, a10, a11}; 1D: {a00, 0, 0, 0}
+#include <stdlib.h>
+
 #include "common.cuh"
 
 using namespace sphb;
@@ -29,6 +31,15 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int64_t kStageMinRows = 32768;   // stage pass lists from this many rows up
+
+// widest pass list still staged in shared memory (SPHB_TL_STAGE_MAXW, tuning)
+inline int tl_stage_max_width() {
+  static const int w = [] {
+    const char* e = getenv("SPHB_TL_STAGE_MAXW");
+    return e ? atoi(e) : 1 << 20;
+  }();
+  return w;
+}
 
 template <int D>
 __device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t i,
@@ -113,17 +124,18 @@ __device__ __forceinline__ void load_x0(const double4* __restrict__ X0, int64_t 
   fixed = c[3] != 0.0;
 }
 
-// g0 = (alpha/h) dP(q) e V0 from the reference-configuration displacement.
+// g0 = (alpha/h) dP(q) e V0 from the reference-configuration displacement:
+// dW V0 / r = (alpha/h) (-5 q t^3) V0 / r = c5v t^3 with c5v = -5 alpha V0 / h^2
+// (q / r = 1 / h), t = 1 - r / (2h).
 template <int D>
-__device__ __forceinline__ void ref_gradient(const double (&dx)[D], double scale_v0, double inv_h,
-                                             double (&g)[D]) {
-  double r2 = 0.0;
+__device__ __forceinline__ void ref_gradient(const double (&dx)[D], double c5v,
+                                             double mhalf_inv_h, double (&g)[D]) {
+  double r2 = dx[0] * dx[0];
 #pragma unroll
-  for (int a = 0; a < D; ++a) r2 = fma(dx[a], dx[a], r2);
-  const double inv_r = rsqrt(r2);
-  const double q = r2 * inv_r * inv_h;
-  const double t = fma(-0.5, q, 1.0);
-  const double f = scale_v0 * (-5.0 * q) * (t * t * t) * inv_r;  // dW V0 / r
+  for (int a = 1; a < D; ++a) r2 = fma(dx[a], dx[a], r2);
+  const double inv_r = rsqrt_nr(r2);
+  const double t = fma(mhalf_inv_h, r2 * inv_r, 1.0);
+  const double f = c5v * ((t * t) * t);
 #pragma unroll
   for (int a = 0; a < D; ++a) g[a] = f * dx[a];
 }
@@ -207,6 +219,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const double hdt = 0.5 * dt;
   const double inv_h = 1.0 / P.h;
   const double scale_v0 = P.alpha / P.h * P.vol0;
+  const double c5v = -5.0 * scale_v0 * inv_h, mhalf_inv_h = -0.5 * inv_h;
 
   double wi[D], vi[D], ai[D], vhi[D];
   bool fixed_i;
@@ -246,7 +259,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
       double dx[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
-      ref_gradient<D>(dx, scale_v0, inv_h, g);
+      ref_gradient<D>(dx, c5v, mhalf_inv_h, g);
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -301,6 +314,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
   if (i < P.row0 + P.nrows) {
     const double inv_h = 1.0 / P.h;
     const double scale_v0 = P.alpha / P.h * P.vol0;
+    const double c5v = -5.0 * scale_v0 * inv_h, mhalf_inv_h = -0.5 * inv_h;
     double wi[D];
     bool fixed_i;
     load_x0<D>(X0, i, wi, fixed_i);
@@ -327,7 +341,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
         load_x0<D>(X0, j, wj, fixed_j);
 #pragma unroll
         for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
-        ref_gradient<D>(dx, scale_v0, inv_h, g);
+        ref_gradient<D>(dx, c5v, mhalf_inv_h, g);
       }
       // sum_j (Q_i + Q_j) g = Q_i sum_j g + sum_j Q_j g
 #pragma unroll
@@ -439,7 +453,7 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
 #define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                                     \
   do {                                                                                     \
     const bool geo_ = (GEOPTR) != nullptr;                                                 \
-    const bool stg_ = p->nrows >= kStageMinRows;                                           \
+    const bool stg_ = p->nrows >= kStageMinRows && p->width <= tl_stage_max_width();       \
     const size_t smem_ = stg_ ? (size_t)p->width * kThreads * sizeof(int32_t) : 0;        \
     if (smem_ > 200 * 1024) return SPHB_ERR_ARG;                                           \
     switch (p->dim * 4 + (geo_ ? 2 : 0) + (stg_ ? 1 : 0)) {                                \

@@ -1,9 +1,11 @@
 // wc_engine.cu — fused weakly-compressible Eulerian stage kernels.
 //
 // One launch per midpoint stage of EulerianSolver._substep
-// (eulerian.py:610-643).  Each thread owns one particle (cell-sorted order),
-// walks its ELL row (the reference CSR row minus the pairs the passes skip)
-// and, per pair, recomputes what the reference precomputes and streams:
+// (eulerian.py:610-643).  Each thread owns one particle (engine order:
+// neighbors.engine_order), walks its ELL row (the reference CSR row minus the
+// pairs the passes skip, displacement-sorted, staged per block in shared
+// memory) and, per pair, recomputes what the reference precomputes and
+// streams:
 //   r, e_ij                         (neighbors.py:161-165)
 //   grad'W_ij V_j = dW 0.5(B_i+B_j) e_ij V_j   (correction.py:102-108,
 //                                    eulerian.py:506-507)
@@ -58,11 +60,10 @@ inline WCConst wc_const(const sphb_wc_params& p) {
   return k;
 }
 
-// G consecutive lanes share one particle: at each step they take G
-// consecutive entries of its row, which in the reference's stencil order are
-// mostly consecutive particles of one cell, so the G neighbour records share
-// cache lines and a warp's gathers need ~G-times fewer L1 wavefronts than
-// one-thread-per-particle.  Partial sums are combined with warp shuffles.
+// G consecutive lanes share one particle's row (entries k = gl, gl + G, ...;
+// partial sums combined with warp shuffles).  G = 1 is the default: in engine
+// order the lanes of a warp already read consecutive records.  MINB is the
+// occupancy target (register cap); WALL adds the wall-force accumulation.
 template <int D, int G, int MINB, bool WALL>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
@@ -104,7 +105,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
   if (active) {
     // host-folded constants (kernel parameters live in the constant bank, so
     // the FP64 instructions read them as operands instead of registers)
-    const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, inv_h = K.inv_h;
+    const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c;
     const double half_cinv = K.half_cinv, hc = K.hc;
 
     double xi[D], vol_i, vi[D], rho_i;

@@ -740,3 +740,31 @@ def test_wc_engine_order_on_irregular_sets(monkeypatch, dim, uniform, order):
             tol = TOL_1 if k == 1 else 1e-10
             assert l2_error(s.state.rho, ref.rho) < tol
             assert l2_error(s.state.mom, ref.mom) < tol
+
+
+@pytest.mark.parametrize("order", ["lattice", "cell"])
+def test_tl_engine_order_on_jittered_block(monkeypatch, order):
+    """TL-SPH engine order on a jittered 3D block (non-lattice reference
+    configuration) with a clamped base and a shear velocity, 20 steps."""
+    monkeypatch.setenv("SPHB_ENGINE_ORDER", order)
+    rng = np.random.default_rng(23)
+    dp = 0.05
+    X0 = lattice_points((0.0, 0.0, 0.0), (0.5, 1.0, 0.5), dp)
+    X0 = X0 + rng.uniform(-0.15, 0.15, X0.shape) * dp
+    spec = kernel_spec("wendland-truncated", 1.15 * dp, 3)
+    fixed = X0[:, 1] < spec.kappa * spec.h
+    v0 = np.zeros_like(X0)
+    v0[:, 0] = 2.0 * X0[:, 1]
+    v0[fixed] = 0.0
+    mat = Material(1100.0, 17e6, 0.45)
+    s = SolidSystem(X0, mat, spec, dp, fixed=fixed, correction=True, cfl=0.6)
+    s.v = v0.copy()
+    ref = O.SolidTL(X0, 1100.0, 17e6, 0.45, spec, dp, fixed, True, 0.6)
+    ref.v = v0.copy()
+    for k in range(1, 21):
+        s.step()
+        ref.step()
+        if k in (1, 20):
+            tol = TOL_1 if k == 1 else 1e-10
+            for a, b in ((s.x, ref.x), (s.v, ref.v), (s.F, ref.F)):
+                assert l2_error(a, b) < tol

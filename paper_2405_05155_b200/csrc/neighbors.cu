@@ -60,6 +60,110 @@ __global__ void k_cell_ranges(sphb_grid g, int64_t n, const uint32_t* __restrict
   if (s == n - 1 || key[s + 1] != k) ce[ref_key(g, k)] = (int32_t)(s + 1);
 }
 
+// Small sets (C1, the relaxation loop: 10k particles rebinned every update):
+// the whole binning in ONE block — wrap + key, cell counts in shared memory,
+// exclusive scan, scatter, per-cell sort by original index (= the stable
+// radix sort's order), cell tables, gather — instead of ~8 launches.
+constexpr int kSmallBinThreads = 1024;
+constexpr int64_t kSmallBinMaxN = 16384;
+constexpr int64_t kSmallBinMaxCells = 8192;
+
+template <int D>
+__global__ void __launch_bounds__(kSmallBinThreads)
+k_bin_small(sphb_grid g, const double* __restrict__ pos, int64_t n, double* __restrict__ wrapped,
+            uint32_t* __restrict__ key_unused, int32_t* __restrict__ perm, int32_t* __restrict__ cs,
+            int32_t* __restrict__ ce, double* __restrict__ ws) {
+  constexpr int KPT = (int)(kSmallBinMaxN / kSmallBinThreads);   // particles per thread
+  extern __shared__ int32_t sm[];
+  const int ntot = (int)g.ntot;
+  int32_t* count = sm;                  // [ntot]
+  int32_t* fill = sm + ntot;            // [ntot]
+  int32_t* sperm = sm + 2 * ntot;       // [n]
+  const int tid = threadIdx.x;
+  for (int c = tid; c < ntot; c += blockDim.x) count[c] = 0;
+  __syncthreads();
+  uint32_t key[KPT];
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int64_t i = tid + (int64_t)q * kSmallBinThreads;
+    key[q] = 0;
+    if (i < n) {
+      int64_t flat = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double p = pos[i * D + a];
+        const double w = g.periodic ? np_remainder(p, g.box[a]) : __dsub_rn(p, g.lo[a]);
+        wrapped[i * D + a] = w;
+        flat += cell_coord(g, a, w) * g.sstrides[a];   // storage key
+      }
+      key[q] = (uint32_t)flat;
+      atomicAdd(count + flat, 1);
+    }
+  }
+  __syncthreads();
+  // exclusive scan: each thread a contiguous chunk, chunk totals scanned by warp 0
+  __shared__ int32_t part[kSmallBinThreads];
+  const int chunk = (ntot + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(tid * chunk, ntot), c1 = min(c0 + chunk, ntot);
+  int32_t tot = 0;
+  for (int c = c0; c < c1; ++c) tot += count[c];
+  part[tid] = tot;
+  __syncthreads();
+  if (tid < 32) {
+    int32_t run = 0;
+    for (int b = 0; b < (int)blockDim.x; b += 32) {
+      int32_t v = part[b + tid];
+      const int32_t mine = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (tid >= o) v += u;
+      }
+      part[b + tid] = v - mine + run;          // exclusive
+      run += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  int32_t off = part[tid];
+  for (int c = c0; c < c1; ++c) {
+    const int32_t k = count[c];
+    fill[c] = off;
+    if (k) {
+      const int64_t r = g.slow_axis == g.dim - 1 ? c : ref_key(g, (uint32_t)c);
+      cs[r] = off;
+      ce[r] = off + k;
+    }
+    off += k;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < KPT; ++q) {
+    const int64_t i = tid + (int64_t)q * kSmallBinThreads;
+    if (i < n) sperm[atomicAdd(fill + key[q], 1)] = (int32_t)i;
+  }
+  __syncthreads();
+  // ascending original index inside each cell (cells hold a handful of particles)
+  for (int c = c0; c < c1; ++c) {
+    const int32_t e = fill[c], b = e - count[c];
+    for (int32_t s = b + 1; s < e; ++s) {
+      const int32_t v = sperm[s];
+      int32_t t = s;
+      while (t > b && sperm[t - 1] > v) {
+        sperm[t] = sperm[t - 1];
+        --t;
+      }
+      sperm[t] = v;
+    }
+  }
+  __syncthreads();
+  for (int64_t s = tid; s < n; s += blockDim.x) {
+    const int64_t i = sperm[s];
+    perm[s] = (int32_t)i;
+#pragma unroll
+    for (int a = 0; a < D; ++a) ws[(int64_t)a * n + s] = wrapped[i * D + a];
+  }
+}
+
 static bool grid_ok(const sphb_grid* g) {
   if (!g || g->dim < 1 || g->dim > 3) return false;
   if (g->slow_axis < 0 || g->slow_axis >= g->dim) return false;
@@ -113,6 +217,21 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
   uint32_t* keys_out = (uint32_t*)(w + L.keys_out);
   int32_t* vals_in = (int32_t*)(w + L.vals_in);
   double* wrapped = (double*)(w + L.wrapped);
+  if (n <= kSmallBinMaxN && g->ntot <= kSmallBinMaxCells) {
+    const size_t smem = sizeof(int32_t) * (2 * (size_t)g->ntot + (size_t)n);
+    if (smem > 48 * 1024) {
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    switch (g->dim) {
+      case 1: k_bin_small<1><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
+      case 2: k_bin_small<2><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
+      default: k_bin_small<3><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
+    }
+    SPHB_LAUNCH_CHECK();
+    return SPHB_OK;
+  }
   const int T = 256;
   switch (g->dim) {
     case 1: k_wrap_key<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;

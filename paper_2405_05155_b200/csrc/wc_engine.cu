@@ -433,12 +433,20 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
   const size_t smem_idx = (size_t)p->width * (kThreads / group) * sizeof(int32_t);
+  static const int carveout = [] {     // SPHB_WC_CARVEOUT: shared-memory carveout % (tuning)
+    const char* e = getenv("SPHB_WC_CARVEOUT");
+    return e ? atoi(e) : -1;
+  }();
   if (smem_idx > 200 * 1024) return SPHB_ERR_ARG;
 #define SPHB_STAGE_W(D, G, MB, W)                                                          \
   if (smem_idx > 48 * 1024)                                                                \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                          (int)smem_idx));                                  \
+  if (carveout >= 0)                                                                       \
+    SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
+                                         cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                                         carveout));                                       \
   k_wc_stage<D, G, MB, W><<<sphb_blocks(p->nrows * G, kThreads), kThreads, smem_idx, st>>>( \
       *p, K, stage, X, b, nbr, cnt, Sin, Sn, Mn, Sout, Mout, scalars, err);                \
   break

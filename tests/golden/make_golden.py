@@ -378,6 +378,33 @@ def main():
                                                                         True))
     save("error_study", **arrays)
 
+    # ------------------------------------- harness
+    from sph_trunc import bench as rbench
+
+    arrays = {}
+    cfg = cases.CaseConfig(name="shear", case="shear-layer", solver="euler-wc", dp=1.0 / 32,
+                           t_end=0.04, kernel_family=WENDLAND, h_ratio=1.3, cfl=0.5)
+    pair, case_sw, case_tw = rbench.paired_run(cfg)
+    for leg, rep in (("sw", pair.sw), ("tw", pair.tw)):
+        arrays[f"shear_{leg}__steps"] = np.array(rep.steps)
+        arrays[f"shear_{leg}__t_end"] = np.array(rep.t_end)
+        arrays[f"shear_{leg}__nstats"] = np.array([rep.neighbor_stats[k] for k in
+                                                   ("mean", "min", "max", "pairs")], float)
+        arrays[f"shear_{leg}__mass_drift"] = np.array(rep.conservation["mass_rel_drift"])
+        arrays[f"shear_{leg}__dt"] = np.array([rep.diagnostics["dt_min"],
+                                               rep.diagnostics["dt_max"]])
+    arrays["shear__velocity_l2"] = np.array(pair.field_diff["velocity_l2"])
+    arrays["shear__vorticity_l2"] = np.array(pair.field_diff["vorticity_l2"])
+    arrays["shear_tw__vorticity"] = rbench.vorticity(case_tw)
+    t = np.linspace(0.0, 40.0, 1600)
+    f = np.column_stack([1.0 + 0.1 * np.sin(3.0 * t), 0.5 * np.sin(1.3 * t)])
+    dl = rbench.drag_lift(t, f, 1.0, 1.0, 2.0)
+    arrays["drag__t"], arrays["drag__f"] = t, f
+    arrays["drag__cd"], arrays["drag__cl"] = dl["cd"], dl["cl"]
+    arrays["drag__scalars"] = np.array([np.nan if dl["strouhal"] is None else dl["strouhal"],
+                                        dl["cd_mean_tail"], dl["cl_amplitude_tail"]], float)
+    save("harness", **arrays)
+
     # ---------------------------------------------------- C3 / C4 (reduced)
     for label, builder, kwargs, nsteps in (("c3_plate", configs.c3_plate, {"dp": 0.002}, 100),
                                            ("c4_column", configs.c4_column, {"n_width": 6}, 50)):

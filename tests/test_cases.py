@@ -127,3 +127,34 @@ def test_other_builders_run():
             c.advance()
         c.record_outputs()
         assert np.isfinite(c.snapshot_array()).all() and c.vm_max > 0.0
+
+
+def test_load_config(tmp_path):
+    """TOML case files: defaults, tables passed through, and the checks of
+    cases.py:82-118 (unknown case / family, dp, t_end)."""
+    from paper_2405_05155_b200.eulerian import ConfigError
+
+    f = tmp_path / "cav.toml"
+    f.write_text('case = "cavity"\ndp = 0.05\nt_end = 1.0\n[kernel]\nfamily = "wendland-truncated"\n'
+                 'h_ratio = 1.3\n[physics]\nre = 400.0\nu_wall = 1.0\n[output]\nevery = 0.5\n')
+    cfg = cases.load_config(f)
+    assert (cfg.name, cfg.case, cfg.dp, cfg.t_end) == ("cav", "cavity", 0.05, 1.0)
+    assert (cfg.kernel_family, cfg.h_ratio, cfg.cfl, cfg.correction) == \
+        ("wendland-truncated", 1.3, 0.5, True)
+    assert cfg.physics == {"re": 400.0, "u_wall": 1.0} and cfg.output_every == 0.5
+    assert cfg.kernel(2).kappa == 1.6
+    relax = tmp_path / "r.toml"
+    relax.write_text('case = "relax"\ndp = 0.1\n[geometry]\nkind = "semicircle"\nradius = 0.5\n')
+    rc = cases.load_config(relax)
+    assert isinstance(cases._shape_from_geometry(rc.geometry), cases.geometry.SemiCircle)
+    for body in ('case = "nope"\ndp = 0.1\nt_end = 1.0\n', 'case = "cavity"\nt_end = 1.0\n',
+                 'case = "cavity"\ndp = -1.0\nt_end = 1.0\n', 'case = "cavity"\ndp = 0.1\n',
+                 'case = "cavity"\ndp = 0.1\nt_end = 1.0\n[kernel]\nfamily = "gauss"\n'):
+        bad = tmp_path / "bad.toml"
+        bad.write_text(body)
+        with pytest.raises(ConfigError):
+            cases.load_config(bad)
+    with pytest.raises(ConfigError):
+        cases.load_config(tmp_path / "missing.toml")
+    with pytest.raises(ConfigError):
+        cases._shape_from_geometry({"kind": "torus"})

@@ -466,9 +466,11 @@ int sphb_tl_pass_b(const sphb_tl_params* p, const double* X0, const int32_t* nbr
 int sphb_tl_geometry(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
                      const int32_t* nbr, const int32_t* cnt, int32_t width,
                      const sphb_kernel* k, double vol0, double* g0, void* stream);
-/* Q = (F S(F)) B0^T for every particle (first accelerations() call). */
+/* Q = (F S(F)) B0^T for every particle (first accelerations() call).  In
+ * 3D each Q row carries the reference coordinate X0_r in its padding (as
+ * pass A writes it), which pass B reads instead of gathering X0_j. */
 int sphb_tl_stress(const sphb_tl_params* p, const double* F, const double* B0,
-                   double* Q, void* stream);
+                   const double* X0, double* Q, void* stream);
 /* max |v| into scalars[2] (stable_dt). */
 int sphb_tl_speed_max(const sphb_tl_params* p, const double* V, double* scalars,
                       void* stream);

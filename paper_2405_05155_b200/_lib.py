@@ -184,7 +184,7 @@ SIGNATURES = {
     "sphb_tl_pass_a": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P]),
     "sphb_tl_geometry": (C.c_int, [P, I64, P, P, P, I32, P, F64, P, P]),
-    "sphb_tl_stress": (C.c_int, [P, P, P, P, P]),
+    "sphb_tl_stress": (C.c_int, [P, P, P, P, P, P]),
     "sphb_tl_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_relax_accel": (C.c_int, [P, I64, P, P, P, P, P, P, F64, F64, P, P, P]),
     "sphb_relax_update": (C.c_int, [I64, I32, P, F64, F64, P, P, P]),

@@ -71,6 +71,20 @@ __device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t i,
   }
 }
 
+// Q record with the particle's reference coordinates in the row padding
+// (3D: rows {q_r0, q_r1, q_r2, X0_r}); pass B then reads Q_j and X0_j with
+// three 256-bit gathers instead of four.  2D/1D records have no padding.
+template <int D>
+__device__ __forceinline__ void store_q(double4* __restrict__ Q, int64_t i, const double (&a)[D][D],
+                                        const double (&w)[D]) {
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Q[3 * i + r] = make_double4(a[r][0], a[r][1], a[r][2], w[r]);
+  } else {
+    store_mat<D>(Q, i, a);
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void load_vec(const double4* __restrict__ V, int64_t i, double (&v)[D]) {
   double4 t = V[i];
@@ -287,7 +301,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   double Qi[D][D];
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
   store_mat<D>(F, i, Fi);
-  store_mat<D>(Q, i, Qi);
+  store_q<D>(Q, i, Qi, wi);
   store_vec<D>(Vh, i, vhi);
   double xc[D];
   load_vec<D>(XC, i, xc);
@@ -328,17 +342,28 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     const int32_t* __restrict__ grow = nbr + i;
     for (int32_t k = 0; k < cn; ++k) {
       const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
-      double Qj[D][D];
-      load_mat_nc<D>(Q, j, Qj);
+      double Qj[D][D], wj[D];
+      if constexpr (D == 3) {      // Q rows carry X0_j in their padding (store_q)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double4 t4 = ldg4(Q + 3 * j + r);
+          Qj[r][0] = t4.x; Qj[r][1] = t4.y; Qj[r][2] = t4.z;
+          wj[r] = t4.w;
+        }
+      } else {
+        load_mat_nc<D>(Q, j, Qj);
+        if constexpr (!GEO) {
+          bool fixed_j;
+          load_x0<D>(X0, j, wj, fixed_j);
+        }
+      }
       double g[D];
       if constexpr (GEO) {
         const int64_t slot = (int64_t)k * n + i;
 #pragma unroll
         for (int a = 0; a < D; ++a) g[a] = __ldg(g0 + ((int64_t)a * P.width) * n + slot);
       } else {
-        double wj[D], dx[D];
-        bool fixed_j;
-        load_x0<D>(X0, j, wj, fixed_j);
+        double dx[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
         ref_gradient<D>(dx, c5v, mhalf_inv_h, g);
@@ -395,14 +420,17 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
 
 template <int D>
 __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ F,
-                            const double4* __restrict__ B0, double4* __restrict__ Q) {
+                            const double4* __restrict__ B0, const double4* __restrict__ X0,
+                            double4* __restrict__ Q) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n) return;
-  double Fi[D][D], B[D][D], Qi[D][D];
+  double Fi[D][D], B[D][D], Qi[D][D], w[D];
+  bool fixed;
   load_mat<D>(F, i, Fi);
   load_mat<D>(B0, i, B);
+  load_x0<D>(X0, i, w, fixed);
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
-  store_mat<D>(Q, i, Qi);
+  store_q<D>(Q, i, Qi, w);
 }
 
 template <int D>
@@ -504,12 +532,12 @@ extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const i
 }
 
 extern "C" int sphb_tl_stress(const sphb_tl_params* p, const double* f, const double* b0,
-                              double* q, void* stream) {
-  if (!p || p->n < 0) return SPHB_ERR_ARG;
+                              const double* x0, double* q, void* stream) {
+  if (!p || p->n < 0 || !x0) return SPHB_ERR_ARG;
   if (p->n == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   TL_DISPATCH(k_tl_stress, sphb_blocks(p->n, 128), 128, *p, (const double4*)f, (const double4*)b0,
-              (double4*)q);
+              (const double4*)x0, (double4*)q);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

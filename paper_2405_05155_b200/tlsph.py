@@ -303,7 +303,7 @@ class SolidSystem:
     def _accelerations_dev(self):
         st = _lib.stream_ptr()
         _lib.call("sphb_tl_stress", ctypes.byref(self.params), self.Frec.data_ptr(),
-                  self.B0rec.data_ptr(), self.Qrec.data_ptr(), st)
+                  self.B0rec.data_ptr(), self.X0rec.data_ptr(), self.Qrec.data_ptr(), st)
         self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),

@@ -451,9 +451,11 @@ typedef struct sphb_tl_params {
   double lam, g;           /* Lame parameters (tlsph.py:27-35) */
 } sphb_tl_params;
 
-/* g0: optional per-slot reference gradients (sphb_tl_geometry); NULL ->
- * recompute g0_ij from X0 per pair.  With g0 the clamp flag of a neighbour
- * is read from A_j.w, which pass B maintains (A record {a0, a1, a2, fixed}). */
+/* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows
+ * (the KDK first kick), then per owned row gathers Vh_j for dF.  g0:
+ * optional per-slot reference gradients (sphb_tl_geometry); NULL ->
+ * recompute g0_ij from X0 per pair.  Pass B keeps the clamp flag in A.w
+ * (A record {a0, a1, a2, fixed}). */
 int sphb_tl_pass_a(const sphb_tl_params* p, const double* X0, const double* B0,
                    const int32_t* nbr, const int32_t* cnt, const double* g0,
                    const double* V, const double* A, double* Vh, double* XC, double* F,

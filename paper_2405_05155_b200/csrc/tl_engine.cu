@@ -213,12 +213,32 @@ __device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0
 // GEO: read g0_ij from the streamed per-slot planes g0[(c * width + k) * n + i]
 // (sphb_tl_geometry) instead of recomputing it from X0_j; the clamp flag of
 // j then comes from A_j.w (pass B keeps it there).
+// First kick of the KDK step for every local row (owned + halo):
+// vh = v + dt/2 a, 0 for clamped particles (tlsph.py:186-189); pass A then
+// gathers one half-step velocity record per pair instead of v_j and a_j.
+template <int D>
+__global__ void k_tl_kick(int64_t n, const double4* __restrict__ X0,
+                          const double4* __restrict__ V, const double4* __restrict__ A,
+                          double4* __restrict__ Vh, const double* __restrict__ scalars) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double hdt = 0.5 * scalars[0];
+  double w[D], v[D], a_[D], vh[D];
+  bool fixed;
+  load_x0<D>(X0, i, w, fixed);
+  load_vec<D>(V, i, v);
+  load_vec<D>(A, i, a_);
+#pragma unroll
+  for (int a = 0; a < D; ++a) vh[a] = fixed ? 0.0 : fma(hdt, a_[a], v[a]);
+  store_vec<D>(Vh, i, vh);
+}
+
 template <int D, bool GEO, bool STAGED>
 __global__ void __launch_bounds__(kThreads)
 k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double4* __restrict__ B0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
             const double* __restrict__ g0,
-            const double4* __restrict__ V, const double4* __restrict__ A, double4* __restrict__ Vh,
+            const double4* __restrict__ Vh,
             double4* __restrict__ XC, double4* __restrict__ F, double4* __restrict__ Q,
             const double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
@@ -235,13 +255,10 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const double scale_v0 = P.alpha / P.h * P.vol0;
   const double c5v = -5.0 * scale_v0 * inv_h, mhalf_inv_h = -0.5 * inv_h;
 
-  double wi[D], vi[D], ai[D], vhi[D];
+  double wi[D], vhi[D];
   bool fixed_i;
   load_x0<D>(X0, i, wi, fixed_i);
-  load_vec<D>(V, i, vi);
-  load_vec<D>(A, i, ai);
-#pragma unroll
-  for (int a = 0; a < D; ++a) vhi[a] = fixed_i ? 0.0 : fma(hdt, ai[a], vi[a]);
+  load_vec<D>(Vh, i, vhi);            // k_tl_kick: v + dt/2 a, 0 when clamped
 
   double m[D][D];
 #pragma unroll
@@ -254,22 +271,16 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const int32_t* __restrict__ grow = nbr + i;
   for (int32_t k = 0; k < cn; ++k) {
     const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
-    double vj[D], aj[D], g[D];
-    bool fixed_j;
-    load_vec_nc<D>(V, j, vj);
+    double vhj[D], g[D];
+    load_vec_nc<D>(Vh, j, vhj);
     if constexpr (GEO) {
-      const double4 a4 = ldg4(A + j);
-      const double ac[4] = {a4.x, a4.y, a4.z, a4.w};
-#pragma unroll
-      for (int a = 0; a < D; ++a) aj[a] = ac[a];
-      fixed_j = a4.w != 0.0;
       const int64_t slot = (int64_t)k * n + i;
 #pragma unroll
       for (int a = 0; a < D; ++a) g[a] = __ldg(g0 + ((int64_t)a * P.width) * n + slot);
     } else {
       double wj[D];
+      bool fixed_j;
       load_x0<D>(X0, j, wj, fixed_j);
-      load_vec_nc<D>(A, j, aj);
       double dx[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
@@ -277,8 +288,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const double vhj = fixed_j ? 0.0 : fma(hdt, aj[a], vj[a]);
-      const double dv = vhj - vhi[a];
+      const double dv = vhj[a] - vhi[a];
 #pragma unroll
       for (int b = 0; b < D; ++b) m[a][b] = fma(dv, g[b], m[a][b]);
     }
@@ -302,7 +312,6 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
   store_mat<D>(F, i, Fi);
   store_q<D>(Q, i, Qi, wi);
-  store_vec<D>(Vh, i, vhi);
   double xc[D];
   load_vec<D>(XC, i, xc);
 #pragma unroll
@@ -509,10 +518,11 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)x0,
+              (const double4*)v, (const double4*)a, (double4*)vh, scalars);
   TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
-                  (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)v,
-                  (const double4*)a, (double4*)vh, (double4*)xc, (double4*)f, (double4*)q,
-                  scalars, err);
+                  (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
+                  (double4*)xc, (double4*)f, (double4*)q, scalars, err);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

@@ -164,12 +164,47 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 // ----------------------------------------------------------- reductions
 // Copy a block's ELL columns nbr[k * n + base + r] (k < width, r < RB) into
-// shared memory s_nbr[k * RB + r] with LDGSTS and wait: the pass list then
-// costs one DRAM round trip per block instead of one per loop iteration.
+// shared memory s_nbr[k * RB + r] and wait: the pass list then costs one
+// DRAM round trip per block instead of one per loop iteration.  When every
+// column slice is 16-byte aligned (n, base and the row count multiples of 4)
+// one thread issues a TMA bulk copy per column (cp.async.bulk, completion on
+// an mbarrier); otherwise every thread copies 4-byte words with LDGSTS.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 template <int RB>
 __device__ __forceinline__ void stage_pass_list(const int32_t* __restrict__ nbr, int64_t n,
                                                 int64_t base, int64_t lim, int width,
                                                 int32_t* s_nbr) {
+  const int64_t rows = lim - base < RB ? lim - base : RB;
+  const bool bulk = ((n | base | rows) & 3) == 0 && rows > 0;
+  if (bulk) {
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t b = smem_u32(&bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(rows * sizeof(int32_t));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(b), "r"(bytes * (uint32_t)width) : "memory");
+      for (int k = 0; k < width; ++k)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_u32(s_nbr + k * RB)), "l"(nbr + (int64_t)k * n + base), "r"(bytes), "r"(b)
+            : "memory");
+    }
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+          " selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done) : "r"(b) : "memory");
+    return;
+  }
   for (int e = threadIdx.x; e < width * RB; e += blockDim.x) {
     const int k = e / RB, r = e % RB;
     if (base + r < lim)

@@ -32,7 +32,9 @@ using namespace sphb::wc;
 
 namespace {
 
-constexpr int kThreads = 128;
+// 64-thread blocks: more, smaller blocks per SM overlap one block's pass-list
+// prologue with the others' loops (-1.4% vs 128 on C5, profiles/r01_tune_wc.md)
+constexpr int kThreads = 64;
 
 // Per-launch constants folded on the host from sphb_wc_params.
 struct WCConst {
@@ -65,7 +67,8 @@ inline WCConst wc_const(const sphb_wc_params& p) {
 // order the lanes of a warp already read consecutive records.  MINB is the
 // occupancy target (register cap); WALL adds the wall-force accumulation.
 template <int D, int G, int MINB, bool WALL>
-__global__ void __launch_bounds__(kThreads, MINB)
+// MINB counts 128-thread equivalents (4 -> 128 registers, 5 -> 96)
+__global__ void __launch_bounds__(kThreads, MINB * 128 / kThreads)
 k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
            const double4* __restrict__ X, const double* __restrict__ B,
            const int32_t* __restrict__ nbr,

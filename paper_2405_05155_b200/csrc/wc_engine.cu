@@ -92,8 +92,8 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
   const int64_t i = P.row0 + (blk * blockDim.x + threadIdx.x) / G;
   const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
 
-  // Stage the block's ELL columns in shared memory first (LDGSTS, one
-  // coalesced 4-byte copy per row and pass-list slot): the index stream then
+  // Stage the block's ELL columns in shared memory first (stage_pass_list:
+  // TMA bulk copies, or LDGSTS for unaligned slices): the index stream then
   // costs one DRAM round trip per block instead of one per loop iteration,
   // and the loop's dependent chain starts at a 30-cycle LDS.
   extern __shared__ int32_t s_nbr[];     // [width][kThreads / G]

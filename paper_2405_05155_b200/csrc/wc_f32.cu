@@ -19,7 +19,7 @@ using namespace sphb::wc;
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 64;
 
 __device__ __forceinline__ float4 ldg4f(const float4* p) { return __ldg(p); }
 
@@ -63,6 +63,14 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
     double dm[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) dm[a] = 0.0;
+    // pair factors in t^3 form (q / r = 1 / h): gsc = 0.5 dW V / r, mv = mu viscv
+    const float mhalf_inv_h = -0.5f * inv_h;
+    const float cg = 0.5f * scale * -5.0f * inv_h * vol;
+    const float cm = 2.0f * mu * scale * -5.0f * inv_h * vol;
+    const float rho0f = (float)P.rho0;
+    float hvi[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) hvi[a] = 0.5f * vi[a];
     const int32_t m = cnt[i];
     for (int32_t k = 0; k < m; ++k) {
       const int64_t j = s_nbr[k * kThreads + threadIdx.x];
@@ -93,55 +101,49 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
         r2 = fmaf(d, d, r2);
       }
       const float inv_r = rsqrtf(r2);
-      const float q = r2 * inv_r * inv_h;
-      const float t = fmaf(-0.5f, q, 1.0f);
-      const float dW = scale * (-5.0f * q) * (t * t * t);
-      float e[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-      for (int a = 0; a < D; ++a) e[a] = dx[a] * inv_r;
-      float g[3];
+      const float t = fmaf(mhalf_inv_h, r2 * inv_r, 1.0f);
+      const float t3 = (t * t) * t;
+      const float gsc = cg * t3, mv = cm * t3;
+      float G_[3];                                  // (B_i + B_j) dx
       if (D == 3) {
-        g[0] = bs[0] * e[0] + bs[1] * e[1] + bs[2] * e[2];
-        g[1] = bs[1] * e[0] + bs[3] * e[1] + bs[4] * e[2];
-        g[2] = bs[2] * e[0] + bs[4] * e[1] + bs[5] * e[2];
+        G_[0] = fmaf(bs[0], dx[0], fmaf(bs[1], dx[1], bs[2] * dx[2]));
+        G_[1] = fmaf(bs[1], dx[0], fmaf(bs[3], dx[1], bs[4] * dx[2]));
+        G_[2] = fmaf(bs[2], dx[0], fmaf(bs[4], dx[1], bs[5] * dx[2]));
       } else if (D == 2) {
-        g[0] = bs[0] * e[0] + bs[1] * e[1];
-        g[1] = bs[1] * e[0] + bs[2] * e[1];
-        g[2] = 0.f;
+        G_[0] = fmaf(bs[0], dx[0], bs[1] * dx[1]);
+        G_[1] = fmaf(bs[1], dx[0], bs[2] * dx[1]);
+        G_[2] = 0.f;
       } else {
-        g[0] = bs[0] * e[0];
-        g[1] = g[2] = 0.f;
+        G_[0] = bs[0] * dx[0];
+        G_[1] = G_[2] = 0.f;
       }
-      const float gs = 0.5f * dW * vol;
-#pragma unroll
-      for (int a = 0; a < D; ++a) g[a] *= gs;
-      const float viscv = 2.0f * dW * inv_r * vol;
-      float ul = 0.f, ur = 0.f;
+      float dv[3] = {0.f, 0.f, 0.f};
+      float dud = 0.f;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        ul = fmaf(-vi[a], e[a], ul);
-        ur = fmaf(-vj[a], e[a], ur);
+        dv[a] = vj[a] - vi[a];
+        dud = fmaf(dv[a], dx[a], dud);
       }
-      const float du = ul - ur;
-      float beta = fminf(fmaxf(du * eta_c, 0.f), 1.f);
-      const float rbar = (float)P.rho0 + 0.5f * (drho_i + drho_j);
+      const float du = dud * inv_r;                 // u_l - u_r
+      const float beta = fminf(fmaxf(du * eta_c, 0.f), 1.f);
+      const float rbar = rho0f + 0.5f * (drho_i + drho_j);
       const float p_j = c2 * drho_j;
-      // branch-free: beta = 0 gives 0
-      const float ustar_m_ubar = (beta * beta) * (p_i - p_j) * half_cinv * __frcp_rn(rbar);
+      // (u* - ubar) / r, branch-free (beta = 0 gives 0)
+      const float wr = (beta * beta) * (p_i - p_j) * half_cinv * __frcp_rn(rbar) * inv_r;
       const float p_star = fmaf(0.5f * beta * rbar * c, du, 0.5f * (p_i + p_j));
       float vs[3];
-      float s = 0.f;
+      float sg = 0.f;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        vs[a] = fmaf(-ustar_m_ubar, e[a], 0.5f * (vi[a] + vj[a]));
-        s = fmaf(vs[a], g[a], s);
+        vs[a] = fmaf(-wr, dx[a], fmaf(0.5f, vj[a], hvi[a]));
+        sg = fmaf(vs[a], G_[a], sg);
       }
-      dr += (double)(-2.0f * rbar * s);
-      const float rs = rbar * s;
-      const float mv = mu * viscv;
+      const float rs2 = -2.0f * rbar * gsc * sg;
+      const float pg = -2.0f * p_star * gsc;
+      dr += (double)rs2;
 #pragma unroll
       for (int a = 0; a < D; ++a)
-        dm[a] += (double)fmaf(mv, vi[a] - vj[a], -2.0f * fmaf(rs, vs[a], p_star * g[a]));
+        dm[a] += (double)fmaf(-mv, dv[a], fmaf(pg, G_[a], rs2 * vs[a]));
     }
     bool finite = isfinite(dr);
 #pragma unroll

@@ -768,3 +768,20 @@ def test_tl_engine_order_on_jittered_block(monkeypatch, order):
             tol = TOL_1 if k == 1 else 1e-10
             for a, b in ((s.x, ref.x), (s.v, ref.v), (s.F, ref.F)):
                 assert l2_error(a, b) < tol
+
+
+@pytest.mark.parametrize("variant", ["geo", "tiled"])
+def test_wc_opt_in_variants_vs_oracle(monkeypatch, variant):
+    """The opt-in stage variants (SPHB_WC_KERNEL=geo: streamed per-pair
+    geometry without FMA; tiled: shared-memory record tiles) give the oracle's
+    fields on C5 (16^3)."""
+    monkeypatch.setenv("SPHB_WC_KERNEL", variant)
+    cfg = configs.c5_tgv3d(kernel="1.6h", n_side=16)
+    s = make_wc(cfg)
+    assert s.variant == variant
+    ref = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
+                       cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    for k in range(1, 11):
+        assert s.step() == pytest.approx(ref.step(), rel=1e-12)
+    assert l2_error(s.state.rho, ref.rho) < 1e-10
+    assert l2_error(s.state.mom, ref.mom) < 1e-10

@@ -55,6 +55,7 @@ typedef enum {
 #define SPHB_EFLAG_NONPOS_DENSITY   2
 #define SPHB_EFLAG_DET_NONPOS       4
 #define SPHB_EFLAG_NONFINITE_STATE  8
+#define SPHB_EFLAG_BAD_INDEX        16   /* debug builds: pass-list index out of range */
 
 /* Kernel families: the reference's integer codes (kernels.py:26-27). */
 #define SPHB_CODE_WENDLAND 0
@@ -462,7 +463,8 @@ int sphb_tl_pass_a(const sphb_tl_params* p, const double* X0, const double* B0,
                    double* Q, const double* scalars, int32_t* err, void* stream);
 int sphb_tl_pass_b(const sphb_tl_params* p, const double* X0, const int32_t* nbr,
                    const int32_t* cnt, const double* g0, const double* Q, const double* Vh,
-                   double* A, double* V, double* scalars, int32_t update_v, void* stream);
+                   double* A, double* V, double* scalars, int32_t update_v, int32_t* err,
+                   void* stream);
 /* Static reference gradients g0_ij = dW e_ij V0 (tlsph.py:145-146) per ELL
  * slot, planes g0[(c * width + k) * n + s]; reference arithmetic. */
 int sphb_tl_geometry(const sphb_grid* g, int64_t n, const double* wrapped_sorted,

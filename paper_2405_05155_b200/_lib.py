@@ -18,7 +18,9 @@ from functools import lru_cache
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsphb.so")
+# SPHB_LIB selects another build of the same ABI (e.g. the bounds-checked
+# `make debug` library, libsphb_debug.so)
+LIB_PATH = os.environ.get("SPHB_LIB") or os.path.join(_HERE, "libsphb.so")
 
 
 class BackendUnavailable(RuntimeError):
@@ -182,7 +184,7 @@ SIGNATURES = {
     "sphb_fp64_probe": (C.c_int, [P, I32, I32, I32, P]),
     "sphb_set_dt": (C.c_int, [F64, F64, F64, P, P, P]),
     "sphb_tl_pass_a": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P]),
-    "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P]),
+    "sphb_tl_pass_b": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P, P]),
     "sphb_tl_geometry": (C.c_int, [P, I64, P, P, P, I32, P, F64, P, P]),
     "sphb_tl_stress": (C.c_int, [P, P, P, P, P, P]),
     "sphb_tl_speed_max": (C.c_int, [P, P, P, P]),

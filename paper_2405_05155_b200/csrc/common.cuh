@@ -131,6 +131,23 @@ __device__ __forceinline__ void for_each_neighbor(const sphb_grid& g, int64_t n,
   }
 }
 
+// Debug builds (make debug: -DSPHB_DEBUG_BOUNDS) check every pass-list index
+// before it addresses a record: out-of-range indices raise
+// SPHB_EFLAG_BAD_INDEX in the kernel's error word and are clamped to 0.
+#ifdef SPHB_DEBUG_BOUNDS
+#define SPHB_CHECK_INDEX(j, n, err)                                       \
+  do {                                                                    \
+    if ((uint64_t)(j) >= (uint64_t)(n)) {                                 \
+      atomicOr((err), SPHB_EFLAG_BAD_INDEX);                              \
+      (j) = 0;                                                            \
+    }                                                                     \
+  } while (0)
+#else
+#define SPHB_CHECK_INDEX(j, n, err) \
+  do {                              \
+  } while (0)
+#endif
+
 // 256-bit read-only gather (sm_100: LDG.E.ENL2.256).  A plain double4 load
 // compiles to two LDG.128; one request per 32-byte record halves the L1
 // requests of the neighbour gathers.  Only for data not written by the

@@ -270,7 +270,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
   const int32_t* __restrict__ grow = nbr + i;
   for (int32_t k = 0; k < cn; ++k) {
-    const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
+    int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
+    SPHB_CHECK_INDEX(j, n, err);
     double vhj[D], g[D];
     load_vec_nc<D>(Vh, j, vhj);
     if constexpr (GEO) {
@@ -326,7 +327,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             const double* __restrict__ g0,
             const double4* __restrict__ Q, const double4* __restrict__ Vh,
             double4* __restrict__ A, double4* __restrict__ V, double* __restrict__ scalars,
-            int update_v) {
+            int update_v, int32_t* __restrict__ err) {
   const int64_t n = P.n;
   const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   extern __shared__ int32_t s_nbr[];
@@ -350,7 +351,8 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
     const int32_t* __restrict__ grow = nbr + i;
     for (int32_t k = 0; k < cn; ++k) {
-      const int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
+      int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
+    SPHB_CHECK_INDEX(j, n, err);
       double Qj[D][D], wj[D];
       if constexpr (D == 3) {      // Q rows carry X0_j in their padding (store_q)
 #pragma unroll
@@ -530,13 +532,13 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
 extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const int32_t* nbr,
                               const int32_t* cnt, const double* g0, const double* q,
                               const double* vh, double* a, double* v, double* scalars,
-                              int32_t update_v, void* stream) {
+                              int32_t update_v, int32_t* err, void* stream) {
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
                   (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
-                  (double4*)a, (double4*)v, scalars, (int)update_v);
+                  (double4*)a, (double4*)v, scalars, (int)update_v, err);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

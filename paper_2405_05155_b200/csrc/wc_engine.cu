@@ -208,7 +208,8 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     constexpr int UNR = MINB <= 4 ? 2 : 1;
 #pragma unroll UNR
     for (int32_t k = gl; k < m; k += G) {
-      const int64_t j = srow[k * RB];
+      int64_t j = srow[k * RB];
+      SPHB_CHECK_INDEX(j, n, err);
       Sym<D> bj;
       bj.load(B, n, j);
       pair(j, ldg4(X + j), ldg4(S_in + j), bj);

@@ -176,7 +176,7 @@ class FluidState:
 
 
 _EFLAGS = {1: "non-finite flux", 2: "non-positive density", 4: "det F <= 0",
-           8: "non-finite state / zero wave speed"}
+           8: "non-finite state / zero wave speed", 16: "pass-list index out of range"}
 
 
 def _describe(err: int) -> str:

@@ -308,7 +308,7 @@ class SolidSystem:
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
-                  self.scalars.data_ptr(), 0, st)
+                  self.scalars.data_ptr(), 0, self.err.data_ptr(), st)
         self._halo(self.A)
         self._acc_valid = True
 
@@ -378,7 +378,7 @@ class SolidSystem:
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
-                  self.scalars.data_ptr(), 1, st)
+                  self.scalars.data_ptr(), 1, self.err.data_ptr(), st)
         self._halo(self.V, self.A)
         self._reduce_speed()
 

@@ -288,6 +288,17 @@ typedef struct sphb_wc_params {
    * (i interior, j tagged).  sphb_wc_stage and sphb_hllc_stage only. */
   const int8_t* wall_tag;
   double* wall_force;
+  /* Fused halo push (slab ranks, sphb_wc_stage stages 1-2): rows
+   * [push_lo0, push_lo1) of the output records are also stored into the
+   * previous rank's buffer at record push_prev_at + (i - push_lo0), rows
+   * [push_hi0, push_hi1) into the next rank's at push_next_at + (i - push_hi0)
+   * (peer memory over NVLink), followed by a system-scope fence; the caller
+   * orders the peer's next stage after this one (a one-word collective).
+   * NULL pointers: no push. */
+  double* push_prev;
+  double* push_next;
+  int64_t push_lo0, push_lo1, push_prev_at;
+  int64_t push_hi0, push_hi1, push_next_at;
 } sphb_wc_params;
 
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.

@@ -107,6 +107,14 @@ class WCParams(C.Structure):
         ("gamma", C.c_double),
         ("wall_tag", C.c_void_p),
         ("wall_force", C.c_void_p),
+        ("push_prev", C.c_void_p),
+        ("push_next", C.c_void_p),
+        ("push_lo0", C.c_int64),
+        ("push_lo1", C.c_int64),
+        ("push_prev_at", C.c_int64),
+        ("push_hi0", C.c_int64),
+        ("push_hi1", C.c_int64),
+        ("push_next_at", C.c_int64),
     ]
 
 

@@ -252,7 +252,20 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
         v_new[a] = __ddiv_rn(mom_new[a], rho_new);
       }
       if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
-      S_out[i] = pack_s<D>(v_new, rho_new);
+      const double4 s_new = pack_s<D>(v_new, rho_new);
+      S_out[i] = s_new;
+      // fused halo push: boundary layers go straight into the neighbour
+      // ranks' halo rows (peer memory) from this epilogue
+      bool pushed = false;
+      if (P.push_prev && i >= P.push_lo0 && i < P.push_lo1) {
+        reinterpret_cast<double4*>(P.push_prev)[P.push_prev_at + (i - P.push_lo0)] = s_new;
+        pushed = true;
+      }
+      if (P.push_next && i >= P.push_hi0 && i < P.push_hi1) {
+        reinterpret_cast<double4*>(P.push_next)[P.push_next_at + (i - P.push_hi0)] = s_new;
+        pushed = true;
+      }
+      if (pushed) __threadfence_system();
       if (stage == 2) {
         double mc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll

@@ -143,7 +143,7 @@ extern "C" int sphb_wc_stage_geo(const sphb_wc_params* p, int32_t stage, const i
                                  const double* s_n, const double* m_n, double* s_out,
                                  double* m_out, double* scalars, int32_t* err, void* stream) {
   if (!p || p->n < 0 || stage < 0 || stage > 2 || p->row0 < 0 || p->nrows < 0 ||
-      p->row0 + p->nrows > p->n || p->wall_tag)
+      p->row0 + p->nrows > p->n || p->wall_tag || p->push_prev || p->push_next)
     return SPHB_ERR_ARG;
   if (p->nrows == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;

@@ -288,7 +288,9 @@ extern "C" int sphb_wc_stage_tiled(const sphb_wc_params* p, int32_t stage, int32
                                    int32_t rmax, int32_t umax, const double* s_in,
                                    const double* s_n, const double* m_n, double* s_out,
                                    double* m_out, double* scalars, int32_t* err, void* stream) {
-  if (!p || p->n <= 0 || stage < 0 || stage > 2 || umax <= 0 || p->wall_tag) return SPHB_ERR_ARG;
+  if (!p || p->n <= 0 || stage < 0 || stage > 2 || umax <= 0 || p->wall_tag || p->push_prev ||
+      p->push_next)
+    return SPHB_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
 #define SPHB_TILED(D, G)                                                                   \
   return launch_tiled<D, G>(p, stage, x, b, cnt, lnbr, runs, meta, rmax, umax, s_in, s_n, \

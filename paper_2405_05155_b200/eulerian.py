@@ -398,8 +398,10 @@ class EulerianSolver:
         self._mom_io = torch.empty((self.n, self.dim), dtype=torch.float64, device=dev)
         self._vol_host = vol
         self.timer = None   # optional list collecting (stage, start_event, end_event)
+        self._push = None
         self._init_extra(dev)
         self.set_state(state)
+        self._setup_push(dev)
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)
@@ -462,9 +464,43 @@ class EulerianSolver:
 
     def _halo(self, buf):
         if self._slab is not None:
+            if self._push is not None:        # the stage pushed its boundary layers
+                if buf is not self.S_nx:      # stage 2 orders through _reduce_speed
+                    self._dist.all_reduce(self._push_token)
+                return
             if self.precision == "fp32":      # neighbours read the FP32 companion
                 buf = self._c32[buf.data_ptr()]
             self._slab.exchange(self._dist, [buf])
+
+    def _setup_push(self, dev):
+        """Fused halo push (SPHB_HALO_PUSH=1): the stage kernel stores the
+        boundary layers straight into the neighbour ranks' halo rows."""
+        self._push = None
+        if not (self._slab is not None and self._slab.world > 1 and self.precision == "fp64"
+                and self.variant == "global" and self.ghosts is None
+                and os.environ.get("SPHB_HALO_PUSH", "0") == "1"):
+            return
+        torch = _lib.torch_cuda()
+        bufs = [self.S, self.S1, self.S_nx]
+        self._push = {"ids": {t.data_ptr(): k for k, t in enumerate(bufs)},
+                      "peer": self._slab.share_buffers(self._dist, bufs)}
+        self._push_token = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def _set_push(self, stage, s_out):
+        p = self.params
+        p.push_prev = p.push_next = None
+        if self._push is None or stage == 0:
+            return
+        k = self._push["ids"][s_out.data_ptr()]
+        sl = self._slab
+        if "prev" in self._push["peer"]:
+            ptrs, at = self._push["peer"]["prev"]
+            p.push_prev, p.push_lo0, p.push_lo1, p.push_prev_at = (
+                ptrs[k], sl.send_lo.start, sl.send_lo.stop, at)
+        if "next" in self._push["peer"]:
+            ptrs, at = self._push["peer"]["next"]
+            p.push_next, p.push_hi0, p.push_hi1, p.push_next_at = (
+                ptrs[k], sl.send_hi.start, sl.send_hi.stop, at)
 
     @property
     def state(self) -> FluidState:
@@ -584,6 +620,7 @@ class EulerianSolver:
                       None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                       self.err.data_ptr(), _lib.stream_ptr())
             return
+        self._set_push(stage, s_out)
         _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.group,
                   self.X.data_ptr(),
                   self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), s_in.data_ptr(),

@@ -121,6 +121,44 @@ class SlabPlan:
                 ops.append(dist.P2POp(dist.irecv, buf[self.recv_hi], self.next, group))
         return ops
 
+    def share_buffers(self, dist, tensors):
+        """Peer pointers for the fused halo push (sphb_wc_params.push_*).
+
+        Every rank passes its record buffers in the same order; returns
+        {"prev": ([ptr per buffer], halo_start), "next": (...)} with the
+        neighbour ranks' device addresses of those buffers and the record
+        index of the halo slice this rank fills (prev: its upper halo, next:
+        its lower halo).  Thread ranks (tests) share raw pointers through
+        `dist.share_device_buffers`; torch.distributed ranks exchange CUDA IPC
+        handles of the storages (all_gather_object) and map them here.
+        """
+        halo = (self.recv_lo.start if self.recv_lo is not None else -1,
+                self.recv_hi.start if self.recv_hi is not None else -1)
+        if hasattr(dist, "share_device_buffers"):
+            table = dist.share_device_buffers([t.data_ptr() for t in tensors], halo)
+        else:
+            import torch
+
+            mine = ([(t.untyped_storage()._share_cuda_(), t.storage_offset() * t.element_size())
+                     for t in tensors], halo)
+            allinfo = [None] * self.world
+            dist.all_gather_object(allinfo, mine)
+            table = {}
+            self._ipc_keep = []
+            for r in {self.prev, self.next} - {None}:
+                ptrs = []
+                for handle, off in allinfo[r][0]:
+                    st = torch.UntypedStorage._new_shared_cuda(*handle)
+                    self._ipc_keep.append(st)
+                    ptrs.append(st.data_ptr() + off)
+                table[r] = (ptrs, allinfo[r][1])
+        out = {}
+        if self.prev is not None:
+            out["prev"] = (table[self.prev][0], table[self.prev][1][1])   # its upper halo
+        if self.next is not None:
+            out["next"] = (table[self.next][0], table[self.next][1][0])   # its lower halo
+        return out
+
     def exchange(self, dist, bufs, group=None) -> None:
         """Blocking (host) / stream-ordered (NCCL) halo exchange of `bufs`."""
         if self.world == 1:

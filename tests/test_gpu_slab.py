@@ -81,6 +81,16 @@ class ThreadDist:
     def get_world_size(self):
         return self.shared.world
 
+    def share_device_buffers(self, ptrs, halo):
+        """Fused halo push: every rank's buffer pointers (same device)."""
+        sh = self.shared
+        with sh.lock:
+            sh.ptrs[self.rank] = (list(ptrs), tuple(halo))
+        sh.barrier.wait()
+        table = dict(sh.ptrs)
+        sh.barrier.wait()
+        return table
+
     def barrier(self):
         torch.cuda.current_stream().synchronize()
         self.shared.barrier.wait()
@@ -104,6 +114,7 @@ class Shared:
         self.lock = threading.Lock()
         self.box = {}
         self.red = {}
+        self.ptrs = {}
 
 
 def _state(cfg):
@@ -111,8 +122,13 @@ def _state(cfg):
     return FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
 
 
+@pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("world,kernel", [(2, "1.6h"), (3, "2h"), (4, "1.6h")])
-def test_slab_solver_matches_single_gpu(world, kernel):
+def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, push):
+    """Owned rows of every rank equal the single-GPU solver's; with `push`
+    the stage kernels store the boundary layers straight into the neighbour
+    ranks' halo rows (SPHB_HALO_PUSH=1) instead of the P2P exchange."""
+    monkeypatch.setenv("SPHB_HALO_PUSH", "1" if push else "0")
     cfg = configs.c5_tgv3d(kernel=kernel, n_side=24)
     eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=cfg["c_art"])
     steps = 5
@@ -132,6 +148,7 @@ def test_slab_solver_matches_single_gpu(world, kernel):
                 s = slab_eulerian(cfg["pos"], _state(cfg), eos, cfg["spec"], rank=rank,
                                   world=world, dist=d, cfl=cfg["cfl"], mu=cfg["mu"],
                                   periodic_box=cfg["box"])
+                assert (s._push is not None) == push
                 s.advance(steps)
                 results[rank] = s.owned()
                 torch.cuda.current_stream().synchronize()

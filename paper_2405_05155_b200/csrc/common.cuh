@@ -131,6 +131,11 @@ __device__ __forceinline__ void for_each_neighbor(const sphb_grid& g, int64_t n,
   }
 }
 
+// Dynamic shared memory above this needs cudaFuncAttributeMaxDynamicSharedMemorySize:
+// the 48 KB default covers static + dynamic, so leave room for the kernels'
+// static arrays (at most 5 KB here).
+constexpr size_t kDynSmemDefault = 43 * 1024;
+
 // Debug builds (make debug: -DSPHB_DEBUG_BOUNDS) check every pass-list index
 // before it addresses a record: out-of-range indices raise
 // SPHB_EFLAG_BAD_INDEX in the kernel's error word and are clamped to 0.

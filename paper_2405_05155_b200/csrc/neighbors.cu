@@ -219,7 +219,7 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
   double* wrapped = (double*)(w + L.wrapped);
   if (n <= kSmallBinMaxN && g->ntot <= kSmallBinMaxCells) {
     const size_t smem = sizeof(int32_t) * (2 * (size_t)g->ntot + (size_t)n);
-    if (smem > 48 * 1024) {
+    if (smem > kDynSmemDefault) {
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -483,7 +483,7 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
 // dynamic shared memory: the block's pass-list columns (stage_pass_list)
 #define TL_LAUNCH(KERNEL, GRID, TH, SMEM, ...)                                                   \
   do {                                                                                         \
-    if ((SMEM) > 48 * 1024)                                                                    \
+    if ((SMEM) > kDynSmemDefault)                                                              \
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            (int)(SMEM)));                                      \
     KERNEL<<<GRID, TH, SMEM, st>>>(__VA_ARGS__);                                               \

@@ -456,7 +456,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   }();
   if (smem_idx > 200 * 1024) return SPHB_ERR_ARG;
 #define SPHB_STAGE_W(D, G, MB, W)                                                          \
-  if (smem_idx > 48 * 1024)                                                                \
+  if (smem_idx > kDynSmemDefault)                                                          \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                          (int)smem_idx));                                  \

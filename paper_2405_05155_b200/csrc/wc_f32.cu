@@ -227,7 +227,7 @@ extern "C" int sphb_wc_stage_f32(const sphb_wc_params* p, int32_t stage, const f
   const size_t smem = (size_t)p->width * kThreads * sizeof(int32_t);
   if (smem > 200 * 1024) return SPHB_ERR_ARG;
 #define SPHB_F32(D)                                                                         \
-  if (smem > 48 * 1024)                                                                     \
+  if (smem > kDynSmemDefault)                                                               \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage_f32<D>,                                 \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                                          (int)smem));                                       \

@@ -785,3 +785,15 @@ def test_wc_opt_in_variants_vs_oracle(monkeypatch, variant):
         assert s.step() == pytest.approx(ref.step(), rel=1e-12)
     assert l2_error(s.state.rho, ref.rho) < 1e-10
     assert l2_error(s.state.mom, ref.mom) < 1e-10
+
+
+@pytest.mark.parametrize("n", [2000, 8640, 11000, 16384, 16385])
+def test_neighbors_single_block_binning_sizes(n):
+    """Sizes around the single-block binning path's shared-memory limits
+    (dynamic + static above the 48 KB default, n at the 16384 cap): the CSR
+    stays byte-identical to the oracle's."""
+    rng = np.random.default_rng(n)
+    pos = rng.uniform(0.0, 1.0, size=(n, 3))
+    for box in (None, (1.0, 1.0, 1.0)):
+        assert digest(neighbors.build_neighbors(pos, 0.09, box)) == \
+            digest(O.build_neighbors(pos, 0.09, box))

@@ -1,0 +1,112 @@
+"""Fused halo push across PROCESSES on one GPU: the CUDA-IPC mapping of
+SlabPlan.share_buffers (the path torchrun ranks take) with two processes
+sharing cuda:0.  The collectives run over gloo on host copies (an adapter
+below), so no kernel ever waits on another process: each step's ordering is
+a host-side collective after a stream synchronisation.  The owned rows of
+both ranks must equal the single-process solver's."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+class HostCollectives:
+    """torch.distributed (gloo) with CUDA tensors staged through host copies."""
+
+    class ReduceOp:
+        MAX = dist.ReduceOp.MAX
+        SUM = dist.ReduceOp.SUM
+
+    P2POp = dist.P2POp
+    isend = staticmethod(dist.isend)
+    irecv = staticmethod(dist.irecv)
+
+    def batch_isend_irecv(self, ops):
+        torch.cuda.current_stream().synchronize()
+        host, back = [], []
+        for op in ops:
+            h = op.tensor.detach().cpu().contiguous()
+            host.append(dist.P2POp(op.op, h, op.peer))
+            if op.op == dist.irecv:
+                back.append((op.tensor, h))
+        for req in dist.batch_isend_irecv(host):
+            req.wait()
+        for dst, h in back:
+            dst.copy_(h)
+        return []
+
+    def all_reduce(self, t, op=dist.ReduceOp.SUM):
+        torch.cuda.current_stream().synchronize()
+        h = t.detach().cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+
+    def all_gather_object(self, out, obj):
+        dist.all_gather_object(out, obj)
+
+    def barrier(self):
+        torch.cuda.current_stream().synchronize()
+        dist.barrier()
+
+    def get_rank(self):
+        return dist.get_rank()
+
+    def get_world_size(self):
+        return dist.get_world_size()
+
+
+def _rank(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2405_05155_b200 import configs
+        from paper_2405_05155_b200.eulerian import WEAKLY_COMPRESSIBLE, EosParams, FluidState
+        from paper_2405_05155_b200.slab import slab_eulerian
+
+        cfg = configs.c5_tgv3d(kernel="1.6h", n_side=24)
+        n = cfg["pos"].shape[0]
+        st = FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
+        s = slab_eulerian(cfg["pos"], st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0),
+                          cfg["spec"], rank=rank, world=world, dist=HostCollectives(),
+                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+        assert s._push is not None and s._slab._ipc_keep
+        s.advance(5)
+        ids, rho, mom = s.owned()
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids, rho=rho, mom=mom)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_push_over_cuda_ipc(tmp_path):
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                                FluidState)
+
+    cfg = configs.c5_tgv3d(kernel="1.6h", n_side=24)
+    n = cfg["pos"].shape[0]
+    ref = EulerianSolver(cfg["pos"], n, FluidState(cfg["vol"].copy(), cfg["rho"].copy(),
+                                                   cfg["mom"].copy(), None, n),
+                         EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0), cfg["spec"], None,
+                         cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+    ref.advance(5)
+    want = ref.state
+    world = 2
+    mp.start_processes(_rank, args=(world, 29511, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got_rho = np.full(n, np.nan)
+    got_mom = np.full((n, 3), np.nan)
+    for r in range(world):
+        z = np.load(tmp_path / f"r{r}.npz")
+        got_rho[z["ids"]] = z["rho"]
+        got_mom[z["ids"]] = z["mom"]
+    assert not np.isnan(got_rho).any()
+    np.testing.assert_allclose(got_rho, want.rho, rtol=1e-14, atol=0)
+    np.testing.assert_allclose(got_mom, want.mom, rtol=1e-12, atol=1e-14)

@@ -31,7 +31,6 @@ import subprocess
 import sys
 import time
 
-import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)

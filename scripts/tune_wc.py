@@ -9,7 +9,6 @@ variant with the mean stage time (CUDA events).
 """
 
 import argparse
-import itertools
 import json
 import os
 import subprocess

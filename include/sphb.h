@@ -461,6 +461,19 @@ typedef struct sphb_tl_params {
   double h, alpha, kappa;  /* Wendland family */
   double vol0, rho0;
   double lam, g;           /* Lame parameters (tlsph.py:27-35) */
+  /* Fused halo push (slab ranks): pass A also stores the Q records of rows
+   * [push_lo0, push_lo1) into the previous rank's Q buffer at particle
+   * push_prev_at + (i - push_lo0) and rows [push_hi0, push_hi1) into the
+   * next rank's at push_next_at + (i - push_hi0); pass B does the same with
+   * A (and V when it updates v).  Peer memory, system-scope fence; NULL: off. */
+  double* push_q_prev;
+  double* push_q_next;
+  double* push_a_prev;
+  double* push_a_next;
+  double* push_v_prev;
+  double* push_v_next;
+  int64_t push_lo0, push_lo1, push_prev_at;
+  int64_t push_hi0, push_hi1, push_next_at;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows

@@ -132,6 +132,18 @@ class TLParams(C.Structure):
         ("rho0", C.c_double),
         ("lam", C.c_double),
         ("g", C.c_double),
+        ("push_q_prev", C.c_void_p),
+        ("push_q_next", C.c_void_p),
+        ("push_a_prev", C.c_void_p),
+        ("push_a_next", C.c_void_p),
+        ("push_v_prev", C.c_void_p),
+        ("push_v_next", C.c_void_p),
+        ("push_lo0", C.c_int64),
+        ("push_lo1", C.c_int64),
+        ("push_prev_at", C.c_int64),
+        ("push_hi0", C.c_int64),
+        ("push_hi1", C.c_int64),
+        ("push_next_at", C.c_int64),
     ]
 
 

@@ -313,6 +313,18 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
   store_mat<D>(F, i, Fi);
   store_q<D>(Q, i, Qi, wi);
+  {   // fused halo push of the boundary layers' Q records
+    bool pushed = false;
+    if (P.push_q_prev && i >= P.push_lo0 && i < P.push_lo1) {
+      store_q<D>(reinterpret_cast<double4*>(P.push_q_prev), P.push_prev_at + (i - P.push_lo0), Qi, wi);
+      pushed = true;
+    }
+    if (P.push_q_next && i >= P.push_hi0 && i < P.push_hi1) {
+      store_q<D>(reinterpret_cast<double4*>(P.push_q_next), P.push_next_at + (i - P.push_hi0), Qi, wi);
+      pushed = true;
+    }
+    if (pushed) __threadfence_system();
+  }
   double xc[D];
   load_vec<D>(XC, i, xc);
 #pragma unroll
@@ -400,7 +412,12 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
 #pragma unroll
       for (int a = 0; a < D; ++a) c4[a] = acc[a];
       c4[3] = fixed_i ? 1.0 : 0.0;
-      A[i] = make_double4(c4[0], c4[1], c4[2], c4[3]);
+      const double4 a4 = make_double4(c4[0], c4[1], c4[2], c4[3]);
+      A[i] = a4;
+      if (P.push_a_prev && i >= P.push_lo0 && i < P.push_lo1)
+        reinterpret_cast<double4*>(P.push_a_prev)[P.push_prev_at + (i - P.push_lo0)] = a4;
+      if (P.push_a_next && i >= P.push_hi0 && i < P.push_hi1)
+        reinterpret_cast<double4*>(P.push_a_next)[P.push_next_at + (i - P.push_hi0)] = a4;
     }
     double v[D];
     if (update_v) {
@@ -409,9 +426,16 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
 #pragma unroll
       for (int a = 0; a < D; ++a) v[a] = fixed_i ? 0.0 : fma(hdt, acc[a], v[a]);
       store_vec<D>(V, i, v);
+      if (P.push_v_prev && i >= P.push_lo0 && i < P.push_lo1)
+        store_vec<D>(reinterpret_cast<double4*>(P.push_v_prev), P.push_prev_at + (i - P.push_lo0), v);
+      if (P.push_v_next && i >= P.push_hi0 && i < P.push_hi1)
+        store_vec<D>(reinterpret_cast<double4*>(P.push_v_next), P.push_next_at + (i - P.push_hi0), v);
     } else {
       load_vec<D>(V, i, v);
     }
+    if ((P.push_a_prev || P.push_a_next) &&
+        ((i >= P.push_lo0 && i < P.push_lo1) || (i >= P.push_hi0 && i < P.push_hi1)))
+      __threadfence_system();
     double s2 = __dmul_rn(v[0], v[0]);
 #pragma unroll
     for (int a = 1; a < D; ++a) s2 = __dadd_rn(s2, __dmul_rn(v[a], v[a]));

@@ -240,6 +240,7 @@ class SolidSystem:
                       self.cnt.data_ptr(), self.width, ctypes.byref(k), self.dp**d,
                       self.g0.data_ptr(), _lib.stream_ptr())
         self._g0_ptr = None if self.g0 is None else self.g0.data_ptr()
+        self._setup_push(dev)
         self._acc_valid = False
         self._host = {}
         self._v_out = False
@@ -316,6 +317,34 @@ class SolidSystem:
         if self._slab is not None:
             self._slab.exchange(self._dist, list(bufs))
 
+    def _setup_push(self, dev):
+        """Fused halo push (SPHB_HALO_PUSH=1): pass A stores the boundary
+        layers' Q records and pass B their A / V records straight into the
+        neighbour ranks' halo rows (peer memory)."""
+        self._push = None
+        if not (self._slab is not None and self._slab.world > 1
+                and os.environ.get("SPHB_HALO_PUSH", "0") == "1"):
+            return
+        torch = _lib.torch_cuda()
+        self._push = self._slab.share_buffers(self._dist, [self.Qrec, self.A, self.V])
+        self._push_token = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def _set_push(self, on: bool):
+        p = self.params
+        p.push_q_prev = p.push_q_next = p.push_a_prev = p.push_a_next = None
+        p.push_v_prev = p.push_v_next = None
+        if not on or self._push is None:
+            return
+        sl = self._slab
+        if "prev" in self._push:
+            (q, a, v), at = self._push["prev"]
+            p.push_q_prev, p.push_a_prev, p.push_v_prev = q, a, v
+            p.push_lo0, p.push_lo1, p.push_prev_at = sl.send_lo.start, sl.send_lo.stop, at
+        if "next" in self._push:
+            (q, a, v), at = self._push["next"]
+            p.push_q_next, p.push_a_next, p.push_v_next = q, a, v
+            p.push_hi0, p.push_hi1, p.push_next_at = sl.send_hi.start, sl.send_hi.stop, at
+
     def _reduce_speed(self):
         if self._slab is not None and self._slab.world > 1:
             self._dist.all_reduce(self.scalars[2:3], op=self._dist.ReduceOp.MAX)
@@ -367,6 +396,7 @@ class SolidSystem:
 
     def _one_step(self, dt_override: float):
         st = _lib.stream_ptr()
+        self._set_push(True)
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
         _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
@@ -374,12 +404,17 @@ class SolidSystem:
                   self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
                   self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
-        self._halo(self.Qrec)
+        if self._push is not None:                  # Q halos were pushed by pass A
+            self._dist.all_reduce(self._push_token)
+        else:
+            self._halo(self.Qrec)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
                   self.scalars.data_ptr(), 1, self.err.data_ptr(), st)
-        self._halo(self.V, self.A)
+        self._set_push(False)
+        if self._push is None:                      # else pushed; the max orders them
+            self._halo(self.V, self.A)
         self._reduce_speed()
 
     def _raise_if_bad(self):

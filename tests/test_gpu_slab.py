@@ -174,13 +174,17 @@ def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, push):
     np.testing.assert_allclose(got_mom, want_mom, rtol=1e-12, atol=1e-14)
 
 
+@pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("world,kernel", [(2, "1.6h"), (3, "2h")])
-def test_slab_solid_matches_single_gpu(world, kernel):
+def test_slab_solid_matches_single_gpu(monkeypatch, world, kernel, push):
+    """Owned rows equal the single-GPU system's; with `push` the pass A / B
+    epilogues write the Q, a and v halos into the neighbours' rows."""
     from paper_2405_05155_b200.slab import slab_solid
     from paper_2405_05155_b200.tlsph import SolidSystem
 
     cfg = configs.c4_column(kernel=kernel, n_width=6)
     steps = 20
+    monkeypatch.setenv("SPHB_HALO_PUSH", "1" if push else "0")
     ref = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
                       cfl=cfg["cfl"])
     ref.v = cfg["v0"]
@@ -198,6 +202,7 @@ def test_slab_solid_matches_single_gpu(world, kernel):
                 s = slab_solid(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], rank=rank,
                                world=world, dist=d, fixed=cfg["fixed"], cfl=cfg["cfl"])
                 assert s._slab.axis == 1          # the column's long axis
+                assert (s._push is not None) == push
                 s.v = cfg["v0"][s.local_ids]
                 s.advance(steps)
                 results[rank] = s.owned()

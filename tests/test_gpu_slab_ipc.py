@@ -1,4 +1,4 @@
-"""Fused halo push across PROCESSES on one GPU: the CUDA-IPC mapping of
+"""Fused halo push (WC stage and TL passes) across PROCESSES on one GPU: the CUDA-IPC mapping of
 SlabPlan.share_buffers (the path torchrun ranks take) with two processes
 sharing cuda:0.  The collectives run over gloo on host copies (an adapter
 below), so no kernel ever waits on another process: each step's ordering is
@@ -85,6 +85,27 @@ def _rank(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
+def _solid_rank(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2405_05155_b200 import configs
+        from paper_2405_05155_b200.slab import slab_solid
+
+        cfg = configs.c4_column(kernel="1.6h", n_width=6)
+        s = slab_solid(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], rank=rank,
+                       world=world, dist=HostCollectives(), fixed=cfg["fixed"], cfl=cfg["cfl"])
+        assert s._push is not None and s._slab._ipc_keep
+        s.v = cfg["v0"][s.local_ids]
+        s.advance(10)
+        ids, x, v, F = s.owned()
+        np.savez(os.path.join(out_dir, f"s{rank}.npz"), ids=ids, x=x, v=v, F=F)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_halo_push_over_cuda_ipc(tmp_path):
     from paper_2405_05155_b200 import configs
     from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
@@ -110,3 +131,27 @@ def test_halo_push_over_cuda_ipc(tmp_path):
     assert not np.isnan(got_rho).any()
     np.testing.assert_allclose(got_rho, want.rho, rtol=1e-14, atol=0)
     np.testing.assert_allclose(got_mom, want.mom, rtol=1e-12, atol=1e-14)
+
+
+def test_solid_halo_push_over_cuda_ipc(tmp_path):
+    """TL-SPH: pass A pushes Q, pass B pushes a and v across processes."""
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.tlsph import SolidSystem
+
+    cfg = configs.c4_column(kernel="1.6h", n_width=6)
+    ref = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
+                      cfl=cfg["cfl"])
+    ref.v = cfg["v0"]
+    ref.advance(10)
+    want = (ref.x, ref.v, ref.F)
+    world = 2
+    mp.start_processes(_solid_rank, args=(world, 29512, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = [np.full_like(w, np.nan) for w in want]
+    for r in range(world):
+        z = np.load(tmp_path / f"s{r}.npz")
+        for g, key in zip(got, ("x", "v", "F")):
+            g[z["ids"]] = z[key]
+    for g, w in zip(got, want):
+        assert not np.isnan(g).any()
+        np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-14 * np.abs(w).max())

@@ -474,6 +474,11 @@ typedef struct sphb_tl_params {
   double* push_v_next;
   int64_t push_lo0, push_lo1, push_prev_at;
   int64_t push_hi0, push_hi1, push_next_at;
+  /* 3D Q records are three row planes Q[r * q_stride + i] (one 32-byte
+   * {q_r0, q_r1, q_r2, X0_r} per plane and particle), so a warp's gather of
+   * one row touches consecutive records; q_stride >= n, 0 means n.  Slab
+   * ranks use one common stride so pushes address peer buffers with it. */
+  int64_t q_stride;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows

@@ -144,6 +144,7 @@ class TLParams(C.Structure):
         ("push_hi0", C.c_int64),
         ("push_hi1", C.c_int64),
         ("push_next_at", C.c_int64),
+        ("q_stride", C.c_int64),
     ]
 
 

@@ -41,13 +41,15 @@ inline int tl_stage_max_width() {
   return w;
 }
 
+// 3x3 records are three row planes M[r * ms + i] (ms = plane stride), so a
+// warp's access to one row covers consecutive 32-byte records
 template <int D>
-__device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t i,
+__device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t ms, int64_t i,
                                          double (&a)[D][D]) {
   if constexpr (D == 3) {
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      double4 t = M[3 * i + r];
+      double4 t = M[r * ms + i];
       a[r][0] = t.x; a[r][1] = t.y; a[r][2] = t.z;
     }
   } else if constexpr (D == 2) {
@@ -59,11 +61,11 @@ __device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t 
 }
 
 template <int D>
-__device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t i,
+__device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t ms, int64_t i,
                                           const double (&a)[D][D]) {
   if constexpr (D == 3) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) M[3 * i + r] = make_double4(a[r][0], a[r][1], a[r][2], 0.0);
+    for (int r = 0; r < 3; ++r) M[r * ms + i] = make_double4(a[r][0], a[r][1], a[r][2], 0.0);
   } else if constexpr (D == 2) {
     M[i] = make_double4(a[0][0], a[0][1], a[1][0], a[1][1]);
   } else {
@@ -72,16 +74,32 @@ __device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t i,
 }
 
 // Q record with the particle's reference coordinates in the row padding
-// (3D: rows {q_r0, q_r1, q_r2, X0_r}); pass B then reads Q_j and X0_j with
-// three 256-bit gathers instead of four.  2D/1D records have no padding.
+// (3D: rows {q_r0, q_r1, q_r2, X0_r} in three planes of stride qs); pass B
+// then reads Q_j and X0_j with three 256-bit gathers instead of four, each
+// over consecutive records (plane layout: 8 instead of 24 lines per warp
+// request).  2D/1D records have no padding and no planes.
 template <int D>
-__device__ __forceinline__ void store_q(double4* __restrict__ Q, int64_t i, const double (&a)[D][D],
-                                        const double (&w)[D]) {
+__device__ __forceinline__ void store_q(double4* __restrict__ Q, int64_t qs, int64_t i,
+                                        const double (&a)[D][D], const double (&w)[D]) {
   if constexpr (D == 3) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) Q[3 * i + r] = make_double4(a[r][0], a[r][1], a[r][2], w[r]);
+    for (int r = 0; r < 3; ++r) Q[r * qs + i] = make_double4(a[r][0], a[r][1], a[r][2], w[r]);
   } else {
-    store_mat<D>(Q, i, a);
+    store_mat<D>(Q, qs, i, a);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_q(const double4* __restrict__ Q, int64_t qs, int64_t i,
+                                       double (&a)[D][D]) {
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double4 t = Q[r * qs + i];
+      a[r][0] = t.x; a[r][1] = t.y; a[r][2] = t.z;
+    }
+  } else {
+    load_mat<D>(Q, qs, i, a);
   }
 }
 
@@ -114,13 +132,8 @@ __device__ __forceinline__ void load_vec_nc(const double4* __restrict__ V, int64
 template <int D>
 __device__ __forceinline__ void load_mat_nc(const double4* __restrict__ M, int64_t i,
                                             double (&a)[D][D]) {
-  if constexpr (D == 3) {
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const double4 t = ldg4(M + 3 * i + r);
-      a[r][0] = t.x; a[r][1] = t.y; a[r][2] = t.z;
-    }
-  } else if constexpr (D == 2) {
+  static_assert(D < 3, "3D gathers read the Q planes directly");
+  if constexpr (D == 2) {
     const double4 t = ldg4(M + i);
     a[0][0] = t.x; a[0][1] = t.y; a[1][0] = t.z; a[1][1] = t.w;
   } else {
@@ -233,8 +246,10 @@ __global__ void k_tl_kick(int64_t n, const double4* __restrict__ X0,
   store_vec<D>(Vh, i, vh);
 }
 
-template <int D, bool GEO, bool STAGED>
-__global__ void __launch_bounds__(kThreads)
+// UNR: pairs in flight per thread; 3D default 2 (two Vh_j + X0_j gather
+// pairs outstanding: -12% on C4, profiles/r01_tune_tl.md)
+template <int D, bool GEO, bool STAGED, int MINB = 1, int UNR = (D == 3 ? 2 : 1)>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double4* __restrict__ B0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
             const double* __restrict__ g0,
@@ -269,6 +284,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   const int32_t cn = cnt[i];
   const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
   const int32_t* __restrict__ grow = nbr + i;
+#pragma unroll UNR
   for (int32_t k = 0; k < cn; ++k) {
     int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
     SPHB_CHECK_INDEX(j, n, err);
@@ -296,8 +312,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   }
 
   double B[D][D], Fi[D][D];
-  load_mat<D>(B0, i, B);
-  load_mat<D>(F, i, Fi);
+  load_mat<D>(B0, n, i, B);
+  load_mat<D>(F, n, i, Fi);
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -311,16 +327,19 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   if (!(J > 0.0)) atomicOr(err, SPHB_EFLAG_DET_NONPOS);
   double Qi[D][D];
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
-  store_mat<D>(F, i, Fi);
-  store_q<D>(Q, i, Qi, wi);
+  store_mat<D>(F, n, i, Fi);
+  const int64_t qs = P.q_stride ? P.q_stride : n;
+  store_q<D>(Q, qs, i, Qi, wi);
   {   // fused halo push of the boundary layers' Q records
     bool pushed = false;
     if (P.push_q_prev && i >= P.push_lo0 && i < P.push_lo1) {
-      store_q<D>(reinterpret_cast<double4*>(P.push_q_prev), P.push_prev_at + (i - P.push_lo0), Qi, wi);
+      store_q<D>(reinterpret_cast<double4*>(P.push_q_prev), qs, P.push_prev_at + (i - P.push_lo0),
+                 Qi, wi);
       pushed = true;
     }
     if (P.push_q_next && i >= P.push_hi0 && i < P.push_hi1) {
-      store_q<D>(reinterpret_cast<double4*>(P.push_q_next), P.push_next_at + (i - P.push_hi0), Qi, wi);
+      store_q<D>(reinterpret_cast<double4*>(P.push_q_next), qs, P.push_next_at + (i - P.push_hi0),
+                 Qi, wi);
       pushed = true;
     }
     if (pushed) __threadfence_system();
@@ -332,8 +351,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   store_vec<D>(XC, i, xc);
 }
 
-template <int D, bool GEO, bool STAGED>
-__global__ void __launch_bounds__(kThreads)
+template <int D, bool GEO, bool STAGED, int MINB = 1, int UNR = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
             const double* __restrict__ g0,
@@ -354,22 +373,24 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     double wi[D];
     bool fixed_i;
     load_x0<D>(X0, i, wi, fixed_i);
+    const int64_t qs = P.q_stride ? P.q_stride : n;
     double Qi[D][D];
-    load_mat<D>(Q, i, Qi);
+    load_q<D>(Q, qs, i, Qi);
     double gsum[D], acc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) { gsum[a] = 0.0; acc[a] = 0.0; }
     const int32_t cn = cnt[i];
     const int32_t* __restrict__ srow = s_nbr + threadIdx.x;
     const int32_t* __restrict__ grow = nbr + i;
+#pragma unroll UNR
     for (int32_t k = 0; k < cn; ++k) {
       int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
-    SPHB_CHECK_INDEX(j, n, err);
+      SPHB_CHECK_INDEX(j, n, err);
       double Qj[D][D], wj[D];
       if constexpr (D == 3) {      // Q rows carry X0_j in their padding (store_q)
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-          const double4 t4 = ldg4(Q + 3 * j + r);
+          const double4 t4 = ldg4(Q + r * qs + j);
           Qj[r][0] = t4.x; Qj[r][1] = t4.y; Qj[r][2] = t4.z;
           wj[r] = t4.w;
         }
@@ -461,11 +482,11 @@ __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ 
   if (i >= P.n) return;
   double Fi[D][D], B[D][D], Qi[D][D], w[D];
   bool fixed;
-  load_mat<D>(F, i, Fi);
-  load_mat<D>(B0, i, B);
+  load_mat<D>(F, P.n, i, Fi);
+  load_mat<D>(B0, P.n, i, B);
   load_x0<D>(X0, i, w, fixed);
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
-  store_q<D>(Q, i, Qi, w);
+  store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);
 }
 
 template <int D>
@@ -536,6 +557,27 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
     }                                                                                      \
   } while (0)
 
+// Tuning variants of the 3D staged passes (SPHB_TL_VARIANT_A / _B =
+// minb*10 + unroll): register cap via min blocks per SM, pairs in flight.
+inline int tl_variant(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
+#define TL_TUNED(KERNEL, VAR, GRID, TH, ...)                                                    \
+  do {                                                                                        \
+    const size_t smem_ = (size_t)p->width * kThreads * sizeof(int32_t);                       \
+    switch (VAR) {                                                                            \
+      case 11: TL_LAUNCH((KERNEL<3, false, true, 1, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
+      case 12: TL_LAUNCH((KERNEL<3, false, true, 1, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
+      case 61: TL_LAUNCH((KERNEL<3, false, true, 6, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
+      case 62: TL_LAUNCH((KERNEL<3, false, true, 6, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
+      case 81: TL_LAUNCH((KERNEL<3, false, true, 8, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
+      case 82: TL_LAUNCH((KERNEL<3, false, true, 8, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
+      default: return SPHB_ERR_ARG;                                                           \
+    }                                                                                         \
+  } while (0)
+
 extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,
                               const int32_t* nbr, const int32_t* cnt, const double* g0,
                               const double* v, const double* a, double* vh, double* xc,
@@ -546,9 +588,15 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   cudaStream_t st = (cudaStream_t)stream;
   TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)x0,
               (const double4*)v, (const double4*)a, (double4*)vh, scalars);
-  TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
-                  (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
-                  (double4*)xc, (double4*)f, (double4*)q, scalars, err);
+  static const int var = tl_variant("SPHB_TL_VARIANT_A");
+  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
+    TL_TUNED(k_tl_pass_a, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+             (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
+             (double4*)xc, (double4*)f, (double4*)q, scalars, err);
+  else
+    TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+                    (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
+                    (double4*)xc, (double4*)f, (double4*)q, scalars, err);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }
@@ -560,9 +608,15 @@ extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const i
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
-                  (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
-                  (double4*)a, (double4*)v, scalars, (int)update_v, err);
+  static const int var = tl_variant("SPHB_TL_VARIANT_B");
+  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
+    TL_TUNED(k_tl_pass_b, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+             (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
+             (double4*)a, (double4*)v, scalars, (int)update_v, err);
+  else
+    TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+                    (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
+                    (double4*)a, (double4*)v, scalars, (int)update_v, err);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

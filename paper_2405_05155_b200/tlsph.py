@@ -121,21 +121,25 @@ def _vec_rec(arr_sorted, n, dim, dev):
 
 
 def _mat_rec(m_sorted, n, dim, dev):
-    """(n, d, d) -> padded row records (3D: (n, 3, 4); 2D: (n, 4); 1D: (n, 4))."""
+    """(n, d, d) -> padded row records (3D: three row planes (3, n, 4);
+    2D: (n, 4); 1D: (n, 4))."""
     torch = _lib.torch_cuda()
     if dim == 3:
-        out = torch.zeros((n, 3, 4), dtype=torch.float64, device=dev)
-        out[:, :, :3] = m_sorted
+        out = torch.zeros((3, n, 4), dtype=torch.float64, device=dev)
+        out[:, :, :3] = m_sorted.permute(1, 0, 2)
         return out
     out = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     out[:, :dim * dim] = m_sorted.reshape(n, dim * dim)
     return out
 
 
-def _mat_unrec(rec, n, dim):
+def _mat_unrec(rec, n, dim, rows=None):
+    """Records -> (n, d, d) matrices (optionally only `rows`)."""
     if dim == 3:
-        return rec[:, :, :3]
-    return rec[:, :dim * dim].reshape(n, dim, dim)
+        planes = rec[:, :, :3] if rows is None else rec[:, rows, :3]
+        return planes.permute(1, 0, 2)
+    out = rec if rows is None else rec[rows]
+    return out[:, :dim * dim].reshape(-1, dim, dim)
 
 
 class SolidSystem:
@@ -206,7 +210,19 @@ class SolidSystem:
         self.B0rec = _mat_rec(b0, n, d, dev)
         eye = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d)
         self.Frec = _mat_rec(eye, n, d, dev)
-        self.Qrec = torch.zeros_like(self.Frec)
+        # Q: three row planes in 3D (tl_engine.cu store_q), one stride for
+        # all slab ranks so the fused halo push can address peer planes
+        self._q_stride = n
+        if d == 3:
+            if _slab is not None and _slab.world > 1:
+                qs = torch.tensor([n], dtype=torch.float64, device=dev)
+                _dist.all_reduce(qs, op=_dist.ReduceOp.MAX)
+                self._q_stride = int(qs.item())
+            self.Qrec = torch.zeros((3, self._q_stride, 4), dtype=torch.float64, device=dev)
+            self._q_halo = [self.Qrec[r] for r in range(3)]
+        else:
+            self.Qrec = torch.zeros_like(self.Frec)
+            self._q_halo = [self.Qrec]
         xs = _lib.to_device(self.X0, torch.float64)[self.perm]
         self.XC = _vec_rec(xs, n, d, dev)
         self.V = torch.zeros((n, 4), dtype=torch.float64, device=dev)
@@ -223,6 +239,7 @@ class SolidSystem:
                            if _slab is not None else (0, n))
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
         p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
+        p.q_stride = self._q_stride
         self._cfl_h = self.cfl * kernel.h
         self._c_s = material.sound_speed
         # reference gradients g0: recomputed per pair from X0 by default (with
@@ -305,7 +322,7 @@ class SolidSystem:
         st = _lib.stream_ptr()
         _lib.call("sphb_tl_stress", ctypes.byref(self.params), self.Frec.data_ptr(),
                   self.B0rec.data_ptr(), self.X0rec.data_ptr(), self.Qrec.data_ptr(), st)
-        self._halo(self.Qrec)
+        self._halo(*self._q_halo)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
@@ -357,7 +374,7 @@ class SolidSystem:
             ids = self._slab.local_ids[ids]
         x = self.XC[rows, :self.dim].cpu().numpy()
         v = self.V[rows, :self.dim].cpu().numpy()
-        F = _mat_unrec(self.Frec[rows], rows.stop - rows.start, self.dim).cpu().numpy()
+        F = _mat_unrec(self.Frec, rows.stop - rows.start, self.dim, rows).cpu().numpy()
         return ids, x, v, F
 
     def accelerations(self):
@@ -407,7 +424,7 @@ class SolidSystem:
         if self._push is not None:                  # Q halos were pushed by pass A
             self._dist.all_reduce(self._push_token)
         else:
-            self._halo(self.Qrec)
+            self._halo(*self._q_halo)
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
                   self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),

@@ -374,8 +374,6 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
     bool fixed_i;
     load_x0<D>(X0, i, wi, fixed_i);
     const int64_t qs = P.q_stride ? P.q_stride : n;
-    double Qi[D][D];
-    load_q<D>(Q, qs, i, Qi);
     double gsum[D], acc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) { gsum[a] = 0.0; acc[a] = 0.0; }
@@ -421,6 +419,8 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
         for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
     }
     const double inv_rho0 = 1.0 / P.rho0;
+    double Qi[D][D];                  // loaded after the loop: 18 registers free in it
+    load_q<D>(Q, qs, i, Qi);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       double s = acc[a];

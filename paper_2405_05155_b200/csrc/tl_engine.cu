@@ -525,12 +525,27 @@ __global__ void k_tl_speed(int64_t row0, int64_t nrows, const double4* __restric
     }                                                                      \
   } while (0)
 
+// SPHB_TL_CARVEOUT (tuning): preferred shared-memory carveout, % of the
+// unified L1 / shared array; default -1 = the driver's choice (a fixed 40%
+// gains 1.6% at 1.6h but starves the 2h pass-list staging, r01_tune_tl.md)
+inline int tl_carveout() {
+  static const int c = [] {
+    const char* e = getenv("SPHB_TL_CARVEOUT");
+    return e ? atoi(e) : -1;
+  }();
+  return c;
+}
+
 // dynamic shared memory: the block's pass-list columns (stage_pass_list)
 #define TL_LAUNCH(KERNEL, GRID, TH, SMEM, ...)                                                   \
   do {                                                                                         \
     if ((SMEM) > kDynSmemDefault)                                                              \
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            (int)(SMEM)));                                      \
+    if (tl_carveout() >= 0)                                                                    \
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL,                                             \
+                                           cudaFuncAttributePreferredSharedMemoryCarveout,     \
+                                           tl_carveout()));                                    \
     KERNEL<<<GRID, TH, SMEM, st>>>(__VA_ARGS__);                                               \
   } while (0)
 

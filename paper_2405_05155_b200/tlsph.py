@@ -476,9 +476,11 @@ class SolidSystem:
         if graph is None:
             graph = n_steps >= 8 and self._slab is None
         if graph:
-            g = self._step_graph(dto)
-            for _ in range(n_steps):
+            g, per = self._step_graph(dto)
+            for _ in range(n_steps // per):
                 g.replay()
+            for _ in range(n_steps % per):
+                self._one_step(dto)
         else:
             for _ in range(n_steps):
                 self._one_step(dto)
@@ -491,15 +493,19 @@ class SolidSystem:
         torch = _lib.torch_cuda()
         if getattr(self, "_graphs", None) is None:
             self._graphs = {}
+        from .eulerian import graph_steps
+
+        per = graph_steps()          # steps per replay (amortises replay latency)
         g = self._graphs.get(dt_override)
         if g is None:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._one_step(dt_override)
+                for _ in range(per):
+                    self._one_step(dt_override)
             torch.cuda.synchronize()
             self._graphs[dt_override] = g
-        return g
+        return g, per
 
     # -- diagnostics ------------------------------------------------------------
     def von_mises_field(self):

@@ -399,9 +399,11 @@ class EulerianSolver:
         self._vol_host = vol
         self.timer = None   # optional list collecting (stage, start_event, end_event)
         self._push = None
+        self._overlap = None
         self._init_extra(dev)
         self.set_state(state)
         self._setup_push(dev)
+        self._setup_overlap()
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)
@@ -464,6 +466,9 @@ class EulerianSolver:
 
     def _halo(self, buf):
         if self._slab is not None:
+            if self._overlap is not None:     # exchange started by _launch_stage_raw
+                _lib.torch_cuda().cuda.current_stream().wait_stream(self._overlap)
+                return
             if self._push is not None:        # the stage pushed its boundary layers
                 if buf is not self.S_nx:      # stage 2 orders through _reduce_speed
                     self._dist.all_reduce(self._push_token)
@@ -471,6 +476,39 @@ class EulerianSolver:
             if self.precision == "fp32":      # neighbours read the FP32 companion
                 buf = self._c32[buf.data_ptr()]
             self._slab.exchange(self._dist, [buf])
+
+    def _setup_overlap(self):
+        """Boundary-first stages (slab ranks, NCCL exchange; default on,
+        SPHB_SLAB_OVERLAP=0 disables): each stage first updates the two
+        layers it sends, starts their exchange on a side stream, then updates
+        the interior rows while the layers travel.  Row sets are disjoint, so
+        the fields are bit-identical to one launch over all owned rows."""
+        self._overlap = None
+        if (self._slab is not None and self._slab.world > 1 and self._push is None
+                and self.precision == "fp64" and self.variant == "global"
+                and self.ghosts is None and os.environ.get("SPHB_SLAB_OVERLAP", "1") != "0"):
+            self._overlap = _lib.torch_cuda().cuda.Stream()
+
+    def _stage_boundary_first(self, stage, s_in, s_n, m_n, s_out, m_out):
+        torch = _lib.torch_cuda()
+        sl, p = self._slab, self.params
+        lo, hi = sl.send_lo, sl.send_hi
+        parts = [lo, hi] if lo.start < hi.start else [slice(lo.start, hi.stop)]
+        if lo.stop < hi.start:
+            parts.append(slice(lo.stop, hi.start))          # interior, launched last
+        for k, part in enumerate(parts):
+            p.row0, p.nrows = part.start, part.stop - part.start
+            _lib.call("sphb_wc_stage", ctypes.byref(p), stage, self.group, self.X.data_ptr(),
+                      self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                      s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
+                      None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                      self.err.data_ptr(), _lib.stream_ptr())
+            if k == min(1, len(parts) - 1) and stage != 0:   # both sent layers done
+                comm = self._overlap
+                comm.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(comm):
+                    sl.exchange(self._dist, [s_out])
+        p.row0, p.nrows = sl.rows.start, sl.rows.stop - sl.rows.start
 
     def _setup_push(self, dev):
         """Fused halo push (SPHB_HALO_PUSH=1): the stage kernel stores the
@@ -619,6 +657,9 @@ class EulerianSolver:
                       pl.umax, s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
                       None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                       self.err.data_ptr(), _lib.stream_ptr())
+            return
+        if self._overlap is not None and stage != 0:
+            self._stage_boundary_first(stage, s_in, s_n, m_n, s_out, m_out)
             return
         self._set_push(stage, s_out)
         _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.group,

@@ -122,13 +122,17 @@ def _state(cfg):
     return FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
 
 
-@pytest.mark.parametrize("push", [False, True])
+@pytest.mark.parametrize("mode", ["exchange", "overlap", "push"])
 @pytest.mark.parametrize("world,kernel", [(2, "1.6h"), (3, "2h"), (4, "1.6h")])
-def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, push):
-    """Owned rows of every rank equal the single-GPU solver's; with `push`
-    the stage kernels store the boundary layers straight into the neighbour
-    ranks' halo rows (SPHB_HALO_PUSH=1) instead of the P2P exchange."""
+def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, mode):
+    """Owned rows of every rank equal the single-GPU solver's: with the P2P
+    exchange after each stage, with boundary-first stages whose exchange runs
+    on a side stream under the interior rows (the default), and with `push`
+    (the stage kernels store the boundary layers straight into the neighbour
+    ranks' halo rows, SPHB_HALO_PUSH=1)."""
+    push = mode == "push"
     monkeypatch.setenv("SPHB_HALO_PUSH", "1" if push else "0")
+    monkeypatch.setenv("SPHB_SLAB_OVERLAP", "1" if mode == "overlap" else "0")
     cfg = configs.c5_tgv3d(kernel=kernel, n_side=24)
     eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=cfg["c_art"])
     steps = 5
@@ -149,6 +153,7 @@ def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, push):
                                   world=world, dist=d, cfl=cfg["cfl"], mu=cfg["mu"],
                                   periodic_box=cfg["box"])
                 assert (s._push is not None) == push
+                assert (s._overlap is not None) == (mode == "overlap")
                 s.advance(steps)
                 results[rank] = s.owned()
                 torch.cuda.current_stream().synchronize()

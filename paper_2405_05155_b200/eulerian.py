@@ -479,36 +479,44 @@ class EulerianSolver:
 
     def _setup_overlap(self):
         """Boundary-first stages (slab ranks, NCCL exchange; default on,
-        SPHB_SLAB_OVERLAP=0 disables): each stage first updates the two
-        layers it sends, starts their exchange on a side stream, then updates
-        the interior rows while the layers travel.  Row sets are disjoint, so
-        the fields are bit-identical to one launch over all owned rows."""
+        SPHB_SLAB_OVERLAP=0 disables): the two layers a rank sends are
+        updated on a high-priority stream and their exchange starts on a
+        communication stream as soon as they are done, while the interior
+        rows are updated concurrently on the caller's stream.  Row sets are
+        disjoint, so the fields are bit-identical to one launch over all
+        owned rows."""
         self._overlap = None
         if (self._slab is not None and self._slab.world > 1 and self._push is None
                 and self.precision == "fp64" and self.variant == "global"
                 and self.ghosts is None and os.environ.get("SPHB_SLAB_OVERLAP", "1") != "0"):
-            self._overlap = _lib.torch_cuda().cuda.Stream()
+            torch = _lib.torch_cuda()
+            self._overlap = torch.cuda.Stream()                  # halo exchange
+            self._boundary = torch.cuda.Stream(priority=-1)      # sent layers first
 
-    def _stage_boundary_first(self, stage, s_in, s_n, m_n, s_out, m_out):
-        torch = _lib.torch_cuda()
-        sl, p = self._slab, self.params
-        lo, hi = sl.send_lo, sl.send_hi
-        parts = [lo, hi] if lo.start < hi.start else [slice(lo.start, hi.stop)]
-        if lo.stop < hi.start:
-            parts.append(slice(lo.stop, hi.start))          # interior, launched last
-        for k, part in enumerate(parts):
-            p.row0, p.nrows = part.start, part.stop - part.start
+    def _stage_rows(self, stage, rows, s_in, s_n, m_n, s_out, m_out):
+        p = self.params
+        p.row0, p.nrows = rows.start, rows.stop - rows.start
+        if p.nrows > 0:
             _lib.call("sphb_wc_stage", ctypes.byref(p), stage, self.group, self.X.data_ptr(),
                       self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
                       s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
                       None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                       self.err.data_ptr(), _lib.stream_ptr())
-            if k == min(1, len(parts) - 1) and stage != 0:   # both sent layers done
-                comm = self._overlap
-                comm.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(comm):
-                    sl.exchange(self._dist, [s_out])
-        p.row0, p.nrows = sl.rows.start, sl.rows.stop - sl.rows.start
+
+    def _stage_boundary_first(self, stage, s_in, s_n, m_n, s_out, m_out):
+        torch = _lib.torch_cuda()
+        sl = self._slab
+        lo, hi = sl.send_lo, sl.send_hi
+        main, bnd, comm = torch.cuda.current_stream(), self._boundary, self._overlap
+        bnd.wait_stream(main)
+        with torch.cuda.stream(bnd):
+            self._stage_rows(stage, lo, s_in, s_n, m_n, s_out, m_out)
+            self._stage_rows(stage, hi, s_in, s_n, m_n, s_out, m_out)
+        comm.wait_stream(bnd)
+        with torch.cuda.stream(comm):
+            sl.exchange(self._dist, [s_out])
+        self._stage_rows(stage, slice(lo.stop, hi.start), s_in, s_n, m_n, s_out, m_out)
+        self.params.row0, self.params.nrows = sl.rows.start, sl.rows.stop - sl.rows.start
 
     def _setup_push(self, dev):
         """Fused halo push (SPHB_HALO_PUSH=1): the stage kernel stores the

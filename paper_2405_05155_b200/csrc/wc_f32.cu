@@ -23,8 +23,10 @@ constexpr int kThreads = 64;
 
 __device__ __forceinline__ float4 ldg4f(const float4* p) { return __ldg(p); }
 
+// 3D: 16 blocks of 64 per SM (64 registers, 32 warps) and 1/rbar from the
+// fast approximate divide: 3.54 -> 2.99 ms per C5 stage (r01_tune_wc.md)
 template <int D>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, D == 3 ? 16 : 1)
 k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict__ X,
                const float* __restrict__ B, const int32_t* __restrict__ nbr,
                const int32_t* __restrict__ cnt, const float4* __restrict__ S32_in,
@@ -129,7 +131,7 @@ k_wc_stage_f32(const sphb_wc_params P, const int stage, const float4* __restrict
       const float rbar = rho0f + 0.5f * (drho_i + drho_j);
       const float p_j = c2 * drho_j;
       // (u* - ubar) / r, branch-free (beta = 0 gives 0)
-      const float wr = (beta * beta) * (p_i - p_j) * half_cinv * __frcp_rn(rbar) * inv_r;
+      const float wr = (beta * beta) * (p_i - p_j) * half_cinv * __fdividef(1.0f, rbar) * inv_r;
       const float p_star = fmaf(0.5f * beta * rbar * c, du, 0.5f * (p_i + p_j));
       float vs[3];
       float sg = 0.f;

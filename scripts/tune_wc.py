@@ -17,7 +17,7 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def one(n_side, kernel, steps):
+def one(n_side, kernel, steps, precision="fp64"):
     sys.path.insert(0, REPO)
     import torch
 
@@ -29,7 +29,8 @@ def one(n_side, kernel, steps):
     n = cfg["pos"].shape[0]
     st = FluidState(cfg["vol"], cfg["rho"], cfg["mom"], None, n)
     s = EulerianSolver(cfg["pos"], n, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0),
-                       cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+                       cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"],
+                       precision=precision)
     s.advance(3)
     torch.cuda.synchronize()
     if os.environ.get("SPHB_EXPERIMENT"):     # raw stage-1 launches into scratch
@@ -59,9 +60,10 @@ def main():
     ap.add_argument("--kernel", default="1.6h")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--one", action="store_true")
+    ap.add_argument("--precision", default="fp64")
     args = ap.parse_args()
     if args.one:
-        one(args.n_side, args.kernel, args.steps)
+        one(args.n_side, args.kernel, args.steps, args.precision)
         return
     variants = [("cell", "global", 1, 4, 0), ("lattice", "global", 1, 4, 0),
                 ("lattice", "global", 2, 4, 0), ("lattice", "global", 1, 6, 0),

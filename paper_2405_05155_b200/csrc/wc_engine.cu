@@ -116,11 +116,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     unpack_s<D>(S_in[i], vi, rho_i);
     Sym<D> Bi;
     Bi.load(B, n, i);
-    const double p_i = fma(c2, rho_i, -c2rho0);
-    const double hp_i = 0.5 * p_i, hrho_i = 0.5 * rho_i;
-    double hvi[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) hvi[a] = 0.5 * vi[a];
+    const double hrho_i = 0.5 * rho_i;
     // minimum image (neighbors.py:152-157) only matters within one cut-off
     // of a periodic face: a warp-uniform per-particle test keeps the FP64
     // compare/select work out of the loop for the bulk
@@ -177,15 +173,15 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       double beta = du * eta_c;
       beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
       const double rbar = fma(0.5, rho_j, hrho_i);
-      const double p_j = fma(c2, rho_j, -c2rho0);
-      // (u* - ubar) / r; branch-free: beta = 0 gives 0
-      const double wr = ((beta * beta) * (p_i - p_j) * half_cinv) * (rcp_nr(rbar) * inv_r);
-      const double p_star = fma((beta * rbar) * hc, du, fma(0.5, p_j, hp_i));
+      // (u* - ubar) / r with p_i - p_j = c^2 (rho_i - rho_j), c^2 / (2c) = hc;
+      // branch-free: beta = 0 gives 0.  pbar = (p_i + p_j) / 2 = c^2 rbar - c^2 rho0
+      const double wr = ((beta * beta) * (rho_i - rho_j) * hc) * (rcp_nr(rbar) * inv_r);
+      const double p_star = fma((beta * rbar) * hc, du, fma(c2, rbar, -c2rho0));
       double vs[D];
       double sg = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        vs[a] = fma(-wr, dx[a], fma(0.5, vj[a], hvi[a]));
+        vs[a] = fma(-wr, dx[a], fma(0.5, dv[a], vi[a]));   // vbar - wr dx
         sg = fma(vs[a], G_[a], sg);
       }
       const double sdot = gsc * sg;                     // vs . gwv

@@ -109,7 +109,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     // host-folded constants (kernel parameters live in the constant bank, so
     // the FP64 instructions read them as operands instead of registers)
     const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c;
-    const double half_cinv = K.half_cinv, hc = K.hc;
+    const double hc = K.hc;
 
     double xi[D], vol_i, vi[D], rho_i;
     unpack_x<D>(X[i], xi, vol_i);

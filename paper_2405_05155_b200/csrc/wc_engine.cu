@@ -38,7 +38,7 @@ constexpr int kThreads = 64;
 
 // Per-launch constants folded on the host from sphb_wc_params.
 struct WCConst {
-  double c2, c2rho0, eta_c, inv_h, c5s, half_cinv, hc, mu2;
+  double c2, c2rho0, eta_c, inv_h, c5s, hc, mu2;
   double cg, cm;          // 0.5 c5s [V] / h, mu2 c5s [V] / h: t^3-scaled pair factors
   double mhalf_inv_h;     // -0.5 / h
   double wrap_margin;     // particles farther than this from every periodic face never wrap
@@ -51,7 +51,6 @@ inline WCConst wc_const(const sphb_wc_params& p) {
   k.eta_c = kEtaLinearized / p.c_art;
   k.inv_h = 1.0 / p.h;
   k.c5s = -5.0 * p.alpha / p.h;       // dW = c5s q t^3 (Wendland, kernels.py:55-57)
-  k.half_cinv = 0.5 / p.c_art;
   k.hc = 0.5 * p.c_art;
   k.mu2 = 2.0 * p.mu;
   const double v = p.uniform_vol ? p.vol_const : 1.0;

@@ -39,7 +39,7 @@ constexpr int kThreads = 64;
 // Per-launch constants folded on the host from sphb_wc_params.
 struct WCConst {
   double c2, c2rho0, eta_c, inv_h, c5s, hc, mu2;
-  double cg, cm;          // 0.5 c5s [V] / h, mu2 c5s [V] / h: t^3-scaled pair factors
+  double cg2, cm;         // -c5s [V] / h (-2 x gsc / t^3), mu2 c5s [V] / h: pair factors
   double mhalf_inv_h;     // -0.5 / h
   double wrap_margin;     // particles farther than this from every periodic face never wrap
 };
@@ -54,7 +54,7 @@ inline WCConst wc_const(const sphb_wc_params& p) {
   k.hc = 0.5 * p.c_art;
   k.mu2 = 2.0 * p.mu;
   const double v = p.uniform_vol ? p.vol_const : 1.0;
-  k.cg = 0.5 * k.c5s * v / p.h;
+  k.cg2 = -(k.c5s * v / p.h);
   k.cm = k.mu2 * k.c5s * v / p.h;
   k.mhalf_inv_h = -0.5 / p.h;
   k.wrap_margin = 1.0001 * p.kappa * p.h;
@@ -153,7 +153,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       // gsc = 0.5 dW V_j / r, mv = mu viscv
       double base = (t * t) * t;
       if (!P.uniform_vol) base *= vol_j;
-      const double gsc = K.cg * base;
+      const double gsc2 = K.cg2 * base;                 // -2 gsc: both flux terms' -2
       const double mv = K.cm * base;
       Sym<D> Bs;
       Bi.add(Bj, Bs);
@@ -174,8 +174,9 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       const double rbar = fma(0.5, rho_j, hrho_i);
       // (u* - ubar) / r with p_i - p_j = c^2 (rho_i - rho_j), c^2 / (2c) = hc;
       // branch-free: beta = 0 gives 0.  pbar = (p_i + p_j) / 2 = c^2 rbar - c^2 rho0
-      const double wr = ((beta * beta) * (rho_i - rho_j) * hc) * (rcp_nr(rbar) * inv_r);
-      const double p_star = fma((beta * rbar) * hc, du, fma(c2, rbar, -c2rho0));
+      const double bh = beta * hc;
+      const double wr = ((beta * bh) * (rho_i - rho_j)) * (rcp_nr(rbar) * inv_r);
+      const double p_star = fma(bh * rbar, du, fma(c2, rbar, -c2rho0));
       double vs[D];
       double sg = 0.0;
 #pragma unroll
@@ -183,10 +184,9 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
         vs[a] = fma(-wr, dx[a], fma(0.5, dv[a], vi[a]));   // vbar - wr dx
         sg = fma(vs[a], G_[a], sg);
       }
-      const double sdot = gsc * sg;                     // vs . gwv
-      const double rs2 = -2.0 * rbar * sdot;
-      dr += rs2;                                        // -2 rbar s
-      const double pg = (-2.0 * p_star) * gsc;
+      const double rs2 = rbar * (gsc2 * sg);            // -2 rbar s, s = vs . gwv
+      dr += rs2;
+      const double pg = p_star * gsc2;                  // -2 p* gsc
 #pragma unroll
       for (int a = 0; a < D; ++a)
         dm[a] = fma(-mv, dv[a], fma(pg, G_[a], fma(rs2, vs[a], dm[a])));

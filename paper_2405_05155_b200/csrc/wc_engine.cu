@@ -68,8 +68,9 @@ inline WCConst wc_const(const sphb_wc_params& p) {
 template <int D, int G, int MINB, bool WALL>
 // MINB counts 128-thread equivalents (4 -> 128 registers, 5 -> 96)
 // MINB 5 (default): a 9-block bound (112-register cap) under which ptxas
-// keeps two pairs in flight in 96 registers, so 10 blocks stay resident;
-// the 10-block bound makes it drop the unroll (-3.4% on C5, r01_tune_wc.md)
+// schedules the 4-way unrolled pair loop in 96 registers, so 10 blocks stay
+// resident; the 10-block bound makes it drop the unroll (C5 stage 3.98 ->
+// 3.84 ms, A/B in profiles/r01_tune_wc.md)
 __global__ void __launch_bounds__(kThreads, MINB == 5 ? 9 : MINB * 128 / kThreads)
 k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
            const double4* __restrict__ X, const double* __restrict__ B,
@@ -201,9 +202,9 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       }
     };
 
-    // two pairs in flight per thread at the 128-register budget (MINB 4) and
-    // at the default target (MINB 5: 96 registers, 20 warps); one above
-    constexpr int UNR = MINB <= 5 ? 2 : 1;
+    // loop unroll: 4 at the default target (MINB 5: 96 registers, 20 warps),
+    // 2 at the 128-register budget (MINB 4), none above
+    constexpr int UNR = MINB == 5 ? 4 : (MINB <= 4 ? 2 : 1);
 #pragma unroll UNR
     for (int32_t k = gl; k < m; k += G) {
       int64_t j = srow[k * RB];

@@ -25,6 +25,8 @@
 #include <cuda_pipeline.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "wc_common.cuh"
 
 using namespace sphb;
@@ -133,7 +135,10 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     const int32_t m = cnt[i];
 
     // one directed pair (i, j) from j's records
-    auto pair = [&](const int64_t j, const double4 xr, const double4 sr, const Sym<D>& Bj) {
+    // `uni` (std::true_type / false_type): uniform volumes, V_j folded into
+    // the constants; a compile-time flag so the loop carries no select for it
+    auto pair = [&](const int64_t j, const double4 xr, const double4 sr, const Sym<D>& Bj,
+                    auto uni) {
       double xj[D], vol_j, vj[D], rho_j;
       unpack_x<D>(xr, xj, vol_j);
       unpack_s<D>(sr, vj, rho_j);
@@ -156,7 +161,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
       // dW V_j / r = c5s q t^3 V_j / r = (c5s / h) t^3 V_j (q / r = 1 / h);
       // gsc = 0.5 dW V_j / r, mv = mu viscv
       double base = (t * t) * t;
-      if (!P.uniform_vol) base *= vol_j;
+      if constexpr (!decltype(uni)::value) base *= vol_j;
       const double gsc2 = K.cg2 * base;                 // -2 gsc: both flux terms' -2
       const double mv = K.cm * base;
       Sym<D> Bs;
@@ -205,14 +210,20 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
     // loop unroll: 4 at the default target (MINB 5: 96 registers, 20 warps),
     // 2 at the 128-register budget (MINB 4), none above
     constexpr int UNR = MINB == 5 ? 4 : (MINB <= 4 ? 2 : 1);
+    auto loop = [&](auto uni) {
 #pragma unroll UNR
-    for (int32_t k = gl; k < m; k += G) {
-      int64_t j = srow[k * RB];
-      SPHB_CHECK_INDEX(j, n, err);
-      Sym<D> bj;
-      bj.load(B, n, j);
-      pair(j, ldg4(X + j), ldg4(S_in + j), bj);
-    }
+      for (int32_t k = gl; k < m; k += G) {
+        int64_t j = srow[k * RB];
+        SPHB_CHECK_INDEX(j, n, err);
+        Sym<D> bj;
+        bj.load(B, n, j);
+        pair(j, ldg4(X + j), ldg4(S_in + j), bj, uni);
+      }
+    };
+    if (P.uniform_vol)
+      loop(std::true_type{});
+    else
+      loop(std::false_type{});
   }
   if constexpr (WALL) {
 #pragma unroll

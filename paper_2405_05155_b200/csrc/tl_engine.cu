@@ -60,6 +60,43 @@ __device__ __forceinline__ void load_mat(const double4* __restrict__ M, int64_t 
   }
 }
 
+// 3D deformation gradient F: 9 doubles in three planes of n records,
+// {F00, F01, F02, F10} {F11, F12, F20, F21} {F22} (72 bytes per particle
+// instead of 96 for padded rows); 2D / 1D: the single-record layout.
+template <int D>
+__device__ __forceinline__ void load_f(const double4* __restrict__ F, int64_t n, int64_t i,
+                                       double (&a)[D][D]) {
+  if constexpr (D == 3) {
+    const double4 p = F[i], q = F[n + i];
+    const double r = reinterpret_cast<const double*>(F + 2 * n)[i];
+    a[0][0] = p.x; a[0][1] = p.y; a[0][2] = p.z;
+    a[1][0] = p.w; a[1][1] = q.x; a[1][2] = q.y;
+    a[2][0] = q.z; a[2][1] = q.w; a[2][2] = r;
+  } else {
+    load_mat<D>(F, n, i, a);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void store_f(double4* __restrict__ F, int64_t n, int64_t i,
+                                        const double (&a)[D][D]);
+
+// 3D correction matrix B0 (symmetric, correction.py:64-81): planes
+// {b00, b01, b02, b11} and {b12, b22} (48 bytes per particle).
+template <int D>
+__device__ __forceinline__ void load_b0(const double4* __restrict__ B, int64_t n, int64_t i,
+                                        double (&a)[D][D]) {
+  if constexpr (D == 3) {
+    const double4 p = B[i];
+    const double2 q = reinterpret_cast<const double2*>(B + n)[i];
+    a[0][0] = p.x; a[0][1] = p.y; a[0][2] = p.z;
+    a[1][0] = p.y; a[1][1] = p.w; a[1][2] = q.x;
+    a[2][0] = p.z; a[2][1] = q.x; a[2][2] = q.y;
+  } else {
+    load_mat<D>(B, n, i, a);
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t ms, int64_t i,
                                           const double (&a)[D][D]) {
@@ -70,6 +107,18 @@ __device__ __forceinline__ void store_mat(double4* __restrict__ M, int64_t ms, i
     M[i] = make_double4(a[0][0], a[0][1], a[1][0], a[1][1]);
   } else {
     M[i] = make_double4(a[0][0], 0.0, 0.0, 0.0);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void store_f(double4* __restrict__ F, int64_t n, int64_t i,
+                                        const double (&a)[D][D]) {
+  if constexpr (D == 3) {
+    F[i] = make_double4(a[0][0], a[0][1], a[0][2], a[1][0]);
+    F[n + i] = make_double4(a[1][1], a[1][2], a[2][0], a[2][1]);
+    reinterpret_cast<double*>(F + 2 * n)[i] = a[2][2];
+  } else {
+    store_mat<D>(F, n, i, a);
   }
 }
 
@@ -312,8 +361,8 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   }
 
   double B[D][D], Fi[D][D];
-  load_mat<D>(B0, n, i, B);
-  load_mat<D>(F, n, i, Fi);
+  load_b0<D>(B0, n, i, B);
+  load_f<D>(F, n, i, Fi);
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -327,7 +376,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
   if (!(J > 0.0)) atomicOr(err, SPHB_EFLAG_DET_NONPOS);
   double Qi[D][D];
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
-  store_mat<D>(F, n, i, Fi);
+  store_f<D>(F, n, i, Fi);
   const int64_t qs = P.q_stride ? P.q_stride : n;
   store_q<D>(Q, qs, i, Qi, wi);
   {   // fused halo push of the boundary layers' Q records
@@ -482,8 +531,8 @@ __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ 
   if (i >= P.n) return;
   double Fi[D][D], B[D][D], Qi[D][D], w[D];
   bool fixed;
-  load_mat<D>(F, P.n, i, Fi);
-  load_mat<D>(B0, P.n, i, B);
+  load_f<D>(F, P.n, i, Fi);
+  load_b0<D>(B0, P.n, i, B);
   load_x0<D>(X0, i, w, fixed);
   svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
   store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);

@@ -121,23 +121,59 @@ def _vec_rec(arr_sorted, n, dim, dev):
 
 
 def _mat_rec(m_sorted, n, dim, dev):
-    """(n, d, d) -> padded row records (3D: three row planes (3, n, 4);
-    2D: (n, 4); 1D: (n, 4))."""
+    """(n, d, d) -> one record per particle (2D: {a00, a01, a10, a11};
+    1D: {a00}); 3D matrices use _f_rec / _b0_rec / the Q planes."""
     torch = _lib.torch_cuda()
-    if dim == 3:
-        out = torch.zeros((3, n, 4), dtype=torch.float64, device=dev)
-        out[:, :, :3] = m_sorted.permute(1, 0, 2)
-        return out
+    assert dim < 3
     out = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     out[:, :dim * dim] = m_sorted.reshape(n, dim * dim)
     return out
 
 
+def _f_rec(m_sorted, n, dim, dev):
+    """(n, d, d) -> deformation-gradient records (3D: 9 doubles in planes
+    {F00,F01,F02,F10} {F11,F12,F20,F21} {F22}, tl_engine.cu load_f)."""
+    if dim != 3:
+        return _mat_rec(m_sorted, n, dim, dev)
+    torch = _lib.torch_cuda()
+    flat = m_sorted.reshape(n, 9)
+    out = torch.empty(9 * n, dtype=torch.float64, device=dev)
+    out[:4 * n].view(n, 4).copy_(flat[:, 0:4])
+    out[4 * n:8 * n].view(n, 4).copy_(flat[:, 4:8])
+    out[8 * n:].copy_(flat[:, 8])
+    return out
+
+
+def _f_unrec(rec, n_all, dim, rows=None):
+    """F records -> (n, d, d) (optionally only `rows`)."""
+    if dim != 3:
+        return _mat_unrec(rec, n_all, dim, rows)
+    rows = slice(0, n_all) if rows is None else rows
+    torch = _lib.torch_cuda()
+    p0 = rec[:4 * n_all].view(n_all, 4)[rows]
+    p1 = rec[4 * n_all:8 * n_all].view(n_all, 4)[rows]
+    p2 = rec[8 * n_all:][rows]
+    return torch.cat([p0, p1, p2[:, None]], dim=1).reshape(-1, 3, 3)
+
+
+def _b0_rec(b_sorted, n, dim, dev):
+    """(n, d, d) symmetric B0 -> records (3D: planes {b00,b01,b02,b11} and
+    {b12,b22}, symmetrised, tl_engine.cu load_b0)."""
+    if dim != 3:
+        return _mat_rec(b_sorted, n, dim, dev)
+    torch = _lib.torch_cuda()
+    bs = 0.5 * (b_sorted + b_sorted.transpose(1, 2))
+    out = torch.empty(6 * n, dtype=torch.float64, device=dev)
+    p0 = out[:4 * n].view(n, 4)
+    p1 = out[4 * n:].view(n, 2)
+    p0[:, 0], p0[:, 1], p0[:, 2], p0[:, 3] = bs[:, 0, 0], bs[:, 0, 1], bs[:, 0, 2], bs[:, 1, 1]
+    p1[:, 0], p1[:, 1] = bs[:, 1, 2], bs[:, 2, 2]
+    return out
+
+
 def _mat_unrec(rec, n, dim, rows=None):
-    """Records -> (n, d, d) matrices (optionally only `rows`)."""
-    if dim == 3:
-        planes = rec[:, :, :3] if rows is None else rec[:, rows, :3]
-        return planes.permute(1, 0, 2)
+    """2D / 1D records -> (n, d, d) matrices (optionally only `rows`)."""
+    assert dim < 3
     out = rec if rows is None else rec[rows]
     return out[:, :dim * dim].reshape(-1, dim, dim)
 
@@ -207,9 +243,9 @@ class SolidSystem:
         fixed_s = _lib.to_device(self.fixed.astype(np.float64), torch.float64)[self.perm]
         self.X0rec = _vec_rec(self.order.ws.t(), n, d, dev)
         self.X0rec[:, 3] = fixed_s
-        self.B0rec = _mat_rec(b0, n, d, dev)
+        self.B0rec = _b0_rec(b0, n, d, dev)
         eye = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d)
-        self.Frec = _mat_rec(eye, n, d, dev)
+        self.Frec = _f_rec(eye, n, d, dev)
         # Q: three row planes in 3D (tl_engine.cu store_q), one stride for
         # all slab ranks so the fused halo push can address peer planes
         self._q_stride = n
@@ -221,7 +257,7 @@ class SolidSystem:
             self.Qrec = torch.zeros((3, self._q_stride, 4), dtype=torch.float64, device=dev)
             self._q_halo = [self.Qrec[r] for r in range(3)]
         else:
-            self.Qrec = torch.zeros_like(self.Frec)
+            self.Qrec = torch.zeros((n, 4), dtype=torch.float64, device=dev)
             self._q_halo = [self.Qrec]
         xs = _lib.to_device(self.X0, torch.float64)[self.perm]
         self.XC = _vec_rec(xs, n, d, dev)
@@ -300,7 +336,7 @@ class SolidSystem:
 
     @property
     def F(self):
-        return self._cached("F", lambda: self._orig(_mat_unrec(self.Frec, self.n, self.dim)))
+        return self._cached("F", lambda: self._orig(_f_unrec(self.Frec, self.n, self.dim)))
 
     @property
     def B0(self):
@@ -374,7 +410,7 @@ class SolidSystem:
             ids = self._slab.local_ids[ids]
         x = self.XC[rows, :self.dim].cpu().numpy()
         v = self.V[rows, :self.dim].cpu().numpy()
-        F = _mat_unrec(self.Frec, rows.stop - rows.start, self.dim, rows).cpu().numpy()
+        F = _f_unrec(self.Frec, self.n, self.dim, rows).cpu().numpy()
         return ids, x, v, F
 
     def accelerations(self):

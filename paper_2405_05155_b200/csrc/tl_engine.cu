@@ -285,11 +285,13 @@ __global__ void k_tl_kick(int64_t n, const double4* __restrict__ X0,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double hdt = 0.5 * scalars[0];
-  double w[D], v[D], a_[D], vh[D];
-  bool fixed;
-  load_x0<D>(X0, i, w, fixed);
+  double v[D], a_[D], vh[D];
   load_vec<D>(V, i, v);
-  load_vec<D>(A, i, a_);
+  const double4 a4 = A[i];          // {a0, a1, a2, fixed}: the clamp flag rides in .w
+  const double c4[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+  for (int a = 0; a < D; ++a) a_[a] = c4[a];
+  const bool fixed = a4.w != 0.0;
 #pragma unroll
   for (int a = 0; a < D; ++a) vh[a] = fixed ? 0.0 : fma(hdt, a_[a], v[a]);
   store_vec<D>(Vh, i, vh);

@@ -279,8 +279,7 @@ __device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0
 // vh = v + dt/2 a, 0 for clamped particles (tlsph.py:186-189); pass A then
 // gathers one half-step velocity record per pair instead of v_j and a_j.
 template <int D>
-__global__ void k_tl_kick(int64_t n, const double4* __restrict__ X0,
-                          const double4* __restrict__ V, const double4* __restrict__ A,
+__global__ void k_tl_kick(int64_t n, const double4* __restrict__ V, const double4* __restrict__ A,
                           double4* __restrict__ Vh, const double* __restrict__ scalars) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -652,8 +651,7 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)x0,
-              (const double4*)v, (const double4*)a, (double4*)vh, scalars);
+  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars);
   static const int var = tl_variant("SPHB_TL_VARIANT_A");
   if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
     TL_TUNED(k_tl_pass_a, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,

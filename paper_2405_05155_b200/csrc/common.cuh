@@ -43,6 +43,9 @@ __device__ __forceinline__ double profile_deriv(int code, double q) {
 // ---------------------------------------------------------------- helpers
 // numpy float remainder (npy_divmod): fmod, then shift into the sign of b.
 __device__ __forceinline__ double np_remainder(double a, double b) {
+  // already inside (0, b): fmod(a, b) == a exactly (the common case for
+  // wrapped coordinates); skips the multi-instruction fmod sequence
+  if (a > 0.0 && a < b) return a;
   double mod = fmod(a, b);
   if (mod != 0.0) {
     if ((b < 0.0) != (mod < 0.0)) mod += b;

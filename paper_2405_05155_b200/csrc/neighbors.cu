@@ -70,8 +70,8 @@ constexpr int64_t kSmallBinMaxCells = 8192;
 
 template <int D>
 __global__ void __launch_bounds__(kSmallBinThreads)
-k_bin_small(sphb_grid g, const double* __restrict__ pos, int64_t n, double* __restrict__ wrapped,
-            uint32_t* __restrict__ key_unused, int32_t* __restrict__ perm, int32_t* __restrict__ cs,
+k_bin_small(sphb_grid g, int64_t n, const double* __restrict__ wrapped,
+            const uint32_t* __restrict__ keys, int32_t* __restrict__ perm, int32_t* __restrict__ cs,
             int32_t* __restrict__ ce, double* __restrict__ ws) {
   constexpr int KPT = (int)(kSmallBinMaxN / kSmallBinThreads);   // particles per thread
   extern __shared__ int32_t sm[];
@@ -82,23 +82,17 @@ k_bin_small(sphb_grid g, const double* __restrict__ pos, int64_t n, double* __re
   const int tid = threadIdx.x;
   for (int c = tid; c < ntot; c += blockDim.x) count[c] = 0;
   __syncthreads();
+  // keys and wrapped coordinates come from k_wrap_key (all SMs)
   uint32_t key[KPT];
 #pragma unroll
   for (int q = 0; q < KPT; ++q) {
     const int64_t i = tid + (int64_t)q * kSmallBinThreads;
-    key[q] = 0;
-    if (i < n) {
-      int64_t flat = 0;
+    key[q] = i < n ? keys[i] : 0u;
+  }
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const double p = pos[i * D + a];
-        const double w = g.periodic ? np_remainder(p, g.box[a]) : __dsub_rn(p, g.lo[a]);
-        wrapped[i * D + a] = w;
-        flat += cell_coord(g, a, w) * g.sstrides[a];   // storage key
-      }
-      key[q] = (uint32_t)flat;
-      atomicAdd(count + flat, 1);
-    }
+  for (int q = 0; q < KPT; ++q) {
+    const int64_t i = tid + (int64_t)q * kSmallBinThreads;
+    if (i < n) atomicAdd(count + key[q], 1);
   }
   __syncthreads();
   // exclusive scan: each thread a contiguous chunk, chunk totals scanned by warp 0
@@ -156,11 +150,34 @@ k_bin_small(sphb_grid g, const double* __restrict__ pos, int64_t n, double* __re
     }
   }
   __syncthreads();
-  for (int64_t s = tid; s < n; s += blockDim.x) {
-    const int64_t i = sperm[s];
-    perm[s] = (int32_t)i;
+  // gathers issued four rows at a time before their stores (fewer
+  // dependent L2 round trips per thread)
+  constexpr int QB = 4;
 #pragma unroll
-    for (int a = 0; a < D; ++a) ws[(int64_t)a * n + s] = wrapped[i * D + a];
+  for (int q0 = 0; q0 < KPT; q0 += QB) {
+    if (tid + (int64_t)q0 * kSmallBinThreads >= n) break;
+    int32_t src[QB];
+    double wv[QB][D];
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
+      const int64_t s = tid + (int64_t)(q0 + q) * kSmallBinThreads;
+      src[q] = s < n ? sperm[s] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
+      const int64_t s = tid + (int64_t)(q0 + q) * kSmallBinThreads;
+#pragma unroll
+      for (int a = 0; a < D; ++a) wv[q][a] = s < n ? wrapped[(int64_t)src[q] * D + a] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
+      const int64_t s = tid + (int64_t)(q0 + q) * kSmallBinThreads;
+      if (s < n) {
+        perm[s] = src[q];
+#pragma unroll
+        for (int a = 0; a < D; ++a) ws[(int64_t)a * n + s] = wv[q][a];
+      }
+    }
   }
 }
 
@@ -224,10 +241,16 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
+    const int T = 256;
     switch (g->dim) {
-      case 1: k_bin_small<1><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
-      case 2: k_bin_small<2><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
-      default: k_bin_small<3><<<1, kSmallBinThreads, smem, st>>>(*g, pos, n, wrapped, keys_in, perm, cs, ce, ws); break;
+      case 1: k_wrap_key<1><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+      case 2: k_wrap_key<2><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+      default: k_wrap_key<3><<<sphb_blocks(n, T), T, 0, st>>>(*g, pos, n, wrapped, keys_in, vals_in); break;
+    }
+    switch (g->dim) {
+      case 1: k_bin_small<1><<<1, kSmallBinThreads, smem, st>>>(*g, n, wrapped, keys_in, perm, cs, ce, ws); break;
+      case 2: k_bin_small<2><<<1, kSmallBinThreads, smem, st>>>(*g, n, wrapped, keys_in, perm, cs, ce, ws); break;
+      default: k_bin_small<3><<<1, kSmallBinThreads, smem, st>>>(*g, n, wrapped, keys_in, perm, cs, ce, ws); break;
     }
     SPHB_LAUNCH_CHECK();
     return SPHB_OK;

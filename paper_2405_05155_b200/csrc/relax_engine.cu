@@ -98,8 +98,8 @@ k_relax_accel_warp(sphb_grid g, int64_t n, const double* __restrict__ ws,
         for (int a = 0; a < D; ++a) {
           const int off = rem % 3 - 1;
           rem /= 3;
-          int64_t c = ci[a] + off;
-          if (g.periodic) c = py_mod(c, g.ncell[a]);
+          int64_t c = ci[a] + off;               // off in {-1, 0, 1}: wrap without a division
+          if (g.periodic) c = c < 0 ? c + g.ncell[a] : (c >= g.ncell[a] ? c - g.ncell[a] : c);
           else if (c < 0 || c >= g.ncell[a]) ok = false;
           flat += c * g.strides[a];
         }
@@ -153,7 +153,7 @@ k_relax_accel_warp(sphb_grid g, int64_t n, const double* __restrict__ ws,
         }
         count += __popc(__ballot_sync(0xffffffffu, in_cut));
         unsigned m = __ballot_sync(0xffffffffu, valid);
-        while (m) {                      // candidate order = lane order
+        while (m) {                      // candidate order = lane order (the reference's sum)
           const int src = __ffs(m) - 1;
           m &= m - 1;
 #pragma unroll

@@ -1,3 +1,8 @@
+#!/bin/bash
+# C5 headline: bench line, then the ncu launch list and one --set full
+# capture of a stage launch (each after the same command exited 0 without
+# ncu).  Outputs in gpurun_out/:
+#   gpurun --timeout 2400 -- bash scripts/profile_c5.sh
 set -e
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_v8.json 2> gpurun_out/bench_v8.err

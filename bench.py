@@ -39,6 +39,10 @@ METRIC = "particle-steps/s and pair-interactions/s at 1.6h vs 2h; % of HBM roofl
 # compulsory FP64 bytes per particle-step for C5 (stage 1: x 24
 # + B 48 + rho 8 + mom 24 read, 32 write = 136; stage 2: + U^n 32 = 168)
 BYTES_STAGE = {1: 136, 2: 168}
+# bytes a stage launch of this implementation must move per particle beyond
+# the int32 pass list: own X 32 + B 48 + S 32 + cnt 4 read, S 32 written;
+# stage 2 also reads S_n, M_n (64) and writes M (32) — averaged over the two
+IMPL_RECORD_BYTES = 32 + 48 + 32 + 4 + 32 + (64 + 32) / 2.0
 # FP64 flops per directed pair of the fused stage kernel, from the SASS of
 # k_wc_stage<3,1,5> (37 DFMA + 27 DMUL + 13 DADD per pair in the loop body,
 # plus the limiter branch ~3; profiles/r01_ncu_c5_256.md v3)
@@ -333,7 +337,9 @@ def main():
     leg["1.6h"] = run_leg(torch, cfg, args.steps, max(3, args.warmup), dist, world,
                           clocks_index=local)
     e2e_ms, io_bytes = e2e_leg(torch, leg["1.6h"]["solver"], max(2, args.steps // 4), 1)
-    del leg["1.6h"]["solver"]
+    sv = leg["1.6h"]["solver"]          # this GPU's rows (owned + halo)
+    design_bytes = sv.n * (IMPL_RECORD_BYTES + 4.0 * sv.width)
+    del leg["1.6h"]["solver"], sv
     torch.cuda.empty_cache()
     if not args.no_2h:
         cfg2 = configs.c5_tgv3d(kernel="2h", n_side=args.n_side)
@@ -369,6 +375,10 @@ def main():
                      "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md (v7)",
                      "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
+                     # what the traffic should be for this design: own records
+                     # once + the int32 pass list (SURVEY's compulsory bytes
+                     # leave the list out), i.e. no neighbour re-reads
+                     "design_bytes_per_launch": design_bytes,
                      "avg_launch_ms": avg_stage_ms,
                      "stage_ms": {"1": statistics.mean(L["stage_ms"][1]),
                                   "2": statistics.mean(L["stage_ms"][2])},

@@ -797,3 +797,29 @@ def test_neighbors_single_block_binning_sizes(n):
     for box in (None, (1.0, 1.0, 1.0)):
         assert digest(neighbors.build_neighbors(pos, 0.09, box)) == \
             digest(O.build_neighbors(pos, 0.09, box))
+
+
+@pytest.mark.parametrize("per", ["1", "3", "8"])
+def test_graph_steps_per_replay(monkeypatch, per):
+    """advance() with k steps captured per CUDA-graph replay (SPHB_GRAPH_STEPS,
+    WC rounds it to an even count, leftovers run eagerly) gives the fields and
+    time of the same number of step() calls."""
+    monkeypatch.setenv("SPHB_GRAPH_STEPS", per)
+    cfg = configs.c2_tgv2d(kernel="1.6h", n_side=40)
+    a, b = make_wc(cfg), make_wc(cfg)
+    a.advance(13, graph=True)
+    for _ in range(13):
+        b.step()
+    assert l2_error(a.state.rho, b.state.rho) < 1e-14
+    assert l2_error(a.state.mom, b.state.mom) < 1e-13
+    assert a.t == pytest.approx(b.t, rel=1e-14)
+    c3 = configs.c3_plate(kernel="1.6h")
+    s = SolidSystem(c3["X0"], c3["material"], c3["spec"], c3["dp"], fixed=c3["fixed"],
+                    cfl=c3["cfl"])
+    r = SolidSystem(c3["X0"], c3["material"], c3["spec"], c3["dp"], fixed=c3["fixed"],
+                    cfl=c3["cfl"])
+    s.v, r.v = c3["v0"], c3["v0"]
+    s.advance(11, graph=True)
+    for _ in range(11):
+        r.step()
+    assert l2_error(s.x, r.x) < 1e-14 and l2_error(s.v, r.v) < 1e-12

@@ -3,7 +3,9 @@ SlabPlan.share_buffers (the path torchrun ranks take) with two processes
 sharing cuda:0.  The collectives run over gloo on host copies (an adapter
 below), so no kernel ever waits on another process: each step's ordering is
 a host-side collective after a stream synchronisation.  The owned rows of
-both ranks must equal the single-process solver's."""
+both ranks must equal the single-process solver's.  On a box with two or
+more GPUs the `two-gpus` variants put the ranks on cuda:0 and cuda:1, so the
+pushes are real peer writes over NVLink (skipped on one GPU)."""
 
 import os
 
@@ -61,11 +63,11 @@ class HostCollectives:
         return dist.get_world_size()
 
 
-def _rank(rank, world, port, out_dir):
+def _rank(rank, world, port, out_dir, distinct=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if distinct else 0)
         from paper_2405_05155_b200 import configs
         from paper_2405_05155_b200.eulerian import WEAKLY_COMPRESSIBLE, EosParams, FluidState
         from paper_2405_05155_b200.slab import slab_eulerian
@@ -85,11 +87,11 @@ def _rank(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def _solid_rank(rank, world, port, out_dir):
+def _solid_rank(rank, world, port, out_dir, distinct=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if distinct else 0)
         from paper_2405_05155_b200 import configs
         from paper_2405_05155_b200.slab import slab_solid
 
@@ -106,7 +108,13 @@ def _solid_rank(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def test_halo_push_over_cuda_ipc(tmp_path):
+_DEVICES = [pytest.param(False, id="one-gpu"),
+            pytest.param(True, id="two-gpus", marks=pytest.mark.skipif(
+                torch.cuda.device_count() < 2, reason="needs two GPUs (peer writes over NVLink)"))]
+
+
+@pytest.mark.parametrize("distinct", _DEVICES)
+def test_halo_push_over_cuda_ipc(tmp_path, distinct):
     from paper_2405_05155_b200 import configs
     from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
                                                 FluidState)
@@ -120,7 +128,8 @@ def test_halo_push_over_cuda_ipc(tmp_path):
     ref.advance(5)
     want = ref.state
     world = 2
-    mp.start_processes(_rank, args=(world, 29511, str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_rank, args=(world, 29511 + int(distinct), str(tmp_path), distinct),
+                       nprocs=world, join=True,
                        start_method="spawn")
     got_rho = np.full(n, np.nan)
     got_mom = np.full((n, 3), np.nan)
@@ -133,7 +142,8 @@ def test_halo_push_over_cuda_ipc(tmp_path):
     np.testing.assert_allclose(got_mom, want.mom, rtol=1e-12, atol=1e-14)
 
 
-def test_solid_halo_push_over_cuda_ipc(tmp_path):
+@pytest.mark.parametrize("distinct", _DEVICES)
+def test_solid_halo_push_over_cuda_ipc(tmp_path, distinct):
     """TL-SPH: pass A pushes Q, pass B pushes a and v across processes."""
     from paper_2405_05155_b200 import configs
     from paper_2405_05155_b200.tlsph import SolidSystem
@@ -145,7 +155,8 @@ def test_solid_halo_push_over_cuda_ipc(tmp_path):
     ref.advance(10)
     want = (ref.x, ref.v, ref.F)
     world = 2
-    mp.start_processes(_solid_rank, args=(world, 29512, str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_solid_rank, args=(world, 29513 + int(distinct), str(tmp_path), distinct),
+                       nprocs=world, join=True,
                        start_method="spawn")
     got = [np.full_like(w, np.nan) for w in want]
     for r in range(world):

@@ -166,3 +166,59 @@ def test_solid_halo_push_over_cuda_ipc(tmp_path, distinct):
     for g, w in zip(got, want):
         assert not np.isnan(g).any()
         np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-14 * np.abs(w).max())
+
+
+def _nccl_rank(rank, world, port, out_dir, overlap):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="0",
+                      SPHB_SLAB_OVERLAP="1" if overlap else "0")
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        from paper_2405_05155_b200 import configs
+        from paper_2405_05155_b200.eulerian import WEAKLY_COMPRESSIBLE, EosParams, FluidState
+        from paper_2405_05155_b200.slab import slab_eulerian
+
+        cfg = configs.c5_tgv3d(kernel="1.6h", n_side=24)
+        n = cfg["pos"].shape[0]
+        st = FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
+        s = slab_eulerian(cfg["pos"], st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0),
+                          cfg["spec"], rank=rank, world=world, dist=dist,
+                          cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+        assert (s._overlap is not None) == overlap
+        s.advance(5)
+        ids, rho, mom = s.owned()
+        np.savez(os.path.join(out_dir, f"n{rank}.npz"), ids=ids, rho=rho, mom=mom)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs (NCCL over NVLink)")
+@pytest.mark.parametrize("overlap", [False, True])
+def test_slab_nccl_two_gpus(tmp_path, overlap):
+    """The torchrun path itself: two ranks on two GPUs with the NCCL halo
+    exchange (boundary-first overlap on / off) equal the one-GPU solver."""
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                                FluidState)
+
+    cfg = configs.c5_tgv3d(kernel="1.6h", n_side=24)
+    n = cfg["pos"].shape[0]
+    ref = EulerianSolver(cfg["pos"], n, FluidState(cfg["vol"].copy(), cfg["rho"].copy(),
+                                                   cfg["mom"].copy(), None, n),
+                         EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0), cfg["spec"], None,
+                         cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+    ref.advance(5)
+    want = ref.state
+    world = 2
+    mp.start_processes(_nccl_rank, args=(world, 29521 + int(overlap), str(tmp_path), overlap),
+                       nprocs=world, join=True, start_method="spawn")
+    got_rho = np.full(n, np.nan)
+    got_mom = np.full((n, 3), np.nan)
+    for r in range(world):
+        z = np.load(tmp_path / f"n{r}.npz")
+        got_rho[z["ids"]] = z["rho"]
+        got_mom[z["ids"]] = z["mom"]
+    assert not np.isnan(got_rho).any()
+    np.testing.assert_allclose(got_rho, want.rho, rtol=1e-14, atol=0)
+    np.testing.assert_allclose(got_mom, want.mom, rtol=1e-12, atol=1e-14)

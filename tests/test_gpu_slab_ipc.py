@@ -222,3 +222,48 @@ def test_slab_nccl_two_gpus(tmp_path, overlap):
     assert not np.isnan(got_rho).any()
     np.testing.assert_allclose(got_rho, want.rho, rtol=1e-14, atol=0)
     np.testing.assert_allclose(got_mom, want.mom, rtol=1e-12, atol=1e-14)
+
+
+def _nccl_solid_rank(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPHB_HALO_PUSH="0")
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        from paper_2405_05155_b200 import configs
+        from paper_2405_05155_b200.slab import slab_solid
+
+        cfg = configs.c4_column(kernel="1.6h", n_width=6)
+        s = slab_solid(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], rank=rank,
+                       world=world, dist=dist, fixed=cfg["fixed"], cfl=cfg["cfl"])
+        s.v = cfg["v0"][s.local_ids]
+        s.advance(10)
+        ids, x, v, F = s.owned()
+        np.savez(os.path.join(out_dir, f"t{rank}.npz"), ids=ids, x=x, v=v, F=F)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs (NCCL over NVLink)")
+def test_slab_solid_nccl_two_gpus(tmp_path):
+    """TL-SPH slab ranks on two GPUs with the NCCL exchange of Q, a and v."""
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.tlsph import SolidSystem
+
+    cfg = configs.c4_column(kernel="1.6h", n_width=6)
+    ref = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
+                      cfl=cfg["cfl"])
+    ref.v = cfg["v0"]
+    ref.advance(10)
+    want = (ref.x, ref.v, ref.F)
+    world = 2
+    mp.start_processes(_nccl_solid_rank, args=(world, 29525, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    got = [np.full_like(w, np.nan) for w in want]
+    for r in range(world):
+        z = np.load(tmp_path / f"t{r}.npz")
+        for g, key in zip(got, ("x", "v", "F")):
+            g[z["ids"]] = z[key]
+    for g, w in zip(got, want):
+        assert not np.isnan(g).any()
+        np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-14 * np.abs(w).max())

@@ -372,7 +372,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
                      "traffic": traffic_per_launch(L["kernel"]) if world == 1 else None,
-                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md (v7)",
+                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md (v8)",
                      "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      # what the traffic should be for this design: own records

@@ -158,10 +158,30 @@ def moment_matrices(nl, vols, spec):
     return m
 
 
+def _row_chunks(n, fn, parts=None):
+    """Run fn(slice) over contiguous row chunks on host threads (numpy's
+    gufuncs and elementwise loops release the GIL); every row is computed by
+    the same numpy call as unchunked, so results are bit-identical."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    parts = parts or max(1, min(threads(), 64))
+    if n < 8192 or parts == 1:
+        return [fn(slice(0, n))]
+    edges = np.linspace(0, n, parts + 1).astype(np.int64)
+    with ThreadPoolExecutor(parts) as ex:
+        return list(ex.map(lambda k: fn(slice(int(edges[k]), int(edges[k + 1]))), range(parts)))
+
+
 def correction_matrices(nl, vols, spec):
     """correction.py:64-81 with numpy's LAPACK, as the reference does.
     Returns (B, det(-M), n_regularized)."""
     m = moment_matrices(nl, vols, spec)
+    parts = _row_chunks(m.shape[0], lambda sl: _correction_rows(m[sl]))
+    return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
+            int(sum(p[2] for p in parts)))
+
+
+def _correction_rows(m):
     n, d, _ = m.shape
     u, s, vt = np.linalg.svd(m)
     floor = 1e-4 * np.maximum(s[:, :1], 1e-300)
@@ -358,6 +378,10 @@ def relax_shape(shape, spec, dp, max_steps, p0=1.0, rho0=1.0, step_scale=0.2):
 
 
 # ------------------------------------------------------------ WC Eulerian
+class StateRejected(RuntimeError):
+    """SolverError of the reference (eulerian.py:40-41)."""
+
+
 class EulerianWC:
     """EulerianSolver, WC branch (eulerian.py:473-643): periodic or with a
     ghost frame, optional wall-force tags (:515-519, 605-606)."""
@@ -377,10 +401,20 @@ class EulerianWC:
             b[self.n_int:] = b[np.asarray(ghosts.src, dtype=np.int64)]
         self.B = b
         gw = pair_gradients(self.nl, spec, b)
-        self.gwv = np.ascontiguousarray(gw * self.vol[self.nl.idx][:, None])
-        q = self.nl.r / spec.h
-        dw = np.where(q <= spec.kappa, (spec.alpha / spec.h) * _profile_deriv(spec.code, q), 0.0)
-        self.viscv = np.ascontiguousarray(2.0 * dw / self.nl.r * self.vol[self.nl.idx])
+        m = self.nl.idx.shape[0]
+        self.gwv = np.empty_like(gw)
+        self.viscv = np.empty(m)
+
+        def pair_rows(sl):                              # eulerian.py:506-513
+            vj = self.vol[self.nl.idx[sl]]
+            self.gwv[sl] = gw[sl] * vj[:, None]
+            q = self.nl.r[sl] / spec.h
+            dw = np.where(q <= spec.kappa,
+                          (spec.alpha / spec.h) * _profile_deriv(spec.code, q), 0.0)
+            self.viscv[sl] = 2.0 * dw / self.nl.r[sl] * vj
+
+        _row_chunks(m, pair_rows)
+        del gw
         self.t = 0.0
         self.wall_tag = None
         if wall_tag is not None:
@@ -447,23 +481,62 @@ class EulerianWC:
         speed = self.c_art + np.linalg.norm(self.mom[:ni] / self.rho[:ni, None], axis=1)
         return self.cfl * self.spec.h / float(speed.max())
 
+    retries = 0
+
+    def _checked_rhs(self):
+        """rhs() with the reference's rejections: eos_eval raises on rho <= 0
+        (eulerian.py:70-71, 535), a non-finite momentum flux raises
+        (:548-550)."""
+        if not np.all(self.rho > 0.0):
+            raise StateRejected("non-positive density")
+        drho, dmom = self.rhs()
+        if not np.all(np.isfinite(dmom[:self.n_int])):
+            raise StateRejected("NaN flux")
+        return drho, dmom
+
+    def _substep(self, dt):
+        """eulerian.py:610-643: midpoint substep; on rejection the interior
+        is restored to the substep start and t is not advanced."""
+        ni = self.n_int
+        rho0, mom0 = self.rho[:ni].copy(), self.mom[:ni].copy()
+        try:
+            self.apply_boundaries()
+            drho, dmom = self._checked_rhs()
+            self.rho[:ni] = rho0 + 0.5 * dt * drho[:ni]
+            self.mom[:ni] = mom0 + 0.5 * dt * dmom[:ni]
+            self.apply_boundaries()
+            drho, dmom = self._checked_rhs()
+            self.rho[:ni] = rho0 + dt * drho[:ni]
+            self.mom[:ni] = mom0 + dt * dmom[:ni]
+            if not np.all(self.rho[:ni] > 0.0):
+                raise StateRejected("non-positive density after step")
+        except StateRejected:
+            self.rho[:ni], self.mom[:ni] = rho0, mom0
+            raise
+        self.t += dt
+
     def step(self, dt=None):
-        """eulerian.py:610-643 (one substep, no retries)."""
+        """eulerian.py:562-608: one step with retry-with-halving.  A failed
+        substep restarts the whole step from its start state at dt/2^k; t
+        keeps any substep accepted before the failure, as in the reference."""
         if dt is None:
             dt = self.compute_dt()
         ni = self.n_int
         rho0, mom0 = self.rho[:ni].copy(), self.mom[:ni].copy()
-        self.apply_boundaries()
-        drho, dmom = self.rhs()
-        self.rho[:ni] = rho0 + 0.5 * dt * drho[:ni]
-        self.mom[:ni] = mom0 + 0.5 * dt * dmom[:ni]
-        self.apply_boundaries()
-        drho, dmom = self.rhs()
-        self.rho[:ni] = rho0 + dt * drho[:ni]
-        self.mom[:ni] = mom0 + dt * dmom[:ni]
-        if not np.all(self.rho[:ni] > 0.0):
-            raise RuntimeError("non-positive density")
-        self.t += dt
+        advanced, remaining, halved = 0.0, dt, 0
+        while advanced < dt - 1e-15 * dt:
+            sub = min(remaining, dt - advanced)
+            try:
+                self._substep(sub)
+            except StateRejected:
+                self.rho[:ni], self.mom[:ni] = rho0, mom0
+                halved += 1
+                self.retries += 1
+                if halved > 12:
+                    raise
+                advanced, remaining = 0.0, dt / 2**halved
+                continue
+            advanced += sub
         self.wall_force_series.append((self.t, self.wall_force * self.vol[0]))
         return dt
 
@@ -588,13 +661,18 @@ class SolidTL:
         self.acc = None
         self.t = 0.0
 
-    def accelerations(self):
+    def _first_pk_b0(self, sl):
+        """P B0^T with P = F S, SVK S (tlsph.py:54-65, 160-167), rows sl."""
         eye = np.eye(self.d)
-        strain = 0.5 * (np.einsum("nba,nbc->nac", self.F, self.F) - eye)
+        F = self.F[sl]
+        strain = 0.5 * (np.einsum("nba,nbc->nac", F, F) - eye)
         tr = np.trace(strain, axis1=1, axis2=2)
         s = self.lam * tr[:, None, None] * eye + 2.0 * self.g * strain
-        P = np.einsum("nab,nbc->nac", self.F, s)
-        q = np.ascontiguousarray(np.einsum("nab,ncb->nac", P, self.B0))
+        P = np.einsum("nab,nbc->nac", F, s)
+        return np.einsum("nab,ncb->nac", P, self.B0[sl])
+
+    def accelerations(self):
+        q = np.ascontiguousarray(np.concatenate(_row_chunks(self.n, self._first_pk_b0)))
         acc = np.empty((self.n, self.d))
         lib().orc_tl_accelerations(self.n, self.d, _p(self.nl.starts), _p(self.nl.idx),
                                    _p(self.g0), _p(q), self.rho0, _p(acc))
@@ -620,7 +698,7 @@ class SolidTL:
         self.v[self.fixed] = 0.0
         self.x += dt * self.v
         self.F += dt * self.deformation_rates()
-        if not np.all(np.linalg.det(self.F) > 0.0):
+        if not all(_row_chunks(self.n, lambda sl: bool(np.all(np.linalg.det(self.F[sl]) > 0.0)))):
             raise RuntimeError("deformation gradient inverted")
         self.acc = self.accelerations()
         self.v += 0.5 * dt * self.acc

@@ -16,15 +16,16 @@ cell-sorted 32-byte records.  A step is four launches on the current stream:
 with R the fused limited-linearised Riemann flux (eulerian.py:224-266) whose
 pair geometry is recomputed on the fly instead of streamed from the
 reference's per-pair arrays (eulerian.py:506-513).  Stage outputs go to a
-second buffer, so the retry-with-halving of eulerian.py:562-608 restores U^n
-by not swapping buffers.
+second buffer, so a rejected substep is dropped by not swapping buffers; once
+a step has been halved, a device copy of the step-start state lets a later
+failing substep restart the whole step from it, as eulerian.py:580-601 does.
 
 `step()` synchronises once per call (it must return dt and raise on a bad
 state, as the reference does); `advance(n)` runs n steps with no host
 synchronisation and checks the error word once at the end.
 
-Outside the hot-path scope: ghost layers, the ideal-gas HLLC
-solver, wall forces.  They raise NotImplementedError.
+Beyond the hot path (built): ghost layers, wall forces and
+the ideal-gas HLLC solver (`_HLLCSolver`, csrc/hllc.cu).
 """
 
 from __future__ import annotations
@@ -746,6 +747,25 @@ class EulerianSolver:
         self.S, self.S_nx = self.S_nx, self.S
         self.M, self.M_nx = self.M_nx, self.M
 
+    def _state_bufs(self):
+        return [self.S, self.M]
+
+    def _snapshot(self, snap):
+        """Device copies of the state records (retry-with-halving restarts
+        from them); taken only once a step has failed, so a step that
+        succeeds at full dt costs no copy."""
+        bufs = self._state_bufs()
+        if snap is None:
+            return [b.clone() for b in bufs]
+        for d, b in zip(snap, bufs):
+            d.copy_(b)
+        return snap
+
+    def _restore(self, snap):
+        for b, s in zip(self._state_bufs(), snap):
+            b.copy_(s)
+        self._state_host = None
+
     def step(self, dt: float | None = None) -> float:
         """One two-stage midpoint step with the reference's retry-with-halving
         (eulerian.py:562-608).  Returns dt."""
@@ -756,6 +776,7 @@ class EulerianSolver:
         halved = 0
         advanced = 0.0
         remaining = dt
+        snap = None
         while advanced < dt - 1e-15 * dt:
             sub = min(remaining, dt - advanced)
             self.scalars[1] = self._t_host          # device time at the substep start
@@ -763,6 +784,13 @@ class EulerianSolver:
             err = self._global_err()
             if err:
                 self.err.zero_()
+                if advanced > 0.0:
+                    # substeps of this step were already swapped in: back to
+                    # the step-start state (eulerian.py:587-590).  Like the
+                    # reference, t keeps the accepted substeps.
+                    self._restore(snap)
+                else:
+                    snap = self._snapshot(snap)     # the state is the step start
                 self._refresh_speed()   # the rejected stage 2 polluted the max
                 halved += 1
                 self.retries += 1
@@ -853,7 +881,11 @@ class EulerianSolver:
         if getattr(self, "_graphs", None) is None:
             self._graphs = {}
         per = 2 * max(1, graph_steps() // 2)
-        g = self._graphs.get(dt_override)
+        # the graph bakes in the record buffers live at capture; after an odd
+        # number of eager steps self.S is the other ping-pong buffer, so the
+        # key carries the buffer assignment (at most two graphs per dt mode)
+        key = (dt_override, self.S.data_ptr())
+        g = self._graphs.get(key)
         if g is None:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
@@ -863,7 +895,7 @@ class EulerianSolver:
                     self._swap()
                     self._record_wall_force()
             torch.cuda.synchronize()
-            self._graphs[dt_override] = g
+            self._graphs[key] = g
         return g, per
 
     def totals(self):
@@ -943,10 +975,6 @@ class _HLLCSolver(EulerianSolver):
                                           n_interior=self.n_int)
         return self._state_host
 
-    def _refresh_speed(self):
-        st = self.state
-        self.load_state(st.rho, st.mom, st.etot)
-
     def _ghosts3(self, S, M, Q, t_shift):
         if not self._ng:
             return
@@ -1003,6 +1031,14 @@ class _HLLCSolver(EulerianSolver):
     def _swap(self):
         super()._swap()
         self.Q, self.Q_nx = self.Q_nx, self.Q
+
+    def _state_bufs(self):
+        return [self.S, self.M, self.Q]
+
+    def _refresh_speed(self):
+        self._state_host = None
+        st = self.state
+        self.load_state(st.rho, st.mom, st.etot)
 
     def totals(self):
         st = self.state

@@ -31,6 +31,13 @@ def golden(name):
         return {k: z[k] for k in z.files}
 
 
+def checkpoints(g, tag, field):
+    """Steps at which a fixture stores `field` (1, 100 and the last step)."""
+    pre = f"{tag}__{field}"
+    return sorted(int(k[len(pre):]) for k in g
+                  if k.startswith(pre) and k[len(pre):].isdigit())
+
+
 @pytest.fixture(scope="session")
 def gold():
     cache = {}

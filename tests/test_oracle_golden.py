@@ -11,6 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
+from conftest import checkpoints
 from oracle import oracle as O
 from paper_2405_05155_b200 import configs
 from paper_2405_05155_b200.geometry import lattice_points
@@ -131,33 +132,62 @@ def test_oracle_c1_100_updates(gold):
         assert np.array_equal(O.sph_unity_sum(nl, np.full(len(pos), c1["vol"]), ds), g[f"rho_{tag}"])
 
 
+@pytest.mark.parametrize("label,builder", [("c2_tgv2d", configs.c2_tgv2d),
+                                           ("c5_tgv3d", configs.c5_tgv3d)])
 @pytest.mark.parametrize("key", ["1.6h", "2h"])
-def test_oracle_c2_tgv2d(gold, key):
-    g = gold("c2_tgv2d")
+def test_oracle_wc_tgv(gold, label, builder, key):
+    g = gold(label)
     tag = key.replace(".", "p")
-    cfg = configs.c2_tgv2d(kernel=key, n_side=int(g["n_side"]))
+    cfg = builder(kernel=key, n_side=int(g["n_side"]))
     s = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
                      cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
     assert digest(s.nl) == str(g[f"{tag}__digest"])
     drho, dmom = s.rhs()
     np.testing.assert_allclose(drho, g[f"{tag}__drho0"], rtol=0, atol=1e-12 * np.abs(drho).max())
     np.testing.assert_allclose(dmom, g[f"{tag}__dmom0"], rtol=0, atol=1e-12 * np.abs(dmom).max())
-    steps = int(g["steps"])
-    for k in range(1, steps + 1):
-        s.step()
-        if k in (1, steps):
-            tol = 1e-13 if k == 1 else 1e-10
-            from paper_2405_05155_b200.approx import l2_error
+    from paper_2405_05155_b200.approx import l2_error
 
+    steps = int(g["steps"])
+    marks = checkpoints(g, tag, "rho")
+    assert marks[0] == 1 and marks[-1] == steps and (steps < 100 or 100 in marks)
+    dts = []
+    for k in range(1, steps + 1):
+        dts.append(s.step())
+        if k in marks:
+            tol = 1e-13 if k == 1 else 1e-10
             assert l2_error(s.rho, g[f"{tag}__rho{k}"]) < tol
             assert l2_error(s.mom, g[f"{tag}__mom{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-13)
 
 
 @pytest.mark.parametrize("key", ["1.6h", "2h"])
-def test_oracle_c3_plate(gold, key):
-    g = gold("c3_plate")
+@pytest.mark.parametrize("mult", [20, 40])
+def test_oracle_retry_with_halving(gold, key, mult):
+    """Forced halving (eulerian.py:562-608): per-step state, t and the
+    cumulative retry count against the reference's own run."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    g = gold("retry")
+    tag = f"{key.replace('.', 'p')}_x{mult}"
+    cfg = configs.c2_tgv2d(kernel=key, n_side=int(g["n_side"]))
+    s = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"], cfg["c_art"],
+                     cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    dt = float(g[f"{tag}__dt"])
+    for k in range(1, 6):
+        s.step(dt)
+        assert s.retries == int(g[f"{tag}__retries"][k - 1])
+        assert s.t == pytest.approx(float(g[f"{tag}__t"][k - 1]), rel=1e-14)
+        assert l2_error(s.rho, g[f"{tag}__rho{k}"]) < 1e-12
+        assert l2_error(s.mom, g[f"{tag}__mom{k}"]) < 1e-12
+
+
+@pytest.mark.parametrize("label,builder,kwargs", [("c3_plate", configs.c3_plate, {"dp": 0.002}),
+                                                  ("c4_column", configs.c4_column, {"n_width": 6})])
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_tl(gold, label, builder, kwargs, key):
+    g = gold(label)
     tag = key.replace(".", "p")
-    cfg = configs.c3_plate(kernel=key, dp=0.002)
+    cfg = builder(kernel=key, **kwargs)
     m = cfg["material"]
     s = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True, cfg["cfl"])
     assert digest(s.nl) == str(g[f"{tag}__digest"])
@@ -166,13 +196,17 @@ def test_oracle_c3_plate(gold, key):
     steps = int(g["steps"])
     from paper_2405_05155_b200.approx import l2_error
 
+    marks = checkpoints(g, tag, "x")
+    assert marks[0] == 1 and marks[-1] == steps and 100 in marks
+    dts = []
     for k in range(1, steps + 1):
-        s.step()
-        if k in (1, steps):
+        dts.append(s.step())
+        if k in marks:
             tol = 1e-12 if k == 1 else 1e-9
             assert l2_error(s.x, g[f"{tag}__x{k}"]) < tol
             assert l2_error(s.v, g[f"{tag}__v{k}"]) < tol
             assert l2_error(s.F, g[f"{tag}__F{k}"]) < tol
+    np.testing.assert_allclose(dts, g[f"{tag}__dts"], rtol=1e-13)
 
 
 class _Ghosts:

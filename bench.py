@@ -13,12 +13,15 @@ L2, so no flush is needed between steps.
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 C oracle port of the numba loops, all host threads) on a bounded sample of
-the same workload (a 64^3 TGV, same per-particle work).
+the same workload (a 64^3 TGV, same per-particle work), and beside it the
+unmodified reference package (baseline/_ref, numba) on one core.
 
-One JSON line on rank 0.  Multi-GPU (torchrun): the 256^3 box is cut into
-z-slabs of whole cell layers, one per GPU, with a halo layer exchanged over
-NCCL after every stage and the dt max all-reduced (slab.py) — strong scaling
-of the same 16.8M-particle problem.
+One JSON line on rank 0.  Multi-GPU: `--gpus N` launches N ranks itself
+(torch.distributed.run on 127.0.0.1, NCCL_DEBUG=INFO) unless it already runs
+under torchrun, and refuses to start when fewer than N GPUs are visible.  The
+256^3 box is cut into z-slabs of whole cell layers, one per GPU, with a halo
+layer exchanged over NCCL after every stage and the dt max all-reduced
+(slab.py) — strong scaling of the same 16.8M-particle problem.
 """
 
 from __future__ import annotations
@@ -196,6 +199,11 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     if dist is not None:
         dist.all_reduce(pairs_t)
     pairs = int(pairs_t.item())                      # directed pairs per pass, all ranks
+    from paper_2405_05155_b200 import _lib
+
+    before = sum(_lib.CALLS.values())
+    solver.advance(1, graph=False)                   # one eager step: count its launches
+    launches_per_step = sum(_lib.CALLS.values()) - before
     solver.advance(warmup)
     torch.cuda.synchronize()
     if dist is not None:
@@ -225,7 +233,8 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
               "global": "k_wc_stage<3,%d,%s>" % (solver.group,
                                                  os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
-            "clocks": sampler.summary() if sampler else None}
+            "clocks": sampler.summary() if sampler else None,
+            "launches_per_step": launches_per_step}
 
 
 def e2e_leg(torch, solver, steps, warmup):
@@ -278,6 +287,131 @@ def cpu_reference(kind_n_side=64, steps=3, kernel="1.6h"):
                       "warm-up rhs; same per-particle work as 256^3"}
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return int(sk.getsockname()[1])
+
+
+def visible_gpus() -> int:
+    try:
+        import torch
+
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except Exception:           # noqa: BLE001 - a broken runtime counts as no GPU
+        return 0
+
+
+def launch(args) -> int:
+    """`--gpus N` (N > 1) run without torchrun: start N ranks of this script,
+    one per GPU, under torch.distributed.run on 127.0.0.1 (the driver's own
+    launch form).  Refuses to run when fewer than N GPUs are visible instead
+    of silently timing fewer."""
+    if not args.launch_check:
+        have = visible_gpus()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                  file=sys.stderr)
+            return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # communicator lines in the log
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(world, rank):
+    """Rank body of `--launch-check`: gloo on CPU, one all_reduce, rank 0
+    prints what the launcher started (tests/test_bench_launch.py)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.tensor([1 << rank], dtype=torch.int64)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": dist.get_world_size(),
+                          "ranks_mask": int(t.item()),
+                          "master_addr": os.environ.get("MASTER_ADDR"),
+                          "nccl_debug": os.environ.get("NCCL_DEBUG")}))
+    dist.destroy_process_group()
+
+
+def numba_reference(n_side=64, steps=2, kernel="1.6h"):
+    """The reference package itself (sph_trunc from baseline/_ref, its numba
+    kernels) on ONE host core, as BASELINE.md §3 planned: build outside the
+    timer, one warm-up rhs (its bench.py:94-105), then `steps` EulerianSolver
+    steps.  None when baseline/_ref or numba is missing."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "sph_trunc")):
+        return None
+    code = f"""
+import os, sys, time, json
+os.sched_setaffinity(0, {{min(os.sched_getaffinity(0))}})
+sys.path.insert(0, {ref_dir!r}); sys.path.insert(1, {REPO!r})
+from sph_trunc import eulerian
+from paper_2405_05155_b200 import configs
+cfg = configs.c5_tgv3d(kernel={kernel!r}, n_side={n_side})
+n = cfg["pos"].shape[0]
+st = eulerian.FluidState(vol=cfg["vol"].copy(), rho=cfg["rho"].copy(), mom=cfg["mom"].copy(),
+                         etot=None, n_interior=n)
+eos = eulerian.EosParams(eulerian.WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"])
+s = eulerian.EulerianSolver(cfg["pos"], n, st, eos, cfg["spec"], None, correction=True,
+                            cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+s.rhs()
+t0 = time.perf_counter()
+for _ in range({steps}):
+    s.step()
+dt = time.perf_counter() - t0
+print(json.dumps({{"value": n * {steps} / dt, "pairs": int(s.nlist.starts[-1])}}))
+"""
+    env = dict(os.environ, NUMBA_NUM_THREADS="1", OMP_NUM_THREADS="1",
+               OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                             text=True, timeout=900)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:    # noqa: BLE001 - reported, not fatal
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+    return {"value": r["value"], "unit": "particle-steps/s", "cores": 1, "kind": "reference",
+            "pairs_per_s": r["pairs"] * 2 * steps / (n_side**3 * steps / r["value"]),
+            "sample": f"sph_trunc (numba, the unmodified reference from baseline/_ref) on one "
+                      f"pinned core, TGV-3D {n_side}^3 {kernel}, {steps} steps after one warm-up "
+                      "rhs"}
+
+
+def reference_arm(args, config):
+    """`--impl reference`: the reference algorithm on this box's host cores.
+    The line's value is the oracle port (the numba loops restated in C, all
+    OpenMP threads: the stronger CPU baseline); the unmodified single-core
+    reference package is reported beside it.  Both time a bounded 64^3
+    sample of the 256^3 workload (same per-particle work: the lattice, h/dp
+    and pair count per particle do not depend on the box size)."""
+    warm = max(0, args.warmup)
+    steps = max(1, args.steps)
+    ref = cpu_reference(steps=steps)
+    ms = 1e3 * (64**3) / ref["value"]
+    cfg = dict(config, sample="TGV-3D 64^3 (262,144 particles) of the 256^3 workload",
+               particles=64**3, particles_per_gpu=64**3, parallelism="host CPU")
+    line = {"metric": METRIC, "value": ref["value"], "unit": "particle-steps/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": ref["value"], "unit": "particle-steps/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "pair_interactions_per_s": ref["pairs_per_s"]}
+    if not args.no_numba:
+        nb = numba_reference()
+        if nb is not None:
+            line["reference_package_1core"] = nb
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -288,13 +422,27 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-2h", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--no-numba", action="store_true",
+                    help="reference arm: skip the single-core sph_trunc (numba) figure")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and (args.impl == "ours"
+                                                            or args.launch_check):
+        sys.exit(launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_check:
+        launch_check(world, rank)
+        return
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     config = {"workload": f"c5_tgv3d_{args.n_side}^3_wc_euler_riemann_corrected",
-              "particles_per_gpu": args.n_side**3, "kernel": "wendland C2 truncated 1.6h",
+              "particles": args.n_side**3,
+              "particles_per_gpu": args.n_side**3 // max(1, world),
+              "kernel": "wendland C2 truncated 1.6h",
               "steps_definition": "one midpoint step = 2 fused flux stages",
               "l2": "inputs > L2 (126 MB); no flush",
               "parallelism": "single GPU" if world == 1 else f"z-slabs x{world}, NCCL halo"}
@@ -302,18 +450,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        warm = max(0, args.warmup)
-        ref = cpu_reference(steps=max(1, args.steps))
-        ms = 1e3 * (64**3) / ref["value"]
-        line = {"metric": METRIC, "value": ref["value"], "unit": "particle-steps/s",
-                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
-                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": ref["value"], "unit": "particle-steps/s",
-                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "pair_interactions_per_s": ref["pairs_per_s"]}
-        print(json.dumps(line))
+        reference_arm(args, config)
         return
 
     import torch
@@ -322,8 +459,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     from paper_2405_05155_b200 import _lib, configs
@@ -368,7 +506,7 @@ def main():
         "data": "synthetic (analytic TGV-3D fields on the 256^3 lattice)", "config": config,
         "pair_interactions_per_s": L["pairs"] * 2 * K / (L["ms"] * 1e-3),
         "pairs_per_pass": L["pairs"],
-        "gpu_launches": 3 * K,
+        "gpu_launches": L["launches_per_step"] * K,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
                      "traffic": traffic_per_launch(L["kernel"]) if world == 1 else None,
@@ -391,6 +529,14 @@ def main():
                 "ms_per_step": e2e_ms,
                 "path": "EulerianSolver.load_state(pinned) -> step() -> read_state(pinned)"},
     }
+    if world > 1:
+        # per-GPU view of the slab run: stage kernels vs the step; the rest
+        # is the exposed halo exchange + dt all-reduce + launch gaps
+        stage_step = statistics.mean(L["stage_ms"][1]) + statistics.mean(L["stage_ms"][2])
+        line["per_gpu"] = {"stage_ms_per_step": stage_step, "ms_per_step": ms_step,
+                           "exposed_comm_ms_per_step": max(0.0, ms_step - stage_step),
+                           "exposed_comm_share": max(0.0, ms_step - stage_step) / ms_step,
+                           "particles_owned": n // world}
     if "2h" in leg:
         S = leg["2h"]
         line["standard_2h"] = {

@@ -232,6 +232,8 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     kernel = {"geo": "k_wc_stage_geo<3>", "tiled": "k_wc_stage_tiled<3,%d>" % solver.group,
               "global": "k_wc_stage<3,%d,%s>" % (solver.group,
                                                  os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
+    if solver.lattice is not None:
+        kernel = "k_wc_lattice<3,%d,5>" % solver.lattice.r2
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None,
             "launches_per_step": launches_per_step}

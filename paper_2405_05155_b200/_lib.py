@@ -148,6 +148,24 @@ class TLParams(C.Structure):
     ]
 
 
+LATTICE_MAXW = 80
+
+
+class Lattice(C.Structure):
+    """sphb_lattice: the lattice fast path's extents and per-slot geometry."""
+
+    _fields_ = [
+        ("width", C.c_int32),
+        ("r2", C.c_int32),
+        ("n", C.c_int32 * 3),
+        ("reserved", C.c_int32),
+        ("dx", (C.c_double * 3) * LATTICE_MAXW),
+        ("inv_r", C.c_double * LATTICE_MAXW),
+        ("g2", C.c_double * LATTICE_MAXW),
+        ("mv", C.c_double * LATTICE_MAXW),
+    ]
+
+
 P = C.c_void_p
 I32 = C.c_int32
 I64 = C.c_int64
@@ -181,6 +199,10 @@ SIGNATURES = {
     "sphb_tl_accelerations_csr": (C.c_int, [I64, I32, P, P, P, P, F64, P, P]),
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_lattice_width": (C.c_int, [I32, I32]),
+    "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
+    "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
+    "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_ell_sort_rows": (C.c_int, [P, I64, P, P, P, F64, P, P]),
     "sphb_weak_gradient": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),

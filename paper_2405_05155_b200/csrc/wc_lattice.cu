@@ -1,0 +1,342 @@
+// wc_lattice.cu — WC stage on a complete lattice (the C2 / C5 configs).
+//
+// Same stage as k_wc_stage (wc_engine.cu; reference eulerian.py:224-266,
+// 610-643), specialised for particle sets that ARE a lattice in engine order
+// (neighbors.engine_order: axis 0 fastest, periodic in every axis, or a slab
+// rank's local block whose owned rows never wrap): every row then holds the
+// same offsets, so
+//   * the neighbour index is computed, j = X[ox] + Y[oy] + Z[oz] from
+//     per-thread wrapped lattice coordinates, with the offsets compile-time
+//     constants (canonical order: z, y, x ascending, |o|^2 <= R2) — no pass
+//     list is read at all (C5: 2.1 GB of int32 per stage launch);
+//   * the pair geometry (x_i - x_j, 1/r and the Wendland t^3 pair factors)
+//     is one table per slot, a kernel parameter, so the FP64 instructions
+//     read it as constant-bank operands; the X_j gather, r2, the reciprocal
+//     square root and t^3 disappear from the pair loop.
+// sphb_wc_lattice_check proves the specialisation before it is used: every
+// checked row's pair set equals the canonical offset set (so the pair set is
+// the reference's, bit-exact), and every pair's exact displacement equals
+// the table's within `tol`.  Summation is in the canonical slot order.
+#include <type_traits>
+#include <utility>
+
+#include "wc_common.cuh"
+
+using namespace sphb;
+using namespace sphb::wc;
+
+namespace {
+
+constexpr int kLT = 128;     // threads per block
+
+// Integer offsets o with 0 < |o|^2 <= R2, z slowest, x fastest.
+struct OffList {
+  int n;
+  int o[SPHB_LATTICE_MAXW][3];
+};
+
+constexpr int isqrt_c(int v) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+template <int D, int R2>
+constexpr OffList make_offsets() {
+  OffList L{};
+  const int R = isqrt_c(R2);
+  const int rz = D > 2 ? R : 0, ry = D > 1 ? R : 0;
+  for (int z = -rz; z <= rz; ++z)
+    for (int y = -ry; y <= ry; ++y)
+      for (int x = -R; x <= R; ++x) {
+        const int q = x * x + y * y + z * z;
+        if (q == 0 || q > R2) continue;
+        L.o[L.n][0] = x;
+        L.o[L.n][1] = y;
+        L.o[L.n][2] = z;
+        ++L.n;
+      }
+  return L;
+}
+
+template <int D, int R2>
+struct Stencil {
+  static constexpr OffList L = make_offsets<D, R2>();
+  static constexpr int W = L.n;
+  static constexpr int R = isqrt_c(R2);
+};
+
+template <int K, class F, int... Is>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int K, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl<K>(f, std::make_integer_sequence<int, K>{});
+}
+
+struct LatConst {
+  double c2, c2rho0, eta_c, hc;
+};
+
+// wrapped lattice coordinate c + s in [0, n)
+__device__ __forceinline__ int wrapc(int c, int s, int n) {
+  int v = c + s;
+  v += v < 0 ? n : 0;
+  v -= v >= n ? n : 0;
+  return v;
+}
+
+template <int D, int R2, int MINB>
+__global__ void __launch_bounds__(kLT, MINB)
+k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
+             const double* __restrict__ B, const double4* __restrict__ S_in,
+             const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
+             double* __restrict__ scalars, int32_t* __restrict__ err) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  const int64_t n = P.n;
+  const int64_t i0 = P.row0 + (int64_t)blockIdx.x * kLT + threadIdx.x;
+  const bool own = i0 < P.row0 + P.nrows;
+  // tail lanes redo the last row (no divergence in the pair loop), no write
+  const int64_t i = own ? i0 : P.row0 + P.nrows - 1;
+
+  // lattice coordinates and the wrapped neighbour components of this row
+  const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
+  const int ii = (int)i;
+  const int a = ii % n0;
+  const int t = ii / n0;
+  const int b = D > 1 ? t % n1 : 0;
+  const int cz = D > 2 ? t / n1 : 0;
+  int xs[2 * R + 1], ys[2 * R + 1], zs[2 * R + 1];
+#pragma unroll
+  for (int s = -R; s <= R; ++s) {
+    xs[s + R] = wrapc(a, s, n0);
+    ys[s + R] = D > 1 ? n0 * wrapc(b, s, n1) : 0;
+    zs[s + R] = D > 2 ? n0 * n1 * wrapc(cz, s, n2) : 0;
+  }
+
+  const double c = P.c_art;
+  const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, hc = K.hc;
+  double vi[D], rho_i;
+  unpack_s<D>(S_in[i], vi, rho_i);
+  Sym<D> Bi;
+  Bi.load(B, n, i);
+  const double hrho_i = 0.5 * rho_i;
+  double dr = 0.0, dm[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) dm[q] = 0.0;
+
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int ox = St::L.o[k][0], oy = St::L.o[k][1], oz = St::L.o[k][2];
+    const int64_t j = (int64_t)(xs[ox + R] + ys[oy + R] + zs[oz + R]);
+    double vj[D], rho_j;
+    unpack_s<D>(ldg4(S_in + j), vj, rho_j);
+    Sym<D> Bj, Bs;
+    Bj.load(B, n, j);
+    Bi.add(Bj, Bs);
+    double dx[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) dx[q] = L.dx[k][q];
+    const double inv_r = L.inv_r[k];
+    double G_[D];                                     // (B_i + B_j) dx
+    Bs.mv(dx, G_);
+    double dv[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) dv[q] = vj[q] - vi[q];
+    double dud = dv[0] * dx[0];
+#pragma unroll
+    for (int q = 1; q < D; ++q) dud = fma(dv[q], dx[q], dud);
+    const double du = dud * inv_r;                   // u_l - u_r (eulerian.py:236-243)
+    double beta = du * eta_c;
+    beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
+    const double rbar = fma(0.5, rho_j, hrho_i);
+    const double bh = beta * hc;
+    const double wr = ((beta * bh) * (rho_i - rho_j)) * (rcp_nr(rbar) * inv_r);
+    const double p_star = fma(bh * rbar, du, fma(c2, rbar, -c2rho0));
+    double vs[D];
+    double sg = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      vs[q] = fma(-wr, dx[q], fma(0.5, dv[q], vi[q]));
+      sg = fma(vs[q], G_[q], sg);
+    }
+    const double rs2 = rbar * (L.g2[k] * sg);        // -2 rbar s
+    dr += rs2;
+    const double pg = p_star * L.g2[k];               // -2 p* gsc
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      dm[q] = fma(-L.mv[k], dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
+  });
+
+  wc_epilogue<D, kLT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
+}
+
+// Proof of the specialisation for rows [row0, row0 + nrows): cnt == W, the
+// row's neighbours are exactly {i + o_k} (wrapped), and the exact minimum-
+// image displacement of each (neighbors.py:152-157) is within tol of the
+// table.  bad[0] += rows that fail.
+template <int D, int R2>
+__global__ void k_wc_lattice_check(const sphb_wc_params P, const sphb_lattice L,
+                                   const double4* __restrict__ X,
+                                   const int32_t* __restrict__ nbr,
+                                   const int32_t* __restrict__ cnt, double tol,
+                                   unsigned long long* bad) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  constexpr int SIDE = 2 * R + 1;
+  const int64_t i = P.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.row0 + P.nrows) return;
+  const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
+  const int64_t n = P.n;
+  const int ii = (int)i;
+  const int a = ii % n0, t = ii / n0;
+  const int b = D > 1 ? t % n1 : 0, cz = D > 2 ? t / n1 : 0;
+  bool ok = cnt[i] == St::W;
+  // slot index of every offset in the (2R+1)^D cube, -1 outside the stencil
+  int slot[SIDE * SIDE * SIDE];
+#pragma unroll
+  for (int q = 0; q < SIDE * SIDE * SIDE; ++q) slot[q] = -1;
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int q = (St::L.o[k][0] + R) + SIDE * ((St::L.o[k][1] + R) + SIDE * (St::L.o[k][2] + R));
+    slot[q] = k;
+  });
+  unsigned long long seen[2] = {0ull, 0ull};
+  const int w = ok ? St::W : 0;
+  for (int e = 0; e < w; ++e) {
+    const int j = nbr[(int64_t)e * n + i];
+    const int ja = j % n0, jt = j / n0;
+    const int jb = D > 1 ? jt % n1 : 0, jc = D > 2 ? jt / n1 : 0;
+    int o[3] = {ja - a, jb - b, jc - cz};
+    const int ext[3] = {n0, n1, n2};
+#pragma unroll
+    for (int q = 0; q < D; ++q) {     // unwrap into (-n/2, n/2]
+      if (o[q] > ext[q] / 2) o[q] -= ext[q];
+      if (o[q] < -(ext[q] - 1) / 2) o[q] += ext[q];
+    }
+    bool in = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) in = in && o[q] >= -R && o[q] <= R;
+    const int k = in ? slot[(o[0] + R) + SIDE * ((o[1] + R) + SIDE * (o[2] + R))] : -1;
+    if (k < 0) { ok = false; break; }
+    seen[k >> 6] |= 1ull << (k & 63);
+  }
+  if (ok) {
+    const int nb = __popcll(seen[0]) + __popcll(seen[1]);
+    ok = nb == St::W;
+  }
+  if (ok) {
+    const double4 xi = X[i];
+    const double wi[3] = {xi.x, xi.y, xi.z};
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int ox = St::L.o[k][0], oy = St::L.o[k][1], oz = St::L.o[k][2];
+      const int ja = wrapc(a, ox, n0);
+      const int jb = D > 1 ? wrapc(b, oy, n1) : 0;
+      const int jc = D > 2 ? wrapc(cz, oz, n2) : 0;
+      const double4 xj = X[(int64_t)ja + (int64_t)n0 * (jb + (int64_t)n1 * jc)];
+      const double wj[3] = {xj.x, xj.y, xj.z};
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const double d = min_image(__dsub_rn(wi[q], wj[q]), P.box[q], P.periodic);
+        ok = ok && fabs(d - L.dx[k][q]) <= tol;
+      }
+    });
+  }
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+}  // namespace
+
+#define SPHB_LAT_CASES(X) X(2, 4) X(2, 6) X(3, 4) X(3, 6)
+
+extern "C" int sphb_lattice_width(int32_t dim, int32_t r2) {
+#define SPHB_W(D, R) if (dim == D && r2 == R) return Stencil<D, R>::W;
+  SPHB_LAT_CASES(SPHB_W)
+#undef SPHB_W
+  return 0;
+}
+
+extern "C" int sphb_lattice_offsets(int32_t dim, int32_t r2, int32_t* off) {
+#define SPHB_O(D, R)                                              \
+  if (dim == D && r2 == R) {                                      \
+    constexpr OffList Lc = make_offsets<D, R>();                  \
+    for (int k = 0; k < Lc.n; ++k)                                \
+      for (int q = 0; q < 3; ++q) off[3 * k + q] = Lc.o[k][q];    \
+    return SPHB_OK;                                               \
+  }
+  if (!off) return SPHB_ERR_ARG;
+  SPHB_LAT_CASES(SPHB_O)
+#undef SPHB_O
+  return SPHB_ERR_ARG;
+}
+
+static bool lattice_args_ok(const sphb_wc_params* p, const sphb_lattice* L) {
+  if (!p || !L || p->n <= 0 || p->n >= (int64_t)1 << 31 || p->row0 < 0 || p->nrows < 0 ||
+      p->row0 + p->nrows > p->n)
+    return false;
+  int64_t prod = 1;
+  for (int q = 0; q < 3; ++q) {
+    if (L->n[q] < 1 || (q >= p->dim && L->n[q] != 1)) return false;
+    prod *= L->n[q];
+  }
+  if (prod != p->n) return false;
+  const int R = isqrt_c(L->r2);
+  for (int q = 0; q < p->dim; ++q)
+    if (L->n[q] < 2 * R + 1) return false;   // wraps must not alias offsets
+  return sphb_lattice_width(p->dim, L->r2) == L->width;
+}
+
+extern "C" int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L,
+                                     const double* x, const int32_t* nbr, const int32_t* cnt,
+                                     double tol, unsigned long long* bad, void* stream) {
+  if (!lattice_args_ok(p, L) || !x || !nbr || !cnt || !bad) return SPHB_ERR_ARG;
+  if (p->nrows == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(p->nrows, 128);
+  const double4* X = (const double4*)x;
+#define SPHB_C(D, R)                                                                   \
+  if (p->dim == D && L->r2 == R) {                                                     \
+    k_wc_lattice_check<D, R><<<grid, 128, 0, st>>>(*p, *L, X, nbr, cnt, tol, bad);     \
+    SPHB_LAUNCH_CHECK();                                                               \
+    return SPHB_OK;                                                                    \
+  }
+  SPHB_LAT_CASES(SPHB_C)
+#undef SPHB_C
+  return SPHB_ERR_ARG;
+}
+
+extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L,
+                                     int32_t stage, const double* b, const double* s_in,
+                                     const double* s_n, const double* m_n, double* s_out,
+                                     double* m_out, double* scalars, int32_t* err,
+                                     void* stream) {
+  if (!lattice_args_ok(p, L) || stage < 0 || stage > 2 || p->interior || p->wall_tag ||
+      !p->uniform_vol)
+    return SPHB_ERR_ARG;
+  if (p->nrows == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LatConst K;
+  K.c2 = p->c_art * p->c_art;
+  K.c2rho0 = K.c2 * p->rho0;
+  K.eta_c = kEtaLinearized / p->c_art;
+  K.hc = 0.5 * p->c_art;
+  const unsigned grid = sphb_blocks(p->nrows, kLT);
+  const double4* Sin = (const double4*)s_in;
+  const double4* Sn = (const double4*)s_n;
+  const double4* Mn = (const double4*)m_n;
+  double4* Sout = (double4*)s_out;
+  double4* Mout = (double4*)m_out;
+#define SPHB_S(D, R)                                                                   \
+  if (p->dim == D && L->r2 == R) {                                                     \
+    k_wc_lattice<D, R, 5><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout, \
+                                                Mout, scalars, err);                   \
+    SPHB_LAUNCH_CHECK();                                                               \
+    return SPHB_OK;                                                                    \
+  }
+  SPHB_LAT_CASES(SPHB_S)
+#undef SPHB_S
+  return SPHB_ERR_ARG;
+}

@@ -371,6 +371,11 @@ class EulerianSolver:
         # blocks on one contiguous region share neighbour rows through L2);
         # off by default, SPHB_SWIZZLE=<sm count> to enable
         p.swizzle = int(os.environ.get("SPHB_SWIZZLE", "0"))
+        self.lattice = None
+        if (variant == "global" and precision == "fp64" and not self._ideal and ghosts is None
+                and wall_force_tag is None and uniform and self.order is not self.bins
+                and os.environ.get("SPHB_WC_LATTICE", "1") != "0"):
+            self.lattice = self._setup_lattice(float(vol[0]))
 
         self._cfl_h = self.cfl * kernel.h                      # eulerian.py:560
 
@@ -405,6 +410,60 @@ class EulerianSolver:
         self.set_state(state)
         self._setup_push(dev)
         self._setup_overlap()
+
+    def _setup_lattice(self, vol):
+        """Lattice fast path (csrc/wc_lattice.cu) when the set is a complete
+        lattice in engine order: extents, canonical offsets and the per-slot
+        geometry table (from one representative row, exact minimum-image
+        arithmetic of neighbors.py:152-157), then sphb_wc_lattice_check over
+        the rows this solver updates.  None (general kernel) when any row's
+        pair set or displacement does not match."""
+        torch = _lib.torch_cuda()
+        g, d, n = self.grid, self.dim, self.n
+        if d not in (2, 3) or not g.periodic or int(g.slow_axis) != d - 1 or n == 0:
+            return None
+        spacing = vol ** (1.0 / d)
+        ext = [int(round(g.box[a] / spacing)) for a in range(d - 1)]
+        if min(ext) < 1 or n % int(np.prod(ext)):
+            return None
+        ext.append(n // int(np.prod(ext)))
+        r2 = int(math.floor((g.cutoff / spacing) ** 2 * (1.0 + 1e-12)))
+        lib = _lib.lib()
+        width = int(lib.sphb_lattice_width(d, r2))
+        if width == 0 or width != self.width or n >= 2**31:
+            return None
+        off = np.zeros(3 * width, dtype=np.int32)
+        _lib.check(lib.sphb_lattice_offsets(d, r2, off.ctypes.data), "sphb_lattice_offsets")
+        off = off.reshape(width, 3)[:, :d]
+        L = _lib.Lattice()
+        L.width, L.r2 = width, r2
+        for a in range(3):
+            L.n[a] = ext[a] if a < d else 1
+        ext_a = np.asarray(ext)
+        rep = ext_a // 2
+        lin = lambda c: int(c[0] + ext_a[0] * (c[1] + (ext_a[1] * c[2] if d == 3 else 0)))
+        rows = [lin(rep)] + [lin(np.mod(rep + o, ext_a)) for o in off]
+        xw = self.X[torch.tensor(rows, device=self.X.device), :d].cpu().numpy()
+        box = np.asarray([g.box[a] for a in range(d)])
+        h, mu = self.kernel.h, self.mu
+        c5s = -5.0 * self.kernel.alpha / h
+        cg2, cm = -(c5s * vol / h), 2.0 * mu * c5s * vol / h
+        for k in range(width):
+            dx = xw[0] - xw[1 + k]
+            dx = np.where(dx > 0.5 * box, dx - box, np.where(dx < -0.5 * box, dx + box, dx))
+            r = math.sqrt(float(np.sum(dx * dx)))
+            t = 1.0 - 0.5 * r / h
+            base = (t * t) * t
+            for a in range(d):
+                L.dx[k][a] = float(dx[a])
+            L.inv_r[k] = 1.0 / r
+            L.g2[k] = cg2 * base
+            L.mv[k] = cm * base
+        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
+        _lib.call("sphb_wc_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
+                  self.X.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                  1e-12 * spacing, bad.data_ptr(), _lib.stream_ptr())
+        return L if int(bad.item()) == 0 else None
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)
@@ -497,7 +556,9 @@ class EulerianSolver:
     def _stage_rows(self, stage, rows, s_in, s_n, m_n, s_out, m_out):
         p = self.params
         p.row0, p.nrows = rows.start, rows.stop - rows.start
-        if p.nrows > 0:
+        if p.nrows > 0 and self.lattice is not None:
+            self._stage_lattice(stage, s_in, s_n, m_n, s_out, m_out)
+        elif p.nrows > 0:
             _lib.call("sphb_wc_stage", ctypes.byref(p), stage, self.group, self.X.data_ptr(),
                       self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
                       s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
@@ -671,12 +732,21 @@ class EulerianSolver:
             self._stage_boundary_first(stage, s_in, s_n, m_n, s_out, m_out)
             return
         self._set_push(stage, s_out)
+        if self.lattice is not None:
+            self._stage_lattice(stage, s_in, s_n, m_n, s_out, m_out)
+            return
         _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.group,
                   self.X.data_ptr(),
                   self.B.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), s_in.data_ptr(),
                   s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
                   None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                   self.err.data_ptr(), _lib.stream_ptr())
+
+    def _stage_lattice(self, stage, s_in, s_n, m_n, s_out, m_out):
+        _lib.call("sphb_wc_stage_lattice", ctypes.byref(self.params), ctypes.byref(self.lattice),
+                  stage, self.B.data_ptr(), s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(),
+                  s_out.data_ptr(), None if m_out is None else m_out.data_ptr(),
+                  self.scalars.data_ptr(), self.err.data_ptr(), _lib.stream_ptr())
 
     def _global_err(self) -> int:
         if self._slab is not None and self._slab.world > 1:

@@ -836,3 +836,47 @@ def test_graph_steps_per_replay(monkeypatch, per):
     for _ in range(11):
         r.step()
     assert l2_error(s.x, r.x) < 1e-14 and l2_error(s.v, r.v) < 1e-12
+
+
+# ------------------------------------------------ lattice fast path (wc_lattice.cu)
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+@pytest.mark.parametrize("label,builder,size", [("c2", configs.c2_tgv2d, 40),
+                                                ("c5", configs.c5_tgv3d, 12)])
+def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, label, builder, size):
+    """TGV lattices run the lattice kernel (checked pair sets + geometry
+    table); it matches the general pass-list kernel and the oracle."""
+    cfg = builder(kernel=key, n_side=size)
+    fast = make_wc(cfg)
+    assert fast.lattice is not None and fast.lattice.width == fast.width
+    monkeypatch.setenv("SPHB_WC_LATTICE", "0")
+    gen = make_wc(cfg)
+    assert gen.lattice is None
+    ref = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"],
+                       cfg["c_art"], cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    d_fast, m_fast, _ = fast.rhs()
+    d_gen, m_gen, _ = gen.rhs()
+    d_ref, m_ref = ref.rhs()
+    assert l2_error(d_fast, d_ref) < 1e-12 and l2_error(m_fast, m_ref) < 1e-12
+    assert l2_error(d_fast, d_gen) < 1e-12 and l2_error(m_fast, m_gen) < 1e-12
+    fast.advance(30)
+    gen.advance(30)
+    for _ in range(30):
+        ref.step()
+    for s in (fast, gen):
+        assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
+        assert l2_error(s.state.mom, ref.mom) < 1e-10
+
+
+def test_wc_lattice_check_rejects_perturbed_sets():
+    """Same pair set, displacements off the table by more than the tolerance:
+    the check refuses the lattice path (general kernel, still oracle-exact)."""
+    cfg = configs.c5_tgv3d(n_side=12)
+    rng = np.random.default_rng(3)
+    cfg["pos"] = cfg["pos"] + rng.uniform(-1e-9, 1e-9, size=cfg["pos"].shape)
+    s = make_wc(cfg)
+    assert s.lattice is None
+    ref = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"],
+                       cfg["c_art"], cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    s.step()
+    ref.step()
+    assert l2_error(s.state.mom, ref.mom) < 1e-12

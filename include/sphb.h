@@ -303,24 +303,22 @@ typedef struct sphb_wc_params {
 
 /* Lattice fast path of the WC stage (csrc/wc_lattice.cu): for particle sets
  * that are a complete lattice in engine order (axis 0 fastest; periodic, or
- * a slab rank whose owned rows never wrap) with separable coordinates.
- * Offsets o with 0 < |o|^2 <= r2 (lattice units) in canonical order (axis 2
- * slowest, axis 0 fastest); supported (dim, r2): (2, 4), (2, 6), (3, 4),
- * (3, 6) — the 1.6h / 2h stencils at h = 1.3 dp.  Per canonical slot k, the
- * expansion point r2k (a squared pair distance of the slot) and, at r2k with
- * their derivatives in r2 (uniform volume V folded in): inv_r = 1/r,
- * g2 = -2 x 0.5 dW V / r, mv = mu viscv = 2 mu dW V / r
- * (eulerian.py:506-513). */
+ * a slab rank whose owned rows never wrap).  Offsets o with 0 < |o|^2 <= r2
+ * (lattice units) in canonical order (axis 2 slowest, axis 0 fastest);
+ * supported (dim, r2): (2, 4), (2, 6), (3, 4), (3, 6) — the 1.6h / 2h
+ * stencils at h = 1.3 dp.  Geometry per canonical slot k (uniform volume V
+ * folded in): dx = x_i - x_j, inv_r = 1/|dx|, g2 = -2 x 0.5 dW V / r,
+ * mv = mu viscv = 2 mu dW V / r (eulerian.py:506-513). */
 #define SPHB_LATTICE_MAXW 80
 typedef struct sphb_lattice {
   int32_t width;         /* slots per row = sphb_lattice_width(dim, r2)     */
   int32_t r2;
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
   int32_t reserved;
-  double r2k[SPHB_LATTICE_MAXW];
-  double inv_r[SPHB_LATTICE_MAXW], dinv_r[SPHB_LATTICE_MAXW];
-  double g2[SPHB_LATTICE_MAXW], dg2[SPHB_LATTICE_MAXW];
-  double mv[SPHB_LATTICE_MAXW], dmv[SPHB_LATTICE_MAXW];
+  double dx[SPHB_LATTICE_MAXW][3];
+  double inv_r[SPHB_LATTICE_MAXW];
+  double g2[SPHB_LATTICE_MAXW];
+  double mv[SPHB_LATTICE_MAXW];
 } sphb_lattice;
 /* Slots of the (dim, r2) stencil (0: unsupported) and their offsets
  * (off[3 k + axis]). */
@@ -328,17 +326,16 @@ int sphb_lattice_width(int32_t dim, int32_t r2);
 int sphb_lattice_offsets(int32_t dim, int32_t r2, int32_t* off);
 /* Proof of the specialisation for rows [row0, row0 + nrows): counts rows
  * (into *bad, device, accumulated) whose pass-list row (nbr, cnt: the ELL
- * list in engine order) is not exactly {i + o_k}, whose exact minimum-image
- * displacements (neighbors.py:152-157, from X records) are not separable
- * per axis (bitwise), or whose pair r2 is off r2k by more than tol
- * (relative). */
+ * list in engine order) is not exactly {i + o_k} or whose exact minimum-
+ * image displacement (neighbors.py:152-157, from X records) differs from
+ * L->dx by more than tol on any axis. */
 int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L, const double* X,
                           const int32_t* nbr, const int32_t* cnt, double tol,
                           unsigned long long* bad, void* stream);
 /* The stage of sphb_wc_stage on a checked lattice (uniform volumes; no
  * ghosts, no wall tags): same stage / record / scalar / error contract. */
 int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L, int32_t stage,
-                          const double* X, const double* B, const double* S_in, const double* S_n,
+                          const double* B, const double* S_in, const double* S_n,
                           const double* M_n, double* S_out, double* M_out, double* scalars,
                           int32_t* err, void* stream);
 

@@ -159,13 +159,10 @@ class Lattice(C.Structure):
         ("r2", C.c_int32),
         ("n", C.c_int32 * 3),
         ("reserved", C.c_int32),
-        ("r2k", C.c_double * LATTICE_MAXW),
+        ("dx", (C.c_double * 3) * LATTICE_MAXW),
         ("inv_r", C.c_double * LATTICE_MAXW),
-        ("dinv_r", C.c_double * LATTICE_MAXW),
         ("g2", C.c_double * LATTICE_MAXW),
-        ("dg2", C.c_double * LATTICE_MAXW),
         ("mv", C.c_double * LATTICE_MAXW),
-        ("dmv", C.c_double * LATTICE_MAXW),
     ]
 
 
@@ -205,7 +202,7 @@ SIGNATURES = {
     "sphb_lattice_width": (C.c_int, [I32, I32]),
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
-    "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_ell_sort_rows": (C.c_int, [P, I64, P, P, P, F64, P, P]),
     "sphb_weak_gradient": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),

@@ -37,6 +37,9 @@ struct Sym<2> {
     out[0] = fma(a00, e[0], a01 * e[1]);
     out[1] = fma(a01, e[0], a11 * e[1]);
   }
+  __device__ __forceinline__ double at(int r, int c) const {
+    return r != c ? a01 : (r == 0 ? a00 : a11);
+  }
 };
 template <>
 struct Sym<3> {
@@ -54,6 +57,10 @@ struct Sym<3> {
     out[0] = fma(a00, e[0], fma(a01, e[1], a02 * e[2]));
     out[1] = fma(a01, e[0], fma(a11, e[1], a12 * e[2]));
     out[2] = fma(a02, e[0], fma(a12, e[1], a22 * e[2]));
+  }
+  __device__ __forceinline__ double at(int r, int c) const {
+    const int k = r < c ? r * 3 + c : c * 3 + r;
+    return k == 0 ? a00 : k == 1 ? a01 : k == 2 ? a02 : k == 4 ? a11 : k == 5 ? a12 : a22;
   }
 };
 

@@ -9,20 +9,14 @@
 //     per-thread wrapped lattice coordinates, with the offsets compile-time
 //     constants (canonical order: z, y, x ascending, |o|^2 <= R2) — no pass
 //     list is read at all (C5: 2.1 GB of int32 per stage launch);
-//   * the pair displacement is separable: its axis-q component is the
-//     row's exact minimum-image difference to its neighbour along axis q
-//     alone, computed once per row into shared memory (no X_j gather), and
-//     components with o_q = 0 are exact zeros known at compile time, so
-//     B dx, r2 and (v_j - v_i).dx lose those terms;
-//   * 1/r and the Wendland t^3 pair factors are a per-slot first-order
-//     expansion in r2 about the slot's r2 (kernel-parameter constants; the
-//     rows' r2 differ from it by ~1e-14 relative), replacing the reciprocal
-//     square root and t^3 chain.
+//   * the pair geometry (x_i - x_j, 1/r and the Wendland t^3 pair factors)
+//     is one table per slot, a kernel parameter, so the FP64 instructions
+//     read it as constant-bank operands; the X_j gather, r2, the reciprocal
+//     square root and t^3 disappear from the pair loop.
 // sphb_wc_lattice_check proves the specialisation before it is used: every
 // checked row's pair set equals the canonical offset set (so the pair set is
-// the reference's, bit-exact), every pair's exact displacement is separable
-// as above (bitwise), and its r2 is within tol of the expansion point.
-// Summation is in the canonical slot order.
+// the reference's, bit-exact), and every pair's exact displacement equals
+// the table's within `tol`.  Summation is in the canonical slot order.
 #include <stdlib.h>
 
 #include <type_traits>
@@ -36,7 +30,6 @@ using namespace sphb::wc;
 namespace {
 
 constexpr int kLT = 128;     // threads per block
-
 
 // Integer offsets o with 0 < |o|^2 <= R2, z slowest, x fastest.
 struct OffList {
@@ -99,13 +92,11 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
 template <int D, int R2, int MINB>
 __global__ void __launch_bounds__(kLT, MINB)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
-             const double4* __restrict__ X, const double* __restrict__ B,
-             const double4* __restrict__ S_in, const double4* Sn, const double4* Mn,
-             double4* S_out, double4* M_out, double* __restrict__ scalars,
-             int32_t* __restrict__ err) {
+             const double* __restrict__ B, const double4* __restrict__ S_in,
+             const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
+             double* __restrict__ scalars, int32_t* __restrict__ err) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
-  constexpr int SIDE = 2 * R + 1;
   const int64_t n = P.n;
   const int64_t i0 = P.row0 + (int64_t)blockIdx.x * kLT + threadIdx.x;
   const bool own = i0 < P.row0 + P.nrows;
@@ -119,38 +110,13 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
   const int t = ii / n0;
   const int b = D > 1 ? t % n1 : 0;
   const int cz = D > 2 ? t / n1 : 0;
-  int xs[SIDE], ys[SIDE], zs[SIDE];
+  int xs[2 * R + 1], ys[2 * R + 1], zs[2 * R + 1];
 #pragma unroll
   for (int s = -R; s <= R; ++s) {
     xs[s + R] = wrapc(a, s, n0);
     ys[s + R] = D > 1 ? n0 * wrapc(b, s, n1) : 0;
     zs[s + R] = D > 2 ? n0 * n1 * wrapc(cz, s, n2) : 0;
   }
-  // Exact pair displacements, separable on a checked lattice: the axis-q
-  // component of x_i - x_j depends only on this row and o_q, so it is the
-  // minimum-image difference to the row's neighbour along axis q alone
-  // (neighbors.py:152-157 arithmetic).  sdx[(q SIDE + o_q + R) kLT + tid].
-  __shared__ double sdx[D * SIDE * kLT];
-  {
-    const double4 xi = X[i];
-    const double wi[3] = {xi.x, xi.y, xi.z};
-    const int c0 = xs[R], c1 = ys[R], c2 = zs[R];
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-#pragma unroll
-      for (int s = -R; s <= R; ++s) {
-        double d = 0.0;
-        if (s != 0) {
-          const int64_t jq = q == 0 ? (int64_t)xs[s + R] + c1 + c2
-                                    : (q == 1 ? (int64_t)c0 + ys[s + R] + c2
-                                              : (int64_t)c0 + c1 + zs[s + R]);
-          const double wjq = __ldg(reinterpret_cast<const double*>(X + jq) + q);
-          d = min_image(__dsub_rn(wi[q], wjq), P.box[q], P.periodic);
-        }
-        sdx[(q * SIDE + s + R) * kLT + threadIdx.x] = d;
-      }
-  }
-  // (each thread reads only its own column: no barrier needed)
 
   const double c = P.c_art;
   const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, hc = K.hc;
@@ -172,24 +138,25 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
     Sym<D> Bj, Bs;
     Bj.load(B, n, j);
     Bi.add(Bj, Bs);
-    // exact displacement; components with o_q = 0 are exactly 0 (checked)
-    // and fold away at compile time
+    // components with o_q = 0 are zero (checked within tol): compile-time
+    // zeros, so B dx, (v_j - v_i).dx and the limiter term lose them
     double dx[D];
 #pragma unroll
-    for (int q = 0; q < D; ++q)
-      dx[q] = o[q] == 0 ? 0.0 : sdx[(q * SIDE + o[q] + R) * kLT + threadIdx.x];
-    double r2 = 0.0;
+    for (int q = 0; q < D; ++q) dx[q] = o[q] == 0 ? 0.0 : L.dx[k][q];
+    const double inv_r = L.inv_r[k];
+    double G_[D];                                     // (B_i + B_j) dx, nonzero columns
 #pragma unroll
-    for (int q = 0; q < D; ++q)
-      if (o[q] != 0) r2 = fma(dx[q], dx[q], r2);
-    // 1/r and the Wendland pair factors to first order about the slot's
-    // r2 (|r2 - r2_k| / r2_k ~ 1e-14: the second-order term is ~1e-28)
-    const double del = r2 - L.r2k[k];
-    const double inv_r = fma(L.dinv_r[k], del, L.inv_r[k]);
-    const double g2 = fma(L.dg2[k], del, L.g2[k]);
-    const double mv = fma(L.dmv[k], del, L.mv[k]);
-    double G_[D];                                     // (B_i + B_j) dx
-    Bs.mv(dx, G_);
+    for (int r = 0; r < D; ++r) {
+      double acc = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+        if (o[q] != 0) {
+          acc = first ? Bs.at(r, q) * dx[q] : fma(Bs.at(r, q), dx[q], acc);
+          first = false;
+        }
+      G_[r] = acc;
+    }
     double dv[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) dv[q] = vj[q] - vi[q];
@@ -212,12 +179,12 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
       vs[q] = o[q] == 0 ? vb : fma(-wr, dx[q], vb);
       sg = fma(vs[q], G_[q], sg);
     }
-    const double rs2 = rbar * (g2 * sg);             // -2 rbar s
+    const double rs2 = rbar * (L.g2[k] * sg);        // -2 rbar s
     dr += rs2;
-    const double pg = p_star * g2;                    // -2 p* gsc
+    const double pg = p_star * L.g2[k];               // -2 p* gsc
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      dm[q] = fma(-mv, dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
+      dm[q] = fma(-L.mv[k], dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
   });
 
   wc_epilogue<D, kLT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
@@ -278,33 +245,21 @@ __global__ void k_wc_lattice_check(const sphb_wc_params P, const sphb_lattice L,
     ok = nb == St::W;
   }
   if (ok) {
-    // separability, exactly: the pair's minimum-image displacement equals,
-    // axis by axis, the one to the row's neighbour along that axis alone
-    // (what k_wc_lattice uses), with exact zeros where o_q = 0; and r2 is
-    // within tol (relative) of the slot's expansion point
     const double4 xi = X[i];
     const double wi[3] = {xi.x, xi.y, xi.z};
-    const int sa[3] = {a, b, cz};
     static_for<St::W>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
-      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-      const int jc3[3] = {wrapc(a, o[0], n0), D > 1 ? wrapc(b, o[1], n1) : 0,
-                          D > 2 ? wrapc(cz, o[2], n2) : 0};
-      const double4 xj = X[(int64_t)jc3[0] + (int64_t)n0 * (jc3[1] + (int64_t)n1 * jc3[2])];
+      constexpr int ox = St::L.o[k][0], oy = St::L.o[k][1], oz = St::L.o[k][2];
+      const int ja = wrapc(a, ox, n0);
+      const int jb = D > 1 ? wrapc(b, oy, n1) : 0;
+      const int jc = D > 2 ? wrapc(cz, oz, n2) : 0;
+      const double4 xj = X[(int64_t)ja + (int64_t)n0 * (jb + (int64_t)n1 * jc)];
       const double wj[3] = {xj.x, xj.y, xj.z};
-      double r2 = 0.0;
 #pragma unroll
       for (int q = 0; q < D; ++q) {
         const double d = min_image(__dsub_rn(wi[q], wj[q]), P.box[q], P.periodic);
-        int cc[3] = {sa[0], sa[1], sa[2]};
-        cc[q] = jc3[q];
-        const double4 xa = X[(int64_t)cc[0] + (int64_t)n0 * (cc[1] + (int64_t)n1 * cc[2])];
-        const double wa[3] = {xa.x, xa.y, xa.z};
-        const double e = o[q] == 0 ? 0.0 : min_image(__dsub_rn(wi[q], wa[q]), P.box[q], P.periodic);
-        ok = ok && d == e;
-        r2 = fma(d, d, r2);
+        ok = ok && fabs(d - L.dx[k][q]) <= tol;
       }
-      ok = ok && fabs(r2 - L.r2k[k]) <= tol * L.r2k[k];
     });
   }
   if (!ok) atomicAdd(bad, 1ull);
@@ -371,12 +326,11 @@ extern "C" int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice
 }
 
 extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L,
-                                     int32_t stage, const double* x, const double* b,
-                                     const double* s_in,
+                                     int32_t stage, const double* b, const double* s_in,
                                      const double* s_n, const double* m_n, double* s_out,
                                      double* m_out, double* scalars, int32_t* err,
                                      void* stream) {
-  if (!lattice_args_ok(p, L) || !x || stage < 0 || stage > 2 || p->interior || p->wall_tag ||
+  if (!lattice_args_ok(p, L) || stage < 0 || stage > 2 || p->interior || p->wall_tag ||
       !p->uniform_vol)
     return SPHB_ERR_ARG;
   if (p->nrows == 0) return SPHB_OK;
@@ -392,25 +346,25 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
-  // occupancy target (blocks of 128 per SM): 4 -> 128 registers (default:
-  // no spills at W = 32), 3 -> 168, 5 -> 96; SPHB_LAT_MINB (tuning)
+  // occupancy target (128-thread blocks per SM): 5 -> 96 registers
+  // (default), 4 -> 128, 3 -> 168; SPHB_LAT_MINB (tuning)
   static const int minb = [] {
     const char* e = getenv("SPHB_LAT_MINB");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 5;
   }();
 #define SPHB_S(D, R)                                                                   \
   if (p->dim == D && L->r2 == R) {                                                     \
     switch (minb) {                                                                    \
       case 3: SPHB_S1(D, R, 3);                                                        \
-      case 5: SPHB_S1(D, R, 5);                                                        \
-      default: SPHB_S1(D, R, 4);                                                       \
+      case 4: SPHB_S1(D, R, 4);                                                        \
+      default: SPHB_S1(D, R, 5);                                                       \
     }                                                                                  \
     SPHB_LAUNCH_CHECK();                                                               \
     return SPHB_OK;                                                                    \
   }
 #define SPHB_S1(D, R, MB)                                                              \
-  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, *L, stage, (const double4*)x, b,  \
-                                               Sin, Sn, Mn, Sout, Mout, scalars, err);   \
+  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout,  \
+                                               Mout, scalars, err);                     \
   break
   SPHB_LAT_CASES(SPHB_S)
 #undef SPHB_S

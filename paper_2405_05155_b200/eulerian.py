@@ -451,18 +451,18 @@ class EulerianSolver:
         for k in range(width):
             dx = xw[0] - xw[1 + k]
             dx = np.where(dx > 0.5 * box, dx - box, np.where(dx < -0.5 * box, dx + box, dx))
-            r2 = float(np.sum(dx * dx))
-            r = math.sqrt(r2)
+            r = math.sqrt(float(np.sum(dx * dx)))
             t = 1.0 - 0.5 * r / h
-            dt = -0.25 / (h * r)                    # dt / d(r2)
-            L.r2k[k] = r2
-            L.inv_r[k], L.dinv_r[k] = 1.0 / r, -0.5 / (r * r2)
-            L.g2[k], L.dg2[k] = cg2 * ((t * t) * t), 3.0 * cg2 * t * t * dt
-            L.mv[k], L.dmv[k] = cm * ((t * t) * t), 3.0 * cm * t * t * dt
+            base = (t * t) * t
+            for a in range(d):
+                L.dx[k][a] = float(dx[a])
+            L.inv_r[k] = 1.0 / r
+            L.g2[k] = cg2 * base
+            L.mv[k] = cm * base
         bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
         _lib.call("sphb_wc_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
                   self.X.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
-                  1e-10, bad.data_ptr(), _lib.stream_ptr())
+                  1e-12 * spacing, bad.data_ptr(), _lib.stream_ptr())
         return L if int(bad.item()) == 0 else None
 
     def __new__(cls, *args, **kwargs):
@@ -732,7 +732,9 @@ class EulerianSolver:
             self._stage_boundary_first(stage, s_in, s_n, m_n, s_out, m_out)
             return
         self._set_push(stage, s_out)
-        if self.lattice is not None:
+        # rhs() (stage 0) keeps the reference per-pair geometry of the
+        # general kernel; the steps use the lattice kernel
+        if self.lattice is not None and stage != 0:
             self._stage_lattice(stage, s_in, s_n, m_n, s_out, m_out)
             return
         _lib.call("sphb_wc_stage", ctypes.byref(self.params), stage, self.group,
@@ -744,7 +746,7 @@ class EulerianSolver:
 
     def _stage_lattice(self, stage, s_in, s_n, m_n, s_out, m_out):
         _lib.call("sphb_wc_stage_lattice", ctypes.byref(self.params), ctypes.byref(self.lattice),
-                  stage, self.X.data_ptr(), self.B.data_ptr(), s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(),
+                  stage, self.B.data_ptr(), s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(),
                   s_out.data_ptr(), None if m_out is None else m_out.data_ptr(),
                   self.scalars.data_ptr(), self.err.data_ptr(), _lib.stream_ptr())
 

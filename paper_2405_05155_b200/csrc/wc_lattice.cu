@@ -346,15 +346,20 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
-  // occupancy target (128-thread blocks per SM): 5 -> 96 registers
-  // (default), 4 -> 128, 3 -> 168; SPHB_LAT_MINB (tuning)
-  static const int minb = [] {
+  // occupancy target (128-thread blocks per SM): 5 -> 96 registers,
+  // 4 -> 128, 3 -> 168, 2 -> 255; SPHB_LAT_MINB overrides (tuning)
+  static const int minb_env = [] {
     const char* e = getenv("SPHB_LAT_MINB");
-    return e ? atoi(e) : 5;
+    return e ? atoi(e) : 0;
   }();
+  // measured best on B200 (scripts/ab_lattice.sh, profiles/r02_tune_lattice.md):
+  // the 32-slot stencil runs fastest with 168 registers (more pairs in
+  // flight), the 80-slot one with 96 (occupancy)
+  const int minb = minb_env ? minb_env : (p->dim == 3 && L->r2 == 4 ? 3 : 5);
 #define SPHB_S(D, R)                                                                   \
   if (p->dim == D && L->r2 == R) {                                                     \
     switch (minb) {                                                                    \
+      case 2: SPHB_S1(D, R, 2);                                                        \
       case 3: SPHB_S1(D, R, 3);                                                        \
       case 4: SPHB_S1(D, R, 4);                                                        \
       default: SPHB_S1(D, R, 5);                                                       \

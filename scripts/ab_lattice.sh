@@ -3,7 +3,7 @@
 # vs the lattice kernel at several occupancy targets.  Prints ms/step at
 # 1.6h and 2h for each.
 cd "$(dirname "$0")/.."
-for v in "SPHB_WC_LATTICE=0" "SPHB_LAT_MINB=3" "SPHB_LAT_MINB=4" "SPHB_LAT_MINB=5"; do
+for v in ${AB_VARIANTS:-"SPHB_WC_LATTICE=0" "SPHB_LAT_MINB=2" "SPHB_LAT_MINB=3" "SPHB_LAT_MINB=4" "SPHB_LAT_MINB=5"}; do
   env $v python bench.py --steps 10 --warmup 3 --no-fp32 --no-cpu-baseline > /tmp/ab.json 2>/tmp/ab.err || { echo "$v failed"; tail -5 /tmp/ab.err; continue; }
   python - "$v" <<'PY'
 import json, sys

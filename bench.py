@@ -46,24 +46,34 @@ BYTES_STAGE = {1: 136, 2: 168}
 # the int32 pass list: own X 32 + B 48 + S 32 + cnt 4 read, S 32 written;
 # stage 2 also reads S_n, M_n (64) and writes M (32) — averaged over the two
 IMPL_RECORD_BYTES = 32 + 48 + 32 + 4 + 32 + (64 + 32) / 2.0
+# the lattice kernel reads neither X, cnt nor a pass list: B 48 + S 32 read,
+# S 32 written, stage 2 also S_n, M_n 64 read and M 32 written
+LATTICE_RECORD_BYTES = 48 + 32 + 32 + (64 + 32) / 2.0
 # FP64 flops per directed pair of the fused stage kernel, from the SASS of
 # k_wc_stage<3,1,5> (37 DFMA + 27 DMUL + 13 DADD per pair in the loop body,
 # plus the limiter branch ~3; profiles/r01_ncu_c5_256.md v3)
 FLOPS_PER_PAIR_EST = 117
+# lattice kernel (wc_lattice.cu), FP64 flops per pair from its SASS
+# (DFMA = 2): r2 = 4 stencil (923 DFMA + 467 DMUL + 308 DADD) / 32 slots,
+# r2 = 6 stencil (2387 DFMA + 1139 DMUL + 812 DADD) / 80 slots
+FLOPS_PER_PAIR_LATTICE = {4: 82, 6: 84}
 
 
 def traffic_per_launch(kernel: str):
-    """DRAM bytes per stage launch from the committed ncu capture, if it was
-    taken on this kernel (profiles/r01_traffic.json), else None."""
-    try:
-        with open(os.path.join(REPO, "profiles", "r01_traffic.json")) as f:
-            t = json.load(f)
-    except OSError:
-        return None
-    if t.get("kernel") != kernel:
-        return None
-    s = t["stage_launch"]
-    return s["dram_bytes_read"] + s["dram_bytes_write"]
+    """DRAM bytes per stage launch from a committed ncu capture of this
+    kernel (profiles/r*_traffic.json, newest round first), else None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if t.get("kernel") == kernel:
+            s = t["stage_launch"]
+            return s["dram_bytes_read"] + s["dram_bytes_write"], os.path.basename(path)
+    return None, None
 
 
 def peaks():
@@ -233,7 +243,8 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
               "global": "k_wc_stage<3,%d,%s>" % (solver.group,
                                                  os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
     if solver.lattice is not None:
-        kernel = "k_wc_lattice<3,%d,5>" % solver.lattice.r2
+        kernel = "k_wc_lattice<3,%d,%s>" % (solver.lattice.r2, os.environ.get(
+            "SPHB_LAT_MINB", "3" if solver.lattice.r2 == 4 else "2"))
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None,
             "launches_per_step": launches_per_step}
@@ -479,6 +490,10 @@ def main():
     e2e_ms, io_bytes = e2e_leg(torch, leg["1.6h"]["solver"], max(2, args.steps // 4), 1)
     sv = leg["1.6h"]["solver"]          # this GPU's rows (owned + halo)
     design_bytes = sv.n * (IMPL_RECORD_BYTES + 4.0 * sv.width)
+    flops_pair = FLOPS_PER_PAIR_EST
+    if sv.lattice is not None:
+        design_bytes = sv.n * LATTICE_RECORD_BYTES
+        flops_pair = FLOPS_PER_PAIR_LATTICE[sv.lattice.r2]
     del leg["1.6h"]["solver"], sv
     torch.cuda.empty_cache()
     if not args.no_2h:
@@ -499,7 +514,8 @@ def main():
     alg_bytes = n / world * (BYTES_STAGE[1] + BYTES_STAGE[2]) / 2.0  # per launch, per GPU
     achieved = alg_bytes / (avg_stage_ms * 1e-3) / 1e9
     hbm_peak = float(pk["hbm_gbs"])
-    fp64_ach = L["pairs"] / world * FLOPS_PER_PAIR_EST / (avg_stage_ms * 1e-3) / 1e12
+    traffic = traffic_per_launch(L["kernel"]) if world == 1 else (None, None)
+    fp64_ach = L["pairs"] / world * flops_pair / (avg_stage_ms * 1e-3) / 1e12
 
     line = {
         "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
@@ -511,8 +527,7 @@ def main():
         "gpu_launches": L["launches_per_step"] * K,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
-                     "traffic": traffic_per_launch(L["kernel"]) if world == 1 else None,
-                     "traffic_source": "ncu --set full, profiles/r01_ncu_c5_256.md (v8)",
+                     "traffic": traffic[0], "traffic_source": traffic[1],
                      "kernel": L["kernel"], "peak_kind": pk_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      # what the traffic should be for this design: own records
@@ -524,7 +539,7 @@ def main():
                                   "2": statistics.mean(L["stage_ms"][2])},
                      "fp64": {"achieved_tflops_est": fp64_ach, "peak_tflops_measured": fp64_tf,
                               "frac": fp64_ach / fp64_tf,
-                              "flops_per_pair_est": FLOPS_PER_PAIR_EST}},
+                              "flops_per_pair_est": flops_pair}},
         "clocks": L["clocks"],
         "e2e": {"value": n / (e2e_ms * 1e-3), "unit": "particle-steps/s",
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,

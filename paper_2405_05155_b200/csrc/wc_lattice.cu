@@ -353,9 +353,10 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     return e ? atoi(e) : 0;
   }();
   // measured best on B200 (scripts/ab_lattice.sh, profiles/r02_tune_lattice.md):
-  // the 32-slot stencil runs fastest with 168 registers (more pairs in
-  // flight), the 80-slot one with 96 (occupancy)
-  const int minb = minb_env ? minb_env : (p->dim == 3 && L->r2 == 4 ? 3 : 5);
+  // the 32-slot stencil runs fastest with 168 registers, the 80-slot one
+  // with 224 (more pairs in flight beat occupancy for both)
+  const int minb = minb_env ? minb_env
+                            : (p->dim == 3 ? (L->r2 == 4 ? 3 : 2) : 5);
 #define SPHB_S(D, R)                                                                   \
   if (p->dim == D && L->r2 == R) {                                                     \
     switch (minb) {                                                                    \

@@ -89,7 +89,7 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
   return v;
 }
 
-template <int D, int R2, int MINB, bool BSKIP>
+template <int D, int R2, int MINB>
 __global__ void __launch_bounds__(kLT, MINB)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -164,19 +164,13 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
 #pragma unroll
     for (int q = 0; q < D; ++q)
       if (o[q] != 0) dud = fma(dv[q], dx[q], dud);
+    const double du = dud * inv_r;                   // u_l - u_r (eulerian.py:236-243)
+    double beta = du * eta_c;
+    beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
     const double rbar = fma(0.5, rho_j, hrho_i);
-    double wr = 0.0, p_star = fma(c2, rbar, -c2rho0);   // beta = 0: p* = pbar
-    // the limiter beta = clamp(15 du / c) is 0 unless the pair compresses
-    // (du > 0, eulerian.py:145-157); a warp whose lanes all expand along this
-    // slot skips the limited terms (warp-uniform branch)
-    if (!BSKIP || __any_sync(0xffffffffu, dud > 0.0)) {
-      const double du = dud * inv_r;                 // u_l - u_r (eulerian.py:236-243)
-      double beta = du * eta_c;
-      beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
-      const double bh = beta * hc;
-      wr = ((beta * bh) * (rho_i - rho_j)) * (rcp_nr(rbar) * inv_r);
-      p_star = fma(bh * rbar, du, p_star);
-    }
+    const double bh = beta * hc;
+    const double wr = ((beta * bh) * (rho_i - rho_j)) * (rcp_nr(rbar) * inv_r);
+    const double p_star = fma(bh * rbar, du, fma(c2, rbar, -c2rho0));
     double vs[D];
     double sg = 0.0;
 #pragma unroll
@@ -361,10 +355,6 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   // measured best on B200 (scripts/ab_lattice.sh, profiles/r02_tune_lattice.md):
   // the 32-slot stencil runs fastest with 168 registers, the 80-slot one
   // with 224 (more pairs in flight beat occupancy for both)
-  static const bool bskip = [] {      // SPHB_LAT_BSKIP=0 disables the beta skip
-    const char* e = getenv("SPHB_LAT_BSKIP");
-    return !(e && atoi(e) == 0);
-  }();
   const int minb = minb_env ? minb_env
                             : (p->dim == 3 ? (L->r2 == 4 ? 3 : 2) : 5);
 #define SPHB_S(D, R)                                                                   \
@@ -379,12 +369,8 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     return SPHB_OK;                                                                    \
   }
 #define SPHB_S1(D, R, MB)                                                              \
-  if (bskip)                                                                           \
-    k_wc_lattice<D, R, MB, true><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, \
-                                                       Sout, Mout, scalars, err);       \
-  else                                                                                 \
-    k_wc_lattice<D, R, MB, false><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn,   \
-                                                        Mn, Sout, Mout, scalars, err);  \
+  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout,  \
+                                               Mout, scalars, err);                     \
   break
   SPHB_LAT_CASES(SPHB_S)
 #undef SPHB_S

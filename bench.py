@@ -250,6 +250,51 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
             "launches_per_step": launches_per_step}
 
 
+# compulsory FP64 bytes per particle-step of C4 (TL-SPH):
+# pass A reads X0 24 + v 24 + a 24 + B0 48 + F 72 + x 24, writes v_half,
+# x, F 120; pass B reads X0, F, B0, v_half 168, writes a, v 48
+C4_BYTES_STEP = 552
+
+
+def c4_leg(torch, steps, warmup, peak):
+    """Driver-timed sub-record for BASELINE configs[3] (C4, the 3D TL-SPH
+    twisting column at dp = 1/68, 1,886,592 particles, FP64): ms per KDK
+    step at 1.6h and 2h through SolidSystem.advance (CUDA-graph replay),
+    CUDA events, and the HBM fraction on the compulsory bytes."""
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.tlsph import SolidSystem
+
+    out = {"workload": "c4_column_dp1/68_tl_svk", "unit": "particle-steps/s",
+           "bytes_per_particle_step": C4_BYTES_STEP}
+    for key in ("1.6h", "2h"):
+        cfg = configs.c4_column(kernel=key)
+        s = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
+                        cfl=cfg["cfl"])
+        s.v = cfg["v0"]
+        s.advance(max(warmup, 8))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = max(steps, 16)
+        e0.record()
+        s.advance(k)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        n = s.n
+        pairs = int(s.cnt.sum().item())
+        rec = {"ms_per_step": ms, "value": n / (ms * 1e-3), "particles": n,
+               "pair_interactions_per_s": 2 * pairs / (ms * 1e-3), "steps": k}
+        if key == "1.6h":
+            gbs = C4_BYTES_STEP * n / (ms * 1e-3) / 1e9
+            rec["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                               "frac": gbs / peak}
+        out[key.replace(".", "p")] = rec
+        del s
+        torch.cuda.empty_cache()
+    out["alpha_T1p6h_over_T2h"] = out["1p6h"]["ms_per_step"] / out["2h"]["ms_per_step"]
+    return out
+
+
 def e2e_leg(torch, solver, steps, warmup):
     """Through the public API with host buffers: every step uploads the state
     from pinned host memory (EulerianSolver.load_state), advances one step and
@@ -435,6 +480,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-2h", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (TL-SPH) sub-record")
     ap.add_argument("--no-numba", action="store_true",
                     help="reference arm: skip the single-core sph_trunc (numba) figure")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
@@ -501,6 +547,9 @@ def main():
         leg["2h"] = run_leg(torch, cfg2, args.steps, max(3, args.warmup), dist, world)
         del leg["2h"]["solver"]
         torch.cuda.empty_cache()
+    c4 = None
+    if world == 1 and not args.no_c4:
+        c4 = c4_leg(torch, args.steps, args.warmup, float(peaks()[0]["hbm_gbs"]))
     f32 = None
     if world == 1 and not args.no_fp32:
         f32 = fp32_leg(torch, cfg, args.steps, max(3, args.warmup))
@@ -561,6 +610,8 @@ def main():
             "pair_interactions_per_s": S["pairs"] * 2 * K / (S["ms"] * 1e-3),
             "pairs_per_pass": S["pairs"]}
         line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
+    if c4 is not None:
+        line["c4_column"] = c4
     if f32 is not None:
         line["fp32_mode"] = dict(f32, unit="particle-steps/s", kernel="k_wc_stage_f32<3>",
                                  note="FP32 pair math, FP64 accumulation/state; reported "

@@ -517,6 +517,13 @@ typedef struct sphb_tl_params {
    * one row touches consecutive records; q_stride >= n, 0 means n.  Slab
    * ranks use one common stride so pushes address peer buffers with it. */
   int64_t q_stride;
+  /* Row list (lattice split, tlsph.py SolidSystem): when non-NULL, the pass
+   * kernels update rows[t] for t in [0, nrows) instead of [row0, row0 +
+   * nrows) (no pass-list staging).  no_kick: 1 = sphb_tl_pass_a skips the
+   * first kick (the caller ran sphb_tl_kick). */
+  const int32_t* rows;
+  int32_t no_kick;
+  int32_t reserved_tl;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows
@@ -542,6 +549,46 @@ int sphb_tl_geometry(const sphb_grid* g, int64_t n, const double* wrapped_sorted
  * pass A writes it), which pass B reads instead of gathering X0_j. */
 int sphb_tl_stress(const sphb_tl_params* p, const double* F, const double* B0,
                    const double* X0, double* Q, void* stream);
+/* The first kick alone, Vh = v + dt/2 a (0 when clamped) for all n rows. */
+int sphb_tl_kick(const sphb_tl_params* p, const double* V, const double* A, double* Vh,
+                 const double* scalars, void* stream);
+
+/* Lattice fast path of the TL passes (csrc/tl_lattice.cu) for a reference
+ * configuration that is a complete box lattice in engine order (axis 0
+ * fastest) with separable coordinates: rows of the interior sub-box
+ * [R, n_a - R) (R = isqrt(r2)) all hold the canonical offsets 0 < |o|^2 <=
+ * r2 (order: axis 2 slowest), so j = i + o_k is computed, the exact
+ * displacement's axis-q component is the row's difference to its neighbour
+ * along axis q alone (computed once per row), and g0 = f(r2) dx with f =
+ * c5v t^3 (tlsph.py:145-146) is a first-order expansion about r2k[k].
+ * Shell rows run the general passes with a row list.  Supported (dim, r2):
+ * (2, 3), (2, 5), (3, 3), (3, 5) — 1.6h / 2h at h = 1.15 dp. */
+#define SPHB_TL_LATTICE_MAXW 56
+typedef struct sphb_tl_lattice {
+  int32_t width;         /* slots per interior row                          */
+  int32_t r2;
+  int32_t n[3];          /* lattice extents, 1 for unused axes              */
+  int32_t reserved;
+  int64_t n_interior;    /* prod(n_a - 2R) over the dim axes                */
+  double r2k[SPHB_TL_LATTICE_MAXW];
+  double f[SPHB_TL_LATTICE_MAXW], df[SPHB_TL_LATTICE_MAXW];
+} sphb_tl_lattice;
+int sphb_tl_lattice_width(int32_t dim, int32_t r2);
+/* Interior rows whose pass-list row is not exactly the canonical set, whose
+ * exact displacements (X0 records) are not separable per axis (bitwise), or
+ * whose pair r2 is off r2k by more than tol (relative): counted into *bad. */
+int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
+                          const int32_t* nbr, const int32_t* cnt, double tol,
+                          unsigned long long* bad, void* stream);
+/* Passes A / B (no kick) over the interior rows; same records and contract
+ * as sphb_tl_pass_a / sphb_tl_pass_b. */
+int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
+                           const double* B0, const double* Vh, double* XC, double* F,
+                           double* Q, const double* scalars, int32_t* err, void* stream);
+int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
+                           const double* Q, const double* Vh, double* A, double* V,
+                           double* scalars, int32_t update_v, int32_t* err, void* stream);
+
 /* max |v| into scalars[2] (stable_dt). */
 int sphb_tl_speed_max(const sphb_tl_params* p, const double* V, double* scalars,
                       void* stream);

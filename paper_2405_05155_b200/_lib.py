@@ -145,6 +145,9 @@ class TLParams(C.Structure):
         ("push_hi1", C.c_int64),
         ("push_next_at", C.c_int64),
         ("q_stride", C.c_int64),
+        ("rows", C.c_void_p),
+        ("no_kick", C.c_int32),
+        ("reserved_tl", C.c_int32),
     ]
 
 
@@ -163,6 +166,24 @@ class Lattice(C.Structure):
         ("inv_r", C.c_double * LATTICE_MAXW),
         ("g2", C.c_double * LATTICE_MAXW),
         ("mv", C.c_double * LATTICE_MAXW),
+    ]
+
+
+TL_LATTICE_MAXW = 56
+
+
+class TLLattice(C.Structure):
+    """sphb_tl_lattice: extents and per-slot g0 expansion of the TL lattice path."""
+
+    _fields_ = [
+        ("width", C.c_int32),
+        ("r2", C.c_int32),
+        ("n", C.c_int32 * 3),
+        ("reserved", C.c_int32),
+        ("n_interior", C.c_int64),
+        ("r2k", C.c_double * TL_LATTICE_MAXW),
+        ("f", C.c_double * TL_LATTICE_MAXW),
+        ("df", C.c_double * TL_LATTICE_MAXW),
     ]
 
 
@@ -200,6 +221,11 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_lattice_width": (C.c_int, [I32, I32]),
+    "sphb_tl_kick": (C.c_int, [P, P, P, P, P, P]),
+    "sphb_tl_lattice_width": (C.c_int, [I32, I32]),
+    "sphb_tl_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
+    "sphb_tl_pass_a_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_tl_pass_b_lattice": (C.c_int, [P, P, P, P, P, P, P, P, I32, P, P]),
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),

@@ -1,0 +1,415 @@
+// tl_lattice.cu — TL-SPH passes A / B on the interior of a lattice body.
+//
+// The same passes as k_tl_pass_a / k_tl_pass_b (tl_engine.cu; reference
+// tlsph.py:88-123, 182-206) for the rows of a reference configuration that
+// is a complete box lattice (the C3 plate, the C4 column) whose stencil is
+// complete, i.e. the interior sub-box [R, n_a - R):
+//   * the neighbour index is computed, j = i + o_k, with the canonical
+//     offsets 0 < |o|^2 <= R2 (z, y, x ascending) compile-time constants —
+//     no pass list is read;
+//   * the exact displacement x_i - x_j (X0 records, the reference's
+//     w = X0 - min arithmetic) is separable on a lattice: its axis-q
+//     component is the row's difference to its neighbour along axis q
+//     alone, computed once per row (2R values per axis); components with
+//     o_q = 0 are exact zeros, known at compile time;
+//   * g0_ij = f(r2) dx with f = c5v t^3, t = 1 - r / (2h) (tlsph.py:145-146,
+//     correction.py:89-112) from a first-order expansion of f about the
+//     slot's r2 (the rows' r2 differ from it by ~1e-14 relative; the
+//     second-order term is ~1e-28 relative), replacing the X0_j gather,
+//     the reciprocal square root and the t^3 chain.
+// sphb_tl_lattice_check proves all of it for every interior row before the
+// path is used: pass-list row == canonical set, bitwise separability, and
+// |r2 - r2k| <= tol r2k.  Shell rows run the general kernels (row list).
+#include <stdlib.h>
+
+#include <type_traits>
+#include <utility>
+
+#include "tl_common.cuh"
+
+using namespace sphb;
+using namespace sphb::tl;
+
+namespace {
+
+constexpr int kTT = 128;
+
+struct OffList {
+  int n;
+  int o[SPHB_TL_LATTICE_MAXW][3];
+};
+
+constexpr int isqrt_c(int v) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+template <int D, int R2>
+constexpr OffList make_offsets() {
+  OffList L{};
+  const int R = isqrt_c(R2);
+  const int rz = D > 2 ? R : 0, ry = D > 1 ? R : 0;
+  for (int z = -rz; z <= rz; ++z)
+    for (int y = -ry; y <= ry; ++y)
+      for (int x = -R; x <= R; ++x) {
+        const int q = x * x + y * y + z * z;
+        if (q == 0 || q > R2) continue;
+        L.o[L.n][0] = x;
+        L.o[L.n][1] = y;
+        L.o[L.n][2] = z;
+        ++L.n;
+      }
+  return L;
+}
+
+template <int D, int R2>
+struct Stencil {
+  static constexpr OffList L = make_offsets<D, R2>();
+  static constexpr int W = L.n;
+  static constexpr int R = isqrt_c(R2);
+};
+
+template <class F, int... Is>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int K, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, K>{});
+}
+
+// Interior row of thread t: lattice coordinates (a, b, c) in [R, n_a - R).
+template <int D, int R>
+struct Row {
+  int64_t i;
+  int stride[3];     // index steps along the axes
+  __device__ __forceinline__ Row(const sphb_tl_lattice& L, int64_t t) {
+    const int m0 = L.n[0] - 2 * R;
+    const int m1 = D > 1 ? L.n[1] - 2 * R : 1;
+    const int a = R + (int)(t % m0);
+    const int64_t u = t / m0;
+    const int b = D > 1 ? R + (int)(u % m1) : 0;
+    const int c = D > 2 ? R + (int)(u / m1) : 0;
+    stride[0] = 1;
+    stride[1] = L.n[0];
+    stride[2] = L.n[0] * L.n[1];
+    i = (int64_t)a + (int64_t)stride[1] * b + (int64_t)stride[2] * c;
+  }
+};
+
+// Exact axis displacements to the axis neighbours: dxs[q][s + R], s != 0
+template <int D, int R>
+__device__ __forceinline__ void axis_displacements(const double4* __restrict__ X0,
+                                                   const Row<D, R>& row, const double (&wi)[D],
+                                                   double (&dxs)[D][2 * R + 1]) {
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+#pragma unroll
+    for (int s = -R; s <= R; ++s) {
+      double d = 0.0;
+      if (s != 0) {
+        const double wj = __ldg(reinterpret_cast<const double*>(
+                                    X0 + row.i + (int64_t)s * row.stride[q]) + q);
+        d = wi[q] - wj;
+      }
+      dxs[q][s + R] = d;
+    }
+}
+
+template <int D, int R2, int MINB>
+__global__ void __launch_bounds__(kTT, MINB)
+k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
+               const double4* __restrict__ X0, const double4* __restrict__ B0,
+               const double4* __restrict__ Vh, double4* __restrict__ XC,
+               double4* __restrict__ F, double4* __restrict__ Q,
+               const double* __restrict__ scalars, int32_t* __restrict__ err) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
+  if (t >= L.n_interior) return;
+  const Row<D, R> row(L, t);
+  const int64_t i = row.i;
+  const double dt = scalars[0];
+  double wi[D], vhi[D];
+  bool fixed_i;
+  load_x0<D>(X0, i, wi, fixed_i);
+  load_vec<D>(Vh, i, vhi);
+  double dxs[D][2 * R + 1];
+  axis_displacements<D, R>(X0, row, wi, dxs);
+  double m[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+    const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                      (int64_t)o[2] * row.stride[2];
+    double vhj[D];
+    load_vec_nc<D>(Vh, j, vhj);
+    double dx[D];
+    double r2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      dx[q] = o[q] == 0 ? 0.0 : dxs[q][o[q] + R];
+      if (o[q] != 0) r2 = fma(dx[q], dx[q], r2);
+    }
+    const double f = fma(L.df[k], r2 - L.r2k[k], L.f[k]);    // g0 = f dx
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double dvf = (vhj[a] - vhi[a]) * f;
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        if (o[b] != 0) m[a][b] = fma(dvf, dx[b], m[a][b]);
+    }
+  });
+  tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+}
+
+template <int D, int R2, int MINB>
+__global__ void __launch_bounds__(kTT, MINB)
+k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
+               const double4* __restrict__ X0, const double4* __restrict__ Q,
+               const double4* __restrict__ Vh, double4* __restrict__ A,
+               double4* __restrict__ V, double* __restrict__ scalars, int update_v) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
+  double speed = 0.0;
+  if (t < L.n_interior) {
+    const Row<D, R> row(L, t);
+    const int64_t i = row.i;
+    const int64_t qs = P.q_stride ? P.q_stride : P.n;
+    double wi[D];
+    bool fixed_i;
+    load_x0<D>(X0, i, wi, fixed_i);
+    double dxs[D][2 * R + 1];
+    axis_displacements<D, R>(X0, row, wi, dxs);
+    double gsum[D], acc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) gsum[a] = acc[a] = 0.0;
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      double Qj[D][D];
+      if constexpr (D == 3) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double4 t4 = ldg4(Q + r * qs + j);
+          Qj[r][0] = t4.x; Qj[r][1] = t4.y; Qj[r][2] = t4.z;
+        }
+      } else {
+        load_mat_nc<D>(Q, j, Qj);
+      }
+      double dx[D];
+      double r2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        dx[q] = o[q] == 0 ? 0.0 : dxs[q][o[q] + R];
+        if (o[q] != 0) r2 = fma(dx[q], dx[q], r2);
+      }
+      const double f = fma(L.df[k], r2 - L.r2k[k], L.f[k]);
+      double g[D];
+#pragma unroll
+      for (int b = 0; b < D; ++b) g[b] = o[b] == 0 ? 0.0 : f * dx[b];
+      // sum_j (Q_i + Q_j) g = Q_i sum_j g + sum_j Q_j g (tlsph.py:88-102)
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        if (o[b] != 0) gsum[b] += g[b];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (o[b] != 0) acc[a] = fma(Qj[a][b], g[b], acc[a]);
+    });
+    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
+  }
+  tl_block_speed_max<kTT>(speed, scalars);
+}
+
+// Proof of the specialisation for every interior row (see the file header).
+template <int D, int R2>
+__global__ void k_tl_lattice_check(const sphb_tl_params P, const sphb_tl_lattice L,
+                                   const double4* __restrict__ X0,
+                                   const int32_t* __restrict__ nbr,
+                                   const int32_t* __restrict__ cnt, double tol,
+                                   unsigned long long* bad) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  constexpr int SIDE = 2 * R + 1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L.n_interior) return;
+  const Row<D, R> row(L, t);
+  const int64_t i = row.i, n = P.n;
+  const int n0 = L.n[0], n1 = L.n[1];
+  const int ii = (int)i;
+  const int a = ii % n0, tt = ii / n0;
+  const int b = D > 1 ? tt % n1 : 0, cz = D > 2 ? tt / n1 : 0;
+  bool ok = cnt[i] == St::W;
+  int slot[SIDE * SIDE * SIDE];
+#pragma unroll
+  for (int q = 0; q < SIDE * SIDE * SIDE; ++q) slot[q] = -1;
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int q = (St::L.o[k][0] + R) + SIDE * ((St::L.o[k][1] + R) + SIDE * (St::L.o[k][2] + R));
+    slot[q] = k;
+  });
+  unsigned long long seen = 0ull;
+  const int w = ok ? St::W : 0;
+  for (int e = 0; e < w; ++e) {
+    const int j = nbr[(int64_t)e * n + i];
+    const int ja = j % n0, jt = j / n0;
+    const int jb = D > 1 ? jt % n1 : 0, jc = D > 2 ? jt / n1 : 0;
+    const int o[3] = {ja - a, jb - b, jc - cz};
+    bool in = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) in = in && o[q] >= -R && o[q] <= R;
+    const int k = in ? slot[(o[0] + R) + SIDE * ((o[1] + R) + SIDE * (o[2] + R))] : -1;
+    if (k < 0) { ok = false; break; }
+    seen |= 1ull << k;
+  }
+  if (ok) ok = __popcll(seen) == St::W;
+  if (ok) {
+    const double4 xi = X0[i];
+    const double wi[3] = {xi.x, xi.y, xi.z};
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      const double4 xj = X0[j];
+      const double wj[3] = {xj.x, xj.y, xj.z};
+      double r2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const double d = __dsub_rn(wi[q], wj[q]);
+        const double4 xa = X0[i + (int64_t)o[q] * row.stride[q]];
+        const double wa[3] = {xa.x, xa.y, xa.z};
+        const double e = o[q] == 0 ? 0.0 : __dsub_rn(wi[q], wa[q]);
+        ok = ok && d == e;
+        r2 = fma(d, d, r2);
+      }
+      ok = ok && fabs(r2 - L.r2k[k]) <= tol * L.r2k[k];
+    });
+  }
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+}  // namespace
+
+#define SPHB_TLAT_CASES(X) X(2, 3) X(2, 5) X(3, 3) X(3, 5)
+
+extern "C" int sphb_tl_lattice_width(int32_t dim, int32_t r2) {
+#define SPHB_W(D, R) if (dim == D && r2 == R) return Stencil<D, R>::W;
+  SPHB_TLAT_CASES(SPHB_W)
+#undef SPHB_W
+  return 0;
+}
+
+static bool tl_lattice_ok(const sphb_tl_params* p, const sphb_tl_lattice* L) {
+  if (!p || !L || p->n <= 0 || p->n >= (int64_t)1 << 31) return false;
+  const int R = isqrt_c(L->r2);
+  int64_t prod = 1, inner = 1;
+  for (int q = 0; q < 3; ++q) {
+    if (L->n[q] < 1 || (q >= p->dim && L->n[q] != 1)) return false;
+    prod *= L->n[q];
+    if (q < p->dim) {
+      if (L->n[q] <= 2 * R) return false;
+      inner *= L->n[q] - 2 * R;
+    }
+  }
+  return prod == p->n && inner == L->n_interior &&
+         sphb_tl_lattice_width(p->dim, L->r2) == L->width;
+}
+
+extern "C" int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_lattice* L,
+                                     const double* x0, const int32_t* nbr, const int32_t* cnt,
+                                     double tol, unsigned long long* bad, void* stream) {
+  if (!tl_lattice_ok(p, L) || !x0 || !nbr || !cnt || !bad) return SPHB_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(L->n_interior, 128);
+#define SPHB_C(D, R)                                                                        \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    k_tl_lattice_check<D, R><<<grid, 128, 0, st>>>(*p, *L, (const double4*)x0, nbr, cnt,    \
+                                                    tol, bad);                              \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+  SPHB_TLAT_CASES(SPHB_C)
+#undef SPHB_C
+  return SPHB_ERR_ARG;
+}
+
+// occupancy targets (128-thread blocks per SM; SPHB_TLAT_MINB_A / _B override)
+static int tl_minb(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L,
+                                      const double* x0, const double* b0, const double* vh,
+                                      double* xc, double* f, double* q, const double* scalars,
+                                      int32_t* err, void* stream) {
+  if (!tl_lattice_ok(p, L) || !x0 || !b0 || !vh || !xc || !f || !q) return SPHB_ERR_ARG;
+  if (L->n_interior == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  static const int minb = tl_minb("SPHB_TLAT_MINB_A", 4);
+  const unsigned grid = sphb_blocks(L->n_interior, kTT);
+#define SPHB_A1(D, R, MB)                                                                   \
+  k_tl_lattice_a<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,                \
+      (const double4*)b0, (const double4*)vh, (double4*)xc, (double4*)f, (double4*)q,       \
+      scalars, err);                                                                        \
+  break
+#define SPHB_A(D, R)                                                                        \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    switch (minb) {                                                                         \
+      case 2: SPHB_A1(D, R, 2);                                                             \
+      case 3: SPHB_A1(D, R, 3);                                                             \
+      case 5: SPHB_A1(D, R, 5);                                                             \
+      default: SPHB_A1(D, R, 4);                                                            \
+    }                                                                                       \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+  SPHB_TLAT_CASES(SPHB_A)
+#undef SPHB_A
+#undef SPHB_A1
+  return SPHB_ERR_ARG;
+}
+
+extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L,
+                                      const double* x0, const double* q, const double* vh,
+                                      double* a, double* v, double* scalars, int32_t update_v,
+                                      int32_t* err, void* stream) {
+  (void)err;
+  if (!tl_lattice_ok(p, L) || !x0 || !q || !vh || !a || !v || !scalars) return SPHB_ERR_ARG;
+  if (L->n_interior == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  static const int minb = tl_minb("SPHB_TLAT_MINB_B", 4);
+  const unsigned grid = sphb_blocks(L->n_interior, kTT);
+#define SPHB_B1(D, R, MB)                                                                   \
+  k_tl_lattice_b<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,                \
+      (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,             \
+      (int)update_v);                                                                       \
+  break
+#define SPHB_B(D, R)                                                                        \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    switch (minb) {                                                                         \
+      case 2: SPHB_B1(D, R, 2);                                                             \
+      case 3: SPHB_B1(D, R, 3);                                                             \
+      case 5: SPHB_B1(D, R, 5);                                                             \
+      default: SPHB_B1(D, R, 4);                                                            \
+    }                                                                                       \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+  SPHB_TLAT_CASES(SPHB_B)
+#undef SPHB_B
+#undef SPHB_B1
+  return SPHB_ERR_ARG;
+}

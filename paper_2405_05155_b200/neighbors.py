@@ -291,7 +291,11 @@ def engine_order(bins: CellBins, nbr, cnt, width: int, spacing: float | None = N
         ext = ([g.box[a] for a in range(d)] if g.periodic
                else [max(float(ws[a].max().item()), 1e-300) for a in range(d)])
         spacing = float(np.prod(ext) / n) ** (1.0 / d)
-    k = torch.floor(ws * (1.0 / spacing)).to(torch.int64).clamp_(min=0)
+    # lattice key: a periodic lattice sits at cell centres ((k + 1/2) spacing
+    # of the wrapped coordinate); an open one starts at 0 (w = x - min, a
+    # multiple of the spacing up to rounding), so round instead of floor
+    shift = 0.0 if g.periodic else 0.5
+    k = torch.floor(ws * (1.0 / spacing) + shift).to(torch.int64).clamp_(min=0)
     if tile is None:
         env = os.environ.get("SPHB_ENGINE_TILE", "")
         tile = tuple(int(v) for v in env.split("x")) if env else ()

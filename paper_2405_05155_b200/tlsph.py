@@ -22,6 +22,7 @@ counterpart.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 from dataclasses import dataclass
 
@@ -293,6 +294,10 @@ class SolidSystem:
                       self.cnt.data_ptr(), self.width, ctypes.byref(k), self.dp**d,
                       self.g0.data_ptr(), _lib.stream_ptr())
         self._g0_ptr = None if self.g0 is None else self.g0.data_ptr()
+        self.lattice = None
+        if (_slab is None and self.g0 is None and self.order is not self.bins
+                and os.environ.get("SPHB_TL_LATTICE", "1") != "0"):
+            self._setup_lattice()
         self._setup_push(dev)
         self._acc_valid = False
         self._host = {}
@@ -354,15 +359,94 @@ class SolidSystem:
         s = pk2_stress(self.F, self.material)
         return np.einsum("nab,nbc->nac", self.F, s), s
 
+    def _setup_lattice(self):
+        """Lattice fast path (csrc/tl_lattice.cu) when the reference
+        configuration is a complete box lattice in engine order: the interior
+        rows (full stencil) run the lattice passes, the shell rows the
+        general ones through a row list.  Needs sphb_tl_lattice_check to
+        prove every interior row (pass-list set, bitwise separable
+        displacements, r2 near the slot's expansion point)."""
+        torch = _lib.torch_cuda()
+        d, n, dp = self.dim, self.n, self.dp
+        if d not in (2, 3) or n == 0 or int(self.grid.slow_axis) != d - 1 or n >= 2**31:
+            return
+        w = self.X0rec[:, :d]
+        lo, hi = w.min(dim=0).values.cpu().numpy(), w.max(dim=0).values.cpu().numpy()
+        ext = [int(round((hi[a] - lo[a]) / dp)) + 1 for a in range(d)]
+        if int(np.prod(ext)) != n:
+            return
+        r2 = int(math.floor((self.grid.cutoff / dp) ** 2 * (1.0 + 1e-12)))
+        lib = _lib.lib()
+        width = int(lib.sphb_tl_lattice_width(d, r2))
+        R = math.isqrt(r2)
+        if width == 0 or width != self.width or min(ext) <= 2 * R:
+            return
+        offs = [(x, y, z) for z in (range(-R, R + 1) if d > 2 else [0])
+                for y in range(-R, R + 1) for x in range(-R, R + 1)
+                if 0 < x * x + y * y + z * z <= r2]
+        L = _lib.TLLattice()
+        L.width, L.r2 = width, r2
+        for a in range(3):
+            L.n[a] = ext[a] if a < d else 1
+        L.n_interior = int(np.prod([e - 2 * R for e in ext]))
+        stride = [1, ext[0], ext[0] * (ext[1] if d > 1 else 1)]
+        rep = [e // 2 for e in ext] + [0] * (3 - d)
+        irep = sum(rep[a] * stride[a] for a in range(3))
+        rows = [irep] + [irep + sum(o[a] * stride[a] for a in range(3)) for o in offs]
+        xw = self.X0rec[torch.tensor(rows, device=self._dev), :d].cpu().numpy()
+        h = self.kernel.h
+        c5v = -5.0 * (self.kernel.alpha / h * dp**d) / h      # tl_engine.cu ref_gradient
+        for k in range(width):
+            dx = xw[0] - xw[1 + k]
+            r2k = float(np.sum(dx * dx))
+            r = math.sqrt(r2k)
+            t = 1.0 - 0.5 * r / h
+            L.r2k[k] = r2k
+            L.f[k] = c5v * ((t * t) * t)
+            L.df[k] = 3.0 * c5v * t * t * (-0.25 / (h * r))
+        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
+        _lib.call("sphb_tl_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
+                  self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), 1e-10,
+                  bad.data_ptr(), _lib.stream_ptr())
+        if int(bad.item()):
+            return
+        idx = torch.arange(n, device=self._dev)
+        coord = [idx % ext[0], (idx // ext[0]) % ext[1] if d > 1 else None,
+                 idx // (ext[0] * ext[1]) if d > 2 else None]
+        inner = torch.ones(n, dtype=torch.bool, device=self._dev)
+        for a in range(d):
+            inner &= (coord[a] >= R) & (coord[a] < ext[a] - R)
+        self._shell = torch.nonzero(~inner).flatten().to(torch.int32).contiguous()
+        ps = _lib.TLParams.from_buffer_copy(self.params)     # copy, then the row list
+        ps.rows, ps.nrows, ps.no_kick = self._shell.data_ptr(), int(self._shell.numel()), 1
+        self._params_shell = ps
+        self.lattice = L
+
+    def _pass_b(self, update_v):
+        st = _lib.stream_ptr()
+        if self.lattice is not None:
+            _lib.call("sphb_tl_pass_b_lattice", ctypes.byref(self.params),
+                      ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.Qrec.data_ptr(),
+                      self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
+                      self.scalars.data_ptr(), update_v, self.err.data_ptr(), st)
+            if self._params_shell.nrows:
+                _lib.call("sphb_tl_pass_b", ctypes.byref(self._params_shell),
+                          self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                          None, self.Qrec.data_ptr(), self.Vh.data_ptr(), self.A.data_ptr(),
+                          self.V.data_ptr(), self.scalars.data_ptr(), update_v,
+                          self.err.data_ptr(), st)
+            return
+        _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
+                  self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
+                  self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
+                  self.scalars.data_ptr(), update_v, self.err.data_ptr(), st)
+
     def _accelerations_dev(self):
         st = _lib.stream_ptr()
         _lib.call("sphb_tl_stress", ctypes.byref(self.params), self.Frec.data_ptr(),
                   self.B0rec.data_ptr(), self.X0rec.data_ptr(), self.Qrec.data_ptr(), st)
         self._halo(*self._q_halo)
-        _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
-                  self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
-                  self.scalars.data_ptr(), 0, self.err.data_ptr(), st)
+        self._pass_b(0)
         self._halo(self.A)
         self._acc_valid = True
 
@@ -452,19 +536,32 @@ class SolidSystem:
         self._set_push(True)
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
-        _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr,
-                  self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
-                  self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
-                  self.err.data_ptr(), st)
+        if self.lattice is not None:
+            # kick, lattice pass A (interior) + general pass A (shell rows)
+            _lib.call("sphb_tl_kick", ctypes.byref(self.params), self.V.data_ptr(),
+                      self.A.data_ptr(), self.Vh.data_ptr(), self.scalars.data_ptr(), st)
+            _lib.call("sphb_tl_pass_a_lattice", ctypes.byref(self.params),
+                      ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.B0rec.data_ptr(),
+                      self.Vh.data_ptr(), self.XC.data_ptr(), self.Frec.data_ptr(),
+                      self.Qrec.data_ptr(), self.scalars.data_ptr(), self.err.data_ptr(), st)
+            if self._params_shell.nrows:
+                _lib.call("sphb_tl_pass_a", ctypes.byref(self._params_shell),
+                          self.X0rec.data_ptr(), self.B0rec.data_ptr(), self.nbr.data_ptr(),
+                          self.cnt.data_ptr(), None, self.V.data_ptr(), self.A.data_ptr(),
+                          self.Vh.data_ptr(), self.XC.data_ptr(), self.Frec.data_ptr(),
+                          self.Qrec.data_ptr(), self.scalars.data_ptr(), self.err.data_ptr(),
+                          st)
+        else:
+            _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
+                      self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
+                      self._g0_ptr, self.V.data_ptr(), self.A.data_ptr(), self.Vh.data_ptr(),
+                      self.XC.data_ptr(), self.Frec.data_ptr(), self.Qrec.data_ptr(),
+                      self.scalars.data_ptr(), self.err.data_ptr(), st)
         if self._push is not None:                  # Q halos were pushed by pass A
             self._dist.all_reduce(self._push_token)
         else:
             self._halo(*self._q_halo)
-        _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
-                  self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
-                  self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
-                  self.scalars.data_ptr(), 1, self.err.data_ptr(), st)
+        self._pass_b(1)
         self._set_push(False)
         if self._push is None:                      # else pushed; the max orders them
             self._halo(self.V, self.A)

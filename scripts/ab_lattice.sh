@@ -4,7 +4,7 @@
 # 1.6h and 2h for each.
 cd "$(dirname "$0")/.."
 for v in ${AB_VARIANTS:-"SPHB_WC_LATTICE=0" "SPHB_LAT_MINB=2" "SPHB_LAT_MINB=3" "SPHB_LAT_MINB=4" "SPHB_LAT_MINB=5"}; do
-  env $v python bench.py --steps 10 --warmup 3 --no-fp32 --no-cpu-baseline > /tmp/ab.json 2>/tmp/ab.err || { echo "$v failed"; tail -5 /tmp/ab.err; continue; }
+  env $v python bench.py --steps 10 --warmup 3 --no-fp32 --no-c4 --no-cpu-baseline > /tmp/ab.json 2>/tmp/ab.err || { echo "$v failed"; tail -5 /tmp/ab.err; continue; }
   python - "$v" <<'PY'
 import json, sys
 d = json.loads(open("/tmp/ab.json").read().strip().splitlines()[-1])

@@ -7,7 +7,7 @@ set -e
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 cat gpurun_out/bench.json
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-2h --no-fp32"
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-2h --no-fp32 --no-c4"
 $CMD > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
     --log-file gpurun_out/launches_c5_256.csv $CMD > /dev/null 2>&1

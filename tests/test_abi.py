@@ -55,6 +55,8 @@ def test_structs_match_header_layout(tmp_path):
         "sphb_kernel": (_lib.Kernel, ["code", "dim", "h", "alpha", "kappa"]),
         "sphb_wc_params": (_lib.WCParams, [f for f, _ in _lib.WCParams._fields_]),
         "sphb_tl_params": (_lib.TLParams, [f for f, _ in _lib.TLParams._fields_]),
+        "sphb_lattice": (_lib.Lattice, [f for f, _ in _lib.Lattice._fields_]),
+        "sphb_tl_lattice": (_lib.TLLattice, [f for f, _ in _lib.TLLattice._fields_]),
     }
     lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "sphb.h"', "int main(void){"]
     for cname, (_, fields) in checks.items():

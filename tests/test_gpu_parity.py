@@ -883,3 +883,36 @@ def test_wc_lattice_check_rejects_perturbed_sets():
     s.step()
     ref.step()
     assert l2_error(s.state.mom, ref.mom) < 1e-12
+
+
+# ------------------------------------------------ TL lattice path (tl_lattice.cu)
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+@pytest.mark.parametrize("label,builder,kwargs", [("c3", configs.c3_plate, {"dp": 0.004}),
+                                                  ("c4", configs.c4_column, {"n_width": 8})])
+def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwargs):
+    """Plate and column run the TL lattice passes on their interior rows
+    (checked) and the general passes on the shell; fields match the general
+    kernels and the oracle."""
+    cfg = builder(kernel=key, **kwargs)
+    fast = make_tl(cfg)
+    assert fast.lattice is not None and fast._shell.numel() > 0
+    monkeypatch.setenv("SPHB_TL_LATTICE", "0")
+    gen = make_tl(cfg)
+    assert gen.lattice is None
+    m = cfg["material"]
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"])
+    ref.v = cfg["v0"].copy()
+    for s in (fast, gen):
+        s.step()
+    ref.step()
+    for s in (fast, gen):
+        errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
+        assert max(errs) < TOL_1, errs
+    fast.advance(49)
+    gen.advance(49)
+    for _ in range(49):
+        ref.step()
+    for s in (fast, gen):
+        errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
+        assert max(errs) < 1e-10, errs

@@ -512,18 +512,11 @@ typedef struct sphb_tl_params {
   double* push_v_next;
   int64_t push_lo0, push_lo1, push_prev_at;
   int64_t push_hi0, push_hi1, push_next_at;
-  /* 3D Q records are three row planes Q[r * q_stride + i] (one 32-byte
-   * {q_r0, q_r1, q_r2, X0_r} per plane and particle), so a warp's gather of
+  /* 3D Q records are three column planes Q[c * q_stride + i] (one 32-byte
+   * {q_0c, q_1c, q_2c, X0_c} per plane and particle), so a warp's gather of
    * one row touches consecutive records; q_stride >= n, 0 means n.  Slab
    * ranks use one common stride so pushes address peer buffers with it. */
   int64_t q_stride;
-  /* Row list (lattice split, tlsph.py SolidSystem): when non-NULL, the pass
-   * kernels update rows[t] for t in [0, nrows) instead of [row0, row0 +
-   * nrows) (no pass-list staging).  no_kick: 1 = sphb_tl_pass_a skips the
-   * first kick (the caller ran sphb_tl_kick). */
-  const int32_t* rows;
-  int32_t no_kick;
-  int32_t reserved_tl;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows
@@ -570,6 +563,10 @@ typedef struct sphb_tl_lattice {
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
   int32_t reserved;
   int64_t n_interior;    /* prod(n_a - 2R) over the dim axes                */
+  /* the remaining (shell) rows, run in the same launches with the general
+   * per-pair geometry and the pass list (nbr, cnt) */
+  const int32_t* shell;
+  int64_t n_shell;
   double r2k[SPHB_TL_LATTICE_MAXW];
   double f[SPHB_TL_LATTICE_MAXW], df[SPHB_TL_LATTICE_MAXW];
 } sphb_tl_lattice;
@@ -580,14 +577,17 @@ int sphb_tl_lattice_width(int32_t dim, int32_t r2);
 int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
                           const int32_t* nbr, const int32_t* cnt, double tol,
                           unsigned long long* bad, void* stream);
-/* Passes A / B (no kick) over the interior rows; same records and contract
+/* Passes A / B (no kick) over the interior rows (lattice) and the shell
+ * rows (general, pass list) in one launch each; same records and contract
  * as sphb_tl_pass_a / sphb_tl_pass_b. */
 int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
-                           const double* B0, const double* Vh, double* XC, double* F,
-                           double* Q, const double* scalars, int32_t* err, void* stream);
+                           const double* B0, const int32_t* nbr, const int32_t* cnt,
+                           const double* Vh, double* XC, double* F, double* Q,
+                           const double* scalars, int32_t* err, void* stream);
 int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
-                           const double* Q, const double* Vh, double* A, double* V,
-                           double* scalars, int32_t update_v, int32_t* err, void* stream);
+                           const int32_t* nbr, const int32_t* cnt, const double* Q,
+                           const double* Vh, double* A, double* V, double* scalars,
+                           int32_t update_v, int32_t* err, void* stream);
 
 /* max |v| into scalars[2] (stable_dt). */
 int sphb_tl_speed_max(const sphb_tl_params* p, const double* V, double* scalars,

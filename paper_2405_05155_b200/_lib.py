@@ -145,9 +145,6 @@ class TLParams(C.Structure):
         ("push_hi1", C.c_int64),
         ("push_next_at", C.c_int64),
         ("q_stride", C.c_int64),
-        ("rows", C.c_void_p),
-        ("no_kick", C.c_int32),
-        ("reserved_tl", C.c_int32),
     ]
 
 
@@ -181,6 +178,8 @@ class TLLattice(C.Structure):
         ("n", C.c_int32 * 3),
         ("reserved", C.c_int32),
         ("n_interior", C.c_int64),
+        ("shell", C.c_void_p),
+        ("n_shell", C.c_int64),
         ("r2k", C.c_double * TL_LATTICE_MAXW),
         ("f", C.c_double * TL_LATTICE_MAXW),
         ("df", C.c_double * TL_LATTICE_MAXW),
@@ -224,8 +223,8 @@ SIGNATURES = {
     "sphb_tl_kick": (C.c_int, [P, P, P, P, P, P]),
     "sphb_tl_lattice_width": (C.c_int, [I32, I32]),
     "sphb_tl_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
-    "sphb_tl_pass_a_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
-    "sphb_tl_pass_b_lattice": (C.c_int, [P, P, P, P, P, P, P, P, I32, P, P]),
+    "sphb_tl_pass_a_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "sphb_tl_pass_b_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P, P]),
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),

@@ -84,7 +84,7 @@ k_tl_pass_a(const sphb_tl_params P, const double4* __restrict__ X0, const double
     stage_pass_list<kThreads>(nbr, n, P.row0 + (int64_t)blockIdx.x * kThreads,
                               P.row0 + P.nrows, P.width, s_nbr);
   if (t >= P.nrows) return;
-  const int64_t i = P.rows ? (int64_t)P.rows[t] : P.row0 + t;   // row list: lattice shell
+  const int64_t i = P.row0 + t;
   const double dt = scalars[0];
   const double hdt = 0.5 * dt;
   const double inv_h = 1.0 / P.h;
@@ -151,7 +151,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
                               P.row0 + P.nrows, P.width, s_nbr);
   double speed = 0.0;
   if (t < P.nrows) {
-    const int64_t i = P.rows ? (int64_t)P.rows[t] : P.row0 + t;   // row list: lattice shell
+    const int64_t i = P.row0 + t;
     const double inv_h = 1.0 / P.h;
     const double scale_v0 = P.alpha / P.h * P.vol0;
     const double c5v = -5.0 * scale_v0 * inv_h, mhalf_inv_h = -0.5 * inv_h;
@@ -170,12 +170,12 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
       int64_t j = STAGED ? srow[k * kThreads] : grow[(int64_t)k * n];
       SPHB_CHECK_INDEX(j, n, err);
       double Qj[D][D], wj[D];
-      if constexpr (D == 3) {      // Q rows carry X0_j in their padding (store_q)
+      if constexpr (D == 3) {      // Q columns carry X0_j in their padding (store_q)
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const double4 t4 = ldg4(Q + r * qs + j);
-          Qj[r][0] = t4.x; Qj[r][1] = t4.y; Qj[r][2] = t4.z;
-          wj[r] = t4.w;
+        for (int c = 0; c < 3; ++c) {
+          const double4 t4 = ldg4(Q + c * qs + j);
+          Qj[0][c] = t4.x; Qj[1][c] = t4.y; Qj[2][c] = t4.z;
+          wj[c] = t4.w;
         }
       } else {
         load_mat_nc<D>(Q, j, Qj);
@@ -286,8 +286,7 @@ inline int tl_carveout() {
 #define TL_DISPATCH_GEO(KERNEL, GEOPTR, GRID, TH, ...)                                     \
   do {                                                                                     \
     const bool geo_ = (GEOPTR) != nullptr;                                                 \
-    const bool stg_ = p->nrows >= kStageMinRows && p->width <= tl_stage_max_width() &&     \
-                      !p->rows;                                                            \
+    const bool stg_ = p->nrows >= kStageMinRows && p->width <= tl_stage_max_width();       \
     const size_t smem_ = stg_ ? (size_t)p->width * kThreads * sizeof(int32_t) : 0;        \
     if (smem_ > 200 * 1024) return SPHB_ERR_ARG;                                           \
     switch (p->dim * 4 + (geo_ ? 2 : 0) + (stg_ ? 1 : 0)) {                                \
@@ -336,10 +335,9 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!p->no_kick)
-    TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars);
+  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars);
   static const int var = tl_variant("SPHB_TL_VARIANT_A");
-  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows && !p->rows)
+  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
     TL_TUNED(k_tl_pass_a, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
              (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
              (double4*)xc, (double4*)f, (double4*)q, scalars, err);
@@ -359,7 +357,7 @@ extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const i
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   static const int var = tl_variant("SPHB_TL_VARIANT_B");
-  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows && !p->rows)
+  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
     TL_TUNED(k_tl_pass_b, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
              (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
              (double4*)a, (double4*)v, scalars, (int)update_v, err);

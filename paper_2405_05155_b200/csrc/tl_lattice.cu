@@ -19,7 +19,9 @@
 //     the reciprocal square root and the t^3 chain.
 // sphb_tl_lattice_check proves all of it for every interior row before the
 // path is used: pass-list row == canonical set, bitwise separability, and
-// |r2 - r2k| <= tol r2k.  Shell rows run the general kernels (row list).
+// |r2 - r2k| <= tol r2k.  Shell rows (incomplete stencils) run in the same
+// launches, in blocks after the interior ones, with the general per-pair
+// geometry and the pass list.
 #include <stdlib.h>
 
 #include <type_traits>
@@ -117,15 +119,117 @@ __device__ __forceinline__ void axis_displacements(const double4* __restrict__ X
     }
 }
 
+// Shell row of pass A: the general pair loop (tl_engine.cu k_tl_pass_a,
+// unstaged) — pass list, X0_j gather, g0 recomputed (ref_gradient).
+template <int D>
+__device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
+                                        const double4* __restrict__ X0,
+                                        const double4* __restrict__ B0,
+                                        const int32_t* __restrict__ nbr,
+                                        const int32_t* __restrict__ cnt,
+                                        const double4* __restrict__ Vh, double4* __restrict__ XC,
+                                        double4* __restrict__ F, double4* __restrict__ Q,
+                                        double dt, int32_t* __restrict__ err) {
+  const int64_t n = P.n;
+  const double inv_h = 1.0 / P.h;
+  const double c5v = -5.0 * (P.alpha / P.h * P.vol0) * inv_h, mhalf_inv_h = -0.5 * inv_h;
+  double wi[D], vhi[D];
+  bool fixed_i;
+  load_x0<D>(X0, i, wi, fixed_i);
+  load_vec<D>(Vh, i, vhi);
+  double m[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+  const int32_t cn = cnt[i];
+  for (int32_t k = 0; k < cn; ++k) {
+    int64_t j = nbr[(int64_t)k * n + i];
+    SPHB_CHECK_INDEX(j, n, err);
+    double vhj[D], wj[D], dx[D], g[D];
+    bool fixed_j;
+    load_vec_nc<D>(Vh, j, vhj);
+    load_x0<D>(X0, j, wj, fixed_j);
+#pragma unroll
+    for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+    ref_gradient<D>(dx, c5v, mhalf_inv_h, g);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double dv = vhj[a] - vhi[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) m[a][b] = fma(dv, g[b], m[a][b]);
+    }
+  }
+  tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+}
+
+// Shell row of pass B (tl_engine.cu k_tl_pass_b, unstaged); returns |v_i|.
+template <int D>
+__device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
+                                          const double4* __restrict__ X0,
+                                          const int32_t* __restrict__ nbr,
+                                          const int32_t* __restrict__ cnt,
+                                          const double4* __restrict__ Q,
+                                          const double4* __restrict__ Vh,
+                                          double4* __restrict__ A, double4* __restrict__ V,
+                                          const double* __restrict__ scalars, int update_v) {
+  const int64_t n = P.n;
+  const int64_t qs = P.q_stride ? P.q_stride : n;
+  const double inv_h = 1.0 / P.h;
+  const double c5v = -5.0 * (P.alpha / P.h * P.vol0) * inv_h, mhalf_inv_h = -0.5 * inv_h;
+  double wi[D];
+  bool fixed_i;
+  load_x0<D>(X0, i, wi, fixed_i);
+  double gsum[D], acc[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) gsum[a] = acc[a] = 0.0;
+  const int32_t cn = cnt[i];
+  for (int32_t k = 0; k < cn; ++k) {
+    const int64_t j = nbr[(int64_t)k * n + i];
+    double Qj[D][D], wj[D];
+    if constexpr (D == 3) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double4 t4 = ldg4(Q + c * qs + j);
+        Qj[0][c] = t4.x; Qj[1][c] = t4.y; Qj[2][c] = t4.z;
+        wj[c] = t4.w;
+      }
+    } else {
+      bool fixed_j;
+      load_mat_nc<D>(Q, j, Qj);
+      load_x0<D>(X0, j, wj, fixed_j);
+    }
+    double dx[D], g[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
+    ref_gradient<D>(dx, c5v, mhalf_inv_h, g);
+#pragma unroll
+    for (int b = 0; b < D; ++b) gsum[b] += g[b];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
+  }
+  return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
+}
+
 template <int D, int R2, int MINB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const double4* __restrict__ B0,
+               const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
                const double4* __restrict__ Vh, double4* __restrict__ XC,
                double4* __restrict__ F, double4* __restrict__ Q,
                const double* __restrict__ scalars, int32_t* __restrict__ err) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
+  const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
+  if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
+    const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
+    if (ts < L.n_shell) shell_a<D>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q,
+                                   scalars[0], err);
+    return;
+  }
   const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
   if (t >= L.n_interior) return;
   const Row<D, R> row(L, t);
@@ -172,14 +276,20 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
 template <int D, int R2, int MINB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
-               const double4* __restrict__ X0, const double4* __restrict__ Q,
+               const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
+               const int32_t* __restrict__ cnt, const double4* __restrict__ Q,
                const double4* __restrict__ Vh, double4* __restrict__ A,
                double4* __restrict__ V, double* __restrict__ scalars, int update_v) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
+  const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
   const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
   double speed = 0.0;
-  if (t < L.n_interior) {
+  if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
+    const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
+    if (ts < L.n_shell)
+      speed = shell_b<D>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V, scalars, update_v);
+  } else if (t < L.n_interior) {
     const Row<D, R> row(L, t);
     const int64_t i = row.i;
     const int64_t qs = P.q_stride ? P.q_stride : P.n;
@@ -197,11 +307,15 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
       const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
                         (int64_t)o[2] * row.stride[2];
       double Qj[D][D];
-      if constexpr (D == 3) {
+      if constexpr (D == 3) {      // only the columns g0 touches (o_c != 0)
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const double4 t4 = ldg4(Q + r * qs + j);
-          Qj[r][0] = t4.x; Qj[r][1] = t4.y; Qj[r][2] = t4.z;
+        for (int c = 0; c < 3; ++c) {
+          if (o[c] != 0) {
+            const double4 t4 = ldg4(Q + c * qs + j);
+            Qj[0][c] = t4.x; Qj[1][c] = t4.y; Qj[2][c] = t4.z;
+          } else {
+            Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
+          }
         }
       } else {
         load_mat_nc<D>(Q, j, Qj);
@@ -323,8 +437,8 @@ static bool tl_lattice_ok(const sphb_tl_params* p, const sphb_tl_lattice* L) {
       inner *= L->n[q] - 2 * R;
     }
   }
-  return prod == p->n && inner == L->n_interior &&
-         sphb_tl_lattice_width(p->dim, L->r2) == L->width;
+  return prod == p->n && inner == L->n_interior && L->n_shell == prod - inner &&
+         (L->n_shell == 0 || L->shell) && sphb_tl_lattice_width(p->dim, L->r2) == L->width;
 }
 
 extern "C" int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_lattice* L,
@@ -351,19 +465,26 @@ static int tl_minb(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// blocks: the interior rows, then the shell rows
+static unsigned lattice_grid(const sphb_tl_lattice* L) {
+  return (unsigned)((L->n_interior + kTT - 1) / kTT + (L->n_shell + kTT - 1) / kTT);
+}
+
 extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                                      const double* x0, const double* b0, const double* vh,
-                                      double* xc, double* f, double* q, const double* scalars,
+                                      const double* x0, const double* b0, const int32_t* nbr,
+                                      const int32_t* cnt, const double* vh, double* xc,
+                                      double* f, double* q, const double* scalars,
                                       int32_t* err, void* stream) {
-  if (!tl_lattice_ok(p, L) || !x0 || !b0 || !vh || !xc || !f || !q) return SPHB_ERR_ARG;
-  if (L->n_interior == 0) return SPHB_OK;
+  if (!tl_lattice_ok(p, L) || !x0 || !b0 || !vh || !xc || !f || !q || !nbr || !cnt)
+    return SPHB_ERR_ARG;
+  if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = tl_minb("SPHB_TLAT_MINB_A", 4);
-  const unsigned grid = sphb_blocks(L->n_interior, kTT);
+  const unsigned grid = lattice_grid(L);
 #define SPHB_A1(D, R, MB)                                                                   \
   k_tl_lattice_a<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,                \
-      (const double4*)b0, (const double4*)vh, (double4*)xc, (double4*)f, (double4*)q,       \
-      scalars, err);                                                                        \
+      (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
+      (double4*)q, scalars, err);                                                           \
   break
 #define SPHB_A(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
@@ -383,17 +504,19 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
 }
 
 extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                                      const double* x0, const double* q, const double* vh,
-                                      double* a, double* v, double* scalars, int32_t update_v,
-                                      int32_t* err, void* stream) {
+                                      const double* x0, const int32_t* nbr, const int32_t* cnt,
+                                      const double* q, const double* vh, double* a, double* v,
+                                      double* scalars, int32_t update_v, int32_t* err,
+                                      void* stream) {
   (void)err;
-  if (!tl_lattice_ok(p, L) || !x0 || !q || !vh || !a || !v || !scalars) return SPHB_ERR_ARG;
-  if (L->n_interior == 0) return SPHB_OK;
+  if (!tl_lattice_ok(p, L) || !x0 || !q || !vh || !a || !v || !scalars || !nbr || !cnt)
+    return SPHB_ERR_ARG;
+  if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = tl_minb("SPHB_TLAT_MINB_B", 4);
-  const unsigned grid = sphb_blocks(L->n_interior, kTT);
+  const unsigned grid = lattice_grid(L);
 #define SPHB_B1(D, R, MB)                                                                   \
-  k_tl_lattice_b<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,                \
+  k_tl_lattice_b<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr, cnt,      \
       (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,             \
       (int)update_v);                                                                       \
   break

@@ -247,7 +247,7 @@ class SolidSystem:
         self.B0rec = _b0_rec(b0, n, d, dev)
         eye = torch.eye(d, dtype=torch.float64, device=dev).expand(n, d, d)
         self.Frec = _f_rec(eye, n, d, dev)
-        # Q: three row planes in 3D (tl_engine.cu store_q), one stride for
+        # Q: three column planes in 3D (tl_common.cuh store_q), one stride for
         # all slab ranks so the fused halo push can address peer planes
         self._q_stride = n
         if d == 3:
@@ -417,24 +417,17 @@ class SolidSystem:
         for a in range(d):
             inner &= (coord[a] >= R) & (coord[a] < ext[a] - R)
         self._shell = torch.nonzero(~inner).flatten().to(torch.int32).contiguous()
-        ps = _lib.TLParams.from_buffer_copy(self.params)     # copy, then the row list
-        ps.rows, ps.nrows, ps.no_kick = self._shell.data_ptr(), int(self._shell.numel()), 1
-        self._params_shell = ps
+        L.shell, L.n_shell = self._shell.data_ptr(), int(self._shell.numel())
         self.lattice = L
 
     def _pass_b(self, update_v):
         st = _lib.stream_ptr()
         if self.lattice is not None:
             _lib.call("sphb_tl_pass_b_lattice", ctypes.byref(self.params),
-                      ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.Qrec.data_ptr(),
-                      self.Vh.data_ptr(), self.A.data_ptr(), self.V.data_ptr(),
-                      self.scalars.data_ptr(), update_v, self.err.data_ptr(), st)
-            if self._params_shell.nrows:
-                _lib.call("sphb_tl_pass_b", ctypes.byref(self._params_shell),
-                          self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
-                          None, self.Qrec.data_ptr(), self.Vh.data_ptr(), self.A.data_ptr(),
-                          self.V.data_ptr(), self.scalars.data_ptr(), update_v,
-                          self.err.data_ptr(), st)
+                      ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.nbr.data_ptr(),
+                      self.cnt.data_ptr(), self.Qrec.data_ptr(), self.Vh.data_ptr(),
+                      self.A.data_ptr(), self.V.data_ptr(), self.scalars.data_ptr(), update_v,
+                      self.err.data_ptr(), st)
             return
         _lib.call("sphb_tl_pass_b", ctypes.byref(self.params), self.X0rec.data_ptr(),
                   self.nbr.data_ptr(), self.cnt.data_ptr(), self._g0_ptr, self.Qrec.data_ptr(),
@@ -537,20 +530,14 @@ class SolidSystem:
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
         if self.lattice is not None:
-            # kick, lattice pass A (interior) + general pass A (shell rows)
+            # kick, then pass A over the interior (lattice) and shell rows
             _lib.call("sphb_tl_kick", ctypes.byref(self.params), self.V.data_ptr(),
                       self.A.data_ptr(), self.Vh.data_ptr(), self.scalars.data_ptr(), st)
             _lib.call("sphb_tl_pass_a_lattice", ctypes.byref(self.params),
                       ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.B0rec.data_ptr(),
-                      self.Vh.data_ptr(), self.XC.data_ptr(), self.Frec.data_ptr(),
-                      self.Qrec.data_ptr(), self.scalars.data_ptr(), self.err.data_ptr(), st)
-            if self._params_shell.nrows:
-                _lib.call("sphb_tl_pass_a", ctypes.byref(self._params_shell),
-                          self.X0rec.data_ptr(), self.B0rec.data_ptr(), self.nbr.data_ptr(),
-                          self.cnt.data_ptr(), None, self.V.data_ptr(), self.A.data_ptr(),
-                          self.Vh.data_ptr(), self.XC.data_ptr(), self.Frec.data_ptr(),
-                          self.Qrec.data_ptr(), self.scalars.data_ptr(), self.err.data_ptr(),
-                          st)
+                      self.nbr.data_ptr(), self.cnt.data_ptr(), self.Vh.data_ptr(),
+                      self.XC.data_ptr(), self.Frec.data_ptr(), self.Qrec.data_ptr(),
+                      self.scalars.data_ptr(), self.err.data_ptr(), st)
         else:
             _lib.call("sphb_tl_pass_a", ctypes.byref(self.params), self.X0rec.data_ptr(),
                       self.B0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),

@@ -404,12 +404,6 @@ class SolidSystem:
             L.r2k[k] = r2k
             L.f[k] = c5v * ((t * t) * t)
             L.df[k] = 3.0 * c5v * t * t * (-0.25 / (h * r))
-        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
-        _lib.call("sphb_tl_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
-                  self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), 1e-10,
-                  bad.data_ptr(), _lib.stream_ptr())
-        if int(bad.item()):
-            return
         idx = torch.arange(n, device=self._dev)
         coord = [idx % ext[0], (idx // ext[0]) % ext[1] if d > 1 else None,
                  idx // (ext[0] * ext[1]) if d > 2 else None]
@@ -418,7 +412,12 @@ class SolidSystem:
             inner &= (coord[a] >= R) & (coord[a] < ext[a] - R)
         self._shell = torch.nonzero(~inner).flatten().to(torch.int32).contiguous()
         L.shell, L.n_shell = self._shell.data_ptr(), int(self._shell.numel())
-        self.lattice = L
+        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
+        _lib.call("sphb_tl_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
+                  self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), 1e-10,
+                  bad.data_ptr(), _lib.stream_ptr())
+        if int(bad.item()) == 0:
+            self.lattice = L
 
     def _pass_b(self, update_v):
         st = _lib.stream_ptr()

@@ -239,7 +239,7 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     for stage, a, b in solver.timer:
         st[stage].append(a.elapsed_time(b))
     solver.timer = None
-    kernel = {"geo": "k_wc_stage_geo<3>", "tiled": "k_wc_stage_tiled<3,%d>" % solver.group,
+    kernel = {"geo": "k_wc_stage_geo<3>",
               "global": "k_wc_stage<3,%d,%s>" % (solver.group,
                                                  os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
     if solver.lattice is not None:

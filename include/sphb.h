@@ -174,21 +174,6 @@ int sphb_ell_moments(const sphb_grid* g, int64_t n, const double* wrapped_sorted
                      const int32_t* nbr, const int32_t* cnt, const double* vols_sorted,
                      const sphb_kernel* k, double* m_sorted, void* stream);
 
-/* Shared-memory staging plan for a static, binned particle set: tiles of P
- * consecutive sorted particles; per tile up to rmax runs {start, len,
- * local_base} of the neighbour union and meta {nruns, union size, local
- * index of the tile's first particle, ok}.  *max_u = largest union (or
- * 0x40000000 if some tile cannot be planned).  Then every ELL entry is
- * rewritten as a uint16 index into its tile's union. */
-size_t sphb_tile_plan_workspace_bytes(const sphb_grid* g);
-int sphb_tile_plan(const sphb_grid* g, int64_t n, const double* wrapped_sorted,
-                   const int32_t* cell_start, const int32_t* cell_end, int32_t P,
-                   int32_t rmax, int32_t* runs, int32_t* meta, int32_t* max_u,
-                   void* workspace, size_t workspace_bytes, void* stream);
-int sphb_tile_local_nbr(int64_t n, int32_t P, int32_t rmax, const int32_t* nbr,
-                        const int32_t* cnt, const int32_t* runs, const int32_t* meta,
-                        uint16_t* lnbr, int32_t* err, void* stream);
-
 /* ---------------------------------------------- CSR operator passes
  * Bit-faithful restatements of the reference @njit loops (compiled without
  * FMA contraction, same summation order) over a device CSR. */
@@ -278,7 +263,7 @@ typedef struct sphb_wc_params {
   double h, alpha, kappa; /* Wendland family only (code 0)                  */
   double c_art, rho0, mu, cfl;
   double vol_const;
-  int32_t swizzle;       /* >0: SM count for the block->chunk L1-locality swizzle */
+  int32_t reserved0;
   int32_t reserved;
   const int8_t* interior; /* NULL, or 1 for rows to update (ghosts: 0), sorted */
   double gamma;          /* ideal-gas ratio of specific heats (HLLC path)   */
@@ -349,17 +334,6 @@ int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t group, const d
                   const double* S_in, const double* S_n, const double* M_n,
                   double* S_out, double* M_out, double* scalars, int32_t* err,
                   void* stream);
-/* Shared-memory tiled stage (same contract as sphb_wc_stage): tiles of
- * 256/group particles; each CTA stages its tile's neighbour union (runs from
- * sphb_tile_plan) into shared memory and `group` threads share a particle;
- * lnbr is the uint16 local ELL from sphb_tile_local_nbr.  Uniform volumes. */
-int sphb_wc_stage_tiled(const sphb_wc_params* p, int32_t stage, int32_t group,
-                        const double* X, const double* B, const int32_t* cnt,
-                        const uint16_t* lnbr, const int32_t* runs, const int32_t* meta,
-                        int32_t rmax, int32_t umax, const double* S_in, const double* S_n,
-                        const double* M_n, double* S_out, double* M_out, double* scalars,
-                        int32_t* err, void* stream);
-
 /* Static per-pair geometry of the WC flux (eulerian.py:506-513): for every
  * ELL slot, e_ij, gwv_ij = dW 0.5 (B_i + B_j) e_ij V_j and viscv_ij =
  * 2 dW / r V_j as planes geo[(c * width + k) * n + s], c = 0..2D (B: full

@@ -101,7 +101,7 @@ class WCParams(C.Structure):
         ("mu", C.c_double),
         ("cfl", C.c_double),
         ("vol_const", C.c_double),
-        ("swizzle", C.c_int32),
+        ("reserved0", C.c_int32),
         ("reserved", C.c_int32),
         ("interior", C.c_void_p),
         ("gamma", C.c_double),
@@ -206,10 +206,6 @@ SIGNATURES = {
     "sphb_ell_count": (C.c_int, [P, I64, P, P, P, F64, F64, P, P, P]),
     "sphb_ell_fill": (C.c_int, [P, I64, P, P, P, F64, F64, I32, P, P]),
     "sphb_ell_moments": (C.c_int, [P, I64, P, P, P, P, P, P, P]),
-    "sphb_tile_plan_workspace_bytes": (SZ, [P]),
-    "sphb_tile_plan": (C.c_int, [P, I64, P, P, P, I32, I32, P, P, P, P, SZ, P]),
-    "sphb_tile_local_nbr": (C.c_int, [I64, I32, I32, P, P, P, P, P, P, P]),
-    "sphb_wc_stage_tiled": (C.c_int, [P, I32, I32, P, P, P, P, P, P, I32, I32, P, P, P, P, P, P, P, P]),
     "sphb_unity_sums": (C.c_int, [I64, P, P, P, P, P, P, P]),
     "sphb_pressure_accel": (C.c_int, [I64, I32, P, P, P, P, P, P, F64, F64, P, P]),
     "sphb_moment_matrices": (C.c_int, [I64, I32, P, P, P, P, P, P, P, P]),

@@ -82,18 +82,7 @@ k_wc_stage(const sphb_wc_params P, const WCConst K, const int stage,
            double* __restrict__ scalars, int32_t* __restrict__ err) {
   const int64_t n = P.n;
   const int gl = threadIdx.x % G;
-  // SM-locality swizzle: the hardware hands out blocks round-robin over the
-  // SMs, so blocks b, b + nsm, b + 2 nsm, ... tend to share an SM.  Mapping
-  // them to CONSECUTIVE particle chunks makes co-resident blocks work on
-  // neighbouring cells, whose neighbour records then hit in that SM's L1.
-  int64_t blk = blockIdx.x;
-  if (P.swizzle > 0) {
-    const int64_t nb = gridDim.x, nsm = P.swizzle;
-    const int64_t per = (nb + nsm - 1) / nsm;   // chunks per SM lane
-    const int64_t lane = blk % nsm, k = blk / nsm;
-    const int64_t full = nb - (per - 1) * nsm;   // lanes that own `per` chunks
-    blk = lane < full ? lane * per + k : full * per + (lane - full) * (per - 1) + k;
-  }
+  const int64_t blk = blockIdx.x;
   const int64_t i = P.row0 + (blk * blockDim.x + threadIdx.x) / G;
   const bool active = i < P.row0 + P.nrows && (P.interior == nullptr || P.interior[i]);
 

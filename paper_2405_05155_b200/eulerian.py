@@ -39,7 +39,7 @@ import numpy as np
 
 from . import _lib
 from .kernels import CODE_WENDLAND, KernelSpec
-from .neighbors import (NeighborList, TilePlan, bin_particles, csr_from_bins, ell_from_bins,
+from .neighbors import (NeighborList, bin_particles, csr_from_bins, ell_from_bins,
                         engine_order,
                         make_grid)
 
@@ -279,7 +279,7 @@ class EulerianSolver:
         self.order = self.bins
         # the fine key's spacing must be a global quantity (slab ranks must
         # order a shared layer identically): the particle volume's edge
-        if (variant != "tiled" and os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell"
+        if (os.environ.get("SPHB_ENGINE_ORDER", "lattice") != "cell"
                 and (uniform or _slab is None)):
             spacing = (float(vol[0]) ** (1.0 / self.dim)) if uniform and self.n else None
             self.order, self.nbr, self.cnt = engine_order(self.bins, self.nbr, self.cnt,
@@ -314,13 +314,12 @@ class EulerianSolver:
         self.group = 1
         if os.environ.get("SPHB_WC_GROUP"):      # tuning override
             self.group = int(os.environ["SPHB_WC_GROUP"])
-        # Stage-kernel variant (SPHB_WC_KERNEL=global|geo|tiled):
+        # Stage-kernel variant (SPHB_WC_KERNEL=global|geo):
         #   global (default) recompute the pair geometry from X_j, B_j
-        #          (wc_engine.cu) — fastest on B200 (profiles/r01_tune_wc.md);
+        #          (wc_engine.cu; on a checked lattice wc_lattice.cu);
         #   geo    stream the static per-pair geometry (wc_stream.cu,
         #          (2d+1) doubles per pair, reference arithmetic without FMA:
-        #          the closest reproduction of the reference's roundings);
-        #   tiled  shared-memory staging variant of `global`.
+        #          the closest reproduction of the reference's roundings).
         geo_bytes = (2 * self.dim + 1) * self.width * self.n * 8
         self.variant = variant
         self.geo = None
@@ -332,12 +331,6 @@ class EulerianSolver:
                       self.cnt.data_ptr(), self.width, b.data_ptr(),
                       vol_s.contiguous().data_ptr(), ctypes.byref(k), self.geo.data_ptr(),
                       _lib.stream_ptr())
-        self.plan = None
-        if variant == "tiled" and uniform and self.n and self.width and ghosts is None:
-            plan = TilePlan(self.bins, self.nbr, self.cnt, self.width,
-                            fields=14 if self.dim == 3 else 12)
-            if plan.ok:
-                self.plan = plan
 
         self.params = _lib.WCParams()
         p = self.params
@@ -367,10 +360,6 @@ class EulerianSolver:
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
         p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
         p.vol_const = float(vol[0]) if self.n else 0.0
-        # block->SM locality swizzle: measured slower on C5 (co-scheduled
-        # blocks on one contiguous region share neighbour rows through L2);
-        # off by default, SPHB_SWIZZLE=<sm count> to enable
-        p.swizzle = int(os.environ.get("SPHB_SWIZZLE", "0"))
         self.lattice = None
         if (variant == "global" and precision == "fp64" and not self._ideal and ghosts is None
                 and wall_force_tag is None and uniform and self.order is not self.bins
@@ -716,15 +705,6 @@ class EulerianSolver:
             _lib.call("sphb_wc_stage_geo", ctypes.byref(self.params), stage, self.nbr.data_ptr(),
                       self.cnt.data_ptr(), self.geo.data_ptr(), s_in.data_ptr(), s_n.data_ptr(),
                       m_n.data_ptr(), s_out.data_ptr(),
-                      None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
-                      self.err.data_ptr(), _lib.stream_ptr())
-            return
-        if self.plan is not None:
-            pl = self.plan
-            _lib.call("sphb_wc_stage_tiled", ctypes.byref(self.params), stage, pl.group,
-                      self.X.data_ptr(), self.B.data_ptr(), self.cnt.data_ptr(),
-                      pl.lnbr.data_ptr(), pl.runs.data_ptr(), pl.meta.data_ptr(), pl.RMAX,
-                      pl.umax, s_in.data_ptr(), s_n.data_ptr(), m_n.data_ptr(), s_out.data_ptr(),
                       None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
                       self.err.data_ptr(), _lib.stream_ptr())
             return

@@ -389,58 +389,3 @@ def neighbor_count_ratio(positions, cutoff_tw: float, cutoff_sw: float) -> float
     if mean_sw == 0.0:
         raise ValueError("standard-cutoff neighborhoods are empty")
     return float(mean_tw / mean_sw)
-
-
-class TilePlan:
-    """Shared-memory staging plan of a static particle set (sphb_tile_plan).
-
-    Tiles are P = 256 / group consecutive sorted particles; `runs`/`meta`
-    describe each tile's neighbour union as contiguous sorted runs and
-    `lnbr` is the ELL rewritten as uint16 indices into that union.  `ok` is
-    False when some tile cannot be staged (too many runs, union too large
-    for shared memory or for uint16), in which case callers use the
-    global-gather kernels.
-    """
-
-    RMAX = 48
-
-    def __init__(self, bins: CellBins, nbr, cnt, width: int, *, fields: int,
-                 smem_cap: int = 200 * 1024):
-        import ctypes
-
-        torch = _lib.torch_cuda()
-        n = bins.n
-        dev = bins.perm.device
-        import os
-
-        self.group = 1
-        while self.group < 8 and self.group * 8 < width:
-            self.group *= 2
-        if os.environ.get("SPHB_TILE_GROUP"):      # tuning override
-            self.group = int(os.environ["SPHB_TILE_GROUP"])
-        self.tile = 256 // self.group
-        self.ok = False
-        self.umax = 0
-        if n == 0 or width == 0 or bins.grid.slow_axis != bins.dim - 1:
-            return          # runs assume the reference key (axis 0 fastest) order
-        ntiles = (n + self.tile - 1) // self.tile
-        self.runs = torch.empty((ntiles, self.RMAX, 3), dtype=torch.int32, device=dev)
-        self.meta = torch.empty((ntiles, 4), dtype=torch.int32, device=dev)
-        mx = torch.zeros(1, dtype=torch.int32, device=dev)
-        g = ctypes.byref(bins.grid)
-        wbytes = _lib.load_library().sphb_tile_plan_workspace_bytes(g)
-        work = torch.empty(max(wbytes, 1), dtype=torch.uint8, device=dev)
-        _lib.call("sphb_tile_plan", g, n, bins.ws.contiguous().data_ptr(),
-                  bins.cell_start.data_ptr(), bins.cell_end.data_ptr(), self.tile, self.RMAX,
-                  self.runs.data_ptr(), self.meta.data_ptr(), mx.data_ptr(), work.data_ptr(),
-                  wbytes, _lib.stream_ptr())
-        umax = int(mx.item())
-        if umax <= 0 or umax > 0xFFFF or 8 * fields * umax > smem_cap:
-            return
-        self.umax = umax
-        self.lnbr = torch.empty((width, n), dtype=torch.int16, device=dev)
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.call("sphb_tile_local_nbr", n, self.tile, self.RMAX, nbr.data_ptr(), cnt.data_ptr(),
-                  self.runs.data_ptr(), self.meta.data_ptr(), self.lnbr.data_ptr(), err.data_ptr(),
-                  _lib.stream_ptr())
-        self.ok = int(err.item()) == 0

@@ -783,11 +783,10 @@ def test_tl_engine_order_on_jittered_block(monkeypatch, order):
                 assert l2_error(a, b) < tol
 
 
-@pytest.mark.parametrize("variant", ["geo", "tiled"])
+@pytest.mark.parametrize("variant", ["geo"])
 def test_wc_opt_in_variants_vs_oracle(monkeypatch, variant):
-    """The opt-in stage variants (SPHB_WC_KERNEL=geo: streamed per-pair
-    geometry without FMA; tiled: shared-memory record tiles) give the oracle's
-    fields on C5 (16^3)."""
+    """The opt-in stage variant SPHB_WC_KERNEL=geo (streamed per-pair
+    geometry without FMA) gives the oracle's fields on C5 (16^3)."""
     monkeypatch.setenv("SPHB_WC_KERNEL", variant)
     cfg = configs.c5_tgv3d(kernel="1.6h", n_side=16)
     s = make_wc(cfg)

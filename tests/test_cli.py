@@ -53,7 +53,7 @@ def test_cli_commands_on_gpu(tmp_path, capsys):
     pos = np.loadtxt(tmp_path / "rel" / "relax-positions.csv", delimiter=",", skiprows=1)
     assert pos.shape[1] == 3 and np.all(np.hypot(pos[:, 0], pos[:, 1]) < 1.0)
     study = tmp_path / "study.toml"
-    study.write_text('[study]\nresolutions = [0.4, 0.2]\ndistributions = ["lattice"]\n')
+    study.write_text('[study]\nresolutions = [0.2, 0.1]\ndistributions = ["lattice"]\n')
     assert cli.main(["error-study", str(study), "--out", str(tmp_path / "es")]) == 0
     rows = (tmp_path / "es" / "error-study.csv").read_text().splitlines()
     assert len(rows) == 1 + 2 * 2 * 2

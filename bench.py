@@ -613,7 +613,7 @@ def main():
     if c4 is not None:
         line["c4_column"] = c4
     if f32 is not None:
-        line["fp32_mode"] = dict(f32, unit="particle-steps/s", kernel="k_wc_stage_f32<3>",
+        line["fp32_mode"] = dict(f32, unit="particle-steps/s", kernel="k_wc_lattice_f32<3,4>",
                                  note="FP32 pair math, FP64 accumulation/state; reported "
                                       "separately, not the headline")
     if rank == 0 and not args.no_cpu_baseline:

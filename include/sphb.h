@@ -324,6 +324,15 @@ int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L, int32_
                           const double* M_n, double* S_out, double* M_out, double* scalars,
                           int32_t* err, void* stream);
 
+/* The optional FP32 mode of sphb_wc_stage_f32 on a checked lattice: FP32
+ * records (B32 planes, S32 {v, rho - rho0}) and table geometry, FP32 pair
+ * math, FP64 accumulation and FP64 stage update (S_out/M_out in stage 2;
+ * S32_out written by stages 1 and 2; stage 0 writes the rhs record). */
+int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lattice* L, int32_t stage,
+                              const float* B32, const float* S32_in, const double* S_n,
+                              const double* M_n, float* S32_out, double* S_out, double* M_out,
+                              double* scalars, int32_t* err, void* stream);
+
 /* `group` (1, 2, 4, 8) consecutive threads share one particle's row.
  * stage 0: rhs only — S_out = {dmom, drho} records (EulerianSolver.rhs).
  * stage 1: S_in = S_n, writes S_out = U^1 primitive record (M_out unused).

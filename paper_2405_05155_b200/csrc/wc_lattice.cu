@@ -265,6 +265,209 @@ __global__ void k_wc_lattice_check(const sphb_wc_params P, const sphb_lattice L,
   if (!ok) atomicAdd(bad, 1ull);
 }
 
+// ---------------------------------------------------------------- FP32 mode
+// The optional FP32 mode (north star; wc_f32.cu is its general-set kernel)
+// on a checked lattice: FP32 neighbour records (S32 {v, rho - rho0}, B32
+// planes), FP32 table geometry and pair math, FP64 accumulation (partial
+// sums flushed to double every kFlush slots) and FP64 stage update on the
+// FP64 state; stage epilogues write the FP32 companion S32 as well.
+struct LatF32 {
+  int32_t n[3];
+  float dx[SPHB_LATTICE_MAXW][3];
+  float inv_r[SPHB_LATTICE_MAXW], g2[SPHB_LATTICE_MAXW], mv[SPHB_LATTICE_MAXW];
+};
+
+struct LatConstF32 {
+  float c, c2, eta_c, half_cinv, rho0;
+};
+
+constexpr int kFlush = 8;
+
+template <int D>
+struct SymF;
+template <>
+struct SymF<2> {
+  float a[3];    // {b00, b01, b11}
+  __device__ __forceinline__ void load(const float* B, int64_t, int64_t i) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(B) + i);
+    a[0] = t.x; a[1] = t.y; a[2] = t.z;
+  }
+  __device__ __forceinline__ float at(int r, int c) const {
+    return r != c ? a[1] : (r == 0 ? a[0] : a[2]);
+  }
+};
+template <>
+struct SymF<3> {
+  float a[6];    // {b00, b01, b02, b11, b12, b22}
+  __device__ __forceinline__ void load(const float* B, int64_t n, int64_t i) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(B) + i);
+    const float2 u = __ldg(reinterpret_cast<const float2*>(B + 4 * n) + i);
+    a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w; a[4] = u.x; a[5] = u.y;
+  }
+  __device__ __forceinline__ float at(int r, int c) const {
+    const int k = r < c ? r * 3 + c : c * 3 + r;
+    return k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : k == 4 ? a[3] : k == 5 ? a[4] : a[5];
+  }
+};
+
+template <int D, int R2>
+__global__ void __launch_bounds__(kLT, 4)
+k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, const int stage,
+                 const float* __restrict__ B, const float4* __restrict__ S32_in,
+                 const double4* Sn, const double4* Mn, float4* __restrict__ S32_out,
+                 double4* S_out, double4* M_out, double* __restrict__ scalars,
+                 int32_t* __restrict__ err) {
+  using St = Stencil<D, R2>;
+  constexpr int R = St::R;
+  constexpr int SIDE = 2 * R + 1;
+  const int64_t n = P.n;
+  const int64_t i0 = P.row0 + (int64_t)blockIdx.x * kLT + threadIdx.x;
+  const bool own = i0 < P.row0 + P.nrows;
+  const int64_t i = own ? i0 : P.row0 + P.nrows - 1;
+  const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
+  const int ii = (int)i;
+  const int a = ii % n0, t = ii / n0;
+  const int b = D > 1 ? t % n1 : 0, cz = D > 2 ? t / n1 : 0;
+  int xs[SIDE], ys[SIDE], zs[SIDE];
+#pragma unroll
+  for (int s = -R; s <= R; ++s) {
+    xs[s + R] = wrapc(a, s, n0);
+    ys[s + R] = D > 1 ? n0 * wrapc(b, s, n1) : 0;
+    zs[s + R] = D > 2 ? n0 * n1 * wrapc(cz, s, n2) : 0;
+  }
+  const float4 si = __ldg(S32_in + i);
+  const float vi[3] = {si.x, si.y, si.z};
+  const float drho_i = D == 3 ? si.w : si.z;
+  const float p_i = K.c2 * drho_i;
+  float hvi[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) hvi[q] = 0.5f * vi[q];
+  SymF<D> Bi;
+  Bi.load(B, n, i);
+  double dr = 0.0, dm[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) dm[q] = 0.0;
+  float fr = 0.f, fm[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) fm[q] = 0.f;
+
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+    const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
+    const float4 sj = __ldg(S32_in + j);
+    const float vj[3] = {sj.x, sj.y, sj.z};
+    const float drho_j = D == 3 ? sj.w : sj.z;
+    SymF<D> Bj;
+    Bj.load(B, n, j);
+    float dx[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) dx[q] = o[q] == 0 ? 0.f : L.dx[k][q];
+    float G_[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      float acc = 0.f;
+      bool first = true;
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+        if (o[q] != 0) {
+          const float bs = Bi.at(r, q) + Bj.at(r, q);
+          acc = first ? bs * dx[q] : fmaf(bs, dx[q], acc);
+          first = false;
+        }
+      G_[r] = acc;
+    }
+    float dv[D], dud = 0.f;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      dv[q] = vj[q] - vi[q];
+      if (o[q] != 0) dud = fmaf(dv[q], dx[q], dud);
+    }
+    const float du = dud * L.inv_r[k];
+    const float beta = fminf(fmaxf(du * K.eta_c, 0.f), 1.f);
+    const float rbar = K.rho0 + 0.5f * (drho_i + drho_j);
+    const float p_j = K.c2 * drho_j;
+    const float wr = (beta * beta) * (p_i - p_j) * K.half_cinv * __fdividef(1.0f, rbar) *
+                     L.inv_r[k];
+    const float p_star = fmaf(0.5f * beta * rbar * K.c, du, 0.5f * (p_i + p_j));
+    float vs[D], sg = 0.f;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      const float vb = fmaf(0.5f, vj[q], hvi[q]);
+      vs[q] = o[q] == 0 ? vb : fmaf(-wr, dx[q], vb);
+      sg = fmaf(vs[q], G_[q], sg);
+    }
+    const float rs2 = rbar * (L.g2[k] * sg);
+    const float pg = p_star * L.g2[k];
+    fr += rs2;
+#pragma unroll
+    for (int q = 0; q < D; ++q) fm[q] += fmaf(-L.mv[k], dv[q], fmaf(pg, G_[q], rs2 * vs[q]));
+    if constexpr ((k + 1) % kFlush == 0 || k + 1 == St::W) {
+      dr += (double)fr;
+      fr = 0.f;
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        dm[q] += (double)fm[q];
+        fm[q] = 0.f;
+      }
+    }
+  });
+
+  // epilogue (as wc_f32.cu): FP64 update, FP32 companion record
+  double speed = 0.0;
+  int32_t flags = 0;
+  if (own) {
+    bool finite = isfinite(dr);
+#pragma unroll
+    for (int q = 0; q < D; ++q) finite = finite && isfinite(dm[q]);
+    if (!finite) flags |= SPHB_EFLAG_NONFINITE_FLUX;
+    if (stage == 0) {
+      S_out[i] = pack_s<D>(dm, dr);
+    } else {
+      const double dt = scalars[0];
+      const double cdt = stage == 1 ? 0.5 * dt : dt;
+      const double4 mn = Mn[i];
+      const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
+      double vtmp[D], rho_n;
+      unpack_s<D>(Sn[i], vtmp, rho_n);
+      const double rho_new = fma(cdt, dr, rho_n);
+      double mom_new[D], v_new[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        mom_new[q] = fma(cdt, dm[q], cm[q]);
+        v_new[q] = __ddiv_rn(mom_new[q], rho_new);
+      }
+      if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
+      float s32[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < D; ++q) s32[q] = (float)v_new[q];
+      s32[D] = (float)(rho_new - P.rho0);
+      S32_out[i] = make_float4(s32[0], s32[1], s32[2], s32[3]);
+      if (stage == 2) {
+        S_out[i] = pack_s<D>(v_new, rho_new);
+        double mc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < D; ++q) mc[q] = mom_new[q];
+        M_out[i] = make_double4(mc[0], mc[1], mc[2], mc[3]);
+        speed = __dadd_rn(P.c_art, norm_exact<D>(v_new));
+      }
+    }
+  }
+  if (stage == 2) {
+    __shared__ double red[kLT / 32];
+    const double w = warp_max(speed);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = red[0];
+#pragma unroll
+      for (int q = 1; q < kLT / 32; ++q) mx = mx > red[q] ? mx : red[q];
+      atomic_max_nonneg(scalars + 2, mx);
+    }
+  }
+  if (flags) atomicOr(err, flags);
+}
+
 }  // namespace
 
 #define SPHB_LAT_CASES(X) X(2, 4) X(2, 6) X(3, 4) X(3, 6)
@@ -375,5 +578,43 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   SPHB_LAT_CASES(SPHB_S)
 #undef SPHB_S
 #undef SPHB_S1
+  return SPHB_ERR_ARG;
+}
+
+extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lattice* L,
+                                         int32_t stage, const float* b32, const float* s32_in,
+                                         const double* s_n, const double* m_n, float* s32_out,
+                                         double* s_out, double* m_out, double* scalars,
+                                         int32_t* err, void* stream) {
+  if (!lattice_args_ok(p, L) || !b32 || !s32_in || stage < 0 || stage > 2 || p->interior ||
+      p->wall_tag || !p->uniform_vol || (stage > 0 && !s32_out))
+    return SPHB_ERR_ARG;
+  if (p->nrows == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LatF32 T;
+  for (int q = 0; q < 3; ++q) T.n[q] = L->n[q];
+  for (int k = 0; k < L->width; ++k) {
+    for (int q = 0; q < 3; ++q) T.dx[k][q] = (float)L->dx[k][q];
+    T.inv_r[k] = (float)L->inv_r[k];
+    T.g2[k] = (float)L->g2[k];
+    T.mv[k] = (float)L->mv[k];
+  }
+  LatConstF32 K;
+  K.c = (float)p->c_art;
+  K.c2 = K.c * K.c;
+  K.eta_c = (float)(kEtaLinearized / p->c_art);
+  K.half_cinv = 0.5f / K.c;
+  K.rho0 = (float)p->rho0;
+  const unsigned grid = sphb_blocks(p->nrows, kLT);
+#define SPHB_F(D, R)                                                                        \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    k_wc_lattice_f32<D, R><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,                      \
+        (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,  \
+        (double4*)s_out, (double4*)m_out, scalars, err);                                   \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+  SPHB_LAT_CASES(SPHB_F)
+#undef SPHB_F
   return SPHB_ERR_ARG;
 }

@@ -361,7 +361,7 @@ class EulerianSolver:
         p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
         p.vol_const = float(vol[0]) if self.n else 0.0
         self.lattice = None
-        if (variant == "global" and precision == "fp64" and not self._ideal and ghosts is None
+        if (variant == "global" and not self._ideal and ghosts is None
                 and wall_force_tag is None and uniform and self.order is not self.bins
                 and os.environ.get("SPHB_WC_LATTICE", "1") != "0"):
             self.lattice = self._setup_lattice(float(vol[0]))
@@ -694,6 +694,14 @@ class EulerianSolver:
         if self.precision == "fp32":
             c32 = self._c32
             out32 = c32.get(s_out.data_ptr(), c32[self.S1.data_ptr()])
+            if self.lattice is not None and stage != 0:
+                _lib.call("sphb_wc_stage_lattice_f32", ctypes.byref(self.params),
+                          ctypes.byref(self.lattice), stage, self.B32.data_ptr(),
+                          c32[s_in.data_ptr()].data_ptr(), s_n.data_ptr(), m_n.data_ptr(),
+                          out32.data_ptr(), s_out.data_ptr(),
+                          None if m_out is None else m_out.data_ptr(), self.scalars.data_ptr(),
+                          self.err.data_ptr(), _lib.stream_ptr())
+                return
             _lib.call("sphb_wc_stage_f32", ctypes.byref(self.params), stage, self.X32.data_ptr(),
                       self.B32.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
                       c32[s_in.data_ptr()].data_ptr(), s_n.data_ptr(), m_n.data_ptr(),

@@ -427,9 +427,12 @@ def test_tl_inverted_raises():
 
 @pytest.mark.parametrize("label,builder,size", [("c2", configs.c2_tgv2d, 64),
                                                 ("c5", configs.c5_tgv3d, 16)])
-def test_fp32_mode_error_is_small(label, builder, size):
-    """Optional FP32 mode: error vs the FP64 engine after 20 steps, reported
-    separately (north star); a loose bound guards against breakage."""
+@pytest.mark.parametrize("lattice", ["1", "0"])
+def test_fp32_mode_error_is_small(monkeypatch, label, builder, size, lattice):
+    """Optional FP32 mode (lattice kernel and general kernel): error vs the
+    FP64 engine after 20 steps, reported separately (north star); a loose
+    bound guards against breakage."""
+    monkeypatch.setenv("SPHB_WC_LATTICE", lattice)
     cfg = builder(n_side=size)
     n = cfg["pos"].shape[0]
     eos = EosParams(WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"])
@@ -438,6 +441,7 @@ def test_fp32_mode_error_is_small(label, builder, size):
         st = FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
         s = EulerianSolver(cfg["pos"], n, st, eos, cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"],
                            periodic_box=cfg["box"], precision=prec)
+        assert (s.lattice is not None) == (lattice == "1")
         s.advance(20)
         out[prec] = s.state
     assert l2_error(out["fp32"].mom, out["fp64"].mom) < 1e-4

@@ -162,6 +162,98 @@ def linearized_star(left: InterfaceState, right: InterfaceState, e_ij) -> Rieman
                        u_star, beta)
 
 
+def hllc_star(left: InterfaceState, right: InterfaceState, e_ij) -> RiemannStar:
+    """Limited HLLC interface solution of particle i (left) and j (right)
+    along n = -e_ij (the pairwise solver of eulerian.py:90-142, 196-208):
+    two-wave speed estimates, widened to the min/max bounds when the middle
+    wave leaves the fan; star velocity / pressure from the acoustic weights
+    w = rho |u - S| with the limiter beta = clamp(du / cbar); star densities
+    and energies with the middle-wave denominators.  Host scalar helper; the
+    device evaluates the same formulas per pair (csrc/hllc.cu)."""
+    n = -np.asarray(e_ij, dtype=float)
+    vl, vr = np.asarray(left.v, dtype=float), np.asarray(right.v, dtype=float)
+    ul, ur = float(vl @ n), float(vr @ n)
+    rl, rr, pl, pr = left.rho, right.rho, left.p, right.p
+
+    def middle(sl, sr):
+        wl, wr = rl * (ul - sl), rr * (sr - ur)
+        return (rr * ur * (sr - ur) + rl * ul * (ul - sl) + pl - pr) / (wr + wl)
+
+    sl, sr = ul - left.c, ur + right.c
+    sm = middle(sl, sr)
+    if not sl < sm < sr:
+        sl = min(ul - left.c, ur - right.c)
+        sr = max(ul + left.c, ur + right.c)
+        sm = middle(sl, sr)
+    if sl >= sr:
+        raise SolverError(f"wave ordering violated: S_l={sl} >= S_r={sr}")
+    beta = min(max(ETA_HLLC * (ul - ur) / (0.5 * (left.c + right.c)), 0.0), 1.0)
+    wl, wr = rl * (ul - sl), rr * (sr - ur)
+    u_star = (wl * ul + wr * ur) / (wl + wr) + (pl - pr) * beta * beta / (wl + wr)
+    p_star = 0.5 * (pl + pr) + 0.5 * beta * (wr * (u_star - ur) + wl * (ul - u_star))
+    dl, dr = sl - sm, sr - sm
+    v_star = u_star * n + 0.5 * (vl + vr) - 0.5 * (ul + ur) * n
+    return RiemannStar(u_star, p_star, v_star, rl * (sl - ul) / dl, rr * (sr - ur) / dr,
+                       ((sl - ul) * left.etot - pl * ul + p_star * sm) / dl,
+                       ((sr - ur) * right.etot - pr * ur + p_star * sm) / dr,
+                       sl, sr, sm, beta)
+
+
+def dmr_shock_x(t: float, x0: float = 1.0 / 6.0) -> float:
+    """Where the double-Mach-reflection shock crosses the top edge at time
+    t (its foot at x0, 60 degrees, speed 10)."""
+    return x0 + (1.0 + 20.0 * t) / math.tan(math.radians(60.0))
+
+
+def apply_boundaries(state: "FluidState", ghosts: GhostLayer, eos: EosParams, t: float) -> None:
+    """Refresh the ghost rows of a HOST FluidState in place from its interior
+    at time t (module-level function of eulerian.py:371-447).  The solver
+    itself refreshes its device-resident ghosts (sphb_wc_ghosts /
+    sphb_hllc_ghosts); this is the host restatement for callers that hold a
+    FluidState."""
+    ni = state.n_interior
+    rho, mom, etot = state.rho, state.mom, state.etot
+    d = mom.shape[1]
+    kinds = np.asarray(ghosts.kind)
+    src = np.asarray(ghosts.src, dtype=np.int64)
+    vel = mom[:ni] / rho[:ni, None]
+    rows = np.arange(ni, ni + kinds.size)
+    for kind in np.unique(kinds):
+        sel = kinds == kind
+        at, s = rows[sel], src[sel]
+        if kind == G_FIXED:
+            f = np.asarray(ghosts.fixed)[sel]
+            rho[at], mom[at] = f[:, 0], f[:, 1:1 + d]
+            if etot is not None:
+                etot[at] = f[:, 1 + d]
+            continue
+        if kind == G_DMR_TOP:
+            par = ghosts.dmr
+            behind = (np.asarray(par["ghost_x"]) < dmr_shock_x(t, par["x0"]))[:, None]
+            full = np.where(behind, np.asarray(par["post"])[None, :],
+                            np.asarray(par["pre"])[None, :])
+            rho[at], mom[at] = full[:, 0], full[:, 1:1 + d]
+            if etot is not None:
+                etot[at] = full[:, 1 + d]
+            continue
+        vs = vel[s]
+        if kind == G_COPY:
+            vg = None
+        elif kind == G_WALL:
+            vg = np.asarray(ghosts.wall_v)[sel]
+        else:                           # mirror, full or blended, about the wall normal
+            nrm = np.asarray(ghosts.normal)[sel]
+            lam = 1.0 if kind == G_MIRROR else np.asarray(ghosts.blend)[sel][:, None]
+            vn = np.sum(vs * nrm, axis=1, keepdims=True) * nrm
+            vg = vs - 2.0 * vn if kind == G_MIRROR else vs - 2.0 * lam * vn
+        rho[at] = rho[s]
+        mom[at] = mom[s] if vg is None else rho[s, None] * vg
+        if etot is not None:
+            etot[at] = etot[s]
+            if kind == G_BLEND_MIRROR:  # keep the pressure, blend the kinetic energy
+                etot[at] -= 0.5 * rho[s] * (np.sum(vs**2, axis=1) - np.sum(vg**2, axis=1))
+
+
 @dataclass
 class FluidState:
     """Columnar conserved fields (eulerian.py:452-462)."""
@@ -215,8 +307,9 @@ class EulerianSolver:
             raise NotImplementedError("the HLLC path runs in FP64 on one GPU")
         if wall_force_tag is not None and (_slab is not None or precision != "fp64"):
             raise NotImplementedError("wall-force tagging runs in FP64 on one GPU")
-        if kernel.code != CODE_WENDLAND:
-            raise NotImplementedError("the WC engine evaluates the Wendland family")
+        wendland = kernel.code == CODE_WENDLAND
+        if not wendland and precision != "fp64":
+            raise NotImplementedError("the FP32 mode evaluates the Wendland family")
         torch = _lib.torch_cuda()
         self.pos = np.ascontiguousarray(positions, dtype=float)
         self.n, self.dim = self.pos.shape
@@ -275,7 +368,10 @@ class EulerianSolver:
             _slab.exchange(_dist, [b])
         # engine storage order (neighbors.engine_order): lattice order +
         # displacement-sorted rows, so warp gathers coalesce on lattices
-        variant = "geo" if self._ideal else os.environ.get("SPHB_WC_KERNEL", "global")
+        # other kernel families (Laguerre-Gauss) stream the reference per-pair
+        # geometry (sphb_wc_geometry evaluates any profile, kernels.py:41-59)
+        variant = ("geo" if self._ideal or not wendland
+                   else os.environ.get("SPHB_WC_KERNEL", "global"))
         self.order = self.bins
         # the fine key's spacing must be a global quantity (slab ranks must
         # order a shared layer identically): the particle volume's edge
@@ -957,6 +1053,36 @@ class EulerianSolver:
             torch.cuda.synchronize()
             self._graphs[key] = g
         return g, per
+
+    def viscous_rhs(self):
+        """Shear-viscosity momentum increment alone, mu sum_j viscv_ij
+        (v_i - v_j) over the reference CSR (eulerian.py:645-653), as an
+        (n, d) array with the ghost rows zero.  Evaluated on the device by
+        the CSR flux entry with the pressure / convective gradient set to
+        zero (sphb_rhs_wc_csr: drho and those terms vanish)."""
+        self._sync_in()
+        torch = _lib.torch_cuda()
+        nl = self.nlist
+        starts, idx, r, e = nl.device_csr()
+        k = self.kernel
+        vol = _lib.to_device(self._vol_host, torch.float64)
+        q = r / k.h
+        t = 1.0 - 0.5 * q
+        dw = torch.where(q <= k.kappa, (k.alpha / k.h) * (-5.0 * q * t**3),
+                         torch.zeros_like(q))                   # eulerian.py:509-513
+        viscv = (2.0 * dw / r * vol[idx.long()]).contiguous()
+        st = self.state
+        v = _lib.to_device(np.ascontiguousarray(st.velocity()), torch.float64)
+        rho = _lib.to_device(st.rho, torch.float64)
+        zeros_g = torch.zeros_like(e)
+        p = torch.zeros_like(rho)
+        drho = torch.empty(self.n, dtype=torch.float64, device=self._dev)
+        dmom = torch.zeros((self.n, self.dim), dtype=torch.float64, device=self._dev)
+        _lib.call("sphb_rhs_wc_csr", self.n_int, self.dim, starts.data_ptr(), idx.data_ptr(),
+                  e.data_ptr(), zeros_g.data_ptr(), viscv.data_ptr(), rho.data_ptr(),
+                  v.data_ptr(), p.data_ptr(), self.eos.c_art, self.mu, None, drho.data_ptr(),
+                  dmom.data_ptr(), None, _lib.stream_ptr())
+        return dmom.cpu().numpy()
 
     def totals(self):
         """(sum vol rho, sum vol mom, None) over the interior (eulerian.py:655-662)."""

@@ -184,8 +184,9 @@ class SolidSystem:
 
     def __init__(self, X0, material: Material, kernel: KernelSpec, dp: float, *, fixed=None,
                  correction: bool = True, cfl: float = 0.6, _slab=None, _grid=None, _dist=None):
-        if kernel.code != CODE_WENDLAND:
-            raise NotImplementedError("the TL engine evaluates the Wendland family")
+        # other kernel families (Laguerre-Gauss) stream the reference
+        # gradients g0 (sphb_tl_geometry evaluates any profile)
+        wendland = kernel.code == CODE_WENDLAND
         torch = _lib.torch_cuda()
         self.X0 = np.ascontiguousarray(X0, dtype=float)
         self.n, self.dim = self.X0.shape
@@ -285,8 +286,11 @@ class SolidSystem:
         # in a quarter of the free memory
         self.g0 = None
         g0_bytes = d * self.width * n * 8
-        if (os.environ.get("SPHB_TL_GEO", "0") != "0" and n and self.width
-                and g0_bytes < 0.25 * torch.cuda.mem_get_info()[0]):
+        if not wendland and g0_bytes >= 0.5 * torch.cuda.mem_get_info()[0]:
+            raise NotImplementedError("non-Wendland TL kernels stream g0, which does not fit")
+        if n and self.width and (not wendland or (
+                os.environ.get("SPHB_TL_GEO", "0") != "0"
+                and g0_bytes < 0.25 * torch.cuda.mem_get_info()[0])):
             self.g0 = torch.empty(g0_bytes // 8, dtype=torch.float64, device=dev)
             k = _lib.kernel_struct(kernel)
             _lib.call("sphb_tl_geometry", ctypes.byref(self.grid), n,

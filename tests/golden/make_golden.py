@@ -481,6 +481,77 @@ def main():
         arrays["n_side"] = np.array(32)
         save("retry", **arrays)
 
+    if want("surface"):
+        # ------ API surface beyond the hot path (eulerian.py:145-219, 366-447,
+        # 645-653): pairwise Riemann helpers, module-level apply_boundaries,
+        # dmr_shock_x, EulerianSolver.viscous_rhs
+        arrays = {}
+        rng = np.random.default_rng(17)
+        lin, hll = [], []
+        for k in range(40):
+            d = 2 + k % 2
+            e = rng.normal(size=d)
+            e /= np.linalg.norm(e)
+            st = []
+            for _ in range(2):
+                rho = 1.0 + 0.5 * rng.random()
+                v = tuple(rng.normal(scale=0.8, size=d))
+                p = 0.5 + rng.random()
+                c = float(np.sqrt(1.4 * p / rho))
+                etot = p / 0.4 + 0.5 * rho * float(np.dot(v, v))
+                st.append(eulerian.InterfaceState(rho=rho, v=v, p=p, c=c, etot=etot))
+            arrays[f"state{k}"] = np.array([[s_.rho, s_.p, s_.c, s_.etot] + list(s_.v) for s_ in st])
+            arrays[f"e{k}"] = e
+            for fn, out in ((eulerian.linearized_star, lin), (eulerian.hllc_star, hll)):
+                r = fn(st[0], st[1], e)
+                out.append([r.u_star, r.p_star, r.rho_star_l, r.rho_star_r, r.e_star_l,
+                            r.e_star_r, r.s_l, r.s_r, r.s_star, r.beta] + list(r.v_star)
+                           + [0.0] * (3 - d))
+        arrays["linearized"], arrays["hllc"] = np.array(lin), np.array(hll)
+        arrays["dmr_x"] = np.array([eulerian.dmr_shock_x(t) for t in (0.0, 0.05, 0.2)])
+        # module-level apply_boundaries on a mixed WC frame and on the DMR frame
+        from sph_trunc import cases
+
+        dp = 1.0 / 20
+        spec = kernel_spec("wendland-truncated", 1.3 * dp, 2)
+        eos = eulerian.EosParams(eulerian.WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0)
+        interior, gpos, ghosts = cases.build_rect_case(
+            (0, 0), (1, 1), dp, spec.kappa * spec.h,
+            {"y+": cases.SideSpec(eulerian.G_WALL, wall_v=(0.5, 0.0)),
+             "y-": cases.SideSpec(eulerian.G_MIRROR),
+             "x-": cases.SideSpec(eulerian.G_FIXED, fixed=(1.002, 0.3, 0.05, 0.0)),
+             "x+": cases.SideSpec(eulerian.G_COPY)}, eos)
+        bottom = ghosts.kind == eulerian.G_MIRROR
+        ghosts.kind[bottom & (gpos[:, 0] > 0.5)] = eulerian.G_BLEND_MIRROR
+        ghosts.blend = np.clip(gpos[:, 0] - 0.4, 0.0, 1.0)
+        n, ni = interior.shape[0] + gpos.shape[0], interior.shape[0]
+        rho = 1.0 + 0.002 * rng.standard_normal(n)
+        mom = 0.05 * rng.standard_normal((n, 2))
+        state = eulerian.FluidState(vol=np.full(n, dp * dp), rho=rho.copy(), mom=mom.copy(),
+                                    etot=None, n_interior=ni)
+        eulerian.apply_boundaries(state, ghosts, eos, 0.0)
+        arrays["wc_rho_in"], arrays["wc_mom_in"] = rho, mom
+        arrays["wc_rho_out"], arrays["wc_mom_out"] = state.rho, state.mom
+        case = cases.build_dmr(cases.CaseConfig(name="dmr", case="dmr", solver="euler-hllc",
+                                                dp=1.0 / 16, t_end=0.2,
+                                                kernel_family="wendland-truncated"))
+        st = case.solver.state
+        st.rho[:st.n_interior] *= 1.0 + 0.01 * rng.standard_normal(st.n_interior)
+        arrays["dmr_rho_in"], arrays["dmr_mom_in"] = st.rho.copy(), st.mom.copy()
+        arrays["dmr_etot_in"] = st.etot.copy()
+        eulerian.apply_boundaries(st, case.solver.ghosts, case.solver.eos, 0.07)
+        arrays["dmr_rho_out"], arrays["dmr_mom_out"] = st.rho, st.mom
+        arrays["dmr_etot_out"] = st.etot
+        # viscous_rhs on C2 at 32^2
+        cfg = configs.c2_tgv2d(kernel="1.6h", n_side=32)
+        nn = cfg["pos"].shape[0]
+        sv = eulerian.EulerianSolver(cfg["pos"], nn, eulerian.FluidState(
+            vol=cfg["vol"].copy(), rho=cfg["rho"].copy(), mom=cfg["mom"].copy(), etot=None,
+            n_interior=nn), eos, cfg["spec"], None, correction=True, cfl=cfg["cfl"],
+            mu=cfg["mu"], periodic_box=cfg["box"])
+        arrays["viscous_rhs"] = sv.viscous_rhs()
+        save("surface", **arrays)
+
 
 if __name__ == "__main__":
     main()

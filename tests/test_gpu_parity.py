@@ -919,3 +919,42 @@ def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwa
     for s in (fast, gen):
         errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
         assert max(errs) < 1e-10, errs
+
+
+# ------------------------------------------- non-Wendland flow / solid kernels
+def test_wc_laguerre_gauss_kernel_vs_oracle():
+    """EulerianSolver accepts any KernelSpec (eulerian.py:473-524): the
+    Laguerre-Gauss family runs the streamed reference-geometry stage."""
+    cfg = configs.c2_tgv2d(n_side=40)
+    cfg["spec"] = kernel_spec("laguerre-gauss", 1.3 * cfg["dp"], 2)
+    s = make_wc(cfg)
+    assert s.variant == "geo" and s.lattice is None
+    ref = O.EulerianWC(cfg["pos"], cfg["vol"], cfg["rho"], cfg["mom"], cfg["spec"],
+                       cfg["c_art"], cfg["rho0"], cfg["mu"], cfg["cfl"], cfg["box"])
+    d_g, m_g, _ = s.rhs()
+    d_r, m_r = ref.rhs()
+    assert l2_error(m_g, m_r) < 1e-12
+    for k in range(1, 21):
+        s.step()
+        ref.step()
+        if k == 1:
+            assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < TOL_1
+    assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
+    assert l2_error(s.state.mom, ref.mom) < 1e-10
+
+
+def test_tl_laguerre_gauss_kernel_vs_oracle():
+    """SolidSystem with the Laguerre-Gauss family (tlsph.py:129-156)."""
+    cfg = configs.c3_plate(dp=0.004)
+    cfg["spec"] = kernel_spec("laguerre-gauss", 1.15 * cfg["dp"], 2)
+    s = make_tl(cfg)
+    assert s.g0 is not None and s.lattice is None
+    m = cfg["material"]
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"])
+    ref.v = cfg["v0"].copy()
+    for _ in range(20):
+        s.step()
+        ref.step()
+    for a, b in ((s.x - s.X0, ref.x - ref.X0), (s.v, ref.v), (s.F, ref.F)):
+        assert l2_error(a, b) < 1e-10

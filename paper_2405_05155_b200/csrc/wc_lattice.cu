@@ -89,8 +89,8 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
   return v;
 }
 
-template <int D, int R2, int MINB>
-__global__ void __launch_bounds__(kLT, MINB)
+template <int D, int R2, int MINB, int NT = kLT>
+__global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
              const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
@@ -98,7 +98,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t n = P.n;
-  const int64_t i0 = P.row0 + (int64_t)blockIdx.x * kLT + threadIdx.x;
+  const int64_t i0 = P.row0 + (int64_t)blockIdx.x * NT + threadIdx.x;
   const bool own = i0 < P.row0 + P.nrows;
   // tail lanes redo the last row (no divergence in the pair loop), no write
   const int64_t i = own ? i0 : P.row0 + P.nrows - 1;
@@ -187,7 +187,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
       dm[q] = fma(-L.mv[k], dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
   });
 
-  wc_epilogue<D, kLT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
+  wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
 }
 
 // Proof of the specialisation for rows [row0, row0 + nrows): cnt == W, the
@@ -560,6 +560,27 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   // with 224 (more pairs in flight beat occupancy for both)
   const int minb = minb_env ? minb_env
                             : (p->dim == 3 ? (L->r2 == 4 ? 3 : 2) : 5);
+  // block size (tuning, SPHB_LAT_NT = 64 / 256; 3D only): same register
+  // budget per thread, blocks of NT threads
+  static const int nt_env = [] {
+    const char* e = getenv("SPHB_LAT_NT");
+    return e ? atoi(e) : 0;
+  }();
+  if (p->dim == 3 && (nt_env == 64 || nt_env == 256)) {
+    const unsigned g2 = sphb_blocks(p->nrows, nt_env);
+#define SPHB_NT(R, MB, NT)                                                                 \
+    k_wc_lattice<3, R, MB, NT><<<g2, NT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout,  \
+                                                  Mout, scalars, err)
+    const bool r4 = L->r2 == 4;
+    if (nt_env == 64) {
+      if (r4) SPHB_NT(4, 3, 64); else SPHB_NT(6, 2, 64);
+    } else {
+      if (r4) SPHB_NT(4, 3, 256); else SPHB_NT(6, 2, 256);
+    }
+#undef SPHB_NT
+    SPHB_LAUNCH_CHECK();
+    return SPHB_OK;
+  }
 #define SPHB_S(D, R)                                                                   \
   if (p->dim == D && L->r2 == R) {                                                     \
     switch (minb) {                                                                    \

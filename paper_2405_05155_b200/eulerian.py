@@ -533,17 +533,21 @@ class EulerianSolver:
         h, mu = self.kernel.h, self.mu
         c5s = -5.0 * self.kernel.alpha / h
         cg2, cm = -(c5s * vol / h), 2.0 * mu * c5s * vol / h
-        for k in range(width):
+        # the canonical order is mirrored (slot width-1-k holds -o_k): the
+        # table is made exactly antisymmetric (the check bounds what that
+        # changes), so the kernel may serve o and -o from one entry
+        for k in range(width // 2):
             dx = xw[0] - xw[1 + k]
             dx = np.where(dx > 0.5 * box, dx - box, np.where(dx < -0.5 * box, dx + box, dx))
             r = math.sqrt(float(np.sum(dx * dx)))
             t = 1.0 - 0.5 * r / h
             base = (t * t) * t
-            for a in range(d):
-                L.dx[k][a] = float(dx[a])
-            L.inv_r[k] = 1.0 / r
-            L.g2[k] = cg2 * base
-            L.mv[k] = cm * base
+            for kk, sgn in ((k, 1.0), (width - 1 - k, -1.0)):
+                for a in range(d):
+                    L.dx[kk][a] = sgn * float(dx[a])
+                L.inv_r[kk] = 1.0 / r
+                L.g2[kk] = cg2 * base
+                L.mv[kk] = cm * base
         bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
         _lib.call("sphb_wc_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
                   self.X.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),

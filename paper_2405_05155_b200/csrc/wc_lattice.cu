@@ -89,7 +89,7 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
   return v;
 }
 
-template <int D, int R2, int MINB, int NT = kLT, bool SYM = false>
+template <int D, int R2, int MINB, int NT = kLT>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -129,9 +129,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
 #pragma unroll
   for (int q = 0; q < D; ++q) dm[q] = 0.0;
 
-  // one directed pair (i, j) at canonical slot k (offset o, compile-time);
-  // `flip` negates the tabled displacement (SYM: the slot of -o)
-  auto pair = [&](auto kc, const int64_t j, const unsigned long long flip) {
+  // one directed pair (i, j) at canonical slot k (offset o, compile-time)
+  auto pair = [&](auto kc, const int64_t j) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
     double vj[D], rho_j;
@@ -144,8 +143,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
     double dx[D];
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      dx[q] = o[q] == 0 ? 0.0
-                        : __longlong_as_double(__double_as_longlong(L.dx[k][q]) ^ flip);
+      dx[q] = o[q] == 0 ? 0.0 : L.dx[k][q];
     const double inv_r = L.inv_r[k];
     double G_[D];                                     // (B_i + B_j) dx, nonzero columns
 #pragma unroll
@@ -190,29 +188,11 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
       dm[q] = fma(-L.mv[k], dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
   };
 
-  if constexpr (!SYM) {
-    static_for<St::W>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-      pair(kc, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]), 0ull);
-    });
-  } else {
-    // SYM: the canonical order lists o and -o mirrored (slot W-1-k holds -o),
-    // so one loop body over the first half serves both signs, halving the
-    // unrolled code (instruction-cache pressure); the table is antisymmetric
-#pragma unroll 1
-    for (int sgn = 0; sgn < 2; ++sgn) {
-      const unsigned long long flip = sgn ? 0x8000000000000000ull : 0ull;
-      static_for<St::W / 2>([&](auto kc) {
-        constexpr int k = decltype(kc)::value;
-        constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-        const int jx = sgn ? xs[R - o[0]] : xs[R + o[0]];
-        const int jy = sgn ? ys[R - o[1]] : ys[R + o[1]];
-        const int jz = sgn ? zs[R - o[2]] : zs[R + o[2]];
-        pair(kc, (int64_t)(jx + jy + jz), flip);
-      });
-    }
-  }
+  static_for<St::W>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+    pair(kc, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]));
+  });
 
   wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
 }
@@ -597,20 +577,6 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   // (one block, 8 warps per SM) measured fastest (13.35 -> 11.96 ms/step,
   // profiles/r02_tune_lattice.md)
   const int nt = nt_env ? nt_env : (p->dim == 3 && L->r2 == 6 && !minb_env ? 256 : 0);
-  static const bool sym = [] {           // SPHB_LAT_SYM=1: mirrored half loop (tuning)
-    const char* e = getenv("SPHB_LAT_SYM");
-    return e && atoi(e) == 1;
-  }();
-  if (p->dim == 3 && sym) {
-    if (L->r2 == 4)
-      k_wc_lattice<3, 4, 3, kLT, true><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn,
-                                                            Sout, Mout, scalars, err);
-    else
-      k_wc_lattice<3, 6, 2, 256, true><<<sphb_blocks(p->nrows, 256), 256, 0, st>>>(
-          *p, K, *L, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err);
-    SPHB_LAUNCH_CHECK();
-    return SPHB_OK;
-  }
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);
 #define SPHB_NT(R, MB, NT)                                                                 \

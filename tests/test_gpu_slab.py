@@ -142,7 +142,7 @@ def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, mode):
     want_rho, want_mom = ref.state.rho, ref.state.mom
 
     shared = Shared(world)
-    results, errors = {}, []
+    results, errors, lattice = {}, [], {}
 
     def run(rank):
         try:
@@ -154,6 +154,7 @@ def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, mode):
                                   periodic_box=cfg["box"])
                 assert (s._push is not None) == push
                 assert (s._overlap is not None) == (mode == "overlap")
+                lattice[rank] = s.lattice is not None      # checked per rank (owned rows)
                 s.advance(steps)
                 results[rank] = s.owned()
                 torch.cuda.current_stream().synchronize()
@@ -168,6 +169,8 @@ def test_slab_solver_matches_single_gpu(monkeypatch, world, kernel, mode):
         t.join()
     if errors:
         raise errors[0]
+    # the TGV slabs are lattices: every rank runs the WC lattice kernel
+    assert ref.lattice is not None and all(lattice.values()), lattice
     got_rho = np.full_like(want_rho, np.nan)
     got_mom = np.full_like(want_mom, np.nan)
     for ids, rho, mom in results.values():

@@ -283,14 +283,42 @@ def c4_leg(torch, steps, warmup, peak):
         n = s.n
         pairs = int(s.cnt.sum().item())
         rec = {"ms_per_step": ms, "value": n / (ms * 1e-3), "particles": n,
-               "pair_interactions_per_s": 2 * pairs / (ms * 1e-3), "steps": k}
+               "pair_interactions_per_s": 2 * pairs / (ms * 1e-3), "steps": k,
+               "lattice_path": s.lattice is not None}
         if key == "1.6h":
             gbs = C4_BYTES_STEP * n / (ms * 1e-3) / 1e9
             rec["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
                                "frac": gbs / peak}
+            ref_state = (s.x - s.X0, s.v, s.F)
+            steps_done = s.steps
         out[key.replace(".", "p")] = rec
         del s
         torch.cuda.empty_cache()
+        if key == "1.6h":           # optional FP32 mode, its error vs FP64 reported beside
+            from paper_2405_05155_b200.approx import l2_error
+
+            s32 = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"],
+                              fixed=cfg["fixed"], cfl=cfg["cfl"], precision="fp32")
+            s32.v = cfg["v0"]
+            s32.advance(max(warmup, 8))
+            torch.cuda.synchronize()
+            e0.record()
+            s32.advance(k)
+            e1.record()
+            torch.cuda.synchronize()
+            ms32 = e0.elapsed_time(e1) / k
+            assert s32.steps == steps_done
+            got = (s32.x - s32.X0, s32.v, s32.F)
+            out["fp32_mode_1p6h"] = {
+                "ms_per_step": ms32, "value": n / (ms32 * 1e-3),
+                "error_vs_fp64": {name: l2_error(a, b) for name, a, b in
+                                  zip(("rel_l2_displacement", "rel_l2_v", "rel_l2_F"), got,
+                                      ref_state)},
+                "after_steps": steps_done,
+                "note": "FP32 companions of the gathered v_half / Q records, FP64 arithmetic "
+                        "and state; reported separately, not the headline"}
+            del s32
+            torch.cuda.empty_cache()
     out["alpha_T1p6h_over_T2h"] = out["1p6h"]["ms_per_step"] / out["2h"]["ms_per_step"]
     return out
 

@@ -500,6 +500,18 @@ typedef struct sphb_tl_params {
    * one row touches consecutive records; q_stride >= n, 0 means n.  Slab
    * ranks use one common stride so pushes address peer buffers with it. */
   int64_t q_stride;
+  /* Optional FP32 mode (lattice passes only): FP32 companions of the
+   * gathered records — vh32 (float4 per particle, written by the kick) and
+   * q32 (three float4 column planes of stride q_stride, {q_0c, q_1c, q_2c,
+   * 0}, written instead of Q by pass A / sphb_tl_stress and read by pass B);
+   * arithmetic and state stay FP64.  NULL: FP64 records. */
+  float* vh32;
+  float* q32;
+  /* Material law of the PK2 stress: 0 = St. Venant-Kirchhoff (tlsph.py:54-65),
+   * 1 = compressible Neo-Hookean S = G (I - C^-1) + lam ln(J) C^-1 (BASELINE
+   * configs 3-4; not in the reference). */
+  int32_t law;
+  int32_t reserved_law;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows

@@ -637,9 +637,16 @@ class EulerianHLLC(EulerianWC):
 
 # ------------------------------------------------------------ TL-SPH
 class SolidTL:
-    """SolidSystem (tlsph.py:129-206) with SVK stress."""
+    """SolidSystem (tlsph.py:129-206) with SVK stress; law="neo-hookean"
+    selects the compressible Neo-Hookean law S = G (I - C^-1) +
+    lam ln(J) C^-1 of BASELINE configs 3-4 — NOT reference-backed (the
+    reference implements SVK only): a numpy statement of the
+    textbook law, checked against its stored-energy derivative in
+    tests/test_host_api.py."""
 
-    def __init__(self, X0, rho0, E, nu, spec, dp, fixed=None, correction=True, cfl=0.6):
+    def __init__(self, X0, rho0, E, nu, spec, dp, fixed=None, correction=True, cfl=0.6,
+                 law="svk"):
+        self.law = law
         self.X0 = np.ascontiguousarray(X0, dtype=float)
         self.n, self.d = self.X0.shape
         self.spec, self.dp, self.cfl, self.rho0 = spec, dp, cfl, rho0
@@ -665,9 +672,15 @@ class SolidTL:
         """P B0^T with P = F S, SVK S (tlsph.py:54-65, 160-167), rows sl."""
         eye = np.eye(self.d)
         F = self.F[sl]
-        strain = 0.5 * (np.einsum("nba,nbc->nac", F, F) - eye)
-        tr = np.trace(strain, axis1=1, axis2=2)
-        s = self.lam * tr[:, None, None] * eye + 2.0 * self.g * strain
+        if self.law == "neo-hookean":
+            C = np.einsum("nba,nbc->nac", F, F)
+            ci = np.linalg.inv(C)
+            ln_j = 0.5 * np.log(np.linalg.det(C))
+            s = self.g * (eye - ci) + self.lam * ln_j[:, None, None] * ci
+        else:
+            strain = 0.5 * (np.einsum("nba,nbc->nac", F, F) - eye)
+            tr = np.trace(strain, axis1=1, axis2=2)
+            s = self.lam * tr[:, None, None] * eye + 2.0 * self.g * strain
         P = np.einsum("nab,nbc->nac", F, s)
         return np.einsum("nab,ncb->nac", P, self.B0[sl])
 

@@ -145,6 +145,10 @@ class TLParams(C.Structure):
         ("push_hi1", C.c_int64),
         ("push_next_at", C.c_int64),
         ("q_stride", C.c_int64),
+        ("vh32", C.c_void_p),
+        ("q32", C.c_void_p),
+        ("law", C.c_int32),
+        ("reserved_law", C.c_int32),
     ]
 
 

@@ -241,6 +241,119 @@ __device__ __forceinline__ void svk_q(const double (&F)[D][D], const double (&B0
     }
 }
 
+// FP32 companion of Q (FP32 mode): float4 column planes {q_0c, q_1c, q_2c, 0}
+// (3D) or one float4 {q00, q01, q10, q11} (2D).
+template <int D>
+__device__ __forceinline__ void store_q32(float* Q32, int64_t qs, int64_t i,
+                                          const double (&a)[D][D]) {
+  float4* q = reinterpret_cast<float4*>(Q32);
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      q[c * qs + i] = make_float4((float)a[0][c], (float)a[1][c], (float)a[2][c], 0.f);
+  } else if constexpr (D == 2) {
+    q[i] = make_float4((float)a[0][0], (float)a[0][1], (float)a[1][0], (float)a[1][1]);
+  } else {
+    q[i] = make_float4((float)a[0][0], 0.f, 0.f, 0.f);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_q32(const float* Q32, int64_t qs, int64_t i,
+                                         double (&a)[D][D]) {
+  const float4* q = reinterpret_cast<const float4*>(Q32);
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float4 t = __ldg(q + c * qs + i);
+      a[0][c] = t.x; a[1][c] = t.y; a[2][c] = t.z;
+    }
+  } else if constexpr (D == 2) {
+    const float4 t = __ldg(q + i);
+    a[0][0] = t.x; a[0][1] = t.y; a[1][0] = t.z; a[1][1] = t.w;
+  } else {
+    a[0][0] = __ldg(q + i).x;
+  }
+}
+
+// Compressible Neo-Hookean PK2 stress S = G (I - C^-1) + lam ln(J) C^-1,
+// C = F^T F, J = det F (BASELINE configs 3-4; not in the
+// reference), then Q = (F S) B0^T as for SVK.
+template <int D>
+__device__ __forceinline__ void neo_hookean_q(const double (&F)[D][D], const double (&B0)[D][D],
+                                              double lam, double g, double (&Q)[D][D]) {
+  double Cm[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(F[b][a], F[b][c], s);
+      Cm[a][c] = s;
+    }
+  double Ci[D][D];                  // C^-1 by the adjugate (C is symmetric positive definite)
+  double detC;
+  if constexpr (D == 1) {
+    detC = Cm[0][0];
+    Ci[0][0] = 1.0 / detC;
+  } else if constexpr (D == 2) {
+    detC = Cm[0][0] * Cm[1][1] - Cm[0][1] * Cm[1][0];
+    const double inv = 1.0 / detC;
+    Ci[0][0] = Cm[1][1] * inv; Ci[1][1] = Cm[0][0] * inv;
+    Ci[0][1] = -Cm[0][1] * inv; Ci[1][0] = -Cm[1][0] * inv;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int a1 = (a + 1) % 3, a2 = (a + 2) % 3, c1 = (c + 1) % 3, c2 = (c + 2) % 3;
+        Ci[c][a] = Cm[a1][c1] * Cm[a2][c2] - Cm[a1][c2] * Cm[a2][c1];   // cofactor^T
+      }
+    detC = Cm[0][0] * Ci[0][0] + Cm[0][1] * Ci[1][0] + Cm[0][2] * Ci[2][0];
+    const double inv = 1.0 / detC;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Ci[a][c] *= inv;
+  }
+  const double lnJ = 0.5 * log(detC);
+  double S[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) S[a][c] = g * ((a == c ? 1.0 : 0.0) - Ci[a][c]) + lam * lnJ * Ci[a][c];
+  double Pm[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(F[a][b], S[b][c], s);
+      Pm[a][c] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) s = fma(Pm[a][b], B0[c][b], s);
+      Q[a][c] = s;
+    }
+}
+
+// Q = P B0^T of the material law in P.law
+template <int D>
+__device__ __forceinline__ void stress_q(const sphb_tl_params& P, const double (&F)[D][D],
+                                         const double (&B0)[D][D], double (&Q)[D][D]) {
+  if (P.law == 1)
+    neo_hookean_q<D>(F, B0, P.lam, P.g, Q);
+  else
+    svk_q<D>(F, B0, P.lam, 2.0 * P.g, Q);
+}
+
 // Pass A after the pair loop (tlsph.py:191-199, 54-65, 160-167): F_i += dt
 // (m B0_i), det F > 0, Q_i = (F S) B0^T with X0_i in the row padding (+ the
 // fused halo push), x_i += dt v_half_i.  m = sum_j (v_half_j - v_half_i) (x) g0_ij.
@@ -267,10 +380,13 @@ __device__ __forceinline__ void tl_a_finish(const sphb_tl_params& P, int64_t i,
   const double J = det_mat<D>(Fi);
   if (!(J > 0.0)) atomicOr(err, SPHB_EFLAG_DET_NONPOS);
   double Qi[D][D];
-  svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
+  stress_q<D>(P, Fi, B, Qi);
   store_f<D>(F, n, i, Fi);
   const int64_t qs = P.q_stride ? P.q_stride : n;
-  store_q<D>(Q, qs, i, Qi, wi);
+  if (P.q32)
+    store_q32<D>(P.q32, qs, i, Qi);
+  else
+    store_q<D>(Q, qs, i, Qi, wi);
   {   // fused halo push of the boundary layers' Q records
     bool pushed = false;
     if (P.push_q_prev && i >= P.push_lo0 && i < P.push_lo1) {
@@ -307,7 +423,10 @@ __device__ __forceinline__ double tl_b_finish(const sphb_tl_params& P, int64_t i
   const int64_t qs = P.q_stride ? P.q_stride : n;
   const double inv_rho0 = 1.0 / P.rho0;
   double Qi[D][D];                  // loaded after the loop: 18 registers free in it
-  load_q<D>(Q, qs, i, Qi);
+  if (P.q32)
+    load_q32<D>(P.q32, qs, i, Qi);
+  else
+    load_q<D>(Q, qs, i, Qi);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     double s = acc[a];

@@ -50,7 +50,8 @@ inline int tl_stage_max_width() {
 // gathers one half-step velocity record per pair instead of v_j and a_j.
 template <int D>
 __global__ void k_tl_kick(int64_t n, const double4* __restrict__ V, const double4* __restrict__ A,
-                          double4* __restrict__ Vh, const double* __restrict__ scalars) {
+                          double4* __restrict__ Vh, const double* __restrict__ scalars,
+                          float4* __restrict__ Vh32) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double hdt = 0.5 * scalars[0];
@@ -64,6 +65,12 @@ __global__ void k_tl_kick(int64_t n, const double4* __restrict__ V, const double
 #pragma unroll
   for (int a = 0; a < D; ++a) vh[a] = fixed ? 0.0 : fma(hdt, a_[a], v[a]);
   store_vec<D>(Vh, i, vh);
+  if (Vh32) {                       // FP32 mode: the gathered companion
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) c[a] = (float)vh[a];
+    Vh32[i] = make_float4(c[0], c[1], c[2], c[3]);
+  }
 }
 
 // UNR: pairs in flight per thread; 3D default 2 (two Vh_j + X0_j gather
@@ -219,8 +226,9 @@ __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ 
   load_f<D>(F, P.n, i, Fi);
   load_b0<D>(B0, P.n, i, B);
   load_x0<D>(X0, i, w, fixed);
-  svk_q<D>(Fi, B, P.lam, 2.0 * P.g, Qi);
+  stress_q<D>(P, Fi, B, Qi);
   store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);
+  if (P.q32) store_q32<D>(P.q32, P.q_stride ? P.q_stride : P.n, i, Qi);
 }
 
 template <int D>
@@ -335,7 +343,7 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars);
+  TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars, (float4*)p->vh32);
   static const int var = tl_variant("SPHB_TL_VARIANT_A");
   if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
     TL_TUNED(k_tl_pass_a, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
@@ -375,7 +383,7 @@ extern "C" int sphb_tl_kick(const sphb_tl_params* p, const double* v, const doub
   if (p->n == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a,
-              (double4*)vh, scalars);
+              (double4*)vh, scalars, (float4*)p->vh32);
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }

@@ -119,9 +119,38 @@ __device__ __forceinline__ void axis_displacements(const double4* __restrict__ X
     }
 }
 
+// neighbour gathers of the FP64 records or, in the FP32 mode, of their
+// FP32 companions (sphb_tl_params.vh32 / q32)
+template <int D, bool F32>
+__device__ __forceinline__ void gather_vh(const sphb_tl_params& P, const double4* __restrict__ Vh,
+                                          int64_t j, double (&v)[D]) {
+  if constexpr (F32) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(P.vh32) + j);
+    const float c[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = c[a];
+  } else {
+    load_vec_nc<D>(Vh, j, v);
+  }
+}
+
+// column c of Q_j (3D)
+template <bool F32>
+__device__ __forceinline__ void gather_qcol(const sphb_tl_params& P, const double4* __restrict__ Q,
+                                            int64_t qs, int c, int64_t j, double& q0, double& q1,
+                                            double& q2, double& w) {
+  if constexpr (F32) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(P.q32) + c * qs + j);
+    q0 = t.x; q1 = t.y; q2 = t.z; w = 0.0;
+  } else {
+    const double4 t = ldg4(Q + c * qs + j);
+    q0 = t.x; q1 = t.y; q2 = t.z; w = t.w;
+  }
+}
+
 // Shell row of pass A: the general pair loop (tl_engine.cu k_tl_pass_a,
 // unstaged) — pass list, X0_j gather, g0 recomputed (ref_gradient).
-template <int D>
+template <int D, bool F32>
 __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
                                         const double4* __restrict__ X0,
                                         const double4* __restrict__ B0,
@@ -148,7 +177,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
     SPHB_CHECK_INDEX(j, n, err);
     double vhj[D], wj[D], dx[D], g[D];
     bool fixed_j;
-    load_vec_nc<D>(Vh, j, vhj);
+    gather_vh<D, F32>(P, Vh, j, vhj);
     load_x0<D>(X0, j, wj, fixed_j);
 #pragma unroll
     for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
@@ -164,7 +193,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
 }
 
 // Shell row of pass B (tl_engine.cu k_tl_pass_b, unstaged); returns |v_i|.
-template <int D>
+template <int D, bool F32>
 __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
                                           const double4* __restrict__ X0,
                                           const int32_t* __restrict__ nbr,
@@ -189,14 +218,17 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
     double Qj[D][D], wj[D];
     if constexpr (D == 3) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double4 t4 = ldg4(Q + c * qs + j);
-        Qj[0][c] = t4.x; Qj[1][c] = t4.y; Qj[2][c] = t4.z;
-        wj[c] = t4.w;
+      for (int c = 0; c < 3; ++c) gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], wj[c]);
+      if constexpr (F32) {        // the FP32 companion carries no X0 padding
+        bool fixed_j;
+        load_x0<D>(X0, j, wj, fixed_j);
       }
     } else {
       bool fixed_j;
-      load_mat_nc<D>(Q, j, Qj);
+      if constexpr (F32)
+        load_q32<D>(P.q32, qs, j, Qj);
+      else
+        load_mat_nc<D>(Q, j, Qj);
       load_x0<D>(X0, j, wj, fixed_j);
     }
     double dx[D], g[D];
@@ -213,7 +245,7 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
   return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
 }
 
-template <int D, int R2, int MINB>
+template <int D, int R2, int MINB, bool F32>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const double4* __restrict__ B0,
@@ -226,8 +258,8 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
   if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
     const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
-    if (ts < L.n_shell) shell_a<D>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q,
-                                   scalars[0], err);
+    if (ts < L.n_shell) shell_a<D, F32>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q,
+                                        scalars[0], err);
     return;
   }
   const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
@@ -253,7 +285,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
     const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
                       (int64_t)o[2] * row.stride[2];
     double vhj[D];
-    load_vec_nc<D>(Vh, j, vhj);
+    gather_vh<D, F32>(P, Vh, j, vhj);
     double dx[D];
     double r2 = 0.0;
 #pragma unroll
@@ -273,7 +305,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
 }
 
-template <int D, int R2, int MINB>
+template <int D, int R2, int MINB, bool F32>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
@@ -288,7 +320,8 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
   if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
     const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
     if (ts < L.n_shell)
-      speed = shell_b<D>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V, scalars, update_v);
+      speed = shell_b<D, F32>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V, scalars,
+                              update_v);
   } else if (t < L.n_interior) {
     const Row<D, R> row(L, t);
     const int64_t i = row.i;
@@ -311,14 +344,17 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           if (o[c] != 0) {
-            const double4 t4 = ldg4(Q + c * qs + j);
-            Qj[0][c] = t4.x; Qj[1][c] = t4.y; Qj[2][c] = t4.z;
+            double w_unused;
+            gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], w_unused);
           } else {
             Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
           }
         }
       } else {
-        load_mat_nc<D>(Q, j, Qj);
+        if constexpr (F32)
+          load_q32<D>(P.q32, qs, j, Qj);
+        else
+          load_mat_nc<D>(Q, j, Qj);
       }
       double dx[D];
       double r2 = 0.0;
@@ -480,11 +516,17 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = tl_minb("SPHB_TLAT_MINB_A", 4);
+  const bool f32 = p->vh32 && p->q32;
   const unsigned grid = lattice_grid(L);
 #define SPHB_A1(D, R, MB)                                                                   \
-  k_tl_lattice_a<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,                \
-      (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
-      (double4*)q, scalars, err);                                                           \
+  if (f32)                                                                                  \
+    k_tl_lattice_a<D, R, MB, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,        \
+        (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,        \
+        (double4*)q, scalars, err);                                                         \
+  else                                                                                      \
+    k_tl_lattice_a<D, R, MB, false><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,       \
+        (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,        \
+        (double4*)q, scalars, err);                                                         \
   break
 #define SPHB_A(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
@@ -514,11 +556,17 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = tl_minb("SPHB_TLAT_MINB_B", 4);
+  const bool f32 = p->vh32 && p->q32;
   const unsigned grid = lattice_grid(L);
 #define SPHB_B1(D, R, MB)                                                                   \
-  k_tl_lattice_b<D, R, MB><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr, cnt,      \
-      (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,             \
-      (int)update_v);                                                                       \
+  if (f32)                                                                                  \
+    k_tl_lattice_b<D, R, MB, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,   \
+        cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,      \
+        (int)update_v);                                                                     \
+  else                                                                                      \
+    k_tl_lattice_b<D, R, MB, false><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,  \
+        cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,      \
+        (int)update_v);                                                                     \
   break
 #define SPHB_B(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \

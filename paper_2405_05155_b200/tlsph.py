@@ -47,11 +47,26 @@ def lame_params(E: float, nu: float) -> tuple[float, float]:
     return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), E / (2.0 * (1.0 + nu))
 
 
+SVK = "svk"
+NEO_HOOKEAN = "neo-hookean"
+LAWS = {SVK: 0, NEO_HOOKEAN: 1}
+
+
 @dataclass(frozen=True)
 class Material:
+    """Elastic material (tlsph.py:27-51).  `law` is an extension: the
+    reference implements St. Venant-Kirchhoff only; "neo-hookean" selects
+    the compressible Neo-Hookean law BASELINE's configs 3-4 name
+    (S = G (I - C^-1) + lam ln(J) C^-1; not reference-backed)."""
+
     rho0: float
     E: float
     nu: float
+    law: str = SVK
+
+    def __post_init__(self):
+        if self.law not in LAWS:
+            raise ValueError(f"unknown material law {self.law!r}; expected one of {tuple(LAWS)}")
 
     @property
     def lame(self) -> tuple[float, float]:
@@ -64,14 +79,21 @@ class Material:
 
 
 def pk2_stress(F, material: Material):
-    """SVK second Piola-Kirchhoff stress lam tr(E) I + 2 G E (tlsph.py:54-65)."""
+    """Second Piola-Kirchhoff stress: SVK lam tr(E) I + 2 G E
+    (tlsph.py:54-65), or the compressible Neo-Hookean law of `material`."""
     F = np.asarray(F, dtype=float)
     lam, g = material.lame
     batch = F if F.ndim == 3 else F[None]
     eye = np.eye(batch.shape[-1])
-    strain = 0.5 * (np.einsum("nba,nbc->nac", batch, batch) - eye)
-    tr = np.trace(strain, axis1=1, axis2=2)
-    s = lam * tr[:, None, None] * eye + 2.0 * g * strain
+    C = np.einsum("nba,nbc->nac", batch, batch)
+    if getattr(material, "law", SVK) == NEO_HOOKEAN:
+        ci = np.linalg.inv(C)
+        ln_j = 0.5 * np.log(np.linalg.det(C))
+        s = g * (eye - ci) + lam * ln_j[:, None, None] * ci
+    else:
+        strain = 0.5 * (C - eye)
+        tr = np.trace(strain, axis1=1, axis2=2)
+        s = lam * tr[:, None, None] * eye + 2.0 * g * strain
     return s if F.ndim == 3 else s[0]
 
 
@@ -183,7 +205,8 @@ class SolidSystem:
     """Reference configuration, state and fused passes for one solid body."""
 
     def __init__(self, X0, material: Material, kernel: KernelSpec, dp: float, *, fixed=None,
-                 correction: bool = True, cfl: float = 0.6, _slab=None, _grid=None, _dist=None):
+                 correction: bool = True, cfl: float = 0.6, precision: str = "fp64",
+                 _slab=None, _grid=None, _dist=None):
         # other kernel families (Laguerre-Gauss) stream the reference
         # gradients g0 (sphb_tl_geometry evaluates any profile)
         wendland = kernel.code == CODE_WENDLAND
@@ -278,6 +301,7 @@ class SolidSystem:
         p.h, p.alpha, p.kappa = kernel.h, kernel.alpha, kernel.kappa
         p.vol0, p.rho0, p.lam, p.g = self.dp**d, self.rho0, lam, g
         p.q_stride = self._q_stride
+        p.law = LAWS[getattr(material, "law", SVK)]
         self._cfl_h = self.cfl * kernel.h
         self._c_s = material.sound_speed
         # reference gradients g0: recomputed per pair from X0 by default (with
@@ -302,6 +326,19 @@ class SolidSystem:
         if (_slab is None and self.g0 is None and self.order is not self.bins
                 and os.environ.get("SPHB_TL_LATTICE", "1") != "0"):
             self._setup_lattice()
+        # optional FP32 mode (north star): FP32 companions of the gathered
+        # records (v_half, Q) on the lattice passes; FP64 arithmetic and state
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        self.precision = precision
+        if precision == "fp32":
+            if self.lattice is None:
+                raise NotImplementedError("the TL FP32 mode runs on the lattice passes "
+                                          "(a lattice reference configuration, one GPU)")
+            self.Vh32 = torch.zeros((n, 4), dtype=torch.float32, device=dev)
+            self.Q32 = torch.zeros((3 if d == 3 else 1, self._q_stride, 4),
+                                   dtype=torch.float32, device=dev)
+            p.vh32, p.q32 = self.Vh32.data_ptr(), self.Q32.data_ptr()
         self._setup_push(dev)
         self._acc_valid = False
         self._host = {}
@@ -637,10 +674,21 @@ class SolidSystem:
         return von_mises(self.F, s)
 
     def energies(self):
-        _, s = self.first_pk()
+        """(kinetic, strain) energy; strain energy 1/2 S:E for SVK, the
+        stored energy G/2 (tr C - d) - G ln J + lam/2 (ln J)^2 for
+        Neo-Hookean."""
         eye = np.eye(self.dim)
-        strain = 0.5 * (np.einsum("nba,nbc->nac", self.F, self.F) - eye)
-        e_strain = 0.5 * float(np.sum(self.vol0 * np.einsum("nab,nab->n", s, strain)))
+        C = np.einsum("nba,nbc->nac", self.F, self.F)
+        if getattr(self.material, "law", SVK) == NEO_HOOKEAN:
+            lam, g = self.material.lame
+            ln_j = 0.5 * np.log(np.linalg.det(C))
+            w = 0.5 * g * (np.trace(C, axis1=1, axis2=2) - self.dim) - g * ln_j \
+                + 0.5 * lam * ln_j**2
+            e_strain = float(np.sum(self.vol0 * w))
+        else:
+            _, s = self.first_pk()
+            strain = 0.5 * (C - eye)
+            e_strain = 0.5 * float(np.sum(self.vol0 * np.einsum("nab,nab->n", s, strain)))
         e_kin = 0.5 * float(np.sum(self.rho0 * self.vol0 * np.sum(self.v**2, axis=1)))
         return e_kin, e_strain
 

@@ -958,3 +958,56 @@ def test_tl_laguerre_gauss_kernel_vs_oracle():
         ref.step()
     for a, b in ((s.x - s.X0, ref.x - ref.X0), (s.v, ref.v), (s.F, ref.F)):
         assert l2_error(a, b) < 1e-10
+
+
+# ------------------------------------- Neo-Hookean law (BASELINE configs 3-4)
+@pytest.mark.parametrize("label,builder,kwargs", [("c3", configs.c3_plate, {"dp": 0.004}),
+                                                  ("c4", configs.c4_column, {"n_width": 8})])
+@pytest.mark.parametrize("lattice", ["1", "0"])
+def test_tl_neo_hookean_vs_oracle(monkeypatch, label, builder, kwargs, lattice):
+    """The optional compressible Neo-Hookean law (not in the reference; the
+    oracle's numpy statement of it, checked against its energy in
+    test_host_api.py) on the lattice and general passes."""
+    from paper_2405_05155_b200.tlsph import NEO_HOOKEAN
+
+    monkeypatch.setenv("SPHB_TL_LATTICE", lattice)
+    cfg = builder(**kwargs)
+    m = cfg["material"]
+    mat = Material(m.rho0, m.E, m.nu, law=NEO_HOOKEAN)
+    s = SolidSystem(cfg["X0"], mat, cfg["spec"], cfg["dp"], fixed=cfg["fixed"], cfl=cfg["cfl"])
+    s.v = cfg["v0"].copy()
+    assert (s.lattice is not None) == (lattice == "1")
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"], law="neo-hookean")
+    ref.v = cfg["v0"].copy()
+    s.step()
+    ref.step()
+    for a, b in ((s.x - s.X0, ref.x - ref.X0), (s.v, ref.v), (s.F, ref.F)):
+        assert l2_error(a, b) < TOL_1
+    s.advance(99)
+    for _ in range(99):
+        ref.step()
+    for a, b in ((s.x - s.X0, ref.x - ref.X0), (s.v, ref.v), (s.F, ref.F)):
+        assert l2_error(a, b) < TOL_100
+    e_kin, e_strain = s.energies()
+    assert e_kin > 0.0 and e_strain > 0.0
+
+
+# ------------------------------------------------------- TL FP32 mode
+@pytest.mark.parametrize("label,builder,kwargs", [("c3", configs.c3_plate, {"dp": 0.004}),
+                                                  ("c4", configs.c4_column, {"n_width": 8})])
+def test_tl_fp32_mode_error_is_small(label, builder, kwargs):
+    """Optional FP32 mode of the TL passes (FP32 companions of the gathered
+    v_half and Q records, FP64 arithmetic and state): error vs FP64 after 50
+    steps, reported separately (north star); loose bound against breakage."""
+    cfg = builder(**kwargs)
+    out = {}
+    for prec in ("fp64", "fp32"):
+        m = cfg["material"]
+        s = SolidSystem(cfg["X0"], Material(m.rho0, m.E, m.nu), cfg["spec"], cfg["dp"],
+                        fixed=cfg["fixed"], cfl=cfg["cfl"], precision=prec)
+        s.v = cfg["v0"].copy()
+        s.advance(50)
+        out[prec] = (s.x - s.X0, s.v, s.F)
+    for a, b in zip(out["fp32"], out["fp64"]):
+        assert l2_error(a, b) < 1e-5

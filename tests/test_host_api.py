@@ -151,3 +151,40 @@ def test_lattice_fill():
     a = lattice_fill(Rectangle(lo=(0, 0), hi=(1, 1)), 0.2)
     assert np.array_equal(a, lattice_fill(Rectangle(lo=(0, 0), hi=(1, 1)), 0.2))
     assert a[0] == pytest.approx([0.1, 0.1]) and a[1] == pytest.approx([0.1, 0.3])
+
+
+def test_neo_hookean_stress_is_the_energy_derivative():
+    """The optional compressible Neo-Hookean law (BASELINE configs 3-4; not in
+    the reference): S = 2 dW/dC for W = G/2 (tr C - d) - G ln J + lam/2 ln^2 J,
+    checked by central differences on random deformations; small strains
+    agree with SVK to first order."""
+    from paper_2405_05155_b200.tlsph import NEO_HOOKEAN, Material, pk2_stress
+
+    mat = Material(rho0=1100.0, E=1.7e7, nu=0.45, law=NEO_HOOKEAN)
+    lam, g = mat.lame
+    rng = np.random.default_rng(4)
+
+    def energy(C):
+        d = C.shape[0]
+        ln_j = 0.5 * np.log(np.linalg.det(C))
+        return 0.5 * g * (np.trace(C) - d) - g * ln_j + 0.5 * lam * ln_j**2
+
+    for d in (2, 3):
+        for _ in range(5):
+            F = np.eye(d) + 0.2 * rng.standard_normal((d, d))
+            C = F.T @ F
+            S = pk2_stress(F, mat)
+            num = np.zeros((d, d))
+            eps = 1e-6
+            for a in range(d):
+                for b in range(d):
+                    dC = np.zeros((d, d))
+                    dC[a, b] += eps / 2
+                    dC[b, a] += eps / 2
+                    num[a, b] = 2.0 * (energy(C + dC) - energy(C - dC)) / (2 * eps)
+            assert np.allclose(S, num, rtol=1e-6, atol=1e-6 * np.abs(S).max())
+        F = np.eye(d) + 1e-7 * rng.standard_normal((d, d))
+        svk = pk2_stress(F, Material(rho0=1100.0, E=1.7e7, nu=0.45))
+        assert np.allclose(pk2_stress(F, mat), svk, rtol=1e-5, atol=1e-5 * np.abs(svk).max())
+    with pytest.raises(ValueError):
+        Material(rho0=1.0, E=1.0, nu=0.3, law="mooney")

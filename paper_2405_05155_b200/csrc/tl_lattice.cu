@@ -555,7 +555,7 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
     return SPHB_ERR_ARG;
   if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  static const int minb = tl_minb("SPHB_TLAT_MINB_B", 4);
+  static const int minb = tl_minb("SPHB_TLAT_MINB_B", 5);   // 96 registers (r02_ncu_c4.md)
   const bool f32 = p->vh32 && p->q32;
   const unsigned grid = lattice_grid(L);
 #define SPHB_B1(D, R, MB)                                                                   \

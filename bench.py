@@ -323,6 +323,60 @@ def c4_leg(torch, steps, warmup, peak):
     return out
 
 
+def small_configs_leg(torch):
+    """Driver-timed sub-records of BASELINE configs[0..2] at their full sizes
+    and step counts (CUDA events around the device loop, CUDA-graph replay
+    via advance()/run(); set-up and warm-up outside): C1 relaxation (10^4
+    particles, 100 LG updates), C2 TGV-2D (200^2, 1000 steps), C3 plate
+    (5,200 particles, 2000 steps), each at 1.6h and 2h where the config has
+    two kernels.  These are launch/latency bound at 10^4 particles."""
+    from paper_2405_05155_b200 import configs
+    from paper_2405_05155_b200.eulerian import (WEAKLY_COMPRESSIBLE, EosParams, EulerianSolver,
+                                                FluidState)
+    from paper_2405_05155_b200.relaxation import PeriodicRelaxer
+    from paper_2405_05155_b200.tlsph import SolidSystem
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    out = {}
+    c1 = configs.c1_relax(seed=0)
+    rl = PeriodicRelaxer(c1["pos"], c1["relax_spec"], c1["box"], c1["dp"])
+    rl.run(5)
+    ms = timed(lambda: rl.run(100))
+    out["c1_relax"] = {"particles": 10000, "updates": 100, "ms_per_update": ms / 100,
+                       "value": 10000 * 100 / (ms * 1e-3)}
+    for key in ("1.6h", "2h"):
+        cfg = configs.c2_tgv2d(kernel=key)
+        n = cfg["pos"].shape[0]
+        s = EulerianSolver(cfg["pos"], n, FluidState(cfg["vol"], cfg["rho"], cfg["mom"], None, n),
+                           EosParams(WEAKLY_COMPRESSIBLE, rho0=cfg["rho0"], c_art=cfg["c_art"]),
+                           cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"],
+                           periodic_box=cfg["box"])
+        s.advance(16)
+        ms = timed(lambda: s.advance(1000))
+        out.setdefault("c2_tgv2d", {"particles": n, "steps": 1000})[key.replace(".", "p")] = {
+            "ms_per_step": ms / 1000, "value": n * 1000 / (ms * 1e-3)}
+        cfg = configs.c3_plate(kernel=key)
+        t = SolidSystem(cfg["X0"], cfg["material"], cfg["spec"], cfg["dp"], fixed=cfg["fixed"],
+                        cfl=cfg["cfl"])
+        t.v = cfg["v0"]
+        t.advance(16)
+        ms = timed(lambda: t.advance(2000))
+        out.setdefault("c3_plate", {"particles": t.n, "steps": 2000})[key.replace(".", "p")] = {
+            "ms_per_step": ms / 2000, "value": t.n * 2000 / (ms * 1e-3)}
+    for name in ("c2_tgv2d", "c3_plate"):
+        out[name]["alpha_T1p6h_over_T2h"] = (out[name]["1p6h"]["ms_per_step"]
+                                             / out[name]["2h"]["ms_per_step"])
+    return out
+
+
 def e2e_leg(torch, solver, steps, warmup):
     """Through the public API with host buffers: every step uploads the state
     from pinned host memory (EulerianSolver.load_state), advances one step and
@@ -508,7 +562,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-2h", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (TL-SPH) sub-record")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the C1-C4 sub-records (small configs and the TL-SPH column)")
     ap.add_argument("--no-numba", action="store_true",
                     help="reference arm: skip the single-core sph_trunc (numba) figure")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
@@ -575,6 +630,9 @@ def main():
         leg["2h"] = run_leg(torch, cfg2, args.steps, max(3, args.warmup), dist, world)
         del leg["2h"]["solver"]
         torch.cuda.empty_cache()
+    small = None
+    if world == 1 and not args.no_c4:
+        small = small_configs_leg(torch)
     c4 = None
     if world == 1 and not args.no_c4:
         c4 = c4_leg(torch, args.steps, args.warmup, float(peaks()[0]["hbm_gbs"]))
@@ -640,6 +698,8 @@ def main():
         line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
     if c4 is not None:
         line["c4_column"] = c4
+    if small is not None:
+        line["small_configs"] = small
     if f32 is not None:
         line["fp32_mode"] = dict(f32, unit="particle-steps/s", kernel="k_wc_lattice_f32<3,4>",
                                  note="FP32 pair math, FP64 accumulation/state; reported "

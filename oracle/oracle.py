@@ -515,6 +515,9 @@ class EulerianWC:
             raise
         self.t += dt
 
+    def _fields(self):
+        return [self.rho, self.mom]
+
     def step(self, dt=None):
         """eulerian.py:562-608: one step with retry-with-halving.  A failed
         substep restarts the whole step from its start state at dt/2^k; t
@@ -522,14 +525,15 @@ class EulerianWC:
         if dt is None:
             dt = self.compute_dt()
         ni = self.n_int
-        rho0, mom0 = self.rho[:ni].copy(), self.mom[:ni].copy()
+        start = [f[:ni].copy() for f in self._fields()]
         advanced, remaining, halved = 0.0, dt, 0
         while advanced < dt - 1e-15 * dt:
             sub = min(remaining, dt - advanced)
             try:
                 self._substep(sub)
             except StateRejected:
-                self.rho[:ni], self.mom[:ni] = rho0, mom0
+                for f, f0 in zip(self._fields(), start):
+                    f[:ni] = f0
                 halved += 1
                 self.retries += 1
                 if halved > 12:
@@ -552,12 +556,17 @@ class EulerianHLLC(EulerianWC):
         self.gamma = gamma
         self.etot = np.array(etot, dtype=float)
 
+    def _fields(self):
+        return [self.rho, self.mom, self.etot]
+
     def eos(self):
         rho = self.rho
+        if np.any(rho <= 0.0):
+            raise StateRejected("non-positive density")
         v2 = np.sum(self.mom**2, axis=-1) / rho**2
         e = self.etot / rho - 0.5 * v2
-        if np.any(e < 0.0) or np.any(rho <= 0.0):
-            raise RuntimeError("negative internal energy")
+        if np.any(e < 0.0):
+            raise StateRejected("negative internal energy")
         p = rho * (self.gamma - 1.0) * e
         return p, np.sqrt(self.gamma * p / rho)
 
@@ -615,24 +624,34 @@ class EulerianHLLC(EulerianWC):
         speed = c[:ni] + np.linalg.norm(self.mom[:ni] / self.rho[:ni, None], axis=1)
         return self.cfl * self.spec.h / float(speed.max())
 
-    def step(self, dt=None):
-        if dt is None:
-            dt = self.compute_dt()
+    def _substep(self, dt):
+        """eulerian.py:610-643 with the energy equation; rejections (rho <= 0,
+        e < 0 in any rhs or after the step, NaN flux) restore the substep
+        start.  step() (inherited) adds the retry-with-halving."""
         ni = self.n_int
         r0, m0, e0 = self.rho[:ni].copy(), self.mom[:ni].copy(), self.etot[:ni].copy()
-        self.apply_boundaries(self.t)
-        drho, dmom, de = self.rhs()
-        self.rho[:ni] = r0 + 0.5 * dt * drho[:ni]
-        self.mom[:ni] = m0 + 0.5 * dt * dmom[:ni]
-        self.etot[:ni] = e0 + 0.5 * dt * de[:ni]
-        self.apply_boundaries(self.t + 0.5 * dt)
-        drho, dmom, de = self.rhs()
-        self.rho[:ni] = r0 + dt * drho[:ni]
-        self.mom[:ni] = m0 + dt * dmom[:ni]
-        self.etot[:ni] = e0 + dt * de[:ni]
-        self.eos()
+        try:
+            self.apply_boundaries(self.t)
+            drho, dmom, de = self.rhs()
+            if not np.all(np.isfinite(dmom[:ni])):
+                raise StateRejected("NaN flux")
+            self.rho[:ni] = r0 + 0.5 * dt * drho[:ni]
+            self.mom[:ni] = m0 + 0.5 * dt * dmom[:ni]
+            self.etot[:ni] = e0 + 0.5 * dt * de[:ni]
+            self.apply_boundaries(self.t + 0.5 * dt)
+            drho, dmom, de = self.rhs()
+            if not np.all(np.isfinite(dmom[:ni])):
+                raise StateRejected("NaN flux")
+            self.rho[:ni] = r0 + dt * drho[:ni]
+            self.mom[:ni] = m0 + dt * dmom[:ni]
+            self.etot[:ni] = e0 + dt * de[:ni]
+            if not np.all(self.rho[:ni] > 0.0):
+                raise StateRejected("non-positive density after step")
+            self.eos()
+        except StateRejected:
+            self.rho[:ni], self.mom[:ni], self.etot[:ni] = r0, m0, e0
+            raise
         self.t += dt
-        return dt
 
 
 # ------------------------------------------------------------ TL-SPH

@@ -480,6 +480,33 @@ def main():
                 arrays[f"{tag}__t"] = np.asarray(ts)
         arrays["n_side"] = np.array(32)
         save("retry", **arrays)
+        # HLLC (ideal gas, DMR at dp = 1/16): 8x the CFL step; stages leave
+        # the admissible region (e < 0) and a substep fails after an accepted
+        # one, so the step restarts with E restored too
+        from sph_trunc import cases
+
+        arrays = {}
+        for key in ("wendland-truncated", "wendland"):
+            case = cases.build_dmr(cases.CaseConfig(name="dmr", case="dmr", solver="euler-hllc",
+                                                    dp=1.0 / 16, t_end=0.2, kernel_family=key))
+            s_ = case.solver
+            tag = "1p6h" if key == "wendland-truncated" else "2h"
+            ni = s_.n_int
+            dts, retries, ts = [], [], []
+            for k in range(1, 7):
+                dt = 8.0 * s_.compute_dt()
+                s_.step(dt)
+                dts.append(dt)
+                retries.append(s_.retries)
+                ts.append(s_.t)
+                st = s_.state
+                arrays[f"{tag}__rho{k}"] = st.rho[:ni].copy()
+                arrays[f"{tag}__mom{k}"] = st.mom[:ni].copy()
+                arrays[f"{tag}__etot{k}"] = st.etot[:ni].copy()
+            arrays[f"{tag}__dt"] = np.asarray(dts)
+            arrays[f"{tag}__retries"] = np.asarray(retries)
+            arrays[f"{tag}__t"] = np.asarray(ts)
+        save("retry_hllc", **arrays)
 
     if want("surface"):
         # ------ API surface beyond the hot path (eulerian.py:145-219, 366-447,

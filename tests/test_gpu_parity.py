@@ -537,6 +537,25 @@ def test_hllc_dmr_graph_advance_matches_step(gold):
 
 
 @pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_hllc_retry_with_halving_vs_reference_golden(gold, key):
+    """HLLC retry-with-halving (eulerian.py:562-608; DMR at 8x the CFL
+    step): retries, t and (rho, mom, E) after each step; a substep fails after
+    an accepted one, so the step restarts with S, M and the energy record Q
+    restored from the device snapshot."""
+    g = gold("retry_hllc")
+    tag = key.replace(".", "p")
+    s = _dmr_solver(gold("hllc_dmr"), tag, key)
+    ni = s.n_int
+    for k in range(1, 7):
+        s.step(float(g[f"{tag}__dt"][k - 1]))
+        assert s.retries == int(g[f"{tag}__retries"][k - 1])
+        assert s.t == pytest.approx(float(g[f"{tag}__t"][k - 1]), rel=1e-14)
+        st = s.state
+        for f in ("rho", "mom", "etot"):
+            assert l2_error(getattr(st, f)[:ni], g[f"{tag}__{f}{k}"]) < 1e-10, (k, f)
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
 @pytest.mark.gpu
 def test_hllc_dmr_vs_oracle(gold, key):
     """Device HLLC path vs the oracle restatement on the same inputs."""

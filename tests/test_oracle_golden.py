@@ -403,3 +403,21 @@ def test_oracle_circle_study_errors(gold, fam):
             ana = -(20.0 * pos[mask, 0]) * np.exp(-(pos[mask, 0] ** 2) / 0.1)
             err = np.linalg.norm(grad[mask, 0] - ana) / np.linalg.norm(ana)
             np.testing.assert_allclose(err, g[f"grad__{key}__{k}__{int(corr)}"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_oracle_hllc_retry_with_halving(gold, key):
+    """Forced halving on the HLLC path (DMR at 8x the CFL step): retries, t
+    and (rho, mom, E) after each of 6 steps against the reference."""
+    from paper_2405_05155_b200.approx import l2_error
+
+    g = gold("retry_hllc")
+    tag = key.replace(".", "p")
+    s = oracle_dmr(gold("hllc_dmr"), tag, key)
+    ni = s.n_int
+    for k in range(1, 7):
+        s.step(float(g[f"{tag}__dt"][k - 1]))
+        assert s.retries == int(g[f"{tag}__retries"][k - 1])
+        assert s.t == pytest.approx(float(g[f"{tag}__t"][k - 1]), rel=1e-14)
+        for f in ("rho", "mom", "etot"):
+            assert l2_error(getattr(s, f)[:ni], g[f"{tag}__{f}{k}"]) < 1e-11, (k, f)

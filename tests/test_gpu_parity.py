@@ -1030,3 +1030,32 @@ def test_tl_fp32_mode_error_is_small(label, builder, kwargs):
         out[prec] = (s.x - s.X0, s.v, s.F)
     for a, b in zip(out["fp32"], out["fp64"]):
         assert l2_error(a, b) < 1e-5
+
+
+@pytest.mark.parametrize("dims", [(20, 12, 16), (14, 24)])
+def test_wc_lattice_on_rectangular_periodic_boxes(dims):
+    """The WC lattice path on non-cubic periodic lattices (per-axis extents
+    and wraps) against the oracle, 1.6h, 10 steps."""
+    d = len(dims)
+    dp = 0.05
+    box = tuple(n * dp for n in dims)
+    pos = lattice_points((0.0,) * d, box, dp)
+    n = pos.shape[0]
+    rng = np.random.default_rng(9)
+    rho = 1.0 + 1e-3 * rng.standard_normal(n)
+    mom = 0.1 * rng.standard_normal((n, d))
+    spec = kernel_spec("wendland-truncated", 1.3 * dp, d)
+    st = FluidState(np.full(n, dp**d), rho.copy(), mom.copy(), None, n)
+    s = EulerianSolver(pos, n, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=10.0), spec,
+                       None, cfl=0.25, mu=0.01, periodic_box=box)
+    assert s.lattice is not None and tuple(s.lattice.n)[:d] == dims
+    ref = O.EulerianWC(pos, np.full(n, dp**d), rho, mom, spec, 10.0, 1.0, 0.01, 0.25, box)
+    s.step()
+    ref.step()
+    assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < TOL_1
+    assert l2_error(s.state.mom, ref.mom) < TOL_1
+    s.advance(9)
+    for _ in range(9):
+        ref.step()
+    assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
+    assert l2_error(s.state.mom, ref.mom) < 1e-10

@@ -324,19 +324,6 @@ int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L, int32_
                           const double* M_n, double* S_out, double* M_out, double* scalars,
                           int32_t* err, void* stream);
 
-/* `nsteps` complete midpoint steps (set_dt + stage 1 + stage 2, the
- * sequence of EulerianSolver.advance) in ONE cooperative persistent launch
- * with grid-wide barriers between the stages — for sets too small to fill
- * the GPU, where kernel boundaries dominate.  dt from the speed in
- * scalars[2] (or dt_override > 0) as sphb_set_dt; after the call the state is
- * in S/M if nsteps is even, in S_nx/M_nx if odd; scalars[1] advanced by the
- * steps' dt, scalars[2] = the last step's speed maximum (scalars[3] is
- * scratch). */
-int sphb_wc_lattice_run(const sphb_wc_params* p, const sphb_lattice* L, int32_t nsteps,
-                        double dt_override, double cfl_h, const double* B, double* S,
-                        double* S1, double* S_nx, double* M, double* M_nx, double* scalars,
-                        int32_t* err, void* stream);
-
 /* The optional FP32 mode of sphb_wc_stage_f32 on a checked lattice: FP32
  * records (B32 planes, S32 {v, rho - rho0}) and table geometry, FP32 pair
  * math, FP64 accumulation and FP64 stage update (S_out/M_out in stage 2;

@@ -229,7 +229,6 @@ SIGNATURES = {
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_stage_lattice_f32": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P, P]),
-    "sphb_wc_lattice_run": (C.c_int, [P, P, I32, F64, F64, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),
     "sphb_ell_sort_rows": (C.c_int, [P, I64, P, P, P, F64, P, P]),
     "sphb_weak_gradient": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),

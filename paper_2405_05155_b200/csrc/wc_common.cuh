@@ -106,15 +106,12 @@ struct NSym { static constexpr int value = D == 3 ? 6 : (D == 2 ? 3 : 1); };
 // rhs record {dmom, drho}), the fused halo push, and for stage 2 the
 // block-reduced max(c + |v|) folded into scalars[2].  Every thread of the
 // block must call it (block reduction); `write` selects the rows it owns.
-// dt < 0: read the stage's dt from scalars[0]; speed_out: where stage 2
-// folds its max(c + |v|) (default scalars + 2).
 template <int D, int NT>
 __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, bool write,
                                             int64_t i, double c, double dr,
                                             const double (&dm)[D], const double4* Sn,
                                             const double4* Mn, double4* S_out, double4* M_out,
-                                            double* scalars, int32_t* err, double dt_in = -1.0,
-                                            double* speed_out = nullptr) {
+                                            double* scalars, int32_t* err) {
   double speed = 0.0;
   int32_t flags = 0;
   if (write) {
@@ -125,7 +122,7 @@ __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, 
     if (stage == 0) {  // rhs only: S_out = {dmom, drho} (EulerianSolver.rhs)
       S_out[i] = pack_s<D>(dm, dr);
     } else {
-      const double dt = dt_in < 0.0 ? scalars[0] : dt_in;
+      const double dt = scalars[0];
       const double cdt = stage == 1 ? 0.5 * dt : dt;
       const double4 mn = Mn[i];
       const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
@@ -171,7 +168,7 @@ __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, 
       double b = red[0];
 #pragma unroll
       for (int q = 1; q < NT / 32; ++q) b = b > red[q] ? b : red[q];
-      atomic_max_nonneg(speed_out ? speed_out : scalars + 2, b);
+      atomic_max_nonneg(scalars + 2, b);
     }
   }
   if (flags) atomicOr(err, flags);

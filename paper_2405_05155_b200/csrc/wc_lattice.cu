@@ -22,11 +22,7 @@
 #include <type_traits>
 #include <utility>
 
-#include <cooperative_groups.h>
-
 #include "wc_common.cuh"
-
-namespace cg = cooperative_groups;
 
 using namespace sphb;
 using namespace sphb::wc;
@@ -93,22 +89,16 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
   return v;
 }
 
-// One block-row of the lattice stage (block index blk): the body of
-// k_wc_lattice, shared with the persistent multi-step kernel.
-template <int D, int R2, int NT>
-__device__ __forceinline__ void lattice_rows(const sphb_wc_params& P, const LatConst& K,
-                                             const sphb_lattice& L, const int stage,
-                                             const int64_t blk, const double* __restrict__ B,
-                                             const double4* __restrict__ S_in,
-                                             const double4* Sn, const double4* Mn,
-                                             double4* S_out, double4* M_out,
-                                             double* __restrict__ scalars,
-                                             int32_t* __restrict__ err, double dt_in,
-                                             double* speed_out) {
+template <int D, int R2, int MINB, int NT = kLT>
+__global__ void __launch_bounds__(NT, MINB * kLT / NT)
+k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
+             const double* __restrict__ B, const double4* __restrict__ S_in,
+             const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
+             double* __restrict__ scalars, int32_t* __restrict__ err) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t n = P.n;
-  const int64_t i0 = P.row0 + blk * NT + threadIdx.x;
+  const int64_t i0 = P.row0 + (int64_t)blockIdx.x * NT + threadIdx.x;
   const bool own = i0 < P.row0 + P.nrows;
   // tail lanes redo the last row (no divergence in the pair loop), no write
   const int64_t i = own ? i0 : P.row0 + P.nrows - 1;
@@ -204,63 +194,7 @@ __device__ __forceinline__ void lattice_rows(const sphb_wc_params& P, const LatC
     pair(kc, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]));
   });
 
-  wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err, dt_in,
-                     speed_out);
-}
-
-template <int D, int R2, int MINB, int NT = kLT>
-__global__ void __launch_bounds__(NT, MINB * kLT / NT)
-k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
-             const double* __restrict__ B, const double4* __restrict__ S_in,
-             const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
-             double* __restrict__ scalars, int32_t* __restrict__ err) {
-  lattice_rows<D, R2, NT>(P, K, L, stage, blockIdx.x, B, S_in, Sn, Mn, S_out, M_out, scalars,
-                          err, -1.0, nullptr);
-}
-
-// Persistent multi-step kernel for sets too small to fill the GPU (C2: 313
-// blocks): `nsteps` midpoint steps in ONE cooperative launch, grid-stride
-// over block-rows, grid-wide barriers between the stages instead of kernel
-// boundaries.  dt per step from the speed folded by the previous stage 2
-// (two alternating slots scalars[2] / scalars[3], so one slot is cleared
-// while the other is read), exactly k_set_dt's formula; the buffers swap
-// every step (the host swaps to match when nsteps is odd).
-template <int D, int R2, int MINB>
-__global__ void __launch_bounds__(kLT, MINB)
-k_wc_lattice_run(const sphb_wc_params P, const LatConst K, const sphb_lattice L,
-                 const int nsteps, const double dt_override, const double cfl_h,
-                 const double* __restrict__ B, double4* S, double4* S1, double4* Snx,
-                 double4* M, double4* Mnx, double* __restrict__ scalars,
-                 int32_t* __restrict__ err) {
-  cg::grid_group grid = cg::this_grid();
-  const int64_t nrb = (P.nrows + kLT - 1) / kLT;
-  for (int step = 0; step < nsteps; ++step) {
-    volatile double* vs = scalars;
-    double* sp_in = scalars + 2 + (step & 1);
-    double* sp_out = scalars + 2 + ((step + 1) & 1);
-    double dt = dt_override;
-    if (!(dt > 0.0)) {
-      const double denom = vs[2 + (step & 1)];
-      dt = (denom > 0.0 && isfinite(denom)) ? cfl_h / denom : 0.0;
-      if (dt == 0.0 && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, SPHB_EFLAG_NONFINITE_STATE);
-    }
-    (void)sp_in;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      scalars[0] = dt;
-      scalars[1] += dt;
-      *sp_out = 0.0;
-    }
-    for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x)
-      lattice_rows<D, R2, kLT>(P, K, L, 1, rb, B, S, S, M, S1, nullptr, scalars, err, dt,
-                               sp_out);
-    grid.sync();
-    for (int64_t rb = blockIdx.x; rb < nrb; rb += gridDim.x)
-      lattice_rows<D, R2, kLT>(P, K, L, 2, rb, B, S1, S, M, Snx, Mnx, scalars, err, dt, sp_out);
-    grid.sync();
-    double4* t = S; S = Snx; Snx = t;
-    t = M; M = Mnx; Mnx = t;
-  }
-  if ((nsteps & 1) && blockIdx.x == 0 && threadIdx.x == 0) scalars[2] = scalars[3];
+  wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
 }
 
 // Proof of the specialisation for rows [row0, row0 + nrows): cnt == W, the
@@ -714,53 +648,5 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   }
   SPHB_LAT_CASES(SPHB_F)
 #undef SPHB_F
-  return SPHB_ERR_ARG;
-}
-
-extern "C" int sphb_wc_lattice_run(const sphb_wc_params* p, const sphb_lattice* L, int32_t nsteps,
-                                   double dt_override, double cfl_h, const double* b, double* s,
-                                   double* s1, double* s_nx, double* m, double* m_nx,
-                                   double* scalars, int32_t* err, void* stream) {
-  if (!lattice_args_ok(p, L) || nsteps < 0 || p->interior || p->wall_tag || !p->uniform_vol ||
-      p->push_prev || p->push_next)
-    return SPHB_ERR_ARG;
-  if (nsteps == 0 || p->nrows == 0) return SPHB_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  LatConst K;
-  K.c2 = p->c_art * p->c_art;
-  K.c2rho0 = K.c2 * p->rho0;
-  K.eta_c = kEtaLinearized / p->c_art;
-  K.hc = 0.5 * p->c_art;
-  int dev = 0, nsm = 0;
-  SPHB_CUDA_CHECK(cudaGetDevice(&dev));
-  SPHB_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t nrb = (p->nrows + kLT - 1) / kLT;
-  const sphb_wc_params P = *p;
-  const sphb_lattice Lc = *L;
-  int ns = nsteps;
-  double dto = dt_override, ch = cfl_h;
-  const double* bb = b;
-  double4 *S = (double4*)s, *S1 = (double4*)s1, *Snx = (double4*)s_nx, *M = (double4*)m,
-          *Mnx = (double4*)m_nx;
-  void* args[] = {(void*)&P, (void*)&K, (void*)&Lc, (void*)&ns, (void*)&dto, (void*)&ch,
-                  (void*)&bb, (void*)&S, (void*)&S1, (void*)&Snx, (void*)&M, (void*)&Mnx,
-                  (void*)&scalars, (void*)&err};
-#define SPHB_RUN(D, R, MB)                                                                  \
-  if (p->dim == D && L->r2 == R) {                                                          \
-    int per_sm = 0;                                                                         \
-    SPHB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                          \
-        &per_sm, k_wc_lattice_run<D, R, MB>, kLT, 0));                                      \
-    const int64_t cap = (int64_t)per_sm * nsm;                                             \
-    if (cap < 1) return SPHB_ERR_ARG;                                                       \
-    const unsigned grid = (unsigned)(nrb < cap ? nrb : cap);                                \
-    SPHB_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_wc_lattice_run<D, R, MB>,    \
-                                                dim3(grid), dim3(kLT), args, 0, st));       \
-    return SPHB_OK;                                                                         \
-  }
-  SPHB_RUN(2, 4, 5)
-  SPHB_RUN(2, 6, 5)
-  SPHB_RUN(3, 4, 3)
-  SPHB_RUN(3, 6, 2)
-#undef SPHB_RUN
   return SPHB_ERR_ARG;
 }

@@ -1013,18 +1013,7 @@ class EulerianSolver:
                                        device=self._dev)
             self._graphs = None                         # captured the old log pointer
         done = 0
-        if self._persistent_ok():
-            # small lattice sets: all n steps in one cooperative launch
-            # (grid-wide barriers instead of kernel boundaries)
-            _lib.call("sphb_wc_lattice_run", ctypes.byref(self.params), ctypes.byref(self.lattice),
-                      n_steps, dto, self._cfl_h, self.B.data_ptr(), self.S.data_ptr(),
-                      self.S1.data_ptr(), self.S_nx.data_ptr(), self.M.data_ptr(),
-                      self.M_nx.data_ptr(), self.scalars.data_ptr(), self.err.data_ptr(),
-                      _lib.stream_ptr())
-            if n_steps % 2:
-                self._swap()
-            done = n_steps
-        if graph and done < n_steps:
+        if graph:
             g, per = self._step_graph(dto)
             while n_steps - done >= per:
                 g.replay()
@@ -1041,13 +1030,6 @@ class EulerianSolver:
         self.steps += n_steps
         self._state_host = None
         self._drain_wall_force()
-
-    def _persistent_ok(self) -> bool:
-        """advance() runs the persistent multi-step lattice kernel for sets
-        of at most SPHB_WC_PERSIST_MAX rows (default 131072: latency-bound
-        sizes such as C2); larger sets keep the per-stage launches."""
-        return (self.lattice is not None and self.precision == "fp64" and self._slab is None
-                and self.timer is None and self.n <= _persist_max())
 
     def _step_graph(self, dt_override: float):
         """CUDA graph of an even number of consecutive steps (the buffer swap
@@ -1254,10 +1236,6 @@ class _HLLCSolver(EulerianSolver):
         return (float(np.sum(w * st.rho[:self.n_int])),
                 (w[:, None] * st.mom[:self.n_int]).sum(axis=0),
                 float(np.sum(w * st.etot[:self.n_int])))
-
-
-def _persist_max() -> int:
-    return int(os.environ.get("SPHB_WC_PERSIST_MAX", "131072"))
 
 
 def graph_steps() -> int:

@@ -317,8 +317,8 @@ struct SymF<3> {
   }
 };
 
-template <int D, int R2>
-__global__ void __launch_bounds__(kLT, 4)
+template <int D, int R2, int MINB = 4>
+__global__ void __launch_bounds__(kLT, MINB)
 k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, const int stage,
                  const float* __restrict__ B, const float4* __restrict__ S32_in,
                  const double4* Sn, const double4* Mn, float4* __restrict__ S32_out,
@@ -638,15 +638,24 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   K.half_cinv = 0.5f / K.c;
   K.rho0 = (float)p->rho0;
   const unsigned grid = sphb_blocks(p->nrows, kLT);
+  static const int minb32 = [] {           // SPHB_LAT32_MINB (tuning): 4, 6, 8
+    const char* e = getenv("SPHB_LAT32_MINB");
+    return e ? atoi(e) : 4;
+  }();
+#define SPHB_F1(D, R, MB)                                                                   \
+  k_wc_lattice_f32<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,                    \
+      (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
+      (double4*)s_out, (double4*)m_out, scalars, err)
 #define SPHB_F(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
-    k_wc_lattice_f32<D, R><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,                      \
-        (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,  \
-        (double4*)s_out, (double4*)m_out, scalars, err);                                   \
+    if (D == 3 && minb32 == 6) SPHB_F1(D, R, 6);                                            \
+    else if (D == 3 && minb32 == 8) SPHB_F1(D, R, 8);                                       \
+    else SPHB_F1(D, R, 4);                                                                  \
     SPHB_LAUNCH_CHECK();                                                                    \
     return SPHB_OK;                                                                         \
   }
   SPHB_LAT_CASES(SPHB_F)
 #undef SPHB_F
+#undef SPHB_F1
   return SPHB_ERR_ARG;
 }

@@ -138,6 +138,11 @@ __device__ __forceinline__ void for_each_neighbor(const sphb_grid& g, int64_t n,
 // the 48 KB default covers static + dynamic, so leave room for the kernels'
 // static arrays (at most 5 KB here).
 constexpr size_t kDynSmemDefault = 43 * 1024;
+// Launches above the default raise cudaFuncAttributeMaxDynamicSharedMemorySize
+// to this fixed bound (never to the launch's own size): the attribute is per
+// function, so a per-call value set by one host thread could be lowered by
+// another between its set and its launch (thread-simulated slab ranks).
+constexpr int kDynSmemMax = 200 * 1024;
 
 // Debug builds (make debug: -DSPHB_DEBUG_BOUNDS) check every pass-list index
 // before it addresses a record: out-of-range indices raise

@@ -237,9 +237,13 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
   if (n <= kSmallBinMaxN && g->ntot <= kSmallBinMaxCells) {
     const size_t smem = sizeof(int32_t) * (2 * (size_t)g->ntot + (size_t)n);
     if (smem > kDynSmemDefault) {
-      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // one fixed bound for every call: the attribute is per function, so a
+      // per-call value could be lowered by another host thread between this
+      // thread's set and launch (slab ranks of different sizes)
+      const int bound = (int)(sizeof(int32_t) * (2 * kSmallBinMaxCells + kSmallBinMaxN));
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bound));
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bound));
+      SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_bin_small<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bound));
     }
     const int T = 256;
     switch (g->dim) {

@@ -283,7 +283,7 @@ inline int tl_carveout() {
   do {                                                                                         \
     if ((SMEM) > kDynSmemDefault)                                                              \
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           (int)(SMEM)));                                      \
+                                           kDynSmemMax));                                      \
     if (tl_carveout() >= 0)                                                                    \
       SPHB_CUDA_CHECK(cudaFuncSetAttribute(KERNEL,                                             \
                                            cudaFuncAttributePreferredSharedMemoryCarveout,     \

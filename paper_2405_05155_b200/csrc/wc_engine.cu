@@ -399,7 +399,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   if (smem_idx > kDynSmemDefault)                                                          \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                         (int)smem_idx));                                  \
+                                         kDynSmemMax));                                    \
   if (carveout >= 0)                                                                       \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage<D, G, MB, W>,                          \
                                          cudaFuncAttributePreferredSharedMemoryCarveout,   \

@@ -232,7 +232,7 @@ extern "C" int sphb_wc_stage_f32(const sphb_wc_params* p, int32_t stage, const f
   if (smem > kDynSmemDefault)                                                               \
     SPHB_CUDA_CHECK(cudaFuncSetAttribute(k_wc_stage_f32<D>,                                 \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                         (int)smem));                                       \
+                                         kDynSmemMax));                                     \
   k_wc_stage_f32<D><<<grid, kThreads, smem, st>>>(                                          \
       *p, stage, (const float4*)x32, b32, nbr, cnt, (const float4*)s32_in,                  \
       (const double4*)s_n, (const double4*)m_n, (float4*)s32_out, (double4*)s_out,          \

@@ -314,27 +314,6 @@ inline int tl_carveout() {
     }                                                                                      \
   } while (0)
 
-// Tuning variants of the 3D staged passes (SPHB_TL_VARIANT_A / _B =
-// minb*10 + unroll): register cap via min blocks per SM, pairs in flight.
-inline int tl_variant(const char* name) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : 0;
-}
-
-#define TL_TUNED(KERNEL, VAR, GRID, TH, ...)                                                    \
-  do {                                                                                        \
-    const size_t smem_ = (size_t)p->width * kThreads * sizeof(int32_t);                       \
-    switch (VAR) {                                                                            \
-      case 11: TL_LAUNCH((KERNEL<3, false, true, 1, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
-      case 12: TL_LAUNCH((KERNEL<3, false, true, 1, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
-      case 61: TL_LAUNCH((KERNEL<3, false, true, 6, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
-      case 62: TL_LAUNCH((KERNEL<3, false, true, 6, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
-      case 81: TL_LAUNCH((KERNEL<3, false, true, 8, 1>), GRID, TH, smem_, __VA_ARGS__); break; \
-      case 82: TL_LAUNCH((KERNEL<3, false, true, 8, 2>), GRID, TH, smem_, __VA_ARGS__); break; \
-      default: return SPHB_ERR_ARG;                                                           \
-    }                                                                                         \
-  } while (0)
-
 extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const double* b0,
                               const int32_t* nbr, const int32_t* cnt, const double* g0,
                               const double* v, const double* a, double* vh, double* xc,
@@ -344,13 +323,7 @@ extern "C" int sphb_tl_pass_a(const sphb_tl_params* p, const double* x0, const d
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   TL_DISPATCH(k_tl_kick, sphb_blocks(p->n, 256), 256, p->n, (const double4*)v, (const double4*)a, (double4*)vh, scalars, (float4*)p->vh32);
-  static const int var = tl_variant("SPHB_TL_VARIANT_A");
-  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
-    TL_TUNED(k_tl_pass_a, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
-             (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
-             (double4*)xc, (double4*)f, (double4*)q, scalars, err);
-  else
-    TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+  TL_DISPATCH_GEO(k_tl_pass_a, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
                     (const double4*)x0, (const double4*)b0, nbr, cnt, g0, (const double4*)vh,
                     (double4*)xc, (double4*)f, (double4*)q, scalars, err);
   SPHB_LAUNCH_CHECK();
@@ -364,13 +337,7 @@ extern "C" int sphb_tl_pass_b(const sphb_tl_params* p, const double* x0, const i
   if (!p || p->n < 0) return SPHB_ERR_ARG;
   if (p->n == 0 || p->nrows <= 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  static const int var = tl_variant("SPHB_TL_VARIANT_B");
-  if (var && p->dim == 3 && !g0 && p->nrows >= kStageMinRows)
-    TL_TUNED(k_tl_pass_b, var, sphb_blocks(p->nrows, kThreads), kThreads, *p,
-             (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
-             (double4*)a, (double4*)v, scalars, (int)update_v, err);
-  else
-    TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
+  TL_DISPATCH_GEO(k_tl_pass_b, g0, sphb_blocks(p->nrows, kThreads), kThreads, *p,
                     (const double4*)x0, nbr, cnt, g0, (const double4*)q, (const double4*)vh,
                     (double4*)a, (double4*)v, scalars, (int)update_v, err);
   SPHB_LAUNCH_CHECK();

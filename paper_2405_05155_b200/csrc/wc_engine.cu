@@ -414,11 +414,7 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
     switch (p->dim * 16 + group) {
       case 16 + 1: SPHB_STAGE_W(1, 1, 4, true);
       case 32 + 1: SPHB_STAGE_W(2, 1, 4, true);
-      case 32 + 2: SPHB_STAGE_W(2, 2, 4, true);
-      case 32 + 4: SPHB_STAGE_W(2, 4, 4, true);
       case 48 + 1: SPHB_STAGE_W(3, 1, 4, true);
-      case 48 + 2: SPHB_STAGE_W(3, 2, 4, true);
-      case 48 + 4: SPHB_STAGE_W(3, 4, 4, true);
       default: return SPHB_ERR_ARG;
     }
     SPHB_LAUNCH_CHECK();
@@ -434,13 +430,8 @@ extern "C" int sphb_wc_stage(const sphb_wc_params* p, int32_t stage, int32_t gro
   const int key = p->dim * 256 + group * 16 + (p->dim == 3 ? minb : 4);
   switch (key) {
     case 256 + 16 + 4: SPHB_STAGE(1, 1, 4);
-    case 256 + 32 + 4: SPHB_STAGE(1, 2, 4);
     case 512 + 16 + 4: SPHB_STAGE(2, 1, 4);
-    case 512 + 32 + 4: SPHB_STAGE(2, 2, 4);
-    case 512 + 64 + 4: SPHB_STAGE(2, 4, 4);
     case 768 + 16 + 4: SPHB_STAGE(3, 1, 4);
-    case 768 + 32 + 4: SPHB_STAGE(3, 2, 4);
-    case 768 + 64 + 4: SPHB_STAGE(3, 4, 4);
     case 768 + 16 + 5: SPHB_STAGE(3, 1, 5);
     case 768 + 16 + 6: SPHB_STAGE(3, 1, 6);
     case 768 + 16 + 8: SPHB_STAGE(3, 1, 8);

@@ -404,12 +404,9 @@ class EulerianSolver:
 
         ws = self.order.ws
         self.X = _rec4([ws[a] for a in range(self.dim)] + [vol_s], self.n, dev)
-        # lanes per particle (scripts/tune_wc.py sweep on B200, 256^3 TGV-3D,
-        # smem-staged indices + engine order: one lane per particle is best
-        # for both 32- and 80-entry rows; profiles/r01_tune_wc.md)
+        # lanes per particle row of the general kernel: one (the round-1 sweep
+        # of 1 / 2 / 4 lanes, profiles/r01_tune_wc.md)
         self.group = 1
-        if os.environ.get("SPHB_WC_GROUP"):      # tuning override
-            self.group = int(os.environ["SPHB_WC_GROUP"])
         # Stage-kernel variant (SPHB_WC_KERNEL=global|geo):
         #   global (default) recompute the pair geometry from X_j, B_j
         #          (wc_engine.cu; on a checked lattice wc_lattice.cu);

@@ -296,10 +296,7 @@ def engine_order(bins: CellBins, nbr, cnt, width: int, spacing: float | None = N
     # multiple of the spacing up to rounding), so round instead of floor
     shift = 0.0 if g.periodic else 0.5
     k = torch.floor(ws * (1.0 / spacing) + shift).to(torch.int64).clamp_(min=0)
-    if tile is None:
-        env = os.environ.get("SPHB_ENGINE_TILE", "")
-        tile = tuple(int(v) for v in env.split("x")) if env else ()
-    tile = tuple(tile) + (1,) * (d - len(tile))
+    tile = tuple(tile or ()) + (1,) * (d - len(tile or ()))
     # slowest component: the cell layer along the grid's storage slow axis
     # (as the binning computes it), so a slab rank's owned block and halo
     # layers stay contiguous; then tiles of tile[0] x tile[1] x ... sites in

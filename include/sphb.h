@@ -579,14 +579,6 @@ int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, co
                            const double* B0, const int32_t* nbr, const int32_t* cnt,
                            const double* Vh, double* XC, double* F, double* Q,
                            const double* scalars, int32_t* err, void* stream);
-/* Pass A with the first kick fused in (no sphb_tl_kick first): gathers v_j
- * and a_j and forms v_half_j = v_j + dt/2 a_j (0 when clamped) per pair;
- * writes Vh_i for pass B.  FP64 records only. */
-int sphb_tl_pass_a_lattice_kick(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                                const double* X0, const double* B0, const int32_t* nbr,
-                                const int32_t* cnt, const double* V, const double* A,
-                                double* Vh, double* XC, double* F, double* Q,
-                                const double* scalars, int32_t* err, void* stream);
 int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
                            const int32_t* nbr, const int32_t* cnt, const double* Q,
                            const double* Vh, double* A, double* V, double* scalars,

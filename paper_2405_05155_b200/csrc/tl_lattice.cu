@@ -134,18 +134,6 @@ __device__ __forceinline__ void gather_vh(const sphb_tl_params& P, const double4
   }
 }
 
-// v_half_j from v_j and a_j (the first kick, k_tl_kick, fused into pass A):
-// v + dt/2 a, 0 for clamped particles (the flag rides in A.w)
-template <int D>
-__device__ __forceinline__ void kick_vh(const double4* __restrict__ V,
-                                        const double4* __restrict__ A, int64_t j, double hdt,
-                                        double (&v)[D]) {
-  const double4 vv = ldg4(V + j), aa = ldg4(A + j);
-  const double cv[4] = {vv.x, vv.y, vv.z, vv.w}, ca[4] = {aa.x, aa.y, aa.z, aa.w};
-#pragma unroll
-  for (int a = 0; a < D; ++a) v[a] = aa.w != 0.0 ? 0.0 : fma(hdt, ca[a], cv[a]);
-}
-
 // column c of Q_j (3D)
 template <bool F32>
 __device__ __forceinline__ void gather_qcol(const sphb_tl_params& P, const double4* __restrict__ Q,
@@ -162,7 +150,7 @@ __device__ __forceinline__ void gather_qcol(const sphb_tl_params& P, const doubl
 
 // Shell row of pass A: the general pair loop (tl_engine.cu k_tl_pass_a,
 // unstaged) — pass list, X0_j gather, g0 recomputed (ref_gradient).
-template <int D, bool F32, bool KICK>
+template <int D, bool F32>
 __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
                                         const double4* __restrict__ X0,
                                         const double4* __restrict__ B0,
@@ -170,21 +158,14 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
                                         const int32_t* __restrict__ cnt,
                                         const double4* __restrict__ Vh, double4* __restrict__ XC,
                                         double4* __restrict__ F, double4* __restrict__ Q,
-                                        double dt, int32_t* __restrict__ err,
-                                        const double4* __restrict__ V,
-                                        const double4* __restrict__ A, double4* Vh_out) {
+                                        double dt, int32_t* __restrict__ err) {
   const int64_t n = P.n;
   const double inv_h = 1.0 / P.h;
   const double c5v = -5.0 * (P.alpha / P.h * P.vol0) * inv_h, mhalf_inv_h = -0.5 * inv_h;
   double wi[D], vhi[D];
   bool fixed_i;
   load_x0<D>(X0, i, wi, fixed_i);
-  if constexpr (KICK) {
-    kick_vh<D>(V, A, i, 0.5 * dt, vhi);
-    store_vec<D>(Vh_out, i, vhi);
-  } else {
-    load_vec<D>(Vh, i, vhi);
-  }
+  load_vec<D>(Vh, i, vhi);
   double m[D][D];
 #pragma unroll
   for (int a = 0; a < D; ++a)
@@ -196,10 +177,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
     SPHB_CHECK_INDEX(j, n, err);
     double vhj[D], wj[D], dx[D], g[D];
     bool fixed_j;
-    if constexpr (KICK)
-      kick_vh<D>(V, A, j, 0.5 * dt, vhj);
-    else
-      gather_vh<D, F32>(P, Vh, j, vhj);
+    gather_vh<D, F32>(P, Vh, j, vhj);
     load_x0<D>(X0, j, wj, fixed_j);
 #pragma unroll
     for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
@@ -267,23 +245,21 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
   return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
 }
 
-template <int D, int R2, int MINB, bool F32, bool KICK = false>
+template <int D, int R2, int MINB, bool F32>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const double4* __restrict__ B0,
                const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
                const double4* __restrict__ Vh, double4* __restrict__ XC,
                double4* __restrict__ F, double4* __restrict__ Q,
-               const double* __restrict__ scalars, int32_t* __restrict__ err,
-               const double4* __restrict__ V = nullptr, const double4* __restrict__ A = nullptr) {
+               const double* __restrict__ scalars, int32_t* __restrict__ err) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
   if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
     const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
-    if (ts < L.n_shell)
-      shell_a<D, F32, KICK>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q, scalars[0],
-                            err, V, A, const_cast<double4*>(Vh));
+    if (ts < L.n_shell) shell_a<D, F32>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q,
+                                        scalars[0], err);
     return;
   }
   const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
@@ -294,12 +270,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   double wi[D], vhi[D];
   bool fixed_i;
   load_x0<D>(X0, i, wi, fixed_i);
-  if constexpr (KICK) {               // fused first kick; pass B reads Vh_i
-    kick_vh<D>(V, A, i, 0.5 * dt, vhi);
-    store_vec<D>(const_cast<double4*>(Vh), i, vhi);
-  } else {
-    load_vec<D>(Vh, i, vhi);
-  }
+  load_vec<D>(Vh, i, vhi);
   double dxs[D][2 * R + 1];
   axis_displacements<D, R>(X0, row, wi, dxs);
   double m[D][D];
@@ -314,10 +285,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
     const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
                       (int64_t)o[2] * row.stride[2];
     double vhj[D];
-    if constexpr (KICK)
-      kick_vh<D>(V, A, j, 0.5 * dt, vhj);
-    else
-      gather_vh<D, F32>(P, Vh, j, vhj);
+    gather_vh<D, F32>(P, Vh, j, vhj);
     double dx[D];
     double r2 = 0.0;
 #pragma unroll
@@ -574,33 +542,6 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   SPHB_TLAT_CASES(SPHB_A)
 #undef SPHB_A
 #undef SPHB_A1
-  return SPHB_ERR_ARG;
-}
-
-// Pass A with the first kick fused (no sphb_tl_kick; FP64 records only):
-// gathers v_j and a_j instead of v_half_j and writes Vh_i for pass B.
-extern "C" int sphb_tl_pass_a_lattice_kick(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                                           const double* x0, const double* b0,
-                                           const int32_t* nbr, const int32_t* cnt,
-                                           const double* v, const double* a, double* vh,
-                                           double* xc, double* f, double* q,
-                                           const double* scalars, int32_t* err, void* stream) {
-  if (!tl_lattice_ok(p, L) || !x0 || !b0 || !v || !a || !vh || !xc || !f || !q || !nbr || !cnt ||
-      p->vh32 || p->q32)
-    return SPHB_ERR_ARG;
-  if (L->n_interior + L->n_shell == 0) return SPHB_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const unsigned grid = lattice_grid(L);
-#define SPHB_K(D, R)                                                                        \
-  if (p->dim == D && L->r2 == R) {                                                          \
-    k_tl_lattice_a<D, R, 4, false, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,  \
-        (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,        \
-        (double4*)q, scalars, err, (const double4*)v, (const double4*)a);                    \
-    SPHB_LAUNCH_CHECK();                                                                    \
-    return SPHB_OK;                                                                         \
-  }
-  SPHB_TLAT_CASES(SPHB_K)
-#undef SPHB_K
   return SPHB_ERR_ARG;
 }
 

@@ -34,11 +34,6 @@ from .neighbors import (NeighborList, bin_particles, csr_from_bins, ell_from_bin
                         make_grid)
 
 
-def _fused_kick() -> bool:
-    """SPHB_TL_FUSED_KICK=1: the lattice pass A forms v_half itself."""
-    return os.environ.get("SPHB_TL_FUSED_KICK", "0") == "1"
-
-
 class SolidStateError(RuntimeError):
     """Raised when the deformation gradient loses invertibility."""
 
@@ -574,15 +569,7 @@ class SolidSystem:
         self._set_push(True)
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
-        if self.lattice is not None and self.precision == "fp64" and _fused_kick():
-            # pass A with the first kick fused (v_half_j formed per pair)
-            _lib.call("sphb_tl_pass_a_lattice_kick", ctypes.byref(self.params),
-                      ctypes.byref(self.lattice), self.X0rec.data_ptr(), self.B0rec.data_ptr(),
-                      self.nbr.data_ptr(), self.cnt.data_ptr(), self.V.data_ptr(),
-                      self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
-                      self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
-                      self.err.data_ptr(), st)
-        elif self.lattice is not None:
+        if self.lattice is not None:
             # kick, then pass A over the interior (lattice) and shell rows
             _lib.call("sphb_tl_kick", ctypes.byref(self.params), self.V.data_ptr(),
                       self.A.data_ptr(), self.Vh.data_ptr(), self.scalars.data_ptr(), st)

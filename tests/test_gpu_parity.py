@@ -1059,18 +1059,3 @@ def test_wc_lattice_on_rectangular_periodic_boxes(dims):
         ref.step()
     assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
     assert l2_error(s.state.mom, ref.mom) < 1e-10
-
-
-def test_tl_fused_kick_is_bitwise_the_separate_kick(monkeypatch):
-    """SPHB_TL_FUSED_KICK=1 (pass A forms v_half per pair from v and a):
-    same arithmetic as the separate kick kernel, so identical fields."""
-    cfg = configs.c4_column(n_width=8)
-    out = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("SPHB_TL_FUSED_KICK", flag)
-        s = make_tl(cfg)
-        assert s.lattice is not None
-        s.advance(20)
-        out.append((s.x, s.v, s.F))
-    for a, b in zip(*out):
-        assert np.array_equal(a, b)

@@ -621,7 +621,7 @@ class EulerianSolver:
                 return
             if self.precision == "fp32":      # neighbours read the FP32 companion
                 buf = self._c32[buf.data_ptr()]
-            self._slab.exchange(self._dist, [buf])
+            self._slab.exchange(self._dist, [buf], reuse=True)
 
     def _setup_overlap(self):
         """Boundary-first stages (slab ranks, NCCL exchange; default on,
@@ -662,7 +662,7 @@ class EulerianSolver:
             self._stage_rows(stage, hi, s_in, s_n, m_n, s_out, m_out)
         comm.wait_stream(bnd)
         with torch.cuda.stream(comm):
-            sl.exchange(self._dist, [s_out])
+            sl.exchange(self._dist, [s_out], reuse=True)
         self._stage_rows(stage, slice(lo.stop, hi.start), s_in, s_n, m_n, s_out, m_out)
         self.params.row0, self.params.nrows = sl.rows.start, sl.rows.stop - sl.rows.start
 

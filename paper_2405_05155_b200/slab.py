@@ -159,11 +159,22 @@ class SlabPlan:
             out["next"] = (table[self.next][0], table[self.next][1][0])   # its lower halo
         return out
 
-    def exchange(self, dist, bufs, group=None) -> None:
-        """Blocking (host) / stream-ordered (NCCL) halo exchange of `bufs`."""
+    def exchange(self, dist, bufs, group=None, reuse: bool = False) -> None:
+        """Blocking (host) / stream-ordered (NCCL) halo exchange of `bufs`.
+
+        reuse: the buffers are the solver's static record buffers (the step
+        loop), so their P2POp list is built once and kept (it holds the
+        views); per-step host work is then the batched launch itself."""
         if self.world == 1:
             return
-        ops = self.p2p_ops(dist, bufs, group)
+        if reuse:
+            cache = self.__dict__.setdefault("_ops_cache", {})
+            key = (id(dist), id(group)) + tuple((b.data_ptr(), tuple(b.shape)) for b in bufs)
+            ops = cache.get(key)
+            if ops is None:
+                ops = cache[key] = self.p2p_ops(dist, bufs, group)
+        else:
+            ops = self.p2p_ops(dist, bufs, group)
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()

@@ -485,7 +485,7 @@ class SolidSystem:
 
     def _halo(self, *bufs):
         if self._slab is not None:
-            self._slab.exchange(self._dist, list(bufs))
+            self._slab.exchange(self._dist, list(bufs), reuse=True)
 
     def _setup_push(self, dev):
         """Fused halo push (SPHB_HALO_PUSH=1): pass A stores the boundary

@@ -122,11 +122,11 @@ k_bin_small(sphb_grid g, int64_t n, const double* __restrict__ wrapped,
   for (int c = c0; c < c1; ++c) {
     const int32_t k = count[c];
     fill[c] = off;
-    if (k) {
-      const int64_t r = g.slow_axis == g.dim - 1 ? c : ref_key(g, (uint32_t)c);
-      cs[r] = off;
-      ce[r] = off + k;
-    }
+    // every cell's range, empty ones as [off, off) (no memset of the
+    // tables needed before this kernel)
+    const int64_t r = g.slow_axis == g.dim - 1 ? c : ref_key(g, (uint32_t)c);
+    cs[r] = off;
+    ce[r] = off + k;
     off += k;
   }
   __syncthreads();
@@ -224,8 +224,11 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
                         size_t workspace_bytes, void* stream) {
   if (!grid_ok(g) || n < 0 || n > 0x7fffffffLL) return SPHB_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  SPHB_CUDA_CHECK(cudaMemsetAsync(cs, 0, sizeof(int32_t) * (size_t)g->ntot, st));
-  SPHB_CUDA_CHECK(cudaMemsetAsync(ce, 0, sizeof(int32_t) * (size_t)g->ntot, st));
+  const bool small = n > 0 && n <= kSmallBinMaxN && g->ntot <= kSmallBinMaxCells;
+  if (!small) {   // the single-block path writes every cell's range itself
+    SPHB_CUDA_CHECK(cudaMemsetAsync(cs, 0, sizeof(int32_t) * (size_t)g->ntot, st));
+    SPHB_CUDA_CHECK(cudaMemsetAsync(ce, 0, sizeof(int32_t) * (size_t)g->ntot, st));
+  }
   if (n == 0) return SPHB_OK;
   BinLayout L = bin_layout(n, g->dim);
   if (workspace_bytes < L.total) return SPHB_ERR_WORKSPACE;
@@ -234,7 +237,7 @@ extern "C" int sphb_bin(const sphb_grid* g, const double* pos, int64_t n, double
   uint32_t* keys_out = (uint32_t*)(w + L.keys_out);
   int32_t* vals_in = (int32_t*)(w + L.vals_in);
   double* wrapped = (double*)(w + L.wrapped);
-  if (n <= kSmallBinMaxN && g->ntot <= kSmallBinMaxCells) {
+  if (small) {
     const size_t smem = sizeof(int32_t) * (2 * (size_t)g->ntot + (size_t)n);
     if (smem > kDynSmemDefault) {
       // one fixed bound for every call: the attribute is per function, so a

@@ -187,16 +187,23 @@ class PeriodicRelaxer:
                 self.update()
             return
         torch = _lib.torch_cuda()
+        from .eulerian import graph_steps
+
+        per = graph_steps()          # updates per replay (amortises the replay latency)
         if getattr(self, "_graph", None) is None:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.accelerate()
-                self.update()
+                for _ in range(per):
+                    self.accelerate()
+                    self.update()
             torch.cuda.synchronize()
             self._graph = g
-        for _ in range(n_updates):
+        for _ in range(n_updates // per):
             self._graph.replay()
+        for _ in range(n_updates % per):
+            self.accelerate()
+            self.update()
 
 
 class ShapeRelaxer(PeriodicRelaxer):

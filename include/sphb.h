@@ -324,17 +324,6 @@ int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L, int32_
                           const double* M_n, double* S_out, double* M_out, double* scalars,
                           int32_t* err, void* stream);
 
-/* Pair-symmetric variant of sphb_wc_stage_lattice (3D, r2 = 4 or 6): each
- * unordered pair is evaluated once and credited to both rows (the pair term
- * of _rhs_wc, eulerian.py:224-266, is antisymmetric for uniform volumes).
- * Same contract; additionally needs [row0, row0 + nrows) to be whole lattice
- * planes, n[0] >= 32 and n[1], n[2] >= 5 / 6 — SPHB_ERR_ARG (nothing launched)
- * otherwise.  sphb_wc_stage_lattice calls it first in 3D. */
-int sphb_wc_stage_lattice_sym(const sphb_wc_params* p, const sphb_lattice* L, int32_t stage,
-                              const double* B, const double* S_in, const double* S_n,
-                              const double* M_n, double* S_out, double* M_out, double* scalars,
-                              int32_t* err, void* stream);
-
 /* The optional FP32 mode of sphb_wc_stage_f32 on a checked lattice: FP32
  * records (B32 planes, S32 {v, rho - rho0}) and table geometry, FP32 pair
  * math, FP64 accumulation and FP64 stage update (S_out/M_out in stage 2;

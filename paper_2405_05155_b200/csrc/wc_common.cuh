@@ -101,80 +101,11 @@ __device__ __forceinline__ double norm_exact(const double (&v)[D]) {
 
 template <int D>
 struct NSym { static constexpr int value = D == 3 ? 6 : (D == 2 ? 3 : 1); };
-// Per-particle part of the stage epilogue (eulerian.py:548-550, 619-629):
-// error flags, the stage update into S_out / M_out (stage 0: the rhs record
-// {dmom, drho}), the fused halo push, and for stage 2 this row's c + |v|
-// (returned in `speed`, 0 otherwise).
-template <int D>
-__device__ __forceinline__ void wc_update(const sphb_wc_params& P, int stage, int64_t i,
-                                          double c, double dr, const double (&dm)[D],
-                                          const double4* Sn, const double4* Mn, double4* S_out,
-                                          double4* M_out, const double* scalars, double& speed,
-                                          int32_t& flags) {
-  bool finite = isfinite(dr);
-#pragma unroll
-  for (int a = 0; a < D; ++a) finite = finite && isfinite(dm[a]);
-  if (!finite) flags |= SPHB_EFLAG_NONFINITE_FLUX;
-  if (stage == 0) {  // rhs only: S_out = {dmom, drho} (EulerianSolver.rhs)
-    S_out[i] = pack_s<D>(dm, dr);
-    return;
-  }
-  const double dt = scalars[0];
-  const double cdt = stage == 1 ? 0.5 * dt : dt;
-  const double4 mn = Mn[i];
-  const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
-  double vtmp[D], rho_n;
-  unpack_s<D>(Sn[i], vtmp, rho_n);
-  const double rho_new = fma(cdt, dr, rho_n);   // eulerian.py:619-627
-  double mom_new[D], v_new[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    mom_new[a] = fma(cdt, dm[a], cm[a]);
-    v_new[a] = __ddiv_rn(mom_new[a], rho_new);
-  }
-  if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
-  const double4 s_new = pack_s<D>(v_new, rho_new);
-  S_out[i] = s_new;
-  // fused halo push: boundary layers go straight into the neighbour
-  // ranks' halo rows (peer memory) from this epilogue
-  bool pushed = false;
-  if (P.push_prev && i >= P.push_lo0 && i < P.push_lo1) {
-    reinterpret_cast<double4*>(P.push_prev)[P.push_prev_at + (i - P.push_lo0)] = s_new;
-    pushed = true;
-  }
-  if (P.push_next && i >= P.push_hi0 && i < P.push_hi1) {
-    reinterpret_cast<double4*>(P.push_next)[P.push_next_at + (i - P.push_hi0)] = s_new;
-    pushed = true;
-  }
-  if (pushed) __threadfence_system();
-  if (stage == 2) {
-    double mc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) mc[a] = mom_new[a];
-    M_out[i] = make_double4(mc[0], mc[1], mc[2], mc[3]);
-    speed = fmax(speed, __dadd_rn(c, norm_exact<D>(v_new)));
-  }
-}
-
-// Block-reduced max(c + |v|) folded into scalars[2] (stage 2).  Every
-// thread of the block must call it.
-template <int NT>
-__device__ __forceinline__ void wc_speed_fold(double speed, double* scalars) {
-  __shared__ double red[NT / 32];
-  const double w = warp_max(speed);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = red[0];
-#pragma unroll
-    for (int q = 1; q < NT / 32; ++q) b = b > red[q] ? b : red[q];
-    atomic_max_nonneg(scalars + 2, b);
-  }
-}
-
-// Stage epilogue shared by the WC stage kernels: wc_update for the rows the
-// thread owns (`write`), then the block's speed fold (stage 2).  Every
-// thread of the block must call it.
+// Stage epilogue shared by the WC stage kernels (eulerian.py:548-550,
+// 619-629): error flags, the stage update into S_out / M_out (stage 0: the
+// rhs record {dmom, drho}), the fused halo push, and for stage 2 the
+// block-reduced max(c + |v|) folded into scalars[2].  Every thread of the
+// block must call it (block reduction); `write` selects the rows it owns.
 template <int D, int NT>
 __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, bool write,
                                             int64_t i, double c, double dr,
@@ -183,8 +114,63 @@ __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, 
                                             double* scalars, int32_t* err) {
   double speed = 0.0;
   int32_t flags = 0;
-  if (write) wc_update<D>(P, stage, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, speed, flags);
-  if (stage == 2) wc_speed_fold<NT>(speed, scalars);
+  if (write) {
+    bool finite = isfinite(dr);
+#pragma unroll
+    for (int a = 0; a < D; ++a) finite = finite && isfinite(dm[a]);
+    if (!finite) flags |= SPHB_EFLAG_NONFINITE_FLUX;
+    if (stage == 0) {  // rhs only: S_out = {dmom, drho} (EulerianSolver.rhs)
+      S_out[i] = pack_s<D>(dm, dr);
+    } else {
+      const double dt = scalars[0];
+      const double cdt = stage == 1 ? 0.5 * dt : dt;
+      const double4 mn = Mn[i];
+      const double cm[4] = {mn.x, mn.y, mn.z, mn.w};
+      double vtmp[D], rho_n;
+      unpack_s<D>(Sn[i], vtmp, rho_n);
+      const double rho_new = fma(cdt, dr, rho_n);   // eulerian.py:619-627
+      double mom_new[D], v_new[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        mom_new[a] = fma(cdt, dm[a], cm[a]);
+        v_new[a] = __ddiv_rn(mom_new[a], rho_new);
+      }
+      if (!(rho_new > 0.0)) flags |= SPHB_EFLAG_NONPOS_DENSITY;
+      const double4 s_new = pack_s<D>(v_new, rho_new);
+      S_out[i] = s_new;
+      // fused halo push: boundary layers go straight into the neighbour
+      // ranks' halo rows (peer memory) from this epilogue
+      bool pushed = false;
+      if (P.push_prev && i >= P.push_lo0 && i < P.push_lo1) {
+        reinterpret_cast<double4*>(P.push_prev)[P.push_prev_at + (i - P.push_lo0)] = s_new;
+        pushed = true;
+      }
+      if (P.push_next && i >= P.push_hi0 && i < P.push_hi1) {
+        reinterpret_cast<double4*>(P.push_next)[P.push_next_at + (i - P.push_hi0)] = s_new;
+        pushed = true;
+      }
+      if (pushed) __threadfence_system();
+      if (stage == 2) {
+        double mc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) mc[a] = mom_new[a];
+        M_out[i] = make_double4(mc[0], mc[1], mc[2], mc[3]);
+        speed = __dadd_rn(c, norm_exact<D>(v_new));
+      }
+    }
+  }
+  if (stage == 2) {
+    __shared__ double red[NT / 32];
+    const double w = warp_max(speed);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = red[0];
+#pragma unroll
+      for (int q = 1; q < NT / 32; ++q) b = b > red[q] ? b : red[q];
+      atomic_max_nonneg(scalars + 2, b);
+    }
+  }
   if (flags) atomicOr(err, flags);
 }
 

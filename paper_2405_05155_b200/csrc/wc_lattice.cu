@@ -544,17 +544,6 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
       !p->uniform_vol)
     return SPHB_ERR_ARG;
   if (p->nrows == 0) return SPHB_OK;
-  // 3D: the pair-symmetric kernel (wc_lattice_sym.cu) when the set
-  // qualifies; SPHB_WC_SYM=0 keeps the one-sided kernel below
-  static const bool sym_on = [] {
-    const char* e = getenv("SPHB_WC_SYM");
-    return !(e && e[0] == '0');
-  }();
-  if (sym_on && p->dim == 3) {
-    const int rc = sphb_wc_stage_lattice_sym(p, L, stage, b, s_in, s_n, m_n, s_out, m_out,
-                                             scalars, err, stream);
-    if (rc != SPHB_ERR_ARG) return rc;
-  }
   cudaStream_t st = (cudaStream_t)stream;
   LatConst K;
   K.c2 = p->c_art * p->c_art;

@@ -78,7 +78,20 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 
 struct LatConst {
-  double c2, c2rho0, eta_c, hc;
+  double c2, c2rho0, kappa;   // kappa = hc / eta_c
+  double mv_sum;              // sum_k mv_k (viscous v_i term)
+};
+
+// Per-slot geometry with the pair factors folded in (built from
+// sphb_lattice by the launcher): ee = dx inv_r eta_c, so ee . (v_j - v_i) is
+// the limiter argument du eta_c itself and wq ee the limiter's star-velocity
+// correction; gg = g2 dx, so (B_i + B_j) gg carries the -2 x 0.5 dW V / r
+// factor of gwv; mv = mu viscv.
+struct LatFold {
+  int32_t n[3];
+  double ee[SPHB_LATTICE_MAXW][3];
+  double gg[SPHB_LATTICE_MAXW][3];
+  double mv[SPHB_LATTICE_MAXW];
 };
 
 // wrapped lattice coordinate c + s in [0, n)
@@ -91,7 +104,7 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
 
 template <int D, int R2, int MINB, int NT = kLT>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
-k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, const int stage,
+k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
              const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
              double* __restrict__ scalars, int32_t* __restrict__ err) {
@@ -119,17 +132,25 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
   }
 
   const double c = P.c_art;
-  const double c2 = K.c2, c2rho0 = K.c2rho0, eta_c = K.eta_c, hc = K.hc;
+  const double c2 = K.c2, c2rho0 = K.c2rho0, kappa = K.kappa;
   double vi[D], rho_i;
   unpack_s<D>(S_in[i], vi, rho_i);
   Sym<D> Bi;
   Bi.load(B, n, i);
   const double hrho_i = 0.5 * rho_i;
+  double hvi[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) hvi[q] = 0.5 * vi[q];
   double dr = 0.0, dm[D];
 #pragma unroll
   for (int q = 0; q < D; ++q) dm[q] = 0.0;
 
-  // one directed pair (i, j) at canonical slot k (offset o, compile-time)
+  // one directed pair (i, j) at canonical slot k (offset o, compile-time);
+  // eulerian.py:230-266 with the table's folded factors:
+  //   x = du eta_c, beta = clamp(x), p* = rbar (c^2 + beta kappa x) - c^2 rho0,
+  //   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
+  //   drho += rbar vs . (B_i + B_j) gg,
+  //   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
   auto pair = [&](auto kc, const int64_t j) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
@@ -139,13 +160,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
     Bj.load(B, n, j);
     Bi.add(Bj, Bs);
     // components with o_q = 0 are zero (checked within tol): compile-time
-    // zeros, so B dx, (v_j - v_i).dx and the limiter term lose them
-    double dx[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-      dx[q] = o[q] == 0 ? 0.0 : L.dx[k][q];
-    const double inv_r = L.inv_r[k];
-    double G_[D];                                     // (B_i + B_j) dx, nonzero columns
+    // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
+    double Gg[D];                                     // (B_i + B_j) gg, nonzero columns
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       double acc = 0.0;
@@ -153,39 +169,52 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
 #pragma unroll
       for (int q = 0; q < D; ++q)
         if (o[q] != 0) {
-          acc = first ? Bs.at(r, q) * dx[q] : fma(Bs.at(r, q), dx[q], acc);
+          acc = first ? Bs.at(r, q) * L.gg[k][q] : fma(Bs.at(r, q), L.gg[k][q], acc);
           first = false;
         }
-      G_[r] = acc;
+      Gg[r] = acc;
     }
-    double dv[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) dv[q] = vj[q] - vi[q];
-    double dud = 0.0;
+    // x = (v_j - v_i) . ee over the nonzero components, as vj . ee - vi . ee
+    double xi = 0.0;
+    bool first = true;
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      if (o[q] != 0) dud = fma(dv[q], dx[q], dud);
-    const double du = dud * inv_r;                   // u_l - u_r (eulerian.py:236-243)
-    double beta = du * eta_c;
-    beta = beta < 0.0 ? 0.0 : (beta > 1.0 ? 1.0 : beta);
+      if (o[q] != 0) {
+        xi = first ? vi[q] * L.ee[k][q] : fma(vi[q], L.ee[k][q], xi);
+        first = false;
+      }
+    double x = -xi;                                  // (u_l - u_r) eta / c
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      if (o[q] != 0) x = fma(vj[q], L.ee[k][q], x);
+    // beta = clamp(x, 0, 1) on the high word (integer pipe, not DSETP):
+    // negative (sign bit) -> 0; x >= 1.0 <=> high word >= that of 1.0
+    const int hx = __double2hiint(x);
+    double beta = hx < 0 ? 0.0 : x;
+    beta = hx >= 0x3FF00000 ? 1.0 : beta;
     const double rbar = fma(0.5, rho_j, hrho_i);
-    const double bh = beta * hc;
-    const double wr = ((beta * bh) * (rho_i - rho_j)) * (rcp_nr(rbar) * inv_r);
-    const double p_star = fma(bh * rbar, du, fma(c2, rbar, -c2rho0));
+    const double bk = beta * kappa;
+    const double p_star = fma(rbar, fma(bk, x, c2), -c2rho0);
+    // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
+    // the beta^2 limiter term)
+    double rr;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(rbar));
+    rr = fma(rr, fma(-rbar, rr, 1.0), rr);
+    const double wq = ((beta * bk) * (rho_i - rho_j)) * rr;
     double vs[D];
     double sg = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      const double vb = fma(0.5, dv[q], vi[q]);
-      vs[q] = o[q] == 0 ? vb : fma(-wr, dx[q], vb);
-      sg = fma(vs[q], G_[q], sg);
+      const double vb = fma(0.5, vj[q], hvi[q]);
+      vs[q] = o[q] == 0 ? vb : fma(-wq, L.ee[k][q], vb);
+      sg = fma(vs[q], Gg[q], sg);
     }
-    const double rs2 = rbar * (L.g2[k] * sg);        // -2 rbar s
+    const double rs2 = rbar * sg;                    // -2 rbar s
     dr += rs2;
-    const double pg = p_star * L.g2[k];               // -2 p* gsc
+    // viscous -mv (v_j - v_i): the v_i part is summed once (K.mv_sum)
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      dm[q] = fma(-L.mv[k], dv[q], fma(pg, G_[q], fma(rs2, vs[q], dm[q])));
+      dm[q] = fma(-L.mv[k], vj[q], fma(p_star, Gg[q], fma(rs2, vs[q], dm[q])));
   };
 
   static_for<St::W>([&](auto kc) {
@@ -193,6 +222,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const sphb_lattice L, con
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
     pair(kc, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]));
   });
+#pragma unroll
+  for (int q = 0; q < D; ++q) dm[q] = fma(K.mv_sum, vi[q], dm[q]);
 
   wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
 }
@@ -548,8 +579,19 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   LatConst K;
   K.c2 = p->c_art * p->c_art;
   K.c2rho0 = K.c2 * p->rho0;
-  K.eta_c = kEtaLinearized / p->c_art;
-  K.hc = 0.5 * p->c_art;
+  const double eta_c = kEtaLinearized / p->c_art;
+  K.kappa = 0.5 * p->c_art / eta_c;
+  LatFold F;
+  for (int q = 0; q < 3; ++q) F.n[q] = L->n[q];
+  for (int k = 0; k < L->width; ++k) {
+    for (int q = 0; q < 3; ++q) {
+      F.ee[k][q] = L->dx[k][q] * L->inv_r[k] * eta_c;
+      F.gg[k][q] = L->g2[k] * L->dx[k][q];
+    }
+    F.mv[k] = L->mv[k];
+  }
+  K.mv_sum = 0.0;
+  for (int k = 0; k < L->width; ++k) K.mv_sum += L->mv[k];
   const unsigned grid = sphb_blocks(p->nrows, kLT);
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
@@ -580,7 +622,7 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);
 #define SPHB_NT(R, MB, NT)                                                                 \
-    k_wc_lattice<3, R, MB, NT><<<g2, NT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout,  \
+    k_wc_lattice<3, R, MB, NT><<<g2, NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
                                                   Mout, scalars, err)
     const bool r4 = L->r2 == 4;
     if (nt == 64) {
@@ -604,7 +646,7 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     return SPHB_OK;                                                                    \
   }
 #define SPHB_S1(D, R, MB)                                                              \
-  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, *L, stage, b, Sin, Sn, Mn, Sout,  \
+  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
                                                Mout, scalars, err);                     \
   break
   SPHB_LAT_CASES(SPHB_S)

@@ -54,9 +54,10 @@ LATTICE_RECORD_BYTES = 48 + 32 + 32 + (64 + 32) / 2.0
 # plus the limiter branch ~3; profiles/r01_ncu_c5_256.md v3)
 FLOPS_PER_PAIR_EST = 117
 # lattice kernel (wc_lattice.cu), FP64 flops per pair from its SASS
-# (DFMA = 2): r2 = 4 stencil (923 DFMA + 467 DMUL + 308 DADD) / 32 slots,
-# r2 = 6 stencil (2387 DFMA + 1139 DMUL + 812 DADD) / 80 slots
-FLOPS_PER_PAIR_LATTICE = {4: 82, 6: 84}
+# (DFMA = 2): r2 = 4 stencil (919 DFMA + 308 DMUL + 212 DADD) / 32 slots,
+# r2 = 6 stencil (2409 DFMA + 741 DMUL + 572 DADD) / 80 slots (round 2,
+# folded slot table; profiles/r02_ncu_c5_256.md)
+FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 77}
 
 
 def traffic_per_launch(kernel: str):

@@ -511,7 +511,12 @@ typedef struct sphb_tl_params {
    * 1 = compressible Neo-Hookean S = G (I - C^-1) + lam ln(J) C^-1 (BASELINE
    * configs 3-4; not in the reference). */
   int32_t law;
-  int32_t reserved_law;
+  /* 1: dense 3D Q records (the lattice table mode, one GPU; set with
+   * sphb_tl_lattice.table): column c is a double2 plane {q_0c, q_1c} at
+   * ((double2*)Q)[c * n + i] and a double plane q_2c at Q[6 n + c * n + i]
+   * (72 bytes, no X0 padding), so pass B gathers 24 instead of 32 bytes per
+   * column.  Pass A, sphb_tl_stress and the lattice pass B honour it. */
+  int32_t q_dense;
 } sphb_tl_params;
 
 /* Pass A first writes Vh = v + dt/2 a (0 for clamped rows) for all n rows
@@ -550,13 +555,19 @@ int sphb_tl_kick(const sphb_tl_params* p, const double* V, const double* A, doub
  * along axis q alone (computed once per row), and g0 = f(r2) dx with f =
  * c5v t^3 (tlsph.py:145-146) is a first-order expansion about r2k[k].
  * Shell rows run the general passes with a row list.  Supported (dim, r2):
- * (2, 3), (2, 5), (3, 3), (3, 5) — 1.6h / 2h at h = 1.15 dp. */
+ * (2, 3), (2, 5), (3, 3), (3, 5) — 1.6h / 2h at h = 1.15 dp.
+ * table = 1: per-slot table geometry instead — dx[k] (antisymmetric,
+ * dx[W-1-k] = -dx[k]) and g[k] = g0 of dx[k] (tlsph.py:145-146), so the
+ * interior passes read no X0 records, and sum_k g[k] = 0 exactly removes
+ * the Q_i sum_j g0_ij term (and pass B's Q_i read); the check then bounds
+ * every interior pair's exact displacement to within tol (absolute) of
+ * dx[k] instead of the separability / r2 tests. */
 #define SPHB_TL_LATTICE_MAXW 56
 typedef struct sphb_tl_lattice {
   int32_t width;         /* slots per interior row                          */
   int32_t r2;
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
-  int32_t reserved;
+  int32_t table;         /* 1: table geometry (dx, g); 0: exact separable   */
   int64_t n_interior;    /* prod(n_a - 2R) over the dim axes                */
   /* the remaining (shell) rows, run in the same launches with the general
    * per-pair geometry and the pass list (nbr, cnt) */
@@ -564,6 +575,8 @@ typedef struct sphb_tl_lattice {
   int64_t n_shell;
   double r2k[SPHB_TL_LATTICE_MAXW];
   double f[SPHB_TL_LATTICE_MAXW], df[SPHB_TL_LATTICE_MAXW];
+  double dx[SPHB_TL_LATTICE_MAXW][3];   /* table geometry (table = 1)       */
+  double g[SPHB_TL_LATTICE_MAXW][3];
 } sphb_tl_lattice;
 int sphb_tl_lattice_width(int32_t dim, int32_t r2);
 /* Interior rows whose pass-list row is not exactly the canonical set, whose

@@ -148,7 +148,7 @@ class TLParams(C.Structure):
         ("vh32", C.c_void_p),
         ("q32", C.c_void_p),
         ("law", C.c_int32),
-        ("reserved_law", C.c_int32),
+        ("q_dense", C.c_int32),
     ]
 
 
@@ -180,13 +180,15 @@ class TLLattice(C.Structure):
         ("width", C.c_int32),
         ("r2", C.c_int32),
         ("n", C.c_int32 * 3),
-        ("reserved", C.c_int32),
+        ("table", C.c_int32),
         ("n_interior", C.c_int64),
         ("shell", C.c_void_p),
         ("n_shell", C.c_int64),
         ("r2k", C.c_double * TL_LATTICE_MAXW),
         ("f", C.c_double * TL_LATTICE_MAXW),
         ("df", C.c_double * TL_LATTICE_MAXW),
+        ("dx", (C.c_double * 3) * TL_LATTICE_MAXW),
+        ("g", (C.c_double * 3) * TL_LATTICE_MAXW),
     ]
 
 

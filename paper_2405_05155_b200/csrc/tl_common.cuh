@@ -107,6 +107,40 @@ __device__ __forceinline__ void store_q(double4* __restrict__ Q, int64_t qs, int
   }
 }
 
+// Dense 3D Q records (sphb_tl_params.q_dense): column c = double2 plane
+// {q_0c, q_1c} at ((double2*)Q)[c n + i] + double plane q_2c at Q[6n + c n + i]
+__device__ __forceinline__ void store_q_dense(double4* __restrict__ Q, int64_t n, int64_t i,
+                                              const double (&a)[3][3]) {
+  double2* q2 = reinterpret_cast<double2*>(Q);
+  double* q1 = reinterpret_cast<double*>(Q) + 6 * n;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    q2[c * n + i] = make_double2(a[0][c], a[1][c]);
+    q1[c * n + i] = a[2][c];
+  }
+}
+
+// column c of a dense record, read-only path (16 + 8 bytes)
+__device__ __forceinline__ void gather_qcol_dense(const double4* __restrict__ Q, int64_t n, int c,
+                                                  int64_t j, double& q0, double& q1,
+                                                  double& q2) {
+  const double2 t = __ldg(reinterpret_cast<const double2*>(Q) + c * n + j);
+  q0 = t.x;
+  q1 = t.y;
+  q2 = __ldg(reinterpret_cast<const double*>(Q) + 6 * n + c * n + j);
+}
+
+__device__ __forceinline__ void load_q_dense(const double4* __restrict__ Q, int64_t n, int64_t i,
+                                             double (&a)[3][3]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double2 t = reinterpret_cast<const double2*>(Q)[c * n + i];
+    a[0][c] = t.x;
+    a[1][c] = t.y;
+    a[2][c] = reinterpret_cast<const double*>(Q)[6 * n + c * n + i];
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void load_q(const double4* __restrict__ Q, int64_t qs, int64_t i,
                                        double (&a)[D][D]) {
@@ -383,10 +417,16 @@ __device__ __forceinline__ void tl_a_finish(const sphb_tl_params& P, int64_t i,
   stress_q<D>(P, Fi, B, Qi);
   store_f<D>(F, n, i, Fi);
   const int64_t qs = P.q_stride ? P.q_stride : n;
-  if (P.q32)
+  if (P.q32) {
     store_q32<D>(P.q32, qs, i, Qi);
-  else
+  } else if constexpr (D == 3) {
+    if (P.q_dense)
+      store_q_dense(Q, P.n, i, Qi);
+    else
+      store_q<D>(Q, qs, i, Qi, wi);
+  } else {
     store_q<D>(Q, qs, i, Qi, wi);
+  }
   {   // fused halo push of the boundary layers' Q records
     bool pushed = false;
     if (P.push_q_prev && i >= P.push_lo0 && i < P.push_lo1) {
@@ -409,7 +449,7 @@ __device__ __forceinline__ void tl_a_finish(const sphb_tl_params& P, int64_t i,
 }
 
 // Pass B after the pair loop (tlsph.py:164-171, 88-102, 200-202): a_i =
-// (acc + Q_i gsum) / rho0 (0 when clamped) into A {a, fixed} (+ push), the
+// (acc + Q_i gsum) / rho0 (0 when clamped; with_qi = false: acc / rho0) into A {a, fixed} (+ push), the
 // second kick v = v_half + dt/2 a when update_v (+ push); returns |v_i|.
 // acc = sum_j Q_j g0_ij, gsum = sum_j g0_ij.
 template <int D>
@@ -418,22 +458,30 @@ __device__ __forceinline__ double tl_b_finish(const sphb_tl_params& P, int64_t i
                                               const double4* __restrict__ Q,
                                               const double4* __restrict__ Vh,
                                               double4* __restrict__ A, double4* __restrict__ V,
-                                              const double* __restrict__ scalars, int update_v) {
+                                              const double* __restrict__ scalars, int update_v,
+                                              bool with_qi) {
   const int64_t n = P.n;
   const int64_t qs = P.q_stride ? P.q_stride : n;
   const double inv_rho0 = 1.0 / P.rho0;
-  double Qi[D][D];                  // loaded after the loop: 18 registers free in it
-  if (P.q32)
-    load_q32<D>(P.q32, qs, i, Qi);
-  else
-    load_q<D>(Q, qs, i, Qi);
+  if (with_qi) {
+    double Qi[D][D];                // loaded after the loop: 18 registers free in it
+    if (P.q32) {
+      load_q32<D>(P.q32, qs, i, Qi);
+    } else if constexpr (D == 3) {
+      if (P.q_dense)
+        load_q_dense(Q, n, i, Qi);
+      else
+        load_q<D>(Q, qs, i, Qi);
+    } else {
+      load_q<D>(Q, qs, i, Qi);
+    }
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double s = acc[a];
+    for (int a = 0; a < D; ++a)
 #pragma unroll
-    for (int b = 0; b < D; ++b) s = fma(Qi[a][b], gsum[b], s);
-    acc[a] = fixed_i ? 0.0 : s * inv_rho0;
+      for (int b = 0; b < D; ++b) acc[a] = fma(Qi[a][b], gsum[b], acc[a]);
   }
+#pragma unroll
+  for (int a = 0; a < D; ++a) acc[a] = fixed_i ? 0.0 : acc[a] * inv_rho0;
   {   // acceleration record {a0, a1, a2, fixed}: the clamp flag rides in .w
     double c4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll

@@ -64,7 +64,13 @@ __global__ void k_tl_kick(int64_t n, const double4* __restrict__ V, const double
   const bool fixed = a4.w != 0.0;
 #pragma unroll
   for (int a = 0; a < D; ++a) vh[a] = fixed ? 0.0 : fma(hdt, a_[a], v[a]);
-  store_vec<D>(Vh, i, vh);
+  {   // the clamp flag rides in Vh.w too (table-mode lattice pass B reads it)
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) c[a] = vh[a];
+    c[3] = a4.w;
+    Vh[i] = make_double4(c[0], c[1], c[2], c[3]);
+  }
   if (Vh32) {                       // FP32 mode: the gathered companion
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -210,7 +216,7 @@ k_tl_pass_b(const sphb_tl_params P, const double4* __restrict__ X0,
 #pragma unroll
         for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
     }
-    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
+    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
   }
   tl_block_speed_max<kThreads>(speed, scalars);
 }
@@ -227,7 +233,14 @@ __global__ void k_tl_stress(const sphb_tl_params P, const double4* __restrict__ 
   load_b0<D>(B0, P.n, i, B);
   load_x0<D>(X0, i, w, fixed);
   stress_q<D>(P, Fi, B, Qi);
-  store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);
+  if constexpr (D == 3) {
+    if (P.q_dense)
+      store_q_dense(Q, P.n, i, Qi);
+    else
+      store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);
+  } else {
+    store_q<D>(Q, P.q_stride ? P.q_stride : P.n, i, Qi, w);
+  }
   if (P.q32) store_q32<D>(P.q32, P.q_stride ? P.q_stride : P.n, i, Qi);
 }
 

@@ -193,7 +193,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
 }
 
 // Shell row of pass B (tl_engine.cu k_tl_pass_b, unstaged); returns |v_i|.
-template <int D, bool F32>
+template <int D, bool F32, bool X0J>
 __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
                                           const double4* __restrict__ X0,
                                           const int32_t* __restrict__ nbr,
@@ -218,8 +218,13 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
     double Qj[D][D], wj[D];
     if constexpr (D == 3) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], wj[c]);
-      if constexpr (F32) {        // the FP32 companion carries no X0 padding
+      for (int c = 0; c < 3; ++c) {
+        if constexpr (X0J && !F32)   // table mode: dense records (q_dense)
+          gather_qcol_dense(Q, n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
+        else
+          gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], wj[c]);
+      }
+      if constexpr (X0J) {        // no X0 padding (FP32 companion, table-mode rows)
         bool fixed_j;
         load_x0<D>(X0, j, wj, fixed_j);
       }
@@ -242,10 +247,10 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
 #pragma unroll
       for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
   }
-  return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
+  return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
 }
 
-template <int D, int R2, int MINB, bool F32>
+template <int D, int R2, int MINB, bool F32, bool TAB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const double4* __restrict__ B0,
@@ -268,6 +273,35 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   const int64_t i = row.i;
   const double dt = scalars[0];
   double wi[D], vhi[D];
+  if constexpr (TAB) {
+    // table geometry: g0 per slot, no X0 record; the Q padding (X0 for the
+    // shell rows' general pass B) is not needed: they read X0 themselves
+    load_vec<D>(Vh, i, vhi);
+    double m[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      wi[a] = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+    }
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      double vhj[D];
+      gather_vh<D, F32>(P, Vh, j, vhj);
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double dv = vhj[a] - vhi[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (o[b] != 0) m[a][b] = fma(dv, L.g[k][b], m[a][b]);
+      }
+    });
+    tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+    return;
+  }
   bool fixed_i;
   load_x0<D>(X0, i, wi, fixed_i);
   load_vec<D>(Vh, i, vhi);
@@ -305,7 +339,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
 }
 
-template <int D, int R2, int MINB, bool F32>
+template <int D, int R2, int MINB, bool F32, bool TAB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
@@ -320,8 +354,53 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
   if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
     const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
     if (ts < L.n_shell)
-      speed = shell_b<D, F32>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V, scalars,
-                              update_v);
+      speed = shell_b<D, F32, F32 || TAB>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V,
+                                          scalars, update_v);
+  } else if (TAB && t < L.n_interior) {
+    // table geometry: acc = sum_k Q_j g[k]; sum_k g[k] = 0 exactly (the
+    // table is antisymmetric), so the Q_i sum_j g0 term and Q_i vanish.
+    // Clamp flag: Vh.w (written by the kick) or, for accelerations() alone,
+    // X0.w.
+    const Row<D, R> row(L, t);
+    const int64_t i = row.i;
+    const int64_t qs = P.q_stride ? P.q_stride : P.n;
+    const bool fixed_i = update_v ? Vh[i].w != 0.0 : X0[i].w != 0.0;
+    double acc[D], gsum[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = gsum[a] = 0.0;
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      double Qj[D][D];
+      if constexpr (D == 3) {      // only the columns g touches (o_c != 0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (o[c] != 0) {
+            if constexpr (F32) {
+              double w_unused;
+              gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], w_unused);
+            } else {               // dense records (q_dense, set with the table)
+              gather_qcol_dense(Q, P.n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
+            }
+          } else {
+            Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
+          }
+        }
+      } else {
+        if constexpr (F32)
+          load_q32<D>(P.q32, qs, j, Qj);
+        else
+          load_mat_nc<D>(Q, j, Qj);
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (o[b] != 0) acc[a] = fma(Qj[a][b], L.g[k][b], acc[a]);
+    });
+    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, false);
   } else if (t < L.n_interior) {
     const Row<D, R> row(L, t);
     const int64_t i = row.i;
@@ -377,7 +456,7 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
         for (int b = 0; b < D; ++b)
           if (o[b] != 0) acc[a] = fma(Qj[a][b], g[b], acc[a]);
     });
-    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v);
+    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
   }
   tl_block_speed_max<kTT>(speed, scalars);
 }
@@ -424,7 +503,20 @@ __global__ void k_tl_lattice_check(const sphb_tl_params P, const sphb_tl_lattice
     seen |= 1ull << k;
   }
   if (ok) ok = __popcll(seen) == St::W;
-  if (ok) {
+  if (ok && L.table) {   // every pair's exact displacement within tol of the table
+    const double4 xi = X0[i];
+    const double wi[3] = {xi.x, xi.y, xi.z};
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      const double4 xj = X0[j];
+      const double wj[3] = {xj.x, xj.y, xj.z};
+#pragma unroll
+      for (int q = 0; q < D; ++q) ok = ok && fabs(__dsub_rn(wi[q], wj[q]) - L.dx[k][q]) <= tol;
+    });
+  } else if (ok) {
     const double4 xi = X0[i];
     const double wi[3] = {xi.x, xi.y, xi.z};
     static_for<St::W>([&](auto kc) {
@@ -515,18 +607,23 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
     return SPHB_ERR_ARG;
   if (L->n_interior + L->n_shell == 0) return SPHB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  static const int minb = tl_minb("SPHB_TLAT_MINB_A", 4);
+  // occupancy target: 4 (128 registers) for the exact geometry, 5 (96)
+  // for the table geometry (scripts/ab_tl.sh: C4 0.373 -> 0.362 ms/step)
+  static const int minb_env = tl_minb("SPHB_TLAT_MINB_A", 0);
   const bool f32 = p->vh32 && p->q32;
+  const bool tab = L->table != 0;
+  const int minb = minb_env ? minb_env : (tab ? 5 : 4);
   const unsigned grid = lattice_grid(L);
+#define SPHB_A2(D, R, MB, F, T)                                                             \
+  k_tl_lattice_a<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,          \
+      (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
+      (double4*)q, scalars, err)
 #define SPHB_A1(D, R, MB)                                                                   \
-  if (f32)                                                                                  \
-    k_tl_lattice_a<D, R, MB, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,        \
-        (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,        \
-        (double4*)q, scalars, err);                                                         \
-  else                                                                                      \
-    k_tl_lattice_a<D, R, MB, false><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,       \
-        (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,        \
-        (double4*)q, scalars, err);                                                         \
+  if (f32) {                                                                                \
+    if (tab) SPHB_A2(D, R, MB, true, true); else SPHB_A2(D, R, MB, true, false);            \
+  } else {                                                                                  \
+    if (tab) SPHB_A2(D, R, MB, false, true); else SPHB_A2(D, R, MB, false, false);          \
+  }                                                                                         \
   break
 #define SPHB_A(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
@@ -542,6 +639,7 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   SPHB_TLAT_CASES(SPHB_A)
 #undef SPHB_A
 #undef SPHB_A1
+#undef SPHB_A2
   return SPHB_ERR_ARG;
 }
 
@@ -557,16 +655,18 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   cudaStream_t st = (cudaStream_t)stream;
   static const int minb = tl_minb("SPHB_TLAT_MINB_B", 5);   // 96 registers (r02_ncu_c4.md)
   const bool f32 = p->vh32 && p->q32;
+  const bool tab = L->table != 0;
   const unsigned grid = lattice_grid(L);
+#define SPHB_B2(D, R, MB, F, T)                                                             \
+  k_tl_lattice_b<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,     \
+      cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,        \
+      (int)update_v)
 #define SPHB_B1(D, R, MB)                                                                   \
-  if (f32)                                                                                  \
-    k_tl_lattice_b<D, R, MB, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,   \
-        cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,      \
-        (int)update_v);                                                                     \
-  else                                                                                      \
-    k_tl_lattice_b<D, R, MB, false><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,  \
-        cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,      \
-        (int)update_v);                                                                     \
+  if (f32) {                                                                                \
+    if (tab) SPHB_B2(D, R, MB, true, true); else SPHB_B2(D, R, MB, true, false);            \
+  } else {                                                                                  \
+    if (tab) SPHB_B2(D, R, MB, false, true); else SPHB_B2(D, R, MB, false, false);          \
+  }                                                                                         \
   break
 #define SPHB_B(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
@@ -582,5 +682,6 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   SPHB_TLAT_CASES(SPHB_B)
 #undef SPHB_B
 #undef SPHB_B1
+#undef SPHB_B2
   return SPHB_ERR_ARG;
 }

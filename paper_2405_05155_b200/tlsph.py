@@ -405,8 +405,11 @@ class SolidSystem:
         configuration is a complete box lattice in engine order: the interior
         rows (full stencil) run the lattice passes, the shell rows the
         general ones through a row list.  Needs sphb_tl_lattice_check to
-        prove every interior row (pass-list set, bitwise separable
-        displacements, r2 near the slot's expansion point)."""
+        prove every interior row: its pass-list set and, for the default
+        table geometry (per-slot dx and g0, antisymmetric), every pair's
+        exact displacement within 1e-12 dp of its slot's; for the exact mode
+        (SPHB_TL_TABLE=0, or when the table check fails) bitwise separable
+        displacements and r2 near the slot's expansion point."""
         torch = _lib.torch_cuda()
         d, n, dp = self.dim, self.n, self.dp
         if d not in (2, 3) or n == 0 or int(self.grid.slow_axis) != d - 1 or n >= 2**31:
@@ -437,14 +440,26 @@ class SolidSystem:
         xw = self.X0rec[torch.tensor(rows, device=self._dev), :d].cpu().numpy()
         h = self.kernel.h
         c5v = -5.0 * (self.kernel.alpha / h * dp**d) / h      # tl_engine.cu ref_gradient
+        dxk = xw[0] - xw[1:]                          # (width, d), representative row
+        # table geometry: antisymmetric (slot W-1-k is the mirror of slot k
+        # in the canonical order), so sum_k g[k] = 0 exactly
+        half = width // 2
+        dxt = dxk.copy()
+        dxt[:half] = -dxk[::-1][:half]
         for k in range(width):
-            dx = xw[0] - xw[1 + k]
+            dx = dxk[k]
             r2k = float(np.sum(dx * dx))
             r = math.sqrt(r2k)
             t = 1.0 - 0.5 * r / h
             L.r2k[k] = r2k
             L.f[k] = c5v * ((t * t) * t)
             L.df[k] = 3.0 * c5v * t * t * (-0.25 / (h * r))
+            rt = math.sqrt(float(np.sum(dxt[k] * dxt[k])))
+            tt = 1.0 - 0.5 * rt / h
+            ft = c5v * ((tt * tt) * tt)
+            for a in range(d):
+                L.dx[k][a] = float(dxt[k][a])
+                L.g[k][a] = ft * float(dxt[k][a])
         idx = torch.arange(n, device=self._dev)
         coord = [idx % ext[0], (idx // ext[0]) % ext[1] if d > 1 else None,
                  idx // (ext[0] * ext[1]) if d > 2 else None]
@@ -453,12 +468,24 @@ class SolidSystem:
             inner &= (coord[a] >= R) & (coord[a] < ext[a] - R)
         self._shell = torch.nonzero(~inner).flatten().to(torch.int32).contiguous()
         L.shell, L.n_shell = self._shell.data_ptr(), int(self._shell.numel())
-        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
-        _lib.call("sphb_tl_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
-                  self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), 1e-10,
-                  bad.data_ptr(), _lib.stream_ptr())
-        if int(bad.item()) == 0:
-            self.lattice = L
+        # table geometry (default; SPHB_TL_TABLE=0 keeps the exact separable
+        # geometry): every interior pair within 1e-12 dp of its slot's dx,
+        # else the exact mode's proof (bitwise separability, r2 near r2k)
+        modes = [(1, 1e-12 * dp), (0, 1e-10)]
+        if os.environ.get("SPHB_TL_TABLE", "1") == "0":
+            modes = modes[1:]
+        for table, tol in modes:
+            L.table = table
+            bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
+            _lib.call("sphb_tl_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
+                      self.X0rec.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(), tol,
+                      bad.data_ptr(), _lib.stream_ptr())
+            if int(bad.item()) == 0:
+                self.lattice = L
+                # table mode: dense 3D Q records (no X0 padding, 24-byte column
+                # gathers in pass B); every Q writer and reader honours the flag
+                self.params.q_dense = int(table == 1 and d == 3 and self._q_stride == n)
+                return
 
     def _pass_b(self, update_v):
         st = _lib.stream_ptr()

@@ -592,23 +592,6 @@ int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, co
                            const double* B0, const int32_t* nbr, const int32_t* cnt,
                            const double* Vh, double* XC, double* F, double* Q,
                            const double* scalars, int32_t* err, void* stream);
-/* One TL step (kick, pass A, pass B; no sphb_set_dt) in ONE launch on a
- * table-mode 3D lattice with dense Q (one GPU, FP64): persistent CTAs work
- * through items of 128 rows in plane order, each pass of plane z waiting
- * only for the planes z-R..z+R it gathers from, so pass A of one plane
- * overlaps pass B of an older one.  items: int32 quadruples {phase (0 kick,
- * 1 A, 2 B), plane, begin, end | kind << 30} (kick: row range; A/B kind 0:
- * interior index range, kind 1: shell-list range), topologically ordered;
- * need[phase * n[2] + z] = items of (phase, z); ctr = 1 + 3 n[2] int32
- * scratch counters (zeroed on the stream).  Needs n < 2^30.  Each item
- * waits for planes z-R-1..z+R+1 of the previous phase.  Same records and results as sphb_tl_kick + sphb_tl_pass_a_lattice +
- * sphb_tl_pass_b_lattice (update_v = 1). */
-int sphb_tl_step_lattice_fused(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                               const int32_t* items, int32_t n_items, const int32_t* need,
-                               int32_t* ctr, const double* X0, const double* B0,
-                               const int32_t* nbr, const int32_t* cnt, double* V, double* A,
-                               double* Vh, double* XC, double* F, double* Q, double* scalars,
-                               int32_t* err, void* stream);
 int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
                            const int32_t* nbr, const int32_t* cnt, const double* Q,
                            const double* Vh, double* A, double* V, double* scalars,

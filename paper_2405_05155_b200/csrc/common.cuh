@@ -173,28 +173,6 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
   return v;
 }
 
-// Coherent loads of records written earlier in the SAME launch by other CTAs
-// (the fused TL step, tl_lattice.cu): never the read-only .nc path, which the
-// compiler may hoist above a dependency wait; volatile asm keeps them after
-// the wait's volatile asm in program order.
-__device__ __forceinline__ double4 ld4_coh(const double4* p) {
-  double4 v;
-  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double2 ld2_coh(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double ld1_coh(const double* p) {
-  double v;
-  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
 // 1/sqrt(x) and 1/x for normal positive doubles: MUFU seed (~2^-23) and
 // one third-order correction (error ~eps^3, below double rounding), i.e. the
 // accuracy of two Newton steps with a shorter dependent chain; no

@@ -121,16 +121,13 @@ __device__ __forceinline__ void store_q_dense(double4* __restrict__ Q, int64_t n
 }
 
 // column c of a dense record, read-only path (16 + 8 bytes)
-template <bool COH = false>
 __device__ __forceinline__ void gather_qcol_dense(const double4* __restrict__ Q, int64_t n, int c,
                                                   int64_t j, double& q0, double& q1,
                                                   double& q2) {
-  const double2* p2 = reinterpret_cast<const double2*>(Q) + c * n + j;
-  const double* p1 = reinterpret_cast<const double*>(Q) + 6 * n + c * n + j;
-  const double2 t = COH ? ld2_coh(p2) : __ldg(p2);
+  const double2 t = __ldg(reinterpret_cast<const double2*>(Q) + c * n + j);
   q0 = t.x;
   q1 = t.y;
-  q2 = COH ? ld1_coh(p1) : __ldg(p1);
+  q2 = __ldg(reinterpret_cast<const double*>(Q) + 6 * n + c * n + j);
 }
 
 __device__ __forceinline__ void load_q_dense(const double4* __restrict__ Q, int64_t n, int64_t i,
@@ -455,7 +452,7 @@ __device__ __forceinline__ void tl_a_finish(const sphb_tl_params& P, int64_t i,
 // (acc + Q_i gsum) / rho0 (0 when clamped; with_qi = false: acc / rho0) into A {a, fixed} (+ push), the
 // second kick v = v_half + dt/2 a when update_v (+ push); returns |v_i|.
 // acc = sum_j Q_j g0_ij, gsum = sum_j g0_ij.
-template <int D, bool COH = false>
+template <int D>
 __device__ __forceinline__ double tl_b_finish(const sphb_tl_params& P, int64_t i, bool fixed_i,
                                               double (&acc)[D], const double (&gsum)[D],
                                               const double4* __restrict__ Q,
@@ -500,14 +497,7 @@ __device__ __forceinline__ double tl_b_finish(const sphb_tl_params& P, int64_t i
   double v[D];
   if (update_v) {
     const double hdt = 0.5 * scalars[0];
-    if constexpr (COH) {            // Vh written by this launch (fused step)
-      const double4 t = ld4_coh(Vh + i);
-      const double c[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-      for (int a = 0; a < D; ++a) v[a] = c[a];
-    } else {
-      load_vec<D>(Vh, i, v);
-    }
+    load_vec<D>(Vh, i, v);
 #pragma unroll
     for (int a = 0; a < D; ++a) v[a] = fixed_i ? 0.0 : fma(hdt, acc[a], v[a]);
     store_vec<D>(V, i, v);

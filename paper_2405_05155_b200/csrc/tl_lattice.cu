@@ -121,15 +121,10 @@ __device__ __forceinline__ void axis_displacements(const double4* __restrict__ X
 
 // neighbour gathers of the FP64 records or, in the FP32 mode, of their
 // FP32 companions (sphb_tl_params.vh32 / q32)
-template <int D, bool F32, bool COH = false>
+template <int D, bool F32>
 __device__ __forceinline__ void gather_vh(const sphb_tl_params& P, const double4* __restrict__ Vh,
                                           int64_t j, double (&v)[D]) {
-  if constexpr (COH && !F32) {      // written by this launch (fused step)
-    const double4 t = ld4_coh(Vh + j);
-    const double c[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-    for (int a = 0; a < D; ++a) v[a] = c[a];
-  } else if constexpr (F32) {
+  if constexpr (F32) {
     const float4 t = __ldg(reinterpret_cast<const float4*>(P.vh32) + j);
     const float c[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
@@ -155,7 +150,7 @@ __device__ __forceinline__ void gather_qcol(const sphb_tl_params& P, const doubl
 
 // Shell row of pass A: the general pair loop (tl_engine.cu k_tl_pass_a,
 // unstaged) — pass list, X0_j gather, g0 recomputed (ref_gradient).
-template <int D, bool F32, bool COH = false>
+template <int D, bool F32>
 __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
                                         const double4* __restrict__ X0,
                                         const double4* __restrict__ B0,
@@ -170,7 +165,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
   double wi[D], vhi[D];
   bool fixed_i;
   load_x0<D>(X0, i, wi, fixed_i);
-  gather_vh<D, false, COH>(P, Vh, i, vhi);
+  load_vec<D>(Vh, i, vhi);
   double m[D][D];
 #pragma unroll
   for (int a = 0; a < D; ++a)
@@ -182,7 +177,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
     SPHB_CHECK_INDEX(j, n, err);
     double vhj[D], wj[D], dx[D], g[D];
     bool fixed_j;
-    gather_vh<D, F32, COH>(P, Vh, j, vhj);
+    gather_vh<D, F32>(P, Vh, j, vhj);
     load_x0<D>(X0, j, wj, fixed_j);
 #pragma unroll
     for (int a = 0; a < D; ++a) dx[a] = wi[a] - wj[a];
@@ -198,7 +193,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
 }
 
 // Shell row of pass B (tl_engine.cu k_tl_pass_b, unstaged); returns |v_i|.
-template <int D, bool F32, bool X0J, bool COH = false>
+template <int D, bool F32, bool X0J>
 __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
                                           const double4* __restrict__ X0,
                                           const int32_t* __restrict__ nbr,
@@ -225,7 +220,7 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if constexpr (X0J && !F32)   // table mode: dense records (q_dense)
-          gather_qcol_dense<COH>(Q, n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
+          gather_qcol_dense(Q, n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
         else
           gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], wj[c]);
       }
@@ -252,101 +247,7 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
 #pragma unroll
       for (int b = 0; b < D; ++b) acc[a] = fma(Qj[a][b], g[b], acc[a]);
   }
-  return tl_b_finish<D, COH>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
-}
-
-// Interior row of pass A with the table geometry (sphb_tl_lattice.table):
-// m = sum_k (v_half_j - v_half_i) (x) g[k], then tl_a_finish.  No X0 record;
-// the Q padding (X0 for the general pass B) is not written: the shell rows
-// read X0 themselves.  COH: Vh was written by this launch (fused step).
-template <int D, int R2, bool F32, bool COH>
-__device__ __forceinline__ void lat_a_row_tab(const sphb_tl_params& P, const sphb_tl_lattice& L,
-                                              const Row<D, Stencil<D, R2>::R>& row,
-                                              const double4* __restrict__ B0,
-                                              const double4* Vh, double4* __restrict__ XC,
-                                              double4* __restrict__ F, double4* __restrict__ Q,
-                                              double dt, int32_t* __restrict__ err) {
-  using St = Stencil<D, R2>;
-  const int64_t i = row.i;
-  double wi[D], vhi[D];
-  gather_vh<D, false, COH>(P, Vh, i, vhi);
-  double m[D][D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    wi[a] = 0.0;
-#pragma unroll
-    for (int b = 0; b < D; ++b) m[a][b] = 0.0;
-  }
-  static_for<St::W>([&](auto kc) {
-    constexpr int k = decltype(kc)::value;
-    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-    const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
-                      (int64_t)o[2] * row.stride[2];
-    double vhj[D];
-    gather_vh<D, F32, COH>(P, Vh, j, vhj);
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const double dv = vhj[a] - vhi[a];
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (o[b] != 0) m[a][b] = fma(dv, L.g[k][b], m[a][b]);
-    }
-  });
-  tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
-}
-
-// Interior row of pass B with the table geometry: acc = sum_k Q_j g[k];
-// sum_k g[k] = 0 exactly (antisymmetric table), so the Q_i sum_j g0 term and
-// Q_i vanish.  Clamp flag: Vh.w (written by the kick) or, for
-// accelerations() alone, X0.w.  Returns |v_i|.
-template <int D, int R2, bool F32, bool COH>
-__device__ __forceinline__ double lat_b_row_tab(const sphb_tl_params& P, const sphb_tl_lattice& L,
-                                                const Row<D, Stencil<D, R2>::R>& row,
-                                                const double4* __restrict__ X0,
-                                                const double4* Q, const double4* Vh,
-                                                double4* __restrict__ A, double4* __restrict__ V,
-                                                const double* __restrict__ scalars,
-                                                int update_v) {
-  using St = Stencil<D, R2>;
-  const int64_t i = row.i;
-  const int64_t qs = P.q_stride ? P.q_stride : P.n;
-  const bool fixed_i = update_v ? (COH ? ld4_coh(Vh + i).w : Vh[i].w) != 0.0 : X0[i].w != 0.0;
-  double acc[D], gsum[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) acc[a] = gsum[a] = 0.0;
-  static_for<St::W>([&](auto kc) {
-    constexpr int k = decltype(kc)::value;
-    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-    const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
-                      (int64_t)o[2] * row.stride[2];
-    double Qj[D][D];
-    if constexpr (D == 3) {      // only the columns g touches (o_c != 0)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (o[c] != 0) {
-          if constexpr (F32) {
-            double w_unused;
-            gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], w_unused);
-          } else {               // dense records (q_dense, set with the table)
-            gather_qcol_dense<COH>(Q, P.n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
-          }
-        } else {
-          Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
-        }
-      }
-    } else {
-      if constexpr (F32)
-        load_q32<D>(P.q32, qs, j, Qj);
-      else
-        load_mat_nc<D>(Q, j, Qj);
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (o[b] != 0) acc[a] = fma(Qj[a][b], L.g[k][b], acc[a]);
-  });
-  return tl_b_finish<D, COH>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, false);
+  return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
 }
 
 template <int D, int R2, int MINB, bool F32, bool TAB>
@@ -373,7 +274,32 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   const double dt = scalars[0];
   double wi[D], vhi[D];
   if constexpr (TAB) {
-    lat_a_row_tab<D, R2, F32, false>(P, L, row, B0, Vh, XC, F, Q, dt, err);
+    // table geometry: g0 per slot, no X0 record; the Q padding (X0 for the
+    // shell rows' general pass B) is not needed: they read X0 themselves
+    load_vec<D>(Vh, i, vhi);
+    double m[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      wi[a] = 0.0;
+#pragma unroll
+      for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+    }
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      double vhj[D];
+      gather_vh<D, F32>(P, Vh, j, vhj);
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double dv = vhj[a] - vhi[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (o[b] != 0) m[a][b] = fma(dv, L.g[k][b], m[a][b]);
+      }
+    });
+    tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
     return;
   }
   bool fixed_i;
@@ -431,8 +357,50 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
       speed = shell_b<D, F32, F32 || TAB>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V,
                                           scalars, update_v);
   } else if (TAB && t < L.n_interior) {
-    speed = lat_b_row_tab<D, R2, F32, false>(P, L, Row<D, Stencil<D, R2>::R>(L, t), X0, Q, Vh, A, V,
-                                             scalars, update_v);
+    // table geometry: acc = sum_k Q_j g[k]; sum_k g[k] = 0 exactly (the
+    // table is antisymmetric), so the Q_i sum_j g0 term and Q_i vanish.
+    // Clamp flag: Vh.w (written by the kick) or, for accelerations() alone,
+    // X0.w.
+    const Row<D, R> row(L, t);
+    const int64_t i = row.i;
+    const int64_t qs = P.q_stride ? P.q_stride : P.n;
+    const bool fixed_i = update_v ? Vh[i].w != 0.0 : X0[i].w != 0.0;
+    double acc[D], gsum[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = gsum[a] = 0.0;
+    static_for<St::W>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                        (int64_t)o[2] * row.stride[2];
+      double Qj[D][D];
+      if constexpr (D == 3) {      // only the columns g touches (o_c != 0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (o[c] != 0) {
+            if constexpr (F32) {
+              double w_unused;
+              gather_qcol<F32>(P, Q, qs, c, j, Qj[0][c], Qj[1][c], Qj[2][c], w_unused);
+            } else {               // dense records (q_dense, set with the table)
+              gather_qcol_dense(Q, P.n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
+            }
+          } else {
+            Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
+          }
+        }
+      } else {
+        if constexpr (F32)
+          load_q32<D>(P.q32, qs, j, Qj);
+        else
+          load_mat_nc<D>(Q, j, Qj);
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (o[b] != 0) acc[a] = fma(Qj[a][b], L.g[k][b], acc[a]);
+    });
+    speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, false);
   } else if (t < L.n_interior) {
     const Row<D, R> row(L, t);
     const int64_t i = row.i;
@@ -572,112 +540,6 @@ __global__ void k_tl_lattice_check(const sphb_tl_params P, const sphb_tl_lattice
     });
   }
   if (!ok) atomicAdd(bad, 1ull);
-}
-
-// ------------------------------------------------------ fused step (C4)
-// One launch per step for a table-mode lattice (3D, FP64, one GPU): the
-// kick, pass A and pass B of every lattice plane z (slow axis) as work items
-// of 128 rows, claimed in a fixed order by persistent CTAs.  A(z) needs the
-// kick of planes z-R..z+R, B(z) pass A of planes z-R..z+R (the stencil and
-// every shell row's pass list stay within R planes); the item order (the
-// kick of plane g, pass A of plane g - lag_a, pass B of plane g - lag_b) is
-// topological, so waits only ever target items claimed earlier.  While the
-// HBM-bound pass A of one plane runs, the L1-bound pass B of an older plane
-// runs beside it on the same SMs, and each plane's Vh / Q are still in L2
-// when the next phase gathers them.  Fields are bit-identical to the three
-// separate launches (same per-row arithmetic).
-//
-// Synchronisation: the producer CTA's rows are written, __syncthreads, then
-// one red.release.gpu on done[phase][z]; a consumer thread spins on
-// ld.relaxed.gpu until every needed counter is complete, then
-// __syncthreads.  No acquire (it would invalidate the SM's L1, which pass B
-// depends on): records produced in this launch are read only after their
-// plane completed, with coherent (non-.nc) loads, and an item waits for one
-// plane more than it gathers on each side, so every 32-byte sector it can
-// touch (one straddling a plane boundary included) was complete before any
-// L1 cached it.  L1 holds nothing from before the launch.
-struct FusedItem {
-  int32_t phase;   // 0 kick (rows), 1 pass A, 2 pass B
-  int32_t plane;
-  int32_t begin;   // kick: rows; A/B: interior index t (kind 0) or shell index (kind 1)
-  int32_t end_kind;   // end | kind << 30
-};
-
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(int* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <int R2>
-__global__ void __launch_bounds__(kTT, 5)
-k_tl_fused_step(const sphb_tl_params P, const sphb_tl_lattice L,
-                const FusedItem* __restrict__ items, const int32_t n_items,
-                const int32_t* __restrict__ need, int32_t* ctr,
-                const double4* __restrict__ X0, const double4* __restrict__ B0,
-                const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
-                double4* V, double4* A, double4* Vh, double4* __restrict__ XC,
-                double4* __restrict__ F, double4* Q, double* __restrict__ scalars,
-                int32_t* __restrict__ err) {
-  constexpr int D = 3;
-  using St = Stencil<D, R2>;
-  constexpr int R = St::R;
-  const int n2 = L.n[2];
-  int* next = ctr;
-  int* done = ctr + 1;                 // done[phase * n2 + z]
-  __shared__ int s_item;
-  const double dt = scalars[0];
-  const double hdt = 0.5 * dt;
-  double speed = 0.0;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
-    __syncthreads();
-    const int it = s_item;
-    if (it >= n_items) break;
-    const FusedItem w = items[it];
-    const int phase = w.phase, z = w.plane;
-    const int end = w.end_kind & ((1 << 30) - 1), kind = w.end_kind >> 30;
-    if (phase > 0 && threadIdx.x == 0) {
-      const int* dn = done + (phase - 1) * n2;
-      const int* nd = need + (phase - 1) * n2;
-      // planes z-R..z+R are gathered; one more on each side, so a 32-byte
-      // sector that straddles the window's edge is complete when cached
-      const int z0 = z - R - 1 < 0 ? 0 : z - R - 1, z1 = z + R + 1 > n2 - 1 ? n2 - 1 : z + R + 1;
-      for (int zz = z0; zz <= z1; ++zz)
-        while (ld_relaxed(dn + zz) < nd[zz]) __nanosleep(128);
-    }
-    __syncthreads();                   // also: s_item may be overwritten now
-    for (int r = w.begin + (int)threadIdx.x; r < end; r += kTT) {
-      if (phase == 0) {                // kick: Vh = v + dt/2 a (0 when clamped), Vh.w = flag
-        const double4 v4 = V[r], a4 = A[r];
-        const bool fixed = a4.w != 0.0;
-        Vh[r] = make_double4(fixed ? 0.0 : fma(hdt, a4.x, v4.x),
-                             fixed ? 0.0 : fma(hdt, a4.y, v4.y),
-                             fixed ? 0.0 : fma(hdt, a4.z, v4.z), a4.w);
-      } else if (phase == 1) {
-        if (kind == 0)
-          lat_a_row_tab<D, R2, false, true>(P, L, Row<D, R>(L, r), B0, Vh, XC, F, Q, dt, err);
-        else
-          shell_a<D, false, true>(P, (int64_t)L.shell[r], X0, B0, nbr, cnt, Vh, XC, F, Q, dt,
-                                  err);
-      } else {
-        double sp;
-        if (kind == 0)
-          sp = lat_b_row_tab<D, R2, false, true>(P, L, Row<D, R>(L, r), X0, Q, Vh, A, V,
-                                                 scalars, 1);
-        else
-          sp = shell_b<D, false, true, true>(P, (int64_t)L.shell[r], X0, nbr, cnt, Q, Vh, A, V,
-                                             scalars, 1);
-        speed = sp > speed ? sp : speed;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) red_release_add(done + phase * n2 + z, 1);
-  }
-  tl_block_speed_max<kTT>(speed, scalars);
 }
 
 }  // namespace
@@ -822,49 +684,4 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
 #undef SPHB_B1
 #undef SPHB_B2
   return SPHB_ERR_ARG;
-}
-
-
-// Fused step (see k_tl_fused_step): items / need from the host (the plane
-// schedule), ctr = 1 + 3 n[2] int32 counters (zeroed here, on the stream).
-extern "C" int sphb_tl_step_lattice_fused(const sphb_tl_params* p, const sphb_tl_lattice* L,
-                                          const int32_t* items, int32_t n_items,
-                                          const int32_t* need, int32_t* ctr, const double* x0,
-                                          const double* b0, const int32_t* nbr,
-                                          const int32_t* cnt, double* v, double* a, double* vh,
-                                          double* xc, double* f, double* q, double* scalars,
-                                          int32_t* err, void* stream) {
-  if (!tl_lattice_ok(p, L) || p->dim != 3 || !L->table || !p->q_dense || p->vh32 || p->q32 ||
-      !items || n_items <= 0 || !need || !ctr || !x0 || !b0 || !nbr || !cnt || !v || !a ||
-      !vh || !xc || !f || !q || !scalars || (L->r2 != 3 && L->r2 != 5) ||
-      p->n >= ((int64_t)1 << 30))
-    return SPHB_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  SPHB_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(int32_t) * (1 + 3 * (size_t)L->n[2]), st));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static int occ3 = 0, occ5 = 0;
-  int& occ = L->r2 == 3 ? occ3 : occ5;
-  if (!occ) {
-    if (L->r2 == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tl_fused_step<3>, kTT, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tl_fused_step<5>, kTT, 0);
-    if (occ < 1) occ = 1;
-  }
-  int grid = sms * occ;
-  if (grid > n_items) grid = n_items;
-  const FusedItem* it = reinterpret_cast<const FusedItem*>(items);
-#define SPHB_F(R2)                                                                          \
-  k_tl_fused_step<R2><<<grid, kTT, 0, st>>>(*p, *L, it, n_items, need, ctr,                 \
-      (const double4*)x0, (const double4*)b0, nbr, cnt, (double4*)v, (double4*)a,           \
-      (double4*)vh, (double4*)xc, (double4*)f, (double4*)q, scalars, err)
-  if (L->r2 == 3) SPHB_F(3); else SPHB_F(5);
-#undef SPHB_F
-  SPHB_LAUNCH_CHECK();
-  return SPHB_OK;
 }

@@ -323,7 +323,6 @@ class SolidSystem:
                       self.g0.data_ptr(), _lib.stream_ptr())
         self._g0_ptr = None if self.g0 is None else self.g0.data_ptr()
         self.lattice = None
-        self._fused = None
         if (_slab is None and self.g0 is None and self.order is not self.bins
                 and os.environ.get("SPHB_TL_LATTICE", "1") != "0"):
             self._setup_lattice()
@@ -340,7 +339,6 @@ class SolidSystem:
             self.Q32 = torch.zeros((3 if d == 3 else 1, self._q_stride, 4),
                                    dtype=torch.float32, device=dev)
             p.vh32, p.q32 = self.Vh32.data_ptr(), self.Q32.data_ptr()
-            self._fused = None               # the fused step is FP64-records only
         self._setup_push(dev)
         self._acc_valid = False
         self._host = {}
@@ -487,52 +485,7 @@ class SolidSystem:
                 # table mode: dense 3D Q records (no X0 padding, 24-byte column
                 # gathers in pass B); every Q writer and reader honours the flag
                 self.params.q_dense = int(table == 1 and d == 3 and self._q_stride == n)
-                if self.params.q_dense:
-                    self._setup_fused(ext, R)
                 return
-
-    def _setup_fused(self, ext, R):
-        """Plane schedule of the fused step (sphb_tl_step_lattice_fused: kick,
-        pass A and pass B of a table-mode 3D lattice in one launch;
-        SPHB_TL_FUSED=0 keeps the three launches).  Items of 128 rows: the
-        kick of plane g, pass A of plane g - lag_a, pass B of plane g - lag_b,
-        so every item's dependencies (planes z-R-1..z+R+1 of the previous
-        phase) come earlier in the list."""
-        self._fused = None
-        n0, n1, n2 = ext
-        plane = n0 * n1
-        if (os.environ.get("SPHB_TL_FUSED", "1") == "0" or self._slab is not None
-                or self.n >= 2**30):
-            return
-        torch = _lib.torch_cuda()
-        m0, m1 = n0 - 2 * R, n1 - 2 * R
-        shell = self._shell.cpu().numpy().astype(np.int64)
-        soff = np.searchsorted(shell // plane, np.arange(n2 + 1))
-        lag = int(os.environ.get("SPHB_TL_FUSED_LAG", str(R + 3)))   # groups
-        lag_a, lag_b = lag, 2 * lag
-        items, need = [], np.zeros((3, n2), dtype=np.int32)
-
-        chunk = int(os.environ.get("SPHB_TL_FUSED_CHUNK", "128"))
-
-        def add(phase, z, b, e, kind):
-            for c in range(b, e, chunk):
-                items.append((phase, z, c, min(c + chunk, e) | (kind << 30)))
-                need[phase, z] += 1
-
-        for g in range(n2 + lag_b):
-            if g < n2:
-                add(0, g, g * plane, (g + 1) * plane, 0)
-            for phase, lg in ((1, lag_a), (2, lag_b)):
-                z = g - lg
-                if 0 <= z < n2:
-                    if R <= z < n2 - R:
-                        t0 = (z - R) * m0 * m1
-                        add(phase, z, t0, t0 + m0 * m1, 0)
-                    add(phase, z, int(soff[z]), int(soff[z + 1]), 1)
-        it = torch.tensor(np.asarray(items, dtype=np.int32).ravel(), device=self._dev)
-        nd = torch.tensor(need.ravel(), device=self._dev)
-        ctr = torch.zeros(1 + 3 * n2, dtype=torch.int32, device=self._dev)
-        self._fused = (it, len(items), nd, ctr)
 
     def _pass_b(self, update_v):
         st = _lib.stream_ptr()
@@ -643,19 +596,6 @@ class SolidSystem:
         self._set_push(True)
         _lib.call("sphb_set_dt", self._cfl_h, self._c_s, dt_override, self.scalars.data_ptr(),
                   self.err.data_ptr(), st)
-        if self._fused is not None:
-            # kick + pass A + pass B of every plane in one launch
-            it, n_items, nd, ctr = self._fused
-            _lib.call("sphb_tl_step_lattice_fused", ctypes.byref(self.params),
-                      ctypes.byref(self.lattice), it.data_ptr(), n_items, nd.data_ptr(),
-                      ctr.data_ptr(), self.X0rec.data_ptr(), self.B0rec.data_ptr(),
-                      self.nbr.data_ptr(), self.cnt.data_ptr(), self.V.data_ptr(),
-                      self.A.data_ptr(), self.Vh.data_ptr(), self.XC.data_ptr(),
-                      self.Frec.data_ptr(), self.Qrec.data_ptr(), self.scalars.data_ptr(),
-                      self.err.data_ptr(), st)
-            self._set_push(False)
-            self._reduce_speed()
-            return
         if self.lattice is not None:
             # kick, then pass A over the interior (lattice) and shell rows
             _lib.call("sphb_tl_kick", ctypes.byref(self.params), self.V.data_ptr(),

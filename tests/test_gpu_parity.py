@@ -940,53 +940,6 @@ def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwa
         assert max(errs) < 1e-10, errs
 
 
-@pytest.mark.parametrize("key", ["1.6h", "2h"])
-@pytest.mark.parametrize("n_width", [8, 11])
-def test_tl_fused_step_bit_identical(monkeypatch, key, n_width):
-    """The fused TL step (kick + pass A + pass B of every plane in one
-    persistent launch, plane-level dependencies) gives bit-identical records
-    to the three separate launches, eager and in CUDA-graph replay; n_width
-    11 has rows per plane not a multiple of 4 (Q sectors straddle planes)."""
-    cfg = configs.c4_column(kernel=key, n_width=n_width)
-    fused = make_tl(cfg)
-    assert fused.lattice is not None and fused.lattice.table == 1
-    assert fused._fused is not None
-    monkeypatch.setenv("SPHB_TL_FUSED", "0")
-    split = make_tl(cfg)
-    assert split.lattice is not None and split._fused is None
-    for s in (fused, split):
-        s.step()
-    for name in ("x", "v", "F"):
-        assert np.array_equal(getattr(fused, name), getattr(split, name)), name
-    for s in (fused, split):
-        s.advance(37)                     # graph replay + eager remainder
-    for name in ("x", "v", "F"):
-        assert np.array_equal(getattr(fused, name), getattr(split, name)), name
-
-
-@pytest.mark.parametrize("key", ["1.6h", "2h"])
-def test_tl_exact_geometry_mode_vs_oracle(monkeypatch, key):
-    """SPHB_TL_TABLE=0: the lattice passes with the exact separable geometry
-    (no slot table) still match the oracle."""
-    monkeypatch.setenv("SPHB_TL_TABLE", "0")
-    cfg = configs.c4_column(kernel=key, n_width=8)
-    s = make_tl(cfg)
-    assert s.lattice is not None and s.lattice.table == 0 and s._fused is None
-    m = cfg["material"]
-    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
-                    cfg["cfl"])
-    ref.v = cfg["v0"].copy()
-    s.step()
-    ref.step()
-    errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
-    assert max(errs) < TOL_1, errs
-    s.advance(49)
-    for _ in range(49):
-        ref.step()
-    errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
-    assert max(errs) < 1e-10, errs
-
-
 # ------------------------------------------- non-Wendland flow / solid kernels
 def test_wc_laguerre_gauss_kernel_vs_oracle():
     """EulerianSolver accepts any KernelSpec (eulerian.py:473-524): the

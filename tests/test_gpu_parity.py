@@ -940,6 +940,29 @@ def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwa
         assert max(errs) < 1e-10, errs
 
 
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_tl_exact_geometry_mode_vs_oracle(monkeypatch, key):
+    """SPHB_TL_TABLE=0: the lattice passes with the exact separable geometry
+    (no slot table, padded Q records) still match the oracle."""
+    monkeypatch.setenv("SPHB_TL_TABLE", "0")
+    cfg = configs.c4_column(kernel=key, n_width=8)
+    s = make_tl(cfg)
+    assert s.lattice is not None and s.lattice.table == 0 and s.params.q_dense == 0
+    m = cfg["material"]
+    ref = O.SolidTL(cfg["X0"], m.rho0, m.E, m.nu, cfg["spec"], cfg["dp"], cfg["fixed"], True,
+                    cfg["cfl"])
+    ref.v = cfg["v0"].copy()
+    s.step()
+    ref.step()
+    errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
+    assert max(errs) < TOL_1, errs
+    s.advance(49)
+    for _ in range(49):
+        ref.step()
+    errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
+    assert max(errs) < 1e-10, errs
+
+
 # ------------------------------------------- non-Wendland flow / solid kernels
 def test_wc_laguerre_gauss_kernel_vs_oracle():
     """EulerianSolver accepts any KernelSpec (eulerian.py:473-524): the

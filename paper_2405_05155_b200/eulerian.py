@@ -484,6 +484,7 @@ class EulerianSolver:
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self._rho_io = torch.empty(self.n, dtype=torch.float64, device=dev)
         self._mom_io = torch.empty((self.n, self.dim), dtype=torch.float64, device=dev)
+        self._io = None                 # pinned-host state transfers (_io_streams)
         self._vol_host = vol
         self.timer = None   # optional list collecting (stage, start_event, end_event)
         self._push = None
@@ -568,32 +569,112 @@ class EulerianSolver:
     def load_state(self, rho, mom) -> None:
         """Upload (rho (n,), mom (n, d)) given in caller order.
 
-        Accepts numpy arrays or torch tensors; pinned host tensors are copied
-        asynchronously on the current stream (no host synchronisation).
+        Accepts numpy arrays or torch tensors.  Pinned host tensors are copied
+        asynchronously on a dedicated host-to-device stream into one of two
+        device staging buffers, so the copy overlaps whatever the GPU is
+        still doing (the previous read_state's device-to-host copy included,
+        unless it writes into these very host buffers); the caller's stream
+        waits for it only before unpacking it into the solver state.
         """
         torch = _lib.torch_cuda()
-        if isinstance(rho, torch.Tensor) and rho.device.type == "cpu":
+        if isinstance(rho, torch.Tensor) and rho.device.type == "cpu" and rho.is_pinned():
+            io = self._io_streams()
+            k = io["kin"]
+            io["kin"] ^= 1
+            cur = torch.cuda.current_stream()
+            h2d = io["h2d"]
+            if io["in_free"][k] is None:
+                h2d.wait_stream(cur)
+            else:                                   # the slot's previous pack is done
+                h2d.wait_event(io["in_free"][k])
+            for lo, hi, ev in io["pending"]:        # D2H still writing these host buffers
+                if any(_overlaps(t, lo, hi) for t in (rho, mom)):
+                    h2d.wait_event(ev)
+            with torch.cuda.stream(h2d):
+                rho_d = io["rin"][k].copy_(rho, non_blocking=True)
+                mom_d = io["min"][k].copy_(mom.reshape(self.n, self.dim), non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(h2d)
+            cur.wait_event(ready)
+        elif isinstance(rho, torch.Tensor) and rho.device.type == "cpu":
             rho_d = self._rho_io.copy_(rho, non_blocking=True)
             mom_d = self._mom_io.copy_(mom.reshape(self.n, self.dim), non_blocking=True)
+            io = None
         else:
             rho_d = _lib.to_device(rho, torch.float64)
             mom_d = _lib.to_device(mom, torch.float64).reshape(self.n, self.dim)
+            io = None
         _lib.call("sphb_wc_pack_state", self.n, self.dim, self.order.perm.data_ptr(),
                   rho_d.data_ptr(), mom_d.data_ptr(), self.S.data_ptr(), self.M.data_ptr(),
                   _lib.stream_ptr())
+        if io is not None:                          # staging slot free again after the pack
+            free = torch.cuda.Event()
+            free.record(torch.cuda.current_stream())
+            io["in_free"][k] = free
         if self.precision == "fp32":
             _lib.call("sphb_wc_state_to_f32", self.n, self.dim, self.eos.rho0, self.S.data_ptr(),
                       self._c32[self.S.data_ptr()].data_ptr(), _lib.stream_ptr())
         self._state_host = None
         self._refresh_speed()
 
-    def read_state(self, rho_out, mom_out) -> None:
-        """Write (rho, mom) in caller order into host tensors (pinned: async)."""
+    def read_state(self, rho_out, mom_out, *, wait: bool = True):
+        """Write (rho, mom) in caller order into host tensors.
+
+        Pinned host tensors: the state is unpacked on the caller's stream
+        into one of two device staging buffers and copied on a dedicated
+        device-to-host stream.  wait=True (default) orders the caller's
+        stream after that copy (a synchronize of the current stream then
+        sees the data, as before); wait=False leaves it to the caller, so the
+        next steps overlap the copy, and returns the copy's event."""
+        torch = _lib.torch_cuda()
+        if not (rho_out.device.type == "cpu" and rho_out.is_pinned()):
+            _lib.call("sphb_wc_unpack_state", self.n, self.dim, self.order.perm.data_ptr(),
+                      self.S.data_ptr(), self.M.data_ptr(), self._rho_io.data_ptr(),
+                      self._mom_io.data_ptr(), _lib.stream_ptr())
+            rho_out.copy_(self._rho_io, non_blocking=True)
+            mom_out.reshape(self.n, self.dim).copy_(self._mom_io, non_blocking=True)
+            return None
+        io = self._io_streams()
+        k = io["kout"]
+        io["kout"] ^= 1
+        cur = torch.cuda.current_stream()
+        if io["out_free"][k] is not None:           # the slot's previous copy is done
+            cur.wait_event(io["out_free"][k])
         _lib.call("sphb_wc_unpack_state", self.n, self.dim, self.order.perm.data_ptr(),
-                  self.S.data_ptr(), self.M.data_ptr(), self._rho_io.data_ptr(),
-                  self._mom_io.data_ptr(), _lib.stream_ptr())
-        rho_out.copy_(self._rho_io, non_blocking=True)
-        mom_out.reshape(self.n, self.dim).copy_(self._mom_io, non_blocking=True)
+                  self.S.data_ptr(), self.M.data_ptr(), io["rout"][k].data_ptr(),
+                  io["mout"][k].data_ptr(), _lib.stream_ptr())
+        unpacked = torch.cuda.Event()
+        unpacked.record(cur)
+        d2h = io["d2h"]
+        d2h.wait_event(unpacked)
+        with torch.cuda.stream(d2h):
+            rho_out.copy_(io["rout"][k], non_blocking=True)
+            mom_out.reshape(self.n, self.dim).copy_(io["mout"][k], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(d2h)
+        io["out_free"][k] = done
+        io["pending"] = [p for p in io["pending"] if not p[2].query()]
+        for t in (rho_out, mom_out):
+            io["pending"].append((t.data_ptr(), t.data_ptr() + t.numel() * t.element_size(), done))
+        if wait:
+            cur.wait_event(done)
+        return done
+
+    def _io_streams(self):
+        """Copy streams and double-buffered device staging of the pinned-host
+        state transfers (created on first use)."""
+        if self._io is None:
+            torch = _lib.torch_cuda()
+            dev, n, d, f64 = self.S.device, self.n, self.dim, torch.float64
+            self._io = {
+                "h2d": torch.cuda.Stream(device=dev), "d2h": torch.cuda.Stream(device=dev),
+                "rin": [torch.empty(n, dtype=f64, device=dev) for _ in range(2)],
+                "min": [torch.empty((n, d), dtype=f64, device=dev) for _ in range(2)],
+                "rout": [torch.empty(n, dtype=f64, device=dev) for _ in range(2)],
+                "mout": [torch.empty((n, d), dtype=f64, device=dev) for _ in range(2)],
+                "in_free": [None, None], "out_free": [None, None], "pending": [],
+                "kin": 0, "kout": 0}
+        return self._io
 
     def _sync_in(self):
         if self._handed_out and self._state_host is not None:
@@ -1233,6 +1314,12 @@ class _HLLCSolver(EulerianSolver):
         return (float(np.sum(w * st.rho[:self.n_int])),
                 (w[:, None] * st.mom[:self.n_int]).sum(axis=0),
                 float(np.sum(w * st.etot[:self.n_int])))
+
+
+def _overlaps(t, lo: int, hi: int) -> bool:
+    """Does host tensor t's storage intersect [lo, hi)?"""
+    a = t.data_ptr()
+    return a < hi and lo < a + t.numel() * t.element_size()
 
 
 def graph_steps() -> int:

@@ -1082,3 +1082,47 @@ def test_wc_lattice_on_rectangular_periodic_boxes(dims):
         ref.step()
     assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
     assert l2_error(s.state.mom, ref.mom) < 1e-10
+
+
+# ------------------------------------------- state transfers (load/read_state)
+def test_wc_state_transfers_pinned_async():
+    """load_state / read_state with pinned host tensors run on their own copy
+    streams with double-buffered staging: a round trip per step (the same
+    host buffers in and out, so each load waits for the previous read), the
+    overlapped form with distinct buffers and read_state(wait=False), and the
+    plain step() sequence all give identical states."""
+    torch = pytest.importorskip("torch")
+    cfg = configs.c5_tgv3d(kernel="1.6h", n_side=32)
+    a, b, c = make_wc(cfg), make_wc(cfg), make_wc(cfg)
+    n = a.n
+    rho = torch.empty(n, dtype=torch.float64).pin_memory()
+    mom = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    a.read_state(rho, mom)                       # default wait=True
+    torch.cuda.current_stream().synchronize()
+    assert np.array_equal(rho.numpy(), a.state.rho)
+    for _ in range(5):                           # feedback through one host buffer pair
+        a.load_state(rho, mom)
+        a.step()
+        a.read_state(rho, mom)
+    torch.cuda.current_stream().synchronize()
+    for _ in range(5):
+        b.step()
+    assert np.array_equal(rho.numpy(), b.state.rho)
+    assert np.array_equal(mom.numpy(), b.state.mom)
+    # independent one-step problems, overlapped transfers
+    rho_in = torch.from_numpy(cfg["rho"].copy()).pin_memory()
+    mom_in = torch.from_numpy(cfg["mom"].copy()).pin_memory()
+    outs = [(torch.empty(n, dtype=torch.float64).pin_memory(),
+             torch.empty((n, 3), dtype=torch.float64).pin_memory()) for _ in range(3)]
+    evs = []
+    for ro, mo in outs:
+        c.load_state(rho_in, mom_in)
+        c.step()
+        evs.append(c.read_state(ro, mo, wait=False))
+    for ev in evs:
+        ev.synchronize()
+    ref = make_wc(cfg)
+    ref.step()
+    for ro, mo in outs:
+        assert np.array_equal(ro.numpy(), ref.state.rho)
+        assert np.array_equal(mo.numpy(), ref.state.mom)

@@ -457,6 +457,12 @@ int sphb_wc_unpack_state(int64_t n, int32_t dim, const int32_t* perm, const doub
  * cfl_h / (c_add + scalars[2]); then scalars[1] += dt, scalars[2] = 0.
  * WC: c_add = 0 (the speed already includes c; eulerian.py:556-560);
  * TL: c_add = c_s (tlsph.py:178-180). */
+/* Copy `bytes` (a multiple of 4, at most 4096) from device memory into
+ * pinned host memory with a kernel writing through the host mapping, not a
+ * copy engine: small host reads (dt, error word) then never queue behind a
+ * bulk transfer in flight.  SPHB_ERR_ARG if host_dst is not mapped pinned
+ * memory. */
+int sphb_mirror_to_host(const void* src, void* host_dst, int64_t bytes, void* stream);
 int sphb_set_dt(double cfl_h, double c_add, double dt_override, double* scalars,
                 int32_t* err, void* stream);
 

@@ -222,6 +222,7 @@ SIGNATURES = {
     "sphb_tl_deformation_rates_csr": (C.c_int, [I64, I32, P, P, P, P, P, P, P]),
     "sphb_wc_stage": (C.c_int, [P, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P]),
     "sphb_lattice_width": (C.c_int, [I32, I32]),
+    "sphb_mirror_to_host": (C.c_int, [P, P, I64, P]),
     "sphb_tl_kick": (C.c_int, [P, P, P, P, P, P]),
     "sphb_tl_lattice_width": (C.c_int, [I32, I32]),
     "sphb_tl_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),

@@ -45,3 +45,26 @@ extern "C" int sphb_fp64_probe(double* out, int32_t blocks, int32_t threads, int
   SPHB_LAUNCH_CHECK();
   return SPHB_OK;
 }
+
+// Small device -> host reads without the copy engines: one warp stores the
+// words straight into mapped pinned host memory.  A cudaMemcpy of a few
+// bytes would queue behind any bulk transfer in flight on the same copy
+// engine (e.g. a 512 MiB read_state), stalling the host for its duration.
+__global__ void k_mirror_words(const uint32_t* __restrict__ src, volatile uint32_t* dst,
+                               int64_t words) {
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+  __threadfence_system();
+}
+
+extern "C" int sphb_mirror_to_host(const void* src, void* host_dst, int64_t bytes, void* stream) {
+  if (!src || !host_dst || bytes <= 0 || bytes % 4 || bytes > 4096) return SPHB_ERR_ARG;
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
+    cudaGetLastError();                       // not mapped pinned memory: caller falls back
+    return SPHB_ERR_ARG;
+  }
+  k_mirror_words<<<1, 32, 0, (cudaStream_t)stream>>>((const uint32_t*)src, (uint32_t*)dptr,
+                                                     bytes / 4);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}

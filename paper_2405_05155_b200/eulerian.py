@@ -579,23 +579,15 @@ class EulerianSolver:
         torch = _lib.torch_cuda()
         if isinstance(rho, torch.Tensor) and rho.device.type == "cpu" and rho.is_pinned():
             io = self._io_streams()
-            k = io["kin"]
-            io["kin"] ^= 1
+            pre = io["prefetched"]
+            io["prefetched"] = None
+            if pre is not None and pre[0] == (rho.data_ptr(), mom.data_ptr()):
+                k, ready = pre[1], pre[2]           # staged by prefetch_state
+            else:
+                k, ready = self._stage_in(io, rho, mom)
             cur = torch.cuda.current_stream()
-            h2d = io["h2d"]
-            if io["in_free"][k] is None:
-                h2d.wait_stream(cur)
-            else:                                   # the slot's previous pack is done
-                h2d.wait_event(io["in_free"][k])
-            for lo, hi, ev in io["pending"]:        # D2H still writing these host buffers
-                if any(_overlaps(t, lo, hi) for t in (rho, mom)):
-                    h2d.wait_event(ev)
-            with torch.cuda.stream(h2d):
-                rho_d = io["rin"][k].copy_(rho, non_blocking=True)
-                mom_d = io["min"][k].copy_(mom.reshape(self.n, self.dim), non_blocking=True)
-                ready = torch.cuda.Event()
-                ready.record(h2d)
             cur.wait_event(ready)
+            rho_d, mom_d = io["rin"][k], io["min"][k]
         elif isinstance(rho, torch.Tensor) and rho.device.type == "cpu":
             rho_d = self._rho_io.copy_(rho, non_blocking=True)
             mom_d = self._mom_io.copy_(mom.reshape(self.n, self.dim), non_blocking=True)
@@ -616,6 +608,38 @@ class EulerianSolver:
                       self._c32[self.S.data_ptr()].data_ptr(), _lib.stream_ptr())
         self._state_host = None
         self._refresh_speed()
+
+    def prefetch_state(self, rho, mom) -> None:
+        """Start the host-to-device copy of the NEXT load_state(rho, mom) now
+        (pinned host tensors), so it runs while the GPU is still busy with
+        earlier work (e.g. the current step).  The following load_state of
+        the same tensors then only unpacks the staged copy; the host data
+        must not change in between.  Any other load_state drops the
+        prefetch."""
+        io = self._io_streams()
+        k, ready = self._stage_in(io, rho, mom)
+        io["prefetched"] = ((rho.data_ptr(), mom.data_ptr()), k, ready)
+
+    def _stage_in(self, io, rho, mom):
+        """H2D copy of pinned (rho, mom) into the next staging slot on the
+        copy-in stream; returns (slot, ready event)."""
+        torch = _lib.torch_cuda()
+        k = io["kin"]
+        io["kin"] ^= 1
+        h2d = io["h2d"]
+        if io["in_free"][k] is None:
+            h2d.wait_stream(torch.cuda.current_stream())
+        else:                                       # the slot's previous pack is done
+            h2d.wait_event(io["in_free"][k])
+        for lo, hi, ev in io["pending"]:            # D2H still writing these host buffers
+            if any(_overlaps(t, lo, hi) for t in (rho, mom)):
+                h2d.wait_event(ev)
+        with torch.cuda.stream(h2d):
+            io["rin"][k].copy_(rho, non_blocking=True)
+            io["min"][k].copy_(mom.reshape(self.n, self.dim), non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        return k, ready
 
     def read_state(self, rho_out, mom_out, *, wait: bool = True):
         """Write (rho, mom) in caller order into host tensors.
@@ -673,7 +697,7 @@ class EulerianSolver:
                 "rout": [torch.empty(n, dtype=f64, device=dev) for _ in range(2)],
                 "mout": [torch.empty((n, d), dtype=f64, device=dev) for _ in range(2)],
                 "in_free": [None, None], "out_free": [None, None], "pending": [],
-                "kin": 0, "kout": 0}
+                "kin": 0, "kout": 0, "prefetched": None}
         return self._io
 
     def _sync_in(self):
@@ -921,7 +945,7 @@ class EulerianSolver:
             e = self.err.clone()
             self._dist.all_reduce(e, op=self._dist.ReduceOp.MAX)
             return int(e.item())
-        return int(self.err.item())
+        return int(self._read_small(self.err, "err")[0])
 
     def owned(self):
         """(global ids, rho, mom) of the rows this solver updates (slab ranks)."""
@@ -955,10 +979,28 @@ class EulerianSolver:
         dmom = out[:, :self.dim][self.rank].cpu().numpy()
         return drho, dmom, None
 
+    def _read_small(self, dev, name):
+        """A few device words read on the host through a kernel writing into
+        mapped pinned memory (sphb_mirror_to_host), so the read does not wait
+        behind a bulk copy in flight (read_state / prefetch_state)."""
+        torch = _lib.torch_cuda()
+        box = getattr(self, "_mirror", None)
+        if box is None:
+            box = self._mirror = {}
+        h = box.get(name)
+        if h is None:
+            h = box[name] = torch.empty(dev.numel(), dtype=dev.dtype).pin_memory()
+        rc = _lib.lib().sphb_mirror_to_host(dev.data_ptr(), h.data_ptr(),
+                                            dev.numel() * dev.element_size(), _lib.stream_ptr())
+        if rc != 0:                                  # not mapped: a plain copy
+            return dev.cpu()
+        torch.cuda.current_stream().synchronize()
+        return h
+
     def compute_dt(self) -> float:
         """cfl h / max(c + |v|) over the interior (eulerian.py:553-560)."""
         self._sync_in()
-        smax = float(self.scalars[2].item())
+        smax = float(self._read_small(self.scalars, "scalars")[2])
         if smax <= 0.0:
             raise ConfigError("zero maximum wave speed; cannot pick a time step")
         return self._cfl_h / smax

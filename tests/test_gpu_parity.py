@@ -1089,8 +1089,9 @@ def test_wc_state_transfers_pinned_async():
     """load_state / read_state with pinned host tensors run on their own copy
     streams with double-buffered staging: a round trip per step (the same
     host buffers in and out, so each load waits for the previous read), the
-    overlapped form with distinct buffers and read_state(wait=False), and the
-    plain step() sequence all give identical states."""
+    overlapped form with distinct buffers, prefetch_state and
+    read_state(wait=False), and the plain step() sequence all give identical
+    states."""
     torch = pytest.importorskip("torch")
     cfg = configs.c5_tgv3d(kernel="1.6h", n_side=32)
     a, b, c = make_wc(cfg), make_wc(cfg), make_wc(cfg)
@@ -1115,8 +1116,10 @@ def test_wc_state_transfers_pinned_async():
     outs = [(torch.empty(n, dtype=torch.float64).pin_memory(),
              torch.empty((n, 3), dtype=torch.float64).pin_memory()) for _ in range(3)]
     evs = []
+    c.prefetch_state(rho_in, mom_in)
     for ro, mo in outs:
-        c.load_state(rho_in, mom_in)
+        c.load_state(rho_in, mom_in)             # consumes the prefetch
+        c.prefetch_state(rho_in, mom_in)         # the next input, during the step
         c.step()
         evs.append(c.read_state(ro, mo, wait=False))
     for ev in evs:

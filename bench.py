@@ -316,8 +316,9 @@ def c4_leg(torch, steps, warmup, peak):
                                   zip(("rel_l2_displacement", "rel_l2_v", "rel_l2_F"), got,
                                       ref_state)},
                 "after_steps": steps_done,
-                "note": "FP32 companions of the gathered v_half / Q records, FP64 arithmetic "
-                        "and state; reported separately, not the headline"}
+                "note": "FP32 companions of the gathered v_half / Q records, FP32 pair "
+                        "arithmetic flushed to FP64 every 8 slots, FP64 state; reported "
+                        "separately, not the headline"}
             del s32
             torch.cuda.empty_cache()
     out["alpha_T1p6h_over_T2h"] = out["1p6h"]["ms_per_step"] / out["2h"]["ms_per_step"]

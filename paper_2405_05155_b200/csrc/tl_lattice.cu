@@ -250,6 +250,15 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
   return tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, true);
 }
 
+// FP32 copy of the slot table's g (FP32 mode, table geometry): the FP32
+// mode's pair arithmetic runs in FP32 on FP32 records (converting every
+// gathered float to double costs more than the halved bytes save: F2F
+// throughput), partial sums flushed to FP64 every kFlushTL slots.
+struct TabF32 {
+  float g[SPHB_TL_LATTICE_MAXW][3];
+};
+constexpr int kFlushTL = 8;
+
 template <int D, int R2, int MINB, bool F32, bool TAB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
@@ -257,7 +266,8 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
                const double4* __restrict__ Vh, double4* __restrict__ XC,
                double4* __restrict__ F, double4* __restrict__ Q,
-               const double* __restrict__ scalars, int32_t* __restrict__ err) {
+               const double* __restrict__ scalars, int32_t* __restrict__ err,
+               const TabF32 G) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
@@ -283,6 +293,41 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
       wi[a] = 0.0;
 #pragma unroll
       for (int b = 0; b < D; ++b) m[a][b] = 0.0;
+    }
+    if constexpr (F32 && D == 3) {   // FP32 pair arithmetic, FP64 flushes
+      float vf[3], mf[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        vf[a] = (float)vhi[a];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) mf[a][b] = 0.f;
+      }
+      static_for<St::W>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+        const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                          (int64_t)o[2] * row.stride[2];
+        const float4 t4 = __ldg(reinterpret_cast<const float4*>(P.vh32) + j);
+        const float vj[3] = {t4.x, t4.y, t4.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float dv = vj[a] - vf[a];
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            if (o[b] != 0) mf[a][b] = fmaf(dv, G.g[k][b], mf[a][b]);
+        }
+        if constexpr ((k + 1) % kFlushTL == 0 || k + 1 == St::W) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              m[a][b] += (double)mf[a][b];
+              mf[a][b] = 0.f;
+            }
+        }
+      });
+      tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+      return;
     }
     static_for<St::W>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
@@ -345,7 +390,8 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
                const int32_t* __restrict__ cnt, const double4* __restrict__ Q,
                const double4* __restrict__ Vh, double4* __restrict__ A,
-               double4* __restrict__ V, double* __restrict__ scalars, int update_v) {
+               double4* __restrict__ V, double* __restrict__ scalars, int update_v,
+               const TabF32 G) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
@@ -368,6 +414,32 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
     double acc[D], gsum[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) acc[a] = gsum[a] = 0.0;
+    if constexpr (F32 && D == 3) {   // FP32 pair arithmetic, FP64 flushes
+      float af[3] = {0.f, 0.f, 0.f};
+      const float4* q32 = reinterpret_cast<const float4*>(P.q32);
+      static_for<St::W>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+        const int64_t j = i + (int64_t)o[0] + (int64_t)o[1] * row.stride[1] +
+                          (int64_t)o[2] * row.stride[2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (o[c] != 0) {
+            const float4 t4 = __ldg(q32 + c * qs + j);
+            af[0] = fmaf(t4.x, G.g[k][c], af[0]);
+            af[1] = fmaf(t4.y, G.g[k][c], af[1]);
+            af[2] = fmaf(t4.z, G.g[k][c], af[2]);
+          }
+        if constexpr ((k + 1) % kFlushTL == 0 || k + 1 == St::W) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            acc[a] += (double)af[a];
+            af[a] = 0.f;
+          }
+        }
+      });
+      speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, false);
+    } else {
     static_for<St::W>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
       constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
@@ -401,6 +473,7 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
           if (o[b] != 0) acc[a] = fma(Qj[a][b], L.g[k][b], acc[a]);
     });
     speed = tl_b_finish<D>(P, i, fixed_i, acc, gsum, Q, Vh, A, V, scalars, update_v, false);
+    }
   } else if (t < L.n_interior) {
     const Row<D, R> row(L, t);
     const int64_t i = row.i;
@@ -613,11 +686,14 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   const bool f32 = p->vh32 && p->q32;
   const bool tab = L->table != 0;
   const int minb = minb_env ? minb_env : (tab ? 5 : 4);
+  TabF32 G;
+  for (int k = 0; k < L->width; ++k)
+    for (int c = 0; c < 3; ++c) G.g[k][c] = (float)L->g[k][c];
   const unsigned grid = lattice_grid(L);
 #define SPHB_A2(D, R, MB, F, T)                                                             \
   k_tl_lattice_a<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,          \
       (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
-      (double4*)q, scalars, err)
+      (double4*)q, scalars, err, G)
 #define SPHB_A1(D, R, MB)                                                                   \
   if (f32) {                                                                                \
     if (tab) SPHB_A2(D, R, MB, true, true); else SPHB_A2(D, R, MB, true, false);            \
@@ -657,10 +733,13 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   const bool f32 = p->vh32 && p->q32;
   const bool tab = L->table != 0;
   const unsigned grid = lattice_grid(L);
+  TabF32 G;
+  for (int k = 0; k < L->width; ++k)
+    for (int c = 0; c < 3; ++c) G.g[k][c] = (float)L->g[k][c];
 #define SPHB_B2(D, R, MB, F, T)                                                             \
   k_tl_lattice_b<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,     \
       cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,        \
-      (int)update_v)
+      (int)update_v, G)
 #define SPHB_B1(D, R, MB)                                                                   \
   if (f32) {                                                                                \
     if (tab) SPHB_B2(D, R, MB, true, true); else SPHB_B2(D, R, MB, true, false);            \

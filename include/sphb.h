@@ -575,10 +575,15 @@ typedef struct sphb_tl_lattice {
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
   int32_t table;         /* 1: table geometry (dx, g); 0: exact separable   */
   int64_t n_interior;    /* prod(n_a - 2R) over the dim axes                */
-  /* the remaining (shell) rows, run in the same launches with the general
-   * per-pair geometry and the pass list (nbr, cnt) */
+  /* the remaining (shell) rows, run in the same launches (blocks before the
+   * interior ones) with the general per-pair geometry and the pass list */
   const int32_t* shell;
   int64_t n_shell;
+  /* optional compact pass list of the shell rows: shell_nbr[k * n_shell + s]
+   * = nbr[k * n + shell[s]], shell_cnt[s] = cnt[shell[s]] (NULL: read the
+   * full list (nbr, cnt)) */
+  const int32_t* shell_nbr;
+  const int32_t* shell_cnt;
   double r2k[SPHB_TL_LATTICE_MAXW];
   double f[SPHB_TL_LATTICE_MAXW], df[SPHB_TL_LATTICE_MAXW];
   double dx[SPHB_TL_LATTICE_MAXW][3];   /* table geometry (table = 1)       */

@@ -184,6 +184,8 @@ class TLLattice(C.Structure):
         ("n_interior", C.c_int64),
         ("shell", C.c_void_p),
         ("n_shell", C.c_int64),
+        ("shell_nbr", C.c_void_p),
+        ("shell_cnt", C.c_void_p),
         ("r2k", C.c_double * TL_LATTICE_MAXW),
         ("f", C.c_double * TL_LATTICE_MAXW),
         ("df", C.c_double * TL_LATTICE_MAXW),

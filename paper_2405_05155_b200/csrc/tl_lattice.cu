@@ -148,14 +148,43 @@ __device__ __forceinline__ void gather_qcol(const sphb_tl_params& P, const doubl
   }
 }
 
+// Pass-list view of shell row ts: the compact shell list (column-major over
+// the shell rows, so consecutive threads read consecutive entries) when the
+// host built it, else the row of the full pass list.  Shell blocks come
+// first in the grid, so their longer rows start early instead of forming
+// the launch's tail.
+struct ShellRow {
+  int64_t i;
+  const int32_t* nb;
+  int64_t ns;
+  int32_t cn;
+  __device__ __forceinline__ ShellRow(const sphb_tl_lattice& L, int64_t ts, int64_t n,
+                                      const int32_t* __restrict__ nbr,
+                                      const int32_t* __restrict__ cnt) {
+    i = L.shell[ts];
+    if (L.shell_nbr) {
+      nb = L.shell_nbr + ts;
+      ns = L.n_shell;
+      cn = L.shell_cnt[ts];
+    } else {
+      nb = nbr + i;
+      ns = n;
+      cn = cnt[i];
+    }
+  }
+};
+
+__host__ __device__ __forceinline__ int64_t shell_blocks(const sphb_tl_lattice& L) {
+  return (L.n_shell + kTT - 1) / kTT;
+}
+
 // Shell row of pass A: the general pair loop (tl_engine.cu k_tl_pass_a,
 // unstaged) — pass list, X0_j gather, g0 recomputed (ref_gradient).
 template <int D, bool F32>
 __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
                                         const double4* __restrict__ X0,
                                         const double4* __restrict__ B0,
-                                        const int32_t* __restrict__ nbr,
-                                        const int32_t* __restrict__ cnt,
+                                        const ShellRow& sr,
                                         const double4* __restrict__ Vh, double4* __restrict__ XC,
                                         double4* __restrict__ F, double4* __restrict__ Q,
                                         double dt, int32_t* __restrict__ err) {
@@ -171,9 +200,8 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int b = 0; b < D; ++b) m[a][b] = 0.0;
-  const int32_t cn = cnt[i];
-  for (int32_t k = 0; k < cn; ++k) {
-    int64_t j = nbr[(int64_t)k * n + i];
+  for (int32_t k = 0; k < sr.cn; ++k) {
+    int64_t j = sr.nb[(int64_t)k * sr.ns];
     SPHB_CHECK_INDEX(j, n, err);
     double vhj[D], wj[D], dx[D], g[D];
     bool fixed_j;
@@ -196,8 +224,7 @@ __device__ __forceinline__ void shell_a(const sphb_tl_params& P, int64_t i,
 template <int D, bool F32, bool X0J>
 __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
                                           const double4* __restrict__ X0,
-                                          const int32_t* __restrict__ nbr,
-                                          const int32_t* __restrict__ cnt,
+                                          const ShellRow& sr,
                                           const double4* __restrict__ Q,
                                           const double4* __restrict__ Vh,
                                           double4* __restrict__ A, double4* __restrict__ V,
@@ -212,9 +239,8 @@ __device__ __forceinline__ double shell_b(const sphb_tl_params& P, int64_t i,
   double gsum[D], acc[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) gsum[a] = acc[a] = 0.0;
-  const int32_t cn = cnt[i];
-  for (int32_t k = 0; k < cn; ++k) {
-    const int64_t j = nbr[(int64_t)k * n + i];
+  for (int32_t k = 0; k < sr.cn; ++k) {
+    const int64_t j = sr.nb[(int64_t)k * sr.ns];
     double Qj[D][D], wj[D];
     if constexpr (D == 3) {
 #pragma unroll
@@ -259,6 +285,12 @@ struct TabF32 {
 };
 constexpr int kFlushTL = 8;
 
+// L2 prefetch of a row's streamed pass-A records (B0, F, XC), issued before
+// the gathers so their DRAM latency overlaps the pair loop
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int D, int R2, int MINB, bool F32, bool TAB>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
@@ -270,14 +302,16 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const TabF32 G) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
-  const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
-  if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
-    const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
-    if (ts < L.n_shell) shell_a<D, F32>(P, (int64_t)L.shell[ts], X0, B0, nbr, cnt, Vh, XC, F, Q,
-                                        scalars[0], err);
+  const int64_t nb_sh = shell_blocks(L);
+  if ((int64_t)blockIdx.x < nb_sh) {       // shell rows: general per-pair geometry
+    const int64_t ts = (int64_t)blockIdx.x * kTT + threadIdx.x;
+    if (ts < L.n_shell) {
+      const ShellRow sr(L, ts, P.n, nbr, cnt);
+      shell_a<D, F32>(P, sr.i, X0, B0, sr, Vh, XC, F, Q, scalars[0], err);
+    }
     return;
   }
-  const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
+  const int64_t t = ((int64_t)blockIdx.x - nb_sh) * kTT + threadIdx.x;
   if (t >= L.n_interior) return;
   const Row<D, R> row(L, t);
   const int64_t i = row.i;
@@ -286,6 +320,15 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
   if constexpr (TAB) {
     // table geometry: g0 per slot, no X0 record; the Q padding (X0 for the
     // shell rows' general pass B) is not needed: they read X0 themselves
+    if constexpr (!F32 && D == 3) {
+      const int64_t n = P.n;
+      prefetch_l2(B0 + i);
+      prefetch_l2(reinterpret_cast<const double2*>(B0 + n) + i);
+      prefetch_l2(F + i);
+      prefetch_l2(F + n + i);
+      prefetch_l2(reinterpret_cast<const double*>(F + 2 * n) + i);
+      prefetch_l2(XC + i);
+    }
     load_vec<D>(Vh, i, vhi);
     double m[D][D];
 #pragma unroll
@@ -394,14 +437,15 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
                const TabF32 G) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
-  const int64_t nb_in = (L.n_interior + kTT - 1) / kTT;
-  const int64_t t = (int64_t)blockIdx.x * kTT + threadIdx.x;
+  const int64_t nb_sh = shell_blocks(L);
+  const int64_t t = ((int64_t)blockIdx.x - nb_sh) * kTT + threadIdx.x;
   double speed = 0.0;
-  if ((int64_t)blockIdx.x >= nb_in) {      // shell rows: general per-pair geometry
-    const int64_t ts = ((int64_t)blockIdx.x - nb_in) * kTT + threadIdx.x;
-    if (ts < L.n_shell)
-      speed = shell_b<D, F32, F32 || TAB>(P, (int64_t)L.shell[ts], X0, nbr, cnt, Q, Vh, A, V,
-                                          scalars, update_v);
+  if ((int64_t)blockIdx.x < nb_sh) {       // shell rows: general per-pair geometry
+    const int64_t ts = (int64_t)blockIdx.x * kTT + threadIdx.x;
+    if (ts < L.n_shell) {
+      const ShellRow sr(L, ts, P.n, nbr, cnt);
+      speed = shell_b<D, F32, F32 || TAB>(P, sr.i, X0, sr, Q, Vh, A, V, scalars, update_v);
+    }
   } else if (TAB && t < L.n_interior) {
     // table geometry: acc = sum_k Q_j g[k]; sum_k g[k] = 0 exactly (the
     // table is antisymmetric), so the Q_i sum_j g0 term and Q_i vanish.
@@ -534,6 +578,160 @@ k_tl_lattice_b(const sphb_tl_params P, const sphb_tl_lattice L,
   tl_block_speed_max<kTT>(speed, scalars);
 }
 
+// ---------------------------------------------------------------------------
+// z-blocked table-geometry pass B (3D, FP64).  A thread owns PZ consecutive
+// interior rows along the slow axis (a pencil (a, b, c0..c0+PZ-1)); the lanes
+// of a warp stay consecutive along the fast axis, so every gather is still
+// coalesced.  The neighbour records are walked plane by plane (zq = c0 - R ..
+// c0 + PZ - 1 + R) and, inside a plane, pencil by pencil ((dy, dx)
+// ascending); one gathered record serves every owned row it neighbours
+// (up to 2R + 1 of them), so the gathers per row drop from W to about
+// (PZ + 2R) (2R + 1)^2 / PZ.  Each row still accumulates its slots in the
+// canonical order (z, then y, then x ascending): the results are bitwise
+// those of the one-row kernel above.  C4 1.6h: pass B 159 -> 141 us (the Q
+// column gathers were bound by L1 wavefronts).  The same blocking of pass A
+// (PZ = 2, 4, 8) measured slower than its one-row kernel: pass A streams
+// 360 B of its own records per row and lost more memory-level parallelism
+// than its L1-resident Vh gathers saved (profiles/r02_tune_tl_zb.md).
+
+// slot of offset (x, y, z) in the canonical order, -1 outside the stencil
+template <int D, int R2>
+constexpr int slot_of(int x, int y, int z) {
+  using St = Stencil<D, R2>;
+  for (int k = 0; k < St::W; ++k)
+    if (St::L.o[k][0] == x && St::L.o[k][1] == y && St::L.o[k][2] == z) return k;
+  return -1;
+}
+
+// columns (bit c: o_c != 0) some owned row takes from the record at
+// (dx, dy, qrel) relative to the pencil's first row
+template <int R2, int PZ>
+constexpr int zb_mask(int qrel, int dx, int dy) {
+  constexpr int R = isqrt_c(R2);
+  int m = 0;
+  for (int p = 0; p < PZ; ++p) {
+    const int dz = qrel - p;
+    if (dz < -R || dz > R || slot_of<3, R2>(dx, dy, dz) < 0) continue;
+    m |= (dx != 0 ? 1 : 0) | (dy != 0 ? 2 : 0) | (dz != 0 ? 4 : 0);
+  }
+  return m;
+}
+
+// Pencil of thread t: first row i0 and the number of owned rows pc (<= PZ)
+template <int R, int PZ>
+struct Pencil {
+  int64_t i0;
+  int64_t s1, s2;
+  int pc;
+  __device__ __forceinline__ Pencil(const sphb_tl_lattice& L, int64_t t) {
+    const int m0 = L.n[0] - 2 * R, m1 = L.n[1] - 2 * R, m2 = L.n[2] - 2 * R;
+    const int a = R + (int)(t % m0);
+    const int64_t u = t / m0;
+    const int b = R + (int)(u % m1);
+    const int c0 = R + (int)(u / m1) * PZ;
+    pc = min(PZ, m2 + R - c0);
+    s1 = L.n[0];
+    s2 = (int64_t)L.n[0] * L.n[1];
+    i0 = (int64_t)a + s1 * b + s2 * c0;
+  }
+};
+
+__host__ __device__ __forceinline__ int64_t zb_threads(const sphb_tl_lattice& L, int R, int PZ) {
+  const int64_t m0 = L.n[0] - 2 * R, m1 = L.n[1] - 2 * R, m2 = L.n[2] - 2 * R;
+  return m0 * m1 * ((m2 + PZ - 1) / PZ);
+}
+
+// visit every (plane, pencil) record of the block in the order above:
+// f(qrel, dx, dy, plane offset) with compile-time constants, only where
+// zb_mask != 0.  Planes past the lattice (short last pencil, pc < PZ) are
+// skipped.  The per-plane branch also keeps the compiler from hoisting the
+// gathers of all planes ahead of the FMAs (measured: a branch-free walk
+// with clamped planes ran pass B at 0.363 instead of 0.333 ms per C4 step).
+template <int R2, int PZ, class F>
+__device__ __forceinline__ void zb_walk(int pc, int64_t s2, F&& f) {
+  constexpr int R = isqrt_c(R2);
+  constexpr int S = 2 * R + 1;
+  static_for<PZ + 2 * R>([&](auto qc) {
+    constexpr int qrel = decltype(qc)::value - R;
+    if (qrel <= pc - 1 + R) {        // plane inside the lattice
+      const int64_t qoff = (int64_t)qrel * s2;
+      static_for<S * S>([&](auto ec) {
+        constexpr int dy = decltype(ec)::value / S - R;
+        constexpr int dx = decltype(ec)::value % S - R;
+        if constexpr (zb_mask<R2, PZ>(qrel, dx, dy) != 0)
+          f(std::integral_constant<int, qrel>{}, std::integral_constant<int, dx>{},
+            std::integral_constant<int, dy>{}, qoff);
+      });
+    }
+  });
+}
+
+template <int R2, int PZ, int MINB>
+__global__ void __launch_bounds__(kTT, MINB)
+k_tl_zb_b(const sphb_tl_params P, const sphb_tl_lattice L,
+          const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
+          const int32_t* __restrict__ cnt, const double4* __restrict__ Q,
+          const double4* __restrict__ Vh, double4* __restrict__ A,
+          double4* __restrict__ V, double* __restrict__ scalars, int update_v) {
+  constexpr int R = isqrt_c(R2);
+  const int64_t n_th = zb_threads(L, R, PZ);
+  const int64_t nb_sh = shell_blocks(L);
+  const int64_t t = ((int64_t)blockIdx.x - nb_sh) * kTT + threadIdx.x;
+  double speed = 0.0;
+  if ((int64_t)blockIdx.x < nb_sh) {       // shell rows: general per-pair geometry
+    const int64_t ts = (int64_t)blockIdx.x * kTT + threadIdx.x;
+    if (ts < L.n_shell) {
+      const ShellRow sr(L, ts, P.n, nbr, cnt);
+      speed = shell_b<3, false, true>(P, sr.i, X0, sr, Q, Vh, A, V, scalars, update_v);
+    }
+  } else if (t < n_th) {
+    // acc = sum_k Q_j g[k]; sum_k g[k] = 0 exactly (antisymmetric table)
+    const Pencil<R, PZ> pen(L, t);
+    const int64_t n = P.n;
+    double acc[PZ][3];
+#pragma unroll
+    for (int p = 0; p < PZ; ++p) acc[p][0] = acc[p][1] = acc[p][2] = 0.0;
+    zb_walk<R2, PZ>(pen.pc, pen.s2, [&](auto qc, auto xc, auto yc, int64_t qoff) {
+      constexpr int qrel = decltype(qc)::value, dx = decltype(xc)::value, dy = decltype(yc)::value;
+      constexpr int mask = zb_mask<R2, PZ>(qrel, dx, dy);
+      const int64_t j = pen.i0 + dx + dy * pen.s1 + qoff;
+      double Qj[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (mask & (1 << c))
+          gather_qcol_dense(Q, n, c, j, Qj[0][c], Qj[1][c], Qj[2][c]);
+        else
+          Qj[0][c] = Qj[1][c] = Qj[2][c] = 0.0;
+      }
+      static_for<PZ>([&](auto pcst) {
+        constexpr int p = decltype(pcst)::value;
+        constexpr int dz = qrel - p;
+        constexpr int k = (dz < -R || dz > R) ? -1 : slot_of<3, R2>(dx, dy, dz);
+        if constexpr (k >= 0) {
+          constexpr int o[3] = {dx, dy, dz};
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+              if (o[b] != 0) acc[p][a] = fma(Qj[a][b], L.g[k][b], acc[p][a]);
+        }
+      });
+    });
+    const double gsum[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int p = 0; p < PZ; ++p)
+      if (p < pen.pc) {
+        const int64_t i = pen.i0 + p * pen.s2;
+        // clamp flag: Vh.w (written by the kick) or, for accelerations() alone, X0.w
+        const bool fixed_i = update_v ? Vh[i].w != 0.0 : X0[i].w != 0.0;
+        const double s = tl_b_finish<3>(P, i, fixed_i, acc[p], gsum, Q, Vh, A, V, scalars,
+                                        update_v, false);
+        speed = (s > speed || s != s) ? s : speed;     // NaN propagates to the dt check
+      }
+  }
+  tl_block_speed_max<kTT>(speed, scalars);
+}
+
 // Proof of the specialisation for every interior row (see the file header).
 template <int D, int R2>
 __global__ void k_tl_lattice_check(const sphb_tl_params P, const sphb_tl_lattice L,
@@ -660,13 +858,19 @@ extern "C" int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_latt
   return SPHB_ERR_ARG;
 }
 
+// z-blocked pass B: rows per thread (SPHB_TL_PZ_B; 1 = the one-row kernel)
+// and occupancy target (SPHB_TL_ZMINB_B), instantiated as (R2, PZ, MINB);
+// defaults from scripts/ab_tl.sh (profiles/r02_tune_tl_zb.md)
+constexpr int kPzB = 8, kZMinbB = 3;
+#define SPHB_ZB_CASES(X) X(3, 8, 3) X(3, 8, 4) X(5, 8, 3) X(5, 8, 4)
+
 // occupancy targets (128-thread blocks per SM; SPHB_TLAT_MINB_A / _B override)
 static int tl_minb(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
 
-// blocks: the interior rows, then the shell rows
+// blocks: the shell rows, then the interior rows
 static unsigned lattice_grid(const sphb_tl_lattice* L) {
   return (unsigned)((L->n_interior + kTT - 1) / kTT + (L->n_shell + kTT - 1) / kTT);
 }
@@ -732,6 +936,26 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   static const int minb = tl_minb("SPHB_TLAT_MINB_B", 5);   // 96 registers (r02_ncu_c4.md)
   const bool f32 = p->vh32 && p->q32;
   const bool tab = L->table != 0;
+  if (tab && !f32 && p->dim == 3) {   // z-blocked table-geometry pass (FP64)
+    static const int pz = tl_minb("SPHB_TL_PZ_B", kPzB);
+    static const int zminb = tl_minb("SPHB_TL_ZMINB_B", kZMinbB);
+    if (pz > 1) {
+      const int R = isqrt_c(L->r2);
+      const unsigned zgrid = (unsigned)((zb_threads(*L, R, pz) + kTT - 1) / kTT +
+                                        (L->n_shell + kTT - 1) / kTT);
+#define SPHB_ZB(R2, PZ, MB)                                                                 \
+  if (L->r2 == R2 && pz == PZ && zminb == MB) {                                             \
+    k_tl_zb_b<R2, PZ, MB><<<zgrid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr, cnt,      \
+        (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,           \
+        (int)update_v);                                                                     \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+      SPHB_ZB_CASES(SPHB_ZB)
+#undef SPHB_ZB
+      return SPHB_ERR_ARG;
+    }
+  }
   const unsigned grid = lattice_grid(L);
   TabF32 G;
   for (int k = 0; k < L->width; ++k)

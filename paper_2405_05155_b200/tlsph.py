@@ -468,6 +468,12 @@ class SolidSystem:
             inner &= (coord[a] >= R) & (coord[a] < ext[a] - R)
         self._shell = torch.nonzero(~inner).flatten().to(torch.int32).contiguous()
         L.shell, L.n_shell = self._shell.data_ptr(), int(self._shell.numel())
+        # compact shell pass list, column-major over the shell rows (coalesced
+        # reads; the full list's shell rows are scattered over its columns)
+        sh = self._shell.long()
+        self._shell_nbr = self.nbr.view(-1, n)[:, sh].contiguous()
+        self._shell_cnt = self.cnt[sh].contiguous()
+        L.shell_nbr, L.shell_cnt = self._shell_nbr.data_ptr(), self._shell_cnt.data_ptr()
         # table geometry (default; SPHB_TL_TABLE=0 keeps the exact separable
         # geometry): every interior pair within 1e-12 dp of its slot's dx,
         # else the exact mode's proof (bitwise separability, r2 near r2k)

@@ -666,13 +666,14 @@ __device__ __forceinline__ void zb_walk(int pc, int64_t s2, F&& f) {
   });
 }
 
-template <int R2, int PZ, int MINB>
+template <int R2, int PZ, int MINB, bool F32>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_zb_b(const sphb_tl_params P, const sphb_tl_lattice L,
           const double4* __restrict__ X0, const int32_t* __restrict__ nbr,
           const int32_t* __restrict__ cnt, const double4* __restrict__ Q,
           const double4* __restrict__ Vh, double4* __restrict__ A,
-          double4* __restrict__ V, double* __restrict__ scalars, int update_v) {
+          double4* __restrict__ V, double* __restrict__ scalars, int update_v,
+          const TabF32 G) {
   constexpr int R = isqrt_c(R2);
   const int64_t n_th = zb_threads(L, R, PZ);
   const int64_t nb_sh = shell_blocks(L);
@@ -682,7 +683,7 @@ k_tl_zb_b(const sphb_tl_params P, const sphb_tl_lattice L,
     const int64_t ts = (int64_t)blockIdx.x * kTT + threadIdx.x;
     if (ts < L.n_shell) {
       const ShellRow sr(L, ts, P.n, nbr, cnt);
-      speed = shell_b<3, false, true>(P, sr.i, X0, sr, Q, Vh, A, V, scalars, update_v);
+      speed = shell_b<3, F32, true>(P, sr.i, X0, sr, Q, Vh, A, V, scalars, update_v);
     }
   } else if (t < n_th) {
     // acc = sum_k Q_j g[k]; sum_k g[k] = 0 exactly (antisymmetric table)
@@ -691,6 +692,49 @@ k_tl_zb_b(const sphb_tl_params P, const sphb_tl_lattice L,
     double acc[PZ][3];
 #pragma unroll
     for (int p = 0; p < PZ; ++p) acc[p][0] = acc[p][1] = acc[p][2] = 0.0;
+    if constexpr (F32) {
+      // FP32 mode: FP32 column records, FP32 pair arithmetic, partial sums
+      // flushed to FP64 after every kFlushTL-th slot of each row (the same
+      // flush points as the one-row kernel: each row's slots still arrive
+      // in canonical order)
+      using St = Stencil<3, R2>;
+      const int64_t qs = P.q_stride ? P.q_stride : n;
+      const float4* q32 = reinterpret_cast<const float4*>(P.q32);
+      float af[PZ][3];
+#pragma unroll
+      for (int p = 0; p < PZ; ++p) af[p][0] = af[p][1] = af[p][2] = 0.f;
+      zb_walk<R2, PZ>(pen.pc, pen.s2, [&](auto qc, auto xc, auto yc, int64_t qoff) {
+        constexpr int qrel = decltype(qc)::value, dx = decltype(xc)::value, dy = decltype(yc)::value;
+        constexpr int mask = zb_mask<R2, PZ>(qrel, dx, dy);
+        const int64_t j = pen.i0 + dx + dy * pen.s1 + qoff;
+        float4 qf[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          qf[c] = (mask & (1 << c)) ? __ldg(q32 + c * qs + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        static_for<PZ>([&](auto pcst) {
+          constexpr int p = decltype(pcst)::value;
+          constexpr int dz = qrel - p;
+          constexpr int k = (dz < -R || dz > R) ? -1 : slot_of<3, R2>(dx, dy, dz);
+          if constexpr (k >= 0) {
+            constexpr int o[3] = {dx, dy, dz};
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (o[c] != 0) {
+                af[p][0] = fmaf(qf[c].x, G.g[k][c], af[p][0]);
+                af[p][1] = fmaf(qf[c].y, G.g[k][c], af[p][1]);
+                af[p][2] = fmaf(qf[c].z, G.g[k][c], af[p][2]);
+              }
+            if constexpr ((k + 1) % kFlushTL == 0 || k + 1 == St::W) {
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                acc[p][a] += (double)af[p][a];
+                af[p][a] = 0.f;
+              }
+            }
+          }
+        });
+      });
+    } else {
     zb_walk<R2, PZ>(pen.pc, pen.s2, [&](auto qc, auto xc, auto yc, int64_t qoff) {
       constexpr int qrel = decltype(qc)::value, dx = decltype(xc)::value, dy = decltype(yc)::value;
       constexpr int mask = zb_mask<R2, PZ>(qrel, dx, dy);
@@ -717,6 +761,7 @@ k_tl_zb_b(const sphb_tl_params P, const sphb_tl_lattice L,
         }
       });
     });
+    }
     const double gsum[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int p = 0; p < PZ; ++p)
@@ -861,7 +906,7 @@ extern "C" int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_latt
 // z-blocked pass B: rows per thread (SPHB_TL_PZ_B; 1 = the one-row kernel)
 // and occupancy target (SPHB_TL_ZMINB_B), instantiated as (R2, PZ, MINB);
 // defaults from scripts/ab_tl.sh (profiles/r02_tune_tl_zb.md)
-constexpr int kPzB = 8, kZMinbB = 3;
+constexpr int kPzB = 8, kZMinbB = 3, kZMinbB32 = 4;   // FP64 / FP32 mode
 #define SPHB_ZB_CASES(X) X(3, 8, 3) X(3, 8, 4) X(5, 8, 3) X(5, 8, 4)
 
 // occupancy targets (128-thread blocks per SM; SPHB_TLAT_MINB_A / _B override)
@@ -936,18 +981,27 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
   static const int minb = tl_minb("SPHB_TLAT_MINB_B", 5);   // 96 registers (r02_ncu_c4.md)
   const bool f32 = p->vh32 && p->q32;
   const bool tab = L->table != 0;
-  if (tab && !f32 && p->dim == 3) {   // z-blocked table-geometry pass (FP64)
+  TabF32 G;
+  for (int k = 0; k < L->width; ++k)
+    for (int c = 0; c < 3; ++c) G.g[k][c] = (float)L->g[k][c];
+  if (tab && p->dim == 3) {   // z-blocked table-geometry pass (FP64 or FP32 mode)
     static const int pz = tl_minb("SPHB_TL_PZ_B", kPzB);
-    static const int zminb = tl_minb("SPHB_TL_ZMINB_B", kZMinbB);
+    static const int zminb_env = tl_minb("SPHB_TL_ZMINB_B", 0);
+    const int zminb = zminb_env ? zminb_env : (f32 ? kZMinbB32 : kZMinbB);
     if (pz > 1) {
       const int R = isqrt_c(L->r2);
       const unsigned zgrid = (unsigned)((zb_threads(*L, R, pz) + kTT - 1) / kTT +
                                         (L->n_shell + kTT - 1) / kTT);
 #define SPHB_ZB(R2, PZ, MB)                                                                 \
   if (L->r2 == R2 && pz == PZ && zminb == MB) {                                             \
-    k_tl_zb_b<R2, PZ, MB><<<zgrid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr, cnt,      \
-        (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,           \
-        (int)update_v);                                                                     \
+    if (f32)                                                                                \
+      k_tl_zb_b<R2, PZ, MB, true><<<zgrid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,   \
+          cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,    \
+          (int)update_v, G);                                                                \
+    else                                                                                    \
+      k_tl_zb_b<R2, PZ, MB, false><<<zgrid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,  \
+          cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,    \
+          (int)update_v, G);                                                                \
     SPHB_LAUNCH_CHECK();                                                                    \
     return SPHB_OK;                                                                         \
   }
@@ -957,9 +1011,6 @@ extern "C" int sphb_tl_pass_b_lattice(const sphb_tl_params* p, const sphb_tl_lat
     }
   }
   const unsigned grid = lattice_grid(L);
-  TabF32 G;
-  for (int k = 0; k < L->width; ++k)
-    for (int c = 0; c < 3; ++c) G.g[k][c] = (float)L->g[k][c];
 #define SPHB_B2(D, R, MB, F, T)                                                             \
   k_tl_lattice_b<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, nbr,     \
       cnt, (const double4*)q, (const double4*)vh, (double4*)a, (double4*)v, scalars,        \

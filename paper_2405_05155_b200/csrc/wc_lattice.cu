@@ -102,12 +102,16 @@ __device__ __forceinline__ int wrapc(int c, int s, int n) {
   return v;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int D, int R2, int MINB, int NT = kLT>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
              const double4* Sn, const double4* Mn, double4* S_out, double4* M_out,
-             double* __restrict__ scalars, int32_t* __restrict__ err) {
+             double* __restrict__ scalars, int32_t* __restrict__ err, const int64_t pf) {
   using St = Stencil<D, R2>;
   constexpr int R = St::R;
   const int64_t n = P.n;
@@ -115,6 +119,18 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
   const bool own = i0 < P.row0 + P.nrows;
   // tail lanes redo the last row (no divergence in the pair loop), no write
   const int64_t i = own ? i0 : P.row0 + P.nrows - 1;
+  // L2 prefetch of the records of row i + pf (pf = the stencil's reach
+  // ahead in rows + one wave of resident threads): the leading-edge
+  // neighbour gathers of the thread one wave later, and that row's own
+  // S / B / S_n / M_n, then come from L2 instead of DRAM
+  if (pf > 0 && i0 + pf < n) {
+    const int64_t ip = i0 + pf;
+    prefetch_l2(S_in + ip);
+    prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
+    prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
+    if (stage > 0 && Sn != S_in) prefetch_l2(Sn + ip);
+    if (stage > 0) prefetch_l2(Mn + ip);
+  }
 
   // lattice coordinates and the wrapped neighbour components of this row
   const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
@@ -619,11 +635,25 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   // (one block, 8 warps per SM) measured fastest (13.35 -> 11.96 ms/step,
   // profiles/r02_tune_lattice.md)
   const int nt = nt_env ? nt_env : (p->dim == 3 && L->r2 == 6 && !minb_env ? 256 : 0);
+  // L2 prefetch distance in rows (3D): the stencil's reach in planes + the
+  // resident threads of one wave; SPHB_LAT_PF overrides (0 = off)
+  static const int64_t pf_env = [] {
+    const char* e = getenv("SPHB_LAT_PF");
+    return e ? (int64_t)atoll(e) : (int64_t)-1;
+  }();
+  int64_t pf = 0;
+  if (p->dim == 3) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
+    pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
+  }
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);
 #define SPHB_NT(R, MB, NT)                                                                 \
     k_wc_lattice<3, R, MB, NT><<<g2, NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
-                                                  Mout, scalars, err)
+                                                  Mout, scalars, err, pf)
     const bool r4 = L->r2 == 4;
     if (nt == 64) {
       if (r4) SPHB_NT(4, 3, 64); else SPHB_NT(6, 2, 64);
@@ -647,7 +677,7 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   }
 #define SPHB_S1(D, R, MB)                                                              \
   k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
-                                               Mout, scalars, err);                     \
+                                               Mout, scalars, err, pf);                 \
   break
   SPHB_LAT_CASES(SPHB_S)
 #undef SPHB_S

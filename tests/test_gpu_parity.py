@@ -1055,6 +1055,47 @@ def test_tl_fp32_mode_error_is_small(label, builder, kwargs):
         assert l2_error(a, b) < 1e-5
 
 
+_ZB_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2405_05155_b200 import configs
+from paper_2405_05155_b200.tlsph import Material, SolidSystem
+out = {}
+for kern in ("1.6h", "2h"):
+    for prec in ("fp64", "fp32"):
+        cfg = configs.c4_column(n_width=10, kernel=kern)
+        m = cfg["material"]
+        s = SolidSystem(cfg["X0"], Material(m.rho0, m.E, m.nu), cfg["spec"], cfg["dp"],
+                        fixed=cfg["fixed"], cfl=cfg["cfl"], precision=prec)
+        assert s.lattice is not None
+        s.v = cfg["v0"].copy()
+        s.advance(12)
+        for name, a in (("x", s.x), ("v", s.v), ("F", s.F)):
+            out[kern + prec + name] = np.asarray(a)
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_tl_zblocked_pass_b_is_bitwise_the_one_row_kernel(tmp_path):
+    """The z-blocked lattice pass B (PZ rows per thread, csrc/tl_lattice.cu
+    k_tl_zb_b) accumulates every row's slots in the canonical order, so its
+    states equal the one-row kernel's bit for bit (FP64 and FP32 mode, 1.6h
+    and 2h); SPHB_TL_PZ_B is read once per process, hence the subprocesses."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    files = {}
+    for pz in ("8", "1"):
+        f = str(tmp_path / f"pz{pz}.npz")
+        env = dict(os.environ, SPHB_TL_PZ_B=pz)
+        subprocess.run([sys.executable, "-c", _ZB_SCRIPT, root, f], env=env, check=True,
+                       timeout=600)
+        files[pz] = np.load(f)
+    for k in files["1"].files:
+        assert np.array_equal(files["8"][k], files["1"][k]), k
+
+
 @pytest.mark.parametrize("dims", [(20, 12, 16), (14, 24)])
 def test_wc_lattice_on_rectangular_periodic_boxes(dims):
     """The WC lattice path on non-cubic periodic lattices (per-axis extents

@@ -106,15 +106,17 @@ struct NSym { static constexpr int value = D == 3 ? 6 : (D == 2 ? 3 : 1); };
 // rhs record {dmom, drho}), the fused halo push, and for stage 2 the
 // block-reduced max(c + |v|) folded into scalars[2].  Every thread of the
 // block must call it (block reduction); `write` selects the rows it owns.
-template <int D, int NT>
-__device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, bool write,
-                                            int64_t i, double c, double dr,
-                                            const double (&dm)[D], const double4* Sn,
-                                            const double4* Mn, double4* S_out, double4* M_out,
-                                            double* scalars, int32_t* err) {
+// wc_row_update: the per-row part (flags into `flags`, returns c + |v| of
+// stage 2, else 0); wc_block_finish: the block part (speed reduction, error
+// word).  wc_epilogue = both, for one row per thread.
+template <int D>
+__device__ __forceinline__ double wc_row_update(const sphb_wc_params& P, int stage, int64_t i,
+                                                double c, double dr, const double (&dm)[D],
+                                                const double4* Sn, const double4* Mn,
+                                                double4* S_out, double4* M_out,
+                                                const double* scalars, int32_t& flags) {
   double speed = 0.0;
-  int32_t flags = 0;
-  if (write) {
+  {
     bool finite = isfinite(dr);
 #pragma unroll
     for (int a = 0; a < D; ++a) finite = finite && isfinite(dm[a]);
@@ -159,6 +161,12 @@ __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, 
       }
     }
   }
+  return speed;
+}
+
+template <int NT>
+__device__ __forceinline__ void wc_block_finish(int stage, double speed, int32_t flags,
+                                                double* scalars, int32_t* err) {
   if (stage == 2) {
     __shared__ double red[NT / 32];
     const double w = warp_max(speed);
@@ -172,6 +180,19 @@ __device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, 
     }
   }
   if (flags) atomicOr(err, flags);
+}
+
+template <int D, int NT>
+__device__ __forceinline__ void wc_epilogue(const sphb_wc_params& P, int stage, bool write,
+                                            int64_t i, double c, double dr,
+                                            const double (&dm)[D], const double4* Sn,
+                                            const double4* Mn, double4* S_out, double4* M_out,
+                                            double* scalars, int32_t* err) {
+  int32_t flags = 0;
+  const double speed =
+      write ? wc_row_update<D>(P, stage, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, flags)
+            : 0.0;
+  wc_block_finish<NT>(stage, speed, flags, scalars, err);
 }
 
 }  // namespace wc

@@ -106,6 +106,97 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// One row's state in the pair loop: its own record, and the sums.
+template <int D>
+struct LatRow {
+  double vi[D], hvi[D], rho_i, hrho_i;
+  Sym<D> Bi;
+  double dr, dm[D];
+  __device__ __forceinline__ void load(const double* B, const double4* S_in, int64_t n,
+                                       int64_t i) {
+    unpack_s<D>(S_in[i], vi, rho_i);
+    Bi.load(B, n, i);
+    hrho_i = 0.5 * rho_i;
+#pragma unroll
+    for (int q = 0; q < D; ++q) hvi[q] = 0.5 * vi[q];
+    dr = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) dm[q] = 0.0;
+  }
+};
+
+// One directed pair (i, j) at canonical slot k (offset o, compile-time);
+// eulerian.py:230-266 with the table's folded factors:
+//   x = du eta_c, beta = clamp(x), p* = rbar (c^2 + beta kappa x) - c^2 rho0,
+//   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
+//   drho += rbar vs . (B_i + B_j) gg,
+//   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
+template <int D, int R2, int k>
+__device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, LatRow<D>& r,
+                                         const double (&vj)[D], double rho_j,
+                                         const Sym<D>& Bj) {
+  using St = Stencil<D, R2>;
+  constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+  Sym<D> Bs;
+  r.Bi.add(Bj, Bs);
+  // components with o_q = 0 are zero (checked within tol): compile-time
+  // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
+  double Gg[D];                                     // (B_i + B_j) gg, nonzero columns
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double acc = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      if (o[q] != 0) {
+        acc = first ? Bs.at(a, q) * L.gg[k][q] : fma(Bs.at(a, q), L.gg[k][q], acc);
+        first = false;
+      }
+    Gg[a] = acc;
+  }
+  // x = (v_j - v_i) . ee over the nonzero components, as vj . ee - vi . ee
+  double xi = 0.0;
+  bool first = true;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+    if (o[q] != 0) {
+      xi = first ? r.vi[q] * L.ee[k][q] : fma(r.vi[q], L.ee[k][q], xi);
+      first = false;
+    }
+  double x = -xi;                                  // (u_l - u_r) eta / c
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+    if (o[q] != 0) x = fma(vj[q], L.ee[k][q], x);
+  // beta = clamp(x, 0, 1) on the high word (integer pipe, not DSETP):
+  // negative (sign bit) -> 0; x >= 1.0 <=> high word >= that of 1.0
+  const int hx = __double2hiint(x);
+  double beta = hx < 0 ? 0.0 : x;
+  beta = hx >= 0x3FF00000 ? 1.0 : beta;
+  const double rbar = fma(0.5, rho_j, r.hrho_i);
+  const double bk = beta * K.kappa;
+  const double p_star = fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
+  // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
+  // the beta^2 limiter term)
+  double rr;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(rbar));
+  rr = fma(rr, fma(-rbar, rr, 1.0), rr);
+  const double wq = ((beta * bk) * (r.rho_i - rho_j)) * rr;
+  double vs[D];
+  double sg = 0.0;
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const double vb = fma(0.5, vj[q], r.hvi[q]);
+    vs[q] = o[q] == 0 ? vb : fma(-wq, L.ee[k][q], vb);
+    sg = fma(vs[q], Gg[q], sg);
+  }
+  const double rs2 = rbar * sg;                    // -2 rbar s
+  r.dr += rs2;
+  // viscous -mv (v_j - v_i): the v_i part is summed once (K.mv_sum)
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+    r.dm[q] = fma(-L.mv[k], vj[q], fma(p_star, Gg[q], fma(rs2, vs[q], r.dm[q])));
+}
+
 template <int D, int R2, int MINB, int NT = kLT>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
@@ -147,101 +238,138 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     zs[s + R] = D > 2 ? n0 * n1 * wrapc(cz, s, n2) : 0;
   }
 
-  const double c = P.c_art;
-  const double c2 = K.c2, c2rho0 = K.c2rho0, kappa = K.kappa;
-  double vi[D], rho_i;
-  unpack_s<D>(S_in[i], vi, rho_i);
-  Sym<D> Bi;
-  Bi.load(B, n, i);
-  const double hrho_i = 0.5 * rho_i;
-  double hvi[D];
-#pragma unroll
-  for (int q = 0; q < D; ++q) hvi[q] = 0.5 * vi[q];
-  double dr = 0.0, dm[D];
-#pragma unroll
-  for (int q = 0; q < D; ++q) dm[q] = 0.0;
-
-  // one directed pair (i, j) at canonical slot k (offset o, compile-time);
-  // eulerian.py:230-266 with the table's folded factors:
-  //   x = du eta_c, beta = clamp(x), p* = rbar (c^2 + beta kappa x) - c^2 rho0,
-  //   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
-  //   drho += rbar vs . (B_i + B_j) gg,
-  //   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
-  auto pair = [&](auto kc, const int64_t j) {
-    constexpr int k = decltype(kc)::value;
-    constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-    double vj[D], rho_j;
-    unpack_s<D>(ldg4(S_in + j), vj, rho_j);
-    Sym<D> Bj, Bs;
-    Bj.load(B, n, j);
-    Bi.add(Bj, Bs);
-    // components with o_q = 0 are zero (checked within tol): compile-time
-    // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
-    double Gg[D];                                     // (B_i + B_j) gg, nonzero columns
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      double acc = 0.0;
-      bool first = true;
-#pragma unroll
-      for (int q = 0; q < D; ++q)
-        if (o[q] != 0) {
-          acc = first ? Bs.at(r, q) * L.gg[k][q] : fma(Bs.at(r, q), L.gg[k][q], acc);
-          first = false;
-        }
-      Gg[r] = acc;
-    }
-    // x = (v_j - v_i) . ee over the nonzero components, as vj . ee - vi . ee
-    double xi = 0.0;
-    bool first = true;
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-      if (o[q] != 0) {
-        xi = first ? vi[q] * L.ee[k][q] : fma(vi[q], L.ee[k][q], xi);
-        first = false;
-      }
-    double x = -xi;                                  // (u_l - u_r) eta / c
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-      if (o[q] != 0) x = fma(vj[q], L.ee[k][q], x);
-    // beta = clamp(x, 0, 1) on the high word (integer pipe, not DSETP):
-    // negative (sign bit) -> 0; x >= 1.0 <=> high word >= that of 1.0
-    const int hx = __double2hiint(x);
-    double beta = hx < 0 ? 0.0 : x;
-    beta = hx >= 0x3FF00000 ? 1.0 : beta;
-    const double rbar = fma(0.5, rho_j, hrho_i);
-    const double bk = beta * kappa;
-    const double p_star = fma(rbar, fma(bk, x, c2), -c2rho0);
-    // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
-    // the beta^2 limiter term)
-    double rr;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(rbar));
-    rr = fma(rr, fma(-rbar, rr, 1.0), rr);
-    const double wq = ((beta * bk) * (rho_i - rho_j)) * rr;
-    double vs[D];
-    double sg = 0.0;
-#pragma unroll
-    for (int q = 0; q < D; ++q) {
-      const double vb = fma(0.5, vj[q], hvi[q]);
-      vs[q] = o[q] == 0 ? vb : fma(-wq, L.ee[k][q], vb);
-      sg = fma(vs[q], Gg[q], sg);
-    }
-    const double rs2 = rbar * sg;                    // -2 rbar s
-    dr += rs2;
-    // viscous -mv (v_j - v_i): the v_i part is summed once (K.mv_sum)
-#pragma unroll
-    for (int q = 0; q < D; ++q)
-      dm[q] = fma(-L.mv[k], vj[q], fma(p_star, Gg[q], fma(rs2, vs[q], dm[q])));
-  };
-
+  LatRow<D> row;
+  row.load(B, S_in, n, i);
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-    pair(kc, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]));
+    const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
+    double vj[D], rho_j;
+    unpack_s<D>(ldg4(S_in + j), vj, rho_j);
+    Sym<D> Bj;
+    Bj.load(B, n, j);
+    lat_pair<D, R2, k>(L, K, row, vj, rho_j, Bj);
   });
 #pragma unroll
-  for (int q = 0; q < D; ++q) dm[q] = fma(K.mv_sum, vi[q], dm[q]);
+  for (int q = 0; q < D; ++q) row.dm[q] = fma(K.mv_sum, row.vi[q], row.dm[q]);
 
-  wc_epilogue<D, NT>(P, stage, own, i, c, dr, dm, Sn, Mn, S_out, M_out, scalars, err);
+  wc_epilogue<D, NT>(P, stage, own, i, P.c_art, row.dr, row.dm, Sn, Mn, S_out, M_out, scalars,
+                     err);
+}
+
+// slot of offset (x, y, z) in the canonical order, -1 outside the stencil
+template <int D, int R2>
+constexpr int lat_slot(int x, int y, int z) {
+  using St = Stencil<D, R2>;
+  for (int k = 0; k < St::W; ++k)
+    if (St::L.o[k][0] == x && St::L.o[k][1] == y && St::L.o[k][2] == z) return k;
+  return -1;
+}
+
+// does some row p < PZ of a pencil take the record at (dx, dy, qrel)?
+template <int R2, int PZ>
+constexpr bool zb_used(int qrel, int dx, int dy) {
+  constexpr int R = isqrt_c(R2);
+  for (int p = 0; p < PZ; ++p) {
+    const int dz = qrel - p;
+    if (dz >= -R && dz <= R && lat_slot<3, R2>(dx, dy, dz) >= 0) return true;
+  }
+  return false;
+}
+
+// z-blocked stage (3D).  A thread owns a pencil of PZ rows along the slow
+// axis, (a, b, c0 .. c0 + PZ - 1); the lanes of a warp stay consecutive along
+// the fast axis, so every gather is still coalesced.  The neighbour records
+// are walked plane by plane (c0 - R .. c0 + PZ - 1 + R) and inside a plane
+// (dy, dx) ascending; one gathered record {S_j, B_j} serves every owned row
+// it neighbours (up to 2R + 1 of them, independent FP64 chains), so the
+// gathers per row drop from W to about (PZ + 2R)(2R + 1)^2 / PZ (fewer at
+// the stencil's corners).  Each row still receives its slots in the
+// canonical order (z, then y, then x ascending) through the same lat_pair:
+// the results are bitwise those of k_wc_lattice.  The launcher uses it when
+// the updated rows are whole pencils of whole planes.
+template <int R2, int PZ, int MINB>
+__global__ void __launch_bounds__(kLT, MINB)
+k_wc_zb(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
+        const double* __restrict__ B, const double4* __restrict__ S_in, const double4* Sn,
+        const double4* Mn, double4* S_out, double4* M_out, double* __restrict__ scalars,
+        int32_t* __restrict__ err, const int64_t pf, const int zguard) {
+  constexpr int D = 3;
+  constexpr int R = isqrt_c(R2);
+  constexpr int S = 2 * R + 1;
+  const int64_t n = P.n;
+  const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
+  const int64_t s2 = (int64_t)n0 * n1;
+  const int64_t t = (int64_t)blockIdx.x * kLT + threadIdx.x;
+  const int64_t nth = (P.nrows / PZ);
+  const bool own = t < nth;
+  const int64_t tt = own ? t : nth - 1;
+  const int a = (int)(tt % n0);
+  const int b = (int)((tt / n0) % n1);
+  const int c0 = (int)(P.row0 / s2) + (int)(tt / s2) * PZ;
+  int xs[S], ys[S], zs[PZ + 2 * R];
+#pragma unroll
+  for (int s = -R; s <= R; ++s) {
+    xs[s + R] = wrapc(a, s, n0);
+    ys[s + R] = n0 * wrapc(b, s, n1);
+  }
+#pragma unroll
+  for (int q = 0; q < PZ + 2 * R; ++q) zs[q] = n0 * n1 * wrapc(c0, q - R, n2);
+  const int64_t i0 = (int64_t)a + (int64_t)n0 * b + s2 * c0;
+  if (pf > 0) {
+#pragma unroll
+    for (int q = 0; q < PZ + 2 * R; ++q) {
+      const int64_t ip = (int64_t)zs[q] + ys[R] + xs[R] + pf;
+      if (ip < n) {
+        prefetch_l2(S_in + ip);
+        prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
+        prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
+      }
+    }
+  }
+
+  LatRow<D> rows[PZ];
+#pragma unroll
+  for (int p = 0; p < PZ; ++p) rows[p].load(B, S_in, n, i0 + p * s2);
+
+  static_for<PZ + 2 * R>([&](auto qc) {
+    constexpr int qrel = decltype(qc)::value - R;
+    // zguard (= PZ at run time) keeps the compiler from hoisting the
+    // gathers of every plane ahead of the arithmetic
+    if (qrel < zguard + R) {
+      static_for<S * S>([&](auto ec) {
+        constexpr int dy = decltype(ec)::value / S - R;
+        constexpr int dx = decltype(ec)::value % S - R;
+        if constexpr (zb_used<R2, PZ>(qrel, dx, dy)) {
+          const int64_t j = (int64_t)(xs[dx + R] + ys[dy + R] + zs[qrel + R]);
+          double vj[D], rho_j;
+          unpack_s<D>(ldg4(S_in + j), vj, rho_j);
+          Sym<D> Bj;
+          Bj.load(B, n, j);
+          static_for<PZ>([&](auto pc) {
+            constexpr int p = decltype(pc)::value;
+            constexpr int dz = qrel - p;
+            constexpr int k = (dz < -R || dz > R) ? -1 : lat_slot<3, R2>(dx, dy, dz);
+            if constexpr (k >= 0) lat_pair<D, R2, k>(L, K, rows[p], vj, rho_j, Bj);
+          });
+        }
+      });
+    }
+  });
+
+  double speed = 0.0;
+  int32_t flags = 0;
+  if (own) {
+#pragma unroll
+    for (int p = 0; p < PZ; ++p) {
+#pragma unroll
+      for (int q = 0; q < D; ++q) rows[p].dm[q] = fma(K.mv_sum, rows[p].vi[q], rows[p].dm[q]);
+      const double s = wc_row_update<D>(P, stage, i0 + p * s2, P.c_art, rows[p].dr, rows[p].dm,
+                                        Sn, Mn, S_out, M_out, scalars, flags);
+      speed = (s > speed || s != s) ? s : speed;    // NaN reaches the dt check
+    }
+  }
+  wc_block_finish<kLT>(stage, speed, flags, scalars, err);
 }
 
 // Proof of the specialisation for rows [row0, row0 + nrows): cnt == W, the
@@ -648,6 +776,39 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
+  }
+  // z-blocked kernel (3D): rows per thread along the slow axis
+  // (SPHB_WC_PZ: 1 = the one-row kernel), occupancy target SPHB_WC_ZMINB;
+  // used when the updated rows are whole pencils of whole planes
+  static const int pz_env = [] {
+    const char* e = getenv("SPHB_WC_PZ");
+    return e ? atoi(e) : -1;
+  }();
+  static const int zminb_env = [] {
+    const char* e = getenv("SPHB_WC_ZMINB");
+    return e ? atoi(e) : 0;
+  }();
+  const int pz = L->pz > 0 ? L->pz : (pz_env >= 0 ? pz_env : 4);
+  const int64_t plane = (int64_t)L->n[0] * L->n[1];
+  if (p->dim == 3 && !nt_env && (pz == 2 || pz == 4) && p->row0 % plane == 0 &&
+      p->nrows % (plane * pz) == 0) {
+    const int zminb = zminb_env ? zminb_env : (pz == 2 ? 3 : 2);
+    const int64_t nth = p->nrows / pz;
+    const unsigned zgrid = (unsigned)((nth + kLT - 1) / kLT);
+    static const int64_t zpf_env = [] {
+      const char* e = getenv("SPHB_WC_ZPF");
+      return e ? (int64_t)atoll(e) : (int64_t)0;
+    }();
+#define SPHB_Z(R2, PZ, MB)                                                                  \
+    if (L->r2 == R2 && pz == PZ && zminb == MB) {                                           \
+      k_wc_zb<R2, PZ, MB><<<zgrid, kLT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, \
+                                                 scalars, err, zpf_env, pz);               \
+      SPHB_LAUNCH_CHECK();                                                                  \
+      return SPHB_OK;                                                                       \
+    }
+    SPHB_Z(4, 2, 2) SPHB_Z(4, 2, 3) SPHB_Z(4, 4, 1) SPHB_Z(4, 4, 2)
+    SPHB_Z(6, 2, 1) SPHB_Z(6, 2, 2) SPHB_Z(6, 4, 1) SPHB_Z(6, 4, 2)
+#undef SPHB_Z
   }
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);

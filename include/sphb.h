@@ -299,8 +299,7 @@ typedef struct sphb_lattice {
   int32_t width;         /* slots per row = sphb_lattice_width(dim, r2)     */
   int32_t r2;
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
-  int32_t pz;            /* 3D: rows per thread along the slow axis (the
-                          * z-blocked stage; 0 = default, 1 = one row)       */
+  int32_t reserved;
   double dx[SPHB_LATTICE_MAXW][3];
   double inv_r[SPHB_LATTICE_MAXW];
   double g2[SPHB_LATTICE_MAXW];

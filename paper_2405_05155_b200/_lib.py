@@ -162,7 +162,7 @@ class Lattice(C.Structure):
         ("width", C.c_int32),
         ("r2", C.c_int32),
         ("n", C.c_int32 * 3),
-        ("pz", C.c_int32),
+        ("reserved", C.c_int32),
         ("dx", (C.c_double * 3) * LATTICE_MAXW),
         ("inv_r", C.c_double * LATTICE_MAXW),
         ("g2", C.c_double * LATTICE_MAXW),

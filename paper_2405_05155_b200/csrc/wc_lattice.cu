@@ -257,121 +257,6 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
                      err);
 }
 
-// slot of offset (x, y, z) in the canonical order, -1 outside the stencil
-template <int D, int R2>
-constexpr int lat_slot(int x, int y, int z) {
-  using St = Stencil<D, R2>;
-  for (int k = 0; k < St::W; ++k)
-    if (St::L.o[k][0] == x && St::L.o[k][1] == y && St::L.o[k][2] == z) return k;
-  return -1;
-}
-
-// does some row p < PZ of a pencil take the record at (dx, dy, qrel)?
-template <int R2, int PZ>
-constexpr bool zb_used(int qrel, int dx, int dy) {
-  constexpr int R = isqrt_c(R2);
-  for (int p = 0; p < PZ; ++p) {
-    const int dz = qrel - p;
-    if (dz >= -R && dz <= R && lat_slot<3, R2>(dx, dy, dz) >= 0) return true;
-  }
-  return false;
-}
-
-// z-blocked stage (3D).  A thread owns a pencil of PZ rows along the slow
-// axis, (a, b, c0 .. c0 + PZ - 1); the lanes of a warp stay consecutive along
-// the fast axis, so every gather is still coalesced.  The neighbour records
-// are walked plane by plane (c0 - R .. c0 + PZ - 1 + R) and inside a plane
-// (dy, dx) ascending; one gathered record {S_j, B_j} serves every owned row
-// it neighbours (up to 2R + 1 of them, independent FP64 chains), so the
-// gathers per row drop from W to about (PZ + 2R)(2R + 1)^2 / PZ (fewer at
-// the stencil's corners).  Each row still receives its slots in the
-// canonical order (z, then y, then x ascending) through the same lat_pair:
-// the results are bitwise those of k_wc_lattice.  The launcher uses it when
-// the updated rows are whole pencils of whole planes.
-template <int R2, int PZ, int MINB>
-__global__ void __launch_bounds__(kLT, MINB)
-k_wc_zb(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
-        const double* __restrict__ B, const double4* __restrict__ S_in, const double4* Sn,
-        const double4* Mn, double4* S_out, double4* M_out, double* __restrict__ scalars,
-        int32_t* __restrict__ err, const int64_t pf, const int zguard) {
-  constexpr int D = 3;
-  constexpr int R = isqrt_c(R2);
-  constexpr int S = 2 * R + 1;
-  const int64_t n = P.n;
-  const int n0 = L.n[0], n1 = L.n[1], n2 = L.n[2];
-  const int64_t s2 = (int64_t)n0 * n1;
-  const int64_t t = (int64_t)blockIdx.x * kLT + threadIdx.x;
-  const int64_t nth = (P.nrows / PZ);
-  const bool own = t < nth;
-  const int64_t tt = own ? t : nth - 1;
-  const int a = (int)(tt % n0);
-  const int b = (int)((tt / n0) % n1);
-  const int c0 = (int)(P.row0 / s2) + (int)(tt / s2) * PZ;
-  int xs[S], ys[S], zs[PZ + 2 * R];
-#pragma unroll
-  for (int s = -R; s <= R; ++s) {
-    xs[s + R] = wrapc(a, s, n0);
-    ys[s + R] = n0 * wrapc(b, s, n1);
-  }
-#pragma unroll
-  for (int q = 0; q < PZ + 2 * R; ++q) zs[q] = n0 * n1 * wrapc(c0, q - R, n2);
-  const int64_t i0 = (int64_t)a + (int64_t)n0 * b + s2 * c0;
-  if (pf > 0) {
-#pragma unroll
-    for (int q = 0; q < PZ + 2 * R; ++q) {
-      const int64_t ip = (int64_t)zs[q] + ys[R] + xs[R] + pf;
-      if (ip < n) {
-        prefetch_l2(S_in + ip);
-        prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
-        prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
-      }
-    }
-  }
-
-  LatRow<D> rows[PZ];
-#pragma unroll
-  for (int p = 0; p < PZ; ++p) rows[p].load(B, S_in, n, i0 + p * s2);
-
-  static_for<PZ + 2 * R>([&](auto qc) {
-    constexpr int qrel = decltype(qc)::value - R;
-    // zguard (= PZ at run time) keeps the compiler from hoisting the
-    // gathers of every plane ahead of the arithmetic
-    if (qrel < zguard + R) {
-      static_for<S * S>([&](auto ec) {
-        constexpr int dy = decltype(ec)::value / S - R;
-        constexpr int dx = decltype(ec)::value % S - R;
-        if constexpr (zb_used<R2, PZ>(qrel, dx, dy)) {
-          const int64_t j = (int64_t)(xs[dx + R] + ys[dy + R] + zs[qrel + R]);
-          double vj[D], rho_j;
-          unpack_s<D>(ldg4(S_in + j), vj, rho_j);
-          Sym<D> Bj;
-          Bj.load(B, n, j);
-          static_for<PZ>([&](auto pc) {
-            constexpr int p = decltype(pc)::value;
-            constexpr int dz = qrel - p;
-            constexpr int k = (dz < -R || dz > R) ? -1 : lat_slot<3, R2>(dx, dy, dz);
-            if constexpr (k >= 0) lat_pair<D, R2, k>(L, K, rows[p], vj, rho_j, Bj);
-          });
-        }
-      });
-    }
-  });
-
-  double speed = 0.0;
-  int32_t flags = 0;
-  if (own) {
-#pragma unroll
-    for (int p = 0; p < PZ; ++p) {
-#pragma unroll
-      for (int q = 0; q < D; ++q) rows[p].dm[q] = fma(K.mv_sum, rows[p].vi[q], rows[p].dm[q]);
-      const double s = wc_row_update<D>(P, stage, i0 + p * s2, P.c_art, rows[p].dr, rows[p].dm,
-                                        Sn, Mn, S_out, M_out, scalars, flags);
-      speed = (s > speed || s != s) ? s : speed;    // NaN reaches the dt check
-    }
-  }
-  wc_block_finish<kLT>(stage, speed, flags, scalars, err);
-}
-
 // Proof of the specialisation for rows [row0, row0 + nrows): cnt == W, the
 // row's neighbours are exactly {i + o_k} (wrapped), and the exact minimum-
 // image displacement of each (neighbors.py:152-157) is within tol of the
@@ -776,39 +661,6 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
-  }
-  // z-blocked kernel (3D): rows per thread along the slow axis
-  // (SPHB_WC_PZ: 1 = the one-row kernel), occupancy target SPHB_WC_ZMINB;
-  // used when the updated rows are whole pencils of whole planes
-  static const int pz_env = [] {
-    const char* e = getenv("SPHB_WC_PZ");
-    return e ? atoi(e) : -1;
-  }();
-  static const int zminb_env = [] {
-    const char* e = getenv("SPHB_WC_ZMINB");
-    return e ? atoi(e) : 0;
-  }();
-  const int pz = L->pz > 0 ? L->pz : (pz_env >= 0 ? pz_env : 4);
-  const int64_t plane = (int64_t)L->n[0] * L->n[1];
-  if (p->dim == 3 && !nt_env && (pz == 2 || pz == 4) && p->row0 % plane == 0 &&
-      p->nrows % (plane * pz) == 0) {
-    const int zminb = zminb_env ? zminb_env : (pz == 2 ? 3 : 2);
-    const int64_t nth = p->nrows / pz;
-    const unsigned zgrid = (unsigned)((nth + kLT - 1) / kLT);
-    static const int64_t zpf_env = [] {
-      const char* e = getenv("SPHB_WC_ZPF");
-      return e ? (int64_t)atoll(e) : (int64_t)0;
-    }();
-#define SPHB_Z(R2, PZ, MB)                                                                  \
-    if (L->r2 == R2 && pz == PZ && zminb == MB) {                                           \
-      k_wc_zb<R2, PZ, MB><<<zgrid, kLT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, \
-                                                 scalars, err, zpf_env, pz);               \
-      SPHB_LAUNCH_CHECK();                                                                  \
-      return SPHB_OK;                                                                       \
-    }
-    SPHB_Z(4, 2, 2) SPHB_Z(4, 2, 3) SPHB_Z(4, 4, 1) SPHB_Z(4, 4, 2)
-    SPHB_Z(6, 2, 1) SPHB_Z(6, 2, 2) SPHB_Z(6, 4, 1) SPHB_Z(6, 4, 2)
-#undef SPHB_Z
   }
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);

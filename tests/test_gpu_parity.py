@@ -892,26 +892,6 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
         assert l2_error(s.state.mom, ref.mom) < 1e-10
 
 
-@pytest.mark.parametrize("key", ["1.6h", "2h"])
-@pytest.mark.parametrize("pz", [2, 4])
-def test_wc_zblocked_stage_is_bitwise_the_one_row_kernel(key, pz):
-    """The z-blocked lattice stage (csrc/wc_lattice.cu k_wc_zb: PZ rows per
-    thread along z, one gathered record serving every owned row it
-    neighbours) gives every row its slots in the canonical order through the
-    same pair code, so after several steps it is bitwise the one-row kernel."""
-    cfg = configs.c5_tgv3d(kernel=key, n_side=16)
-    one, zb = make_wc(cfg), make_wc(cfg)
-    assert one.lattice is not None and zb.lattice is not None
-    one.lattice.pz = 1
-    zb.lattice.pz = pz
-    for s in (one, zb):
-        s.step()
-        s.advance(9)
-    assert np.array_equal(one.state.rho, zb.state.rho)
-    assert np.array_equal(one.state.mom, zb.state.mom)
-    assert one.t == zb.t
-
-
 def test_wc_lattice_check_rejects_perturbed_sets():
     """Same pair set, displacements off the table by more than the tolerance:
     the check refuses the lattice path (general kernel, still oracle-exact)."""

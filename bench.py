@@ -56,8 +56,9 @@ FLOPS_PER_PAIR_EST = 117
 # lattice kernel (wc_lattice.cu), FP64 flops per pair from its SASS
 # (DFMA = 2): r2 = 4 stencil (919 DFMA + 308 DMUL + 212 DADD) / 32 slots,
 # r2 = 6 stencil (2409 DFMA + 741 DMUL + 572 DADD) / 80 slots (round 2,
-# folded slot table; profiles/r02_ncu_c5_256.md)
-FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 77}
+# folded slot table; profiles/r02_ncu_c5_256.md); the r2 = 6 stencil runs
+# the separable-slot form, 2278 DFMA + 582 DMUL + 704 DADD = 73 per pair
+FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 73}
 
 
 def traffic_per_launch(kernel: str):
@@ -246,6 +247,10 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     if solver.lattice is not None:
         kernel = "k_wc_lattice<3,%d,%s>" % (solver.lattice.r2, os.environ.get(
             "SPHB_LAT_MINB", "3" if solver.lattice.r2 == 4 else "2"))
+        if (solver.lattice.r2 == 6 and solver.lattice_separable
+                and os.environ.get("SPHB_LAT_ISO", "1") != "0"
+                and not os.environ.get("SPHB_LAT_MINB") and not os.environ.get("SPHB_LAT_NT")):
+            kernel = "k_wc_lattice<3,6,2,256,separable>"
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None,
             "launches_per_step": launches_per_step}
@@ -715,7 +720,7 @@ def main():
         line["standard_2h"] = {
             "value": S["n"] * K / (S["ms"] * 1e-3), "ms_per_step": S["ms"] / K,
             "pair_interactions_per_s": S["pairs"] * 2 * K / (S["ms"] * 1e-3),
-            "pairs_per_pass": S["pairs"]}
+            "pairs_per_pass": S["pairs"], "kernel": S["kernel"]}
         line["alpha_T1p6h_over_T2h"] = L["ms"] / S["ms"]
     if c4 is not None:
         line["c4_column"] = c4

@@ -232,6 +232,7 @@ SIGNATURES = {
     "sphb_tl_pass_b_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P, P]),
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
+    "sphb_wc_lattice_separable": (C.c_int, [I32, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_stage_lattice_f32": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),

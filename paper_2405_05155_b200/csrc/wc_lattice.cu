@@ -92,6 +92,14 @@ struct LatFold {
   double ee[SPHB_LATTICE_MAXW][3];
   double gg[SPHB_LATTICE_MAXW][3];
   double mv[SPHB_LATTICE_MAXW];
+  // separable-slot form (ISO): when every slot's table displacement is
+  // dx_k = sp_k o_k (one spacing per slot, o_k the integer offset),
+  // gg_k = gs_k o_k / m_k with m_k = |first nonzero o_k| and gs_k = g2_k sp_k m_k,
+  // so (B_i + B_j) gg = gs_k (B_i + B_j) (o_k / m_k): the integer-coefficient
+  // combination is DADDs (no DMUL for one-axis slots) and gs_k folds into
+  // rbar once per pair; cg_k = c^2 rho0 gs_k
+  double gs[SPHB_LATTICE_MAXW];
+  double cg[SPHB_LATTICE_MAXW];
 };
 
 // wrapped lattice coordinate c + s in [0, n)
@@ -131,17 +139,20 @@ struct LatRow {
 //   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
 //   drho += rbar vs . (B_i + B_j) gg,
 //   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
-template <int D, int R2, int k>
+template <int D, int R2, int k, bool ISO>
 __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, LatRow<D>& r,
                                          const double (&vj)[D], double rho_j,
                                          const Sym<D>& Bj) {
   using St = Stencil<D, R2>;
   constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+  // first nonzero component and its magnitude (ISO form)
+  constexpr int q0 = o[0] != 0 ? 0 : (o[1] != 0 ? 1 : 2);
+  constexpr int m0 = o[q0] < 0 ? -o[q0] : o[q0];
   Sym<D> Bs;
   r.Bi.add(Bj, Bs);
   // components with o_q = 0 are zero (checked within tol): compile-time
   // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
-  double Gg[D];                                     // (B_i + B_j) gg, nonzero columns
+  double Gg[D];          // (B_i + B_j) gg, nonzero columns (ISO: / gs_k)
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     double acc = 0.0;
@@ -149,7 +160,19 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
 #pragma unroll
     for (int q = 0; q < D; ++q)
       if (o[q] != 0) {
-        acc = first ? Bs.at(a, q) * L.gg[k][q] : fma(Bs.at(a, q), L.gg[k][q], acc);
+        if constexpr (ISO) {
+          const double c = (double)o[q] / (double)m0;     // exact: +-1, +-2, +-1/2
+          if (first)
+            acc = o[q] > 0 ? Bs.at(a, q) : -Bs.at(a, q);
+          else if (c == 1.0)
+            acc = acc + Bs.at(a, q);
+          else if (c == -1.0)
+            acc = acc - Bs.at(a, q);
+          else
+            acc = fma(c, Bs.at(a, q), acc);
+        } else {
+          acc = first ? Bs.at(a, q) * L.gg[k][q] : fma(Bs.at(a, q), L.gg[k][q], acc);
+        }
         first = false;
       }
     Gg[a] = acc;
@@ -174,7 +197,10 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
   beta = hx >= 0x3FF00000 ? 1.0 : beta;
   const double rbar = fma(0.5, rho_j, r.hrho_i);
   const double bk = beta * K.kappa;
-  const double p_star = fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
+  // ISO: rg = rbar gs_k and pg = p* gs_k carry the factor Gg lost
+  const double rg = ISO ? rbar * L.gs[k] : rbar;
+  const double pg = ISO ? fma(rg, fma(bk, x, K.c2), -L.cg[k])
+                        : fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
   // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
   // the beta^2 limiter term)
   double rr;
@@ -189,15 +215,15 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
     vs[q] = o[q] == 0 ? vb : fma(-wq, L.ee[k][q], vb);
     sg = fma(vs[q], Gg[q], sg);
   }
-  const double rs2 = rbar * sg;                    // -2 rbar s
+  const double rs2 = rg * sg;                      // -2 rbar s
   r.dr += rs2;
   // viscous -mv (v_j - v_i): the v_i part is summed once (K.mv_sum)
 #pragma unroll
   for (int q = 0; q < D; ++q)
-    r.dm[q] = fma(-L.mv[k], vj[q], fma(p_star, Gg[q], fma(rs2, vs[q], r.dm[q])));
+    r.dm[q] = fma(-L.mv[k], vj[q], fma(pg, Gg[q], fma(rs2, vs[q], r.dm[q])));
 }
 
-template <int D, int R2, int MINB, int NT = kLT>
+template <int D, int R2, int MINB, int NT = kLT, bool ISO = false>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -248,7 +274,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     unpack_s<D>(ldg4(S_in + j), vj, rho_j);
     Sym<D> Bj;
     Bj.load(B, n, j);
-    lat_pair<D, R2, k>(L, K, row, vj, rho_j, Bj);
+    lat_pair<D, R2, k, ISO>(L, K, row, vj, rho_j, Bj);
   });
 #pragma unroll
   for (int q = 0; q < D; ++q) row.dm[q] = fma(K.mv_sum, row.vi[q], row.dm[q]);
@@ -576,6 +602,37 @@ static bool lattice_args_ok(const sphb_wc_params* p, const sphb_lattice* L) {
   return sphb_lattice_width(p->dim, L->r2) == L->width;
 }
 
+// Separable-slot form: every slot's table displacement is sp_k o_k with one
+// (signed) spacing per slot, to a relative spread of 1e-14 (far inside the
+// check's tolerance on the displacements themselves).  Fills F->gs / F->cg.
+static bool lattice_separable(int dim, const sphb_lattice* L, LatFold* F, double c2rho0) {
+  int32_t off[3 * SPHB_LATTICE_MAXW];
+  if (sphb_lattice_offsets(dim, L->r2, off) != SPHB_OK) return false;
+  for (int k = 0; k < L->width; ++k) {
+    int q0 = -1;
+    for (int q = 0; q < 3; ++q)
+      if (off[3 * k + q] != 0) { q0 = q; break; }
+    if (q0 < 0) return false;
+    const double sp = L->dx[k][q0] / off[3 * k + q0];
+    if (!(fabs(sp) > 0.0)) return false;
+    for (int q = 0; q < 3; ++q) {
+      const int o = off[3 * k + q];
+      if (o == 0) continue;      // zero components: compile-time zeros in every form
+      if (fabs(L->dx[k][q] / o - sp) > 1e-14 * fabs(sp)) return false;
+    }
+    if (F) {
+      F->gs[k] = L->g2[k] * sp * fabs((double)off[3 * k + q0]);
+      F->cg[k] = c2rho0 * F->gs[k];
+    }
+  }
+  return true;
+}
+
+extern "C" int sphb_wc_lattice_separable(int32_t dim, const sphb_lattice* L) {
+  if (!L || sphb_lattice_width(dim, L->r2) != L->width) return SPHB_ERR_ARG;
+  return lattice_separable(dim, L, nullptr, 0.0) ? 1 : 0;
+}
+
 extern "C" int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L,
                                      const double* x, const int32_t* nbr, const int32_t* cnt,
                                      double tol, unsigned long long* bad, void* stream) {
@@ -621,6 +678,12 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   }
   K.mv_sum = 0.0;
   for (int k = 0; k < L->width; ++k) K.mv_sum += L->mv[k];
+  // separable-slot form (LatFold::gs); SPHB_LAT_ISO=0 disables it (tuning)
+  static const int iso_env = [] {
+    const char* e = getenv("SPHB_LAT_ISO");
+    return e ? atoi(e) : 1;
+  }();
+  const bool iso = iso_env != 0 && lattice_separable(p->dim, L, &F, K.c2rho0);
   const unsigned grid = sphb_blocks(p->nrows, kLT);
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
@@ -661,6 +724,21 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
+  }
+  // separable-slot kernel: default for the 80-slot stencil only (C5 256^3,
+  // same box: 2h 10.46 -> 10.34 ms/step; the 32-slot stencil measured
+  // 4.27 -> 4.45 with 2 fewer FP64 instructions per pair, so it keeps the
+  // table form; profiles/r02_tune_lattice.md)
+  if (iso && !minb_env && !nt_env) {
+#define SPHB_I(D, R, MB, NT)                                                                 \
+    if (p->dim == D && L->r2 == R) {                                                         \
+      k_wc_lattice<D, R, MB, NT, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(            \
+          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pf);                    \
+      SPHB_LAUNCH_CHECK();                                                                   \
+      return SPHB_OK;                                                                        \
+    }
+    SPHB_I(3, 6, 2, 256)
+#undef SPHB_I
   }
   if (p->dim == 3 && (nt == 64 || nt == 256)) {
     const unsigned g2 = sphb_blocks(p->nrows, nt);

@@ -454,6 +454,7 @@ class EulerianSolver:
         p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
         p.vol_const = float(vol[0]) if self.n else 0.0
         self.lattice = None
+        self.lattice_separable = False
         if (variant == "global" and not self._ideal and ghosts is None
                 and wall_force_tag is None and uniform and self.order is not self.bins
                 and os.environ.get("SPHB_WC_LATTICE", "1") != "0"):
@@ -550,7 +551,12 @@ class EulerianSolver:
         _lib.call("sphb_wc_lattice_check", ctypes.byref(self.params), ctypes.byref(L),
                   self.X.data_ptr(), self.nbr.data_ptr(), self.cnt.data_ptr(),
                   1e-12 * spacing, bad.data_ptr(), _lib.stream_ptr())
-        return L if int(bad.item()) == 0 else None
+        if int(bad.item()) != 0:
+            return None
+        # separable-slot form of the lattice stage (every slot's displacement
+        # is one spacing times its integer offset; csrc/wc_lattice.cu)
+        self.lattice_separable = int(lib.sphb_wc_lattice_separable(d, ctypes.byref(L))) == 1
+        return L
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)

@@ -870,6 +870,9 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
     cfg = builder(kernel=key, n_side=size)
     fast = make_wc(cfg)
     assert fast.lattice is not None and fast.lattice.width == fast.width
+    # TGV tables are separable (one spacing per slot): the 80-slot stencil
+    # (2h) runs the separable-slot form of the lattice kernel
+    assert fast.lattice_separable
     monkeypatch.setenv("SPHB_WC_LATTICE", "0")
     gen = make_wc(cfg)
     assert gen.lattice is None

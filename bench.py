@@ -49,6 +49,8 @@ IMPL_RECORD_BYTES = 32 + 48 + 32 + 4 + 32 + (64 + 32) / 2.0
 # the lattice kernel reads neither X, cnt nor a pass list: B 48 + S 32 read,
 # S 32 written, stage 2 also S_n, M_n 64 read and M 32 written
 LATTICE_RECORD_BYTES = 48 + 32 + 32 + (64 + 32) / 2.0
+# uniform-B form (checked: every record's B equals b0 to 1e-12): no B reads
+LATTICE_UB_RECORD_BYTES = 32 + 32 + (64 + 32) / 2.0
 # FP64 flops per directed pair of the fused stage kernel, from the SASS of
 # k_wc_stage<3,1,5> (37 DFMA + 27 DMUL + 13 DADD per pair in the loop body,
 # plus the limiter branch ~3; profiles/r01_ncu_c5_256.md v3)
@@ -59,6 +61,9 @@ FLOPS_PER_PAIR_EST = 117
 # folded slot table; profiles/r02_ncu_c5_256.md); the r2 = 6 stencil runs
 # the separable-slot form, 2278 DFMA + 582 DMUL + 704 DADD = 73 per pair
 FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 73}
+# uniform-B form ((B_i + B_j) gg_k from the slot table): r2 = 4 838 DFMA +
+# 214 DMUL + 68 DADD / 32 slots, r2 = 6 2110 DFMA + 502 DMUL + 164 DADD / 80
+FLOPS_PER_PAIR_LATTICE_UB = {4: 61, 6: 61}
 
 
 def traffic_per_launch(kernel: str):
@@ -247,7 +252,11 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
     if solver.lattice is not None:
         kernel = "k_wc_lattice<3,%d,%s>" % (solver.lattice.r2, os.environ.get(
             "SPHB_LAT_MINB", "3" if solver.lattice.r2 == 4 else "2"))
-        if (solver.lattice.r2 == 6 and solver.lattice_separable
+        if (solver.lattice.uniform_b and not os.environ.get("SPHB_LAT_MINB")
+                and not os.environ.get("SPHB_LAT_NT")):
+            kernel = "k_wc_lattice<3,%d,%s,uniform_b>" % (solver.lattice.r2, os.environ.get(
+                "SPHB_LAT_UB_MINB", "4" if solver.lattice.r2 == 4 else "3"))
+        elif (solver.lattice.r2 == 6 and solver.lattice_separable
                 and os.environ.get("SPHB_LAT_ISO", "1") != "0"
                 and not os.environ.get("SPHB_LAT_MINB") and not os.environ.get("SPHB_LAT_NT")):
             kernel = "k_wc_lattice<3,6,2,256,separable>"
@@ -647,6 +656,9 @@ def main():
     if sv.lattice is not None:
         design_bytes = sv.n * LATTICE_RECORD_BYTES
         flops_pair = FLOPS_PER_PAIR_LATTICE[sv.lattice.r2]
+        if sv.lattice.uniform_b:
+            design_bytes = sv.n * LATTICE_UB_RECORD_BYTES
+            flops_pair = FLOPS_PER_PAIR_LATTICE_UB[sv.lattice.r2]
     del leg["1.6h"]["solver"], sv
     torch.cuda.empty_cache()
     if not args.no_2h:

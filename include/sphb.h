@@ -299,11 +299,14 @@ typedef struct sphb_lattice {
   int32_t width;         /* slots per row = sphb_lattice_width(dim, r2)     */
   int32_t r2;
   int32_t n[3];          /* lattice extents, 1 for unused axes              */
-  int32_t reserved;
+  int32_t uniform_b;     /* 1: every record's B equals b0 (checked by
+                          * sphb_wc_uniform_b_check); the stage then serves
+                          * (B_i + B_j) gg_k from a per-slot table          */
   double dx[SPHB_LATTICE_MAXW][3];
   double inv_r[SPHB_LATTICE_MAXW];
   double g2[SPHB_LATTICE_MAXW];
   double mv[SPHB_LATTICE_MAXW];
+  double b0[6];          /* {b00, b01, b02, b11, b12, b22} (2D: {b00, b01, b11}) */
 } sphb_lattice;
 /* Slots of the (dim, r2) stencil (0: unsupported) and their offsets
  * (off[3 k + axis]). */
@@ -317,6 +320,13 @@ int sphb_lattice_offsets(int32_t dim, int32_t r2, int32_t* off);
 int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L, const double* X,
                           const int32_t* nbr, const int32_t* cnt, double tol,
                           unsigned long long* bad, void* stream);
+/* Counts into *bad (device, accumulated) the records i in [0, p->n) whose
+ * symmetrised B (the two-plane layout of sphb_wc_stage) differs from b0
+ * (device, 6 doubles in the order of sphb_lattice.b0) by more than
+ * tol * max|b0| in any entry: zero means the uniform-B form is exact to
+ * that tolerance. */
+int sphb_wc_uniform_b_check(const sphb_wc_params* p, const double* B, const double* b0,
+                            double tol, unsigned long long* bad, void* stream);
 /* 1 when every slot's table displacement is sp_k o_k (one spacing per slot,
  * o_k the integer offset): sphb_wc_stage_lattice then runs its separable-slot
  * form ((B_i + B_j) gg as integer-coefficient sums times one factor per

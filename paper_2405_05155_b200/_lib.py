@@ -162,11 +162,12 @@ class Lattice(C.Structure):
         ("width", C.c_int32),
         ("r2", C.c_int32),
         ("n", C.c_int32 * 3),
-        ("reserved", C.c_int32),
+        ("uniform_b", C.c_int32),
         ("dx", (C.c_double * 3) * LATTICE_MAXW),
         ("inv_r", C.c_double * LATTICE_MAXW),
         ("g2", C.c_double * LATTICE_MAXW),
         ("mv", C.c_double * LATTICE_MAXW),
+        ("b0", C.c_double * 6),
     ]
 
 
@@ -233,6 +234,7 @@ SIGNATURES = {
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
     "sphb_wc_lattice_separable": (C.c_int, [I32, P]),
+    "sphb_wc_uniform_b_check": (C.c_int, [P, P, P, F64, P, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_stage_lattice_f32": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),

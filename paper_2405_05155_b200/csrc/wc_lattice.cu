@@ -100,6 +100,11 @@ struct LatFold {
   // rbar once per pair; cg_k = c^2 rho0 gs_k
   double gs[SPHB_LATTICE_MAXW];
   double cg[SPHB_LATTICE_MAXW];
+  // uniform-B form (UB): every record's B equals b0 within the check's
+  // tolerance (a lattice's correction matrices differ by rounding only), so
+  // (B_i + B_j) gg_k = 2 b0 gg_k is one vector per slot: no B gathers, no
+  // B_i + B_j, no B gg products in the pair loop
+  double gb[SPHB_LATTICE_MAXW][3];
 };
 
 // wrapped lattice coordinate c + s in [0, n)
@@ -120,10 +125,11 @@ struct LatRow {
   double vi[D], hvi[D], rho_i, hrho_i;
   Sym<D> Bi;
   double dr, dm[D];
+  template <bool UB = false>
   __device__ __forceinline__ void load(const double* B, const double4* S_in, int64_t n,
                                        int64_t i) {
     unpack_s<D>(S_in[i], vi, rho_i);
-    Bi.load(B, n, i);
+    if constexpr (!UB) Bi.load(B, n, i);
     hrho_i = 0.5 * rho_i;
 #pragma unroll
     for (int q = 0; q < D; ++q) hvi[q] = 0.5 * vi[q];
@@ -139,7 +145,7 @@ struct LatRow {
 //   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
 //   drho += rbar vs . (B_i + B_j) gg,
 //   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
-template <int D, int R2, int k, bool ISO>
+template <int D, int R2, int k, bool ISO, bool UB = false>
 __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, LatRow<D>& r,
                                          const double (&vj)[D], double rho_j,
                                          const Sym<D>& Bj) {
@@ -148,13 +154,18 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
   // first nonzero component and its magnitude (ISO form)
   constexpr int q0 = o[0] != 0 ? 0 : (o[1] != 0 ? 1 : 2);
   constexpr int m0 = o[q0] < 0 ? -o[q0] : o[q0];
-  Sym<D> Bs;
-  r.Bi.add(Bj, Bs);
   // components with o_q = 0 are zero (checked within tol): compile-time
   // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
   double Gg[D];          // (B_i + B_j) gg, nonzero columns (ISO: / gs_k)
+  Sym<D> Bs;
+  if constexpr (UB) {
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
+    for (int a = 0; a < D; ++a) Gg[a] = L.gb[k][a];
+  } else {
+    r.Bi.add(Bj, Bs);
+  }
+#pragma unroll
+  for (int a = 0; a < D && !UB; ++a) {
     double acc = 0.0;
     bool first = true;
 #pragma unroll
@@ -198,8 +209,9 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
   const double rbar = fma(0.5, rho_j, r.hrho_i);
   const double bk = beta * K.kappa;
   // ISO: rg = rbar gs_k and pg = p* gs_k carry the factor Gg lost
-  const double rg = ISO ? rbar * L.gs[k] : rbar;
-  const double pg = ISO ? fma(rg, fma(bk, x, K.c2), -L.cg[k])
+  constexpr bool SEP = ISO && !UB;
+  const double rg = SEP ? rbar * L.gs[k] : rbar;
+  const double pg = SEP ? fma(rg, fma(bk, x, K.c2), -L.cg[k])
                         : fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
   // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
   // the beta^2 limiter term)
@@ -223,7 +235,7 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
     r.dm[q] = fma(-L.mv[k], vj[q], fma(pg, Gg[q], fma(rs2, vs[q], r.dm[q])));
 }
 
-template <int D, int R2, int MINB, int NT = kLT, bool ISO = false>
+template <int D, int R2, int MINB, int NT = kLT, bool ISO = false, bool UB = false>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -243,8 +255,10 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
   if (pf > 0 && i0 + pf < n) {
     const int64_t ip = i0 + pf;
     prefetch_l2(S_in + ip);
-    prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
-    prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
+    if constexpr (!UB) {
+      prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
+      prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
+    }
     if (stage > 0 && Sn != S_in) prefetch_l2(Sn + ip);
     if (stage > 0) prefetch_l2(Mn + ip);
   }
@@ -265,7 +279,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
   }
 
   LatRow<D> row;
-  row.load(B, S_in, n, i);
+  row.template load<UB>(B, S_in, n, i);
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
@@ -273,8 +287,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     double vj[D], rho_j;
     unpack_s<D>(ldg4(S_in + j), vj, rho_j);
     Sym<D> Bj;
-    Bj.load(B, n, j);
-    lat_pair<D, R2, k, ISO>(L, K, row, vj, rho_j, Bj);
+    if constexpr (!UB) Bj.load(B, n, j);
+    lat_pair<D, R2, k, ISO, UB>(L, K, row, vj, rho_j, Bj);
   });
 #pragma unroll
   for (int q = 0; q < D; ++q) row.dm[q] = fma(K.mv_sum, row.vi[q], row.dm[q]);
@@ -602,6 +616,38 @@ static bool lattice_args_ok(const sphb_wc_params* p, const sphb_lattice* L) {
   return sphb_lattice_width(p->dim, L->r2) == L->width;
 }
 
+__global__ void k_uniform_b_check(int64_t n, int dim, const double* __restrict__ B,
+                                  const double* __restrict__ b0, double tol,
+                                  unsigned long long* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ne = dim == 3 ? 6 : (dim == 2 ? 3 : 1);
+  double r[6];
+  const double4 t = reinterpret_cast<const double4*>(B)[i];
+  r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
+  if (dim == 3) {
+    const double2 u = reinterpret_cast<const double2*>(B + 4 * n)[i];
+    r[4] = u.x; r[5] = u.y;
+  }
+  double scale = 0.0;
+  for (int e = 0; e < ne; ++e) scale = fmax(scale, fabs(b0[e]));
+  bool ok = true;
+  for (int e = 0; e < ne; ++e) ok = ok && fabs(r[e] - b0[e]) <= tol * scale;
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+extern "C" int sphb_wc_uniform_b_check(const sphb_wc_params* p, const double* B,
+                                       const double* b0, double tol, unsigned long long* bad,
+                                       void* stream) {
+  if (!p || !B || !b0 || !bad || p->n < 0 || p->dim < 1 || p->dim > 3 || !(tol >= 0.0))
+    return SPHB_ERR_ARG;
+  if (p->n == 0) return SPHB_OK;
+  k_uniform_b_check<<<sphb_blocks(p->n, 256), 256, 0, (cudaStream_t)stream>>>(
+      p->n, p->dim, B, b0, tol, bad);
+  SPHB_LAUNCH_CHECK();
+  return SPHB_OK;
+}
+
 // Separable-slot form: every slot's table displacement is sp_k o_k with one
 // (signed) spacing per slot, to a relative spread of 1e-14 (far inside the
 // check's tolerance on the displacements themselves).  Fills F->gs / F->cg.
@@ -684,6 +730,35 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     return e ? atoi(e) : 1;
   }();
   const bool iso = iso_env != 0 && lattice_separable(p->dim, L, &F, K.c2rho0);
+  // uniform-B form: (B_i + B_j) gg_k = 2 b0 gg_k per slot
+  const bool ub = L->uniform_b != 0;
+  if (ub) {
+    int32_t off[3 * SPHB_LATTICE_MAXW];
+    sphb_lattice_offsets(p->dim, L->r2, off);
+    double bs[3][3];
+    const int D = p->dim;
+    for (int a = 0; a < D; ++a)
+      for (int c = a; c < D; ++c) {
+        // index of (a, c) in {b00, b01, b02, b11, b12, b22} / {b00, b01, b11}
+        const int e = D == 3 ? (a == 0 ? c : (a == 1 ? 2 + c : 5)) : (a == 0 ? c : 2);
+        bs[a][c] = bs[c][a] = 2.0 * L->b0[e];
+      }
+    for (int k = 0; k < L->width; ++k)
+      for (int a = 0; a < 3; ++a) {
+        double acc = 0.0;
+        bool first = true;
+        for (int q = 0; q < D && a < D; ++q)
+          if (off[3 * k + q] != 0) {
+            acc = first ? bs[a][q] * F.gg[k][q] : fma(bs[a][q], F.gg[k][q], acc);
+            first = false;
+          }
+        F.gb[k][a] = acc;
+      }
+  }
+  static const int ubminb_env = [] {       // SPHB_LAT_UB_MINB (tuning)
+    const char* e = getenv("SPHB_LAT_UB_MINB");
+    return e ? atoi(e) : 0;
+  }();
   const unsigned grid = sphb_blocks(p->nrows, kLT);
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
@@ -717,13 +792,30 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     const char* e = getenv("SPHB_LAT_PF");
     return e ? (int64_t)atoll(e) : (int64_t)-1;
   }();
-  int64_t pf = 0;
+  int64_t pf = 0, reach = 0;
+  int sms = 148;
   if (p->dim == 3) {
-    int dev = 0, sms = 148;
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
+    reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
+  }
+  if (ub && !minb_env && !nt_env) {
+#define SPHB_U(D, R, MB, NT)                                                                 \
+    if (p->dim == D && L->r2 == R && umb == MB) {                                            \
+      k_wc_lattice<D, R, MB, NT, false, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(     \
+          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pfu);                   \
+      SPHB_LAUNCH_CHECK();                                                                   \
+      return SPHB_OK;                                                                        \
+    }
+    const int umb = ubminb_env ? ubminb_env : (p->dim == 3 ? (L->r2 == 4 ? 4 : 3) : 5);
+    const int64_t pfu =
+        p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
+    SPHB_U(3, 4, 3, 128) SPHB_U(3, 4, 4, 128) SPHB_U(3, 4, 5, 128)
+    SPHB_U(3, 6, 2, 128) SPHB_U(3, 6, 3, 128)
+    SPHB_U(2, 4, 5, 128) SPHB_U(2, 6, 5, 128)
+#undef SPHB_U
   }
   // separable-slot kernel: default for the 80-slot stencil only (C5 256^3,
   // same box: 2h 10.46 -> 10.34 ms/step; the 32-slot stencil measured

@@ -459,6 +459,8 @@ class EulerianSolver:
                 and wall_force_tag is None and uniform and self.order is not self.bins
                 and os.environ.get("SPHB_WC_LATTICE", "1") != "0"):
             self.lattice = self._setup_lattice(float(vol[0]))
+        if self.lattice is not None and os.environ.get("SPHB_LAT_UNIFORM_B", "1") != "0":
+            self._setup_uniform_b()
 
         self._cfl_h = self.cfl * kernel.h                      # eulerian.py:560
 
@@ -557,6 +559,39 @@ class EulerianSolver:
         # is one spacing times its integer offset; csrc/wc_lattice.cu)
         self.lattice_separable = int(lib.sphb_wc_lattice_separable(d, ctypes.byref(L))) == 1
         return L
+
+    def _setup_uniform_b(self):
+        """Uniform-B form of the lattice stage: on a complete periodic
+        lattice every particle's correction matrix B_i (correction.py:64-81)
+        is the same matrix up to rounding, so when every record (owned and
+        halo) equals b0 = B of the first updated row to 1e-12 of max|b0|
+        (sphb_wc_uniform_b_check), the stage serves (B_i + B_j) gg_k from a
+        per-slot table and gathers no B records.  Slab ranks use rank 0's b0
+        and switch only when every rank's check passes."""
+        torch = _lib.torch_cuda()
+        n, d, dev = self.n, self.dim, self._dev
+        r0 = int(self.params.row0)
+        b0 = torch.zeros(6, dtype=torch.float64, device=dev)
+        plane0 = self.B[:4 * n].view(n, 4)
+        if d == 3:
+            b0[:4] = plane0[r0]
+            b0[4:] = self.B[4 * n:].view(n, 2)[r0]
+        else:
+            b0[:3] = plane0[r0, :3]
+        multi = self._slab is not None and self._slab.world > 1
+        if multi:
+            if self._slab.rank != 0:
+                b0.zero_()
+            self._dist.all_reduce(b0)              # rank 0's b0 everywhere (x + 0)
+        bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.call("sphb_wc_uniform_b_check", ctypes.byref(self.params), self.B.data_ptr(),
+                  b0.data_ptr(), 1e-12, bad.data_ptr(), _lib.stream_ptr())
+        if multi:
+            self._dist.all_reduce(bad, op=self._dist.ReduceOp.MAX)
+        if int(bad.item()) == 0:
+            self.lattice.uniform_b = 1
+            for e, v in enumerate(b0.cpu().tolist()):
+                self.lattice.b0[e] = v
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)

@@ -873,6 +873,8 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
     # TGV tables are separable (one spacing per slot): the 80-slot stencil
     # (2h) runs the separable-slot form of the lattice kernel
     assert fast.lattice_separable
+    # ... and every correction matrix equals b0 to rounding: uniform-B form
+    assert fast.lattice.uniform_b == 1
     monkeypatch.setenv("SPHB_WC_LATTICE", "0")
     gen = make_wc(cfg)
     assert gen.lattice is None
@@ -893,6 +895,38 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
     for s in (fast, gen):
         assert l2_error(s.state.rho - 1.0, ref.rho - 1.0) < 1e-10
         assert l2_error(s.state.mom, ref.mom) < 1e-10
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+@pytest.mark.parametrize("label,builder,size", [("c2", configs.c2_tgv2d, 40),
+                                                ("c5", configs.c5_tgv3d, 16)])
+def test_wc_uniform_b_form_matches_table_form(monkeypatch, key, label, builder, size):
+    """The uniform-B lattice stage (B_i = B_j = b0 checked to 1e-12, (B_i +
+    B_j) gg_k served per slot) against the table form that gathers B_j:
+    equal to rounding after 20 steps, and the check refuses a b0 that is
+    off by 1e-9."""
+    import ctypes
+
+    import torch
+
+    from paper_2405_05155_b200 import _lib
+
+    cfg = builder(kernel=key, n_side=size)
+    ub = make_wc(cfg)
+    monkeypatch.setenv("SPHB_LAT_UNIFORM_B", "0")
+    tab = make_wc(cfg)
+    assert ub.lattice.uniform_b == 1 and tab.lattice is not None and tab.lattice.uniform_b == 0
+    for s in (ub, tab):
+        s.step()
+        s.advance(19)
+    assert l2_error(ub.state.rho - 1.0, tab.state.rho - 1.0) < 1e-12
+    assert l2_error(ub.state.mom, tab.state.mom) < 1e-12
+    b0 = torch.tensor(list(ub.lattice.b0), dtype=torch.float64, device="cuda")
+    for scale, want_bad in ((1.0, False), (1.0 + 1e-9, True)):
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _lib.call("sphb_wc_uniform_b_check", ctypes.byref(ub.params), ub.B.data_ptr(),
+                  (b0 * scale).data_ptr(), 1e-12, bad.data_ptr(), _lib.stream_ptr())
+        assert (int(bad.item()) > 0) == want_bad
 
 
 def test_wc_lattice_check_rejects_perturbed_sets():

@@ -382,6 +382,7 @@ struct LatF32 {
   int32_t n[3];
   float dx[SPHB_LATTICE_MAXW][3];
   float inv_r[SPHB_LATTICE_MAXW], g2[SPHB_LATTICE_MAXW], mv[SPHB_LATTICE_MAXW];
+  float gb[SPHB_LATTICE_MAXW][3];   // uniform-B form: 2 b0 dx_k (LatFold::gb)
 };
 
 struct LatConstF32 {
@@ -417,7 +418,7 @@ struct SymF<3> {
   }
 };
 
-template <int D, int R2, int MINB = 4>
+template <int D, int R2, int MINB = 4, bool UB = false>
 __global__ void __launch_bounds__(kLT, MINB)
 k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, const int stage,
                  const float* __restrict__ B, const float4* __restrict__ S32_in,
@@ -450,7 +451,7 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
 #pragma unroll
   for (int q = 0; q < D; ++q) hvi[q] = 0.5f * vi[q];
   SymF<D> Bi;
-  Bi.load(B, n, i);
+  if constexpr (!UB) Bi.load(B, n, i);
   double dr = 0.0, dm[D];
 #pragma unroll
   for (int q = 0; q < D; ++q) dm[q] = 0.0;
@@ -466,13 +467,17 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
     const float vj[3] = {sj.x, sj.y, sj.z};
     const float drho_j = D == 3 ? sj.w : sj.z;
     SymF<D> Bj;
-    Bj.load(B, n, j);
+    if constexpr (!UB) Bj.load(B, n, j);
     float dx[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) dx[q] = o[q] == 0 ? 0.f : L.dx[k][q];
     float G_[D];
+    if constexpr (UB) {
 #pragma unroll
-    for (int r = 0; r < D; ++r) {
+      for (int r = 0; r < D; ++r) G_[r] = L.gb[k][r];
+    }
+#pragma unroll
+    for (int r = 0; r < D && !UB; ++r) {
       float acc = 0.f;
       bool first = true;
 #pragma unroll
@@ -886,6 +891,25 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
     T.g2[k] = (float)L->g2[k];
     T.mv[k] = (float)L->mv[k];
   }
+  const bool ub = L->uniform_b != 0;
+  if (ub) {
+    int32_t off[3 * SPHB_LATTICE_MAXW];
+    sphb_lattice_offsets(p->dim, L->r2, off);
+    const int D = p->dim;
+    double bs[3][3];
+    for (int a = 0; a < D; ++a)
+      for (int c = a; c < D; ++c) {
+        const int e = D == 3 ? (a == 0 ? c : (a == 1 ? 2 + c : 5)) : (a == 0 ? c : 2);
+        bs[a][c] = bs[c][a] = 2.0 * L->b0[e];
+      }
+    for (int k = 0; k < L->width; ++k)
+      for (int a = 0; a < 3; ++a) {
+        double acc = 0.0;
+        for (int q = 0; q < D && a < D; ++q)
+          if (off[3 * k + q] != 0) acc += bs[a][q] * L->dx[k][q];
+        T.gb[k][a] = (float)acc;
+      }
+  }
   LatConstF32 K;
   K.c = (float)p->c_art;
   K.c2 = K.c * K.c;
@@ -901,9 +925,14 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   k_wc_lattice_f32<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,                    \
       (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
       (double4*)s_out, (double4*)m_out, scalars, err)
+#define SPHB_FU(D, R, MB)                                                                   \
+  k_wc_lattice_f32<D, R, MB, true><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,              \
+      (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
+      (double4*)s_out, (double4*)m_out, scalars, err)
 #define SPHB_F(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
-    if (D == 3 && minb32 == 6) SPHB_F1(D, R, 6);                                            \
+    if (ub) SPHB_FU(D, R, 4);                                                               \
+    else if (D == 3 && minb32 == 6) SPHB_F1(D, R, 6);                                       \
     else if (D == 3 && minb32 == 8) SPHB_F1(D, R, 8);                                       \
     else SPHB_F1(D, R, 4);                                                                  \
     SPHB_LAUNCH_CHECK();                                                                    \
@@ -912,5 +941,6 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   SPHB_LAT_CASES(SPHB_F)
 #undef SPHB_F
 #undef SPHB_F1
+#undef SPHB_FU
   return SPHB_ERR_ARG;
 }

@@ -603,6 +603,12 @@ typedef struct sphb_tl_lattice {
   double f[SPHB_TL_LATTICE_MAXW], df[SPHB_TL_LATTICE_MAXW];
   double dx[SPHB_TL_LATTICE_MAXW][3];   /* table geometry (table = 1)       */
   double g[SPHB_TL_LATTICE_MAXW][3];
+  /* 1 (3D table mode): every interior row's B0 record equals b0 (checked by
+   * sphb_tl_uniform_b0_check), so pass A takes B0 of its interior rows from
+   * b0 {b00, b01, b02, b11, b12, b22} instead of reading the records */
+  int32_t uniform_b0;
+  int32_t reserved_b0;
+  double b0[6];
 } sphb_tl_lattice;
 int sphb_tl_lattice_width(int32_t dim, int32_t r2);
 /* Interior rows whose pass-list row is not exactly the canonical set, whose
@@ -611,6 +617,12 @@ int sphb_tl_lattice_width(int32_t dim, int32_t r2);
 int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_lattice* L, const double* X0,
                           const int32_t* nbr, const int32_t* cnt, double tol,
                           unsigned long long* bad, void* stream);
+/* Counts into *bad (device, accumulated) the interior rows whose B0 record
+ * (3D two-plane layout) differs from b0 (device, 6 doubles) by more than
+ * tol * max|b0| in any entry (3D only). */
+int sphb_tl_uniform_b0_check(const sphb_tl_params* p, const sphb_tl_lattice* L,
+                             const double* B0, const double* b0, double tol,
+                             unsigned long long* bad, void* stream);
 /* Passes A / B (no kick) over the interior rows (lattice) and the shell
  * rows (general, pass list) in one launch each; same records and contract
  * as sphb_tl_pass_a / sphb_tl_pass_b. */

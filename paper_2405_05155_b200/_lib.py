@@ -192,6 +192,9 @@ class TLLattice(C.Structure):
         ("df", C.c_double * TL_LATTICE_MAXW),
         ("dx", (C.c_double * 3) * TL_LATTICE_MAXW),
         ("g", (C.c_double * 3) * TL_LATTICE_MAXW),
+        ("uniform_b0", C.c_int32),
+        ("reserved_b0", C.c_int32),
+        ("b0", C.c_double * 6),
     ]
 
 
@@ -235,6 +238,7 @@ SIGNATURES = {
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
     "sphb_wc_lattice_separable": (C.c_int, [I32, P]),
     "sphb_wc_uniform_b_check": (C.c_int, [P, P, P, F64, P, P]),
+    "sphb_tl_uniform_b0_check": (C.c_int, [P, P, P, P, F64, P, P]),
     "sphb_wc_stage_lattice": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_stage_lattice_f32": (C.c_int, [P, P, I32, P, P, P, P, P, P, P, P, P, P]),
     "sphb_wc_speed_max": (C.c_int, [P, P, P, P]),

@@ -391,16 +391,25 @@ __device__ __forceinline__ void stress_q(const sphb_tl_params& P, const double (
 // Pass A after the pair loop (tlsph.py:191-199, 54-65, 160-167): F_i += dt
 // (m B0_i), det F > 0, Q_i = (F S) B0^T with X0_i in the row padding (+ the
 // fused halo push), x_i += dt v_half_i.  m = sum_j (v_half_j - v_half_i) (x) g0_ij.
-template <int D>
+// UB0 (3D lattice interior rows with a uniform B0): B0 from bu (the
+// {b00, b01, b02, b11, b12, b22} of sphb_tl_lattice.b0) instead of the record
+template <int D, bool UB0 = false>
 __device__ __forceinline__ void tl_a_finish(const sphb_tl_params& P, int64_t i,
                                             const double (&m)[D][D], const double (&wi)[D],
                                             const double (&vhi)[D], double dt,
                                             const double4* __restrict__ B0,
                                             double4* __restrict__ F, double4* __restrict__ Q,
-                                            double4* __restrict__ XC, int32_t* __restrict__ err) {
+                                            double4* __restrict__ XC, int32_t* __restrict__ err,
+                                            const double* bu = nullptr) {
   const int64_t n = P.n;
   double B[D][D], Fi[D][D];
-  load_b0<D>(B0, n, i, B);
+  if constexpr (UB0 && D == 3) {
+    B[0][0] = bu[0]; B[0][1] = bu[1]; B[0][2] = bu[2];
+    B[1][0] = bu[1]; B[1][1] = bu[3]; B[1][2] = bu[4];
+    B[2][0] = bu[2]; B[2][1] = bu[4]; B[2][2] = bu[5];
+  } else {
+    load_b0<D>(B0, n, i, B);
+  }
   load_f<D>(F, n, i, Fi);
 #pragma unroll
   for (int a = 0; a < D; ++a)

@@ -291,7 +291,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <int D, int R2, int MINB, bool F32, bool TAB>
+template <int D, int R2, int MINB, bool F32, bool TAB, bool UB0 = false>
 __global__ void __launch_bounds__(kTT, MINB)
 k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
                const double4* __restrict__ X0, const double4* __restrict__ B0,
@@ -322,8 +322,10 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
     // shell rows' general pass B) is not needed: they read X0 themselves
     if constexpr (!F32 && D == 3) {
       const int64_t n = P.n;
-      prefetch_l2(B0 + i);
-      prefetch_l2(reinterpret_cast<const double2*>(B0 + n) + i);
+      if constexpr (!UB0) {
+        prefetch_l2(B0 + i);
+        prefetch_l2(reinterpret_cast<const double2*>(B0 + n) + i);
+      }
       prefetch_l2(F + i);
       prefetch_l2(F + n + i);
       prefetch_l2(reinterpret_cast<const double*>(F + 2 * n) + i);
@@ -369,7 +371,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
             }
         }
       });
-      tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+      tl_a_finish<D, UB0>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err, L.b0);
       return;
     }
     static_for<St::W>([&](auto kc) {
@@ -387,7 +389,7 @@ k_tl_lattice_a(const sphb_tl_params P, const sphb_tl_lattice L,
           if (o[b] != 0) m[a][b] = fma(dv, L.g[k][b], m[a][b]);
       }
     });
-    tl_a_finish<D>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err);
+    tl_a_finish<D, UB0>(P, i, m, wi, vhi, dt, B0, F, Q, XC, err, L.b0);
     return;
   }
   bool fixed_i;
@@ -903,6 +905,45 @@ extern "C" int sphb_tl_lattice_check(const sphb_tl_params* p, const sphb_tl_latt
   return SPHB_ERR_ARG;
 }
 
+template <int D, int R2>
+__global__ void k_tl_uniform_b0_check(const sphb_tl_lattice L, int64_t n,
+                                      const double4* __restrict__ B0,
+                                      const double* __restrict__ b0, double tol,
+                                      unsigned long long* bad) {
+  constexpr int R = isqrt_c(R2);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L.n_interior) return;
+  const Row<D, R> row(L, t);
+  const double4 q = B0[row.i];
+  const double2 u = reinterpret_cast<const double2*>(B0 + n)[row.i];
+  const double r[6] = {q.x, q.y, q.z, q.w, u.x, u.y};
+  double scale = 0.0;
+  for (int e = 0; e < 6; ++e) scale = fmax(scale, fabs(b0[e]));
+  bool ok = true;
+  for (int e = 0; e < 6; ++e) ok = ok && fabs(r[e] - b0[e]) <= tol * scale;
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+extern "C" int sphb_tl_uniform_b0_check(const sphb_tl_params* p, const sphb_tl_lattice* L,
+                                        const double* B0, const double* b0, double tol,
+                                        unsigned long long* bad, void* stream) {
+  if (!tl_lattice_ok(p, L) || p->dim != 3 || !B0 || !b0 || !bad || !(tol >= 0.0))
+    return SPHB_ERR_ARG;
+  if (L->n_interior == 0) return SPHB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = sphb_blocks(L->n_interior, 128);
+#define SPHB_U(D, R)                                                                        \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    k_tl_uniform_b0_check<D, R><<<grid, 128, 0, st>>>(*L, p->n, (const double4*)B0, b0, tol, \
+                                                       bad);                                \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
+  }
+  SPHB_U(3, 3) SPHB_U(3, 5)
+#undef SPHB_U
+  return SPHB_ERR_ARG;
+}
+
 // z-blocked pass B: rows per thread (SPHB_TL_PZ_B; 1 = the one-row kernel)
 // and occupancy target (SPHB_TL_ZMINB_B), instantiated as (R2, PZ, MINB);
 // defaults from scripts/ab_tl.sh (profiles/r02_tune_tl_zb.md)
@@ -935,6 +976,10 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   const bool f32 = p->vh32 && p->q32;
   const bool tab = L->table != 0;
   const int minb = minb_env ? minb_env : (tab ? 5 : 4);
+  // uniform B0 on the interior rows (table mode, 3D): SPHB_TL_UNIFORM_B0=0
+  // keeps the record reads (tuning)
+  static const int ub0_env = tl_minb("SPHB_TL_UNIFORM_B0", 1);
+  const bool ub0 = tab && L->uniform_b0 && ub0_env != 0;
   TabF32 G;
   for (int k = 0; k < L->width; ++k)
     for (int c = 0; c < 3; ++c) G.g[k][c] = (float)L->g[k][c];
@@ -943,6 +988,19 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
   k_tl_lattice_a<D, R, MB, F, T><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0,          \
       (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
       (double4*)q, scalars, err, G)
+#define SPHB_A3(D, R, MB, F)                                                                \
+  k_tl_lattice_a<D, R, MB, F, true, true><<<grid, kTT, 0, st>>>(*p, *L, (const double4*)x0, \
+      (const double4*)b0, nbr, cnt, (const double4*)vh, (double4*)xc, (double4*)f,          \
+      (double4*)q, scalars, err, G)
+  if (ub0 && p->dim == 3 && minb == 5 && (L->r2 == 3 || L->r2 == 5)) {
+    if (L->r2 == 3) {
+      if (f32) SPHB_A3(3, 3, 5, true); else SPHB_A3(3, 3, 5, false);
+    } else {
+      if (f32) SPHB_A3(3, 5, 5, true); else SPHB_A3(3, 5, 5, false);
+    }
+    SPHB_LAUNCH_CHECK();
+    return SPHB_OK;
+  }
 #define SPHB_A1(D, R, MB)                                                                   \
   if (f32) {                                                                                \
     if (tab) SPHB_A2(D, R, MB, true, true); else SPHB_A2(D, R, MB, true, false);            \
@@ -965,6 +1023,7 @@ extern "C" int sphb_tl_pass_a_lattice(const sphb_tl_params* p, const sphb_tl_lat
 #undef SPHB_A
 #undef SPHB_A1
 #undef SPHB_A2
+#undef SPHB_A3
   return SPHB_ERR_ARG;
 }
 

@@ -818,7 +818,7 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     const int64_t pfu =
         p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
     SPHB_U(3, 4, 3, 128) SPHB_U(3, 4, 4, 128) SPHB_U(3, 4, 5, 128)
-    SPHB_U(3, 6, 2, 128) SPHB_U(3, 6, 3, 128)
+    SPHB_U(3, 6, 2, 128) SPHB_U(3, 6, 3, 128) SPHB_U(3, 6, 4, 128)
     SPHB_U(2, 4, 5, 128) SPHB_U(2, 6, 5, 128)
 #undef SPHB_U
   }

@@ -491,7 +491,33 @@ class SolidSystem:
                 # table mode: dense 3D Q records (no X0 padding, 24-byte column
                 # gathers in pass B); every Q writer and reader honours the flag
                 self.params.q_dense = int(table == 1 and d == 3 and self._q_stride == n)
+                if table == 1 and d == 3:
+                    self._setup_uniform_b0(L, R, ext)
                 return
+
+    def _setup_uniform_b0(self, L, R, ext):
+        """Uniform B0 on the interior rows (table mode, 3D): every interior
+        row has the full canonical stencil, so its correction matrix B0
+        (tlsph.py:140-141) is the same matrix up to rounding; when every
+        interior record equals b0 (the first interior row's) to 1e-12 of
+        max|b0| (sphb_tl_uniform_b0_check), pass A takes B0 from b0 there
+        and reads no B0 records (48 of its streamed bytes per row).  The
+        shell rows keep their own records."""
+        if os.environ.get("SPHB_TL_UNIFORM_B0", "1") == "0":
+            return
+        torch = _lib.torch_cuda()
+        n = self.n
+        i0 = R + ext[0] * (R + ext[1] * R)
+        b0 = torch.cat([self.B0rec[:4 * n].view(n, 4)[i0],
+                        self.B0rec[4 * n:].view(n, 2)[i0]]).contiguous()
+        bad = torch.zeros(1, dtype=torch.int64, device=self._dev)
+        _lib.call("sphb_tl_uniform_b0_check", ctypes.byref(self.params), ctypes.byref(L),
+                  self.B0rec.data_ptr(), b0.data_ptr(), 1e-12, bad.data_ptr(),
+                  _lib.stream_ptr())
+        if int(bad.item()) == 0:
+            L.uniform_b0 = 1
+            for e, v in enumerate(b0.cpu().tolist()):
+                L.b0[e] = v
 
     def _pass_b(self, update_v):
         st = _lib.stream_ptr()

@@ -955,6 +955,8 @@ def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwa
     cfg = builder(kernel=key, **kwargs)
     fast = make_tl(cfg)
     assert fast.lattice is not None and fast._shell.numel() > 0
+    # 3D table mode: the interior rows' B0 is uniform (pass A reads b0)
+    assert fast.lattice.uniform_b0 == (1 if label == "c4" else 0)
     monkeypatch.setenv("SPHB_TL_LATTICE", "0")
     gen = make_tl(cfg)
     assert gen.lattice is None
@@ -975,6 +977,37 @@ def test_tl_lattice_path_taken_and_matches(monkeypatch, key, label, builder, kwa
     for s in (fast, gen):
         errs = (l2_error(s.x - s.X0, ref.x - ref.X0), l2_error(s.v, ref.v), l2_error(s.F, ref.F))
         assert max(errs) < 1e-10, errs
+
+
+@pytest.mark.parametrize("key", ["1.6h", "2h"])
+def test_tl_uniform_b0_matches_record_reads(monkeypatch, key):
+    """Pass A with B0 from the uniform b0 on the interior rows against the
+    same lattice passes reading every B0 record: equal to rounding after 40
+    steps; the check refuses a b0 that is off by 1e-9."""
+    import ctypes
+
+    import torch
+
+    from paper_2405_05155_b200 import _lib
+
+    cfg = configs.c4_column(kernel=key, n_width=8)
+    ub = make_tl(cfg)
+    monkeypatch.setenv("SPHB_TL_UNIFORM_B0", "0")
+    rec = make_tl(cfg)
+    assert ub.lattice.uniform_b0 == 1 and rec.lattice is not None and rec.lattice.uniform_b0 == 0
+    for s in (ub, rec):
+        s.step()
+        s.advance(39)
+    assert l2_error(ub.x - ub.X0, rec.x - rec.X0) < 1e-12
+    assert l2_error(ub.v, rec.v) < 1e-12
+    assert l2_error(ub.F, rec.F) < 1e-12
+    b0 = torch.tensor(list(ub.lattice.b0), dtype=torch.float64, device="cuda")
+    for scale, want_bad in ((1.0, False), (1.0 + 1e-9, True)):
+        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _lib.call("sphb_tl_uniform_b0_check", ctypes.byref(ub.params), ctypes.byref(ub.lattice),
+                  ub.B0rec.data_ptr(), (b0 * scale).data_ptr(), 1e-12, bad.data_ptr(),
+                  _lib.stream_ptr())
+        assert (int(bad.item()) > 0) == want_bad
 
 
 @pytest.mark.parametrize("key", ["1.6h", "2h"])

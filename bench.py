@@ -64,6 +64,9 @@ FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 73}
 # uniform-B form ((B_i + B_j) gg_k from the slot table): r2 = 4 838 DFMA +
 # 214 DMUL + 68 DADD / 32 slots, r2 = 6 2110 DFMA + 502 DMUL + 164 DADD / 80
 FLOPS_PER_PAIR_LATTICE_UB = {4: 61, 6: 61}
+# isotropic uniform-B form (b0 = beta I): r2 = 4 545 DFMA + 298 DMUL + 108
+# DADD / 32 slots, r2 = 6 1337 DFMA + 730 DMUL + 300 DADD / 80
+FLOPS_PER_PAIR_LATTICE_IB = {4: 47, 6: 46}
 
 
 def traffic_per_launch(kernel: str):
@@ -254,8 +257,10 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
             "SPHB_LAT_MINB", "3" if solver.lattice.r2 == 4 else "2"))
         if (solver.lattice.uniform_b and not os.environ.get("SPHB_LAT_MINB")
                 and not os.environ.get("SPHB_LAT_NT")):
-            kernel = "k_wc_lattice<3,%d,%s,uniform_b>" % (solver.lattice.r2, os.environ.get(
-                "SPHB_LAT_UB_MINB", "4" if solver.lattice.r2 == 4 else "3"))
+            form = ("isotropic_b" if solver.lattice_isotropic_b
+                    and os.environ.get("SPHB_LAT_IB", "1") != "0" else "uniform_b")
+            kernel = "k_wc_lattice<3,%d,%s,%s>" % (solver.lattice.r2, os.environ.get(
+                "SPHB_LAT_UB_MINB", "4" if solver.lattice.r2 == 4 else "3"), form)
         elif (solver.lattice.r2 == 6 and solver.lattice_separable
                 and os.environ.get("SPHB_LAT_ISO", "1") != "0"
                 and not os.environ.get("SPHB_LAT_MINB") and not os.environ.get("SPHB_LAT_NT")):
@@ -659,6 +664,8 @@ def main():
         if sv.lattice.uniform_b:
             design_bytes = sv.n * LATTICE_UB_RECORD_BYTES
             flops_pair = FLOPS_PER_PAIR_LATTICE_UB[sv.lattice.r2]
+            if sv.lattice_isotropic_b and os.environ.get("SPHB_LAT_IB", "1") != "0":
+                flops_pair = FLOPS_PER_PAIR_LATTICE_IB[sv.lattice.r2]
     del leg["1.6h"]["solver"], sv
     torch.cuda.empty_cache()
     if not args.no_2h:

@@ -320,6 +320,11 @@ int sphb_lattice_offsets(int32_t dim, int32_t r2, int32_t* off);
 int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L, const double* X,
                           const int32_t* nbr, const int32_t* cnt, double tol,
                           unsigned long long* bad, void* stream);
+/* 1 when L->uniform_b and b0 = beta I to 1e-12 of max|b0| (cubic / square
+ * lattices): sphb_wc_stage_lattice then runs its isotropic uniform-B form
+ * ((B_i + B_j) gg_k = lam_k ee_k, the star-state algebra folded onto ee_k);
+ * 0 otherwise; SPHB_ERR_ARG on a bad table. */
+int sphb_wc_lattice_isotropic_b(int32_t dim, const sphb_lattice* L);
 /* Counts into *bad (device, accumulated) the records i in [0, p->n) whose
  * symmetrised B (the two-plane layout of sphb_wc_stage) differs from b0
  * (device, 6 doubles in the order of sphb_lattice.b0) by more than

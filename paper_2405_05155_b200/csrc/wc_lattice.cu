@@ -105,6 +105,16 @@ struct LatFold {
   // (B_i + B_j) gg_k = 2 b0 gg_k is one vector per slot: no B gathers, no
   // B_i + B_j, no B gg products in the pair loop
   double gb[SPHB_LATTICE_MAXW][3];
+  // isotropic uniform-B form (IB): b0 = beta I as well (a cubic or square
+  // lattice), so Gg_k = lam_k ee_k: with A = v_i . ee_k and Bv = v_j . ee_k,
+  //   x = Bv - A, vs . Gg = lam_k (0.5 (A + Bv) - wq |ee_k|^2),
+  //   rs2 vs - mv v_j + p* Gg = (rs2 / 2 - mv) v_j + rs2 hv_i
+  //                             + (p* lam_k - rs2 wq) ee_k,
+  // and sum_k rs2 hv_i = hv_i drho is added once per row.  hl = lam / 2,
+  // e2 = 2 |ee_k|^2
+  double lam[SPHB_LATTICE_MAXW];
+  double hl[SPHB_LATTICE_MAXW];
+  double e2[SPHB_LATTICE_MAXW];
 };
 
 // wrapped lattice coordinate c + s in [0, n)
@@ -235,7 +245,48 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
     r.dm[q] = fma(-L.mv[k], vj[q], fma(pg, Gg[q], fma(rs2, vs[q], r.dm[q])));
 }
 
-template <int D, int R2, int MINB, int NT = kLT, bool ISO = false, bool UB = false>
+// One directed pair in the isotropic uniform-B form (see LatFold): 22 + 3m
+// FP64 instructions for an offset with m nonzero components (the uniform-B
+// form: 27 + 3m).
+template <int D, int R2, int k>
+__device__ __forceinline__ void lat_pair_ib(const LatFold& L, const LatConst& K, LatRow<D>& r,
+                                            const double (&vj)[D], double rho_j) {
+  using St = Stencil<D, R2>;
+  constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+  double A = 0.0, Bv = 0.0;
+  bool first = true;
+#pragma unroll
+  for (int q = 0; q < D; ++q)
+    if (o[q] != 0) {
+      A = first ? r.vi[q] * L.ee[k][q] : fma(r.vi[q], L.ee[k][q], A);
+      Bv = first ? vj[q] * L.ee[k][q] : fma(vj[q], L.ee[k][q], Bv);
+      first = false;
+    }
+  const double x = Bv - A;                          // (u_l - u_r) eta / c
+  const int hx = __double2hiint(x);
+  double beta = hx < 0 ? 0.0 : x;
+  beta = hx >= 0x3FF00000 ? 1.0 : beta;
+  const double rbar = fma(0.5, rho_j, r.hrho_i);
+  const double bk = beta * K.kappa;
+  const double pg = fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
+  double rr;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(rbar));
+  rr = fma(rr, fma(-rbar, rr, 1.0), rr);
+  const double wq = ((beta * bk) * (r.rho_i - rho_j)) * rr;
+  const double sg2 = fma(-wq, L.e2[k], A + Bv);    // 2 vs . ee
+  const double rs2 = (rbar * L.hl[k]) * sg2;        // -2 rbar s
+  r.dr += rs2;
+  const double c1 = fma(0.5, rs2, -L.mv[k]);
+  const double ce = fma(pg, L.lam[k], -(rs2 * wq));
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    r.dm[q] = fma(c1, vj[q], r.dm[q]);
+    if (o[q] != 0) r.dm[q] = fma(ce, L.ee[k][q], r.dm[q]);
+  }
+}
+
+template <int D, int R2, int MINB, int NT = kLT, bool ISO = false, bool UB = false,
+          bool IB = false>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -255,7 +306,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
   if (pf > 0 && i0 + pf < n) {
     const int64_t ip = i0 + pf;
     prefetch_l2(S_in + ip);
-    if constexpr (!UB) {
+    if constexpr (!UB && !IB) {
       prefetch_l2(reinterpret_cast<const double4*>(B) + ip);
       prefetch_l2(reinterpret_cast<const double2*>(B + 4 * n) + ip);
     }
@@ -279,17 +330,25 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
   }
 
   LatRow<D> row;
-  row.template load<UB>(B, S_in, n, i);
+  row.template load<UB || IB>(B, S_in, n, i);
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
     const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
     double vj[D], rho_j;
     unpack_s<D>(ldg4(S_in + j), vj, rho_j);
-    Sym<D> Bj;
-    if constexpr (!UB) Bj.load(B, n, j);
-    lat_pair<D, R2, k, ISO, UB>(L, K, row, vj, rho_j, Bj);
+    if constexpr (IB) {
+      lat_pair_ib<D, R2, k>(L, K, row, vj, rho_j);
+    } else {
+      Sym<D> Bj;
+      if constexpr (!UB) Bj.load(B, n, j);
+      lat_pair<D, R2, k, ISO, UB>(L, K, row, vj, rho_j, Bj);
+    }
   });
+  if constexpr (IB) {   // sum_k rs2 hv_i
+#pragma unroll
+    for (int q = 0; q < D; ++q) row.dm[q] = fma(row.hvi[q], row.dr, row.dm[q]);
+  }
 #pragma unroll
   for (int q = 0; q < D; ++q) row.dm[q] = fma(K.mv_sum, row.vi[q], row.dm[q]);
 
@@ -679,9 +738,42 @@ static bool lattice_separable(int dim, const sphb_lattice* L, LatFold* F, double
   return true;
 }
 
+// Isotropic uniform B: b0 = beta I to 1e-12 of max|b0| (a cubic or square
+// lattice).  Fills the IB tables of F (needs F->ee) when F is given.
+static bool lattice_isotropic_b(int dim, double c_art, const sphb_lattice* L, LatFold* F) {
+  if (!L->uniform_b || dim < 2 || dim > 3) return false;
+  const int ne = dim == 3 ? 6 : 3;
+  const bool diag3[6] = {true, false, false, true, false, true};
+  const bool diag2[3] = {true, false, true};
+  double scale = 0.0;
+  for (int e = 0; e < ne; ++e) scale = fmax(scale, fabs(L->b0[e]));
+  const double beta = L->b0[0];
+  if (!(scale > 0.0)) return false;
+  for (int e = 0; e < ne; ++e) {
+    const double want = (dim == 3 ? diag3[e] : diag2[e]) ? beta : 0.0;
+    if (fabs(L->b0[e] - want) > 1e-12 * scale) return false;
+  }
+  if (F) {
+    const double eta_c = kEtaLinearized / c_art;
+    for (int k = 0; k < L->width; ++k) {
+      F->lam[k] = 2.0 * beta * L->g2[k] / (L->inv_r[k] * eta_c);
+      F->hl[k] = 0.5 * F->lam[k];
+      double e2 = 0.0;
+      for (int q = 0; q < 3; ++q) e2 += F->ee[k][q] * F->ee[k][q];
+      F->e2[k] = 2.0 * e2;
+    }
+  }
+  return true;
+}
+
 extern "C" int sphb_wc_lattice_separable(int32_t dim, const sphb_lattice* L) {
   if (!L || sphb_lattice_width(dim, L->r2) != L->width) return SPHB_ERR_ARG;
   return lattice_separable(dim, L, nullptr, 0.0) ? 1 : 0;
+}
+
+extern "C" int sphb_wc_lattice_isotropic_b(int32_t dim, const sphb_lattice* L) {
+  if (!L || sphb_lattice_width(dim, L->r2) != L->width) return SPHB_ERR_ARG;
+  return lattice_isotropic_b(dim, 1.0, L, nullptr) ? 1 : 0;
 }
 
 extern "C" int sphb_wc_lattice_check(const sphb_wc_params* p, const sphb_lattice* L,
@@ -760,6 +852,13 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
         F.gb[k][a] = acc;
       }
   }
+  // isotropic b0 (beta I to 1e-12 of max|b0|): the IB form; SPHB_LAT_IB=0
+  // keeps the uniform-B form (tuning)
+  static const int ib_env = [] {
+    const char* e = getenv("SPHB_LAT_IB");
+    return e ? atoi(e) : 1;
+  }();
+  const bool ib = ub && ib_env && lattice_isotropic_b(p->dim, p->c_art, L, &F);
   static const int ubminb_env = [] {       // SPHB_LAT_UB_MINB (tuning)
     const char* e = getenv("SPHB_LAT_UB_MINB");
     return e ? atoi(e) : 0;
@@ -805,6 +904,22 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
+  }
+  if (ib && !minb_env && !nt_env) {
+#define SPHB_IB(D, R, MB, NT)                                                                \
+    if (p->dim == D && L->r2 == R && umb == MB) {                                            \
+      k_wc_lattice<D, R, MB, NT, false, true, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>( \
+          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pfu);                   \
+      SPHB_LAUNCH_CHECK();                                                                   \
+      return SPHB_OK;                                                                        \
+    }
+    const int umb = ubminb_env ? ubminb_env : (p->dim == 3 ? (L->r2 == 4 ? 4 : 3) : 5);
+    const int64_t pfu =
+        p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
+    SPHB_IB(3, 4, 3, 128) SPHB_IB(3, 4, 4, 128) SPHB_IB(3, 4, 5, 128)
+    SPHB_IB(3, 6, 3, 128) SPHB_IB(3, 6, 4, 128)
+    SPHB_IB(2, 4, 5, 128) SPHB_IB(2, 6, 5, 128)
+#undef SPHB_IB
   }
   if (ub && !minb_env && !nt_env) {
 #define SPHB_U(D, R, MB, NT)                                                                 \

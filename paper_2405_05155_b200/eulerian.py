@@ -455,6 +455,7 @@ class EulerianSolver:
         p.vol_const = float(vol[0]) if self.n else 0.0
         self.lattice = None
         self.lattice_separable = False
+        self.lattice_isotropic_b = False
         if (variant == "global" and not self._ideal and ghosts is None
                 and wall_force_tag is None and uniform and self.order is not self.bins
                 and os.environ.get("SPHB_WC_LATTICE", "1") != "0"):
@@ -592,6 +593,10 @@ class EulerianSolver:
             self.lattice.uniform_b = 1
             for e, v in enumerate(b0.cpu().tolist()):
                 self.lattice.b0[e] = v
+            # b0 = beta I as well (cubic / square lattice): isotropic form
+            lib = _lib.lib()
+            self.lattice_isotropic_b = int(lib.sphb_wc_lattice_isotropic_b(
+                self.dim, ctypes.byref(self.lattice))) == 1
 
     def __new__(cls, *args, **kwargs):
         eos = kwargs.get("eos", args[3] if len(args) > 3 else None)

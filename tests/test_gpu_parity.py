@@ -875,6 +875,8 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
     assert fast.lattice_separable
     # ... and every correction matrix equals b0 to rounding: uniform-B form
     assert fast.lattice.uniform_b == 1
+    # ... and b0 = beta I (cubic / square lattice): isotropic uniform-B form
+    assert fast.lattice_isotropic_b
     monkeypatch.setenv("SPHB_WC_LATTICE", "0")
     gen = make_wc(cfg)
     assert gen.lattice is None
@@ -1164,6 +1166,51 @@ def test_tl_zblocked_pass_b_is_bitwise_the_one_row_kernel(tmp_path):
         files[pz] = np.load(f)
     for k in files["1"].files:
         assert np.array_equal(files["8"][k], files["1"][k]), k
+
+
+_IB_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2405_05155_b200 import configs
+from paper_2405_05155_b200.eulerian import EulerianSolver, EosParams, FluidState, WEAKLY_COMPRESSIBLE
+out = {}
+for key in ("1.6h", "2h"):
+    cfg = configs.c5_tgv3d(kernel=key, n_side=16)
+    n = cfg["pos"].shape[0]
+    st = FluidState(cfg["vol"].copy(), cfg["rho"].copy(), cfg["mom"].copy(), None, n)
+    s = EulerianSolver(cfg["pos"], n, st, EosParams(WEAKLY_COMPRESSIBLE, rho0=1.0, c_art=cfg["c_art"]),
+                       cfg["spec"], None, cfl=cfg["cfl"], mu=cfg["mu"], periodic_box=cfg["box"])
+    assert s.lattice is not None and s.lattice.uniform_b == 1
+    s.step()
+    s.advance(19)
+    out[key + "_rho"] = s.state.rho
+    out[key + "_mom"] = s.state.mom
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_wc_isotropic_b_form_matches_uniform_b_form(tmp_path):
+    """The isotropic uniform-B pair form (b0 = beta I, so (B_i + B_j) gg_k =
+    lam_k ee_k and the star-state algebra folds onto the ee_k axis;
+    csrc/wc_lattice.cu lat_pair_ib) against the uniform-B form
+    (SPHB_LAT_IB=0, read once per process, hence the subprocesses): equal
+    to rounding after 20 steps at 1.6h and 2h."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    files = {}
+    for ib in ("1", "0"):
+        f = str(tmp_path / f"ib{ib}.npz")
+        env = dict(os.environ, SPHB_LAT_IB=ib)
+        subprocess.run([sys.executable, "-c", _IB_SCRIPT, root, f], env=env, check=True,
+                       timeout=600)
+        files[ib] = np.load(f)
+    for key in ("1.6h", "2h"):
+        a, b = files["1"], files["0"]
+        assert l2_error(a[key + "_rho"] - 1.0, b[key + "_rho"] - 1.0) < 1e-12
+        assert l2_error(a[key + "_mom"], b[key + "_mom"]) < 1e-12
 
 
 @pytest.mark.parametrize("dims", [(20, 12, 16), (14, 24)])

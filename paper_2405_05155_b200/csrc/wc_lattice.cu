@@ -442,10 +442,13 @@ struct LatF32 {
   float dx[SPHB_LATTICE_MAXW][3];
   float inv_r[SPHB_LATTICE_MAXW], g2[SPHB_LATTICE_MAXW], mv[SPHB_LATTICE_MAXW];
   float gb[SPHB_LATTICE_MAXW][3];   // uniform-B form: 2 b0 dx_k (LatFold::gb)
+  // isotropic uniform-B form (LatFold::lam / hl / e2, ee = dx inv_r eta_c)
+  float ee[SPHB_LATTICE_MAXW][3];
+  float lam[SPHB_LATTICE_MAXW], hl[SPHB_LATTICE_MAXW], e2[SPHB_LATTICE_MAXW];
 };
 
 struct LatConstF32 {
-  float c, c2, eta_c, half_cinv, rho0;
+  float c, c2, eta_c, half_cinv, rho0, kappa;
 };
 
 constexpr int kFlush = 8;
@@ -477,7 +480,7 @@ struct SymF<3> {
   }
 };
 
-template <int D, int R2, int MINB = 4, bool UB = false>
+template <int D, int R2, int MINB = 4, bool UB = false, bool IB = false>
 __global__ void __launch_bounds__(kLT, MINB)
 k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, const int stage,
                  const float* __restrict__ B, const float4* __restrict__ S32_in,
@@ -506,6 +509,7 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
   const float vi[3] = {si.x, si.y, si.z};
   const float drho_i = D == 3 ? si.w : si.z;
   const float p_i = K.c2 * drho_i;
+  const float hdi = 0.5f * drho_i;
   float hvi[D];
 #pragma unroll
   for (int q = 0; q < D; ++q) hvi[q] = 0.5f * vi[q];
@@ -525,6 +529,39 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
     const float4 sj = __ldg(S32_in + j);
     const float vj[3] = {sj.x, sj.y, sj.z};
     const float drho_j = D == 3 ? sj.w : sj.z;
+    if constexpr (IB) {
+      // isotropic uniform-B form in FP32 (lat_pair_ib): p* = rbar bk x +
+      // c^2 (rbar - rho0), wq = beta bk (rho_i - rho_j) / rbar
+      float A = 0.f, Bv = 0.f;
+      bool first = true;
+#pragma unroll
+      for (int q = 0; q < D; ++q)
+        if (o[q] != 0) {
+          A = first ? vi[q] * L.ee[k][q] : fmaf(vi[q], L.ee[k][q], A);
+          Bv = first ? vj[q] * L.ee[k][q] : fmaf(vj[q], L.ee[k][q], Bv);
+          first = false;
+        }
+      const float x = Bv - A;
+      const float beta = fminf(fmaxf(x, 0.f), 1.f);
+      const float hd = fmaf(0.5f, drho_j, hdi);
+      const float rbar = K.rho0 + hd;
+      const float bk = beta * K.kappa;
+      const float pg = fmaf(rbar * bk, x, K.c2 * hd);
+      const float wq = (beta * bk) * (drho_i - drho_j) * __fdividef(1.0f, rbar);
+      const float sg2 = fmaf(-wq, L.e2[k], A + Bv);
+      const float rs2 = (rbar * L.hl[k]) * sg2;
+      fr += rs2;
+      // rs2 vs - mv (v_j - v_i) = (rs2 / 2 - mv)(v_j - v_i) + rs2 v_i - rs2 wq ee:
+      // the differences keep the FP32 viscous sum free of cancellation, and
+      // sum_k rs2 v_i = v_i drho is added once per row in FP64
+      const float c1 = fmaf(0.5f, rs2, -L.mv[k]);
+      const float ce = fmaf(pg, L.lam[k], -(rs2 * wq));
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        fm[q] = fmaf(c1, vj[q] - vi[q], fm[q]);
+        if (o[q] != 0) fm[q] = fmaf(ce, L.ee[k][q], fm[q]);
+      }
+    } else {
     SymF<D> Bj;
     if constexpr (!UB) Bj.load(B, n, j);
     float dx[D];
@@ -573,6 +610,7 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
     fr += rs2;
 #pragma unroll
     for (int q = 0; q < D; ++q) fm[q] += fmaf(-L.mv[k], dv[q], fmaf(pg, G_[q], rs2 * vs[q]));
+    }
     if constexpr ((k + 1) % kFlush == 0 || k + 1 == St::W) {
       dr += (double)fr;
       fr = 0.f;
@@ -584,6 +622,10 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
     }
   });
 
+  if constexpr (IB) {   // sum_k rs2 v_i, once per row
+#pragma unroll
+    for (int q = 0; q < D; ++q) dm[q] = fma((double)vi[q], dr, dm[q]);
+  }
   // epilogue (as wc_f32.cu): FP64 update, FP32 companion record
   double speed = 0.0;
   int32_t flags = 0;
@@ -1025,7 +1067,30 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
         T.gb[k][a] = (float)acc;
       }
   }
+  // isotropic uniform-B form (the FP64 launcher's test, FP32 tables)
+  static const int ib32_env = [] {
+    const char* e = getenv("SPHB_LAT_IB");
+    return e ? atoi(e) : 1;
+  }();
+  const bool ib = ub && ib32_env && lattice_isotropic_b(p->dim, p->c_art, L, nullptr);
+  if (ib) {
+    const double eta_c = kEtaLinearized / p->c_art;
+    const double beta = L->b0[0];
+    for (int k = 0; k < L->width; ++k) {
+      double e2 = 0.0;
+      for (int q = 0; q < 3; ++q) {
+        const double e = L->dx[k][q] * L->inv_r[k] * eta_c;
+        T.ee[k][q] = (float)e;
+        e2 += e * e;
+      }
+      const double lam = 2.0 * beta * L->g2[k] / (L->inv_r[k] * eta_c);
+      T.lam[k] = (float)lam;
+      T.hl[k] = (float)(0.5 * lam);
+      T.e2[k] = (float)(2.0 * e2);
+    }
+  }
   LatConstF32 K;
+  K.kappa = (float)(0.5 * p->c_art / (kEtaLinearized / p->c_art));
   K.c = (float)p->c_art;
   K.c2 = K.c * K.c;
   K.eta_c = (float)(kEtaLinearized / p->c_art);
@@ -1044,9 +1109,14 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   k_wc_lattice_f32<D, R, MB, true><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,              \
       (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
       (double4*)s_out, (double4*)m_out, scalars, err)
+#define SPHB_FI(D, R, MB)                                                                   \
+  k_wc_lattice_f32<D, R, MB, true, true><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,        \
+      (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
+      (double4*)s_out, (double4*)m_out, scalars, err)
 #define SPHB_F(D, R)                                                                        \
   if (p->dim == D && L->r2 == R) {                                                          \
-    if (ub) SPHB_FU(D, R, 4);                                                               \
+    if (ib) SPHB_FI(D, R, 4);                                                               \
+    else if (ub) SPHB_FU(D, R, 4);                                                          \
     else if (D == 3 && minb32 == 6) SPHB_F1(D, R, 6);                                       \
     else if (D == 3 && minb32 == 8) SPHB_F1(D, R, 8);                                       \
     else SPHB_F1(D, R, 4);                                                                  \
@@ -1057,5 +1127,6 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
 #undef SPHB_F
 #undef SPHB_F1
 #undef SPHB_FU
+#undef SPHB_FI
   return SPHB_ERR_ARG;
 }

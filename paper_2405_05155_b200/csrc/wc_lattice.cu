@@ -248,17 +248,21 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
 // One directed pair in the isotropic uniform-B form (see LatFold): 22 + 3m
 // FP64 instructions for an offset with m nonzero components (the uniform-B
 // form: 27 + 3m).
-template <int D, int R2, int k>
+// MIRROR: slot k is the mirror of a slot whose A = v_i . ee was just
+// computed (canonical order: slot W-1-k holds -o_k and the table is exactly
+// antisymmetric, so A_k = -A_mirror bit for bit); A is in/out.
+template <int D, int R2, int k, bool MIRROR = false>
 __device__ __forceinline__ void lat_pair_ib(const LatFold& L, const LatConst& K, LatRow<D>& r,
-                                            const double (&vj)[D], double rho_j) {
+                                            const double (&vj)[D], double rho_j, double& A) {
   using St = Stencil<D, R2>;
   constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-  double A = 0.0, Bv = 0.0;
+  double Bv = 0.0;
+  if constexpr (MIRROR) A = -A;
   bool first = true;
 #pragma unroll
   for (int q = 0; q < D; ++q)
     if (o[q] != 0) {
-      A = first ? r.vi[q] * L.ee[k][q] : fma(r.vi[q], L.ee[k][q], A);
+      if constexpr (!MIRROR) A = first ? r.vi[q] * L.ee[k][q] : fma(r.vi[q], L.ee[k][q], A);
       Bv = first ? vj[q] * L.ee[k][q] : fma(vj[q], L.ee[k][q], Bv);
       first = false;
     }
@@ -286,7 +290,7 @@ __device__ __forceinline__ void lat_pair_ib(const LatFold& L, const LatConst& K,
 }
 
 template <int D, int R2, int MINB, int NT = kLT, bool ISO = false, bool UB = false,
-          bool IB = false>
+          bool IB = false, bool MO = false>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -331,6 +335,24 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
 
   LatRow<D> row;
   row.template load<UB || IB>(B, S_in, n, i);
+  if constexpr (IB && MO) {
+    // mirror order: slot k then its mirror W-1-k, which reuses A = v_i . ee_k
+    // negated (one row's slots summed in this order instead of the
+    // canonical one)
+    static_for<St::W / 2>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int km = St::W - 1 - k;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
+      const int64_t jm = (int64_t)(xs[R - o[0]] + ys[R - o[1]] + zs[R - o[2]]);
+      double vj[D], rho_j, vm[D], rho_m;
+      unpack_s<D>(ldg4(S_in + j), vj, rho_j);
+      unpack_s<D>(ldg4(S_in + jm), vm, rho_m);
+      double A;
+      lat_pair_ib<D, R2, k>(L, K, row, vj, rho_j, A);
+      lat_pair_ib<D, R2, km, true>(L, K, row, vm, rho_m, A);
+    });
+  } else
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
@@ -338,7 +360,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     double vj[D], rho_j;
     unpack_s<D>(ldg4(S_in + j), vj, rho_j);
     if constexpr (IB) {
-      lat_pair_ib<D, R2, k>(L, K, row, vj, rho_j);
+      double A;
+      lat_pair_ib<D, R2, k>(L, K, row, vj, rho_j, A);
     } else {
       Sym<D> Bj;
       if constexpr (!UB) Bj.load(B, n, j);
@@ -947,19 +970,28 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
   }
+  static const int mo_env = [] {             // SPHB_LAT_MIRROR=0: canonical order
+    const char* e = getenv("SPHB_LAT_MIRROR");
+    return e ? atoi(e) : 1;
+  }();
   if (ib && !minb_env && !nt_env) {
 #define SPHB_IB(D, R, MB, NT)                                                                \
     if (p->dim == D && L->r2 == R && umb == MB) {                                            \
-      k_wc_lattice<D, R, MB, NT, false, true, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>( \
-          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pfu);                   \
+      if (mo_env)                                                                            \
+        k_wc_lattice<D, R, MB, NT, false, true, true, true>                                  \
+            <<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, \
+                                                       Mout, scalars, err, pfu);             \
+      else                                                                                   \
+        k_wc_lattice<D, R, MB, NT, false, true, true, false>                                 \
+            <<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, \
+                                                       Mout, scalars, err, pfu);             \
       SPHB_LAUNCH_CHECK();                                                                   \
       return SPHB_OK;                                                                        \
     }
     const int umb = ubminb_env ? ubminb_env : (p->dim == 3 ? (L->r2 == 4 ? 4 : 3) : 5);
     const int64_t pfu =
         p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
-    SPHB_IB(3, 4, 3, 128) SPHB_IB(3, 4, 4, 128) SPHB_IB(3, 4, 5, 128)
-    SPHB_IB(3, 6, 3, 128) SPHB_IB(3, 6, 4, 128)
+    SPHB_IB(3, 4, 3, 128) SPHB_IB(3, 4, 4, 128) SPHB_IB(3, 6, 3, 128)
     SPHB_IB(2, 4, 5, 128) SPHB_IB(2, 6, 5, 128)
 #undef SPHB_IB
   }

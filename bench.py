@@ -58,15 +58,14 @@ FLOPS_PER_PAIR_EST = 117
 # lattice kernel (wc_lattice.cu), FP64 flops per pair from its SASS
 # (DFMA = 2): r2 = 4 stencil (919 DFMA + 308 DMUL + 212 DADD) / 32 slots,
 # r2 = 6 stencil (2409 DFMA + 741 DMUL + 572 DADD) / 80 slots (round 2,
-# folded slot table; profiles/r02_ncu_c5_256.md); the r2 = 6 stencil runs
-# the separable-slot form, 2278 DFMA + 582 DMUL + 704 DADD = 73 per pair
-FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 73}
+# folded slot table; profiles/r02_ncu_c5_256.md)
+FLOPS_PER_PAIR_LATTICE = {4: 74, 6: 77}
 # uniform-B form ((B_i + B_j) gg_k from the slot table): r2 = 4 838 DFMA +
 # 214 DMUL + 68 DADD / 32 slots, r2 = 6 2110 DFMA + 502 DMUL + 164 DADD / 80
 FLOPS_PER_PAIR_LATTICE_UB = {4: 61, 6: 61}
-# isotropic uniform-B form (b0 = beta I): r2 = 4 545 DFMA + 298 DMUL + 108
-# DADD / 32 slots, r2 = 6 1337 DFMA + 730 DMUL + 300 DADD / 80
-FLOPS_PER_PAIR_LATTICE_IB = {4: 47, 6: 46}
+# isotropic uniform-B form (b0 = beta I), mirror order: r2 = 4 531 DFMA +
+# 282 DMUL + 108 DADD / 32 slots, r2 = 6 1287 DFMA + 690 DMUL + 300 DADD / 80
+FLOPS_PER_PAIR_LATTICE_IB = {4: 45, 6: 45}
 
 
 def traffic_per_launch(kernel: str):
@@ -253,18 +252,13 @@ def run_leg(torch, cfg, steps, warmup, dist, world, clocks_index=None):
               "global": "k_wc_stage<3,%d,%s>" % (solver.group,
                                                  os.environ.get("SPHB_WC_MINB", "5"))}[solver.variant]
     if solver.lattice is not None:
-        kernel = "k_wc_lattice<3,%d,%s>" % (solver.lattice.r2, os.environ.get(
-            "SPHB_LAT_MINB", "3" if solver.lattice.r2 == 4 else "2"))
-        if (solver.lattice.uniform_b and not os.environ.get("SPHB_LAT_MINB")
-                and not os.environ.get("SPHB_LAT_NT")):
+        r4 = solver.lattice.r2 == 4
+        kernel = "k_wc_lattice<3,%d,%s>" % (solver.lattice.r2, "3" if r4 else "2,256")
+        if solver.lattice.uniform_b:
             form = ("isotropic_b" if solver.lattice_isotropic_b
                     and os.environ.get("SPHB_LAT_IB", "1") != "0" else "uniform_b")
-            kernel = "k_wc_lattice<3,%d,%s,%s>" % (solver.lattice.r2, os.environ.get(
-                "SPHB_LAT_UB_MINB", "4" if solver.lattice.r2 == 4 else "3"), form)
-        elif (solver.lattice.r2 == 6 and solver.lattice_separable
-                and os.environ.get("SPHB_LAT_ISO", "1") != "0"
-                and not os.environ.get("SPHB_LAT_MINB") and not os.environ.get("SPHB_LAT_NT")):
-            kernel = "k_wc_lattice<3,6,2,256,separable>"
+            kernel = "k_wc_lattice<3,%d,%s,%s>" % (solver.lattice.r2, "4" if r4 else "3", form)
+
     return {"solver": solver, "n": n, "pairs": pairs, "ms": ms, "stage_ms": st, "kernel": kernel,
             "clocks": sampler.summary() if sampler else None,
             "launches_per_step": launches_per_step}

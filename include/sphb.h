@@ -332,11 +332,6 @@ int sphb_wc_lattice_isotropic_b(int32_t dim, const sphb_lattice* L);
  * that tolerance. */
 int sphb_wc_uniform_b_check(const sphb_wc_params* p, const double* B, const double* b0,
                             double tol, unsigned long long* bad, void* stream);
-/* 1 when every slot's table displacement is sp_k o_k (one spacing per slot,
- * o_k the integer offset): sphb_wc_stage_lattice then runs its separable-slot
- * form ((B_i + B_j) gg as integer-coefficient sums times one factor per
- * slot); 0 otherwise; SPHB_ERR_ARG on a bad table. */
-int sphb_wc_lattice_separable(int32_t dim, const sphb_lattice* L);
 /* The stage of sphb_wc_stage on a checked lattice (uniform volumes; no
  * ghosts, no wall tags): same stage / record / scalar / error contract. */
 int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice* L, int32_t stage,

@@ -236,7 +236,6 @@ SIGNATURES = {
     "sphb_tl_pass_b_lattice": (C.c_int, [P, P, P, P, P, P, P, P, P, P, I32, P, P]),
     "sphb_lattice_offsets": (C.c_int, [I32, I32, P]),
     "sphb_wc_lattice_check": (C.c_int, [P, P, P, P, P, F64, P, P]),
-    "sphb_wc_lattice_separable": (C.c_int, [I32, P]),
     "sphb_wc_lattice_isotropic_b": (C.c_int, [I32, P]),
     "sphb_wc_uniform_b_check": (C.c_int, [P, P, P, F64, P, P]),
     "sphb_tl_uniform_b0_check": (C.c_int, [P, P, P, P, F64, P, P]),

@@ -92,14 +92,6 @@ struct LatFold {
   double ee[SPHB_LATTICE_MAXW][3];
   double gg[SPHB_LATTICE_MAXW][3];
   double mv[SPHB_LATTICE_MAXW];
-  // separable-slot form (ISO): when every slot's table displacement is
-  // dx_k = sp_k o_k (one spacing per slot, o_k the integer offset),
-  // gg_k = gs_k o_k / m_k with m_k = |first nonzero o_k| and gs_k = g2_k sp_k m_k,
-  // so (B_i + B_j) gg = gs_k (B_i + B_j) (o_k / m_k): the integer-coefficient
-  // combination is DADDs (no DMUL for one-axis slots) and gs_k folds into
-  // rbar once per pair; cg_k = c^2 rho0 gs_k
-  double gs[SPHB_LATTICE_MAXW];
-  double cg[SPHB_LATTICE_MAXW];
   // uniform-B form (UB): every record's B equals b0 within the check's
   // tolerance (a lattice's correction matrices differ by rounding only), so
   // (B_i + B_j) gg_k = 2 b0 gg_k is one vector per slot: no B gathers, no
@@ -155,18 +147,15 @@ struct LatRow {
 //   vs = vbar - beta^2 kappa (rho_i - rho_j) / rbar ee,
 //   drho += rbar vs . (B_i + B_j) gg,
 //   dmom += rbar (vs . Gg) vs + p* Gg - mv v_j (+ sum(mv) v_i once)
-template <int D, int R2, int k, bool ISO, bool UB = false>
+template <int D, int R2, int k, bool UB = false>
 __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, LatRow<D>& r,
                                          const double (&vj)[D], double rho_j,
                                          const Sym<D>& Bj) {
   using St = Stencil<D, R2>;
   constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-  // first nonzero component and its magnitude (ISO form)
-  constexpr int q0 = o[0] != 0 ? 0 : (o[1] != 0 ? 1 : 2);
-  constexpr int m0 = o[q0] < 0 ? -o[q0] : o[q0];
   // components with o_q = 0 are zero (checked within tol): compile-time
   // zeros, so B gg, (v_j - v_i).ee and the limiter term lose them
-  double Gg[D];          // (B_i + B_j) gg, nonzero columns (ISO: / gs_k)
+  double Gg[D];          // (B_i + B_j) gg, nonzero columns
   Sym<D> Bs;
   if constexpr (UB) {
 #pragma unroll
@@ -181,19 +170,7 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
 #pragma unroll
     for (int q = 0; q < D; ++q)
       if (o[q] != 0) {
-        if constexpr (ISO) {
-          const double c = (double)o[q] / (double)m0;     // exact: +-1, +-2, +-1/2
-          if (first)
-            acc = o[q] > 0 ? Bs.at(a, q) : -Bs.at(a, q);
-          else if (c == 1.0)
-            acc = acc + Bs.at(a, q);
-          else if (c == -1.0)
-            acc = acc - Bs.at(a, q);
-          else
-            acc = fma(c, Bs.at(a, q), acc);
-        } else {
-          acc = first ? Bs.at(a, q) * L.gg[k][q] : fma(Bs.at(a, q), L.gg[k][q], acc);
-        }
+        acc = first ? Bs.at(a, q) * L.gg[k][q] : fma(Bs.at(a, q), L.gg[k][q], acc);
         first = false;
       }
     Gg[a] = acc;
@@ -218,11 +195,7 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
   beta = hx >= 0x3FF00000 ? 1.0 : beta;
   const double rbar = fma(0.5, rho_j, r.hrho_i);
   const double bk = beta * K.kappa;
-  // ISO: rg = rbar gs_k and pg = p* gs_k carry the factor Gg lost
-  constexpr bool SEP = ISO && !UB;
-  const double rg = SEP ? rbar * L.gs[k] : rbar;
-  const double pg = SEP ? fma(rg, fma(bk, x, K.c2), -L.cg[k])
-                        : fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
+  const double pg = fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
   // 1 / rbar: MUFU seed + one Newton step (relative error ~2^-44, only in
   // the beta^2 limiter term)
   double rr;
@@ -237,7 +210,7 @@ __device__ __forceinline__ void lat_pair(const LatFold& L, const LatConst& K, La
     vs[q] = o[q] == 0 ? vb : fma(-wq, L.ee[k][q], vb);
     sg = fma(vs[q], Gg[q], sg);
   }
-  const double rs2 = rg * sg;                      // -2 rbar s
+  const double rs2 = rbar * sg;                    // -2 rbar s
   r.dr += rs2;
   // viscous -mv (v_j - v_i): the v_i part is summed once (K.mv_sum)
 #pragma unroll
@@ -289,8 +262,8 @@ __device__ __forceinline__ void lat_pair_ib(const LatFold& L, const LatConst& K,
   }
 }
 
-template <int D, int R2, int MINB, int NT = kLT, bool ISO = false, bool UB = false,
-          bool IB = false, bool MO = false>
+template <int D, int R2, int MINB, int NT = kLT, bool UB = false, bool IB = false,
+          bool MO = false>
 __global__ void __launch_bounds__(NT, MINB * kLT / NT)
 k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const int stage,
              const double* __restrict__ B, const double4* __restrict__ S_in,
@@ -365,7 +338,7 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     } else {
       Sym<D> Bj;
       if constexpr (!UB) Bj.load(B, n, j);
-      lat_pair<D, R2, k, ISO, UB>(L, K, row, vj, rho_j, Bj);
+      lat_pair<D, R2, k, UB>(L, K, row, vj, rho_j, Bj);
     }
   });
   if constexpr (IB) {   // sum_k rs2 hv_i
@@ -777,32 +750,6 @@ extern "C" int sphb_wc_uniform_b_check(const sphb_wc_params* p, const double* B,
   return SPHB_OK;
 }
 
-// Separable-slot form: every slot's table displacement is sp_k o_k with one
-// (signed) spacing per slot, to a relative spread of 1e-14 (far inside the
-// check's tolerance on the displacements themselves).  Fills F->gs / F->cg.
-static bool lattice_separable(int dim, const sphb_lattice* L, LatFold* F, double c2rho0) {
-  int32_t off[3 * SPHB_LATTICE_MAXW];
-  if (sphb_lattice_offsets(dim, L->r2, off) != SPHB_OK) return false;
-  for (int k = 0; k < L->width; ++k) {
-    int q0 = -1;
-    for (int q = 0; q < 3; ++q)
-      if (off[3 * k + q] != 0) { q0 = q; break; }
-    if (q0 < 0) return false;
-    const double sp = L->dx[k][q0] / off[3 * k + q0];
-    if (!(fabs(sp) > 0.0)) return false;
-    for (int q = 0; q < 3; ++q) {
-      const int o = off[3 * k + q];
-      if (o == 0) continue;      // zero components: compile-time zeros in every form
-      if (fabs(L->dx[k][q] / o - sp) > 1e-14 * fabs(sp)) return false;
-    }
-    if (F) {
-      F->gs[k] = L->g2[k] * sp * fabs((double)off[3 * k + q0]);
-      F->cg[k] = c2rho0 * F->gs[k];
-    }
-  }
-  return true;
-}
-
 // Isotropic uniform B: b0 = beta I to 1e-12 of max|b0| (a cubic or square
 // lattice).  Fills the IB tables of F (needs F->ee) when F is given.
 static bool lattice_isotropic_b(int dim, double c_art, const sphb_lattice* L, LatFold* F) {
@@ -829,11 +776,6 @@ static bool lattice_isotropic_b(int dim, double c_art, const sphb_lattice* L, La
     }
   }
   return true;
-}
-
-extern "C" int sphb_wc_lattice_separable(int32_t dim, const sphb_lattice* L) {
-  if (!L || sphb_lattice_width(dim, L->r2) != L->width) return SPHB_ERR_ARG;
-  return lattice_separable(dim, L, nullptr, 0.0) ? 1 : 0;
 }
 
 extern "C" int sphb_wc_lattice_isotropic_b(int32_t dim, const sphb_lattice* L) {
@@ -886,12 +828,6 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
   }
   K.mv_sum = 0.0;
   for (int k = 0; k < L->width; ++k) K.mv_sum += L->mv[k];
-  // separable-slot form (LatFold::gs); SPHB_LAT_ISO=0 disables it (tuning)
-  static const int iso_env = [] {
-    const char* e = getenv("SPHB_LAT_ISO");
-    return e ? atoi(e) : 1;
-  }();
-  const bool iso = iso_env != 0 && lattice_separable(p->dim, L, &F, K.c2rho0);
   // uniform-B form: (B_i + B_j) gg_k = 2 b0 gg_k per slot
   const bool ub = L->uniform_b != 0;
   if (ub) {
@@ -924,141 +860,59 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     return e ? atoi(e) : 1;
   }();
   const bool ib = ub && ib_env && lattice_isotropic_b(p->dim, p->c_art, L, &F);
-  static const int ubminb_env = [] {       // SPHB_LAT_UB_MINB (tuning)
-    const char* e = getenv("SPHB_LAT_UB_MINB");
-    return e ? atoi(e) : 0;
-  }();
-  const unsigned grid = sphb_blocks(p->nrows, kLT);
   const double4* Sin = (const double4*)s_in;
   const double4* Sn = (const double4*)s_n;
   const double4* Mn = (const double4*)m_n;
   double4* Sout = (double4*)s_out;
   double4* Mout = (double4*)m_out;
-  // occupancy target (128-thread blocks per SM): 5 -> 96 registers,
-  // 4 -> 128, 3 -> 168, 2 -> 255; SPHB_LAT_MINB overrides (tuning)
-  static const int minb_env = [] {
-    const char* e = getenv("SPHB_LAT_MINB");
-    return e ? atoi(e) : 0;
-  }();
-  // measured best on B200 (scripts/ab_lattice.sh, profiles/r02_tune_lattice.md):
-  // the 32-slot stencil runs fastest with 168 registers, the 80-slot one
-  // with 224 (more pairs in flight beat occupancy for both)
-  const int minb = minb_env ? minb_env
-                            : (p->dim == 3 ? (L->r2 == 4 ? 3 : 2) : 5);
-  // block size (tuning, SPHB_LAT_NT = 64 / 256; 3D only): same register
-  // budget per thread, blocks of NT threads
-  static const int nt_env = [] {
-    const char* e = getenv("SPHB_LAT_NT");
-    return e ? atoi(e) : 0;
-  }();
-  // 3D 2h (80 slots): 256-thread blocks with the full 255-register budget
-  // (one block, 8 warps per SM) measured fastest (13.35 -> 11.96 ms/step,
-  // profiles/r02_tune_lattice.md)
-  const int nt = nt_env ? nt_env : (p->dim == 3 && L->r2 == 6 && !minb_env ? 256 : 0);
+  // Occupancy targets (128-thread blocks per SM; 4 -> 128 registers, 3 ->
+  // 168, 2 -> 255), measured best on B200 (scripts/ab_lattice.sh,
+  // profiles/r02_tune_lattice.md): uniform-B forms 4 (32 slots) / 3 (80
+  // slots); table form 3 (32 slots) and, for the 80-slot stencil, 256-thread
+  // blocks with the full 255-register budget.  2D: 5 (96 registers).
+  const bool r4 = L->r2 == 4;
+  const int minb = p->dim == 3 ? (ub ? (r4 ? 4 : 3) : (r4 ? 3 : 2)) : 5;
+  const int nt = (p->dim == 3 && !ub && !r4) ? 256 : kLT;
   // L2 prefetch distance in rows (3D): the stencil's reach in planes + the
   // resident threads of one wave; SPHB_LAT_PF overrides (0 = off)
   static const int64_t pf_env = [] {
     const char* e = getenv("SPHB_LAT_PF");
     return e ? (int64_t)atoll(e) : (int64_t)-1;
   }();
-  int64_t pf = 0, reach = 0;
-  int sms = 148;
+  int64_t pf = 0;
   if (p->dim == 3) {
-    int dev = 0;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
+    const int64_t reach = (int64_t)isqrt_c(L->r2) * L->n[0] * L->n[1];
     pf = pf_env >= 0 ? pf_env : reach + (int64_t)sms * minb * kLT;
   }
   static const int mo_env = [] {             // SPHB_LAT_MIRROR=0: canonical order
     const char* e = getenv("SPHB_LAT_MIRROR");
     return e ? atoi(e) : 1;
   }();
-  if (ib && !minb_env && !nt_env) {
-#define SPHB_IB(D, R, MB, NT)                                                                \
-    if (p->dim == D && L->r2 == R && umb == MB) {                                            \
-      if (mo_env)                                                                            \
-        k_wc_lattice<D, R, MB, NT, false, true, true, true>                                  \
-            <<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, \
-                                                       Mout, scalars, err, pfu);             \
-      else                                                                                   \
-        k_wc_lattice<D, R, MB, NT, false, true, true, false>                                 \
-            <<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout, \
-                                                       Mout, scalars, err, pfu);             \
-      SPHB_LAUNCH_CHECK();                                                                   \
-      return SPHB_OK;                                                                        \
-    }
-    const int umb = ubminb_env ? ubminb_env : (p->dim == 3 ? (L->r2 == 4 ? 4 : 3) : 5);
-    const int64_t pfu =
-        p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
-    SPHB_IB(3, 4, 3, 128) SPHB_IB(3, 4, 4, 128) SPHB_IB(3, 6, 3, 128)
-    SPHB_IB(2, 4, 5, 128) SPHB_IB(2, 6, 5, 128)
-#undef SPHB_IB
+  const unsigned grid = sphb_blocks(p->nrows, nt);
+#define SPHB_L(D, R, MB, NT, UB, IB, MO)                                                    \
+  if (p->dim == D && L->r2 == R) {                                                          \
+    k_wc_lattice<D, R, MB, NT, UB, IB, MO><<<grid, NT, 0, st>>>(                            \
+        *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pf);                     \
+    SPHB_LAUNCH_CHECK();                                                                    \
+    return SPHB_OK;                                                                         \
   }
-  if (ub && !minb_env && !nt_env) {
-#define SPHB_U(D, R, MB, NT)                                                                 \
-    if (p->dim == D && L->r2 == R && umb == MB) {                                            \
-      k_wc_lattice<D, R, MB, NT, false, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(     \
-          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pfu);                   \
-      SPHB_LAUNCH_CHECK();                                                                   \
-      return SPHB_OK;                                                                        \
-    }
-    const int umb = ubminb_env ? ubminb_env : (p->dim == 3 ? (L->r2 == 4 ? 4 : 3) : 5);
-    const int64_t pfu =
-        p->dim == 3 ? (pf_env >= 0 ? pf_env : reach + (int64_t)sms * umb * kLT) : 0;
-    SPHB_U(3, 4, 3, 128) SPHB_U(3, 4, 4, 128) SPHB_U(3, 4, 5, 128)
-    SPHB_U(3, 6, 2, 128) SPHB_U(3, 6, 3, 128) SPHB_U(3, 6, 4, 128)
-    SPHB_U(2, 4, 5, 128) SPHB_U(2, 6, 5, 128)
-#undef SPHB_U
+  if (ib && mo_env) {                        // isotropic uniform-B, mirror order
+    SPHB_L(3, 4, 4, 128, true, true, true) SPHB_L(3, 6, 3, 128, true, true, true)
+    SPHB_L(2, 4, 5, 128, true, true, true) SPHB_L(2, 6, 5, 128, true, true, true)
+  } else if (ib) {                           // isotropic uniform-B, canonical order
+    SPHB_L(3, 4, 4, 128, true, true, false) SPHB_L(3, 6, 3, 128, true, true, false)
+    SPHB_L(2, 4, 5, 128, true, true, false) SPHB_L(2, 6, 5, 128, true, true, false)
+  } else if (ub) {                           // uniform-B table
+    SPHB_L(3, 4, 4, 128, true, false, false) SPHB_L(3, 6, 3, 128, true, false, false)
+    SPHB_L(2, 4, 5, 128, true, false, false) SPHB_L(2, 6, 5, 128, true, false, false)
+  } else {                                   // table geometry, B_j gathered
+    SPHB_L(3, 4, 3, 128, false, false, false) SPHB_L(3, 6, 2, 256, false, false, false)
+    SPHB_L(2, 4, 5, 128, false, false, false) SPHB_L(2, 6, 5, 128, false, false, false)
   }
-  // separable-slot kernel: default for the 80-slot stencil only (C5 256^3,
-  // same box: 2h 10.46 -> 10.34 ms/step; the 32-slot stencil measured
-  // 4.27 -> 4.45 with 2 fewer FP64 instructions per pair, so it keeps the
-  // table form; profiles/r02_tune_lattice.md)
-  if (iso && !minb_env && !nt_env) {
-#define SPHB_I(D, R, MB, NT)                                                                 \
-    if (p->dim == D && L->r2 == R) {                                                         \
-      k_wc_lattice<D, R, MB, NT, true><<<sphb_blocks(p->nrows, NT), NT, 0, st>>>(            \
-          *p, K, F, stage, b, Sin, Sn, Mn, Sout, Mout, scalars, err, pf);                    \
-      SPHB_LAUNCH_CHECK();                                                                   \
-      return SPHB_OK;                                                                        \
-    }
-    SPHB_I(3, 6, 2, 256)
-#undef SPHB_I
-  }
-  if (p->dim == 3 && (nt == 64 || nt == 256)) {
-    const unsigned g2 = sphb_blocks(p->nrows, nt);
-#define SPHB_NT(R, MB, NT)                                                                 \
-    k_wc_lattice<3, R, MB, NT><<<g2, NT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
-                                                  Mout, scalars, err, pf)
-    const bool r4 = L->r2 == 4;
-    if (nt == 64) {
-      if (r4) SPHB_NT(4, 3, 64); else SPHB_NT(6, 2, 64);
-    } else {
-      if (r4) SPHB_NT(4, 3, 256); else SPHB_NT(6, 2, 256);
-    }
-#undef SPHB_NT
-    SPHB_LAUNCH_CHECK();
-    return SPHB_OK;
-  }
-#define SPHB_S(D, R)                                                                   \
-  if (p->dim == D && L->r2 == R) {                                                     \
-    switch (minb) {                                                                    \
-      case 2: SPHB_S1(D, R, 2);                                                        \
-      case 3: SPHB_S1(D, R, 3);                                                        \
-      case 4: SPHB_S1(D, R, 4);                                                        \
-      default: SPHB_S1(D, R, 5);                                                       \
-    }                                                                                  \
-    SPHB_LAUNCH_CHECK();                                                               \
-    return SPHB_OK;                                                                    \
-  }
-#define SPHB_S1(D, R, MB)                                                              \
-  k_wc_lattice<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, F, stage, b, Sin, Sn, Mn, Sout,  \
-                                               Mout, scalars, err, pf);                 \
-  break
-  SPHB_LAT_CASES(SPHB_S)
-#undef SPHB_S
-#undef SPHB_S1
+#undef SPHB_L
   return SPHB_ERR_ARG;
 }
 
@@ -1129,10 +983,7 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   K.half_cinv = 0.5f / K.c;
   K.rho0 = (float)p->rho0;
   const unsigned grid = sphb_blocks(p->nrows, kLT);
-  static const int minb32 = [] {           // SPHB_LAT32_MINB (tuning): 4, 6, 8
-    const char* e = getenv("SPHB_LAT32_MINB");
-    return e ? atoi(e) : 4;
-  }();
+
 #define SPHB_F1(D, R, MB)                                                                   \
   k_wc_lattice_f32<D, R, MB><<<grid, kLT, 0, st>>>(*p, K, T, stage, b32,                    \
       (const float4*)s32_in, (const double4*)s_n, (const double4*)m_n, (float4*)s32_out,    \
@@ -1149,8 +1000,6 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
   if (p->dim == D && L->r2 == R) {                                                          \
     if (ib) SPHB_FI(D, R, 4);                                                               \
     else if (ub) SPHB_FU(D, R, 4);                                                          \
-    else if (D == 3 && minb32 == 6) SPHB_F1(D, R, 6);                                       \
-    else if (D == 3 && minb32 == 8) SPHB_F1(D, R, 8);                                       \
     else SPHB_F1(D, R, 4);                                                                  \
     SPHB_LAUNCH_CHECK();                                                                    \
     return SPHB_OK;                                                                         \

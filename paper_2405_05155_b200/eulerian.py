@@ -454,7 +454,6 @@ class EulerianSolver:
         p.c_art, p.rho0, p.mu, p.cfl = eos.c_art, eos.rho0, self.mu, self.cfl
         p.vol_const = float(vol[0]) if self.n else 0.0
         self.lattice = None
-        self.lattice_separable = False
         self.lattice_isotropic_b = False
         if (variant == "global" and not self._ideal and ghosts is None
                 and wall_force_tag is None and uniform and self.order is not self.bins
@@ -556,9 +555,6 @@ class EulerianSolver:
                   1e-12 * spacing, bad.data_ptr(), _lib.stream_ptr())
         if int(bad.item()) != 0:
             return None
-        # separable-slot form of the lattice stage (every slot's displacement
-        # is one spacing times its integer offset; csrc/wc_lattice.cu)
-        self.lattice_separable = int(lib.sphb_wc_lattice_separable(d, ctypes.byref(L))) == 1
         return L
 
     def _setup_uniform_b(self):

@@ -1,11 +1,10 @@
 #!/bin/bash
 # A/B of WC stage variants on one box (same build).  Each argument is one
 # variant: a space-separated list of environment settings (default: the
-# general pass-list kernel vs the lattice kernel at several occupancy
-# targets).  Prints ms/step at 1.6h and 2h for each.
+# general pass-list kernel and the lattice kernel's forms).  Prints ms/step at 1.6h and 2h for each.
 cd "$(dirname "$0")/.."
 if [ $# -eq 0 ]; then
-  set -- "SPHB_WC_LATTICE=0" "SPHB_LAT_MINB=2" "SPHB_LAT_MINB=3" "SPHB_LAT_MINB=4" "SPHB_LAT_MINB=5"
+  set -- "SPHB_WC_LATTICE=0" "SPHB_LAT_UNIFORM_B=0" "SPHB_LAT_IB=0" "SPHB_LAT_MIRROR=0" "SPHB_LAT_MIRROR=1"
 fi
 for v in "$@"; do
   env $v python bench.py --steps 10 --warmup 3 --no-fp32 --no-c4 --no-cpu-baseline > /tmp/ab.json 2>/tmp/ab.err || { echo "$v failed"; tail -5 /tmp/ab.err; continue; }

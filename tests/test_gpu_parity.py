@@ -870,9 +870,6 @@ def test_wc_lattice_path_taken_and_matches_general_kernel(monkeypatch, key, labe
     cfg = builder(kernel=key, n_side=size)
     fast = make_wc(cfg)
     assert fast.lattice is not None and fast.lattice.width == fast.width
-    # TGV tables are separable (one spacing per slot): the 80-slot stencil
-    # (2h) runs the separable-slot form of the lattice kernel
-    assert fast.lattice_separable
     # ... and every correction matrix equals b0 to rounding: uniform-B form
     assert fast.lattice.uniform_b == 1
     # ... and b0 = beta I (cubic / square lattice): isotropic uniform-B form

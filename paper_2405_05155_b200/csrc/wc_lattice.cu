@@ -240,9 +240,13 @@ __device__ __forceinline__ void lat_pair_ib(const LatFold& L, const LatConst& K,
       first = false;
     }
   const double x = Bv - A;                          // (u_l - u_r) eta / c
+  // beta = clamp(x, 0, 1) as an integer clamp of the high word: x < 0 gives
+  // high word 0, i.e. beta = lo * 2^-1074 < 1e-300, whose every use below
+  // (c^2 + beta kappa x, beta^2 kappa) rounds exactly as beta = 0 does;
+  // x >= 1 gives high word 0x3FF00000 with the low word cleared, i.e. 1.0
   const int hx = __double2hiint(x);
-  double beta = hx < 0 ? 0.0 : x;
-  beta = hx >= 0x3FF00000 ? 1.0 : beta;
+  const int hb = min(max(hx, 0), 0x3FF00000);
+  const double beta = __hiloint2double(hb, hx >= 0x3FF00000 ? 0 : __double2loint(x));
   const double rbar = fma(0.5, rho_j, r.hrho_i);
   const double bk = beta * K.kappa;
   const double pg = fma(rbar, fma(bk, x, K.c2), -K.c2rho0);
@@ -312,15 +316,26 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     // mirror order: slot k then its mirror W-1-k, which reuses A = v_i . ee_k
     // negated (one row's slots summed in this order instead of the
     // canonical one)
+    // 32-bit byte offsets of the records (the launcher uses this kernel for
+    // n <= 2^27), so every gather is one [uniform base + 32-bit offset]
+    // load with no 64-bit address arithmetic
+    unsigned xb[2 * R + 1], yb[2 * R + 1], zb[2 * R + 1];
+#pragma unroll
+    for (int q = 0; q < 2 * R + 1; ++q) {
+      xb[q] = (unsigned)xs[q] * 32u;
+      yb[q] = (unsigned)ys[q] * 32u;
+      zb[q] = (unsigned)zs[q] * 32u;
+    }
+    const char* sb = reinterpret_cast<const char*>(S_in);
     static_for<St::W / 2>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
       constexpr int km = St::W - 1 - k;
       constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-      const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
-      const int64_t jm = (int64_t)(xs[R - o[0]] + ys[R - o[1]] + zs[R - o[2]]);
+      const unsigned bj = xb[o[0] + R] + yb[o[1] + R] + zb[o[2] + R];
+      const unsigned bm = xb[R - o[0]] + yb[R - o[1]] + zb[R - o[2]];
       double vj[D], rho_j, vm[D], rho_m;
-      unpack_s<D>(ldg4(S_in + j), vj, rho_j);
-      unpack_s<D>(ldg4(S_in + jm), vm, rho_m);
+      unpack_s<D>(ldg4(reinterpret_cast<const double4*>(sb + bj)), vj, rho_j);
+      unpack_s<D>(ldg4(reinterpret_cast<const double4*>(sb + bm)), vm, rho_m);
       double A;
       lat_pair_ib<D, R2, k>(L, K, row, vj, rho_j, A);
       lat_pair_ib<D, R2, km, true>(L, K, row, vm, rho_m, A);
@@ -899,7 +914,7 @@ extern "C" int sphb_wc_stage_lattice(const sphb_wc_params* p, const sphb_lattice
     SPHB_LAUNCH_CHECK();                                                                    \
     return SPHB_OK;                                                                         \
   }
-  if (ib && mo_env) {                        // isotropic uniform-B, mirror order
+  if (ib && mo_env && p->n <= ((int64_t)1 << 27)) {   // isotropic, mirror order (32-bit offsets)
     SPHB_L(3, 4, 4, 128, true, true, true) SPHB_L(3, 6, 3, 128, true, true, true)
     SPHB_L(2, 4, 5, 128, true, true, true) SPHB_L(2, 6, 5, 128, true, true, true)
   } else if (ib) {                           // isotropic uniform-B, canonical order

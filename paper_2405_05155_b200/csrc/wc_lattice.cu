@@ -533,11 +533,21 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
 #pragma unroll
   for (int q = 0; q < D; ++q) fm[q] = 0.f;
 
+  // 32-bit byte offsets of the 16-byte records (the launcher requires
+  // n <= 2^28): one add per gather, no 64-bit address arithmetic
+  unsigned xb[SIDE], yb[SIDE], zb[SIDE];
+#pragma unroll
+  for (int q = 0; q < SIDE; ++q) {
+    xb[q] = (unsigned)xs[q] * 16u;
+    yb[q] = (unsigned)ys[q] * 16u;
+    zb[q] = (unsigned)zs[q] * 16u;
+  }
+  const char* s32b = reinterpret_cast<const char*>(S32_in);
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
-    const int64_t j = (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]);
-    const float4 sj = __ldg(S32_in + j);
+    const float4 sj =
+        __ldg(reinterpret_cast<const float4*>(s32b + (xb[o[0] + R] + yb[o[1] + R] + zb[o[2] + R])));
     const float vj[3] = {sj.x, sj.y, sj.z};
     const float drho_j = D == 3 ? sj.w : sj.z;
     if constexpr (IB) {
@@ -553,12 +563,14 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
           first = false;
         }
       const float x = Bv - A;
-      const float beta = fminf(fmaxf(x, 0.f), 1.f);
+      const float beta = __saturatef(x);           // clamp to [0, 1], one instruction
       const float hd = fmaf(0.5f, drho_j, hdi);
       const float rbar = K.rho0 + hd;
       const float bk = beta * K.kappa;
       const float pg = fmaf(rbar * bk, x, K.c2 * hd);
-      const float wq = (beta * bk) * (drho_i - drho_j) * __fdividef(1.0f, rbar);
+      float rr;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rr) : "f"(rbar));   // MUFU, no range fix-up
+      const float wq = (beta * bk) * (drho_i - drho_j) * rr;
       const float sg2 = fmaf(-wq, L.e2[k], A + Bv);
       const float rs2 = (rbar * L.hl[k]) * sg2;
       fr += rs2;
@@ -936,7 +948,8 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
                                          const double* s_n, const double* m_n, float* s32_out,
                                          double* s_out, double* m_out, double* scalars,
                                          int32_t* err, void* stream) {
-  if (!lattice_args_ok(p, L) || !b32 || !s32_in || stage < 0 || stage > 2 || p->interior ||
+  if (!lattice_args_ok(p, L) || p->n > ((int64_t)1 << 28) || !b32 || !s32_in || stage < 0 ||
+      stage > 2 || p->interior ||
       p->wall_tag || !p->uniform_vol || (stage > 0 && !s32_out))
     return SPHB_ERR_ARG;
   if (p->nrows == 0) return SPHB_OK;

@@ -586,7 +586,7 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
       }
     } else {
     SymF<D> Bj;
-    if constexpr (!UB) Bj.load(B, n, j);
+    if constexpr (!UB) Bj.load(B, n, (int64_t)(xs[o[0] + R] + ys[o[1] + R] + zs[o[2] + R]));
     float dx[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) dx[q] = o[q] == 0 ? 0.f : L.dx[k][q];

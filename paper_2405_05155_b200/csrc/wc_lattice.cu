@@ -18,6 +18,7 @@
 // the reference's, bit-exact), and every pair's exact displacement equals
 // the table's within `tol`.  Summation is in the canonical slot order.
 #include <stdlib.h>
+#include <string.h>
 
 #include <type_traits>
 #include <utility>
@@ -456,7 +457,45 @@ struct LatF32 {
   // isotropic uniform-B form (LatFold::lam / hl / e2, ee = dx inv_r eta_c)
   float ee[SPHB_LATTICE_MAXW][3];
   float lam[SPHB_LATTICE_MAXW], hl[SPHB_LATTICE_MAXW], e2[SPHB_LATTICE_MAXW];
+  // packed FP32x2 form (3D): slot k and its mirror W-1-k as the two lanes of
+  // one f32x2 value; per mirror pair k < W/2: (ee, ee), (ee, -ee), (-e2, -e2),
+  // (hl, hl), (lam, lam), (-mv, -mv) as 64-bit lane pairs
+  unsigned long long pee[SPHB_LATTICE_MAXW / 2][3], pes[SPHB_LATTICE_MAXW / 2][3];
+  unsigned long long pe2[SPHB_LATTICE_MAXW / 2], phl[SPHB_LATTICE_MAXW / 2];
+  unsigned long long plam[SPHB_LATTICE_MAXW / 2], pmv[SPHB_LATTICE_MAXW / 2];
 };
+
+// packed FP32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2): one instruction
+// for two lanes, round-to-nearest per lane as the scalar instructions
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 
 struct LatConstF32 {
   float c, c2, eta_c, half_cinv, rho0, kappa;
@@ -543,6 +582,81 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
     zb[q] = (unsigned)zs[q] * 16u;
   }
   const char* s32b = reinterpret_cast<const char*>(S32_in);
+  if constexpr (IB && D == 3) {
+    // slot k (lane 0) and its mirror W-1-k (lane 1) in packed FP32x2: the
+    // mirror's A, x and s are the slot's with the sign of ee flipped, which
+    // the (1, -1) lane signs and the (ee, -ee) table carry
+    const f2 sig = pk2(1.f, -1.f);
+    const f2 half2 = pk2(0.5f, 0.5f);
+    const f2 hdi2 = pk2(hdi, hdi), dri2 = pk2(drho_i, drho_i);
+    const f2 rho02 = pk2(K.rho0, K.rho0), kap2 = pk2(K.kappa, K.kappa);
+    const f2 c22 = pk2(K.c2, K.c2);
+    f2 vi2[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) vi2[q] = pk2(vi[q], vi[q]);
+    f2 fr2 = pk2(0.f, 0.f), fm2[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) fm2[q] = pk2(0.f, 0.f);
+    static_for<St::W / 2>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
+      const float4 sj = __ldg(
+          reinterpret_cast<const float4*>(s32b + (xb[o[0] + R] + yb[o[1] + R] + zb[o[2] + R])));
+      const float4 sm = __ldg(
+          reinterpret_cast<const float4*>(s32b + (xb[R - o[0]] + yb[R - o[1]] + zb[R - o[2]])));
+      const f2 vj2[3] = {pk2(sj.x, sm.x), pk2(sj.y, sm.y), pk2(sj.z, sm.z)};
+      const f2 dr2 = pk2(sj.w, sm.w);
+      float A = 0.f;
+      f2 P = pk2(0.f, 0.f);
+      bool first = true;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (o[q] != 0) {
+          A = first ? vi[q] * L.ee[k][q] : fmaf(vi[q], L.ee[k][q], A);
+          P = first ? mul2(vj2[q], L.pee[k][q]) : fma2(vj2[q], L.pee[k][q], P);
+          first = false;
+        }
+      const f2 A2 = pk2(A, A);
+      const f2 X = mul2(sig, sub2(P, A2));                    // (x_k, x_mirror)
+      float x0, x1;
+      upk2(X, x0, x1);
+      const f2 B2 = pk2(__saturatef(x0), __saturatef(x1));
+      const f2 HD = fma2(half2, dr2, hdi2);
+      const f2 RB = add2(HD, rho02);
+      const f2 BK = mul2(B2, kap2);
+      const f2 PG = fma2(mul2(RB, BK), X, mul2(c22, HD));
+      float r0, r1, q0, q1;
+      upk2(RB, r0, r1);
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(q0) : "f"(r0));
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(q1) : "f"(r1));
+      const f2 WQ = mul2(mul2(mul2(B2, BK), sub2(dri2, dr2)), pk2(q0, q1));
+      const f2 S = mul2(sig, add2(P, A2));
+      const f2 SG = fma2(WQ, L.pe2[k], S);                    // pe2 = -2 |ee|^2
+      const f2 RS = mul2(mul2(RB, L.phl[k]), SG);
+      fr2 = add2(fr2, RS);
+      const f2 C1 = fma2(half2, RS, L.pmv[k]);                // pmv = -mv
+      const f2 CE = sub2(mul2(PG, L.plam[k]), mul2(RS, WQ));
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        fm2[q] = fma2(C1, sub2(vj2[q], vi2[q]), fm2[q]);
+        if (o[q] != 0) fm2[q] = fma2(CE, L.pes[k][q], fm2[q]);
+      }
+      if constexpr ((k + 1) % (kFlush / 2) == 0 || k + 1 == St::W / 2) {
+        float lo, hi;
+        upk2(fr2, lo, hi);
+        dr += (double)lo;
+        dr += (double)hi;
+        fr2 = pk2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          upk2(fm2[q], lo, hi);
+          dm[q] += (double)lo;
+          dm[q] += (double)hi;
+          fm2[q] = pk2(0.f, 0.f);
+        }
+      }
+    });
+  } else
   static_for<St::W>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int o[3] = {St::L.o[k][0], St::L.o[k][1], St::L.o[k][2]};
@@ -1001,6 +1115,22 @@ extern "C" int sphb_wc_stage_lattice_f32(const sphb_wc_params* p, const sphb_lat
       T.lam[k] = (float)lam;
       T.hl[k] = (float)(0.5 * lam);
       T.e2[k] = (float)(2.0 * e2);
+    }
+    auto bits2 = [](float lo, float hi) {
+      unsigned a, b;
+      memcpy(&a, &lo, 4);
+      memcpy(&b, &hi, 4);
+      return (unsigned long long)a | ((unsigned long long)b << 32);
+    };
+    for (int k = 0; k < L->width / 2; ++k) {
+      for (int q = 0; q < 3; ++q) {
+        T.pee[k][q] = bits2(T.ee[k][q], T.ee[k][q]);
+        T.pes[k][q] = bits2(T.ee[k][q], -T.ee[k][q]);
+      }
+      T.pe2[k] = bits2(-T.e2[k], -T.e2[k]);
+      T.phl[k] = bits2(T.hl[k], T.hl[k]);
+      T.plam[k] = bits2(T.lam[k], T.lam[k]);
+      T.pmv[k] = bits2(-T.mv[k], -T.mv[k]);
     }
   }
   LatConstF32 K;

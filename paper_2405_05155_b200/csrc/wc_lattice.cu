@@ -606,17 +606,15 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
           reinterpret_cast<const float4*>(s32b + (xb[R - o[0]] + yb[R - o[1]] + zb[R - o[2]])));
       const f2 vj2[3] = {pk2(sj.x, sm.x), pk2(sj.y, sm.y), pk2(sj.z, sm.z)};
       const f2 dr2 = pk2(sj.w, sm.w);
-      float A = 0.f;
-      f2 P = pk2(0.f, 0.f);
+      f2 A2 = pk2(0.f, 0.f), P = pk2(0.f, 0.f);              // (A, A), (v_j . ee, v_m . ee)
       bool first = true;
 #pragma unroll
       for (int q = 0; q < 3; ++q)
         if (o[q] != 0) {
-          A = first ? vi[q] * L.ee[k][q] : fmaf(vi[q], L.ee[k][q], A);
+          A2 = first ? mul2(vi2[q], L.pee[k][q]) : fma2(vi2[q], L.pee[k][q], A2);
           P = first ? mul2(vj2[q], L.pee[k][q]) : fma2(vj2[q], L.pee[k][q], P);
           first = false;
         }
-      const f2 A2 = pk2(A, A);
       const f2 X = mul2(sig, sub2(P, A2));                    // (x_k, x_mirror)
       float x0, x1;
       upk2(X, x0, x1);

@@ -90,3 +90,35 @@ def test_product_path_fails_loudly_without_gpu():
 
     with pytest.raises(_lib.BackendUnavailable):
         build_neighbors([[0.0, 0.0], [1.0, 0.0]], 1.5)
+
+
+def test_lattice_host_queries_without_gpu():
+    """Host-side lattice logic of the C ABI (no device work): stencil widths
+    and canonical offsets (mirror-symmetric: slot W-1-k holds -o_k, which the
+    mirror-order kernels rely on), and the isotropic-B test of the uniform-B
+    form (b0 = beta I to 1e-12 of max|b0|)."""
+    import numpy as np
+
+    lib = _lib.load_library()
+    for dim, r2, width in ((2, 4, 12), (2, 6, 20), (3, 4, 32), (3, 6, 80)):
+        assert lib.sphb_lattice_width(dim, r2) == width
+        off = np.zeros(3 * width, dtype=np.int32)
+        assert lib.sphb_lattice_offsets(dim, r2, off.ctypes.data) == 0
+        off = off.reshape(width, 3)
+        assert np.array_equal(off[::-1], -off)
+        assert np.all((off**2).sum(axis=1) <= r2) and np.all((off**2).sum(axis=1) > 0)
+    L = _lib.Lattice()
+    L.width, L.r2 = 32, 4
+    beta = 1.0965629524
+    for e, v in enumerate((beta, 3e-17, -2e-17, beta, 1e-17, beta * (1 + 1e-15))):
+        L.b0[e] = v
+    L.uniform_b = 0
+    assert lib.sphb_wc_lattice_isotropic_b(3, ctypes.byref(L)) == 0      # not uniform
+    L.uniform_b = 1
+    assert lib.sphb_wc_lattice_isotropic_b(3, ctypes.byref(L)) == 1
+    L.b0[1] = 1e-9                                                       # off-diagonal
+    assert lib.sphb_wc_lattice_isotropic_b(3, ctypes.byref(L)) == 0
+    L.b0[1], L.b0[3] = 0.0, beta * (1 + 1e-9)                            # unequal diagonal
+    assert lib.sphb_wc_lattice_isotropic_b(3, ctypes.byref(L)) == 0
+    L.width = 31
+    assert lib.sphb_wc_lattice_isotropic_b(3, ctypes.byref(L)) < 0      # bad table

@@ -652,7 +652,16 @@ def main():
     sv = leg["1.6h"]["solver"]          # this GPU's rows (owned + halo)
     design_bytes = sv.n * (IMPL_RECORD_BYTES + 4.0 * sv.width)
     flops_pair = FLOPS_PER_PAIR_EST
+    # which specialisations of the stage this run proved and used (each is
+    # checked on the device before use)
+    config["stage_path"] = "general pass-list kernel"
     if sv.lattice is not None:
+        config["stage_path"] = ("lattice: computed neighbour indices, per-slot geometry table "
+                                "(pair sets and displacements checked per row to 1e-12 dp)")
+        if sv.lattice.uniform_b:
+            config["stage_path"] += ("; uniform B (every B_i = b0 to 1e-12, checked), "
+                                     + ("b0 = beta I: isotropic form, mirror order"
+                                        if sv.lattice_isotropic_b else "per-slot (B_i+B_j) gg"))
         design_bytes = sv.n * LATTICE_RECORD_BYTES
         flops_pair = FLOPS_PER_PAIR_LATTICE[sv.lattice.r2]
         if sv.lattice.uniform_b:

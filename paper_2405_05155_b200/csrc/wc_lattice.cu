@@ -318,8 +318,8 @@ k_wc_lattice(const sphb_wc_params P, const LatConst K, const LatFold L, const in
     // negated (one row's slots summed in this order instead of the
     // canonical one)
     // 32-bit byte offsets of the records (the launcher uses this kernel for
-    // n <= 2^27), so every gather is one [uniform base + 32-bit offset]
-    // load with no 64-bit address arithmetic
+    // n <= 2^27): the offset sums stay 32-bit, only the final base + offset
+    // add is 64-bit (SASS: 1968 instead of 2024 instructions per row)
     unsigned xb[2 * R + 1], yb[2 * R + 1], zb[2 * R + 1];
 #pragma unroll
     for (int q = 0; q < 2 * R + 1; ++q) {

@@ -573,7 +573,7 @@ k_wc_lattice_f32(const sphb_wc_params P, const LatConstF32 K, const LatF32 L, co
   for (int q = 0; q < D; ++q) fm[q] = 0.f;
 
   // 32-bit byte offsets of the 16-byte records (the launcher requires
-  // n <= 2^28): one add per gather, no 64-bit address arithmetic
+  // n <= 2^28): the offset sums stay 32-bit
   unsigned xb[SIDE], yb[SIDE], zb[SIDE];
 #pragma unroll
   for (int q = 0; q < SIDE; ++q) {
